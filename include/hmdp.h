@@ -1,0 +1,185 @@
+/* hmdp.h — C-ABI of the B200-native deep-potential force evaluation.
+ *
+ * This is the drop-in boundary for the reference's NN force-provider API
+ * (/root/reference/proj/include/halomd/nn/inference.hpp).  Every entry point
+ * takes plain pointers and sizes; no C++ or torch types cross it.  Each
+ * function names the reference interface it replaces.
+ *
+ * Units follow the reference (include/halomd/units.hpp:1-5): nm, kJ/mol, ps,
+ * amu.  Positions, box, energies, forces and virials are FP64 on the host
+ * side, exactly as in NnInput/NnOutput (inference.hpp:18-44).
+ *
+ * Error model (inference.cpp / model.cpp exceptions mapped to codes):
+ *   HMDP_OK                0
+ *   HMDP_INVALID_ARGUMENT  1   std::invalid_argument (shapes, model, geometry)
+ *   HMDP_RUNTIME_ERROR     2   std::runtime_error (receptive field, zero-length
+ *                              edge, non-finite force)
+ *   HMDP_CUDA_ERROR        3   device failure
+ * The message of the last failure on the calling thread is hmdp_last_error().
+ *
+ * Threading: a context owns one CUDA stream and its device buffers; it may be
+ * used from one thread at a time.  Distinct contexts are independent
+ * ("multiple inferences may run concurrently on disjoint inputs").
+ */
+#ifndef HMDP_H
+#define HMDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMDP_OK 0
+#define HMDP_INVALID_ARGUMENT 1
+#define HMDP_RUNTIME_ERROR 2
+#define HMDP_CUDA_ERROR 3
+
+/* Precision, include/halomd/forcefield.hpp:10 (enum class Precision {fp32, fp64}).
+ * HMDP_FP64 runs the whole network in FP64 (the oracle-of-record mode);
+ * HMDP_FP32 runs it in FP32 with FP64 geometry, energy and force accumulation. */
+#define HMDP_FP32 0
+#define HMDP_FP64 1
+
+typedef struct hmdp_ctx hmdp_ctx;
+typedef struct hmdp_md hmdp_md;
+
+/* Thread-local message of the last failed call ("" if none). */
+const char* hmdp_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Model + context.
+ * Replaces: halomd::nn::model_from_json (model.cpp:165-197) + NnModel::validate
+ * (model.cpp:30-48).  `model_json` is the reference's versioned JSON
+ * ({"format":"halomd-model","version":1,...}, model.cpp:147-163).
+ * max_atoms sizes the device buffers (grown on demand); max_neighbors is the
+ * per-atom edge capacity of the device neighbour list (0 = default 64; grown
+ * and retried automatically on overflow outside graph capture).
+ * model_json may be NULL (len 0) for a geometry-only context that serves
+ * hmdp_build_neighbors; model-dependent calls then fail with
+ * HMDP_INVALID_ARGUMENT.
+ * ------------------------------------------------------------------------- */
+int hmdp_create(const char* model_json, size_t len, int device, int max_atoms,
+                int max_neighbors, hmdp_ctx** out);
+int hmdp_destroy(hmdp_ctx* ctx);
+
+/* Host-only model check (no device work): model_from_json + validate. */
+int hmdp_model_validate(const char* model_json, size_t len);
+
+/* Model facts: family (0 embed_fit, 1 message_passing), depth, rc, n_types,
+ * hidden, n_basis; receptive radius = depth * rc (model.hpp:51-52). */
+int hmdp_model_info(const hmdp_ctx* ctx, int* family, int* depth, double* rc, int* n_types,
+                    int* hidden, int* n_basis);
+
+/* ---------------------------------------------------------------------------
+ * Single-domain periodic evaluation = build_input_periodic + evaluate.
+ * Replaces: halomd::nn::build_input_periodic (inference.cpp:449-487) followed by
+ *           halomd::nn::evaluate (inference.cpp:420-424), all atoms owned,
+ *           identity global_index, coverage = infinity.
+ * xyz[3n], types[n], box[3] (orthorhombic, fully periodic).
+ * Outputs: energy (required), per_atom[n] (nullable), forces[3n] (required),
+ * virial9[9] (nullable; W_ab = -sum_e g_e dr_a dr_b / r), virial (nullable;
+ * the reference's scalar, = trace of virial9 up to rounding).
+ * ------------------------------------------------------------------------- */
+int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, const double* box,
+                 int precision, double* energy, double* per_atom, double* forces,
+                 double* virial9, double* virial);
+
+/* ---------------------------------------------------------------------------
+ * Evaluation on an explicit environment (NnInput, inference.hpp:18-38):
+ * directed CSR edges (offset[n+1], nbr[offset[n]], dr[3*offset[n]] = r_j - r_i
+ * image-corrected), is_ghost[n] (nullable = all owned), coverage_radius and the
+ * skip_coverage_check test hook (inference.hpp:31-32).
+ * Replaces: halomd::nn::evaluate (inference.cpp:183-416).  Energies for owned
+ * atoms only, forces for every input atom (ghost forces returned for routing).
+ * Optional stage outputs for per-kernel parity (nullable):
+ *   desc[n * n_types * n_basis], h[(depth) * n * hidden] (h^0..h^{depth-1}),
+ *   edge_g[offset[n]] (dE/dr per edge).
+ * counters (nullable) = {flops, peak_activation_bytes}, the reference's analytic
+ * NnCounters (inference.cpp:389-414).
+ * ------------------------------------------------------------------------- */
+int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char* is_ghost,
+                     const int* offset, const int* nbr, const double* dr,
+                     double coverage_radius, int skip_coverage_check, int precision,
+                     double* energy, double* per_atom, double* forces, double* virial9,
+                     double* virial, double* desc, double* h, double* edge_g,
+                     uint64_t* counters);
+
+/* ---------------------------------------------------------------------------
+ * Device neighbour list exported in the reference's CSR form.
+ * Replaces: halomd::nn::build_input_periodic's CSR (inference.cpp:472-485) over
+ *           halomd::build_neighbor_list(.., rc, skin=0, full) (neighborlist.cpp:42-113).
+ * Pair set and order are bit-exact with the reference (FP64 test, no FMA).
+ * Writes up to `cap` edges; returns the edge count via *n_edges (call again
+ * with a larger cap when *n_edges > cap).  rc > L/2 -> HMDP_INVALID_ARGUMENT.
+ * ------------------------------------------------------------------------- */
+int hmdp_build_neighbors(hmdp_ctx* ctx, int n, const double* xyz, const double* box, double rc,
+                         int cap, int* offset, int* nbr, double* dr, int* n_edges);
+
+/* descriptors() (inference.cpp:430-447), computed on the device in FP64. */
+int hmdp_descriptors(hmdp_ctx* ctx, int n, const int* types, const int* offset, const int* nbr,
+                     const double* dr, double* desc);
+
+/* switch_value / switch_derivative (inference.cpp:34-45); host functions. */
+double hmdp_switch_value(double r, double rc);
+double hmdp_switch_derivative(double r, double rc);
+
+/* Analytic counters for an evaluation of n atoms (n_owned owned) with ne
+ * directed edges (inference.cpp:389-414): out[0] flops, out[1] activation
+ * bytes for the given precision. */
+int hmdp_counters(const hmdp_ctx* ctx, int n, int n_owned, long long ne, int precision,
+                  uint64_t* out);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident entry point for in-process callers that already hold device
+ * buffers (the MD loop, domain decomposition, graph capture).  All pointers are
+ * device pointers; `stream` is a cudaStream_t (NULL = the context's stream).
+ * Neighbour list is rebuilt on the device from d_xyz (skin 0).  Outputs:
+ * d_energy[1], d_forces[3n] (FP64), d_virial9[9] (nullable), d_per_atom[n]
+ * (nullable).  Nothing is synchronised; errors are latched in the context's
+ * device error word and reported by hmdp_check(ctx).
+ * Capturable in a CUDA graph once hmdp_prepare() has sized buffers for n.
+ * ------------------------------------------------------------------------- */
+int hmdp_prepare(hmdp_ctx* ctx, int n, const double* box, int precision);
+int hmdp_compute_device(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_types,
+                        const double* box, int precision, double* d_energy, double* d_forces,
+                        double* d_virial9, double* d_per_atom, void* stream);
+int hmdp_check(hmdp_ctx* ctx);
+
+/* Number of kernels hmdp_compute_device launches per call for this context's
+ * model (for launch accounting in benchmarks). */
+int hmdp_kernels_per_eval(const hmdp_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Device MD loop: velocity Verlet (integrators.cpp:32-47) with the finite-force
+ * check (integrators.cpp:12-18) and the NN force provider, neighbour list
+ * rebuilt every step (skin 0, as build_input_periodic), all on the device and
+ * captured as one CUDA graph per `steps_per_graph` steps.
+ * ------------------------------------------------------------------------- */
+int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
+                   const double* masses, const int* types, const double* box, double dt_ps,
+                   int precision, int steps_per_graph, hmdp_md** out);
+int hmdp_md_run(hmdp_md* md, int steps);
+/* Copies the current state back; any pointer may be NULL. */
+int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* epot);
+int hmdp_md_destroy(hmdp_md* md);
+
+/* ---------------------------------------------------------------------------
+ * Host fixtures (no device work).
+ * hmdp_make_model_json: make_model (model.cpp:70-100) + model_to_json
+ *   (model.cpp:147-163); deterministic mt19937_64 draw order; returns the JSON
+ *   length (excluding NUL) and writes it if buf/cap allow, or -code on error.
+ * hmdp_synthetic_system: generate_synthetic_system (synthetic.cpp:36-130):
+ *   positions, types, masses, velocities (300 K draw) and box.
+ * ------------------------------------------------------------------------- */
+long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_basis,
+                          int hidden, uint64_t seed, char* buf, long cap);
+int hmdp_synthetic_system(int n, double density, double fraction_grouped, uint64_t seed,
+                          double temperature, double* xyz, int* types, double* masses,
+                          double* vel, double* box);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HMDP_H */

@@ -1,0 +1,1020 @@
+// hmdp_api.cu — context, device memory plan and the extern "C" boundary
+// declared in include/hmdp.h.
+//
+// A context owns: the model weights on the device in FP32 and FP64 (row-major
+// and transposed copies), one CUDA stream, grow-only device buffers sized for
+// the largest system seen, a device error word, and pinned host staging for
+// the host-pointer entry points.  There is no CPU fallback: every compute
+// entry point fails with HMDP_CUDA_ERROR when no device is usable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hmdp.h"
+#include "hmdp_device.cuh"
+#include "hmdp_model.h"
+
+namespace hmdp {
+// launchers (hmdp_kernels.cu)
+void launch_cell_bin(int, const double*, const CellGrid&, int*, int*, int*, unsigned*, cudaStream_t);
+void launch_nbr_search(int, const double*, const CellGrid&, const int*, const int*, const int*,
+                       double, int, int*, int*, int*, double*, unsigned*, cudaStream_t);
+void launch_reverse(int, const int*, const int*, const int*, int*, unsigned*, cudaStream_t);
+void launch_csr_rows(int, const int*, int*, int*, cudaStream_t);
+void launch_in_edges(int, int, const int*, int*, int*, int*, int*, cudaStream_t);
+template <typename T>
+int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, double*, double*,
+                   double*, cudaStream_t);
+void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
+void launch_vv_kick_drift(int, double*, double*, const double*, const double*, double, double,
+                          unsigned*, cudaStream_t);
+void launch_vv_kick(int, double*, const double*, const double*, double, unsigned*, cudaStream_t);
+}  // namespace hmdp
+
+using namespace hmdp;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(HMDP_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return HMDP_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HMDP_INVALID_ARGUMENT;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return HMDP_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HMDP_RUNTIME_ERROR;
+    }
+}
+
+// Grow-only device allocation.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        const size_t want = std::max<size_t>(need, 256);
+        ck(cudaMalloc(&p, want), "cudaMalloc");
+        bytes = want;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaMallocHost(&p, std::max<size_t>(need, 4096)), "cudaMallocHost");
+        bytes = std::max<size_t>(need, 4096);
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// Flattened weights for one precision: per MLP {W1, W1T, b1, W2, W2T, b2}.
+template <typename T>
+struct WeightSet {
+    DBuf buf;
+    DevModel<T> dev{};
+
+    void upload(const Model& m, cudaStream_t st) {
+        std::vector<T> host;
+        std::vector<size_t> offs;
+        auto align = [&] {
+            while (host.size() % 32) host.push_back(T(0));
+        };
+        auto push = [&](const std::vector<double>& v) {
+            align();
+            offs.push_back(host.size());
+            for (double x : v) host.push_back(static_cast<T>(x));
+        };
+        auto transpose = [](const std::vector<double>& w, int out, int in) {
+            std::vector<double> t(w.size());
+            for (int o = 0; o < out; ++o)
+                for (int i = 0; i < in; ++i) t[static_cast<size_t>(i) * out + o] = w[o * in + i];
+            return t;
+        };
+        auto push_mlp = [&](const Mlp& p) {
+            const int in = p.sizes[0], hid = p.sizes[1], out = p.sizes[2];
+            push(p.weights[0]);
+            push(transpose(p.weights[0], hid, in));
+            push(p.biases[0]);
+            push(p.weights[1]);
+            push(transpose(p.weights[1], out, hid));
+            push(p.biases[1]);
+        };
+        std::vector<const Mlp*> order = {&m.embedding, &m.fitting};
+        for (size_t l = 0; l < m.message.size(); ++l) {
+            order.push_back(&m.message[l]);
+            order.push_back(&m.update[l]);
+        }
+        for (const Mlp* p : order) push_mlp(*p);
+        align();
+        buf.ensure(host.size() * sizeof(T));
+        ck(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, st),
+           "weights H2D");
+        ck(cudaStreamSynchronize(st), "weights sync");
+        const T* base = buf.as<T>();
+        size_t q = 0;
+        auto next_mlp = [&]() {
+            DevMlp<T> d;
+            d.W1 = base + offs[q++];
+            d.W1T = base + offs[q++];
+            d.b1 = base + offs[q++];
+            d.W2 = base + offs[q++];
+            d.W2T = base + offs[q++];
+            d.b2 = base + offs[q++];
+            return d;
+        };
+        dev = DevModel<T>{};
+        dev.embed = next_mlp();
+        dev.fit = next_mlp();
+        for (size_t l = 0; l < m.message.size(); ++l) {
+            dev.msg[l] = next_mlp();
+            dev.upd[l] = next_mlp();
+        }
+        for (int k = 0; k < kK; ++k) dev.mu[k] = static_cast<T>(m.centers[k]);
+        const T width = static_cast<T>(m.width);
+        dev.rc = static_cast<T>(m.rc);
+        dev.width = width;
+        // BasisT::values / derivatives constants, evaluated in T (inference.cpp:164,174)
+        volatile T two = T(2), one = T(1);
+        const T w2 = width * width;
+        dev.inv2w2 = one / (two * width * width);
+        dev.invw2 = one / w2;
+        dev.n_types = m.n_types;
+        dev.n_msg = static_cast<int>(m.message.size());
+    }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+struct hmdp_ctx {
+    Model model;
+    bool has_model = false;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    WeightSet<float> wf;
+    WeightSet<double> wd;
+    int cap = 64;      // per-atom neighbour capacity (ELL)
+    int ccap = 32;     // per-cell member capacity
+    // atom / edge / cell buffers
+    DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev;
+    DBuf offset, in_start, in_cnt, cursor, in_edge;
+    // network workspace
+    DBuf er, es, eds, eb, edb, g, mz1, mo, dmsg, desc, ez1, h, uz1, dhown;
+    DBuf e_atom, forces, partial, ticket, out, err, desc64;
+    PinnedBuf pin;
+    int last_launches = 0;
+
+    ~hmdp_ctx() {
+        cudaSetDevice(device);
+        for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
+                        &nbr, &dr, &rev, &offset, &in_start, &in_cnt, &cursor, &in_edge, &er, &es,
+                        &eds, &eb, &edb, &g, &mz1, &mo, &dmsg, &desc, &ez1, &h, &uz1, &dhown,
+                        &e_atom, &forces, &partial, &ticket, &out, &err, &desc64})
+            b->release();
+        wf.buf.release();
+        wd.buf.release();
+        pin.release();
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    int n_msg() const { return static_cast<int>(model.message.size()); }
+
+    void ensure_atoms(int n) {
+        const size_t na = static_cast<size_t>(std::max(n, 1));
+        pos.ensure(na * 3 * sizeof(double));
+        types.ensure(na * sizeof(int));
+        ghost.ensure(na);
+        cell_of.ensure(na * sizeof(int));
+        row_start.ensure(na * sizeof(int));
+        nnei.ensure(na * sizeof(int));
+        offset.ensure((na + 1) * sizeof(int));
+        in_start.ensure(na * sizeof(int));
+        in_cnt.ensure(na * sizeof(int));
+        cursor.ensure(na * sizeof(int));
+        e_atom.ensure(na * sizeof(double));
+        forces.ensure(na * 3 * sizeof(double));
+        const size_t nb = (na + 3) / 4;
+        partial.ensure(nb * 16 * sizeof(double));
+        if (!ticket.p) {
+            ticket.ensure(sizeof(unsigned));
+            ck(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), stream), "memset ticket");
+        }
+        out.ensure(16 * sizeof(double));
+        if (!err.p) {
+            err.ensure(sizeof(unsigned));
+            ck(cudaMemsetAsync(err.p, 0, sizeof(unsigned), stream), "memset err");
+        }
+    }
+    void ensure_edges(long long slots) {
+        const size_t s = static_cast<size_t>(std::max<long long>(slots, 1));
+        nbr.ensure(s * sizeof(int));
+        dr.ensure(s * 3 * sizeof(double));
+        rev.ensure(s * sizeof(int));
+        in_edge.ensure(s * sizeof(int));
+    }
+    template <typename T>
+    DevWork<T> work(int n, long long slots) {
+        const size_t na = static_cast<size_t>(std::max(n, 1));
+        const size_t s = static_cast<size_t>(std::max<long long>(slots, 1));
+        const size_t M = static_cast<size_t>(n_msg());
+        const size_t Mw = std::max<size_t>(M, 1);
+        er.ensure(s * sizeof(T));
+        es.ensure(s * sizeof(T));
+        eds.ensure(s * sizeof(T));
+        eb.ensure(s * kK * sizeof(T));
+        edb.ensure(s * kK * sizeof(T));
+        g.ensure(s * sizeof(T));
+        if (M > 0) {
+            mz1.ensure(M * s * kH * sizeof(T));
+            mo.ensure(M * s * kH * sizeof(T));
+            dmsg.ensure(2 * s * kH * sizeof(T));
+        }
+        desc.ensure(na * 32 * sizeof(T));
+        ez1.ensure(na * kH * sizeof(T));
+        h.ensure((M + 1) * na * kH * sizeof(T));
+        uz1.ensure(Mw * na * kH * sizeof(T));
+        dhown.ensure(na * kH * sizeof(T));
+        DevWork<T> w{};
+        w.er = er.as<T>();
+        w.es = es.as<T>();
+        w.eds = eds.as<T>();
+        w.eb = eb.as<T>();
+        w.edb = edb.as<T>();
+        w.g = g.as<T>();
+        w.mz1 = mz1.as<T>();
+        w.mo = mo.as<T>();
+        w.dmsg = dmsg.as<T>();
+        w.desc = desc.as<T>();
+        w.ez1 = ez1.as<T>();
+        w.h = h.as<T>();
+        w.uz1 = uz1.as<T>();
+        w.dhown = dhown.as<T>();
+        w.e_atom = e_atom.as<double>();
+        w.forces = forces.as<double>();
+        w.partial = partial.as<double>();
+        w.ticket = ticket.as<unsigned>();
+        w.out = out.as<double>();
+        w.slots = static_cast<long long>(s);
+        w.err = err.as<unsigned>();
+        return w;
+    }
+
+    // Cell grid for a periodic box (neighborlist.cpp:21-27) + geometry check (:44-49).
+    CellGrid grid(const double* box, double rc, int n) {
+        for (int a = 0; a < 3; ++a) {
+            if (!(box[a] > 0.0) || !std::isfinite(box[a]))
+                fail(HMDP_INVALID_ARGUMENT, "box lengths must be positive and finite");
+            if (rc > 0.5 * box[a])
+                fail(HMDP_INVALID_ARGUMENT,
+                     "rc+skin exceeds half the box length on axis " + std::to_string(a));
+        }
+        CellGrid cg{};
+        long long ncell = 1;
+        for (int a = 0; a < 3; ++a) {
+            cg.nc[a] = std::max(1, static_cast<int>(std::floor(box[a] / rc)));
+            cg.L[a] = box[a];
+            ncell *= cg.nc[a];
+        }
+        const double avg = static_cast<double>(n) / static_cast<double>(ncell);
+        const int want = static_cast<int>(std::ceil(2.0 * avg)) + 32;
+        ccap = std::max(ccap, (want + 31) / 32 * 32);
+        cg.ccap = ccap;
+        cell_count.ensure(static_cast<size_t>(ncell) * sizeof(int));
+        members.ensure(static_cast<size_t>(ncell) * ccap * sizeof(int));
+        return cg;
+    }
+
+    // Device neighbour list for d_pos (already on the device) into the ELL slots.
+    void neighbors(int n, const double* d_pos, const double* box, double rc, cudaStream_t st) {
+        CellGrid cg = grid(box, rc, n);
+        ensure_edges(static_cast<long long>(n) * cap);
+        long long ncell = 1LL * cg.nc[0] * cg.nc[1] * cg.nc[2];
+        ck(cudaMemsetAsync(cell_count.p, 0, ncell * sizeof(int), st), "memset cells");
+        launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
+                        err.as<unsigned>(), st);
+        launch_nbr_search(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
+                          rc * rc, cap, nnei.as<int>(), row_start.as<int>(), nbr.as<int>(),
+                          dr.as<double>(), err.as<unsigned>(), st);
+        launch_reverse(n, row_start.as<int>(), nnei.as<int>(), nbr.as<int>(), rev.as<int>(),
+                       err.as<unsigned>(), st);
+    }
+
+    DevGraph periodic_graph(int n, const int* d_types) {
+        DevGraph gr{};
+        gr.n = n;
+        gr.row_start = row_start.as<int>();
+        gr.nnei = nnei.as<int>();
+        gr.nbr = nbr.as<int>();
+        gr.dr = dr.as<double>();
+        gr.in_start = row_start.as<int>();
+        gr.in_cnt = nnei.as<int>();
+        gr.in_edge = rev.as<int>();
+        gr.types = d_types;
+        gr.is_ghost = nullptr;
+        return gr;
+    }
+
+    template <typename T>
+    int network(const DevGraph& gr, long long slots, double* d_forces, double* d_per_atom,
+                cudaStream_t st) {
+        DevWork<T> w = work<T>(gr.n, slots);
+        if constexpr (sizeof(T) == 4)
+            return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, out.as<double>(), st);
+        else
+            return launch_network<double>(wd.dev, gr, w, d_forces, d_per_atom, out.as<double>(), st);
+    }
+
+    // Reads and clears the device error word; maps it to the reference's errors.
+    // Returns the raw bits (overflow bits are handled by the caller).
+    unsigned take_err() {
+        unsigned bits = 0;
+        ck(cudaMemcpyAsync(&bits, err.p, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "err D2H");
+        ck(cudaMemsetAsync(err.p, 0, sizeof(unsigned), stream), "err clear");
+        ck(cudaStreamSynchronize(stream), "sync");
+        return bits;
+    }
+    static void raise_bits(unsigned bits) {
+        if (bits & kErrZeroEdge) fail(HMDP_RUNTIME_ERROR, "zero-length edge in NN input");
+        if (bits & kErrNonFinite) fail(HMDP_RUNTIME_ERROR, "non-finite force in MD step");
+        if (bits & kErrAsymmetric)
+            fail(HMDP_RUNTIME_ERROR, "internal error: neighbour list is not symmetric");
+        if (bits & (kErrNbrOverflow | kErrCellOverflow))
+            fail(HMDP_RUNTIME_ERROR, "neighbour capacity overflow");
+    }
+    void grow_for(unsigned bits) {
+        if (bits & kErrNbrOverflow) {
+            if (cap >= 256) fail(HMDP_RUNTIME_ERROR, "more than 256 neighbours within rc for an atom");
+            cap = std::min(256, cap * 2);
+        }
+        if (bits & kErrCellOverflow) ccap *= 2;
+    }
+};
+
+struct hmdp_md {
+    hmdp_ctx* ctx = nullptr;
+    int n = 0;
+    int precision = HMDP_FP32;
+    double dt = 0.001, box[3] = {0, 0, 0};
+    DBuf x, v, f, m, types, energy;
+    int steps_per_graph = 1;
+    std::map<int, cudaGraphExec_t> graphs;
+    ~hmdp_md() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+        for (DBuf* b : {&x, &v, &f, &m, &types, &energy}) b->release();
+    }
+};
+
+namespace {
+
+void check_types(int n, const int* types, int n_types) {
+    for (int i = 0; i < n; ++i)
+        if (types[i] < 0 || types[i] >= n_types)
+            fail(HMDP_INVALID_ARGUMENT, "atom type " + std::to_string(types[i]) + " of atom " +
+                                            std::to_string(i) + " out of range");
+}
+
+void set_device(const hmdp_ctx* ctx) { ck(cudaSetDevice(ctx->device), "cudaSetDevice"); }
+
+void need_model(const hmdp_ctx* ctx) {
+    if (!ctx) fail(HMDP_INVALID_ARGUMENT, "null context");
+    if (!ctx->has_model) fail(HMDP_INVALID_ARGUMENT, "context was created without a model");
+}
+
+// Device half of hmdp_compute_device / the periodic host call: neighbour list +
+// network + reduction, all on `st`.
+int enqueue_periodic(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_types,
+                     const double* box, int precision, double* d_forces, double* d_per_atom,
+                     cudaStream_t st) {
+    ctx->neighbors(n, d_xyz, box, ctx->model.rc, st);
+    const DevGraph gr = ctx->periodic_graph(n, d_types);
+    const long long slots = static_cast<long long>(n) * ctx->cap;
+    const int net = precision == HMDP_FP64
+                        ? ctx->network<double>(gr, slots, d_forces, d_per_atom, st)
+                        : ctx->network<float>(gr, slots, d_forces, d_per_atom, st);
+    return 4 + net;  // memset + bin + search + reverse + network kernels
+}
+
+void copy_outputs(hmdp_ctx* ctx, int n, double* energy, double* per_atom, double* forces,
+                  double* virial9, double* virial) {
+    // pinned staging: out[16] + forces[3n] + per_atom[n]
+    const size_t need = (16 + 4 * static_cast<size_t>(n)) * sizeof(double);
+    ctx->pin.ensure(need);
+    double* hp = static_cast<double*>(ctx->pin.p);
+    cudaStream_t st = ctx->stream;
+    ck(cudaMemcpyAsync(hp, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st), "out D2H");
+    if (n > 0) {
+        ck(cudaMemcpyAsync(hp + 16, ctx->forces.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "forces D2H");
+        if (per_atom)
+            ck(cudaMemcpyAsync(hp + 16 + 3 * n, ctx->e_atom.p, n * sizeof(double),
+                               cudaMemcpyDeviceToHost, st),
+               "per-atom D2H");
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+    *energy = hp[0];
+    if (virial) *virial = hp[1];
+    if (virial9) std::memcpy(virial9, hp + 2, 9 * sizeof(double));
+    if (n > 0) {
+        std::memcpy(forces, hp + 16, 3 * n * sizeof(double));
+        if (per_atom) std::memcpy(per_atom, hp + 16 + 3 * n, n * sizeof(double));
+    }
+}
+
+void zero_outputs(int n, double* energy, double* per_atom, double* forces, double* virial9,
+                  double* virial) {
+    *energy = 0.0;
+    if (virial) *virial = 0.0;
+    if (virial9) std::memset(virial9, 0, 9 * sizeof(double));
+    for (int i = 0; i < 3 * n; ++i) forces[i] = 0.0;
+    if (per_atom)
+        for (int i = 0; i < n; ++i) per_atom[i] = 0.0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// extern "C" boundary
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* hmdp_last_error(void) { return g_err.c_str(); }
+
+int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, int max_neighbors,
+                hmdp_ctx** out) {
+    if (!out) {
+        g_err = "out must not be NULL";
+        return HMDP_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    return guarded([&] {
+        const bool has_model = model_json != nullptr && len > 0;
+        Model m;
+        if (has_model) m = model_from_json(std::string(model_json, len));
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev)
+            fail(HMDP_INVALID_ARGUMENT, "device " + std::to_string(device) + " not present");
+        auto ctx = std::make_unique<hmdp_ctx>();
+        ctx->model = std::move(m);
+        ctx->has_model = has_model;
+        ctx->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
+        if (has_model) {
+            ctx->wf.upload(ctx->model, ctx->stream);
+            ctx->wd.upload(ctx->model, ctx->stream);
+        }
+        ctx->ensure_atoms(std::max(max_atoms, 1));
+        ctx->ensure_edges(static_cast<long long>(std::max(max_atoms, 1)) * ctx->cap);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        *out = ctx.release();
+    });
+}
+
+int hmdp_destroy(hmdp_ctx* ctx) {
+    delete ctx;
+    return HMDP_OK;
+}
+
+int hmdp_model_validate(const char* model_json, size_t len) {
+    return guarded([&] {
+        if (!model_json) fail(HMDP_INVALID_ARGUMENT, "model_json must not be NULL");
+        (void)model_from_json(std::string(model_json, len));
+    });
+}
+
+int hmdp_model_info(const hmdp_ctx* ctx, int* family, int* depth, double* rc, int* n_types,
+                    int* hidden, int* n_basis) {
+    if (!ctx) return HMDP_INVALID_ARGUMENT;
+    if (family) *family = ctx->model.family;
+    if (depth) *depth = ctx->model.depth();
+    if (rc) *rc = ctx->model.rc;
+    if (n_types) *n_types = ctx->model.n_types;
+    if (hidden) *hidden = ctx->model.hidden;
+    if (n_basis) *n_basis = ctx->model.n_basis();
+    return HMDP_OK;
+}
+
+int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, const double* box,
+                 int precision, double* energy, double* per_atom, double* forces, double* virial9,
+                 double* virial) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx) fail(HMDP_INVALID_ARGUMENT, "null context");
+        if (n < 0) fail(HMDP_INVALID_ARGUMENT, "n must be >= 0");
+        if (!energy || !forces || !box || (n > 0 && (!xyz || !types)))
+            fail(HMDP_INVALID_ARGUMENT, "required pointer is NULL");
+        set_device(ctx);
+        if (n == 0) {
+            ctx->grid(box, ctx->model.rc, 0);  // geometry errors still apply
+            zero_outputs(n, energy, per_atom, forces, virial9, virial);
+            return;
+        }
+        check_types(n, types, ctx->model.n_types);
+        ctx->ensure_atoms(n);
+        cudaStream_t st = ctx->stream;
+        ck(cudaMemcpyAsync(ctx->pos.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st),
+           "xyz H2D");
+        ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st),
+           "types H2D");
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            ctx->last_launches =
+                enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(), box,
+                                 precision, ctx->forces.as<double>(), ctx->e_atom.as<double>(), st);
+            ck(cudaGetLastError(), "kernel launch");
+            const unsigned bits = ctx->take_err();
+            if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
+                ctx->grow_for(bits);
+                continue;
+            }
+            hmdp_ctx::raise_bits(bits);
+            copy_outputs(ctx, n, energy, per_atom, forces, virial9, virial);
+            return;
+        }
+        fail(HMDP_RUNTIME_ERROR, "neighbour capacity did not converge");
+    });
+}
+
+int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char* is_ghost,
+                     const int* offset, const int* nbr, const double* dr, double coverage_radius,
+                     int skip_coverage_check, int precision, double* energy, double* per_atom,
+                     double* forces, double* virial9, double* virial, double* desc, double* h,
+                     double* edge_g, uint64_t* counters) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx) fail(HMDP_INVALID_ARGUMENT, "null context");
+        if (n < 0) fail(HMDP_INVALID_ARGUMENT, "n must be >= 0");
+        if (!energy || !forces || !offset || (n > 0 && !types))
+            fail(HMDP_INVALID_ARGUMENT, "required pointer is NULL");
+        // NnInput::check (inference.cpp:19-32)
+        const int ne = offset[n];
+        if (offset[0] != 0 || ne < 0) fail(HMDP_INVALID_ARGUMENT, "NnInput CSR offsets inconsistent");
+        for (int i = 0; i < n; ++i)
+            if (offset[i + 1] < offset[i])
+                fail(HMDP_INVALID_ARGUMENT, "NnInput CSR offsets inconsistent");
+        if (ne > 0 && (!nbr || !dr)) fail(HMDP_INVALID_ARGUMENT, "required pointer is NULL");
+        for (int e = 0; e < ne; ++e)
+            if (nbr[e] < 0 || nbr[e] >= n)
+                fail(HMDP_INVALID_ARGUMENT, "NnInput edge neighbor out of range");
+        check_types(n, types, ctx->model.n_types);
+        // receptive-field check before compute (inference.cpp:188-193)
+        const double needed = ctx->model.receptive_radius();
+        if (!skip_coverage_check && coverage_radius < needed - 1e-12) {
+            char msg[256];
+            std::snprintf(msg, sizeof msg,
+                          "receptive-field error: model needs %f nm of environment but input "
+                          "covers %f nm; widen the halo to L×rc or gather to one rank",
+                          needed, coverage_radius);
+            fail(HMDP_RUNTIME_ERROR, msg);
+        }
+        if (counters) {
+            int n_owned = 0;
+            for (int i = 0; i < n; ++i) n_owned += !(is_ghost && is_ghost[i]);
+            ctx->model.counters(n, n_owned, ne, precision == HMDP_FP64 ? 8 : 4, counters);
+        }
+        set_device(ctx);
+        if (n == 0) {
+            zero_outputs(n, energy, per_atom, forces, virial9, virial);
+            return;
+        }
+        ctx->ensure_atoms(n);
+        ctx->ensure_edges(ne);
+        cudaStream_t st = ctx->stream;
+        ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(ctx->offset.p, offset, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+           "H2D");
+        if (ne > 0) {
+            ck(cudaMemcpyAsync(ctx->nbr.p, nbr, ne * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(ctx->dr.p, dr, 3 * static_cast<size_t>(ne) * sizeof(double),
+                               cudaMemcpyHostToDevice, st),
+               "H2D");
+        }
+        if (is_ghost)
+            ck(cudaMemcpyAsync(ctx->ghost.p, is_ghost, n, cudaMemcpyHostToDevice, st), "H2D");
+        launch_csr_rows(n, ctx->offset.as<int>(), ctx->row_start.as<int>(), ctx->nnei.as<int>(), st);
+        launch_in_edges(n, ne, ctx->nbr.as<int>(), ctx->in_cnt.as<int>(), ctx->in_start.as<int>(),
+                        ctx->cursor.as<int>(), ctx->in_edge.as<int>(), st);
+        DevGraph gr{};
+        gr.n = n;
+        gr.row_start = ctx->row_start.as<int>();
+        gr.nnei = ctx->nnei.as<int>();
+        gr.nbr = ctx->nbr.as<int>();
+        gr.dr = ctx->dr.as<double>();
+        gr.in_start = ctx->in_start.as<int>();
+        gr.in_cnt = ctx->in_cnt.as<int>();
+        gr.in_edge = ctx->in_edge.as<int>();
+        gr.types = ctx->types.as<int>();
+        gr.is_ghost = is_ghost ? ctx->ghost.as<unsigned char>() : nullptr;
+        const long long slots = std::max(ne, 1);
+        const bool f64 = precision == HMDP_FP64;
+        ctx->last_launches = f64 ? ctx->network<double>(gr, slots, ctx->forces.as<double>(),
+                                                        ctx->e_atom.as<double>(), st)
+                                 : ctx->network<float>(gr, slots, ctx->forces.as<double>(),
+                                                       ctx->e_atom.as<double>(), st);
+        ck(cudaGetLastError(), "kernel launch");
+        const unsigned bits = ctx->take_err();
+        hmdp_ctx::raise_bits(bits);
+        copy_outputs(ctx, n, energy, per_atom, forces, virial9, virial);
+        // optional stage outputs
+        const int M = ctx->n_msg(), nd = ctx->model.descriptor_dim();
+        auto fetch = [&](const DBuf& b, size_t count, std::vector<double>& dst) {
+            dst.resize(count);
+            if (f64) {
+                ck(cudaMemcpy(dst.data(), b.p, count * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            } else {
+                std::vector<float> tmp(count);
+                ck(cudaMemcpy(tmp.data(), b.p, count * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+                for (size_t q = 0; q < count; ++q) dst[q] = tmp[q];
+            }
+        };
+        std::vector<double> tmp;
+        if (desc) {
+            fetch(ctx->desc, static_cast<size_t>(n) * 32, tmp);
+            for (int i = 0; i < n; ++i)
+                for (int q = 0; q < nd; ++q) desc[static_cast<size_t>(i) * nd + q] = tmp[i * 32 + q];
+        }
+        if (h) {
+            fetch(ctx->h, static_cast<size_t>(M + 1) * n * kH, tmp);
+            std::memcpy(h, tmp.data(), tmp.size() * sizeof(double));
+        }
+        if (edge_g && ne > 0) {
+            fetch(ctx->g, static_cast<size_t>(ne), tmp);
+            std::memcpy(edge_g, tmp.data(), tmp.size() * sizeof(double));
+        }
+    });
+}
+
+int hmdp_build_neighbors(hmdp_ctx* ctx, int n, const double* xyz, const double* box, double rc,
+                         int cap, int* offset, int* nbr, double* dr, int* n_edges) {
+    return guarded([&] {
+        if (!ctx || !box || !offset || !n_edges || n < 0 || (n > 0 && !xyz))
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(ctx);
+        if (n == 0) {
+            ctx->grid(box, rc, 0);
+            offset[0] = 0;
+            *n_edges = 0;
+            return;
+        }
+        ctx->ensure_atoms(n);
+        cudaStream_t st = ctx->stream;
+        ck(cudaMemcpyAsync(ctx->pos.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        for (int attempt = 0;; ++attempt) {
+            ctx->neighbors(n, ctx->pos.as<double>(), box, rc, st);
+            const unsigned bits = ctx->take_err();
+            if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
+                if (attempt > 8) fail(HMDP_RUNTIME_ERROR, "neighbour capacity did not converge");
+                ctx->grow_for(bits);
+                continue;
+            }
+            hmdp_ctx::raise_bits(bits & ~kErrAsymmetric);
+            break;
+        }
+        std::vector<int> cnt(n);
+        ck(cudaMemcpy(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        const size_t slots = static_cast<size_t>(n) * ctx->cap;
+        std::vector<int> enbr(slots);
+        std::vector<double> edr(slots * 3);
+        ck(cudaMemcpy(enbr.data(), ctx->nbr.p, slots * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(edr.data(), ctx->dr.p, slots * 3 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        offset[0] = 0;
+        for (int i = 0; i < n; ++i) offset[i + 1] = offset[i] + cnt[i];
+        *n_edges = offset[n];
+        if (offset[n] > cap) return;
+        for (int i = 0; i < n; ++i)
+            for (int q = 0; q < cnt[i]; ++q) {
+                const size_t src = static_cast<size_t>(i) * ctx->cap + q;
+                const int dst = offset[i] + q;
+                if (nbr) nbr[dst] = enbr[src];
+                if (dr)
+                    for (int a = 0; a < 3; ++a) dr[3 * dst + a] = edr[3 * src + a];
+            }
+    });
+}
+
+int hmdp_descriptors(hmdp_ctx* ctx, int n, const int* types, const int* offset, const int* nbr,
+                     const double* dr, double* desc) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx || !offset || !desc || n < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        const int ne = offset[n];
+        for (int e = 0; e < ne; ++e)
+            if (nbr[e] < 0 || nbr[e] >= n)
+                fail(HMDP_INVALID_ARGUMENT, "NnInput edge neighbor out of range");
+        check_types(n, types, ctx->model.n_types);
+        if (n == 0) return;
+        set_device(ctx);
+        ctx->ensure_atoms(n);
+        ctx->ensure_edges(ne);
+        cudaStream_t st = ctx->stream;
+        ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(ctx->offset.p, offset, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+           "H2D");
+        if (ne > 0) {
+            ck(cudaMemcpyAsync(ctx->nbr.p, nbr, ne * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(ctx->dr.p, dr, 3 * static_cast<size_t>(ne) * sizeof(double),
+                               cudaMemcpyHostToDevice, st),
+               "H2D");
+        }
+        launch_csr_rows(n, ctx->offset.as<int>(), ctx->row_start.as<int>(), ctx->nnei.as<int>(), st);
+        DevGraph gr{};
+        gr.n = n;
+        gr.row_start = ctx->row_start.as<int>();
+        gr.nnei = ctx->nnei.as<int>();
+        gr.nbr = ctx->nbr.as<int>();
+        gr.dr = ctx->dr.as<double>();
+        gr.types = ctx->types.as<int>();
+        const int nd = ctx->model.descriptor_dim();
+        ctx->desc64.ensure(static_cast<size_t>(n) * nd * sizeof(double));
+        launch_descriptors_f64(ctx->wd.dev, gr, ctx->desc64.as<double>(), st);
+        ck(cudaGetLastError(), "kernel launch");
+        ck(cudaMemcpyAsync(desc, ctx->desc64.p, static_cast<size_t>(n) * nd * sizeof(double),
+                           cudaMemcpyDeviceToHost, st),
+           "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+double hmdp_switch_value(double r, double rc) {
+    const double onset = 0.9 * rc;
+    if (r <= onset) return 1.0;
+    if (r >= rc) return 0.0;
+    return 0.5 * (std::cos(M_PI * (r - onset) / (0.1 * rc)) + 1.0);
+}
+double hmdp_switch_derivative(double r, double rc) {
+    const double onset = 0.9 * rc;
+    if (r <= onset || r >= rc) return 0.0;
+    return -0.5 * std::sin(M_PI * (r - onset) / (0.1 * rc)) * M_PI / (0.1 * rc);
+}
+
+int hmdp_counters(const hmdp_ctx* ctx, int n, int n_owned, long long ne, int precision,
+                  uint64_t* out) {
+    if (!ctx || !out) return HMDP_INVALID_ARGUMENT;
+    ctx->model.counters(n, n_owned, ne, precision == HMDP_FP64 ? 8 : 4, out);
+    return HMDP_OK;
+}
+
+int hmdp_prepare(hmdp_ctx* ctx, int n, const double* box, int precision) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx || n < 1 || !box) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(ctx);
+        ctx->ensure_atoms(n);
+        ctx->grid(box, ctx->model.rc, n);
+        ctx->ensure_edges(static_cast<long long>(n) * ctx->cap);
+        const long long slots = static_cast<long long>(n) * ctx->cap;
+        if (precision == HMDP_FP64)
+            ctx->work<double>(n, slots);
+        else
+            ctx->work<float>(n, slots);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int hmdp_compute_device(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_types,
+                        const double* box, int precision, double* d_energy, double* d_forces,
+                        double* d_virial9, double* d_per_atom, void* stream) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx || n < 1 || !d_xyz || !d_types || !box || !d_forces)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        ctx->last_launches = enqueue_periodic(ctx, n, d_xyz, d_types, box, precision, d_forces,
+                                              d_per_atom, st);
+        if (d_energy)
+            ck(cudaMemcpyAsync(d_energy, ctx->out.p, sizeof(double), cudaMemcpyDeviceToDevice, st),
+               "D2D");
+        if (d_virial9)
+            ck(cudaMemcpyAsync(d_virial9, ctx->out.as<double>() + 2, 9 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st),
+               "D2D");
+        ck(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int hmdp_check(hmdp_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) fail(HMDP_INVALID_ARGUMENT, "null context");
+        set_device(ctx);
+        hmdp_ctx::raise_bits(ctx->take_err());
+    });
+}
+
+int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
+    if (!ctx) return -1;
+    const int M = static_cast<int>(ctx->model.message.size());
+    // bin + search + reverse + (embed | embed + M fwd + M bwd + embed_bwd) + force
+    return 3 + (M == 0 ? 1 : 2 + 2 * M) + 1;
+}
+
+// ---------------------------------------------------------------------------
+// Device MD loop
+// ---------------------------------------------------------------------------
+namespace {
+void md_enqueue_steps(hmdp_md* md, int steps, cudaStream_t st) {
+    hmdp_ctx* ctx = md->ctx;
+    const double half = 0.5 * md->dt;
+    for (int s = 0; s < steps; ++s) {
+        launch_vv_kick_drift(md->n, md->x.as<double>(), md->v.as<double>(), md->f.as<double>(),
+                             md->m.as<double>(), half, md->dt, ctx->err.as<unsigned>(), st);
+        enqueue_periodic(ctx, md->n, md->x.as<double>(), md->types.as<int>(), md->box,
+                         md->precision, md->f.as<double>(), nullptr, st);
+        ck(cudaMemcpyAsync(md->energy.p, ctx->out.p, sizeof(double), cudaMemcpyDeviceToDevice, st),
+           "D2D");
+        launch_vv_kick(md->n, md->v.as<double>(), md->f.as<double>(), md->m.as<double>(), half,
+                       ctx->err.as<unsigned>(), st);
+    }
+}
+}  // namespace
+
+int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
+                   const double* masses, const int* types, const double* box, double dt_ps,
+                   int precision, int steps_per_graph, hmdp_md** out) {
+    if (!out) return HMDP_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx || n < 2 || !xyz || !vel || !masses || !types || !box)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        check_types(n, types, ctx->model.n_types);
+        set_device(ctx);
+        auto md = std::make_unique<hmdp_md>();
+        md->ctx = ctx;
+        md->n = n;
+        md->precision = precision;
+        md->dt = dt_ps;
+        md->steps_per_graph = std::max(1, steps_per_graph);
+        std::memcpy(md->box, box, sizeof md->box);
+        md->x.ensure(3 * n * sizeof(double));
+        md->v.ensure(3 * n * sizeof(double));
+        md->f.ensure(3 * n * sizeof(double));
+        md->m.ensure(n * sizeof(double));
+        md->types.ensure(n * sizeof(int));
+        md->energy.ensure(sizeof(double));
+        cudaStream_t st = ctx->stream;
+        ck(cudaMemcpyAsync(md->x.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(md->v.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(md->m.p, masses, n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(md->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ctx->ensure_atoms(n);
+        // initial forces; sizes the neighbour capacity with headroom before any capture
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            enqueue_periodic(ctx, n, md->x.as<double>(), md->types.as<int>(), box, precision,
+                             md->f.as<double>(), nullptr, st);
+            ck(cudaMemcpyAsync(md->energy.p, ctx->out.p, sizeof(double), cudaMemcpyDeviceToDevice, st),
+               "D2D");
+            const unsigned bits = ctx->take_err();
+            if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
+                ctx->grow_for(bits);
+                continue;
+            }
+            hmdp_ctx::raise_bits(bits);
+            break;
+        }
+        // headroom: degree fluctuates during dynamics; ELL capacity >= 1.5x current max
+        std::vector<int> cnt(n);
+        ck(cudaMemcpy(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        const int maxdeg = *std::max_element(cnt.begin(), cnt.end());
+        const int want = std::min(256, std::max(ctx->cap, (3 * maxdeg / 2 + 7) / 8 * 8));
+        if (want > ctx->cap) ctx->cap = want;
+        const long long slots = static_cast<long long>(n) * ctx->cap;
+        ctx->ensure_edges(slots);
+        if (precision == HMDP_FP64)
+            ctx->work<double>(n, slots);
+        else
+            ctx->work<float>(n, slots);
+        ctx->grid(box, ctx->model.rc, n);
+        ck(cudaStreamSynchronize(st), "sync");
+        *out = md.release();
+    });
+}
+
+int hmdp_md_run(hmdp_md* md, int steps) {
+    return guarded([&] {
+        if (!md || steps < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        hmdp_ctx* ctx = md->ctx;
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        int left = steps;
+        while (left > 0) {
+            const int chunk = std::min(left, md->steps_per_graph);
+            auto it = md->graphs.find(chunk);
+            if (it == md->graphs.end()) {
+                cudaGraph_t graph;
+                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+                md_enqueue_steps(md, chunk, st);
+                ck(cudaStreamEndCapture(st, &graph), "end capture");
+                cudaGraphExec_t exec;
+                ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+                cudaGraphDestroy(graph);
+                it = md->graphs.emplace(chunk, exec).first;
+            }
+            ck(cudaGraphLaunch(it->second, st), "graph launch");
+            left -= chunk;
+        }
+        hmdp_ctx::raise_bits(ctx->take_err());
+    });
+}
+
+int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* epot) {
+    return guarded([&] {
+        if (!md) fail(HMDP_INVALID_ARGUMENT, "null md");
+        set_device(md->ctx);
+        cudaStream_t st = md->ctx->stream;
+        const size_t b = 3 * static_cast<size_t>(md->n) * sizeof(double);
+        if (xyz) ck(cudaMemcpyAsync(xyz, md->x.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (vel) ck(cudaMemcpyAsync(vel, md->v.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (forces) ck(cudaMemcpyAsync(forces, md->f.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (epot) ck(cudaMemcpyAsync(epot, md->energy.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int hmdp_md_destroy(hmdp_md* md) {
+    if (md) {
+        cudaSetDevice(md->ctx->device);
+        delete md;
+    }
+    return HMDP_OK;
+}
+
+long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_basis, int hidden,
+                          uint64_t seed, char* buf, long cap) {
+    std::string s;
+    const int code = guarded([&] {
+        if (family != 0 && family != 1) fail(HMDP_INVALID_ARGUMENT, "family must be 0 or 1");
+        s = model_to_json(make_model(family, depth, rc, n_types, n_basis, hidden, seed));
+    });
+    if (code) return -code;
+    if (buf && cap > static_cast<long>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<long>(s.size());
+}
+
+int hmdp_synthetic_system(int n, double density, double fraction_grouped, uint64_t seed,
+                          double temperature, double* xyz, int* types, double* masses, double* vel,
+                          double* box) {
+    return guarded([&] {
+        SyntheticSystem s = synthetic_system(n, density, fraction_grouped, seed, temperature);
+        if (xyz) std::memcpy(xyz, s.xyz.data(), s.xyz.size() * sizeof(double));
+        if (vel) std::memcpy(vel, s.vel.data(), s.vel.size() * sizeof(double));
+        if (masses) std::memcpy(masses, s.masses.data(), s.masses.size() * sizeof(double));
+        if (types) std::memcpy(types, s.types.data(), s.types.size() * sizeof(int));
+        if (box) std::memcpy(box, s.box, sizeof s.box);
+    });
+}
+
+}  // extern "C"

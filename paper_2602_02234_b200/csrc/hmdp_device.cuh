@@ -1,0 +1,100 @@
+// hmdp_device.cuh — device-side data structures shared by the kernels and the
+// host orchestration (hmdp_api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hmdp_model.h"
+
+namespace hmdp {
+
+// Device error word bits (latched with atomicOr, read back after each call).
+enum : unsigned {
+    kErrNbrOverflow = 1u << 0,   // an atom has more neighbours than the ELL capacity
+    kErrCellOverflow = 1u << 1,  // a cell has more members than the cell capacity
+    kErrZeroEdge = 1u << 2,      // zero-length edge (inference.cpp:221)
+    kErrAsymmetric = 1u << 3,    // reverse edge missing in a "symmetric" list
+    kErrNonFinite = 1u << 4,     // non-finite force (integrators.cpp:12-18)
+};
+
+// One two-layer MLP [in, 32, out] on the device, stored both row-major (as in
+// the model file, [out][in]) and transposed ([in][out]) so that the warp
+// kernels always read contiguous rows.
+template <typename T>
+struct DevMlp {
+    const T* W1;   // [32][in]
+    const T* W1T;  // [in][32]
+    const T* b1;   // [32]
+    const T* W2;   // [out][32]
+    const T* W2T;  // [32][out]
+    const T* b2;   // [out]
+};
+
+template <typename T>
+struct DevModel {
+    DevMlp<T> embed, fit;
+    DevMlp<T> msg[kMaxMsg], upd[kMaxMsg];
+    T mu[kK];
+    T rc;       // T(model.rc_model)
+    T width;    // T(basis.width)
+    T inv2w2;   // T(1)/(T(2)*width*width)  (inference.cpp:164)
+    T invw2;    // T(1)/(width*width)        (inference.cpp:174)
+    int n_types;
+    int n_msg;
+};
+
+// Directed edge graph of one evaluation.  Out-edges of atom i occupy slots
+// [row_start[i], row_start[i] + nnei[i]) sorted by neighbour index; in-edges
+// (edges e = (k -> i)) are listed in in_edge[in_start[i] .. + in_cnt[i]).
+// For the symmetric periodic list in_start/in_cnt alias row_start/nnei and
+// in_edge[e] = rev(e), the slot of the mirrored edge.
+struct DevGraph {
+    int n;
+    const int* row_start;
+    const int* nnei;
+    const int* nbr;
+    const double* dr;  // [slot][3], r_j - r_i image-corrected (FP64)
+    const int* in_start;
+    const int* in_cnt;
+    const int* in_edge;
+    const int* types;
+    const unsigned char* is_ghost;  // nullable
+};
+
+// Per-evaluation device workspace (element type T for the network tensors).
+template <typename T>
+struct DevWork {
+    // per edge slot
+    T* er;    // r
+    T* es;    // s(r)
+    T* eds;   // s'(r)
+    T* eb;    // [slot][8] b_k
+    T* edb;   // [slot][8] b_k'
+    T* g;     // dE/dr
+    T* mz1;   // [M][slot][32] message hidden (tanh) activations
+    T* mo;    // [M][slot][32] message outputs
+    T* dmsg;  // [2][slot][32] adjoint w.r.t. h_j of each edge (double-buffered)
+    // per atom
+    T* desc;   // [n][32] descriptor (n_types*8 used)
+    T* ez1;    // [n][32] embedding hidden activations
+    T* h;      // [M+1][n][32]
+    T* uz1;    // [M][n][32] update hidden activations
+    T* dhown;  // [n][32] atom-local part of dE/dh
+    double* e_atom;   // [n]
+    double* forces;   // [n][3]
+    double* partial;  // [blocks][16] per-block E, W, W9
+    unsigned* ticket;
+    double* out;  // [16]: E, W, W9[9]
+    long long slots;  // edge-slot capacity of the per-edge arrays
+    unsigned* err;
+};
+
+struct CellGrid {
+    int nc[3];
+    double L[3];
+    int ccap;
+};
+
+}  // namespace hmdp

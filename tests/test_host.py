@@ -1,0 +1,99 @@
+"""Host-side checks that need no GPU: the C-ABI library loads and exports every
+symbol include/hmdp.h declares; the host fixtures (make_model, synthetic box)
+reproduce the reference bit-for-bit; model validation mirrors model.cpp."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2602_02234_b200 as P
+from paper_2602_02234_b200 import _lib
+from conftest import ROOT, load_golden
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "hmdp.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hmdp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+        assert s in _lib.SIGNATURES, f"{s} missing from the ctypes binding"
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+def test_make_model_matches_reference_json(golden_models):
+    for name, fam, depth in [("dpa2", 0, 1), ("dpa3", 1, 3)]:
+        ref = json.loads(golden_models[name])
+        ours = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1).as_dict()
+        for key in ("family", "rc_model", "n_types", "hidden", "seed"):
+            assert ours[key] == ref[key]
+        assert ours["basis"] == ref["basis"]
+        for net in ("embedding", "fitting"):
+            assert ours[net] == ref[net]  # bit-exact weights (mt19937_64 draw order)
+        assert ours["layers"] == ref["layers"]
+
+
+def test_model_json_roundtrip(golden_models):
+    m = P.model_from_json(golden_models["dpa3"])
+    m2 = P.model_from_json(P.model_to_json(m))
+    assert m2.as_dict() == m.as_dict()
+    assert m.depth() == 3 and m.receptive_radius() == pytest.approx(1.8)
+    assert m.n_params() == 13697
+    assert P.model_from_json(golden_models["dpa2"]).n_params() == 2689
+
+
+@pytest.mark.parametrize("name", ["n64", "1YRF"])
+def test_synthetic_system_matches_reference(name):
+    g = load_golden(name)
+    s = P.generate_synthetic_system(g["types"].shape[0])
+    assert np.array_equal(s.positions, g["positions"])
+    assert np.array_equal(s.velocities, g["velocities"])
+    assert np.array_equal(s.types, g["types"])
+    assert np.array_equal(s.masses, g["masses"])
+    assert np.array_equal(s.box, g["box"])
+
+
+def test_model_validation_errors(golden_models):
+    d = json.loads(golden_models["dpa2"])
+    with pytest.raises(ValueError, match="not a halomd model file"):
+        P.model_from_json(json.dumps(dict(d, format="x")))
+    with pytest.raises(ValueError, match="unsupported model version 2"):
+        P.model_from_json(json.dumps(dict(d, version=2)))
+    with pytest.raises(ValueError, match="unknown model family 'foo'"):
+        P.model_from_json(json.dumps(dict(d, family="foo")))
+    bad = json.loads(golden_models["dpa2"])
+    bad["embedding"]["weights"][0] = bad["embedding"]["weights"][0][:-1]
+    with pytest.raises(ValueError, match="MLP weight shape mismatch"):
+        P.model_from_json(json.dumps(bad))
+    with pytest.raises(ValueError, match="model JSON parse error"):
+        P.model_from_json("{not json")
+    with pytest.raises(ValueError, match="embed_fit has depth 1"):
+        P.make_model(P.ModelFamily.embed_fit, 2, 0.6, 2, 8, 32, 1)
+    with pytest.raises(ValueError, match="depth must be >= 1"):
+        P.make_model(P.ModelFamily.message_passing, 0, 0.6, 2, 8, 32, 1)
+
+
+def test_switch_functions_match_reference():
+    s = dict(np.load(os.path.join(ROOT, "tests", "golden", "switch.npz")))
+    for r, v, d in zip(s["r"], s["value"], s["derivative"]):
+        assert P.switch_value(r, 0.6) == v
+        assert P.switch_derivative(r, 0.6) == d
+
+
+def test_replicate_box():
+    s = P.generate_synthetic_system(64)
+    r = P.replicate(s, (2, 1, 1))
+    assert r.n_atoms == 128 and np.allclose(r.box, s.box * [2, 1, 1])
+    assert np.array_equal(r.positions[64:], s.positions + [s.box[0], 0, 0])
