@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""bench.py — DP force-evaluation MD throughput on B200 (contract in the task brief).
+
+Workload (BASELINE.json configs[1]): DPA3 analog (make_model(message_passing, 3,
+0.6, 2, 8, 32, seed 1)) on the synthetic 1YRF-shaped protein-in-water box
+(582 atoms, generate_synthetic_system seed 7), velocity-Verlet MD at dt = 1 fs,
+neighbour list rebuilt every step (skin 0, as build_input_periodic), each step =
+kick+drift, cell-list neighbour search, full DP energy/force/virial evaluation,
+kick -- one CUDA graph per step.
+
+  value      steps/s over all ranks (N independent replica boxes = weak scaling),
+             each timed step bracketed by CUDA events on the launching stream,
+             L2 flushed (256 MiB write) before every step outside the events.
+  e2e        the same MD through the host-buffer C-ABI call (ForceProvider ->
+             hmdp_compute): pinned H2D positions/types + D2H forces/energy every
+             step, host integration, timed with CUDA events around the loop.
+  roofline   dominant kernel from per-kernel CUDA events (hmdp_profile) in the
+             same graph-per-step loop; achieved = reference-counter FLOPs of that
+             kernel / its mean duration; peak = FP32 FFMA throughput measured
+             here (the kernels are FP32 SIMT, parity-mode precision).
+  cpu_baseline  the reference compiled from its own sources (oracle/_ref), same
+             MD workload, one replica per host thread.
+
+  --impl reference   times only the reference CPU path (rank 0) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODELS = {"dpa2": (0, 1), "dpa3": (1, 3)}
+SYSTEMS = {"1YRF": 582, "1UBQ": 1231, "3LZM": 2643, "2PTC": 4114}
+METRIC = "DPA2/DPA3 force-eval steps/s & ns/day at 1/2/4/8 B200 vs CPU ref; %roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", choices=list(MODELS), default="dpa3")
+    ap.add_argument("--system", choices=list(SYSTEMS), default="1YRF")
+    ap.add_argument("--replicas", type=str, default="1,1,1", help="periodic replication per rank")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def ns_per_day(steps_per_s, dt_fs=1.0):
+    return steps_per_s * dt_fs * 1e-6 * 86400.0
+
+
+# ---------------------------------------------------------------------------
+# algorithmic FLOPs per kernel: the reference counter (inference.cpp:389-414)
+# split along our kernel boundaries; the sum over kernels equals the counter.
+# ---------------------------------------------------------------------------
+def mlp_flops(sizes):
+    return sum(2 * a * b + 4 * b for a, b in zip(sizes[:-1], sizes[1:]))
+
+
+def kernel_flops(model_dict, n, n_owned, ne):
+    H = model_dict["hidden"]
+    K = len(model_dict["basis"]["centers"])
+    fe = mlp_flops(model_dict["embedding"]["sizes"])
+    ff = mlp_flops(model_dict["fitting"]["sizes"])
+    layers = model_dict["layers"]
+    M = len(layers)
+    out = {}
+    if M == 0:
+        out["embed_fit"] = ne * (20 + 10 * K) + 3 * n * fe + 3 * n_owned * ff
+        return out
+    fm = [mlp_flops(l["message"]["sizes"]) for l in layers]
+    fu = [mlp_flops(l["update"]["sizes"]) for l in layers]
+    out["embed"] = ne * (20 + 10 * K) + n * fe
+    out["msg_fwd"] = sum(ne * fm[l] + n * fu[l] for l in range(M - 1)) / max(M - 1, 1)
+    out["msg_fwd_last"] = ne * fm[-1] + n * fu[-1] + 3 * n_owned * ff
+    bwd = [ne * (2 * fm[l] + 6 * H + 3 * K) + n * (2 * fu[l] + 2 * H) for l in range(M)]
+    out["msg_bwd_top"] = bwd[-1]
+    out["msg_bwd"] = sum(bwd[:-1]) / max(M - 1, 1)
+    out["embed_bwd"] = 2 * n * fe
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                s, m, u = float(r[0]), float(r[1]), float(r[2])
+            except ValueError:
+                continue
+            mx.append(m)
+            if u > 0:
+                sm.append(s)
+            for k, name in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref): P concurrent replicas of the same MD workload
+# ---------------------------------------------------------------------------
+def reference_md(model_name, system, steps, warmup, precision, threads, replicas=(1, 1, 1)):
+    import numpy as np
+
+    import oracle as O
+    import paper_2602_02234_b200 as P
+
+    fam, depth = MODELS[model_name]
+    s = P.generate_synthetic_system(SYSTEMS[system])
+    if tuple(replicas) != (1, 1, 1):
+        s = P.replicate(s, replicas)
+    if O.ref_available():
+        rm = O.RefModel(O.ref_model_json(fam, depth))
+        kind = "reference"
+        if warmup:
+            O.ref_md(rm, s.positions, s.velocities, s.types, s.masses, s.box, prec=precision,
+                     steps=warmup, threads=threads)
+        wall, x, v, ep = O.ref_md(rm, s.positions, s.velocities, s.types, s.masses, s.box,
+                                  prec=precision, steps=steps, threads=threads)
+        return steps * threads / wall, wall, kind
+    # fallback: the plain-C restatement, one thread (a scalar port)
+    m = json.loads(P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1).to_json())
+    x, v = s.positions.copy(), s.velocities.copy()
+    half, dt = 0.0005, 0.001
+    f = O.evaluate(m, s.types, *O.neighbors(x, s.box, 0.6), prec=precision)["forces"]
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        v += f * (half / s.masses[:, None])
+        x += v * dt
+        f = O.evaluate(m, s.types, *O.neighbors(x, s.box, 0.6), prec=precision)["forces"]
+        v += f * (half / s.masses[:, None])
+    wall = time.perf_counter() - t0
+    return steps / wall, wall, "port"
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = cpu_count()
+    sps, wall, kind = reference_md(args.model, args.system, args.steps, args.warmup,
+                                   args.precision, threads)
+    n = SYSTEMS[args.system]
+    sample = (f"{args.model} {args.system} ({n} atoms) velocity-Verlet MD, {args.steps} timed "
+              f"steps per replica x {threads} concurrent replicas (one per host thread), "
+              f"{args.precision}")
+    line = {
+        "metric": METRIC, "value": sps, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / sps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
+        "config": {"workload": f"{args.model.upper()} MD step loop on {args.system}-shaped box",
+                   "model": args.model, "system": args.system, "atoms": n,
+                   "precision": args.precision},
+        "impl": "reference",
+        "ns_per_day": ns_per_day(sps),
+        "cpu_baseline": {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": sps, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank, dist):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2602_02234_b200 as P
+    from paper_2602_02234_b200._lib import check, lib
+    from paper_2602_02234_b200.md import DeviceMD
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # one explicit (non-default) stream carries everything: torch's L2 flush and
+    # CUDA events, and every libhmdp launch (hmdp_set_stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    L = lib()
+    fam, depth = MODELS[args.model]
+    prec = P.Precision[args.precision]
+    model = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
+    s = P.generate_synthetic_system(SYSTEMS[args.system])
+    reps = tuple(int(v) for v in args.replicas.split(","))
+    if reps != (1, 1, 1):
+        s = P.replicate(s, reps)
+    n = s.n_atoms
+    ctx = P.Context(model, device=local_rank, max_atoms=n)
+    check(L.hmdp_set_stream(ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
+    inp = P.build_input_periodic(s.positions, s.types, np.arange(n), s.box, 0.6, device=local_rank)
+    ne = int(inp.edge_offset[-1])
+    per_step_kernels = ctx.kernels_per_eval() + 2  # + the two velocity-Verlet kernels
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    md = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
+                  steps_per_graph=1)
+    enqueue = L.hmdp_md_enqueue
+    for _ in range(args.warmup):
+        check(enqueue(md.handle, 1))
+    torch.cuda.synchronize(dev)
+    check(L.hmdp_check(ctx.handle))
+
+    # ---- timed region: one graph launch per MD step, L2 flushed between steps ----
+    K = args.steps
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    wall0 = time.perf_counter()
+    for k in range(K):
+        flush.zero_()
+        ev0[k].record(stream)
+        check(enqueue(md.handle, 1))
+        ev1[k].record(stream)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    t_ms = float(sum(step_ms))
+    check(L.hmdp_check(ctx.handle))
+    if dist:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = world * K / (t_ms * 1e-3)
+
+    # ---- warm-L2 multi-step graph (context, not the headline) ----
+    md_warm = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
+                       steps_per_graph=100)
+    check(enqueue(md_warm.handle, 100))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    check(enqueue(md_warm.handle, 1000))
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    warm_sps = 1000 / (e0.elapsed_time(e1) * 1e-3)
+    md_warm.close()
+
+    # ---- per-kernel timing (events inside the per-step graph) -> roofline ----
+    check(L.hmdp_profile(ctx.handle, 1))
+    md_prof = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
+                       steps_per_graph=1)
+    KP = min(K, 200)
+    sums: dict[str, float] = {}
+    counts: dict[str, int] = {}
+    buf = (ctypes.c_float * 64)()
+    cnt = ctypes.c_int()
+    for k in range(KP + 5):
+        flush.zero_()
+        check(enqueue(md_prof.handle, 1))
+        check(L.hmdp_profile_read(ctx.handle, buf, 64, ctypes.byref(cnt)))
+        if k < 5:
+            continue
+        for i in range(cnt.value):
+            name = L.hmdp_profile_name(ctx.handle, i).decode()
+            sums[name] = sums.get(name, 0.0) + buf[i]
+            counts[name] = counts.get(name, 0) + 1
+    check(L.hmdp_profile(ctx.handle, 0))
+    md_prof.close()
+    if sampler:
+        clocks = sampler.stop()
+    kern_ms = {k: sums[k] / counts[k] for k in sums}
+    kflops = kernel_flops(model.as_dict(), n, n, ne)
+    # FLOP-carrying kernels; the dominant one is the slowest of them
+    cands = {k: v for k, v in kern_ms.items() if k in kflops}
+    dom = max(cands, key=cands.get)
+    peak = ctypes.c_double()
+    check(L.hmdp_peak_fp32(local_rank, 200, ctypes.byref(peak)))
+    achieved = kflops[dom] / (kern_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.model, {}).get(args.system, {}).get(dom)
+        except Exception:
+            traffic = None
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as f:
+        try:
+            mp = json.load(f)
+        except Exception:
+            mp = {}
+
+    # ---- e2e: host-buffer C-ABI provider, host integration ----
+    KE = min(K, 300)
+    prov_ctx = P.Context(model, device=local_rank, max_atoms=n)
+    check(L.hmdp_set_stream(prov_ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
+    xh = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+    th = torch.empty((n,), dtype=torch.int32, pin_memory=True).numpy()
+    xh[:] = s.positions
+    th[:] = s.types
+    vh = s.velocities.copy()
+    inv_m = (0.0005 / s.masses)[:, None]
+    out = prov_ctx.compute(xh, th, s.box, prec)
+    fh = out.forces
+    for _ in range(5):
+        prov_ctx.compute(xh, th, s.box, prec)
+    e0.record(stream)
+    for _ in range(KE):
+        vh += fh * inv_m
+        xh += vh * 0.001
+        out = prov_ctx.compute(xh, th, s.box, prec)
+        fh = out.forces
+        vh += fh * inv_m
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world * KE / (e2e_ms * 1e-3)
+    h2d = xh.nbytes + th.nbytes
+    d2h = out.forces.nbytes + 11 * 8
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = cpu_count()
+        # bounded sample: ~cpu_seconds of wall on all host threads
+        per_step = 0.2 if args.model == "dpa3" else 0.012
+        per_step *= n / 582
+        steps_cpu = max(2, int(args.cpu_seconds / per_step))
+        sps, cwall, kind = reference_md(args.model, args.system, steps_cpu, 1, args.precision,
+                                        threads, reps)
+        cpu = {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind,
+               "sample": f"{steps_cpu} MD steps x {threads} concurrent replicas of the same "
+                         f"{n}-atom box, {args.precision}, {cwall:.1f} s wall"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": t_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
+        "config": {"workload": f"{args.model.upper()} MD step loop on {args.system}-shaped box "
+                               f"(graph per step, nbr rebuild every step)",
+                   "model": args.model, "system": args.system, "atoms": n, "edges": ne,
+                   "replicas_per_rank": list(reps), "precision": args.precision,
+                   "parallelism": f"replicas x{world}",
+                   "l2": "flushed (256 MiB write) before every timed step, outside the events"},
+        "ns_per_day": ns_per_day(value),
+        "warm_l2_graph100": {"steps_per_s": warm_sps, "ns_per_day": ns_per_day(warm_sps),
+                             "note": "100 steps per graph, L2 not flushed, 1 rank"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak.value,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
+                     "kernel": dom, "flops_per_launch": kflops[dom],
+                     "mean_launch_us": kern_ms[dom] * 1e3,
+                     "peak_kind": "measured FP32 FFMA (SIMT) throughput, hmdp_peak_fp32; the "
+                                  "kernels run FP32 FMA, not tensor cores",
+                     "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None},
+        "kernels_us": {k: v * 1e3 for k, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},
+        "gpu_launches": per_step_kernels * K,
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "ForceProvider -> hmdp_compute (pinned host xyz/types in, forces/E out), "
+                        "host velocity Verlet"},
+        "cpu_baseline": cpu,
+        "clocks": clocks if sampler else None,
+        "wall_s_timed_region": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+
+        td.init_process_group("nccl", init_method="env://")
+        dist = td
+    try:
+        run_ours(args, rank, world, local_rank, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

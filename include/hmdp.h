@@ -161,9 +161,29 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
                    const double* masses, const int* types, const double* box, double dt_ps,
                    int precision, int steps_per_graph, hmdp_md** out);
 int hmdp_md_run(hmdp_md* md, int steps);
+/* Asynchronous variant: enqueues the steps on the context's stream and returns;
+ * errors are reported by the next hmdp_check / hmdp_md_run / hmdp_md_get. */
+int hmdp_md_enqueue(hmdp_md* md, int steps);
 /* Copies the current state back; any pointer may be NULL. */
 int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* epot);
 int hmdp_md_destroy(hmdp_md* md);
+
+/* ---------------------------------------------------------------------------
+ * Measurement hooks.
+ * hmdp_set_stream: run the context's work on an external cudaStream_t (e.g. the
+ *   caller's current stream) instead of its own (NULL restores it).
+ * hmdp_profile: when enabled, a CUDA event is recorded after every kernel of an
+ *   evaluation / MD step (also inside captured graphs); hmdp_profile_read returns
+ *   the per-kernel durations (ms) of the most recent execution and
+ *   hmdp_profile_name(i) the i-th kernel's name.
+ * hmdp_peak_fp32: measured FP32 FFMA throughput of the device (TFLOP/s), the
+ *   roofline denominator for the SIMT kernels.
+ * ------------------------------------------------------------------------- */
+int hmdp_set_stream(hmdp_ctx* ctx, void* stream);
+int hmdp_profile(hmdp_ctx* ctx, int enable);
+int hmdp_profile_read(hmdp_ctx* ctx, float* ms, int cap, int* count);
+const char* hmdp_profile_name(const hmdp_ctx* ctx, int i);
+int hmdp_peak_fp32(int device, int ms, double* tflops);
 
 /* ---------------------------------------------------------------------------
  * Host fixtures (no device work).

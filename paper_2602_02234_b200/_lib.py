@@ -51,6 +51,12 @@ SIGNATURES = {
     "hmdp_md_create": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_double, _c_int, _c_int,
                                 ctypes.POINTER(_vp)]),
     "hmdp_md_run": (_c_int, [_vp, _c_int]),
+    "hmdp_md_enqueue": (_c_int, [_vp, _c_int]),
+    "hmdp_set_stream": (_c_int, [_vp, _vp]),
+    "hmdp_profile": (_c_int, [_vp, _c_int]),
+    "hmdp_profile_read": (_c_int, [_vp, _vp, _c_int, _vp]),
+    "hmdp_profile_name": (_cp, [_vp, _c_int]),
+    "hmdp_peak_fp32": (_c_int, [_c_int, _c_int, _vp]),
     "hmdp_md_get": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "hmdp_md_destroy": (_c_int, [_vp]),
     "hmdp_make_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_int, _c_int, _c_int,

@@ -26,16 +26,14 @@ namespace hmdp {
 void launch_cell_bin(int, const double*, const CellGrid&, int*, int*, int*, unsigned*, cudaStream_t);
 void launch_nbr_search(int, const double*, const CellGrid&, const int*, const int*, const int*,
                        double, int, int*, int*, int*, double*, unsigned*, cudaStream_t);
-void launch_reverse(int, const int*, const int*, const int*, int*, unsigned*, cudaStream_t);
 void launch_csr_rows(int, const int*, int*, int*, cudaStream_t);
 void launch_in_edges(int, int, const int*, int*, int*, int*, int*, cudaStream_t);
 template <typename T>
 int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, double*, double*,
-                   double*, cudaStream_t);
+                   double*, int*, cudaStream_t, const Marker&, const MdFuse&);
+void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cudaStream_t);
+double probe_fp32_tflops(int ms);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
-void launch_vv_kick_drift(int, double*, double*, const double*, const double*, double, double,
-                          unsigned*, cudaStream_t);
-void launch_vv_kick(int, double*, const double*, const double*, double, unsigned*, cudaStream_t);
 }  // namespace hmdp
 
 using namespace hmdp;
@@ -141,10 +139,20 @@ struct WeightSet {
                 for (int i = 0; i < in; ++i) t[static_cast<size_t>(i) * out + o] = w[o * in + i];
             return t;
         };
-        auto push_mlp = [&](const Mlp& p) {
+        // pad_in > in zero-pads the input dimension (the embedding's n_types*K
+        // inputs are padded to 32 so every atom mat-vec is 32 wide)
+        auto pad_cols = [](const std::vector<double>& w, int rows, int in, int pad) {
+            std::vector<double> t(static_cast<size_t>(rows) * pad, 0.0);
+            for (int r = 0; r < rows; ++r)
+                for (int c = 0; c < in; ++c) t[static_cast<size_t>(r) * pad + c] = w[r * in + c];
+            return t;
+        };
+        auto push_mlp = [&](const Mlp& p, int pad_in) {
             const int in = p.sizes[0], hid = p.sizes[1], out = p.sizes[2];
-            push(p.weights[0]);
-            push(transpose(p.weights[0], hid, in));
+            const int ip = std::max(in, pad_in);
+            const std::vector<double> w1 = pad_cols(p.weights[0], hid, in, ip);
+            push(w1);
+            push(transpose(w1, hid, ip));
             push(p.biases[0]);
             push(p.weights[1]);
             push(transpose(p.weights[1], out, hid));
@@ -155,7 +163,7 @@ struct WeightSet {
             order.push_back(&m.message[l]);
             order.push_back(&m.update[l]);
         }
-        for (const Mlp* p : order) push_mlp(*p);
+        for (size_t q = 0; q < order.size(); ++q) push_mlp(*order[q], q == 0 ? kH : 0);
         align();
         buf.ensure(host.size() * sizeof(T));
         ck(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, st),
@@ -212,21 +220,58 @@ struct hmdp_ctx {
     DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev;
     DBuf offset, in_start, in_cnt, cursor, in_edge;
     // network workspace
-    DBuf er, es, eds, eb, edb, g, mz1, mo, dmsg, desc, ez1, h, uz1, dhown;
+    DBuf er, es, eds, eb, edb, g, zb, db, pb, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     PinnedBuf pin;
     int last_launches = 0;
+    cudaStream_t user_stream = nullptr;  // hmdp_set_stream; NULL = own stream
+    // per-kernel timing (hmdp_profile): event k is recorded after kernel k
+    bool prof = false;
+    int pcount = 0;
+    std::vector<cudaEvent_t> pev;
+    std::vector<std::string> pname;
+
+    cudaStream_t st() const { return user_stream ? user_stream : stream; }
+    static void mark_cb(void* self, const char* name, cudaStream_t s) {
+        static_cast<hmdp_ctx*>(self)->mark(name, s);
+    }
+    void mark(const char* name, cudaStream_t s) {
+        if (!prof) return;
+        if (pcount >= static_cast<int>(pev.size())) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "event");
+            pev.push_back(e);
+            pname.emplace_back();
+        }
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        ck(cudaStreamIsCapturing(s, &cs), "capture status");
+        if (cs == cudaStreamCaptureStatusActive)  // an event-record node inside the graph
+            ck(cudaEventRecordWithFlags(pev[pcount], s, cudaEventRecordExternal), "event record");
+        else
+            ck(cudaEventRecord(pev[pcount], s), "event record");
+        pname[pcount] = name;
+        ++pcount;
+    }
+    Marker marker() {
+        Marker m;
+        if (prof) {
+            m.fn = &hmdp_ctx::mark_cb;
+            m.user = this;
+        }
+        return m;
+    }
 
     ~hmdp_ctx() {
         cudaSetDevice(device);
         for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
                         &nbr, &dr, &rev, &offset, &in_start, &in_cnt, &cursor, &in_edge, &er, &es,
-                        &eds, &eb, &edb, &g, &mz1, &mo, &dmsg, &desc, &ez1, &h, &uz1, &dhown,
+                        &eds, &eb, &edb, &g, &zb, &db, &pb, &desc, &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64})
             b->release();
         wf.buf.release();
         wd.buf.release();
         pin.release();
+        for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -246,7 +291,7 @@ struct hmdp_ctx {
         cursor.ensure(na * sizeof(int));
         e_atom.ensure(na * sizeof(double));
         forces.ensure(na * 3 * sizeof(double));
-        const size_t nb = (na + 3) / 4;
+        const size_t nb = std::max<size_t>(na, 4096);  // >= atom_grid(n) CTAs
         partial.ensure(nb * 16 * sizeof(double));
         if (!ticket.p) {
             ticket.ensure(sizeof(unsigned));
@@ -278,9 +323,9 @@ struct hmdp_ctx {
         edb.ensure(s * kK * sizeof(T));
         g.ensure(s * sizeof(T));
         if (M > 0) {
-            mz1.ensure(M * s * kH * sizeof(T));
-            mo.ensure(M * s * kH * sizeof(T));
-            dmsg.ensure(2 * s * kH * sizeof(T));
+            zb.ensure(M * s * kH * sizeof(T));
+            db.ensure(2 * s * kH * sizeof(T));
+            pb.ensure(2 * na * kH * sizeof(T));
         }
         desc.ensure(na * 32 * sizeof(T));
         ez1.ensure(na * kH * sizeof(T));
@@ -294,9 +339,9 @@ struct hmdp_ctx {
         w.eb = eb.as<T>();
         w.edb = edb.as<T>();
         w.g = g.as<T>();
-        w.mz1 = mz1.as<T>();
-        w.mo = mo.as<T>();
-        w.dmsg = dmsg.as<T>();
+        w.z = zb.as<T>();
+        w.d = db.as<T>();
+        w.p = pb.as<T>();
         w.desc = desc.as<T>();
         w.ez1 = ez1.as<T>();
         w.h = h.as<T>();
@@ -332,24 +377,39 @@ struct hmdp_ctx {
         const int want = static_cast<int>(std::ceil(2.0 * avg)) + 32;
         ccap = std::max(ccap, (want + 31) / 32 * 32);
         cg.ccap = ccap;
-        cell_count.ensure(static_cast<size_t>(ncell) * sizeof(int));
+        if (cell_count.bytes < static_cast<size_t>(ncell) * sizeof(int)) {
+            cell_count.ensure(static_cast<size_t>(ncell) * sizeof(int));
+            ck(cudaMemsetAsync(cell_count.p, 0, cell_count.bytes, st()), "memset cells");
+        }
         members.ensure(static_cast<size_t>(ncell) * ccap * sizeof(int));
         return cg;
     }
 
     // Device neighbour list for d_pos (already on the device) into the ELL slots.
+    // Invariant between operations: cell counts are zero (cleared by the embed
+    // kernel, or by the memset here when no network runs after the search).
     void neighbors(int n, const double* d_pos, const double* box, double rc, cudaStream_t st) {
         CellGrid cg = grid(box, rc, n);
         ensure_edges(static_cast<long long>(n) * cap);
-        long long ncell = 1LL * cg.nc[0] * cg.nc[1] * cg.nc[2];
-        ck(cudaMemsetAsync(cell_count.p, 0, ncell * sizeof(int), st), "memset cells");
+        ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
+        mark("memset_cells", st);
         launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
                         err.as<unsigned>(), st);
+        mark("cell_bin", st);
+        search(n, d_pos, cg, rc, st);
+    }
+    void search(int n, const double* d_pos, const CellGrid& cg, double rc, cudaStream_t st) {
         launch_nbr_search(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
                           rc * rc, cap, nnei.as<int>(), row_start.as<int>(), nbr.as<int>(),
                           dr.as<double>(), err.as<unsigned>(), st);
-        launch_reverse(n, row_start.as<int>(), nnei.as<int>(), nbr.as<int>(), rev.as<int>(),
-                       err.as<unsigned>(), st);
+        mark("nbr_search", st);
+    }
+    static long long ncells(const CellGrid& cg) { return 1LL * cg.nc[0] * cg.nc[1] * cg.nc[2]; }
+    MdFuse zeroing(const CellGrid& cg) {
+        MdFuse mf;
+        mf.cell_count = cell_count.as<int>();
+        mf.n_cells_zero = static_cast<int>(ncells(cg));
+        return mf;
     }
 
     DevGraph periodic_graph(int n, const int* d_types) {
@@ -369,21 +429,23 @@ struct hmdp_ctx {
 
     template <typename T>
     int network(const DevGraph& gr, long long slots, double* d_forces, double* d_per_atom,
-                cudaStream_t st) {
+                cudaStream_t st, int* d_rev, const MdFuse& mf) {
         DevWork<T> w = work<T>(gr.n, slots);
         if constexpr (sizeof(T) == 4)
-            return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, out.as<double>(), st);
+            return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, out.as<double>(),
+                                         d_rev, st, marker(), mf);
         else
-            return launch_network<double>(wd.dev, gr, w, d_forces, d_per_atom, out.as<double>(), st);
+            return launch_network<double>(wd.dev, gr, w, d_forces, d_per_atom, out.as<double>(),
+                                          d_rev, st, marker(), mf);
     }
 
     // Reads and clears the device error word; maps it to the reference's errors.
     // Returns the raw bits (overflow bits are handled by the caller).
     unsigned take_err() {
         unsigned bits = 0;
-        ck(cudaMemcpyAsync(&bits, err.p, sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "err D2H");
-        ck(cudaMemsetAsync(err.p, 0, sizeof(unsigned), stream), "err clear");
-        ck(cudaStreamSynchronize(stream), "sync");
+        ck(cudaMemcpyAsync(&bits, err.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st()), "err D2H");
+        ck(cudaMemsetAsync(err.p, 0, sizeof(unsigned), st()), "err clear");
+        ck(cudaStreamSynchronize(st()), "sync");
         return bits;
     }
     static void raise_bits(unsigned bits) {
@@ -411,6 +473,8 @@ struct hmdp_md {
     DBuf x, v, f, m, types, energy;
     int steps_per_graph = 1;
     std::map<int, cudaGraphExec_t> graphs;
+    cudaStream_t graph_stream = nullptr;
+    bool graph_prof = false;
     ~hmdp_md() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
         for (DBuf* b : {&x, &v, &f, &m, &types, &energy}) b->release();
@@ -437,14 +501,20 @@ void need_model(const hmdp_ctx* ctx) {
 // network + reduction, all on `st`.
 int enqueue_periodic(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_types,
                      const double* box, int precision, double* d_forces, double* d_per_atom,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool reset_marks = true) {
+    if (reset_marks) {
+        ctx->pcount = 0;
+        ctx->mark("begin", st);
+    }
     ctx->neighbors(n, d_xyz, box, ctx->model.rc, st);
     const DevGraph gr = ctx->periodic_graph(n, d_types);
     const long long slots = static_cast<long long>(n) * ctx->cap;
-    const int net = precision == HMDP_FP64
-                        ? ctx->network<double>(gr, slots, d_forces, d_per_atom, st)
-                        : ctx->network<float>(gr, slots, d_forces, d_per_atom, st);
-    return 4 + net;  // memset + bin + search + reverse + network kernels
+    const MdFuse mf = ctx->zeroing(ctx->grid(box, ctx->model.rc, n));
+    const int net =
+        precision == HMDP_FP64
+            ? ctx->network<double>(gr, slots, d_forces, d_per_atom, st, ctx->rev.as<int>(), mf)
+            : ctx->network<float>(gr, slots, d_forces, d_per_atom, st, ctx->rev.as<int>(), mf);
+    return 2 + net;  // bin + search + network kernels (+ one memset node)
 }
 
 void copy_outputs(hmdp_ctx* ctx, int n, double* energy, double* per_atom, double* forces,
@@ -453,7 +523,7 @@ void copy_outputs(hmdp_ctx* ctx, int n, double* energy, double* per_atom, double
     const size_t need = (16 + 4 * static_cast<size_t>(n)) * sizeof(double);
     ctx->pin.ensure(need);
     double* hp = static_cast<double*>(ctx->pin.p);
-    cudaStream_t st = ctx->stream;
+    cudaStream_t st = ctx->st();
     ck(cudaMemcpyAsync(hp, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st), "out D2H");
     if (n > 0) {
         ck(cudaMemcpyAsync(hp + 16, ctx->forces.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st),
@@ -566,7 +636,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
         }
         check_types(n, types, ctx->model.n_types);
         ctx->ensure_atoms(n);
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(ctx->pos.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st),
            "xyz H2D");
         ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st),
@@ -633,7 +703,7 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
         }
         ctx->ensure_atoms(n);
         ctx->ensure_edges(ne);
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(ctx->offset.p, offset, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
            "H2D");
@@ -662,9 +732,9 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
         const long long slots = std::max(ne, 1);
         const bool f64 = precision == HMDP_FP64;
         ctx->last_launches = f64 ? ctx->network<double>(gr, slots, ctx->forces.as<double>(),
-                                                        ctx->e_atom.as<double>(), st)
+                                                        ctx->e_atom.as<double>(), st, nullptr, MdFuse{})
                                  : ctx->network<float>(gr, slots, ctx->forces.as<double>(),
-                                                       ctx->e_atom.as<double>(), st);
+                                                       ctx->e_atom.as<double>(), st, nullptr, MdFuse{});
         ck(cudaGetLastError(), "kernel launch");
         const unsigned bits = ctx->take_err();
         hmdp_ctx::raise_bits(bits);
@@ -711,7 +781,7 @@ int hmdp_build_neighbors(hmdp_ctx* ctx, int n, const double* xyz, const double* 
             return;
         }
         ctx->ensure_atoms(n);
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(ctx->pos.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         for (int attempt = 0;; ++attempt) {
             ctx->neighbors(n, ctx->pos.as<double>(), box, rc, st);
@@ -724,6 +794,8 @@ int hmdp_build_neighbors(hmdp_ctx* ctx, int n, const double* xyz, const double* 
             hmdp_ctx::raise_bits(bits & ~kErrAsymmetric);
             break;
         }
+        // restore the zero-cell-count invariant (no network kernel ran to clear them)
+        ck(cudaMemsetAsync(ctx->cell_count.p, 0, ctx->cell_count.bytes, st), "memset cells");
         std::vector<int> cnt(n);
         ck(cudaMemcpy(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
         const size_t slots = static_cast<size_t>(n) * ctx->cap;
@@ -760,7 +832,7 @@ int hmdp_descriptors(hmdp_ctx* ctx, int n, const int* types, const int* offset, 
         set_device(ctx);
         ctx->ensure_atoms(n);
         ctx->ensure_edges(ne);
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(ctx->offset.p, offset, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
            "H2D");
@@ -821,7 +893,7 @@ int hmdp_prepare(hmdp_ctx* ctx, int n, const double* box, int precision) {
             ctx->work<double>(n, slots);
         else
             ctx->work<float>(n, slots);
-        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        ck(cudaStreamSynchronize(ctx->st()), "sync");
     });
 }
 
@@ -832,7 +904,7 @@ int hmdp_compute_device(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_
         need_model(ctx);
         if (!ctx || n < 1 || !d_xyz || !d_types || !box || !d_forces)
             fail(HMDP_INVALID_ARGUMENT, "bad arguments");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->st();
         ctx->last_launches = enqueue_periodic(ctx, n, d_xyz, d_types, box, precision, d_forces,
                                               d_per_atom, st);
         if (d_energy)
@@ -857,8 +929,8 @@ int hmdp_check(hmdp_ctx* ctx) {
 int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
     if (!ctx) return -1;
     const int M = static_cast<int>(ctx->model.message.size());
-    // bin + search + reverse + (embed | embed + M fwd + M bwd + embed_bwd) + force
-    return 3 + (M == 0 ? 1 : 2 + 2 * M) + 1;
+    // bin + search + (embed_fit | embed + M fwd + (M-1) bwd + embed_bwd) + force
+    return 2 + (M == 0 ? 1 : 2 + 2 * M - 1) + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -866,17 +938,33 @@ int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
 // ---------------------------------------------------------------------------
 namespace {
 void md_enqueue_steps(hmdp_md* md, int steps, cudaStream_t st) {
+    // chunk = [kick+drift+bin] then per step [search, network..., force+kicks(+drift+bin)];
+    // the last step of the chunk closes with the second half kick only, so the
+    // state between chunks is a complete velocity-Verlet step.
     hmdp_ctx* ctx = md->ctx;
-    const double half = 0.5 * md->dt;
+    const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
+    MdFuse mf = ctx->zeroing(cg);
+    mf.x = md->x.as<double>();
+    mf.v = md->v.as<double>();
+    mf.m = md->m.as<double>();
+    mf.half = 0.5 * md->dt;
+    mf.dt = md->dt;
+    mf.cg = cg;
+    mf.members = ctx->members.as<int>();
+    mf.cell_of = ctx->cell_of.as<int>();
+    ctx->pcount = 0;
+    ctx->mark("step_begin", st);
+    launch_vv_kick_drift_bin(md->n, mf, md->f.as<double>(), ctx->err.as<unsigned>(), st);
+    ctx->mark("vv_kick_drift_bin", st);
+    const DevGraph gr = ctx->periodic_graph(md->n, md->types.as<int>());
+    const long long slots = static_cast<long long>(md->n) * ctx->cap;
     for (int s = 0; s < steps; ++s) {
-        launch_vv_kick_drift(md->n, md->x.as<double>(), md->v.as<double>(), md->f.as<double>(),
-                             md->m.as<double>(), half, md->dt, ctx->err.as<unsigned>(), st);
-        enqueue_periodic(ctx, md->n, md->x.as<double>(), md->types.as<int>(), md->box,
-                         md->precision, md->f.as<double>(), nullptr, st);
-        ck(cudaMemcpyAsync(md->energy.p, ctx->out.p, sizeof(double), cudaMemcpyDeviceToDevice, st),
-           "D2D");
-        launch_vv_kick(md->n, md->v.as<double>(), md->f.as<double>(), md->m.as<double>(), half,
-                       ctx->err.as<unsigned>(), st);
+        ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st);
+        mf.mode = s + 1 < steps ? 2 : 1;
+        if (md->precision == HMDP_FP64)
+            ctx->network<double>(gr, slots, md->f.as<double>(), nullptr, st, ctx->rev.as<int>(), mf);
+        else
+            ctx->network<float>(gr, slots, md->f.as<double>(), nullptr, st, ctx->rev.as<int>(), mf);
     }
 }
 }  // namespace
@@ -905,7 +993,7 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         md->m.ensure(n * sizeof(double));
         md->types.ensure(n * sizeof(int));
         md->energy.ensure(sizeof(double));
-        cudaStream_t st = ctx->stream;
+        cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(md->x.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(md->v.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(md->m.p, masses, n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
@@ -943,30 +1031,52 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
     });
 }
 
+namespace {
+cudaGraphExec_t md_graph(hmdp_md* md, int chunk, cudaStream_t st) {
+    auto it = md->graphs.find(chunk);
+    if (it != md->graphs.end() && md->graph_stream == st && md->graph_prof == md->ctx->prof)
+        return it->second;
+    if (md->graph_stream != st || md->graph_prof != md->ctx->prof) {
+        for (auto& kv : md->graphs) cudaGraphExecDestroy(kv.second);
+        md->graphs.clear();
+        md->graph_stream = st;
+        md->graph_prof = md->ctx->prof;
+    }
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    md_enqueue_steps(md, chunk, st);
+    ck(cudaStreamEndCapture(st, &graph), "end capture");
+    cudaGraphExec_t exec;
+    ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+    cudaGraphDestroy(graph);
+    md->graphs[chunk] = exec;
+    return exec;
+}
+void md_launch(hmdp_md* md, int steps) {
+    hmdp_ctx* ctx = md->ctx;
+    set_device(ctx);
+    cudaStream_t st = ctx->st();
+    int left = steps;
+    while (left > 0) {
+        const int chunk = std::min(left, md->steps_per_graph);
+        ck(cudaGraphLaunch(md_graph(md, chunk, st), st), "graph launch");
+        left -= chunk;
+    }
+}
+}  // namespace
+
 int hmdp_md_run(hmdp_md* md, int steps) {
     return guarded([&] {
         if (!md || steps < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
-        hmdp_ctx* ctx = md->ctx;
-        set_device(ctx);
-        cudaStream_t st = ctx->stream;
-        int left = steps;
-        while (left > 0) {
-            const int chunk = std::min(left, md->steps_per_graph);
-            auto it = md->graphs.find(chunk);
-            if (it == md->graphs.end()) {
-                cudaGraph_t graph;
-                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-                md_enqueue_steps(md, chunk, st);
-                ck(cudaStreamEndCapture(st, &graph), "end capture");
-                cudaGraphExec_t exec;
-                ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
-                cudaGraphDestroy(graph);
-                it = md->graphs.emplace(chunk, exec).first;
-            }
-            ck(cudaGraphLaunch(it->second, st), "graph launch");
-            left -= chunk;
-        }
-        hmdp_ctx::raise_bits(ctx->take_err());
+        md_launch(md, steps);
+        hmdp_ctx::raise_bits(md->ctx->take_err());
+    });
+}
+
+int hmdp_md_enqueue(hmdp_md* md, int steps) {
+    return guarded([&] {
+        if (!md || steps < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        md_launch(md, steps);
     });
 }
 
@@ -974,12 +1084,12 @@ int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* e
     return guarded([&] {
         if (!md) fail(HMDP_INVALID_ARGUMENT, "null md");
         set_device(md->ctx);
-        cudaStream_t st = md->ctx->stream;
+        cudaStream_t st = md->ctx->st();
         const size_t b = 3 * static_cast<size_t>(md->n) * sizeof(double);
         if (xyz) ck(cudaMemcpyAsync(xyz, md->x.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         if (vel) ck(cudaMemcpyAsync(vel, md->v.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         if (forces) ck(cudaMemcpyAsync(forces, md->f.p, b, cudaMemcpyDeviceToHost, st), "D2H");
-        if (epot) ck(cudaMemcpyAsync(epot, md->energy.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        if (epot) ck(cudaMemcpyAsync(epot, md->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
     });
 }
@@ -990,6 +1100,44 @@ int hmdp_md_destroy(hmdp_md* md) {
         delete md;
     }
     return HMDP_OK;
+}
+
+int hmdp_set_stream(hmdp_ctx* ctx, void* stream) {
+    if (!ctx) return HMDP_INVALID_ARGUMENT;
+    ctx->user_stream = static_cast<cudaStream_t>(stream);
+    return HMDP_OK;
+}
+
+int hmdp_profile(hmdp_ctx* ctx, int enable) {
+    if (!ctx) return HMDP_INVALID_ARGUMENT;
+    ctx->prof = enable != 0;
+    ctx->pcount = 0;
+    return HMDP_OK;
+}
+
+int hmdp_profile_read(hmdp_ctx* ctx, float* ms, int cap, int* count) {
+    return guarded([&] {
+        if (!ctx || !count) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(ctx);
+        ck(cudaStreamSynchronize(ctx->st()), "sync");
+        const int k = std::max(0, ctx->pcount - 1);
+        *count = k;
+        for (int i = 0; i < k && i < cap; ++i)
+            ck(cudaEventElapsedTime(ms + i, ctx->pev[i], ctx->pev[i + 1]), "elapsed");
+    });
+}
+
+const char* hmdp_profile_name(const hmdp_ctx* ctx, int i) {
+    if (!ctx || i < 0 || i + 1 >= ctx->pcount) return "";
+    return ctx->pname[i + 1].c_str();
+}
+
+int hmdp_peak_fp32(int device, int ms, double* tflops) {
+    return guarded([&] {
+        if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        *tflops = probe_fp32_tflops(ms);
+    });
 }
 
 long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_basis, int hidden,

@@ -1,0 +1,180 @@
+// hmdp_common.cuh — device helpers shared by the neighbour-search and network
+// kernels (math overloads for the FP32/FP64 template paths, vector loads, warp
+// reductions, the switch function, FP64 geometry with explicit rounding).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "hmdp_device.cuh"
+
+namespace hmdp {
+
+#define FULL_MASK 0xffffffffu
+constexpr int kAT = 128;       // threads per atom-CTA (4 warps)
+constexpr int kCandMax = 512;  // neighbour candidates kept per atom
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float d_tanh(float x) { return tanhf(x); }
+__device__ __forceinline__ double d_tanh(double x) { return tanh(x); }
+__device__ __forceinline__ float d_exp(float x) { return expf(x); }
+__device__ __forceinline__ double d_exp(double x) { return exp(x); }
+__device__ __forceinline__ float d_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double d_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float d_cos(float x) { return cosf(x); }
+__device__ __forceinline__ double d_cos(double x) { return cos(x); }
+__device__ __forceinline__ float d_sin(float x) { return sinf(x); }
+__device__ __forceinline__ double d_sin(double x) { return sin(x); }
+
+template <typename T>
+struct V4 {
+    T x, y, z, w;
+};
+__device__ __forceinline__ V4<float> ld4(const float* p) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    return {v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ V4<double> ld4(const double* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return {a.x, a.y, b.x, b.y};
+}
+// coherent (non-.nc) variant for buffers written earlier in the same kernel
+__device__ __forceinline__ V4<float> ld4c(const float* p) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    return {v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ V4<double> ld4c(const double* p) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *(reinterpret_cast<const double2*>(p) + 1);
+    return {a.x, a.y, b.x, b.y};
+}
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+    *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+    reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+// switch_value_t / switch_derivative_t (inference.cpp:49-62), in T.
+template <typename T>
+__device__ __forceinline__ T sw_val(T r, T rc) {
+    const T onset = T(0.9) * rc;
+    if (r <= onset) return T(1);
+    if (r >= rc) return T(0);
+    return T(0.5) * (d_cos(T(M_PI) * (r - onset) / (T(0.1) * rc)) + T(1));
+}
+template <typename T>
+__device__ __forceinline__ T sw_der(T r, T rc) {
+    const T onset = T(0.9) * rc;
+    if (r <= onset || r >= rc) return T(0);
+    return T(-0.5) * d_sin(T(M_PI) * (r - onset) / (T(0.1) * rc)) * T(M_PI) / (T(0.1) * rc);
+}
+
+// Edge geometry in T from the FP64 displacement (to_vec<T> + norm, inference.cpp:219-223).
+template <typename T>
+__device__ __forceinline__ T edge_len(const double* dr3, T& x, T& y, T& z) {
+    x = static_cast<T>(dr3[0]);
+    y = static_cast<T>(dr3[1]);
+    z = static_cast<T>(dr3[2]);
+    return d_sqrt(x * x + y * y + z * z);
+}
+
+// FP64 helpers with explicit rounding (no FMA contraction) for the bit-exact
+// neighbour test: minimum_image (box.hpp:24-31) and norm2 (vec3.hpp:57-70).
+__device__ __forceinline__ double min_image1(double d, double L) {
+    return __dsub_rn(d, __dmul_rn(L, rint(__ddiv_rn(d, L))));
+}
+__device__ __forceinline__ double norm2_rn(double x, double y, double z) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+}
+
+
+// ---------------------------------------------------------------------------
+// Atom-CTA (128 threads) mat-vec: y[o] = sum_{k<NIN} W[o*ldw + k] * x[k] for
+// o < NOUT, with x in shared memory.  Thread t computes the partial sum of part
+// p = t % P (P = 128/NOUT parts of NIN/P consecutive inputs) for output
+// o = t / P; the P partials sit in adjacent lanes and are combined with xor
+// shuffles, so every thread of the group returns y[o].  Weights are read
+// through L1 (every CTA of an SM shares them); the vector is an smem broadcast.
+// ---------------------------------------------------------------------------
+template <typename T, int NOUT, int NIN>
+__device__ __forceinline__ T bmv(const T* __restrict__ W, int ldw, const T* xs, int t) {
+    constexpr int P = kAT / NOUT;
+    constexpr int KP = NIN / P;
+    static_assert(P * NOUT == kAT && KP * P == NIN && KP % 4 == 0, "bad bmv shape");
+    const int o = t / P, p = t % P;
+    const T* wr = W + o * ldw + p * KP;
+    const T* xr = xs + p * KP;
+    T acc = T(0);
+#pragma unroll
+    for (int q = 0; q < KP; q += 4) {
+        const V4<T> w = ld4(wr + q);
+        acc += w.x * xr[q];
+        acc += w.y * xr[q + 1];
+        acc += w.z * xr[q + 2];
+        acc += w.w * xr[q + 3];
+    }
+#pragma unroll
+    for (int m = 1; m < P; m <<= 1) acc += __shfl_xor_sync(FULL_MASK, acc, m);
+    return acc;
+}
+// output index and "group leader" flag of thread t for an NOUT-output bmv
+template <int NOUT>
+__device__ __forceinline__ int bmv_out(int t) { return t / (kAT / NOUT); }
+template <int NOUT>
+__device__ __forceinline__ bool bmv_lead(int t) { return (t % (kAT / NOUT)) == 0; }
+
+// Sum over the 128 threads of a CTA (every thread gets the total); s4 is a
+// 4-entry shared scratch.  Fixed order: warp tree, then warps 0..3.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* s4) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s4[w] = v;
+    __syncthreads();
+    return ((s4[0] + s4[1]) + s4[2]) + s4[3];
+}
+
+// cell of a position: wrap_position, then static_cast<int>(r / L * n_cells)
+// clamped (neighborlist.cpp:31-33), in exactly rounded FP64 (no contraction)
+__device__ __forceinline__ int cell_index(const double* x3, const CellGrid& cg) {
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double L = cg.L[a];
+        double r = x3[a];
+        r = __dsub_rn(r, __dmul_rn(L, floor(__ddiv_rn(r, L))));
+        if (r >= L) r = 0.0;
+        int v = static_cast<int>(__dmul_rn(__ddiv_rn(r, L), static_cast<double>(cg.nc[a])));
+        v = v < 0 ? 0 : (v > cg.nc[a] - 1 ? cg.nc[a] - 1 : v);
+        c[a] = v;
+    }
+    return (c[2] * cg.nc[1] + c[1]) * cg.nc[0] + c[0];
+}
+
+__device__ __forceinline__ void bin_atom(int i, const double* x3, const CellGrid& cg, int* cell_count,
+                         int* members, int* cell_of, unsigned* err) {
+    const int cid = cell_index(x3, cg);
+    cell_of[i] = cid;
+    const int slot = atomicAdd(cell_count + cid, 1);
+    if (slot < cg.ccap)
+        members[cid * cg.ccap + slot] = i;
+    else
+        atomicOr(err, kErrCellOverflow);
+}
+
+}  // namespace hmdp

@@ -73,13 +73,13 @@ struct DevWork {
     T* eb;    // [slot][8] b_k
     T* edb;   // [slot][8] b_k'
     T* g;     // dE/dr
-    T* mz1;   // [M][slot][32] message hidden (tanh) activations
-    T* mo;    // [M][slot][32] message outputs
-    T* dmsg;  // [2][slot][32] adjoint w.r.t. h_j of each edge (double-buffered)
+    T* z;     // [M][slot][32] message hidden (tanh) activations z_e
+    T* d;     // [2][slot][32] adjoint of z_e pre-activation (double-buffered by layer)
     // per atom
     T* desc;   // [n][32] descriptor (n_types*8 used)
     T* ez1;    // [n][32] embedding hidden activations
     T* h;      // [M+1][n][32]
+    T* p;      // [2][n][32] W1h^(l) h^(l): neighbour projection of message layer l
     T* uz1;    // [M][n][32] update hidden activations
     T* dhown;  // [n][32] atom-local part of dE/dh
     double* e_atom;   // [n]
@@ -91,10 +91,40 @@ struct DevWork {
     unsigned* err;
 };
 
+// Optional per-kernel timing hook: called after every kernel launch with the
+// kernel's name (records a CUDA event when profiling is enabled; capturable).
+struct Marker {
+    void (*fn)(void*, const char*, cudaStream_t) = nullptr;
+    void* user = nullptr;
+    void operator()(const char* name, cudaStream_t st) const {
+        if (fn) fn(user, name, st);
+    }
+};
+
 struct CellGrid {
     int nc[3];
     double L[3];
     int ccap;
+};
+
+// Velocity-Verlet work fused into the force kernel (device MD loop):
+//   mode 0: none
+//   mode 1: second half kick            v += F * (dt/2)/m
+//   mode 2: second half kick, then the next step's first half kick, drift and
+//           cell binning:  v += F*(dt/2)/m; v += F*(dt/2)/m; x += v*dt; bin(x)
+// (integrators.cpp:32-47, with the finite-force check of :12-18 on F).
+// zero_cells (embed kernel): cell counts to clear once the search consumed them.
+struct MdFuse {
+    int mode = 0;
+    double* x = nullptr;
+    double* v = nullptr;
+    const double* m = nullptr;
+    double half = 0.0, dt = 0.0;
+    CellGrid cg{};
+    int* cell_count = nullptr;
+    int* members = nullptr;
+    int* cell_of = nullptr;
+    int n_cells_zero = 0;  // > 0: embed kernel zeroes cell_count[0..n)
 };
 
 }  // namespace hmdp
