@@ -25,7 +25,9 @@ namespace hmdp {
 // launchers (hmdp_kernels.cu)
 void launch_cell_bin(int, const double*, const CellGrid&, int*, int*, int*, unsigned*, cudaStream_t);
 void launch_nbr_search(int, const double*, const CellGrid&, const int*, const int*, const int*,
-                       double, int, int*, int*, int*, double*, unsigned*, cudaStream_t);
+                       double, int, int*, int*, int*, double*, const int*, int*, unsigned*,
+                       cudaStream_t);
+void launch_edge_meta(int, const int*, const int*, int*, const int*, int*, cudaStream_t);
 void launch_csr_rows(int, const int*, int*, int*, cudaStream_t);
 void launch_in_edges(int, int, const int*, int*, int*, int*, int*, cudaStream_t);
 template <typename T>
@@ -33,6 +35,7 @@ int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, doubl
                    double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cudaStream_t);
 double probe_fp32_tflops(int ms);
+cudaError_t net_configure();
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
 
@@ -217,10 +220,10 @@ struct hmdp_ctx {
     int cap = 64;      // per-atom neighbour capacity (ELL)
     int ccap = 32;     // per-cell member capacity
     // atom / edge / cell buffers
-    DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev;
+    DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev, ety, inv_pos;
     DBuf offset, in_start, in_cnt, cursor, in_edge;
     // network workspace
-    DBuf er, es, eds, eb, edb, g, zb, db, pb, desc, ez1, h, uz1, dhown;
+    DBuf er, es, eds, eb, edb, g, grev, zb, db, pe, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     PinnedBuf pin;
     int last_launches = 0;
@@ -264,8 +267,9 @@ struct hmdp_ctx {
     ~hmdp_ctx() {
         cudaSetDevice(device);
         for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
-                        &nbr, &dr, &rev, &offset, &in_start, &in_cnt, &cursor, &in_edge, &er, &es,
-                        &eds, &eb, &edb, &g, &zb, &db, &pb, &desc, &ez1, &h, &uz1, &dhown,
+                        &nbr, &dr, &rev, &ety, &inv_pos, &offset, &in_start, &in_cnt, &cursor,
+                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
+                        &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64})
             b->release();
         wf.buf.release();
@@ -308,6 +312,8 @@ struct hmdp_ctx {
         nbr.ensure(s * sizeof(int));
         dr.ensure(s * 3 * sizeof(double));
         rev.ensure(s * sizeof(int));
+        ety.ensure(s * sizeof(int));
+        inv_pos.ensure(s * sizeof(int));
         in_edge.ensure(s * sizeof(int));
     }
     template <typename T>
@@ -322,10 +328,11 @@ struct hmdp_ctx {
         eb.ensure(s * kK * sizeof(T));
         edb.ensure(s * kK * sizeof(T));
         g.ensure(s * sizeof(T));
+        grev.ensure(s * sizeof(T));
         if (M > 0) {
             zb.ensure(M * s * kH * sizeof(T));
             db.ensure(2 * s * kH * sizeof(T));
-            pb.ensure(2 * na * kH * sizeof(T));
+            pe.ensure(2 * s * kH * sizeof(T));
         }
         desc.ensure(na * 32 * sizeof(T));
         ez1.ensure(na * kH * sizeof(T));
@@ -339,9 +346,10 @@ struct hmdp_ctx {
         w.eb = eb.as<T>();
         w.edb = edb.as<T>();
         w.g = g.as<T>();
+        w.grev = grev.as<T>();
         w.z = zb.as<T>();
         w.d = db.as<T>();
-        w.p = pb.as<T>();
+        w.pe = pe.as<T>();
         w.desc = desc.as<T>();
         w.ez1 = ez1.as<T>();
         w.h = h.as<T>();
@@ -388,7 +396,8 @@ struct hmdp_ctx {
     // Device neighbour list for d_pos (already on the device) into the ELL slots.
     // Invariant between operations: cell counts are zero (cleared by the embed
     // kernel, or by the memset here when no network runs after the search).
-    void neighbors(int n, const double* d_pos, const double* box, double rc, cudaStream_t st) {
+    void neighbors(int n, const double* d_pos, const double* box, double rc, cudaStream_t st,
+                   const int* d_types = nullptr) {
         CellGrid cg = grid(box, rc, n);
         ensure_edges(static_cast<long long>(n) * cap);
         ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
@@ -396,12 +405,15 @@ struct hmdp_ctx {
         launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
                         err.as<unsigned>(), st);
         mark("cell_bin", st);
-        search(n, d_pos, cg, rc, st);
+        search(n, d_pos, cg, rc, st, d_types);
     }
-    void search(int n, const double* d_pos, const CellGrid& cg, double rc, cudaStream_t st) {
+    // d_types (nullable): also record each edge's neighbour type (DevGraph::ety)
+    void search(int n, const double* d_pos, const CellGrid& cg, double rc, cudaStream_t st,
+                const int* d_types) {
         launch_nbr_search(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
                           rc * rc, cap, nnei.as<int>(), row_start.as<int>(), nbr.as<int>(),
-                          dr.as<double>(), err.as<unsigned>(), st);
+                          dr.as<double>(), d_types, d_types ? ety.as<int>() : nullptr,
+                          err.as<unsigned>(), st);
         mark("nbr_search", st);
     }
     static long long ncells(const CellGrid& cg) { return 1LL * cg.nc[0] * cg.nc[1] * cg.nc[2]; }
@@ -415,13 +427,16 @@ struct hmdp_ctx {
     DevGraph periodic_graph(int n, const int* d_types) {
         DevGraph gr{};
         gr.n = n;
+        gr.sym = 1;
         gr.row_start = row_start.as<int>();
         gr.nnei = nnei.as<int>();
         gr.nbr = nbr.as<int>();
+        gr.ety = ety.as<int>();
         gr.dr = dr.as<double>();
         gr.in_start = row_start.as<int>();
         gr.in_cnt = nnei.as<int>();
-        gr.in_edge = rev.as<int>();
+        gr.in_edge = rev.as<int>();  // written by the embed kernel
+        gr.inv_pos = rev.as<int>();
         gr.types = d_types;
         gr.is_ghost = nullptr;
         return gr;
@@ -506,7 +521,7 @@ int enqueue_periodic(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_typ
         ctx->pcount = 0;
         ctx->mark("begin", st);
     }
-    ctx->neighbors(n, d_xyz, box, ctx->model.rc, st);
+    ctx->neighbors(n, d_xyz, box, ctx->model.rc, st, d_types);
     const DevGraph gr = ctx->periodic_graph(n, d_types);
     const long long slots = static_cast<long long>(n) * ctx->cap;
     const MdFuse mf = ctx->zeroing(ctx->grid(box, ctx->model.rc, n));
@@ -583,6 +598,7 @@ int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, i
         ctx->device = device;
         ck(cudaSetDevice(device), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        ck(net_configure(), "kernel smem configuration");
         if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
         if (has_model) {
             ctx->wf.upload(ctx->model, ctx->stream);
@@ -727,6 +743,11 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
         gr.in_start = ctx->in_start.as<int>();
         gr.in_cnt = ctx->in_cnt.as<int>();
         gr.in_edge = ctx->in_edge.as<int>();
+        gr.sym = 0;
+        gr.ety = ctx->ety.as<int>();
+        gr.inv_pos = ctx->inv_pos.as<int>();
+        launch_edge_meta(ne, ctx->nbr.as<int>(), ctx->types.as<int>(), ctx->ety.as<int>(),
+                         ctx->in_edge.as<int>(), ctx->inv_pos.as<int>(), st);
         gr.types = ctx->types.as<int>();
         gr.is_ghost = is_ghost ? ctx->ghost.as<unsigned char>() : nullptr;
         const long long slots = std::max(ne, 1);
@@ -959,7 +980,7 @@ void md_enqueue_steps(hmdp_md* md, int steps, cudaStream_t st) {
     const DevGraph gr = ctx->periodic_graph(md->n, md->types.as<int>());
     const long long slots = static_cast<long long>(md->n) * ctx->cap;
     for (int s = 0; s < steps; ++s) {
-        ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st);
+        ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st, md->types.as<int>());
         mf.mode = s + 1 < steps ? 2 : 1;
         if (md->precision == HMDP_FP64)
             ctx->network<double>(gr, slots, md->f.as<double>(), nullptr, st, ctx->rev.as<int>(), mf);

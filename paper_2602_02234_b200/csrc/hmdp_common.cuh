@@ -107,8 +107,8 @@ __device__ __forceinline__ double norm2_rn(double x, double y, double z) {
 // o < NOUT, with x in shared memory.  Thread t computes the partial sum of part
 // p = t % P (P = 128/NOUT parts of NIN/P consecutive inputs) for output
 // o = t / P; the P partials sit in adjacent lanes and are combined with xor
-// shuffles, so every thread of the group returns y[o].  Weights are read
-// through L1 (every CTA of an SM shares them); the vector is an smem broadcast.
+// shuffles, so every thread of the group returns y[o].  W and x both live in
+// shared memory (the kernel stages its weights once per CTA).
 // ---------------------------------------------------------------------------
 template <typename T, int NOUT, int NIN>
 __device__ __forceinline__ T bmv(const T* __restrict__ W, int ldw, const T* xs, int t) {
@@ -121,7 +121,7 @@ __device__ __forceinline__ T bmv(const T* __restrict__ W, int ldw, const T* xs, 
     T acc = T(0);
 #pragma unroll
     for (int q = 0; q < KP; q += 4) {
-        const V4<T> w = ld4(wr + q);
+        const V4<T> w = ld4c(wr + q);  // weights staged in shared memory
         acc += w.x * xr[q];
         acc += w.y * xr[q + 1];
         acc += w.z * xr[q + 2];

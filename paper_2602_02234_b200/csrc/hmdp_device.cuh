@@ -50,15 +50,26 @@ struct DevModel {
 // (edges e = (k -> i)) are listed in in_edge[in_start[i] .. + in_cnt[i]).
 // For the symmetric periodic list in_start/in_cnt alias row_start/nnei and
 // in_edge[e] = rev(e), the slot of the mirrored edge.
+//
+// "Mirror" slots: the in-edge array position of edge e (e's slot in the list of
+// its target j) is inv_pos[e].  Producers push per-neighbour data there (P_j for
+// message layers, the h_j adjoint dz_e, and g_e for the force), so consumers
+// read their own contiguous range [in_start[i], in_start[i] + in_cnt[i]) without
+// an index indirection.  For the symmetric periodic list the in-edge array IS
+// the out-slot array: in_edge = inv_pos = rev and in_start/in_cnt alias
+// row_start/nnei (sym = 1).
 struct DevGraph {
     int n;
+    int sym;  // 1: in-edge array aliases the out-slots (rev), see above
     const int* row_start;
     const int* nnei;
     const int* nbr;
+    const int* ety;    // [slot] type of the neighbour (written by the search)
     const double* dr;  // [slot][3], r_j - r_i image-corrected (FP64)
     const int* in_start;
     const int* in_cnt;
-    const int* in_edge;
+    const int* in_edge;  // [in-position] -> edge slot
+    const int* inv_pos;  // [edge slot] -> in-position (mirror slot)
     const int* types;
     const unsigned char* is_ghost;  // nullable
 };
@@ -73,13 +84,14 @@ struct DevWork {
     T* eb;    // [slot][8] b_k
     T* edb;   // [slot][8] b_k'
     T* g;     // dE/dr
+    T* grev;  // [in-position] g of the edge mirrored there (pushed by its source)
     T* z;     // [M][slot][32] message hidden (tanh) activations z_e
-    T* d;     // [2][slot][32] adjoint of z_e pre-activation (double-buffered by layer)
+    T* d;     // [2][in-position][32] pushed adjoints dz_e (double-buffered by layer)
+    T* pe;    // [2][slot][32] pushed neighbour projections P_j = W1h h_j, per out-slot
     // per atom
     T* desc;   // [n][32] descriptor (n_types*8 used)
     T* ez1;    // [n][32] embedding hidden activations
     T* h;      // [M+1][n][32]
-    T* p;      // [2][n][32] W1h^(l) h^(l): neighbour projection of message layer l
     T* uz1;    // [M][n][32] update hidden activations
     T* dhown;  // [n][32] atom-local part of dE/dh
     double* e_atom;   // [n]

@@ -30,7 +30,8 @@ __global__ __launch_bounds__(kAT) void k_nbr_search(
     int n, const double* __restrict__ pos, CellGrid cg, const int* __restrict__ cell_count,
     const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
     int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
-    double* __restrict__ dr, unsigned* err) {
+    double* __restrict__ dr, const int* __restrict__ types, int* __restrict__ ety,
+    unsigned* err) {
     __shared__ int s_cand[kCandMax];
     __shared__ int s_cell[32];
     __shared__ int s_off[33];
@@ -128,6 +129,7 @@ __global__ __launch_bounds__(kAT) void k_nbr_search(
             for (int p = 0; p < m; ++p) rank += s_cand[p] < v;
             const long long slot = static_cast<long long>(i) * cap + rank;
             nbr[slot] = v;
+            if (ety) ety[slot] = types[v];
             dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
             dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
             dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
@@ -266,12 +268,19 @@ __global__ void k_vv_kick_drift_bin(int n, MdFuse mf, const double* __restrict__
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+int num_sms() {
+    static thread_local int dev_cached = -1, sms_cached = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&sms_cached, cudaDevAttrMultiProcessorCount, dev);
+        dev_cached = dev;
+    }
+    return sms_cached;
+}
 int atom_grid(int n) {
     // grid-stride over atoms: enough CTAs to fill every SM several times
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int g = sms * 12;
+    const int g = num_sms() * 12;
     return n < g ? (n > 0 ? n : 1) : g;
 }
 
@@ -281,9 +290,27 @@ void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_cou
 }
 void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* cell_count,
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,
-                       int* row_start, int* nbr, double* dr, unsigned* err, cudaStream_t st) {
+                       int* row_start, int* nbr, double* dr, const int* types, int* ety,
+                       unsigned* err, cudaStream_t st) {
     k_nbr_search<<<atom_grid(n), kAT, 0, st>>>(n, pos, cg, cell_count, members, cell_of, range2,
-                                               cap, nnei, row_start, nbr, dr, err);
+                                               cap, nnei, row_start, nbr, dr, types, ety, err);
+}
+
+// Generic CSR path: neighbour types per edge and the mirror index of each edge.
+__global__ void k_edge_meta(int ne, const int* __restrict__ nbr, const int* __restrict__ types,
+                            int* __restrict__ ety) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < ne) ety[e] = types[nbr[e]];
+}
+__global__ void k_inv_pos(int ne, const int* __restrict__ in_edge, int* __restrict__ inv_pos) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < ne) inv_pos[in_edge[q]] = q;
+}
+void launch_edge_meta(int ne, const int* nbr, const int* types, int* ety, const int* in_edge,
+                      int* inv_pos, cudaStream_t st) {
+    if (ne <= 0) return;
+    k_edge_meta<<<(ne + 255) / 256, 256, 0, st>>>(ne, nbr, types, ety);
+    k_inv_pos<<<(ne + 255) / 256, 256, 0, st>>>(ne, in_edge, inv_pos);
 }
 void launch_csr_rows(int n, const int* offset, int* row_start, int* nnei, cudaStream_t st) {
     k_csr_rows<<<(n + 127) / 128, 128, 0, st>>>(n, offset, row_start, nnei);

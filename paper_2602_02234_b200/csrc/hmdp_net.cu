@@ -1,17 +1,28 @@
 // hmdp_net.cu — the DP network kernels (embedding, message layers, fitting,
 // reverse mode, forces/virial), sm_100a.
 //
-// Decomposition: one 128-thread CTA per atom (grid-stride over atoms).  Atom-level
-// MLPs are 4-way split mat-vecs (bmv, hmdp_common.cuh) with the activation vector
-// in shared memory; per-edge work is split over the 4 warps (edge q -> warp q % 4)
-// with lane = channel, so every per-edge row access is one coalesced 128-byte line.
-// Edge -> atom sums are reduced in a fixed order (deterministic, no float atomics):
-// the reference's scatters dh_j += ..., F_j -= ... (inference.cpp:343, :380) become
-// gathers over each atom's in-edges.
+// Decomposition: a 512-thread CTA holds four independent 128-thread "atom
+// groups"; each group processes one atom at a time (grid-stride over atoms) and
+// synchronises with its own named barrier, so the groups never wait on each
+// other.  Every kernel first stages the MLP weights it needs into shared memory
+// (once per CTA, ~1 CTA per SM), so the atom-level mat-vecs (bmv: 4-way split,
+// xor-shuffle reduction) read weights and activations from shared memory only.
+// Per-edge work is split over the group's 4 warps (edge q -> warp q % 4) with
+// lane = channel, so every per-edge row access is one coalesced 128-byte line.
+//
+// Dataflow is "push" into mirror slots (DevGraph, hmdp_device.cuh): the producer
+// of a per-neighbour quantity writes it into the slot its consumer reads
+// contiguously, so no kernel chases an index to gather a neighbour's row:
+//   P_j = W1h h_j        pushed by j into the out-slots of j's in-edges
+//   dz_e (h_j adjoint)   pushed by the edge's source into e's mirror slot
+//   g_e                  pushed by the edge's source into e's mirror slot
+// Every slot is written by exactly one thread and every sum runs in a fixed
+// order: deterministic, no float atomics (the reference's scatters dh_j += ...,
+// F_j -= ..., inference.cpp:343, :380, become these pushes + local sums).
 //
 // Linearity of the message MLP is exploited exactly (same function, fewer FLOPs):
-//   forward   z_e = tanh(W1h h_j + W1b b_e + b1), and W1h h_j is a per-ATOM
-//             projection P_j computed once per layer instead of once per edge;
+//   forward   z_e = tanh(W1h h_j + W1b b_e + b1) with the per-ATOM projection
+//             P_j = W1h h_j computed once per layer instead of once per edge;
 //             msum_i = sum_e s_e (W2 z_e + b2) = W2 (sum_e s_e z_e) + (sum_e s_e) b2
 //   backward  with dmsum_i from the update MLP, v = W2^T dmsum_i, c0 = dmsum_i.b2:
 //             dsc_e = dmsum_i . mo_e = v . z_e + c0,  dz_e = s_e v (1 - z_e^2),
@@ -30,72 +41,150 @@
 
 namespace hmdp {
 
-int atom_grid(int n);  // hmdp_nbr.cu
+int num_sms();  // hmdp_nbr.cu
 
-// Shared per-CTA scratch for one atom.
+constexpr int kG = 4;             // atom groups per CTA
+constexpr int kCTA = kG * kAT;    // 512 threads
+constexpr int kEdgePass = 64;     // edges per pass of a group (16 per warp)
+constexpr int kPW = kEdgePass / 4;
+
+// group-local barrier (named barrier 1 + g over the group's 128 threads)
+__device__ __forceinline__ void gsync(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kAT) : "memory");
+}
+
+// Sum over a group's 128 threads (every thread gets the total); fixed order.
+template <typename T>
+__device__ __forceinline__ T group_sum(T v, T* s4, int g) {
+    v = warp_sum(v);
+    gsync(g);
+    if ((threadIdx.x & 31) == 0) s4[(threadIdx.x >> 5) & 3] = v;
+    gsync(g);
+    return ((s4[0] + s4[1]) + s4[2]) + s4[3];
+}
+
+// Per-group shared scratch for one atom.
 template <typename T>
 struct AtomSmem {
     T v0[64], v1[64], v2[64], v3[64];  // activation vectors
     T part[4][32];                     // per-warp partial channel sums
-    T s4[4];                           // block_sum scratch
+    T s4[4];                           // group_sum scratch
     T sc[4];                           // per-warp scalar partials
 };
 
 // ---------------------------------------------------------------------------
-// Fitting net forward + backward on h (in sm.v0 ... written by the caller into
-// `h_s`), leaves dE/dh in dh_s.  inference.cpp:288-311.  Returns nothing; writes
-// e_i for owned atoms (0 for ghosts) and dh = 0 for ghosts.
+// Weight staging: whole MLPs [in, 32, out] copied to shared memory.
 // ---------------------------------------------------------------------------
+__host__ __device__ constexpr int mlp_elems(int in, int out) {
+    return 32 * in + in * 32 + 32 + ((out * 32 + 3) / 4) * 4 * 2 + ((out + 3) / 4) * 4;
+}
+constexpr int kInEmbed = 32, kInFit = 32, kInMsg = kH + kK, kInUpd = 2 * kH;
+
 template <typename T>
-__device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, T* z_s, T* dz_s,
-                                            T* dh_s, bool owned, double* e_out, T* s4, int t) {
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
-    const T zf = d_tanh(bmv<T, 32, 32>(fit.W1, 32, h_s, t) + __ldg(fit.b1 + o));
-    if (lead) z_s[o] = zf;
-    __syncthreads();
-    // linear head 32 -> 1 and its adjoint (dout = 1)
-    T ez = (t < 32) ? __ldg(fit.W2 + t) * z_s[t] : T(0);
-    const T e = block_sum(ez, s4) + __ldg(fit.b2);
-    if (t == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
-    if (t < 32) dz_s[t] = (__ldg(fit.W2 + t) * T(1)) * (T(1) - z_s[t] * z_s[t]);
-    __syncthreads();
-    const T dh = bmv<T, 32, 32>(fit.W1T, 32, dz_s, t);
-    __syncthreads();  // dh_s may alias dz_s
-    if (lead) dh_s[o] = owned ? dh : T(0);
-    __syncthreads();
+struct Stager {
+    T* base;
+    int off;
+    __device__ const T* put(const T* src, int count) {
+        T* dst = base + off;
+        for (int q = threadIdx.x * 4; q < count; q += kCTA * 4) {
+            const V4<T> v = ld4(src + q);
+            st4(dst + q, v.x, v.y, v.z, v.w);
+        }
+        off += (count + 3) / 4 * 4;
+        return dst;
+    }
+    __device__ DevMlp<T> mlp(const DevMlp<T>& m, int in, int out) {
+        DevMlp<T> d;
+        d.W1 = put(m.W1, 32 * in);
+        d.W1T = put(m.W1T, in * 32);
+        d.b1 = put(m.b1, 32);
+        d.W2 = put(m.W2, (out * 32 + 3) / 4 * 4);
+        d.W2T = put(m.W2T, (32 * out + 3) / 4 * 4);
+        d.b2 = put(m.b2, (out + 3) / 4 * 4);
+        return d;
+    }
+};
+// (the device weight buffer pads every array to a multiple of 32 elements, so
+// the rounded-up copies above never read past an array's allocation)
+
+// Push a 32-vector (smem) into the rows `dst + in_edge[in_start + k] * 32` for
+// k < in_cnt (the out-slots of i's in-edges): 4 rows per group iteration.
+template <typename T>
+__device__ __forceinline__ void push_rows(T* __restrict__ dst, const T* vec, const DevGraph& gr,
+                                          int i, int t) {
+    const int is = gr.in_start[i], ic = gr.in_cnt[i];
+    const T v = vec[t & 31];
+    for (int k = t >> 5; k < ic; k += 4) {
+        const long long slot = gr.in_edge[is + k];
+        dst[slot * kH + (t & 31)] = v;
+    }
 }
 
 // ---------------------------------------------------------------------------
-// Edge radial features + descriptor + embedding (and the message-layer-0 atom
-// projection, or for depth 1 the whole fitting/backward chain).
+// Fitting net forward + backward on h_s: writes e_i for owned atoms (0 for
+// ghosts), leaves dE/dh (0 for ghosts) in dh_s.  inference.cpp:288-311.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, T* z_s, T* dz_s,
+                                            T* dh_s, bool owned, double* e_out, T* s4, int t,
+                                            int g) {
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
+    const T zf = d_tanh(bmv<T, 32, 32>(fit.W1, 32, h_s, t) + fit.b1[o]);
+    if (lead) z_s[o] = zf;
+    gsync(g);
+    // linear head 32 -> 1 and its adjoint (dout = 1)
+    const T ez = (t < 32) ? fit.W2[t] * z_s[t] : T(0);
+    const T e = group_sum(ez, s4, g) + fit.b2[0];
+    if (t == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
+    if (t < 32) dz_s[t] = (fit.W2[t] * T(1)) * (T(1) - z_s[t] * z_s[t]);
+    gsync(g);
+    const T dh = bmv<T, 32, 32>(fit.W1T, 32, dz_s, t);
+    gsync(g);  // dh_s may alias dz_s
+    if (lead) dh_s[o] = owned ? dh : T(0);
+    gsync(g);
+}
+
+// ---------------------------------------------------------------------------
+// Edge radial features + descriptor + embedding; pushes P^0 (message layer 0's
+// neighbour projection) or, for depth 1, runs the whole fitting/backward chain.
+// rev (periodic path): computes the reverse slot of every edge, which is the
+// in-edge array of the symmetric graph (gr.in_edge == gr.inv_pos == rev).
 // ---------------------------------------------------------------------------
 template <typename T, bool FUSE_FIT>
-__global__ __launch_bounds__(kAT) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                               int* __restrict__ rev, MdFuse mf) {
-    __shared__ AtomSmem<T> sm;
-    __shared__ T s_b[kAT][kK + 1];
-    __shared__ int s_ty[kAT];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+__global__ __launch_bounds__(kCTA, 1) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                   int* __restrict__ rev, MdFuse mf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ AtomSmem<T> sms[kG];
+    __shared__ T s_b[kG][kEdgePass][kK + 1];
+    __shared__ int s_ty[kG][kEdgePass];
     // this step's neighbour search is complete: clear the cell counts for the
     // binning fused into the force kernel (device MD) / keep the zero invariant
-    for (int c = blockIdx.x * blockDim.x + t; c < mf.n_cells_zero; c += gridDim.x * blockDim.x)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
+         c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
+    DevMlp<T> fit{}, msg0{};
+    if constexpr (FUSE_FIT)
+        fit = sg.mlp(md.fit, kInFit, 1);
+    else
+        msg0 = sg.mlp(md.msg[0], kInMsg, kH);
+    __syncthreads();
+    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
+    AtomSmem<T>& sm = sms[g];
     const int nd = md.n_types * kK;
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
-    for (int i = blockIdx.x; i < gr.n; i += gridDim.x) {
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
+    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         T desc = T(0);  // thread q < nd accumulates descriptor component q
-        for (int base = 0; base < cnt; base += kAT) {
-            const int m = min(kAT, cnt - base);
+        for (int base = 0; base < cnt; base += kEdgePass) {
+            const int m = min(kEdgePass, cnt - base);
             const int e = start + base + t;
             int j = 0;
             if (t < m) {
-                j = gr.nbr[e];
-                const int ty = gr.types[j];
+                if (rev) j = gr.nbr[e];
                 T x, y, z;
                 const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
                 if (!(r > T(0))) atomicOr(ws.err, kErrZeroEdge);
@@ -116,28 +205,30 @@ __global__ __launch_bounds__(kAT) void k_embed(DevModel<T> md, DevGraph gr, DevW
                 st4(ws.edb + 8ll * e, db[0], db[1], db[2], db[3]);
                 st4(ws.edb + 8ll * e + 4, db[4], db[5], db[6], db[7]);
 #pragma unroll
-                for (int k = 0; k < kK; ++k) s_b[t][k] = b[k];
-                s_ty[t] = ty;
+                for (int k = 0; k < kK; ++k) s_b[g][t][k] = b[k];
+                s_ty[g][t] = gr.ety[e];
             }
-            if (rev) {
+            if (rev && w < 2) {
                 // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Lane l of the
                 // warp owning edges [32w, 32w+32) reads entry l of each neighbour's
-                // list (one memory latency for the warp); a ballot finds i.
+                // list (one memory latency per 8 edges); a ballot finds i.
                 const int mw = min(32, max(0, m - 32 * w));
                 const int rs_l = t < m ? gr.row_start[j] : 0;
                 const int nn_l = t < m ? gr.nnei[j] : 0;
-                int val[32];
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const int rsq = __shfl_sync(FULL_MASK, rs_l, q);
-                    const int nnq = __shfl_sync(FULL_MASK, nn_l, q);
-                    val[q] = (q < mw && lane < nnq) ? gr.nbr[rsq + lane] : -1;
-                }
                 int found = -1;
+                for (int q0 = 0; q0 < mw; q0 += 8) {
+                    int val[8];
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const unsigned bal = __ballot_sync(FULL_MASK, val[q] == i);
-                    if (lane == q && bal) found = rs_l + __ffs(bal) - 1;
+                    for (int u = 0; u < 8; ++u) {
+                        const int rsq = __shfl_sync(FULL_MASK, rs_l, q0 + u);
+                        const int nnq = __shfl_sync(FULL_MASK, nn_l, q0 + u);
+                        val[u] = (q0 + u < mw && lane < nnq) ? gr.nbr[rsq + lane] : -1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const unsigned bal = __ballot_sync(FULL_MASK, val[u] == i);
+                        if (lane == q0 + u && bal) found = rs_l + __ffs(bal) - 1;
+                    }
                 }
                 if (t < m) {
                     if (found < 0 && nn_l > 32) {
@@ -157,88 +248,85 @@ __global__ __launch_bounds__(kAT) void k_embed(DevModel<T> md, DevGraph gr, DevW
                     if (found < 0) atomicOr(ws.err, kErrAsymmetric);
                 }
             }
-            __syncthreads();
+            gsync(g);
             if (t < nd) {  // descriptor: CSR edge order, as inference.cpp:228-238
                 const int ty = t >> 3, k = t & 7;
-                for (int r = 0; r < m; ++r) desc += (s_ty[r] == ty) ? s_b[r][k] : T(0);
+                for (int r = 0; r < m; ++r) desc += (s_ty[g][r] == ty) ? s_b[g][r][k] : T(0);
             }
-            __syncthreads();
+            gsync(g);
         }
         if (t < 32) {
             sm.v0[t] = t < nd ? desc : T(0);
             if (t < nd) ws.desc[static_cast<long long>(i) * 32 + t] = desc;
         }
-        __syncthreads();
+        gsync(g);
         // embedding forward nd (zero-padded to 32) -> 32 (tanh) -> 32
-        const T z1 = d_tanh(bmv<T, 32, 32>(md.embed.W1, 32, sm.v0, t) + __ldg(md.embed.b1 + o));
+        const T z1 = d_tanh(bmv<T, 32, 32>(emb.W1, 32, sm.v0, t) + emb.b1[o]);
         if (lead) {
             sm.v1[o] = z1;
             ws.ez1[static_cast<long long>(i) * kH + o] = z1;
         }
-        __syncthreads();
-        const T h0 = bmv<T, 32, 32>(md.embed.W2, 32, sm.v1, t) + __ldg(md.embed.b2 + o);
+        gsync(g);
+        const T h0 = bmv<T, 32, 32>(emb.W2, 32, sm.v1, t) + emb.b2[o];
         if (lead) {
             sm.v2[o] = h0;
             ws.h[static_cast<long long>(i) * kH + o] = h0;
         }
-        __syncthreads();
+        gsync(g);
         if constexpr (FUSE_FIT) {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            fit_fwd_bwd(md.fit, sm.v2, sm.v3, sm.v0, sm.v3, owned, ws.e_atom + i, sm.s4, t);
+            fit_fwd_bwd(fit, sm.v2, sm.v3, sm.v0, sm.v3, owned, ws.e_atom + i, sm.s4, t, g);
             // embedding backward: linear layer 2 (W2^T), tanh layer 1 (W1^T, padded)
-            const T dz1 = bmv<T, 32, 32>(md.embed.W2T, 32, sm.v3, t) * (T(1) - z1 * z1);
+            const T dz1 = bmv<T, 32, 32>(emb.W2T, 32, sm.v3, t) * (T(1) - z1 * z1);
             if (lead) sm.v0[o] = dz1;
-            __syncthreads();
-            const T dd = bmv<T, 32, 32>(md.embed.W1T, 32, sm.v0, t);
+            gsync(g);
+            const T dd = bmv<T, 32, 32>(emb.W1T, 32, sm.v0, t);
             if (lead) sm.v1[o] = dd;
-            __syncthreads();
-            for (int base = 0; base < cnt; base += kAT) {
-                const int m = min(kAT, cnt - base);
-                if (t < m) {
-                    const long long e = start + base + t;
-                    const int ty = gr.types[gr.nbr[e]];
-                    const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-                    const T* dv = sm.v1 + ty * kK;
-                    T acc = dv[0] * d0.x;
-                    acc += dv[1] * d0.y;
-                    acc += dv[2] * d0.z;
-                    acc += dv[3] * d0.w;
-                    acc += dv[4] * d1.x;
-                    acc += dv[5] * d1.y;
-                    acc += dv[6] * d1.z;
-                    acc += dv[7] * d1.w;
-                    ws.g[e] = acc;
-                }
+            gsync(g);
+            for (int q = t; q < cnt; q += kAT) {
+                const long long e = start + q;
+                const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+                const T* dv = sm.v1 + gr.ety[e] * kK;
+                T acc = dv[0] * d0.x;
+                acc += dv[1] * d0.y;
+                acc += dv[2] * d0.z;
+                acc += dv[3] * d0.w;
+                acc += dv[4] * d1.x;
+                acc += dv[5] * d1.y;
+                acc += dv[6] * d1.z;
+                acc += dv[7] * d1.w;
+                ws.g[e] = acc;
+                ws.grev[gr.inv_pos[e]] = acc;  // mirror for the force gather
             }
         } else {
-            // P^0 = W1h^(0) h^0: the neighbour projection of message layer 0
-            const T p = bmv<T, 32, 32>(md.msg[0].W1, kH + kK, sm.v2, t);
-            if (lead) ws.p[static_cast<long long>(i) * kH + o] = p;
+            // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
+            const T p = bmv<T, 32, 32>(msg0.W1, kInMsg, sm.v2, t);
+            if (lead) sm.v3[o] = p;
+            gsync(g);
+            push_rows(ws.pe, sm.v3, gr, i, t);
         }
-        __syncthreads();
+        gsync(g);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Message-layer backward body for atom i, given dE/dh^{l+1}_i in sm.v0 and the
-// update hidden activations in sm.v2.
+// update hidden activations in sm.v2.  Pushes dz_e to e's mirror slot.
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void msg_backward_body(const DevModel<T>& md, const DevGraph& gr,
-                                                  const DevWork<T>& ws, AtomSmem<T>& sm, int l,
-                                                  int i, bool first_g) {
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+__device__ __forceinline__ void msg_backward_body(const DevMlp<T>& msg, const DevMlp<T>& upd,
+                                                  const DevGraph& gr, const DevWork<T>& ws,
+                                                  AtomSmem<T>& sm, int l, int i, bool first_g,
+                                                  int t, int g) {
+    const int lane = t & 31, w = t >> 5;
     const long long S = ws.slots;
-    const DevMlp<T> msg = md.msg[l];
-    const DevMlp<T> upd = md.upd[l];
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
     // update MLP backward (64 -> 32 tanh -> 32)
     const T zu = sm.v2[o];
     const T dz = bmv<T, 32, 32>(upd.W2T, 32, sm.v0, t) * (T(1) - zu * zu);
     if (lead) sm.v3[o] = dz;
-    __syncthreads();
+    gsync(g);
     const T din = bmv<T, 64, 32>(upd.W1T, 32, sm.v3, t);  // 64 outputs, 2 parts each
     if (bmv_lead<64>(t)) {
         const int k = bmv_out<64>(t);
@@ -247,35 +335,36 @@ __device__ __forceinline__ void msg_backward_body(const DevModel<T>& md, const D
         else
             sm.v1[k - kH] = din;  // dmsum
     }
-    __syncthreads();
+    gsync(g);
     const T v = bmv<T, 32, 32>(msg.W2T, 32, sm.v1, t);  // v = W2^T dmsum
     if (lead) sm.v2[o] = v;
-    const T c0 = block_sum(t < 32 ? sm.v1[t] * __ldg(msg.b2 + t) : T(0), sm.s4);
-    // (block_sum's barriers also publish sm.v2)
+    const T c0 = group_sum(t < 32 ? sm.v1[t] * msg.b2[t] : T(0), sm.s4, g);
+    // (group_sum's barriers also publish sm.v2)
     T w1b[kK];
 #pragma unroll
-    for (int k = 0; k < kK; ++k) w1b[k] = __ldg(msg.W1T + (kH + k) * kH + lane);
+    for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
     const T vl = sm.v2[lane];
     const T* __restrict__ Z = ws.z + l * S * kH;
     T* __restrict__ D = ws.d + (l & 1) * S * kH;
     const int start = gr.row_start[i], cnt = gr.nnei[i];
-    for (int base = 0; base < cnt; base += kAT) {
+    for (int base = 0; base < cnt; base += kEdgePass) {
         // warp w owns edges base + w + 4u; lane u prefetches edge u's scalars
-        const int mw = max(0, (min(kAT, cnt - base) - w + 3) / 4);
+        const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
         const long long el = start + base + w + 4 * (lane < mw ? lane : 0);
         const T s_l = ws.es[el], ds_l = ws.eds[el];
+        const int mir_l = gr.inv_pos[el];
         const V4<T> d0_l = ld4(ws.edb + 8 * el), d1_l = ld4(ws.edb + 8 * el + 4);
-        T zr[32];
+        T zr[kPW];
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
+        for (int u = 0; u < kPW; ++u)
             if (u < mw) zr[u] = Z[(start + base + w + 4 * u) * static_cast<long long>(kH) + lane];
         T tot_l = T(0);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
+        for (int u = 0; u < kPW; ++u) {
             if (u >= mw) break;
-            const long long e = start + base + w + 4 * u;
             const T z = zr[u];
             const T s = __shfl_sync(FULL_MASK, s_l, u), ds = __shfl_sync(FULL_MASK, ds_l, u);
+            const long long mir = __shfl_sync(FULL_MASK, mir_l, u);
             T wv = w1b[0] * __shfl_sync(FULL_MASK, d0_l.x, u);
             wv += w1b[1] * __shfl_sync(FULL_MASK, d0_l.y, u);
             wv += w1b[2] * __shfl_sync(FULL_MASK, d0_l.z, u);
@@ -285,7 +374,7 @@ __device__ __forceinline__ void msg_backward_body(const DevModel<T>& md, const D
             wv += w1b[6] * __shfl_sync(FULL_MASK, d1_l.z, u);
             wv += w1b[7] * __shfl_sync(FULL_MASK, d1_l.w, u);
             const T d = s * vl * (T(1) - z * z);
-            D[e * kH + lane] = d;
+            D[mir * kH + lane] = d;
             const T tot = warp_sum(ds * vl * z + d * wv);
             if (lane == u) tot_l = tot;
         }
@@ -293,31 +382,29 @@ __device__ __forceinline__ void msg_backward_body(const DevModel<T>& md, const D
     }
 }
 
-// S_i = sum over in-edges of dz_e (layer l) -> sm.v1, split over the 4 warps
+// S_i = sum over i's mirror slots of the pushed dz (layer l) -> sm.v1;
+// contiguous rows, split over the 4 warps, fixed summation order.
 template <typename T>
 __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& ws,
-                                          AtomSmem<T>& sm, int l, int i) {
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+                                          AtomSmem<T>& sm, int l, int i, int t, int g) {
+    const int lane = t & 31, w = t >> 5;
     const T* __restrict__ D = ws.d + (l & 1) * ws.slots * kH;
     const int is = gr.in_start[i], ic = gr.in_cnt[i];
-    T sg = T(0);
-    for (int base = 0; base < ic; base += kAT) {
-        const int mw = max(0, (min(kAT, ic - base) - w + 3) / 4);
-        const int idx = lane < mw ? gr.in_edge[is + base + w + 4 * lane] : 0;
-        T dr_[32];
+    T acc = T(0);
+    for (int base = 0; base < ic; base += kEdgePass) {
+        const int mw = max(0, (min(kEdgePass, ic - base) - w + 3) / 4);
+        T dr_[kPW];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            const long long e = __shfl_sync(FULL_MASK, idx, u);
-            if (u < mw) dr_[u] = D[e * kH + lane];
-        }
+        for (int u = 0; u < kPW; ++u)
+            if (u < mw) dr_[u] = D[(is + base + w + 4 * u) * static_cast<long long>(kH) + lane];
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
-            if (u < mw) sg += dr_[u];
+        for (int u = 0; u < kPW; ++u)
+            if (u < mw) acc += dr_[u];
     }
-    sm.part[w][lane] = sg;
-    __syncthreads();
+    sm.part[w][lane] = acc;
+    gsync(g);
     if (t < 32) sm.v1[t] = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
-    __syncthreads();
+    gsync(g);
 }
 
 // ---------------------------------------------------------------------------
@@ -325,40 +412,46 @@ __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& 
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
 template <typename T, bool LAST>
-__global__ __launch_bounds__(kAT) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                 int l) {
-    __shared__ AtomSmem<T> sm;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+__global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                     int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ AtomSmem<T> sms[kG];
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
+    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
+    DevMlp<T> nxt{}, fit{};
+    if constexpr (LAST)
+        fit = sg.mlp(md.fit, kInFit, 1);
+    else
+        nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
+    __syncthreads();
+    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
+    AtomSmem<T>& sm = sms[g];
     const int n = gr.n;
     const long long S = ws.slots;
-    const DevMlp<T> msg = md.msg[l];
-    const DevMlp<T> upd = md.upd[l];
-    const T* __restrict__ Pin = ws.p + (l & 1) * static_cast<long long>(n) * kH;
+    const T* __restrict__ Pin = ws.pe + (l & 1) * S * kH;
     T* __restrict__ Z = ws.z + l * S * kH;
     T w1b[kK];
 #pragma unroll
-    for (int k = 0; k < kK; ++k) w1b[k] = __ldg(msg.W1T + (kH + k) * kH + lane);
-    const T b1 = __ldg(msg.b1 + lane);
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
+    const T b1 = msg.b1[lane];
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
+    for (int i = blockIdx.x * kG + g; i < n; i += gridDim.x * kG) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
+        if (t < 32) sm.v1[t] = ws.h[(static_cast<long long>(l) * n + i) * kH + t];  // h_i
         T acc = T(0), ssum = T(0);
-        for (int base = 0; base < cnt; base += kAT) {
-            const int mw = max(0, (min(kAT, cnt - base) - w + 3) / 4);
+        for (int base = 0; base < cnt; base += kEdgePass) {
+            const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
             const long long el = start + base + w + 4 * (lane < mw ? lane : 0);
-            const int jl = gr.nbr[el];
             const T s_l = ws.es[el];
             const V4<T> b0_l = ld4(ws.eb + 8 * el), b1_l = ld4(ws.eb + 8 * el + 4);
-            T pr[32];
+            T pr[kPW];
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                const int j = __shfl_sync(FULL_MASK, jl, u);
-                if (u < mw) pr[u] = Pin[static_cast<long long>(j) * kH + lane];
-            }
+            for (int u = 0; u < kPW; ++u)
+                if (u < mw) pr[u] = Pin[(start + base + w + 4 * u) * static_cast<long long>(kH) + lane];
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
+            for (int u = 0; u < kPW; ++u) {
                 if (u >= mw) break;
                 const long long e = start + base + w + 4 * u;
                 const T s = __shfl_sync(FULL_MASK, s_l, u);
@@ -379,93 +472,104 @@ __global__ __launch_bounds__(kAT) void k_msg_fwd(DevModel<T> md, DevGraph gr, De
         }
         sm.part[w][lane] = acc;
         if (lane == 0) sm.sc[w] = ssum;
-        if (t < 32) sm.v1[t] = ws.h[(static_cast<long long>(l) * n + i) * kH + t];  // h_i
-        __syncthreads();
+        gsync(g);
         if (t < 32) sm.v0[t] = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
         const T stot = ((sm.sc[0] + sm.sc[1]) + sm.sc[2]) + sm.sc[3];
-        __syncthreads();
+        gsync(g);
         // msum = W2 (sum_e s_e z_e) + (sum_e s_e) b2  -> second half of the update input
-        const T msum = bmv<T, 32, 32>(msg.W2, 32, sm.v0, t) + stot * __ldg(msg.b2 + o);
+        const T msum = bmv<T, 32, 32>(msg.W2, 32, sm.v0, t) + stot * msg.b2[o];
         if (lead) sm.v1[kH + o] = msum;
-        __syncthreads();
+        gsync(g);
         // update MLP on [h_i, msum] (64 -> 32 tanh -> 32), residual
-        const T zu = d_tanh(bmv<T, 32, 64>(upd.W1, 2 * kH, sm.v1, t) + __ldg(upd.b1 + o));
+        const T zu = d_tanh(bmv<T, 32, 64>(upd.W1, kInUpd, sm.v1, t) + upd.b1[o]);
         if (lead) {
             sm.v2[o] = zu;
             ws.uz1[(static_cast<long long>(l) * n + i) * kH + o] = zu;
         }
-        __syncthreads();
-        const T hn = sm.v1[o] + (bmv<T, 32, 32>(upd.W2, 32, sm.v2, t) + __ldg(upd.b2 + o));
+        gsync(g);
+        const T hn = sm.v1[o] + (bmv<T, 32, 32>(upd.W2, 32, sm.v2, t) + upd.b2[o]);
         if (lead) {
             sm.v3[o] = hn;
             ws.h[(static_cast<long long>(l + 1) * n + i) * kH + o] = hn;
         }
-        __syncthreads();
+        gsync(g);
         if constexpr (!LAST) {
-            const T p = bmv<T, 32, 32>(md.msg[l + 1].W1, kH + kK, sm.v3, t);
-            if (lead)
-                ws.p[((l + 1) & 1) * static_cast<long long>(n) * kH + static_cast<long long>(i) * kH + o] = p;
+            const T p = bmv<T, 32, 32>(nxt.W1, kInMsg, sm.v3, t);
+            if (lead) sm.v0[o] = p;
+            gsync(g);
+            push_rows(ws.pe + ((l + 1) & 1) * S * kH, sm.v0, gr, i, t);
         } else {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
             // fitting: h^M in v3 -> dE/dh^M in v0 (v1 scratch for the fit hidden layer)
-            fit_fwd_bwd(md.fit, sm.v3, sm.v1, sm.v0, sm.v0, owned, ws.e_atom + i, sm.s4, t);
-            msg_backward_body(md, gr, ws, sm, l, i, true);
+            fit_fwd_bwd(fit, sm.v3, sm.v1, sm.v0, sm.v0, owned, ws.e_atom + i, sm.s4, t, g);
+            msg_backward_body(msg, upd, gr, ws, sm, l, i, true, t, g);
         }
-        __syncthreads();
+        gsync(g);
     }
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
 template <typename T>
-__global__ __launch_bounds__(kAT) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                 int l) {
-    __shared__ AtomSmem<T> sm;
-    const int t = threadIdx.x;
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
-    for (int i = blockIdx.x; i < gr.n; i += gridDim.x) {
-        gather_in(gr, ws, sm, l + 1, i);
+__global__ __launch_bounds__(kCTA, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                     int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ AtomSmem<T> sms[kG];
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
+    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
+    const DevMlp<T> nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
+    __syncthreads();
+    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
+    AtomSmem<T>& sm = sms[g];
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
+    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+        const T own = ws.dhown[static_cast<long long>(i) * kH + o];
+        const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + o];
+        gather_in(gr, ws, sm, l + 1, i, t, g);
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
-        const T dh = ws.dhown[static_cast<long long>(i) * kH + o] +
-                     bmv<T, 32, 32>(md.msg[l + 1].W1T, 32, sm.v1, t);
+        const T dh = own + bmv<T, 32, 32>(nxt.W1T, 32, sm.v1, t);
         if (lead) {
             sm.v0[o] = dh;
-            sm.v2[o] = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + o];
+            sm.v2[o] = zu;
         }
-        __syncthreads();
-        msg_backward_body(md, gr, ws, sm, l, i, false);
-        __syncthreads();
+        gsync(g);
+        msg_backward_body(msg, upd, gr, ws, sm, l, i, false, t, g);
+        gsync(g);
     }
 }
 
-// Embedding backward + descriptor adjoint (depth > 1).
+// Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T>
-__global__ __launch_bounds__(kAT) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
-    __shared__ AtomSmem<T> sm;
-    const int t = threadIdx.x;
-    constexpr int O = 32;
-    const int o = bmv_out<O>(t);
-    const bool lead = bmv_lead<O>(t);
-    for (int i = blockIdx.x; i < gr.n; i += gridDim.x) {
-        gather_in(gr, ws, sm, 0, i);
-        const T dh = ws.dhown[static_cast<long long>(i) * kH + o] +
-                     bmv<T, 32, 32>(md.msg[0].W1T, 32, sm.v1, t);
-        if (lead) sm.v0[o] = dh;
-        __syncthreads();
+__global__ __launch_bounds__(kCTA, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ AtomSmem<T> sms[kG];
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
+    const DevMlp<T> msg0 = sg.mlp(md.msg[0], kInMsg, kH);
+    __syncthreads();
+    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
+    AtomSmem<T>& sm = sms[g];
+    const int o = bmv_out<32>(t);
+    const bool lead = bmv_lead<32>(t);
+    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+        const T own = ws.dhown[static_cast<long long>(i) * kH + o];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + o];
-        const T dz1 = bmv<T, 32, 32>(md.embed.W2T, 32, sm.v0, t) * (T(1) - z1 * z1);
+        gather_in(gr, ws, sm, 0, i, t, g);
+        const T dh = own + bmv<T, 32, 32>(msg0.W1T, 32, sm.v1, t);
+        if (lead) sm.v0[o] = dh;
+        gsync(g);
+        const T dz1 = bmv<T, 32, 32>(emb.W2T, 32, sm.v0, t) * (T(1) - z1 * z1);
         if (lead) sm.v2[o] = dz1;
-        __syncthreads();
-        const T dd = bmv<T, 32, 32>(md.embed.W1T, 32, sm.v2, t);
+        gsync(g);
+        const T dd = bmv<T, 32, 32>(emb.W1T, 32, sm.v2, t);
         if (lead) sm.v3[o] = dd;
-        __syncthreads();
+        gsync(g);
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         for (int q = t; q < cnt; q += kAT) {
             const long long e = start + q;
-            const int ty = gr.types[gr.nbr[e]];
             const V4<T> d0 = ld4(ws.edb + 8 * e), d1 = ld4(ws.edb + 8 * e + 4);
-            const T* dv = sm.v3 + ty * kK;
+            const T* dv = sm.v3 + gr.ety[e] * kK;
             T acc = dv[0] * d0.x;
             acc += dv[1] * d0.y;
             acc += dv[2] * d0.z;
@@ -474,44 +578,59 @@ __global__ __launch_bounds__(kAT) void k_embed_bwd(DevModel<T> md, DevGraph gr, 
             acc += dv[5] * d1.y;
             acc += dv[6] * d1.z;
             acc += dv[7] * d1.w;
-            ws.g[e] = ws.g[e] + acc;
+            const T gv = ws.g[e] + acc;
+            ws.g[e] = gv;
+            ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
         }
-        __syncthreads();
+        gsync(g);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Forces (gather form), per-atom energy, virial, and the fused velocity-Verlet
 // tail of the device MD loop; deterministic grid reduction of E, W, W_ab.
-//   F_i = sum_{e in out(i)} u_e g_e - sum_{e in in(i)} u_e g_e
+//   F_i = sum_{e in out(i)} u_e g_e - sum_{e' in in(i)} u_e' g_e'
+//       = sum_q u_q (g_q + grev_q)            (symmetric list: u_rev(e) = -u_e)
 //   W   = -sum_e g_e r_e ;  W_ab = -sum_e g_e dr_a u_b
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ __launch_bounds__(kAT) void k_force(DevGraph gr, DevWork<T> ws, double* __restrict__ forces,
-                                               double* __restrict__ per_atom, double* __restrict__ out,
-                                               MdFuse mf) {
-    __shared__ double s_f[4][3];
-    __shared__ double s_part[4][12];
+__global__ __launch_bounds__(kCTA, 1) void k_force(DevGraph gr, DevWork<T> ws,
+                                                   double* __restrict__ forces,
+                                                   double* __restrict__ per_atom,
+                                                   double* __restrict__ out, MdFuse mf) {
+    __shared__ double s_f[kG][4][3];
+    __shared__ double s_part[kCTA / 32][12];
     __shared__ bool s_last;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
     double acc[11];
 #pragma unroll
     for (int q = 0; q < 11; ++q) acc[q] = 0.0;
-    for (int i = blockIdx.x; i < gr.n; i += gridDim.x) {
+    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+        // MD state of atom i, loaded early (independent of the edge loads)
+        double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0;
+        if (mf.mode && t == 0) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                vv[a] = mf.v[3 * i + a];
+                xv[a] = mf.x[3 * i + a];
+            }
+            mi = mf.m[i];
+        }
         double fx = 0.0, fy = 0.0, fz = 0.0;
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         for (int q = t; q < cnt; q += kAT) {
             const int e = start + q;
-            const T g = ws.g[e];
+            const T gg = ws.g[e];
+            const T gm = gr.sym ? ws.grev[e] : T(0);
             T x, y, z;
             const double* d = gr.dr + 3ll * e;
             const T r = edge_len<T>(d, x, y, z);
             const T ux = x / r, uy = y / r, uz = z / r;
-            fx += static_cast<double>(ux * g);
-            fy += static_cast<double>(uy * g);
-            fz += static_cast<double>(uz * g);
-            acc[1] -= static_cast<double>(g * r);
-            const double gd = static_cast<double>(g);
+            fx += static_cast<double>(ux * gg) + static_cast<double>(ux * gm);
+            fy += static_cast<double>(uy * gg) + static_cast<double>(uy * gm);
+            fz += static_cast<double>(uz * gg) + static_cast<double>(uz * gm);
+            acc[1] -= static_cast<double>(gg * r);
+            const double gd = static_cast<double>(gg);
             const double u3[3] = {static_cast<double>(ux), static_cast<double>(uy),
                                   static_cast<double>(uz)};
 #pragma unroll
@@ -519,29 +638,32 @@ __global__ __launch_bounds__(kAT) void k_force(DevGraph gr, DevWork<T> ws, doubl
 #pragma unroll
                 for (int b = 0; b < 3; ++b) acc[2 + 3 * a + b] -= gd * d[a] * u3[b];
         }
-        const int is = gr.in_start[i], ic = gr.in_cnt[i];
-        for (int q = t; q < ic; q += kAT) {
-            const int e = gr.in_edge[is + q];
-            const T g = ws.g[e];
-            T x, y, z;
-            const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
-            fx -= static_cast<double>((x / r) * g);
-            fy -= static_cast<double>((y / r) * g);
-            fz -= static_cast<double>((z / r) * g);
+        if (!gr.sym) {  // generic CSR: the pushed g of each in-edge, its own geometry
+            const int is = gr.in_start[i], ic = gr.in_cnt[i];
+            for (int q = t; q < ic; q += kAT) {
+                const int e = gr.in_edge[is + q];
+                const T gg = ws.grev[is + q];
+                T x, y, z;
+                const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
+                fx -= static_cast<double>((x / r) * gg);
+                fy -= static_cast<double>((y / r) * gg);
+                fz -= static_cast<double>((z / r) * gg);
+            }
         }
         fx = warp_sum(fx);
         fy = warp_sum(fy);
         fz = warp_sum(fz);
         if (lane == 0) {
-            s_f[w][0] = fx;
-            s_f[w][1] = fy;
-            s_f[w][2] = fz;
+            s_f[g][w][0] = fx;
+            s_f[g][w][1] = fy;
+            s_f[g][w][2] = fz;
         }
-        __syncthreads();
+        gsync(g);
         if (t == 0) {
-            const double f3[3] = {((s_f[0][0] + s_f[1][0]) + s_f[2][0]) + s_f[3][0],
-                                  ((s_f[0][1] + s_f[1][1]) + s_f[2][1]) + s_f[3][1],
-                                  ((s_f[0][2] + s_f[1][2]) + s_f[2][2]) + s_f[3][2]};
+            double f3[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                f3[a] = ((s_f[g][0][a] + s_f[g][1][a]) + s_f[g][2][a]) + s_f[g][3][a];
             forces[3 * i] = f3[0];
             forces[3 * i + 1] = f3[1];
             forces[3 * i + 2] = f3[2];
@@ -549,16 +671,16 @@ __global__ __launch_bounds__(kAT) void k_force(DevGraph gr, DevWork<T> ws, doubl
             if (per_atom) per_atom[i] = ei;
             acc[0] += ei;
             if (mf.mode) {
-                const double s = mf.half / mf.m[i];
+                const double s = mf.half / mi;
                 const bool finite = isfinite(f3[0]) && isfinite(f3[1]) && isfinite(f3[2]);
                 if (!finite) atomicOr(ws.err, kErrNonFinite);
                 double x3[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    double va = __dadd_rn(mf.v[3 * i + a], __dmul_rn(f3[a], s));  // closing kick
+                    double va = __dadd_rn(vv[a], __dmul_rn(f3[a], s));  // closing kick
                     if (mf.mode == 2) {
                         va = __dadd_rn(va, __dmul_rn(f3[a], s));  // next step's opening kick
-                        x3[a] = __dadd_rn(mf.x[3 * i + a], __dmul_rn(va, mf.dt));
+                        x3[a] = __dadd_rn(xv[a], __dmul_rn(va, mf.dt));
                         mf.x[3 * i + a] = x3[a];
                     }
                     mf.v[3 * i + a] = va;
@@ -567,74 +689,123 @@ __global__ __launch_bounds__(kAT) void k_force(DevGraph gr, DevWork<T> ws, doubl
                     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, ws.err);
             }
         }
-        __syncthreads();
+        gsync(g);
     }
     // CTA partials (fixed order), then the last CTA reduces them in fixed order
+    const int wc = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < 11; ++q) acc[q] = warp_sum(acc[q]);
     if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 11; ++q) s_part[w][q] = acc[q];
+        for (int q = 0; q < 11; ++q) s_part[wc][q] = acc[q];
     __syncthreads();
-    if (t < 11)
-        ws.partial[blockIdx.x * 16 + t] =
-            ((s_part[0][t] + s_part[1][t]) + s_part[2][t]) + s_part[3][t];
+    if (threadIdx.x < 11) {
+        double v = 0.0;
+        for (int q = 0; q < kCTA / 32; ++q) v += s_part[q][threadIdx.x];
+        ws.partial[blockIdx.x * 16 + threadIdx.x] = v;
+    }
     __threadfence();
     __syncthreads();
-    if (t == 0) s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
     if (s_last) {
         __threadfence();
         double v[11];
 #pragma unroll
         for (int q = 0; q < 11; ++q) v[q] = 0.0;
-        for (unsigned b = t; b < gridDim.x; b += kAT)
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += kCTA)
 #pragma unroll
             for (int q = 0; q < 11; ++q) v[q] += __ldcg(ws.partial + b * 16 + q);
 #pragma unroll
         for (int q = 0; q < 11; ++q) v[q] = warp_sum(v[q]);
+        __syncthreads();
         if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < 11; ++q) s_part[w][q] = v[q];
+            for (int q = 0; q < 11; ++q) s_part[wc][q] = v[q];
         __syncthreads();
-        if (t < 11) out[t] = ((s_part[0][t] + s_part[1][t]) + s_part[2][t]) + s_part[3][t];
-        if (t == 0) *ws.ticket = 0u;  // re-arm for the next launch / graph replay
+        if (threadIdx.x < 11) {
+            double tot = 0.0;
+            for (int q = 0; q < kCTA / 32; ++q) tot += s_part[q][threadIdx.x];
+            out[threadIdx.x] = tot;
+        }
+        if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / graph replay
     }
 }
 
 // ---------------------------------------------------------------------------
+// launch
+// ---------------------------------------------------------------------------
+static int net_grid(int n) {
+    const int want = (n + kG - 1) / kG;
+    const int cap = num_sms() * 2;  // grid-stride beyond two CTAs per SM
+    return want < 1 ? 1 : (want < cap ? want : cap);
+}
+
+// Launch with `smem_elems` T of dynamic shared memory for the staged weights
+// (the > 48 KB opt-in is set by net_configure() when a context is created, never
+// during stream capture).
+template <typename T, typename... Params, typename... Args>
+static void launch_staged(void (*kernel)(Params...), int grid, int smem_elems, cudaStream_t st,
+                          Args... args) {
+    const size_t bytes = static_cast<size_t>(smem_elems) * sizeof(T);
+    kernel<<<grid, kCTA, bytes, st>>>(args...);
+}
+
+template <typename T>
+static cudaError_t configure_t() {
+    const int bytes = 160 * 1024;
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, true>, a, bytes),
+                          cudaFuncSetAttribute(k_embed<T, false>, a, bytes),
+                          cudaFuncSetAttribute(k_msg_fwd<T, true>, a, bytes),
+                          cudaFuncSetAttribute(k_msg_fwd<T, false>, a, bytes),
+                          cudaFuncSetAttribute(k_msg_bwd<T>, a, bytes),
+                          cudaFuncSetAttribute(k_embed_bwd<T>, a, bytes)})
+        if (r != cudaSuccess) e = r;
+    return e;
+}
+// Per device: allow the staged-weight kernels up to 160 KB of dynamic smem.
+cudaError_t net_configure() {
+    const cudaError_t a = configure_t<float>();
+    const cudaError_t b = configure_t<double>();
+    return a != cudaSuccess ? a : b;
+}
+
 template <typename T>
 int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws,
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
-    const int nb = atom_grid(gr.n);
+    const int nb = net_grid(gr.n);
     const int M = md.n_msg;
+    const int e_emb = mlp_elems(kInEmbed, kH), e_fit = mlp_elems(kInFit, 1);
+    const int e_msg = mlp_elems(kInMsg, kH), e_upd = mlp_elems(kInUpd, kH);
     int launches = 0;
     if (M == 0) {
-        k_embed<T, true><<<nb, kAT, 0, st>>>(md, gr, ws, rev, mf);
+        launch_staged<T>(k_embed<T, true>, nb, e_emb + e_fit, st, md, gr, ws, rev, mf);
         mk("embed_fit", st);
         ++launches;
     } else {
-        k_embed<T, false><<<nb, kAT, 0, st>>>(md, gr, ws, rev, mf);
+        launch_staged<T>(k_embed<T, false>, nb, e_emb + e_msg, st, md, gr, ws, rev, mf);
         mk("embed", st);
         for (int l = 0; l < M; ++l) {
             if (l == M - 1) {
-                k_msg_fwd<T, true><<<nb, kAT, 0, st>>>(md, gr, ws, l);
+                launch_staged<T>(k_msg_fwd<T, true>, nb, e_msg + e_upd + e_fit, st, md, gr, ws, l);
                 mk("msg_fwd_last", st);
             } else {
-                k_msg_fwd<T, false><<<nb, kAT, 0, st>>>(md, gr, ws, l);
+                launch_staged<T>(k_msg_fwd<T, false>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
                 mk("msg_fwd", st);
             }
         }
         for (int l = M - 2; l >= 0; --l) {
-            k_msg_bwd<T><<<nb, kAT, 0, st>>>(md, gr, ws, l);
+            launch_staged<T>(k_msg_bwd<T>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
             mk("msg_bwd", st);
         }
-        k_embed_bwd<T><<<nb, kAT, 0, st>>>(md, gr, ws);
+        launch_staged<T>(k_embed_bwd<T>, nb, e_emb + e_msg, st, md, gr, ws);
         mk("embed_bwd", st);
         launches += 2 + M + (M - 1);
     }
-    k_force<T><<<nb, kAT, 0, st>>>(gr, ws, forces, per_atom, out, mf);
+    k_force<T><<<nb, kCTA, 0, st>>>(gr, ws, forces, per_atom, out, mf);
     mk("force", st);
     return launches + 1;
 }
