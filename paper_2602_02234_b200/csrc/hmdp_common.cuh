@@ -177,4 +177,30 @@ __device__ __forceinline__ void bin_atom(int i, const double* x3, const CellGrid
         atomicOr(err, kErrCellOverflow);
 }
 
+
+// Programmatic dependent launch (PDL): a kernel lets its successor start
+// launching right away (the successor's CTAs take SMs as ours retire and stage
+// their weights), and waits for its predecessor's results before touching them.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Host: launch with the programmatic-stream-serialization attribute (also valid
+// under stream capture, where it becomes a programmatic graph edge).
+template <typename... Params, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
+}
 }  // namespace hmdp

@@ -36,6 +36,8 @@ __global__ __launch_bounds__(kAT) void k_nbr_search(
     __shared__ int s_cell[32];
     __shared__ int s_off[33];
     __shared__ int s_wcnt[4];
+    pdl_launch_dependents();
+    pdl_wait();
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const double L0 = cg.L[0], L1 = cg.L[1], L2 = cg.L[2];
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
@@ -292,8 +294,8 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
                        unsigned* err, cudaStream_t st) {
-    k_nbr_search<<<atom_grid(n), kAT, 0, st>>>(n, pos, cg, cell_count, members, cell_of, range2,
-                                               cap, nnei, row_start, nbr, dr, types, ety, err);
+    launch_pdl(k_nbr_search, dim3(atom_grid(n)), dim3(kAT), 0, st, n, pos, cg, cell_count, members,
+               cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety, err);
 }
 
 // Generic CSR path: neighbour types per edge and the mirror index of each edge.

@@ -46,6 +46,7 @@ int num_sms();  // hmdp_nbr.cu
 constexpr int kG = 4;             // atom groups per CTA
 constexpr int kCTA = kG * kAT;    // 512 threads
 constexpr int kEdgePass = 64;     // edges per pass of a group (16 per warp)
+constexpr int kMinCTAs = 1;       // resident CTAs per SM (<= 128 registers per thread)
 constexpr int kPW = kEdgePass / 4;
 
 // group-local barrier (named barrier 1 + g over the group's 128 threads)
@@ -152,17 +153,13 @@ __device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, 
 // in-edge array of the symmetric graph (gr.in_edge == gr.inv_pos == rev).
 // ---------------------------------------------------------------------------
 template <typename T, bool FUSE_FIT>
-__global__ __launch_bounds__(kCTA, 1) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
                                                    int* __restrict__ rev, MdFuse mf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ AtomSmem<T> sms[kG];
     __shared__ T s_b[kG][kEdgePass][kK + 1];
     __shared__ int s_ty[kG][kEdgePass];
-    // this step's neighbour search is complete: clear the cell counts for the
-    // binning fused into the force kernel (device MD) / keep the zero invariant
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
-         c += gridDim.x * blockDim.x)
-        mf.cell_count[c] = 0;
+    pdl_launch_dependents();
     Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
     const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
     DevMlp<T> fit{}, msg0{};
@@ -171,6 +168,12 @@ __global__ __launch_bounds__(kCTA, 1) void k_embed(DevModel<T> md, DevGraph gr, 
     else
         msg0 = sg.mlp(md.msg[0], kInMsg, kH);
     __syncthreads();
+    pdl_wait();
+    // this step's neighbour search is complete: clear the cell counts for the
+    // binning fused into the force kernel (device MD) / keep the zero invariant
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
+         c += gridDim.x * blockDim.x)
+        mf.cell_count[c] = 0;
     const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
     AtomSmem<T>& sm = sms[g];
     const int nd = md.n_types * kK;
@@ -412,10 +415,11 @@ __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& 
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
 template <typename T, bool LAST>
-__global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
                                                      int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ AtomSmem<T> sms[kG];
+    pdl_launch_dependents();
     Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
     const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
     const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
@@ -425,6 +429,7 @@ __global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr
     else
         nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
     __syncthreads();
+    pdl_wait();
     const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
     AtomSmem<T>& sm = sms[g];
     const int n = gr.n;
@@ -510,15 +515,17 @@ __global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
 template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
                                                      int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ AtomSmem<T> sms[kG];
+    pdl_launch_dependents();
     Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
     const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
     const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
     const DevMlp<T> nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
     __syncthreads();
+    pdl_wait();
     const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
@@ -541,13 +548,15 @@ __global__ __launch_bounds__(kCTA, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
+__global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ AtomSmem<T> sms[kG];
+    pdl_launch_dependents();
     Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
     const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
     const DevMlp<T> msg0 = sg.mlp(md.msg[0], kInMsg, kH);
     __syncthreads();
+    pdl_wait();
     const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
@@ -594,13 +603,15 @@ __global__ __launch_bounds__(kCTA, 1) void k_embed_bwd(DevModel<T> md, DevGraph 
 //   W   = -sum_e g_e r_e ;  W_ab = -sum_e g_e dr_a u_b
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_force(DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T> ws,
                                                    double* __restrict__ forces,
                                                    double* __restrict__ per_atom,
                                                    double* __restrict__ out, MdFuse mf) {
     __shared__ double s_f[kG][4][3];
     __shared__ double s_part[kCTA / 32][12];
     __shared__ bool s_last;
+    pdl_launch_dependents();
+    pdl_wait();
     const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
     double acc[11];
 #pragma unroll
@@ -748,7 +759,7 @@ template <typename T, typename... Params, typename... Args>
 static void launch_staged(void (*kernel)(Params...), int grid, int smem_elems, cudaStream_t st,
                           Args... args) {
     const size_t bytes = static_cast<size_t>(smem_elems) * sizeof(T);
-    kernel<<<grid, kCTA, bytes, st>>>(args...);
+    launch_pdl(kernel, dim3(grid), dim3(kCTA), bytes, st, args...);
 }
 
 template <typename T>
@@ -805,7 +816,7 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
         mk("embed_bwd", st);
         launches += 2 + M + (M - 1);
     }
-    k_force<T><<<nb, kCTA, 0, st>>>(gr, ws, forces, per_atom, out, mf);
+    launch_pdl(k_force<T>, dim3(nb), dim3(kCTA), 0, st, gr, ws, forces, per_atom, out, mf);
     mk("force", st);
     return launches + 1;
 }
