@@ -169,6 +169,34 @@ int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* e
 int hmdp_md_destroy(hmdp_md* md);
 
 /* ---------------------------------------------------------------------------
+ * Domain decomposition (multi-GPU, per-layer rc halo).  A rank's local system is
+ * its n_own owned atoms (local 0..n_own-1) followed by halo ghosts; the CSR
+ * carries edges only for owned atoms (their rows of the global periodic list,
+ * neighbour indices remapped to local ids; ghost rows empty).  The caller runs
+ * the phases in order and exchanges halo rows between them with its transport
+ * (NCCL over NVLink in production), through the device buffers returned by
+ * hmdp_dd_buffer (rows of n_loc x 32 in the compute precision, forces n_loc x 3
+ * FP64):
+ *   phase 0 embed                      -> P rows of owned atoms (buffer 0)
+ *   [P rows of ghosts <- their owners]  phase 1 (layer 0) pushes them
+ *   phase 2 layer l forward            -> P rows (l < depth-2) / top backward
+ *   [exchange P, phase 1 (layer l+1)]
+ *   phase 3 layer l ghost sums         -> buffer 2 rows of ghosts
+ *   [owners add the ghosts' sums of their atoms into buffer 1 (zeroed first)]
+ *   phase 4 layer l backward (l = depth-3 .. 0), then phase 3 / exchange again
+ *   phase 5 embedding backward         (reads buffer 1)
+ *   phase 6 forces                     -> buffer 3 rows; ghosts' rows go to owners
+ * hmdp_dd_result: this rank's partial energy (owned atoms) and virial.
+ * Replaces: the SPEC's halo_inference with rc-deep halos
+ * exchanged per message layer instead of one L*rc-deep halo.
+ * ------------------------------------------------------------------------- */
+int hmdp_dd_setup(hmdp_ctx* ctx, int n_loc, int n_own, const int* offset, const int* nbr,
+                  const double* dr, const int* types, int precision);
+int hmdp_dd_phase(hmdp_ctx* ctx, int phase, int layer);
+int hmdp_dd_buffer(hmdp_ctx* ctx, int kind, void** dptr);
+int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* virial);
+
+/* ---------------------------------------------------------------------------
  * Measurement hooks.
  * hmdp_set_stream: run the context's work on an external cudaStream_t (e.g. the
  *   caller's current stream) instead of its own (NULL restores it).

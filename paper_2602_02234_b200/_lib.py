@@ -53,6 +53,10 @@ SIGNATURES = {
     "hmdp_md_run": (_c_int, [_vp, _c_int]),
     "hmdp_md_enqueue": (_c_int, [_vp, _c_int]),
     "hmdp_set_stream": (_c_int, [_vp, _vp]),
+    "hmdp_dd_setup": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_int]),
+    "hmdp_dd_phase": (_c_int, [_vp, _c_int, _c_int]),
+    "hmdp_dd_buffer": (_c_int, [_vp, _c_int, ctypes.POINTER(_vp)]),
+    "hmdp_dd_result": (_c_int, [_vp, _vp, _vp, _vp]),
     "hmdp_profile": (_c_int, [_vp, _c_int]),
     "hmdp_profile_read": (_c_int, [_vp, _vp, _c_int, _vp]),
     "hmdp_profile_name": (_cp, [_vp, _c_int]),

@@ -35,6 +35,9 @@ int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, doubl
                    double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cudaStream_t);
 double probe_fp32_tflops(int ms);
+template <typename T>
+void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
+                     double*, cudaStream_t);
 cudaError_t net_configure();
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
@@ -225,6 +228,11 @@ struct hmdp_ctx {
     // network workspace
     DBuf er, es, eds, eb, edb, g, grev, zb, db, pe, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
+    // domain decomposition (hmdp_dd_*): local graph + halo row buffers
+    DBuf dd_patom, dd_sremote, dd_sghost;
+    DevGraph dd_gr{};
+    int dd_prec = -1;
+    long long dd_slots = 1;
     PinnedBuf pin;
     int last_launches = 0;
     cudaStream_t user_stream = nullptr;  // hmdp_set_stream; NULL = own stream
@@ -270,7 +278,8 @@ struct hmdp_ctx {
                         &nbr, &dr, &rev, &ety, &inv_pos, &offset, &in_start, &in_cnt, &cursor,
                         &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
                         &ez1, &h, &uz1, &dhown,
-                        &e_atom, &forces, &partial, &ticket, &out, &err, &desc64})
+                        &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
+                        &dd_sremote, &dd_sghost})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -427,6 +436,7 @@ struct hmdp_ctx {
     DevGraph periodic_graph(int n, const int* d_types) {
         DevGraph gr{};
         gr.n = n;
+        gr.n_active = n;
         gr.sym = 1;
         gr.row_start = row_start.as<int>();
         gr.nnei = nnei.as<int>();
@@ -736,6 +746,7 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
                         ctx->cursor.as<int>(), ctx->in_edge.as<int>(), st);
         DevGraph gr{};
         gr.n = n;
+        gr.n_active = n;
         gr.row_start = ctx->row_start.as<int>();
         gr.nnei = ctx->nnei.as<int>();
         gr.nbr = ctx->nbr.as<int>();
@@ -866,6 +877,7 @@ int hmdp_descriptors(hmdp_ctx* ctx, int n, const int* types, const int* offset, 
         launch_csr_rows(n, ctx->offset.as<int>(), ctx->row_start.as<int>(), ctx->nnei.as<int>(), st);
         DevGraph gr{};
         gr.n = n;
+        gr.n_active = n;
         gr.row_start = ctx->row_start.as<int>();
         gr.nnei = ctx->nnei.as<int>();
         gr.nbr = ctx->nbr.as<int>();
@@ -1158,6 +1170,132 @@ int hmdp_peak_fp32(int device, int ms, double* tflops) {
         if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
         ck(cudaSetDevice(device), "cudaSetDevice");
         *tflops = probe_fp32_tflops(ms);
+    });
+}
+
+int hmdp_dd_setup(hmdp_ctx* ctx, int n_loc, int n_own, const int* offset, const int* nbr,
+                  const double* dr, const int* types, int precision) {
+    return guarded([&] {
+        need_model(ctx);
+        if (n_loc < 1 || n_own < 0 || n_own > n_loc || !offset || !types)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        const int ne = offset[n_loc];
+        if (offset[0] != 0 || ne < 0) fail(HMDP_INVALID_ARGUMENT, "NnInput CSR offsets inconsistent");
+        for (int i = 0; i < n_loc; ++i)
+            if (offset[i + 1] < offset[i] || (i >= n_own && offset[i + 1] != offset[i]))
+                fail(HMDP_INVALID_ARGUMENT, "halo ghosts must not carry edges");
+        if (ne > 0 && (!nbr || !dr)) fail(HMDP_INVALID_ARGUMENT, "required pointer is NULL");
+        for (int e = 0; e < ne; ++e)
+            if (nbr[e] < 0 || nbr[e] >= n_loc)
+                fail(HMDP_INVALID_ARGUMENT, "NnInput edge neighbor out of range");
+        check_types(n_loc, types, ctx->model.n_types);
+        set_device(ctx);
+        ctx->ensure_atoms(n_loc);
+        ctx->ensure_edges(std::max(ne, 1));
+        cudaStream_t st = ctx->st();
+        ck(cudaMemcpyAsync(ctx->types.p, types, n_loc * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(ctx->offset.p, offset, (n_loc + 1) * sizeof(int), cudaMemcpyHostToDevice, st),
+           "H2D");
+        if (ne > 0) {
+            ck(cudaMemcpyAsync(ctx->nbr.p, nbr, ne * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(ctx->dr.p, dr, 3 * static_cast<size_t>(ne) * sizeof(double),
+                               cudaMemcpyHostToDevice, st),
+               "H2D");
+        }
+        launch_csr_rows(n_loc, ctx->offset.as<int>(), ctx->row_start.as<int>(), ctx->nnei.as<int>(), st);
+        launch_in_edges(n_loc, ne, ctx->nbr.as<int>(), ctx->in_cnt.as<int>(), ctx->in_start.as<int>(),
+                        ctx->cursor.as<int>(), ctx->in_edge.as<int>(), st);
+        launch_edge_meta(ne, ctx->nbr.as<int>(), ctx->types.as<int>(), ctx->ety.as<int>(),
+                         ctx->in_edge.as<int>(), ctx->inv_pos.as<int>(), st);
+        DevGraph gr{};
+        gr.n = n_loc;
+        gr.n_active = n_own;
+        gr.sym = 0;
+        gr.row_start = ctx->row_start.as<int>();
+        gr.nnei = ctx->nnei.as<int>();
+        gr.nbr = ctx->nbr.as<int>();
+        gr.ety = ctx->ety.as<int>();
+        gr.dr = ctx->dr.as<double>();
+        gr.in_start = ctx->in_start.as<int>();
+        gr.in_cnt = ctx->in_cnt.as<int>();
+        gr.in_edge = ctx->in_edge.as<int>();
+        gr.inv_pos = ctx->inv_pos.as<int>();
+        gr.types = ctx->types.as<int>();
+        gr.is_ghost = nullptr;
+        ctx->dd_gr = gr;
+        ctx->dd_prec = precision;
+        const size_t tb = precision == HMDP_FP64 ? sizeof(double) : sizeof(float);
+        const size_t rows = static_cast<size_t>(n_loc) * kH * tb;
+        ctx->dd_patom.ensure(rows);
+        ctx->dd_sremote.ensure(rows);
+        ctx->dd_sghost.ensure(rows);
+        ck(cudaMemsetAsync(ctx->dd_patom.p, 0, rows, st), "memset");
+        ck(cudaMemsetAsync(ctx->dd_sremote.p, 0, rows, st), "memset");
+        ck(cudaMemsetAsync(ctx->dd_sghost.p, 0, rows, st), "memset");
+        ck(cudaMemsetAsync(ctx->e_atom.p, 0, n_loc * sizeof(double), st), "memset");
+        ctx->dd_slots = std::max(ne, 1);
+        if (precision == HMDP_FP64)
+            ctx->work<double>(n_loc, ctx->dd_slots);
+        else
+            ctx->work<float>(n_loc, ctx->dd_slots);
+        ck(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int hmdp_dd_phase(hmdp_ctx* ctx, int phase, int layer) {
+    return guarded([&] {
+        need_model(ctx);
+        if (ctx->dd_prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_dd_setup not called");
+        if (phase < 0 || phase > 6) fail(HMDP_INVALID_ARGUMENT, "unknown phase");
+        const int M = ctx->n_msg();
+        if ((phase >= 1 && phase <= 4) && (layer < 0 || layer > M))
+            fail(HMDP_INVALID_ARGUMENT, "layer out of range");
+        set_device(ctx);
+        const DevGraph& gr = ctx->dd_gr;
+        cudaStream_t st = ctx->st();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            DevWork<T> w = ctx->work<T>(gr.n, ctx->dd_slots);
+            w.p_atom = ctx->dd_patom.as<T>();
+            w.s_remote = ctx->dd_sremote.as<T>();
+            const DevModel<T>& md = [&]() -> const DevModel<T>& {
+                if constexpr (sizeof(T) == 8) return ctx->wd.dev;
+                else return ctx->wf.dev;
+            }();
+            launch_dd_phase<T>(md, gr, w, phase, layer, ctx->dd_sghost.as<T>(),
+                               ctx->forces.as<double>(), ctx->out.as<double>(), st);
+        };
+        if (ctx->dd_prec == HMDP_FP64)
+            run(double{});
+        else
+            run(float{});
+        ck(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int hmdp_dd_buffer(hmdp_ctx* ctx, int kind, void** dptr) {
+    if (!ctx || !dptr) return HMDP_INVALID_ARGUMENT;
+    switch (kind) {
+        case 0: *dptr = ctx->dd_patom.p; break;
+        case 1: *dptr = ctx->dd_sremote.p; break;
+        case 2: *dptr = ctx->dd_sghost.p; break;
+        case 3: *dptr = ctx->forces.p; break;
+        case 4: *dptr = ctx->e_atom.p; break;
+        default: return HMDP_INVALID_ARGUMENT;
+    }
+    return HMDP_OK;
+}
+
+int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* virial) {
+    return guarded([&] {
+        need_model(ctx);
+        set_device(ctx);
+        hmdp_ctx::raise_bits(ctx->take_err());
+        double h[16];
+        ck(cudaMemcpy(h, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        if (energy) *energy = h[0];
+        if (virial) *virial = h[1];
+        if (virial9) std::memcpy(virial9, h + 2, 9 * sizeof(double));
     });
 }
 

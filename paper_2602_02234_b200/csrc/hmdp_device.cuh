@@ -60,7 +60,8 @@ struct DevModel {
 // row_start/nnei (sym = 1).
 struct DevGraph {
     int n;
-    int sym;  // 1: in-edge array aliases the out-slots (rev), see above
+    int n_active;  // atoms [0, n_active) run the network; the rest are halo ghosts
+    int sym;       // 1: in-edge array aliases the out-slots (rev), see above
     const int* row_start;
     const int* nnei;
     const int* nbr;
@@ -88,6 +89,9 @@ struct DevWork {
     T* z;     // [M][slot][32] message hidden (tanh) activations z_e
     T* d;     // [2][in-position][32] pushed adjoints dz_e (double-buffered by layer)
     T* pe;    // [2][slot][32] pushed neighbour projections P_j = W1h h_j, per out-slot
+    // domain decomposition (nullable otherwise)
+    T* p_atom;    // [n][32] per-atom P of the layer just produced (sent to ghost copies)
+    T* s_remote;  // [n][32] adjoint partial sums received from ghost copies elsewhere
     // per atom
     T* desc;   // [n][32] descriptor (n_types*8 used)
     T* ez1;    // [n][32] embedding hidden activations

@@ -179,7 +179,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
     const int nd = md.n_types * kK;
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         T desc = T(0);  // thread q < nd accumulates descriptor component q
         for (int base = 0; base < cnt; base += kEdgePass) {
@@ -304,7 +304,10 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
         } else {
             // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
             const T p = bmv<T, 32, 32>(msg0.W1, kInMsg, sm.v2, t);
-            if (lead) sm.v3[o] = p;
+            if (lead) {
+                sm.v3[o] = p;
+                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
+            }
             gsync(g);
             push_rows(ws.pe, sm.v3, gr, i, t);
         }
@@ -406,7 +409,12 @@ __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& 
     }
     sm.part[w][lane] = acc;
     gsync(g);
-    if (t < 32) sm.v1[t] = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
+    if (t < 32) {
+        T s = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
+        // domain decomposition: partial sums pushed to ghost copies of i on other ranks
+        if (ws.s_remote) s += ws.s_remote[static_cast<long long>(i) * kH + t];
+        sm.v1[t] = s;
+    }
     gsync(g);
 }
 
@@ -442,7 +450,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevG
     const T b1 = msg.b1[lane];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < n; i += gridDim.x * kG) {
+    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         if (t < 32) sm.v1[t] = ws.h[(static_cast<long long>(l) * n + i) * kH + t];  // h_i
         T acc = T(0), ssum = T(0);
@@ -500,7 +508,10 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevG
         gsync(g);
         if constexpr (!LAST) {
             const T p = bmv<T, 32, 32>(nxt.W1, kInMsg, sm.v3, t);
-            if (lead) sm.v0[o] = p;
+            if (lead) {
+                sm.v0[o] = p;
+                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
+            }
             gsync(g);
             push_rows(ws.pe + ((l + 1) & 1) * S * kH, sm.v0, gr, i, t);
         } else {
@@ -530,7 +541,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_bwd(DevModel<T> md, DevG
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
         const T own = ws.dhown[static_cast<long long>(i) * kH + o];
         const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + o];
         gather_in(gr, ws, sm, l + 1, i, t, g);
@@ -561,7 +572,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed_bwd(DevModel<T> md, De
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
         const T own = ws.dhown[static_cast<long long>(i) * kH + o];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + o];
         gather_in(gr, ws, sm, 0, i, t, g);
@@ -744,6 +755,32 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T
 }
 
 // ---------------------------------------------------------------------------
+// Domain-decomposition helpers (halo ghosts are atoms [n_active, n)).
+// ---------------------------------------------------------------------------
+// Push the received per-atom projections P of halo ghosts into their in-edge
+// slots (what the owner would have pushed had the ghost been local).
+template <typename T>
+__global__ void k_dd_push_ghosts(DevGraph gr, const T* __restrict__ p_atom, T* __restrict__ pe) {
+    const int i = gr.n_active + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= gr.n) return;
+    const T v = p_atom[static_cast<long long>(i) * kH + lane];
+    const int is = gr.in_start[i], ic = gr.in_cnt[i];
+    for (int k = 0; k < ic; ++k) pe[static_cast<long long>(gr.in_edge[is + k]) * kH + lane] = v;
+}
+// Partial dE/dh adjoint sums collected at halo ghosts (sent back to the owners).
+template <typename T>
+__global__ void k_dd_ghost_sums(DevGraph gr, const T* __restrict__ d, T* __restrict__ out) {
+    const int i = gr.n_active + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= gr.n) return;
+    const int is = gr.in_start[i], ic = gr.in_cnt[i];
+    T s = T(0);
+    for (int k = 0; k < ic; ++k) s += d[static_cast<long long>(is + k) * kH + lane];
+    out[static_cast<long long>(i) * kH + lane] = s;
+}
+
+// ---------------------------------------------------------------------------
 // launch
 // ---------------------------------------------------------------------------
 static int net_grid(int n) {
@@ -820,6 +857,63 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
     mk("force", st);
     return launches + 1;
 }
+// One phase of a domain-decomposed evaluation (the caller exchanges halo rows
+// between phases).  Phases: 0 embed, 1 push ghost P (into parity `l`), 2 message
+// layer l forward, 3 ghost adjoint sums of layer l, 4 message layer l backward,
+// 5 embedding backward, 6 forces.
+template <typename T>
+void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
+                     int l, T* s_ghost, double* forces, double* out, cudaStream_t st) {
+    const int nb = net_grid(gr.n_active);
+    const int M = md.n_msg;
+    const int e_emb = mlp_elems(kInEmbed, kH), e_fit = mlp_elems(kInFit, 1);
+    const int e_msg = mlp_elems(kInMsg, kH), e_upd = mlp_elems(kInUpd, kH);
+    const int ng = gr.n - gr.n_active;
+    const MdFuse none{};
+    switch (phase) {
+        case 0:
+            if (M == 0)
+                launch_staged<T>(k_embed<T, true>, nb, e_emb + e_fit, st, md, gr, ws,
+                                 static_cast<int*>(nullptr), none);
+            else
+                launch_staged<T>(k_embed<T, false>, nb, e_emb + e_msg, st, md, gr, ws,
+                                 static_cast<int*>(nullptr), none);
+            break;
+        case 1:
+            if (ng > 0)
+                k_dd_push_ghosts<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
+                    gr, ws.p_atom, ws.pe + (l & 1) * ws.slots * kH);
+            break;
+        case 2:
+            if (l == M - 1)
+                launch_staged<T>(k_msg_fwd<T, true>, nb, e_msg + e_upd + e_fit, st, md, gr, ws, l);
+            else
+                launch_staged<T>(k_msg_fwd<T, false>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
+            break;
+        case 3:
+            if (ng > 0)
+                k_dd_ghost_sums<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
+                    gr, ws.d + (l & 1) * ws.slots * kH, s_ghost);
+            break;
+        case 4:
+            launch_staged<T>(k_msg_bwd<T>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
+            break;
+        case 5:
+            launch_staged<T>(k_embed_bwd<T>, nb, e_emb + e_msg, st, md, gr, ws);
+            break;
+        case 6:
+            launch_pdl(k_force<T>, dim3(net_grid(gr.n)), dim3(kCTA), 0, st, gr, ws, forces,
+                       static_cast<double*>(nullptr), out, none);
+            break;
+    }
+}
+template void launch_dd_phase<float>(const DevModel<float>&, const DevGraph&,
+                                     const DevWork<float>&, int, int, float*, double*, double*,
+                                     cudaStream_t);
+template void launch_dd_phase<double>(const DevModel<double>&, const DevGraph&,
+                                      const DevWork<double>&, int, int, double*, double*, double*,
+                                      cudaStream_t);
+
 template int launch_network<float>(const DevModel<float>&, const DevGraph&, const DevWork<float>&,
                                    double*, double*, double*, int*, cudaStream_t, const Marker&,
                                    const MdFuse&);
