@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", choices=["dd", "replicas"], default="dd",
+                    help="N>1: domain decomposition (default) or independent replica boxes")
     return ap.parse_args()
 
 
@@ -434,6 +436,104 @@ def run_ours(args, rank, world, local_rank, dist):
     print(json.dumps(line), flush=True)
 
 
+def run_dd(args, rank, world, local_rank, dist):
+    """N > 1: domain-decomposed force evaluation (weak scaling).  The global box
+    is the per-rank box replicated over the rank grid (1x1x1, 2x1x1, 2x2x1,
+    2x2x2), so each GPU owns one box's worth of atoms.  A step = device neighbour
+    list of the global box, halo plans, and the DD evaluation with its NCCL halo
+    rounds (P^l forward, dE/dh partials backward, ghost forces) plus the (E, W)
+    all-reduce.  value = world * steps / max-over-ranks time (box-steps/s)."""
+    import numpy as np
+    import torch
+
+    import paper_2602_02234_b200 as P
+    from paper_2602_02234_b200 import dd
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    fam, depth = MODELS[args.model]
+    prec = P.Precision[args.precision]
+    model = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
+    base = P.generate_synthetic_system(SYSTEMS[args.system])
+    dims = dd.rank_grid(world)
+    s = P.replicate(base, dims)
+    n = s.n_atoms
+    eng = dd.GpuEngine(P.Context(model, device=local_rank, max_atoms=n), prec)
+
+    class TimedTransport(dd.TorchDistTransport):
+        halo_ms = 0.0
+        rounds = 0
+
+        def exchange(self, send, width, like):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = super().exchange(send, width, like)
+            b.record()
+            b.synchronize()
+            TimedTransport.halo_ms += a.elapsed_time(b)
+            TimedTransport.rounds += 1
+            return out
+
+    tr = TimedTransport()
+    gidx = np.arange(n)
+
+    def step():
+        inp = P.build_input_periodic(s.positions, s.types, gidx, s.box, 0.6, device=local_rank)
+        own = dd.owners(s.positions, s.box, dims)
+        plans = dd.make_plans(inp.edge_offset, inp.edge_neighbor, inp.edge_dr, s.types, own, world)
+        return dd.evaluate_dd(eng, tr, plans, rank, model.depth()), plans
+
+    for _ in range(max(args.warmup, 1)):
+        (E, F, W, W9), plans = step()
+    e_single = P.Context(model, device=local_rank).compute(base.positions, base.types, base.box,
+                                                           P.Precision.fp64).energy
+    K = args.steps
+    TimedTransport.halo_ms, TimedTransport.rounds = 0.0, 0
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        (E, F, W, W9), plans = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t_ms = e0.elapsed_time(e1)
+    tt = torch.tensor([t_ms, TimedTransport.halo_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms, halo_ms = float(tt[0]), float(tt[1])
+    value = world * K / (t_ms * 1e-3)
+    if rank != 0:
+        return
+    p = plans[rank]
+    line = {
+        "metric": METRIC, "value": value, "unit": f"steps/s ({args.system}-box equivalents)",
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
+        "config": {"workload": f"{args.model.upper()} domain-decomposed force evaluation, "
+                               f"{args.system} box replicated {dims} (one box per GPU)",
+                   "model": args.model, "system": args.system, "atoms_total": n,
+                   "rank_grid": list(dims), "precision": args.precision,
+                   "parallelism": f"spatial DD x{world}, rc halo exchanged per message layer "
+                                  f"(NCCL all_to_all), E/W all-reduce",
+                   "rank0_owned": p.n_own, "rank0_ghosts": int(p.ghosts.shape[0])},
+        "ns_per_day_per_box": ns_per_day(value / world),
+        "halo": {"ms_per_step": halo_ms / K, "rounds_per_step": TimedTransport.rounds / K,
+                 "share": halo_ms / t_ms},
+        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * world,
+                        "rel_diff": abs(E - e_single * world) / abs(e_single * world)},
+        "gpu_launches": None,
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": None,
+                "d2h_bytes_per_step": None,
+                "note": "host-orchestrated DD step (host CSR + plans each step)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -445,10 +545,19 @@ def main():
     if world > 1:
         import torch.distributed as td
 
-        td.init_process_group("nccl", init_method="env://")
+        # BENCH_DD_BACKEND=gloo allows a dry run of the N>1 path with several ranks
+        # sharing one GPU (NCCL needs one GPU per rank)
+        td.init_process_group(os.environ.get("BENCH_DD_BACKEND", "nccl"), init_method="env://")
         dist = td
+        if os.environ.get("BENCH_DD_BACKEND", "nccl") != "nccl":
+            import torch
+
+            local_rank = local_rank % max(1, torch.cuda.device_count())
     try:
-        run_ours(args, rank, world, local_rank, dist)
+        if world > 1 and args.mode == "dd":
+            run_dd(args, rank, world, local_rank, dist)
+        else:
+            run_ours(args, rank, world, local_rank, dist)
     finally:
         if dist:
             dist.destroy_process_group()

@@ -134,20 +134,23 @@ class TorchDistTransport:
     def exchange(self, send: dict, width: int, like):
         import torch
 
+        # NCCL moves device buffers directly (NVLink); other backends (gloo, for
+        # tests and single-GPU dry runs) stage through host memory
+        dev = like.device if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu")
         sizes_out = [int(send[p].shape[0]) if p in send else 0 for p in range(self.size)]
-        cnt = torch.tensor(sizes_out, dtype=torch.int64, device=like.device)
+        cnt = torch.tensor(sizes_out, dtype=torch.int64, device=dev)
         cnt_in = torch.empty_like(cnt)
         self.dist.all_to_all_single(cnt_in, cnt, group=self.group)
         sizes_in = [int(v) for v in cnt_in.tolist()]
-        parts = [send[p] for p in range(self.size) if p in send and send[p].shape[0]]
-        flat = torch.cat(parts).reshape(-1) if parts else torch.zeros(0, dtype=like.dtype, device=like.device)
-        out = torch.empty(sum(sizes_in) * width, dtype=like.dtype, device=like.device)
+        parts = [send[p].to(dev) for p in range(self.size) if p in send and send[p].shape[0]]
+        flat = torch.cat(parts).reshape(-1) if parts else torch.zeros(0, dtype=like.dtype, device=dev)
+        out = torch.empty(sum(sizes_in) * width, dtype=like.dtype, device=dev)
         self.dist.all_to_all_single(out, flat.contiguous(), [s * width for s in sizes_in],
                                     [s * width for s in sizes_out], group=self.group)
         res, o = {}, 0
         for p, s in enumerate(sizes_in):
             if s:
-                res[p] = out[o:o + s * width].reshape(s, width)
+                res[p] = out[o:o + s * width].reshape(s, width).to(like.device)
             o += s * width
         return res
 
