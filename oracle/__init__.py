@@ -32,7 +32,7 @@ def build(ref: bool = True) -> None:
     """make -C oracle (restatement always; reference only if /root/reference exists)."""
     targets = ["oracle"]
     if ref and os.path.exists("/root/reference/proj/src/nn/inference.cpp"):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
