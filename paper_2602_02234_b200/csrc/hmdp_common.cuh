@@ -203,4 +203,155 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
 }
+
+// ---------------------------------------------------------------------------
+// Neighbour search body for one 128-thread group (named barrier `bar`).
+// The deduplicated 27 neighbouring cells' member lists form one candidate index
+// space spread over the group (about two candidates per thread at the paper
+// densities); every j with FP64 minimum-image |dr|^2 <= rc^2
+// (neighborlist.cpp:91-93) survives; survivors are ranked ascending (the
+// reference's sorted full pair list, neighborlist.cpp:104-111) and written with
+// their FP64 edge_dr (inference.cpp:474-485) and neighbour type.
+// ---------------------------------------------------------------------------
+struct NbrSmem {
+    int cand[kCandMax];
+    int cell[32];
+    int off[33];
+    int wcnt[4];
+};
+
+__device__ __forceinline__ void group_bar(int bar) {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(kAT) : "memory");
+}
+
+__device__ __forceinline__ void nbr_search_atom(int i, const double* pos,
+                                                const CellGrid& cg, const int* cell_count,
+                                                const int* members,
+                                                const int* cell_of, double range2, int cap,
+                                                int* __restrict__ nnei, int* __restrict__ row_start,
+                                                int* __restrict__ nbr, double* __restrict__ dr,
+                                                const int* __restrict__ types, int* __restrict__ ety,
+                                                unsigned* err, NbrSmem& sm, int t, int bar) {
+    const int lane = t & 31, w = t >> 5;
+    const double L0 = cg.L[0], L1 = cg.L[1], L2 = cg.L[2];
+    const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+    if (w == 0) {
+        const int ci = cell_of[i];
+        const int cx = ci % cg.nc[0], cy = (ci / cg.nc[0]) % cg.nc[1], cz = ci / (cg.nc[0] * cg.nc[1]);
+        int nid = -1;
+        if (lane < 27) {
+            const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+            const int x = ((cx + dx) % cg.nc[0] + cg.nc[0]) % cg.nc[0];
+            const int y = ((cy + dy) % cg.nc[1] + cg.nc[1]) % cg.nc[1];
+            const int z = ((cz + dz) % cg.nc[2] + cg.nc[2]) % cg.nc[2];
+            nid = (z * cg.nc[1] + y) * cg.nc[0] + x;
+        }
+        bool unique = lane < 27;
+        for (int q = 0; q < 27; ++q) {
+            const int other = __shfl_sync(FULL_MASK, nid, q);
+            if (q < lane && other == nid) unique = false;
+        }
+        int cnt = 0;
+        if (unique) {
+            cnt = cell_count[nid];
+            cnt = cnt < cg.ccap ? cnt : cg.ccap;
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += v;
+        }
+        sm.cell[lane] = nid;
+        sm.off[lane + 1] = incl;
+        if (lane == 0) sm.off[0] = 0;
+    }
+    group_bar(bar);
+    const int ncand = sm.off[27];
+    int total = 0;
+    for (int q0 = 0; q0 < ncand; q0 += 2 * kAT) {
+        int jr[2];
+        bool pass[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // candidate indices: independent loads
+            const int q = q0 + u * kAT + t;
+            jr[u] = -1;
+            if (q < ncand) {
+                int lo = 0, hi = 26;  // cell slot owning candidate q
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sm.off[mid] <= q) lo = mid;
+                    else hi = mid - 1;
+                }
+                jr[u] = members[sm.cell[lo] * cg.ccap + (q - sm.off[lo])];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // FP64 pair test, no FMA contraction
+            pass[u] = false;
+            const int j = jr[u];
+            if (j >= 0 && j != i) {
+                const double dx = min_image1(__dsub_rn(pos[3 * j], xi), L0);
+                const double dy = min_image1(__dsub_rn(pos[3 * j + 1], yi), L1);
+                const double dz = min_image1(__dsub_rn(pos[3 * j + 2], zi), L2);
+                pass[u] = !(norm2_rn(dx, dy, dz) > range2);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // group-wide compaction
+            const unsigned bal = __ballot_sync(FULL_MASK, pass[u]);
+            if (lane == 0) sm.wcnt[w] = __popc(bal);
+            group_bar(bar);
+            int off = total;
+            for (int q = 0; q < w; ++q) off += sm.wcnt[q];
+            if (pass[u]) {
+                const int idx = off + __popc(bal & ((1u << lane) - 1u));
+                if (idx < kCandMax) sm.cand[idx] = jr[u];
+            }
+            total += ((sm.wcnt[0] + sm.wcnt[1]) + sm.wcnt[2]) + sm.wcnt[3];
+            group_bar(bar);
+        }
+    }
+    int m = total;
+    if (m > cap || m > kCandMax) {
+        if (t == 0) atomicOr(err, kErrNbrOverflow);
+        m = cap < kCandMax ? cap : kCandMax;
+    }
+    for (int q = t; q < m; q += kAT) {
+        const int v = sm.cand[q];
+        int rank = 0;
+        for (int p = 0; p < m; ++p) rank += sm.cand[p] < v;
+        const long long slot = static_cast<long long>(i) * cap + rank;
+        nbr[slot] = v;
+        if (ety) ety[slot] = types[v];
+        dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
+        dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
+        dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
+    }
+    if (t == 0) {
+        nnei[i] = m;
+        row_start[i] = i * cap;
+    }
+    group_bar(bar);
+}
+
+// Opening of a device-MD chunk for atom i: first half kick + drift + binning
+// (integrators.cpp:35-39 after the finite check of :12-18).
+__device__ __forceinline__ void vv_kick_drift_bin_atom(int i, const MdFuse& mf,
+                                                       const double* f, unsigned* err) {
+    const double s = mf.half / mf.m[i];
+    bool finite = true;
+    double x3[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double fa = f[3 * i + a];
+        finite &= isfinite(fa);
+        const double va = __dadd_rn(mf.v[3 * i + a], __dmul_rn(fa, s));
+        mf.v[3 * i + a] = va;
+        x3[a] = __dadd_rn(mf.x[3 * i + a], __dmul_rn(va, mf.dt));
+        mf.x[3 * i + a] = x3[a];
+    }
+    if (!finite) atomicOr(err, kErrNonFinite);
+    bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, err);
+}
 }  // namespace hmdp

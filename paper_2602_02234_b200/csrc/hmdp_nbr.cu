@@ -1,13 +1,15 @@
 // hmdp_nbr.cu — cell-list neighbour search, CSR/in-edge plumbing, the FP64
-// descriptor API and the velocity-Verlet kernels of the device MD loop.
+// descriptor API and the velocity-Verlet opening kernel of the device MD loop.
+// The per-atom bodies (bin_atom, nbr_search_atom, vv_kick_drift_bin_atom) live
+// in hmdp_common.cuh so the persistent MD kernel (hmdp_net.cu) reuses them.
 //
 // Reference correspondence (paths relative to /root/reference/proj):
-//   bin_atom / k_cell_bin   build_grid + wrap_position   src/neighborlist.cpp:21-38,
-//                                                        include/halomd/box.hpp:34-42
-//   k_nbr_search            build_neighbor_list (full)   src/neighborlist.cpp:42-113
-//                           + CSR edge_dr                src/nn/inference.cpp:474-485
-//   k_descriptors_f64       descriptors()                src/nn/inference.cpp:430-447
-//   k_vv_*                  velocity_verlet_step         src/integrators.cpp:12-47
+//   k_cell_bin          build_grid + wrap_position   src/neighborlist.cpp:21-38,
+//                                                    include/halomd/box.hpp:34-42
+//   k_nbr_search        build_neighbor_list (full)   src/neighborlist.cpp:42-113
+//                       + CSR edge_dr                src/nn/inference.cpp:474-485
+//   k_descriptors_f64   descriptors()                src/nn/inference.cpp:430-447
+//   k_vv_kick_drift_bin velocity_verlet_step         src/integrators.cpp:12-47
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -20,128 +22,19 @@ __global__ void k_cell_bin(int n, const double* __restrict__ pos, CellGrid cg,
     bin_atom(i, pos + 3 * i, cg, cell_count, members, cell_of, err);
 }
 
-// One 128-thread CTA per atom (grid-stride over atoms).  The deduplicated 27
-// neighbouring cells' member lists form one candidate index space spread over
-// the CTA (about two candidates per thread at the paper densities); every j
-// with FP64 minimum-image |dr|^2 <= rc^2 (neighborlist.cpp:91-93) survives;
-// survivors are ranked ascending (the reference's sorted full pair list,
-// neighborlist.cpp:104-111) and written with their FP64 edge_dr.
+// One 128-thread CTA per atom (grid-stride over atoms).
 __global__ __launch_bounds__(kAT) void k_nbr_search(
     int n, const double* __restrict__ pos, CellGrid cg, const int* __restrict__ cell_count,
     const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
     int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
     double* __restrict__ dr, const int* __restrict__ types, int* __restrict__ ety,
     unsigned* err) {
-    __shared__ int s_cand[kCandMax];
-    __shared__ int s_cell[32];
-    __shared__ int s_off[33];
-    __shared__ int s_wcnt[4];
+    __shared__ NbrSmem sm;
     pdl_launch_dependents();
     pdl_wait();
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const double L0 = cg.L[0], L1 = cg.L[1], L2 = cg.L[2];
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
-        if (w == 0) {
-            const int ci = cell_of[i];
-            const int cx = ci % cg.nc[0], cy = (ci / cg.nc[0]) % cg.nc[1],
-                      cz = ci / (cg.nc[0] * cg.nc[1]);
-            int nid = -1;
-            if (lane < 27) {
-                const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
-                const int x = ((cx + dx) % cg.nc[0] + cg.nc[0]) % cg.nc[0];
-                const int y = ((cy + dy) % cg.nc[1] + cg.nc[1]) % cg.nc[1];
-                const int z = ((cz + dz) % cg.nc[2] + cg.nc[2]) % cg.nc[2];
-                nid = (z * cg.nc[1] + y) * cg.nc[0] + x;
-            }
-            bool unique = lane < 27;
-            for (int q = 0; q < 27; ++q) {
-                const int other = __shfl_sync(FULL_MASK, nid, q);
-                if (q < lane && other == nid) unique = false;
-            }
-            int cnt = 0;
-            if (unique) {
-                cnt = cell_count[nid];
-                cnt = cnt < cg.ccap ? cnt : cg.ccap;
-            }
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(FULL_MASK, incl, o);
-                if (lane >= o) incl += v;
-            }
-            s_cell[lane] = nid;
-            s_off[lane + 1] = incl;
-            if (lane == 0) s_off[0] = 0;
-        }
-        __syncthreads();
-        const int ncand = s_off[27];
-        int total = 0;
-        for (int q0 = 0; q0 < ncand; q0 += 2 * kAT) {
-            int jr[2];
-            bool pass[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {  // candidate indices: independent loads
-                const int q = q0 + u * kAT + t;
-                jr[u] = -1;
-                if (q < ncand) {
-                    int lo = 0, hi = 26;  // cell slot owning candidate q
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (s_off[mid] <= q) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    jr[u] = members[s_cell[lo] * cg.ccap + (q - s_off[lo])];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {  // FP64 pair test, no FMA contraction
-                pass[u] = false;
-                const int j = jr[u];
-                if (j >= 0 && j != i) {
-                    const double dx = min_image1(__dsub_rn(pos[3 * j], xi), L0);
-                    const double dy = min_image1(__dsub_rn(pos[3 * j + 1], yi), L1);
-                    const double dz = min_image1(__dsub_rn(pos[3 * j + 2], zi), L2);
-                    pass[u] = !(norm2_rn(dx, dy, dz) > range2);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {  // CTA-wide compaction
-                const unsigned bal = __ballot_sync(FULL_MASK, pass[u]);
-                if (lane == 0) s_wcnt[w] = __popc(bal);
-                __syncthreads();
-                int off = total;
-                for (int q = 0; q < w; ++q) off += s_wcnt[q];
-                if (pass[u]) {
-                    const int idx = off + __popc(bal & ((1u << lane) - 1u));
-                    if (idx < kCandMax) s_cand[idx] = jr[u];
-                }
-                total += ((s_wcnt[0] + s_wcnt[1]) + s_wcnt[2]) + s_wcnt[3];
-                __syncthreads();
-            }
-        }
-        int m = total;
-        if (m > cap || m > kCandMax) {
-            if (t == 0) atomicOr(err, kErrNbrOverflow);
-            m = cap < kCandMax ? cap : kCandMax;
-        }
-        for (int q = t; q < m; q += kAT) {
-            const int v = s_cand[q];
-            int rank = 0;
-            for (int p = 0; p < m; ++p) rank += s_cand[p] < v;
-            const long long slot = static_cast<long long>(i) * cap + rank;
-            nbr[slot] = v;
-            if (ety) ety[slot] = types[v];
-            dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
-            dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
-            dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
-        }
-        if (t == 0) {
-            nnei[i] = m;
-            row_start[i] = i * cap;
-        }
-        __syncthreads();
-    }
+    for (int i = blockIdx.x; i < n; i += gridDim.x)
+        nbr_search_atom(i, pos, cg, cell_count, members, cell_of, range2, cap, nnei, row_start, nbr,
+                        dr, types, ety, err, sm, threadIdx.x, 1);
 }
 
 // CSR offsets -> (row_start, nnei)
@@ -207,7 +100,7 @@ __global__ void k_in_sort(int n, const int* __restrict__ in_start, const int* __
     if (i >= n) return;
     int* a = in_edge + in_start[i];
     const int m = in_cnt[i];
-    for (int p = 1; p < m; ++p) {
+    for (int p = 1; p < m; ++p) {  // insertion sort: lists are ~30 long
         const int v = a[p];
         int q = p - 1;
         while (q >= 0 && a[q] > v) {
@@ -216,6 +109,17 @@ __global__ void k_in_sort(int n, const int* __restrict__ in_start, const int* __
         }
         a[q + 1] = v;
     }
+}
+
+// Generic CSR path: neighbour types per edge and the mirror index of each edge.
+__global__ void k_edge_meta(int ne, const int* __restrict__ nbr, const int* __restrict__ types,
+                            int* __restrict__ ety) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < ne) ety[e] = types[nbr[e]];
+}
+__global__ void k_inv_pos(int ne, const int* __restrict__ in_edge, int* __restrict__ inv_pos) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < ne) inv_pos[in_edge[q]] = q;
 }
 
 // FP64 descriptors() (inference.cpp:430-447): one warp per atom, lane = (type, k).
@@ -245,26 +149,11 @@ __global__ __launch_bounds__(128) void k_descriptors_f64(DevModel<double> md, De
     desc[static_cast<long long>(i) * nd + lane] = acc;
 }
 
-// Opening of a device-MD chunk: first half kick + drift + binning
-// (integrators.cpp:35-39 after the finite check of :12-18).
 __global__ void k_vv_kick_drift_bin(int n, MdFuse mf, const double* __restrict__ f,
                                     unsigned* err) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double s = mf.half / mf.m[i];
-    bool finite = true;
-    double x3[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const double fa = f[3 * i + a];
-        finite &= isfinite(fa);
-        const double va = __dadd_rn(mf.v[3 * i + a], __dmul_rn(fa, s));
-        mf.v[3 * i + a] = va;
-        x3[a] = __dadd_rn(mf.x[3 * i + a], __dmul_rn(va, mf.dt));
-        mf.x[3 * i + a] = x3[a];
-    }
-    if (!finite) atomicOr(err, kErrNonFinite);
-    bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, err);
+    vv_kick_drift_bin_atom(i, mf, f, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -296,17 +185,6 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        unsigned* err, cudaStream_t st) {
     launch_pdl(k_nbr_search, dim3(atom_grid(n)), dim3(kAT), 0, st, n, pos, cg, cell_count, members,
                cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety, err);
-}
-
-// Generic CSR path: neighbour types per edge and the mirror index of each edge.
-__global__ void k_edge_meta(int ne, const int* __restrict__ nbr, const int* __restrict__ types,
-                            int* __restrict__ ety) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < ne) ety[e] = types[nbr[e]];
-}
-__global__ void k_inv_pos(int ne, const int* __restrict__ in_edge, int* __restrict__ inv_pos) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < ne) inv_pos[in_edge[q]] = q;
 }
 void launch_edge_meta(int ne, const int* nbr, const int* types, int* ety, const int* in_edge,
                       int* inv_pos, cudaStream_t st) {

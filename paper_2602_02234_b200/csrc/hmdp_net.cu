@@ -4,11 +4,15 @@
 // Decomposition: a 512-thread CTA holds four independent 128-thread "atom
 // groups"; each group processes one atom at a time (grid-stride over atoms) and
 // synchronises with its own named barrier, so the groups never wait on each
-// other.  Every kernel first stages the MLP weights it needs into shared memory
-// (once per CTA, ~1 CTA per SM), so the atom-level mat-vecs (bmv: 4-way split,
-// xor-shuffle reduction) read weights and activations from shared memory only.
-// Per-edge work is split over the group's 4 warps (edge q -> warp q % 4) with
-// lane = channel, so every per-edge row access is one coalesced 128-byte line.
+// other.  Kernels stage the MLP weights they need into shared memory (once per
+// CTA, ~1 CTA per SM), so the atom-level mat-vecs (bmv: 4-way split, xor-shuffle
+// reduction) read weights and activations from shared memory only.  Per-edge
+// work is split over the group's 4 warps (edge q -> warp q % 4) with lane =
+// channel, so every per-edge row access is one coalesced 128-byte line; the
+// per-edge scalars are staged in shared memory and read as broadcasts.
+//
+// Every phase is a per-group __device__ body (grid-stride over atoms) wrapped by
+// a thin kernel that stages the weights it needs.
 //
 // Dataflow is "push" into mirror slots (DevGraph, hmdp_device.cuh): the producer
 // of a per-neighbour quantity writes it into the slot its consumer reads
@@ -30,13 +34,14 @@
 //             dE/dh_j += W1h^T sum_{e in in(j)} dz_e  (one mat-vec per atom).
 //
 // Reference correspondence (paths relative to /root/reference/proj):
-//   k_embed      edge radial + descriptor + embedding fwd   src/nn/inference.cpp:214-249
-//                [FUSE_FIT: + fitting fwd/bwd + embedding bwd, :288-311, :355-370]
-//   k_msg_fwd    message layer fwd                          :251-286
-//                [LAST: + fitting fwd/bwd + top message layer bwd, :288-353]
-//   k_msg_bwd    message layer bwd (lower layers)           :313-353
-//   k_embed_bwd  embedding + descriptor adjoint             :355-370
-//   k_force      force / virial (gather form) + E, W sums   :288-298, :372-387
+//   embed_body       edge radial + descriptor + embedding fwd   src/nn/inference.cpp:214-249
+//                    [FUSE_FIT: + fitting fwd/bwd + embedding bwd, :288-311, :355-370]
+//   msg_fwd_body     message layer fwd                          :251-286
+//                    [LAST: + fitting fwd/bwd + top message layer bwd, :288-353]
+//   msg_bwd_body     message layer bwd (lower layers)           :313-353
+//   embed_bwd_body   embedding + descriptor adjoint             :355-370
+//   force_body       force / virial (gather form) + E, W sums   :288-298, :372-387
+//                    [+ velocity Verlet tail, src/integrators.cpp:32-47]
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -46,13 +51,10 @@ int num_sms();  // hmdp_nbr.cu
 constexpr int kG = 4;             // atom groups per CTA
 constexpr int kCTA = kG * kAT;    // 512 threads
 constexpr int kEdgePass = 64;     // edges per pass of a group (16 per warp)
-constexpr int kMinCTAs = 1;       // resident CTAs per SM (<= 128 registers per thread)
 constexpr int kPW = kEdgePass / 4;
 
 // group-local barrier (named barrier 1 + g over the group's 128 threads)
-__device__ __forceinline__ void gsync(int g) {
-    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kAT) : "memory");
-}
+__device__ __forceinline__ void gsync(int g) { group_bar(g + 1); }
 
 // Sum over a group's 128 threads (every thread gets the total); fixed order.
 template <typename T>
@@ -71,6 +73,9 @@ struct AtomSmem {
     T part[4][32];                     // per-warp partial channel sums
     T s4[4];                           // group_sum scratch
     T sc[4];                           // per-warp scalar partials
+    alignas(16) T ed[4][16][12];       // per-warp staged edge scalars (s, s', b or b')
+    int emir[4][16];                   // per-warp staged mirror slots
+    double f[4][3];                    // per-warp force partials
 };
 
 // ---------------------------------------------------------------------------
@@ -94,6 +99,12 @@ struct Stager {
         off += (count + 3) / 4 * 4;
         return dst;
     }
+    // per-group scratch placed after the staged weights (same dynamic region)
+    template <class S>
+    __device__ S* scratch(int skip_bytes = 0) const {
+        const size_t a = (reinterpret_cast<size_t>(base + off) + 15) & ~size_t(15);
+        return reinterpret_cast<S*>(a + skip_bytes);
+    }
     __device__ DevMlp<T> mlp(const DevMlp<T>& m, int in, int out) {
         DevMlp<T> d;
         d.W1 = put(m.W1, 32 * in);
@@ -108,6 +119,16 @@ struct Stager {
 // (the device weight buffer pads every array to a multiple of 32 elements, so
 // the rounded-up copies above never read past an array's allocation)
 
+// Group coordinates of this thread.
+struct Grp {
+    int g, t, gid, ngroups;
+    __device__ Grp()
+        : g(threadIdx.x / kAT),
+          t(threadIdx.x % kAT),
+          gid(blockIdx.x * kG + threadIdx.x / kAT),
+          ngroups(gridDim.x * kG) {}
+};
+
 // Push a 32-vector (smem) into the rows `dst + in_edge[in_start + k] * 32` for
 // k < in_cnt (the out-slots of i's in-edges): 4 rows per group iteration.
 template <typename T>
@@ -119,6 +140,33 @@ __device__ __forceinline__ void push_rows(T* __restrict__ dst, const T* vec, con
         const long long slot = gr.in_edge[is + k];
         dst[slot * kH + (t & 31)] = v;
     }
+}
+
+// Sum each of 8 per-lane values over the warp (reduce-scatter butterfly, fixed
+// order): returns, in lane l, the total of value (l >> 2).  9 shuffles instead
+// of the 40 of eight separate warp reductions.
+template <typename T>
+__device__ __forceinline__ T reduce8(T (&a)[8], int lane) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool hi = lane & 16;
+        const T keep = hi ? a[j + 4] : a[j], send = hi ? a[j] : a[j + 4];
+        a[j] = keep + __shfl_xor_sync(FULL_MASK, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const bool hi = lane & 8;
+        const T keep = hi ? a[j + 2] : a[j], send = hi ? a[j] : a[j + 2];
+        a[j] = keep + __shfl_xor_sync(FULL_MASK, send, 8);
+    }
+    {
+        const bool hi = lane & 4;
+        const T keep = hi ? a[1] : a[0], send = hi ? a[0] : a[1];
+        a[0] = keep + __shfl_xor_sync(FULL_MASK, send, 4);
+    }
+    a[0] += __shfl_xor_sync(FULL_MASK, a[0], 2);
+    a[0] += __shfl_xor_sync(FULL_MASK, a[0], 1);
+    return a[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -148,38 +196,28 @@ __device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, 
 
 // ---------------------------------------------------------------------------
 // Edge radial features + descriptor + embedding; pushes P^0 (message layer 0's
-// neighbour projection) or, for depth 1, runs the whole fitting/backward chain.
-// rev (periodic path): computes the reverse slot of every edge, which is the
-// in-edge array of the symmetric graph (gr.in_edge == gr.inv_pos == rev).
+// neighbour projection) or, for depth 1 (FUSE_FIT), runs the whole fitting and
+// backward chain.  rev (periodic path): computes the reverse slot of every
+// edge, which is the in-edge array of the symmetric graph (in_edge == rev).
+// `second` is the fitting net (FUSE_FIT) or message layer 0 (otherwise).
 // ---------------------------------------------------------------------------
 template <typename T, bool FUSE_FIT>
-__global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                   int* __restrict__ rev, MdFuse mf) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ AtomSmem<T> sms[kG];
-    __shared__ T s_b[kG][kEdgePass][kK + 1];
-    __shared__ int s_ty[kG][kEdgePass];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
-    DevMlp<T> fit{}, msg0{};
-    if constexpr (FUSE_FIT)
-        fit = sg.mlp(md.fit, kInFit, 1);
-    else
-        msg0 = sg.mlp(md.msg[0], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
+__device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const DevMlp<T>& second,
+                           const DevGraph& gr, const DevWork<T>& ws, int* __restrict__ rev,
+                           const MdFuse& mf, AtomSmem<T>* sms, const Grp& G) {
     // this step's neighbour search is complete: clear the cell counts for the
-    // binning fused into the force kernel (device MD) / keep the zero invariant
+    // binning fused into the force phase (device MD) / keep the zero invariant
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
          c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
-    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
+    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
     AtomSmem<T>& sm = sms[g];
+    T(*s_b)[kK + 1] = reinterpret_cast<T(*)[kK + 1]>(&sm.ed[0][0][0]);  // [64][9] alias
+    int* s_ty = &sm.emir[0][0];                                          // [64] alias
     const int nd = md.n_types * kK;
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
+    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         T desc = T(0);  // thread q < nd accumulates descriptor component q
         for (int base = 0; base < cnt; base += kEdgePass) {
@@ -208,8 +246,8 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
                 st4(ws.edb + 8ll * e, db[0], db[1], db[2], db[3]);
                 st4(ws.edb + 8ll * e + 4, db[4], db[5], db[6], db[7]);
 #pragma unroll
-                for (int k = 0; k < kK; ++k) s_b[g][t][k] = b[k];
-                s_ty[g][t] = gr.ety[e];
+                for (int k = 0; k < kK; ++k) s_b[t][k] = b[k];
+                s_ty[t] = gr.ety[e];
             }
             if (rev && w < 2) {
                 // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Lane l of the
@@ -254,7 +292,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
             gsync(g);
             if (t < nd) {  // descriptor: CSR edge order, as inference.cpp:228-238
                 const int ty = t >> 3, k = t & 7;
-                for (int r = 0; r < m; ++r) desc += (s_ty[g][r] == ty) ? s_b[g][r][k] : T(0);
+                for (int r = 0; r < m; ++r) desc += (s_ty[r] == ty) ? s_b[r][k] : T(0);
             }
             gsync(g);
         }
@@ -278,7 +316,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
         gsync(g);
         if constexpr (FUSE_FIT) {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            fit_fwd_bwd(fit, sm.v2, sm.v3, sm.v0, sm.v3, owned, ws.e_atom + i, sm.s4, t, g);
+            fit_fwd_bwd(second, sm.v2, sm.v3, sm.v0, sm.v3, owned, ws.e_atom + i, sm.s4, t, g);
             // embedding backward: linear layer 2 (W2^T), tanh layer 1 (W1^T, padded)
             const T dz1 = bmv<T, 32, 32>(emb.W2T, 32, sm.v3, t) * (T(1) - z1 * z1);
             if (lead) sm.v0[o] = dz1;
@@ -303,7 +341,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
             }
         } else {
             // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
-            const T p = bmv<T, 32, 32>(msg0.W1, kInMsg, sm.v2, t);
+            const T p = bmv<T, 32, 32>(second.W1, kInMsg, sm.v2, t);
             if (lead) {
                 sm.v3[o] = p;
                 if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
@@ -316,11 +354,11 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed(DevModel<T> md, DevGra
 }
 
 // ---------------------------------------------------------------------------
-// Message-layer backward body for atom i, given dE/dh^{l+1}_i in sm.v0 and the
+// Message-layer backward for atom i, given dE/dh^{l+1}_i in sm.v0 and the
 // update hidden activations in sm.v2.  Pushes dz_e to e's mirror slot.
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void msg_backward_body(const DevMlp<T>& msg, const DevMlp<T>& upd,
+__device__ __forceinline__ void msg_backward_atom(const DevMlp<T>& msg, const DevMlp<T>& upd,
                                                   const DevGraph& gr, const DevWork<T>& ws,
                                                   AtomSmem<T>& sm, int l, int i, bool first_g,
                                                   int t, int g) {
@@ -350,59 +388,82 @@ __device__ __forceinline__ void msg_backward_body(const DevMlp<T>& msg, const De
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
     const T vl = sm.v2[lane];
-    const T* __restrict__ Z = ws.z + l * S * kH;
+    const T* Z = ws.z + l * S * kH;
     T* __restrict__ D = ws.d + (l & 1) * S * kH;
     const int start = gr.row_start[i], cnt = gr.nnei[i];
     for (int base = 0; base < cnt; base += kEdgePass) {
-        // warp w owns edges base + w + 4u; lane u prefetches edge u's scalars
+        // warp w owns edges base + w + 4u, taken 8 at a time
         const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
-        const long long el = start + base + w + 4 * (lane < mw ? lane : 0);
-        const T s_l = ws.es[el], ds_l = ws.eds[el];
-        const int mir_l = gr.inv_pos[el];
-        const V4<T> d0_l = ld4(ws.edb + 8 * el), d1_l = ld4(ws.edb + 8 * el + 4);
-        T zr[kPW];
+        for (int u0 = 0; u0 < mw; u0 += 8) {
+            const int mu = min(8, mw - u0);
+            const long long e0 = start + base + w + 4 * u0;  // edge of u = 0
+            // lane u stages edge u's scalars (one memory round trip for the batch);
+            // the edge loop then reads them as shared-memory broadcasts
+            if (lane < mu) {
+                const long long e = e0 + 4 * lane;
+                T* row = sm.ed[w][lane];
+                row[0] = ws.es[e];
+                row[1] = ws.eds[e];
+                const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+                st4(row + 4, d0.x, d0.y, d0.z, d0.w);
+                st4(row + 8, d1.x, d1.y, d1.z, d1.w);
+                sm.emir[w][lane] = gr.inv_pos[e];
+            }
+            const T* zrow = Z + e0 * kH + lane;
+            T zr[8];
 #pragma unroll
-        for (int u = 0; u < kPW; ++u)
-            if (u < mw) zr[u] = Z[(start + base + w + 4 * u) * static_cast<long long>(kH) + lane];
-        T tot_l = T(0);
+            for (int u = 0; u < 8; ++u)
+                if (u < mu) zr[u] = zrow[4 * u * kH];
+            __syncwarp();
+            T term[8];
 #pragma unroll
-        for (int u = 0; u < kPW; ++u) {
-            if (u >= mw) break;
-            const T z = zr[u];
-            const T s = __shfl_sync(FULL_MASK, s_l, u), ds = __shfl_sync(FULL_MASK, ds_l, u);
-            const long long mir = __shfl_sync(FULL_MASK, mir_l, u);
-            T wv = w1b[0] * __shfl_sync(FULL_MASK, d0_l.x, u);
-            wv += w1b[1] * __shfl_sync(FULL_MASK, d0_l.y, u);
-            wv += w1b[2] * __shfl_sync(FULL_MASK, d0_l.z, u);
-            wv += w1b[3] * __shfl_sync(FULL_MASK, d0_l.w, u);
-            wv += w1b[4] * __shfl_sync(FULL_MASK, d1_l.x, u);
-            wv += w1b[5] * __shfl_sync(FULL_MASK, d1_l.y, u);
-            wv += w1b[6] * __shfl_sync(FULL_MASK, d1_l.z, u);
-            wv += w1b[7] * __shfl_sync(FULL_MASK, d1_l.w, u);
-            const T d = s * vl * (T(1) - z * z);
-            D[mir * kH + lane] = d;
-            const T tot = warp_sum(ds * vl * z + d * wv);
-            if (lane == u) tot_l = tot;
+            for (int u = 0; u < 8; ++u) {
+                term[u] = T(0);
+                if (u < mu) {
+                    const T* row = sm.ed[w][u];
+                    const T s = row[0], ds = row[1];
+                    const V4<T> d0 = ld4c(row + 4), d1 = ld4c(row + 8);
+                    T wv = w1b[0] * d0.x;
+                    wv += w1b[1] * d0.y;
+                    wv += w1b[2] * d0.z;
+                    wv += w1b[3] * d0.w;
+                    wv += w1b[4] * d1.x;
+                    wv += w1b[5] * d1.y;
+                    wv += w1b[6] * d1.z;
+                    wv += w1b[7] * d1.w;
+                    const T z = zr[u];
+                    const T d = s * vl * (T(1) - z * z);
+                    D[static_cast<long long>(sm.emir[w][u]) * kH + lane] = d;
+                    term[u] = ds * vl * z + d * wv;
+                }
+            }
+            // reduce-scatter butterfly: 8 edge sums in 9 shuffles; lane 4u holds edge u
+            const T tot = reduce8(term, lane);
+            if ((lane & 3) == 0 && (lane >> 2) < mu) {
+                const long long e = e0 + 4 * (lane >> 2);
+                ws.g[e] = (first_g ? T(0) : ws.g[e]) + (tot + sm.ed[w][lane >> 2][1] * c0);
+            }
+            __syncwarp();
         }
-        if (lane < mw) ws.g[el] = (first_g ? T(0) : ws.g[el]) + (tot_l + ds_l * c0);
     }
 }
 
-// S_i = sum over i's mirror slots of the pushed dz (layer l) -> sm.v1;
-// contiguous rows, split over the 4 warps, fixed summation order.
+// S_i = sum over i's mirror slots of the pushed dz (layer l) (+ remote partials
+// in domain decomposition) -> sm.v1; contiguous rows, fixed summation order.
 template <typename T>
 __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& ws,
                                           AtomSmem<T>& sm, int l, int i, int t, int g) {
     const int lane = t & 31, w = t >> 5;
-    const T* __restrict__ D = ws.d + (l & 1) * ws.slots * kH;
+    const T* D = ws.d + (l & 1) * ws.slots * kH;
     const int is = gr.in_start[i], ic = gr.in_cnt[i];
     T acc = T(0);
     for (int base = 0; base < ic; base += kEdgePass) {
         const int mw = max(0, (min(kEdgePass, ic - base) - w + 3) / 4);
+        const T* drow = D + static_cast<long long>(is + base + w) * kH + lane;
         T dr_[kPW];
 #pragma unroll
         for (int u = 0; u < kPW; ++u)
-            if (u < mw) dr_[u] = D[(is + base + w + 4 * u) * static_cast<long long>(kH) + lane];
+            if (u < mw) dr_[u] = drow[4 * u * kH];
 #pragma unroll
         for (int u = 0; u < kPW; ++u)
             if (u < mw) acc += dr_[u];
@@ -420,29 +481,18 @@ __device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& 
 
 // ---------------------------------------------------------------------------
 // Message layer l forward; LAST fuses the fitting net and the top layer's
-// backward (all atom-local).
+// backward (all atom-local).  `third` is message layer l+1 (for P^{l+1}) or the
+// fitting net (LAST).
 // ---------------------------------------------------------------------------
 template <typename T, bool LAST>
-__global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                     int l) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ AtomSmem<T> sms[kG];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
-    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
-    DevMlp<T> nxt{}, fit{};
-    if constexpr (LAST)
-        fit = sg.mlp(md.fit, kInFit, 1);
-    else
-        nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
+__device__ void msg_fwd_body(const DevMlp<T>& msg, const DevMlp<T>& upd, const DevMlp<T>& third,
+                             const DevGraph& gr, const DevWork<T>& ws, int l, AtomSmem<T>* sms,
+                             const Grp& G) {
+    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
     AtomSmem<T>& sm = sms[g];
     const int n = gr.n;
     const long long S = ws.slots;
-    const T* __restrict__ Pin = ws.pe + (l & 1) * S * kH;
+    const T* Pin = ws.pe + (l & 1) * S * kH;
     T* __restrict__ Z = ws.z + l * S * kH;
     T w1b[kK];
 #pragma unroll
@@ -450,38 +500,51 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevG
     const T b1 = msg.b1[lane];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
+    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         if (t < 32) sm.v1[t] = ws.h[(static_cast<long long>(l) * n + i) * kH + t];  // h_i
         T acc = T(0), ssum = T(0);
         for (int base = 0; base < cnt; base += kEdgePass) {
             const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
-            const long long el = start + base + w + 4 * (lane < mw ? lane : 0);
-            const T s_l = ws.es[el];
-            const V4<T> b0_l = ld4(ws.eb + 8 * el), b1_l = ld4(ws.eb + 8 * el + 4);
+            const long long e0 = start + base + w;
+            // lane u stages edge u's scalars (one memory round trip for the pass);
+            // the edge loop reads them as shared-memory broadcasts
+            if (lane < mw) {
+                const long long e = e0 + 4 * lane;
+                T* row = sm.ed[w][lane];
+                row[0] = ws.es[e];
+                const V4<T> b0 = ld4c(ws.eb + 8 * e), bb = ld4c(ws.eb + 8 * e + 4);
+                st4(row + 4, b0.x, b0.y, b0.z, b0.w);
+                st4(row + 8, bb.x, bb.y, bb.z, bb.w);
+            }
+            const T* prow = Pin + e0 * kH + lane;
             T pr[kPW];
 #pragma unroll
             for (int u = 0; u < kPW; ++u)
-                if (u < mw) pr[u] = Pin[(start + base + w + 4 * u) * static_cast<long long>(kH) + lane];
+                if (u < mw) pr[u] = prow[4 * u * kH];
+            __syncwarp();
 #pragma unroll
             for (int u = 0; u < kPW; ++u) {
                 if (u >= mw) break;
-                const long long e = start + base + w + 4 * u;
-                const T s = __shfl_sync(FULL_MASK, s_l, u);
+                const long long e = e0 + 4 * u;
+                const T* row = sm.ed[w][u];
+                const T s = row[0];
+                const V4<T> b0 = ld4c(row + 4), bb = ld4c(row + 8);
                 T a = b1;
-                a += w1b[0] * __shfl_sync(FULL_MASK, b0_l.x, u);
-                a += w1b[1] * __shfl_sync(FULL_MASK, b0_l.y, u);
-                a += w1b[2] * __shfl_sync(FULL_MASK, b0_l.z, u);
-                a += w1b[3] * __shfl_sync(FULL_MASK, b0_l.w, u);
-                a += w1b[4] * __shfl_sync(FULL_MASK, b1_l.x, u);
-                a += w1b[5] * __shfl_sync(FULL_MASK, b1_l.y, u);
-                a += w1b[6] * __shfl_sync(FULL_MASK, b1_l.z, u);
-                a += w1b[7] * __shfl_sync(FULL_MASK, b1_l.w, u);
+                a += w1b[0] * b0.x;
+                a += w1b[1] * b0.y;
+                a += w1b[2] * b0.z;
+                a += w1b[3] * b0.w;
+                a += w1b[4] * bb.x;
+                a += w1b[5] * bb.y;
+                a += w1b[6] * bb.z;
+                a += w1b[7] * bb.w;
                 const T z = d_tanh(a + pr[u]);
                 Z[e * kH + lane] = z;
                 acc += s * z;
                 ssum += s;
             }
+            __syncwarp();
         }
         sm.part[w][lane] = acc;
         if (lane == 0) sm.sc[w] = ssum;
@@ -507,7 +570,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevG
         }
         gsync(g);
         if constexpr (!LAST) {
-            const T p = bmv<T, 32, 32>(nxt.W1, kInMsg, sm.v3, t);
+            const T p = bmv<T, 32, 32>(third.W1, kInMsg, sm.v3, t);
             if (lead) {
                 sm.v0[o] = p;
                 if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
@@ -517,31 +580,24 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_fwd(DevModel<T> md, DevG
         } else {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
             // fitting: h^M in v3 -> dE/dh^M in v0 (v1 scratch for the fit hidden layer)
-            fit_fwd_bwd(fit, sm.v3, sm.v1, sm.v0, sm.v0, owned, ws.e_atom + i, sm.s4, t, g);
-            msg_backward_body(msg, upd, gr, ws, sm, l, i, true, t, g);
+            fit_fwd_bwd(third, sm.v3, sm.v1, sm.v0, sm.v0, owned, ws.e_atom + i, sm.s4, t, g);
+            msg_backward_atom(msg, upd, gr, ws, sm, l, i, true, t, g);
         }
         gsync(g);
     }
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
+// `nxt` is message layer l+1 (its W1h^T maps the gathered adjoints).
 template <typename T>
-__global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                     int l) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ AtomSmem<T> sms[kG];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
-    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
-    const DevMlp<T> nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
+__device__ void msg_bwd_body(const DevMlp<T>& msg, const DevMlp<T>& upd, const DevMlp<T>& nxt,
+                             const DevGraph& gr, const DevWork<T>& ws, int l, AtomSmem<T>* sms,
+                             const Grp& G) {
+    const int g = G.g, t = G.t;
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
+    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
         const T own = ws.dhown[static_cast<long long>(i) * kH + o];
         const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + o];
         gather_in(gr, ws, sm, l + 1, i, t, g);
@@ -552,27 +608,20 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_msg_bwd(DevModel<T> md, DevG
             sm.v2[o] = zu;
         }
         gsync(g);
-        msg_backward_body(msg, upd, gr, ws, sm, l, i, false, t, g);
+        msg_backward_atom(msg, upd, gr, ws, sm, l, i, false, t, g);
         gsync(g);
     }
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T>
-__global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ AtomSmem<T> sms[kG];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
-    const DevMlp<T> msg0 = sg.mlp(md.msg[0], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT;
+__device__ void embed_bwd_body(const DevMlp<T>& emb, const DevMlp<T>& msg0, const DevGraph& gr,
+                               const DevWork<T>& ws, AtomSmem<T>* sms, const Grp& G) {
+    const int g = G.g, t = G.t;
     AtomSmem<T>& sm = sms[g];
     const int o = bmv_out<32>(t);
     const bool lead = bmv_lead<32>(t);
-    for (int i = blockIdx.x * kG + g; i < gr.n_active; i += gridDim.x * kG) {
+    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
         const T own = ws.dhown[static_cast<long long>(i) * kH + o];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + o];
         gather_in(gr, ws, sm, 0, i, t, g);
@@ -588,7 +637,7 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed_bwd(DevModel<T> md, De
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         for (int q = t; q < cnt; q += kAT) {
             const long long e = start + q;
-            const V4<T> d0 = ld4(ws.edb + 8 * e), d1 = ld4(ws.edb + 8 * e + 4);
+            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
             const T* dv = sm.v3 + gr.ety[e] * kK;
             T acc = dv[0] * d0.x;
             acc += dv[1] * d0.y;
@@ -607,27 +656,19 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_embed_bwd(DevModel<T> md, De
 }
 
 // ---------------------------------------------------------------------------
-// Forces (gather form), per-atom energy, virial, and the fused velocity-Verlet
-// tail of the device MD loop; deterministic grid reduction of E, W, W_ab.
+// Forces (gather form), per-atom energy, virial, and the velocity-Verlet tail
+// of the device MD loop; accumulates this thread's E, W, W_ab into acc[11].
 //   F_i = sum_{e in out(i)} u_e g_e - sum_{e' in in(i)} u_e' g_e'
 //       = sum_q u_q (g_q + grev_q)            (symmetric list: u_rev(e) = -u_e)
 //   W   = -sum_e g_e r_e ;  W_ab = -sum_e g_e dr_a u_b
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T> ws,
-                                                   double* __restrict__ forces,
-                                                   double* __restrict__ per_atom,
-                                                   double* __restrict__ out, MdFuse mf) {
-    __shared__ double s_f[kG][4][3];
-    __shared__ double s_part[kCTA / 32][12];
-    __shared__ bool s_last;
-    pdl_launch_dependents();
-    pdl_wait();
-    const int g = threadIdx.x / kAT, t = threadIdx.x % kAT, lane = t & 31, w = t >> 5;
-    double acc[11];
-#pragma unroll
-    for (int q = 0; q < 11; ++q) acc[q] = 0.0;
-    for (int i = blockIdx.x * kG + g; i < gr.n; i += gridDim.x * kG) {
+__device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __restrict__ forces,
+                           double* __restrict__ per_atom, const MdFuse& mf, AtomSmem<T>* sms,
+                           double (&acc)[11], const Grp& G) {
+    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
+    AtomSmem<T>& sm = sms[g];
+    for (int i = G.gid; i < gr.n; i += G.ngroups) {
         // MD state of atom i, loaded early (independent of the edge loads)
         double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0;
         if (mf.mode && t == 0) {
@@ -676,16 +717,15 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T
         fy = warp_sum(fy);
         fz = warp_sum(fz);
         if (lane == 0) {
-            s_f[g][w][0] = fx;
-            s_f[g][w][1] = fy;
-            s_f[g][w][2] = fz;
+            sm.f[w][0] = fx;
+            sm.f[w][1] = fy;
+            sm.f[w][2] = fz;
         }
         gsync(g);
         if (t == 0) {
             double f3[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a)
-                f3[a] = ((s_f[g][0][a] + s_f[g][1][a]) + s_f[g][2][a]) + s_f[g][3][a];
+            for (int a = 0; a < 3; ++a) f3[a] = ((sm.f[0][a] + sm.f[1][a]) + sm.f[2][a]) + sm.f[3][a];
             forces[3 * i] = f3[0];
             forces[3 * i + 1] = f3[1];
             forces[3 * i + 2] = f3[2];
@@ -713,10 +753,17 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T
         }
         gsync(g);
     }
-    // CTA partials (fixed order), then the last CTA reduces them in fixed order
-    const int wc = threadIdx.x >> 5;
+}
+
+// CTA partials of (E, W, W_ab) in a fixed order, then the last CTA to finish
+// reduces all CTAs' partials in a fixed order into out[0..10] (deterministic).
+template <typename T>
+__device__ void reduce_energy_virial(double (&acc)[11], const DevWork<T>& ws,
+                                     double* __restrict__ out, double (*s_part)[12], bool* s_last) {
+    const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < 11; ++q) acc[q] = warp_sum(acc[q]);
+    __syncthreads();
     if (lane == 0)
 #pragma unroll
         for (int q = 0; q < 11; ++q) s_part[wc][q] = acc[q];
@@ -728,9 +775,9 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) *s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
-    if (s_last) {
+    if (*s_last) {
         __threadfence();
         double v[11];
 #pragma unroll
@@ -750,8 +797,85 @@ __global__ __launch_bounds__(kCTA, kMinCTAs) void k_force(DevGraph gr, DevWork<T
             for (int q = 0; q < kCTA / 32; ++q) tot += s_part[q][threadIdx.x];
             out[threadIdx.x] = tot;
         }
-        if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / graph replay
+        if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / step
     }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Standalone kernels (one phase each; weights staged per launch)
+// ---------------------------------------------------------------------------
+template <typename T, bool FUSE_FIT>
+__global__ __launch_bounds__(kCTA, 1) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                   int* __restrict__ rev, MdFuse mf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
+    const DevMlp<T> second =
+        FUSE_FIT ? sg.mlp(md.fit, kInFit, 1) : sg.mlp(md.msg[0], kInMsg, kH);
+    __syncthreads();
+    pdl_wait();
+    embed_body<T, FUSE_FIT>(md, emb, second, gr, ws, rev, mf,
+                            sg.template scratch<AtomSmem<T>>(), Grp());
+}
+
+template <typename T, bool LAST>
+__global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                     int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
+    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
+    const DevMlp<T> third = LAST ? sg.mlp(md.fit, kInFit, 1) : sg.mlp(md.msg[l + 1], kInMsg, kH);
+    __syncthreads();
+    pdl_wait();
+    msg_fwd_body<T, LAST>(msg, upd, third, gr, ws, l, sg.template scratch<AtomSmem<T>>(), Grp());
+}
+
+template <typename T>
+__global__ __launch_bounds__(kCTA, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
+                                                     int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
+    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
+    const DevMlp<T> nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
+    __syncthreads();
+    pdl_wait();
+    msg_bwd_body<T>(msg, upd, nxt, gr, ws, l, sg.template scratch<AtomSmem<T>>(), Grp());
+}
+
+template <typename T>
+__global__ __launch_bounds__(kCTA, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
+    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
+    const DevMlp<T> msg0 = sg.mlp(md.msg[0], kInMsg, kH);
+    __syncthreads();
+    pdl_wait();
+    embed_bwd_body<T>(emb, msg0, gr, ws, sg.template scratch<AtomSmem<T>>(), Grp());
+}
+
+template <typename T>
+__global__ __launch_bounds__(kCTA, 1) void k_force(DevGraph gr, DevWork<T> ws,
+                                                   double* __restrict__ forces,
+                                                   double* __restrict__ per_atom,
+                                                   double* __restrict__ out, MdFuse mf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double s_part[kCTA / 32][12];
+    __shared__ bool s_last;
+    pdl_launch_dependents();
+    pdl_wait();
+    double acc[11];
+#pragma unroll
+    for (int q = 0; q < 11; ++q) acc[q] = 0.0;
+    force_body<T>(gr, ws, forces, per_atom, mf, reinterpret_cast<AtomSmem<T>*>(smem_raw), acc,
+                  Grp());
+    reduce_energy_virial<T>(acc, ws, out, s_part, &s_last);
 }
 
 // ---------------------------------------------------------------------------
@@ -789,31 +913,37 @@ static int net_grid(int n) {
     return want < 1 ? 1 : (want < cap ? want : cap);
 }
 
-// Launch with `smem_elems` T of dynamic shared memory for the staged weights
+template <typename T>
+static size_t smem_bytes(int weight_elems) {
+    return static_cast<size_t>(weight_elems) * sizeof(T) + 16 + kG * sizeof(AtomSmem<T>);
+}
+
+// Launch with the staged weights + the groups' AtomSmem in dynamic shared memory
 // (the > 48 KB opt-in is set by net_configure() when a context is created, never
 // during stream capture).
 template <typename T, typename... Params, typename... Args>
 static void launch_staged(void (*kernel)(Params...), int grid, int smem_elems, cudaStream_t st,
                           Args... args) {
-    const size_t bytes = static_cast<size_t>(smem_elems) * sizeof(T);
-    launch_pdl(kernel, dim3(grid), dim3(kCTA), bytes, st, args...);
+    launch_pdl(kernel, dim3(grid), dim3(kCTA), smem_bytes<T>(smem_elems), st, args...);
 }
+
+constexpr int kMaxSmem = 224 * 1024;
 
 template <typename T>
 static cudaError_t configure_t() {
-    const int bytes = 160 * 1024;
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, true>, a, bytes),
-                          cudaFuncSetAttribute(k_embed<T, false>, a, bytes),
-                          cudaFuncSetAttribute(k_msg_fwd<T, true>, a, bytes),
-                          cudaFuncSetAttribute(k_msg_fwd<T, false>, a, bytes),
-                          cudaFuncSetAttribute(k_msg_bwd<T>, a, bytes),
-                          cudaFuncSetAttribute(k_embed_bwd<T>, a, bytes)})
+    for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, true>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_embed<T, false>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_msg_fwd<T, true>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_msg_fwd<T, false>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_msg_bwd<T>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_embed_bwd<T>, a, kMaxSmem),
+                          cudaFuncSetAttribute(k_force<T>, a, kMaxSmem)})
         if (r != cudaSuccess) e = r;
     return e;
 }
-// Per device: allow the staged-weight kernels up to 160 KB of dynamic smem.
+// Per device: allow the staged-weight kernels up to 224 KB of dynamic smem.
 cudaError_t net_configure() {
     const cudaError_t a = configure_t<float>();
     const cudaError_t b = configure_t<double>();
@@ -853,10 +983,11 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
         mk("embed_bwd", st);
         launches += 2 + M + (M - 1);
     }
-    launch_pdl(k_force<T>, dim3(nb), dim3(kCTA), 0, st, gr, ws, forces, per_atom, out, mf);
+    launch_staged<T>(k_force<T>, nb, 0, st, gr, ws, forces, per_atom, out, mf);
     mk("force", st);
     return launches + 1;
 }
+
 // One phase of a domain-decomposed evaluation (the caller exchanges halo rows
 // between phases).  Phases: 0 embed, 1 push ghost P (into parity `l`), 2 message
 // layer l forward, 3 ghost adjoint sums of layer l, 4 message layer l backward,
@@ -902,8 +1033,8 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
             launch_staged<T>(k_embed_bwd<T>, nb, e_emb + e_msg, st, md, gr, ws);
             break;
         case 6:
-            launch_pdl(k_force<T>, dim3(net_grid(gr.n)), dim3(kCTA), 0, st, gr, ws, forces,
-                       static_cast<double*>(nullptr), out, none);
+            launch_staged<T>(k_force<T>, net_grid(gr.n), 0, st, gr, ws, forces,
+                             static_cast<double*>(nullptr), out, none);
             break;
     }
 }
@@ -913,7 +1044,6 @@ template void launch_dd_phase<float>(const DevModel<float>&, const DevGraph&,
 template void launch_dd_phase<double>(const DevModel<double>&, const DevGraph&,
                                       const DevWork<double>&, int, int, double*, double*, double*,
                                       cudaStream_t);
-
 template int launch_network<float>(const DevModel<float>&, const DevGraph&, const DevWork<float>&,
                                    double*, double*, double*, int*, cudaStream_t, const Marker&,
                                    const MdFuse&);
