@@ -1,18 +1,20 @@
 // hmdp_net.cu — the DP network kernels (embedding, message layers, fitting,
 // reverse mode, forces/virial), sm_100a.
 //
-// Decomposition: a 512-thread CTA holds four independent 128-thread "atom
-// groups"; each group processes one atom at a time (grid-stride over atoms) and
-// synchronises with its own named barrier, so the groups never wait on each
-// other.  Kernels stage the MLP weights they need into shared memory (once per
-// CTA, ~1 CTA per SM), so the atom-level mat-vecs (bmv: 4-way split, xor-shuffle
-// reduction) read weights and activations from shared memory only.  Per-edge
-// work is split over the group's 4 warps (edge q -> warp q % 4) with lane =
-// channel, so every per-edge row access is one coalesced 128-byte line; the
-// per-edge scalars are staged in shared memory and read as broadcasts.
-//
-// Every phase is a per-group __device__ body (grid-stride over atoms) wrapped by
-// a thin kernel that stages the weights it needs.
+// Decomposition: ONE WARP PER ATOM, lane = feature channel.  A CTA of W warps
+// (W = 2..16, chosen from the system size so every SM gets work) stages the
+// weight matrices its phase needs into shared memory once, then its warps
+// grid-stride over atoms independently — no CTA barrier inside the atom loop,
+// only __syncwarp.  Per atom:
+//   * per-edge work runs lane = channel with edges taken 8 at a time (8 row loads
+//     in flight per lane, every row access one coalesced 128-byte line); the
+//     per-edge scalars are loaded lane = edge and staged in the warp's shared
+//     scratch, so the edge loop reads them as shared-memory broadcasts;
+//   * the atom-level MLP layers are warp mat-vecs (wmv): lane o reads row o of
+//     the staged matrix with 128-bit loads (rows padded by 16 bytes, so the 8
+//     lanes of each quarter-warp phase hit distinct banks) and x as broadcasts.
+// Many atoms are in flight per SM (up to 32 warps), which is what this
+// latency-bound workload needs (the FLOPs per step are a few hundred MFLOP).
 //
 // Dataflow is "push" into mirror slots (DevGraph, hmdp_device.cuh): the producer
 // of a per-neighbour quantity writes it into the slot its consumer reads
@@ -20,7 +22,7 @@
 //   P_j = W1h h_j        pushed by j into the out-slots of j's in-edges
 //   dz_e (h_j adjoint)   pushed by the edge's source into e's mirror slot
 //   g_e                  pushed by the edge's source into e's mirror slot
-// Every slot is written by exactly one thread and every sum runs in a fixed
+// Every slot is written by exactly one lane and every sum runs in a fixed
 // order: deterministic, no float atomics (the reference's scatters dh_j += ...,
 // F_j -= ..., inference.cpp:343, :380, become these pushes + local sums).
 //
@@ -34,112 +36,98 @@
 //             dE/dh_j += W1h^T sum_{e in in(j)} dz_e  (one mat-vec per atom).
 //
 // Reference correspondence (paths relative to /root/reference/proj):
-//   embed_body       edge radial + descriptor + embedding fwd   src/nn/inference.cpp:214-249
-//                    [FUSE_FIT: + fitting fwd/bwd + embedding bwd, :288-311, :355-370]
-//   msg_fwd_body     message layer fwd                          :251-286
-//                    [LAST: + fitting fwd/bwd + top message layer bwd, :288-353]
-//   msg_bwd_body     message layer bwd (lower layers)           :313-353
-//   embed_bwd_body   embedding + descriptor adjoint             :355-370
-//   force_body       force / virial (gather form) + E, W sums   :288-298, :372-387
-//                    [+ velocity Verlet tail, src/integrators.cpp:32-47]
+//   k_embed        edge radial + descriptor + embedding fwd   src/nn/inference.cpp:214-249
+//                  [FUSE_FIT: + fitting fwd/bwd + embedding bwd, :288-311, :355-370]
+//   k_msg_fwd      message layer fwd                          :251-286
+//                  [LAST: + fitting fwd/bwd + top message layer bwd, :288-353]
+//   k_msg_bwd      message layer bwd (lower layers)           :313-353
+//   k_embed_bwd    embedding + descriptor adjoint             :355-370
+//   k_force        force / virial (gather form) + E, W sums   :288-298, :372-387
+//                  [+ velocity Verlet tail, src/integrators.cpp:32-47]
 #include "hmdp_common.cuh"
 
 namespace hmdp {
 
 int num_sms();  // hmdp_nbr.cu
 
-constexpr int kG = 4;             // atom groups per CTA
-constexpr int kCTA = kG * kAT;    // 512 threads
-constexpr int kEdgePass = 64;     // edges per pass of a group (16 per warp)
-constexpr int kPW = kEdgePass / 4;
-
-// group-local barrier (named barrier 1 + g over the group's 128 threads)
-__device__ __forceinline__ void gsync(int g) { group_bar(g + 1); }
-
-// Sum over a group's 128 threads (every thread gets the total); fixed order.
+constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
+constexpr int kForceCTA = 256;
+// edges per unrolled batch (row loads in flight per lane; fewer for FP64 registers)
 template <typename T>
-__device__ __forceinline__ T group_sum(T v, T* s4, int g) {
-    v = warp_sum(v);
-    gsync(g);
-    if ((threadIdx.x & 31) == 0) s4[(threadIdx.x >> 5) & 3] = v;
-    gsync(g);
-    return ((s4[0] + s4[1]) + s4[2]) + s4[3];
+constexpr int kU = sizeof(T) == 4 ? 8 : 4;
+constexpr int kInMsg = kH + kK;
+
+// Staged matrices: rows padded by 16 bytes (row stride in elements).
+template <typename T>
+__host__ __device__ constexpr int pad_ld(int cols) {
+    return cols + 16 / static_cast<int>(sizeof(T));
+}
+template <typename T>
+__host__ __device__ constexpr int mat_elems(int rows, int cols) {
+    return rows * pad_ld<T>(cols);
 }
 
-// Per-group shared scratch for one atom.
+// Per-warp shared scratch.
 template <typename T>
-struct AtomSmem {
-    T v0[64], v1[64], v2[64], v3[64];  // activation vectors
-    T part[4][32];                     // per-warp partial channel sums
-    T s4[4];                           // group_sum scratch
-    T sc[4];                           // per-warp scalar partials
-    alignas(16) T ed[4][16][12];       // per-warp staged edge scalars (s, s', b or b')
-    int emir[4][16];                   // per-warp staged mirror slots
-    double f[4][3];                    // per-warp force partials
+struct WarpSmem {
+    alignas(16) T x[64];
+    alignas(16) T y[64];
+    alignas(16) T t[32];
+    alignas(16) T ed[32][12];  // staged edge scalars: (s, s', -, -, b or b'[8])
+    alignas(16) T red[2][32];  // team-sum partials (double-buffered)
+    T reds[2];
+    int emir[32];  // staged mirror slots
+    int ety[32];   // staged neighbour types
 };
 
-// ---------------------------------------------------------------------------
-// Weight staging: whole MLPs [in, 32, out] copied to shared memory.
-// ---------------------------------------------------------------------------
-__host__ __device__ constexpr int mlp_elems(int in, int out) {
-    return 32 * in + in * 32 + 32 + ((out * 32 + 3) / 4) * 4 * 2 + ((out + 3) / 4) * 4;
-}
-constexpr int kInEmbed = 32, kInFit = 32, kInMsg = kH + kK, kInUpd = 2 * kH;
-
+// Bump allocator over the dynamic shared memory: staged matrices, then the
+// warps' scratch.  Matrices are copied with cp.async (16 bytes per request, no
+// register round trip), so every request of every matrix is in flight at once;
+// wait() completes them (followed by the kernel's __syncthreads).
 template <typename T>
-struct Stager {
-    T* base;
-    int off;
-    __device__ const T* put(const T* src, int count) {
-        T* dst = base + off;
-        for (int q = threadIdx.x * 4; q < count; q += kCTA * 4) {
-            const V4<T> v = ld4(src + q);
-            st4(dst + q, v.x, v.y, v.z, v.w);
+struct Smem {
+    T* cur;
+    // rows x cols block of src (leading dimension src_ld), copied by the whole
+    // CTA into rows of stride pad_ld(cols); src rows must be 16-byte aligned
+    template <int R, int C>
+    __device__ const T* mat(const T* src, int src_ld) {
+        T* dst = cur;
+        constexpr int V = 16 / sizeof(T);  // elements per request
+        constexpr int RV = C / V;          // requests per row
+        constexpr int ld = pad_ld<T>(C);
+        static_assert(C % V == 0, "row not a multiple of 16 bytes");
+        for (int q = threadIdx.x; q < R * RV; q += blockDim.x) {
+            const int r = q / RV, v = q % RV;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + r * ld + v * V));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                         "l"(src + static_cast<long long>(r) * src_ld + v * V)
+                         : "memory");
         }
-        off += (count + 3) / 4 * 4;
+        cur += R * ld;
         return dst;
     }
-    // per-group scratch placed after the staged weights (same dynamic region)
-    template <class S>
-    __device__ S* scratch(int skip_bytes = 0) const {
-        const size_t a = (reinterpret_cast<size_t>(base + off) + 15) & ~size_t(15);
-        return reinterpret_cast<S*>(a + skip_bytes);
-    }
-    __device__ DevMlp<T> mlp(const DevMlp<T>& m, int in, int out) {
-        DevMlp<T> d;
-        d.W1 = put(m.W1, 32 * in);
-        d.W1T = put(m.W1T, in * 32);
-        d.b1 = put(m.b1, 32);
-        d.W2 = put(m.W2, (out * 32 + 3) / 4 * 4);
-        d.W2T = put(m.W2T, (32 * out + 3) / 4 * 4);
-        d.b2 = put(m.b2, (out + 3) / 4 * 4);
-        return d;
+    __device__ static void wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+    __device__ WarpSmem<T>& warp_scratch() const {
+        const size_t a = (reinterpret_cast<size_t>(cur) + 15) & ~size_t(15);
+        return reinterpret_cast<WarpSmem<T>*>(a)[threadIdx.x >> 5];
     }
 };
-// (the device weight buffer pads every array to a multiple of 32 elements, so
-// the rounded-up copies above never read past an array's allocation)
 
-// Group coordinates of this thread.
-struct Grp {
-    int g, t, gid, ngroups;
-    __device__ Grp()
-        : g(threadIdx.x / kAT),
-          t(threadIdx.x % kAT),
-          gid(blockIdx.x * kG + threadIdx.x / kAT),
-          ngroups(gridDim.x * kG) {}
-};
-
-// Push a 32-vector (smem) into the rows `dst + in_edge[in_start + k] * 32` for
-// k < in_cnt (the out-slots of i's in-edges): 4 rows per group iteration.
-template <typename T>
-__device__ __forceinline__ void push_rows(T* __restrict__ dst, const T* vec, const DevGraph& gr,
-                                          int i, int t) {
-    const int is = gr.in_start[i], ic = gr.in_cnt[i];
-    const T v = vec[t & 31];
-    for (int k = t >> 5; k < ic; k += 4) {
-        const long long slot = gr.in_edge[is + k];
-        dst[slot * kH + (t & 31)] = v;
+// Warp mat-vec: returns sum_{k<NIN} W[row][k] x[k] (W staged, padded rows; x in
+// shared memory, 16-byte aligned).  Four partial accumulators, fixed order.
+template <typename T, int NIN>
+__device__ __forceinline__ T wmv(const T* W, const T* x, int row) {
+    const T* w = W + row * pad_ld<T>(NIN);
+    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+    for (int k = 0; k < NIN; k += 4) {
+        const V4<T> wv = ld4c(w + k), xv = ld4c(x + k);
+        a0 += wv.x * xv.x;
+        a1 += wv.y * xv.y;
+        a2 += wv.z * xv.z;
+        a3 += wv.w * xv.w;
     }
+    return (a0 + a1) + (a2 + a3);
 }
 
 // Sum each of 8 per-lane values over the warp (reduce-scatter butterfly, fixed
@@ -169,29 +157,119 @@ __device__ __forceinline__ T reduce8(T (&a)[8], int lane) {
     return a[0];
 }
 
-// ---------------------------------------------------------------------------
-// Fitting net forward + backward on h_s: writes e_i for owned atoms (0 for
-// ghosts), leaves dE/dh (0 for ghosts) in dh_s.  inference.cpp:288-311.
-// ---------------------------------------------------------------------------
+// An atom "team" of G consecutive warps of a CTA processes one atom at a time
+// (grid-stride over atoms).  The atom's edges (and in-edge slots) are split
+// round-robin over the team's warps (local edge k of warp w is q = w + G k);
+// per-atom mat-vecs are computed redundantly by every warp of the team, so the
+// only team synchronisation is the fixed-order sum of the warps' edge partials.
+// G = 1 for large systems (throughput); G = 2, 4 for small ones, where the SMs
+// would otherwise hold a single warp per scheduler and the per-atom dependency
+// chain sets the step time.
+template <int G>
+struct Team {
+    int lane, w, first, stride, bar, rb;
+    __device__ Team() : rb(0) {
+        lane = threadIdx.x & 31;
+        const int warp = threadIdx.x >> 5;
+        const int tpc = (blockDim.x >> 5) / G;  // teams per CTA
+        w = warp % G;
+        first = blockIdx.x * tpc + warp / G;
+        stride = gridDim.x * tpc;
+        bar = 1 + warp / G;
+    }
+    __device__ __forceinline__ void sync() const {
+        if constexpr (G > 1)
+            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");
+        else
+            __syncwarp();
+    }
+    // Sum of v (per lane) and s (warp-uniform) over the team's warps in a fixed
+    // order; every warp gets the totals.  Double-buffered scratch: one barrier.
+    template <typename T>
+    __device__ __forceinline__ T sum(T v, T& s, WarpSmem<T>& sm) {
+        if constexpr (G == 1) {
+            return v;
+        } else {
+            sm.red[rb][lane] = v;
+            if (lane == 0) sm.reds[rb] = s;
+            sync();
+            const WarpSmem<T>* b = &sm - w;
+            T a = b[0].red[rb][lane], as = b[0].reds[rb];
+#pragma unroll
+            for (int q = 1; q < G; ++q) {
+                a += b[q].red[rb][lane];
+                as += b[q].reds[rb];
+            }
+            s = as;
+            rb ^= 1;
+            return a;
+        }
+    }
+    template <typename T>
+    __device__ __forceinline__ T sum(T v, WarpSmem<T>& sm) {
+        T dummy = T(0);
+        return sum(v, dummy, sm);
+    }
+    // number of this warp's local edges among cnt
+    __device__ __forceinline__ int local(int cnt) const { return (cnt - w + G - 1) / G; }
+};
+
+// Push the per-lane value P (channel lane) into the rows dst[in_edge[..]] of
+// i's in-edges (the out-slots whose consumer reads P_i); slots split over the team.
+template <typename T, int G>
+__device__ __forceinline__ void push_rows(T* dst, T p, const DevGraph& gr, int i,
+                                          const Team<G>& tm) {
+    const int is = gr.in_start[i] + tm.w;
+    const int ic = tm.local(gr.in_cnt[i]);
+    for (int k0 = 0; k0 < ic; k0 += 32) {
+        const int kk = min(32, ic - k0);
+        const int idx = tm.lane < kk ? gr.in_edge[is + G * (k0 + tm.lane)] : 0;
+        for (int k = 0; k < kk; ++k) {
+            const long long slot = __shfl_sync(FULL_MASK, idx, k);
+            dst[slot * kH + tm.lane] = p;
+        }
+    }
+}
+
+// Sum of the pushed adjoint rows in i's mirror slots (+ remote partials in
+// domain decomposition), lane = channel, fixed order.
+template <typename T, int G>
+__device__ __forceinline__ T gather_in(const T* D, const DevWork<T>& ws, const DevGraph& gr, int i,
+                                       Team<G>& tm, WarpSmem<T>& sm) {
+    const int ic = tm.local(gr.in_cnt[i]);
+    const T* drow = D + static_cast<long long>(gr.in_start[i] + tm.w) * kH + tm.lane;
+    T acc = T(0);
+    constexpr int B = 2 * kU<T>;  // rows in flight
+    for (int k0 = 0; k0 < ic; k0 += B) {
+        T r[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k0 + u < ic) r[u] = drow[(k0 + u) * G * kH];
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k0 + u < ic) acc += r[u];
+    }
+    acc = tm.sum(acc, sm);
+    // domain decomposition: partial sums pushed to ghost copies of i on other ranks
+    if (ws.s_remote) acc += ws.s_remote[static_cast<long long>(i) * kH + tm.lane];
+    return acc;
+}
+
+// Fitting net forward + backward on h (shared, channel-indexed): writes e_i for
+// owned atoms (0 for ghosts; e_out may be null), returns dE/dh[lane] (0 for
+// ghosts).  inference.cpp:288-311.  tmp: 32 elements of shared scratch.
 template <typename T>
-__device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, T* z_s, T* dz_s,
-                                            T* dh_s, bool owned, double* e_out, T* s4, int t,
-                                            int g) {
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
-    const T zf = d_tanh(bmv<T, 32, 32>(fit.W1, 32, h_s, t) + fit.b1[o]);
-    if (lead) z_s[o] = zf;
-    gsync(g);
+__device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2, T fb2,
+                                      const T* h_s, T* tmp, bool owned, double* e_out, int lane) {
+    const T zf = d_tanh(wmv<T, 32>(fW1, h_s, lane) + fb1);
     // linear head 32 -> 1 and its adjoint (dout = 1)
-    const T ez = (t < 32) ? fit.W2[t] * z_s[t] : T(0);
-    const T e = group_sum(ez, s4, g) + fit.b2[0];
-    if (t == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
-    if (t < 32) dz_s[t] = (fit.W2[t] * T(1)) * (T(1) - z_s[t] * z_s[t]);
-    gsync(g);
-    const T dh = bmv<T, 32, 32>(fit.W1T, 32, dz_s, t);
-    gsync(g);  // dh_s may alias dz_s
-    if (lead) dh_s[o] = owned ? dh : T(0);
-    gsync(g);
+    const T e = warp_sum(fw2 * zf) + fb2;
+    if (e_out && lane == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
+    tmp[lane] = (fw2 * T(1)) * (T(1) - zf * zf);
+    __syncwarp();
+    const T dh = wmv<T, 32>(fW1T, tmp, lane);
+    __syncwarp();
+    return owned ? dh : T(0);
 }
 
 // ---------------------------------------------------------------------------
@@ -199,32 +277,51 @@ __device__ __forceinline__ void fit_fwd_bwd(const DevMlp<T>& fit, const T* h_s, 
 // neighbour projection) or, for depth 1 (FUSE_FIT), runs the whole fitting and
 // backward chain.  rev (periodic path): computes the reverse slot of every
 // edge, which is the in-edge array of the symmetric graph (in_edge == rev).
-// `second` is the fitting net (FUSE_FIT) or message layer 0 (otherwise).
 // ---------------------------------------------------------------------------
-template <typename T, bool FUSE_FIT>
-__device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const DevMlp<T>& second,
-                           const DevGraph& gr, const DevWork<T>& ws, int* __restrict__ rev,
-                           const MdFuse& mf, AtomSmem<T>* sms, const Grp& G) {
+template <typename T, int G, bool FUSE_FIT>
+__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed(DevModel<T> md, DevGraph gr,
+                                                             DevWork<T> ws, int* __restrict__ rev,
+                                                             MdFuse mf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
+    const T* eW1 = sg.template mat<32, 32>(md.embed.W1, 32);
+    const T* eW2 = sg.template mat<32, 32>(md.embed.W2, 32);
+    const T *W1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *eW2T = nullptr, *eW1T = nullptr;
+    if constexpr (FUSE_FIT) {
+        fW1 = sg.template mat<32, 32>(md.fit.W1, 32);
+        fW1T = sg.template mat<32, 32>(md.fit.W1T, 32);
+        eW2T = sg.template mat<32, 32>(md.embed.W2T, 32);
+        eW1T = sg.template mat<32, 32>(md.embed.W1T, 32);
+    } else {
+        W1h = sg.template mat<32, 32>(md.msg[0].W1, kInMsg);
+    }
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    const bool lead = tm.w == 0;
+    const T eb1 = md.embed.b1[lane], eb2 = md.embed.b2[lane];
+    const T fb1 = FUSE_FIT ? md.fit.b1[lane] : T(0), fw2 = FUSE_FIT ? md.fit.W2[lane] : T(0);
+    const T fb2 = FUSE_FIT ? md.fit.b2[0] : T(0);
+    const int nd = md.n_types * kK;
+    sg.wait();
+    __syncthreads();
+    pdl_wait();
     // this step's neighbour search is complete: clear the cell counts for the
-    // binning fused into the force phase (device MD) / keep the zero invariant
+    // binning fused into the force kernel (device MD) / keep the zero invariant
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
          c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
-    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
-    AtomSmem<T>& sm = sms[g];
-    T(*s_b)[kK + 1] = reinterpret_cast<T(*)[kK + 1]>(&sm.ed[0][0][0]);  // [64][9] alias
-    int* s_ty = &sm.emir[0][0];                                          // [64] alias
-    const int nd = md.n_types * kK;
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
-    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
-        const int start = gr.row_start[i], cnt = gr.nnei[i];
-        T desc = T(0);  // thread q < nd accumulates descriptor component q
-        for (int base = 0; base < cnt; base += kEdgePass) {
-            const int m = min(kEdgePass, cnt - base);
-            const int e = start + base + t;
+    T(*sb)[12] = sm.ed;
+    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        const int start = gr.row_start[i] + tm.w, cnt = gr.nnei[i];
+        const int mloc = tm.local(cnt);
+        T desc = T(0);  // lane q < nd accumulates descriptor component q
+        for (int base = 0; base < mloc; base += 32) {
+            const int m = min(32, mloc - base);
+            const int e = start + G * (base + lane);
             int j = 0;
-            if (t < m) {
+            if (lane < m) {
                 if (rev) j = gr.nbr[e];
                 T x, y, z;
                 const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
@@ -245,25 +342,24 @@ __device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const De
                 st4(ws.eb + 8ll * e + 4, b[4], b[5], b[6], b[7]);
                 st4(ws.edb + 8ll * e, db[0], db[1], db[2], db[3]);
                 st4(ws.edb + 8ll * e + 4, db[4], db[5], db[6], db[7]);
-#pragma unroll
-                for (int k = 0; k < kK; ++k) s_b[t][k] = b[k];
-                s_ty[t] = gr.ety[e];
+                st4(&sb[lane][4], b[0], b[1], b[2], b[3]);
+                st4(&sb[lane][8], b[4], b[5], b[6], b[7]);
+                sm.ety[lane] = gr.ety[e];
             }
-            if (rev && w < 2) {
-                // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Lane l of the
-                // warp owning edges [32w, 32w+32) reads entry l of each neighbour's
-                // list (one memory latency per 8 edges); a ballot finds i.
-                const int mw = min(32, max(0, m - 32 * w));
-                const int rs_l = t < m ? gr.row_start[j] : 0;
-                const int nn_l = t < m ? gr.nnei[j] : 0;
+            if (rev) {
+                // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Lane l reads
+                // entry l of each neighbour's list (one memory latency per 8 edges);
+                // a ballot finds i.
+                const int rs_l = lane < m ? gr.row_start[j] : 0;
+                const int nn_l = lane < m ? gr.nnei[j] : 0;
                 int found = -1;
-                for (int q0 = 0; q0 < mw; q0 += 8) {
+                for (int q0 = 0; q0 < m; q0 += 8) {
                     int val[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int rsq = __shfl_sync(FULL_MASK, rs_l, q0 + u);
                         const int nnq = __shfl_sync(FULL_MASK, nn_l, q0 + u);
-                        val[u] = (q0 + u < mw && lane < nnq) ? gr.nbr[rsq + lane] : -1;
+                        val[u] = (q0 + u < m && lane < nnq) ? gr.nbr[rsq + lane] : -1;
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
@@ -271,7 +367,7 @@ __device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const De
                         if (lane == q0 + u && bal) found = rs_l + __ffs(bal) - 1;
                     }
                 }
-                if (t < m) {
+                if (lane < m) {
                     if (found < 0 && nn_l > 32) {
                         int lo = rs_l, hi = rs_l + nn_l - 1;
                         while (lo <= hi) {
@@ -289,45 +385,43 @@ __device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const De
                     if (found < 0) atomicOr(ws.err, kErrAsymmetric);
                 }
             }
-            gsync(g);
-            if (t < nd) {  // descriptor: CSR edge order, as inference.cpp:228-238
-                const int ty = t >> 3, k = t & 7;
-                for (int r = 0; r < m; ++r) desc += (s_ty[r] == ty) ? s_b[r][k] : T(0);
+            __syncwarp();
+            if (lane < nd) {  // descriptor: edge order within the warp, as inference.cpp:228-238
+                const int ty = lane >> 3, k = lane & 7;
+                for (int r = 0; r < m; ++r) desc += (sm.ety[r] == ty) ? sb[r][4 + k] : T(0);
             }
-            gsync(g);
+            __syncwarp();
         }
-        if (t < 32) {
-            sm.v0[t] = t < nd ? desc : T(0);
-            if (t < nd) ws.desc[static_cast<long long>(i) * 32 + t] = desc;
-        }
-        gsync(g);
+        desc = tm.sum(desc, sm);
+        sm.x[lane] = lane < nd ? desc : T(0);
+        if (lead && lane < nd) ws.desc[static_cast<long long>(i) * 32 + lane] = desc;
+        __syncwarp();
         // embedding forward nd (zero-padded to 32) -> 32 (tanh) -> 32
-        const T z1 = d_tanh(bmv<T, 32, 32>(emb.W1, 32, sm.v0, t) + emb.b1[o]);
-        if (lead) {
-            sm.v1[o] = z1;
-            ws.ez1[static_cast<long long>(i) * kH + o] = z1;
-        }
-        gsync(g);
-        const T h0 = bmv<T, 32, 32>(emb.W2, 32, sm.v1, t) + emb.b2[o];
-        if (lead) {
-            sm.v2[o] = h0;
-            ws.h[static_cast<long long>(i) * kH + o] = h0;
-        }
-        gsync(g);
+        const T z1 = d_tanh(wmv<T, 32>(eW1, sm.x, lane) + eb1);
+        if (lead) ws.ez1[static_cast<long long>(i) * kH + lane] = z1;
+        sm.y[lane] = z1;
+        __syncwarp();
+        const T h0 = wmv<T, 32>(eW2, sm.y, lane) + eb2;
+        if (lead) ws.h[static_cast<long long>(i) * kH + lane] = h0;
+        sm.x[lane] = h0;
+        __syncwarp();
         if constexpr (FUSE_FIT) {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            fit_fwd_bwd(second, sm.v2, sm.v3, sm.v0, sm.v3, owned, ws.e_atom + i, sm.s4, t, g);
+            const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.x, sm.t, owned,
+                                  lead ? ws.e_atom + i : nullptr, lane);
+            sm.y[lane] = dh;
+            __syncwarp();
             // embedding backward: linear layer 2 (W2^T), tanh layer 1 (W1^T, padded)
-            const T dz1 = bmv<T, 32, 32>(emb.W2T, 32, sm.v3, t) * (T(1) - z1 * z1);
-            if (lead) sm.v0[o] = dz1;
-            gsync(g);
-            const T dd = bmv<T, 32, 32>(emb.W1T, 32, sm.v0, t);
-            if (lead) sm.v1[o] = dd;
-            gsync(g);
-            for (int q = t; q < cnt; q += kAT) {
-                const long long e = start + q;
+            const T dz1 = wmv<T, 32>(eW2T, sm.y, lane) * (T(1) - z1 * z1);
+            sm.t[lane] = dz1;
+            __syncwarp();
+            const T dd = wmv<T, 32>(eW1T, sm.t, lane);
+            sm.x[lane] = dd;
+            __syncwarp();
+            for (int q = lane; q < mloc; q += 32) {
+                const long long e = start + G * q;
                 const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-                const T* dv = sm.v1 + gr.ety[e] * kK;
+                const T* dv = sm.x + gr.ety[e] * kK;
                 T acc = dv[0] * d0.x;
                 acc += dv[1] * d0.y;
                 acc += dv[2] * d0.z;
@@ -341,86 +435,79 @@ __device__ void embed_body(const DevModel<T>& md, const DevMlp<T>& emb, const De
             }
         } else {
             // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
-            const T p = bmv<T, 32, 32>(second.W1, kInMsg, sm.v2, t);
-            if (lead) {
-                sm.v3[o] = p;
-                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
-            }
-            gsync(g);
-            push_rows(ws.pe, sm.v3, gr, i, t);
+            const T p = wmv<T, 32>(W1h, sm.x, lane);
+            if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
+            push_rows(ws.pe, p, gr, i, tm);
         }
-        gsync(g);
+        __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
-// Message-layer backward for atom i, given dE/dh^{l+1}_i in sm.v0 and the
-// update hidden activations in sm.v2.  Pushes dz_e to e's mirror slot.
+// Message-layer backward for atom i, given dE/dh^{l+1}_i (dh, lane = channel)
+// and the update hidden activation zu.  Pushes dz_e to e's mirror slot and
+// accumulates dE/dr_e into g (this warp's share of the edges).
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void msg_backward_atom(const DevMlp<T>& msg, const DevMlp<T>& upd,
-                                                  const DevGraph& gr, const DevWork<T>& ws,
-                                                  AtomSmem<T>& sm, int l, int i, bool first_g,
-                                                  int t, int g) {
-    const int lane = t & 31, w = t >> 5;
+template <typename T, int G>
+__device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, const T* mW2T,
+                                                  T mb2, const T (&w1b)[kK], const DevGraph& gr,
+                                                  const DevWork<T>& ws, WarpSmem<T>& sm, int l,
+                                                  int i, T dh, T zu, bool first_g,
+                                                  const Team<G>& tm) {
+    const int lane = tm.lane;
     const long long S = ws.slots;
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
     // update MLP backward (64 -> 32 tanh -> 32)
-    const T zu = sm.v2[o];
-    const T dz = bmv<T, 32, 32>(upd.W2T, 32, sm.v0, t) * (T(1) - zu * zu);
-    if (lead) sm.v3[o] = dz;
-    gsync(g);
-    const T din = bmv<T, 64, 32>(upd.W1T, 32, sm.v3, t);  // 64 outputs, 2 parts each
-    if (bmv_lead<64>(t)) {
-        const int k = bmv_out<64>(t);
-        if (k < kH)
-            ws.dhown[static_cast<long long>(i) * kH + k] = sm.v0[k] + din;  // residual + update
-        else
-            sm.v1[k - kH] = din;  // dmsum
-    }
-    gsync(g);
-    const T v = bmv<T, 32, 32>(msg.W2T, 32, sm.v1, t);  // v = W2^T dmsum
-    if (lead) sm.v2[o] = v;
-    const T c0 = group_sum(t < 32 ? sm.v1[t] * msg.b2[t] : T(0), sm.s4, g);
-    // (group_sum's barriers also publish sm.v2)
-    T w1b[kK];
-#pragma unroll
-    for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
-    const T vl = sm.v2[lane];
+    sm.t[lane] = dh;
+    __syncwarp();
+    const T dz = wmv<T, 32>(uW2T, sm.t, lane) * (T(1) - zu * zu);
+    sm.y[lane] = dz;
+    __syncwarp();
+    const T din_h = wmv<T, 32>(uW1T, sm.y, lane);       // input rows 0..31: h
+    const T dmsum = wmv<T, 32>(uW1T, sm.y, lane + 32);  // input rows 32..63: msum
+    if (tm.w == 0)
+        ws.dhown[static_cast<long long>(i) * kH + lane] = dh + din_h;  // residual + update
+    sm.x[lane] = dmsum;
+    __syncwarp();
+    const T v = wmv<T, 32>(mW2T, sm.x, lane);  // v = W2^T dmsum
+    const T c0 = warp_sum(dmsum * mb2);
     const T* Z = ws.z + l * S * kH;
-    T* __restrict__ D = ws.d + (l & 1) * S * kH;
-    const int start = gr.row_start[i], cnt = gr.nnei[i];
-    for (int base = 0; base < cnt; base += kEdgePass) {
-        // warp w owns edges base + w + 4u, taken 8 at a time
-        const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
-        for (int u0 = 0; u0 < mw; u0 += 8) {
-            const int mu = min(8, mw - u0);
-            const long long e0 = start + base + w + 4 * u0;  // edge of u = 0
-            // lane u stages edge u's scalars (one memory round trip for the batch);
-            // the edge loop then reads them as shared-memory broadcasts
-            if (lane < mu) {
-                const long long e = e0 + 4 * lane;
-                T* row = sm.ed[w][lane];
-                row[0] = ws.es[e];
-                row[1] = ws.eds[e];
-                const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-                st4(row + 4, d0.x, d0.y, d0.z, d0.w);
-                st4(row + 8, d1.x, d1.y, d1.z, d1.w);
-                sm.emir[w][lane] = gr.inv_pos[e];
-            }
-            const T* zrow = Z + e0 * kH + lane;
-            T zr[8];
+    T* D = ws.d + (l & 1) * S * kH;
+    const int start = gr.row_start[i] + tm.w;
+    const int mloc = tm.local(gr.nnei[i]);
+    for (int base = 0; base < mloc; base += 32) {
+        const int m = min(32, mloc - base);
+        const long long e0 = start + static_cast<long long>(G) * base;  // local edge k: e0 + G k
+        const T* zrow = Z + e0 * kH + lane;
+        // the first batch of z rows is in flight during the scalar staging;
+        // each batch's compute overlaps the next batch's loads
+        T zr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (u < m) zr[u] = zrow[u * G * kH];
+        // lane u stages edge u's scalars (one memory round trip for the batch)
+        if (lane < m) {
+            const long long e = e0 + G * lane;
+            T* row = sm.ed[lane];
+            row[0] = ws.es[e];
+            row[1] = ws.eds[e];
+            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+            st4(row + 4, d0.x, d0.y, d0.z, d0.w);
+            st4(row + 8, d1.x, d1.y, d1.z, d1.w);
+            sm.emir[lane] = gr.inv_pos[e];
+        }
+        __syncwarp();
+        for (int u0 = 0; u0 < m; u0 += 8) {
+            const int mu = min(8, m - u0);
+            T zn[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (u < mu) zr[u] = zrow[4 * u * kH];
-            __syncwarp();
+                if (u0 + 8 + u < m) zn[u] = zrow[(u0 + 8 + u) * G * kH];
             T term[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 term[u] = T(0);
                 if (u < mu) {
-                    const T* row = sm.ed[w][u];
+                    const T* row = sm.ed[u0 + u];
                     const T s = row[0], ds = row[1];
                     const V4<T> d0 = ld4c(row + 4), d1 = ld4c(row + 8);
                     T wv = w1b[0] * d0.x;
@@ -432,213 +519,228 @@ __device__ __forceinline__ void msg_backward_atom(const DevMlp<T>& msg, const De
                     wv += w1b[6] * d1.z;
                     wv += w1b[7] * d1.w;
                     const T z = zr[u];
-                    const T d = s * vl * (T(1) - z * z);
-                    D[static_cast<long long>(sm.emir[w][u]) * kH + lane] = d;
-                    term[u] = ds * vl * z + d * wv;
+                    const T d = s * v * (T(1) - z * z);
+                    D[static_cast<long long>(sm.emir[u0 + u]) * kH + lane] = d;
+                    term[u] = ds * v * z + d * wv;
                 }
             }
             // reduce-scatter butterfly: 8 edge sums in 9 shuffles; lane 4u holds edge u
             const T tot = reduce8(term, lane);
             if ((lane & 3) == 0 && (lane >> 2) < mu) {
-                const long long e = e0 + 4 * (lane >> 2);
-                ws.g[e] = (first_g ? T(0) : ws.g[e]) + (tot + sm.ed[w][lane >> 2][1] * c0);
+                const int u = u0 + (lane >> 2);
+                const long long e = e0 + static_cast<long long>(G) * u;
+                ws.g[e] = (first_g ? T(0) : ws.g[e]) + (tot + sm.ed[u][1] * c0);
             }
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) zr[u] = zn[u];
         }
+        __syncwarp();
     }
-}
-
-// S_i = sum over i's mirror slots of the pushed dz (layer l) (+ remote partials
-// in domain decomposition) -> sm.v1; contiguous rows, fixed summation order.
-template <typename T>
-__device__ __forceinline__ void gather_in(const DevGraph& gr, const DevWork<T>& ws,
-                                          AtomSmem<T>& sm, int l, int i, int t, int g) {
-    const int lane = t & 31, w = t >> 5;
-    const T* D = ws.d + (l & 1) * ws.slots * kH;
-    const int is = gr.in_start[i], ic = gr.in_cnt[i];
-    T acc = T(0);
-    for (int base = 0; base < ic; base += kEdgePass) {
-        const int mw = max(0, (min(kEdgePass, ic - base) - w + 3) / 4);
-        const T* drow = D + static_cast<long long>(is + base + w) * kH + lane;
-        T dr_[kPW];
-#pragma unroll
-        for (int u = 0; u < kPW; ++u)
-            if (u < mw) dr_[u] = drow[4 * u * kH];
-#pragma unroll
-        for (int u = 0; u < kPW; ++u)
-            if (u < mw) acc += dr_[u];
-    }
-    sm.part[w][lane] = acc;
-    gsync(g);
-    if (t < 32) {
-        T s = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
-        // domain decomposition: partial sums pushed to ghost copies of i on other ranks
-        if (ws.s_remote) s += ws.s_remote[static_cast<long long>(i) * kH + t];
-        sm.v1[t] = s;
-    }
-    gsync(g);
 }
 
 // ---------------------------------------------------------------------------
 // Message layer l forward; LAST fuses the fitting net and the top layer's
-// backward (all atom-local).  `third` is message layer l+1 (for P^{l+1}) or the
-// fitting net (LAST).
+// backward (all atom-local).
 // ---------------------------------------------------------------------------
-template <typename T, bool LAST>
-__device__ void msg_fwd_body(const DevMlp<T>& msg, const DevMlp<T>& upd, const DevMlp<T>& third,
-                             const DevGraph& gr, const DevWork<T>& ws, int l, AtomSmem<T>* sms,
-                             const Grp& G) {
-    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
-    AtomSmem<T>& sm = sms[g];
-    const int n = gr.n;
-    const long long S = ws.slots;
-    const T* Pin = ws.pe + (l & 1) * S * kH;
-    T* __restrict__ Z = ws.z + l * S * kH;
+template <typename T, int G, bool LAST>
+__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr,
+                                                               DevWork<T> ws, int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    const DevMlp<T>& msg = md.msg[l];
+    const DevMlp<T>& upd = md.upd[l];
+    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
+    const T* mW2 = sg.template mat<32, 32>(msg.W2, 32);
+    const T* uW1 = sg.template mat<32, 64>(upd.W1, 64);
+    const T* uW2 = sg.template mat<32, 32>(upd.W2, 32);
+    const T *nW1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *uW2T = nullptr, *uW1T = nullptr,
+            *mW2T = nullptr;
+    if constexpr (LAST) {
+        fW1 = sg.template mat<32, 32>(md.fit.W1, 32);
+        fW1T = sg.template mat<32, 32>(md.fit.W1T, 32);
+        uW2T = sg.template mat<32, 32>(upd.W2T, 32);
+        uW1T = sg.template mat<64, 32>(upd.W1T, 32);
+        mW2T = sg.template mat<32, 32>(msg.W2T, 32);
+    } else {
+        nW1h = sg.template mat<32, 32>(md.msg[l + 1].W1, kInMsg);
+    }
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    const bool lead = tm.w == 0;
     T w1b[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
-    const T b1 = msg.b1[lane];
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
-    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
-        const int start = gr.row_start[i], cnt = gr.nnei[i];
-        if (t < 32) sm.v1[t] = ws.h[(static_cast<long long>(l) * n + i) * kH + t];  // h_i
+    const T mb1 = msg.b1[lane], mb2 = msg.b2[lane], ub1 = upd.b1[lane], ub2 = upd.b2[lane];
+    const T fb1 = LAST ? md.fit.b1[lane] : T(0), fw2 = LAST ? md.fit.W2[lane] : T(0);
+    const T fb2 = LAST ? md.fit.b2[0] : T(0);
+    sg.wait();
+    __syncthreads();
+    pdl_wait();
+    const int n = gr.n;
+    const long long S = ws.slots;
+    const T* Pin = ws.pe + (l & 1) * S * kH;
+    T* Z = ws.z + l * S * kH;
+    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        const int start = gr.row_start[i] + tm.w;
+        const int mloc = tm.local(gr.nnei[i]);
+        const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
+        sm.x[lane] = hi;
         T acc = T(0), ssum = T(0);
-        for (int base = 0; base < cnt; base += kEdgePass) {
-            const int mw = max(0, (min(kEdgePass, cnt - base) - w + 3) / 4);
-            const long long e0 = start + base + w;
-            // lane u stages edge u's scalars (one memory round trip for the pass);
-            // the edge loop reads them as shared-memory broadcasts
-            if (lane < mw) {
-                const long long e = e0 + 4 * lane;
-                T* row = sm.ed[w][lane];
+        for (int base = 0; base < mloc; base += 32) {
+            const int m = min(32, mloc - base);
+            const long long e0 = start + static_cast<long long>(G) * base;  // local k: e0 + G k
+            const T* prow = Pin + e0 * kH + lane;
+            // the first batch of P rows is in flight during the scalar staging;
+            // each batch's compute overlaps the next batch's loads
+            T pr[kU<T>];
+#pragma unroll
+            for (int u = 0; u < kU<T>; ++u)
+                if (u < m) pr[u] = prow[u * G * kH];
+            if (lane < m) {
+                const long long e = e0 + G * lane;
+                T* row = sm.ed[lane];
                 row[0] = ws.es[e];
                 const V4<T> b0 = ld4c(ws.eb + 8 * e), bb = ld4c(ws.eb + 8 * e + 4);
                 st4(row + 4, b0.x, b0.y, b0.z, b0.w);
                 st4(row + 8, bb.x, bb.y, bb.z, bb.w);
             }
-            const T* prow = Pin + e0 * kH + lane;
-            T pr[kPW];
-#pragma unroll
-            for (int u = 0; u < kPW; ++u)
-                if (u < mw) pr[u] = prow[4 * u * kH];
             __syncwarp();
+            for (int u0 = 0; u0 < m; u0 += kU<T>) {
+                T pn[kU<T>];
 #pragma unroll
-            for (int u = 0; u < kPW; ++u) {
-                if (u >= mw) break;
-                const long long e = e0 + 4 * u;
-                const T* row = sm.ed[w][u];
-                const T s = row[0];
-                const V4<T> b0 = ld4c(row + 4), bb = ld4c(row + 8);
-                T a = b1;
-                a += w1b[0] * b0.x;
-                a += w1b[1] * b0.y;
-                a += w1b[2] * b0.z;
-                a += w1b[3] * b0.w;
-                a += w1b[4] * bb.x;
-                a += w1b[5] * bb.y;
-                a += w1b[6] * bb.z;
-                a += w1b[7] * bb.w;
-                const T z = d_tanh(a + pr[u]);
-                Z[e * kH + lane] = z;
-                acc += s * z;
-                ssum += s;
+                for (int u = 0; u < kU<T>; ++u)
+                    if (u0 + kU<T> + u < m) pn[u] = prow[(u0 + kU<T> + u) * G * kH];
+#pragma unroll
+                for (int u = 0; u < kU<T>; ++u) {
+                    if (u0 + u >= m) break;
+                    const T* row = sm.ed[u0 + u];
+                    const T s = row[0];
+                    const V4<T> b0 = ld4c(row + 4), bb = ld4c(row + 8);
+                    T a = mb1;
+                    a += w1b[0] * b0.x;
+                    a += w1b[1] * b0.y;
+                    a += w1b[2] * b0.z;
+                    a += w1b[3] * b0.w;
+                    a += w1b[4] * bb.x;
+                    a += w1b[5] * bb.y;
+                    a += w1b[6] * bb.z;
+                    a += w1b[7] * bb.w;
+                    const T z = d_tanh(a + pr[u]);
+                    Z[(e0 + static_cast<long long>(G) * (u0 + u)) * kH + lane] = z;
+                    acc += s * z;
+                    ssum += s;
+                }
+#pragma unroll
+                for (int u = 0; u < kU<T>; ++u) pr[u] = pn[u];
             }
             __syncwarp();
         }
-        sm.part[w][lane] = acc;
-        if (lane == 0) sm.sc[w] = ssum;
-        gsync(g);
-        if (t < 32) sm.v0[t] = ((sm.part[0][t] + sm.part[1][t]) + sm.part[2][t]) + sm.part[3][t];
-        const T stot = ((sm.sc[0] + sm.sc[1]) + sm.sc[2]) + sm.sc[3];
-        gsync(g);
+        acc = tm.sum(acc, ssum, sm);
+        sm.t[lane] = acc;
+        __syncwarp();
         // msum = W2 (sum_e s_e z_e) + (sum_e s_e) b2  -> second half of the update input
-        const T msum = bmv<T, 32, 32>(msg.W2, 32, sm.v0, t) + stot * msg.b2[o];
-        if (lead) sm.v1[kH + o] = msum;
-        gsync(g);
+        const T msum = wmv<T, 32>(mW2, sm.t, lane) + ssum * mb2;
+        sm.x[kH + lane] = msum;
+        __syncwarp();
         // update MLP on [h_i, msum] (64 -> 32 tanh -> 32), residual
-        const T zu = d_tanh(bmv<T, 32, 64>(upd.W1, kInUpd, sm.v1, t) + upd.b1[o]);
-        if (lead) {
-            sm.v2[o] = zu;
-            ws.uz1[(static_cast<long long>(l) * n + i) * kH + o] = zu;
-        }
-        gsync(g);
-        const T hn = sm.v1[o] + (bmv<T, 32, 32>(upd.W2, 32, sm.v2, t) + upd.b2[o]);
-        if (lead) {
-            sm.v3[o] = hn;
-            ws.h[(static_cast<long long>(l + 1) * n + i) * kH + o] = hn;
-        }
-        gsync(g);
+        const T zu = d_tanh(wmv<T, 64>(uW1, sm.x, lane) + ub1);
+        if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
+        sm.y[lane] = zu;
+        __syncwarp();
+        const T hn = hi + (wmv<T, 32>(uW2, sm.y, lane) + ub2);
+        if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
+        sm.t[lane] = hn;
+        __syncwarp();
         if constexpr (!LAST) {
-            const T p = bmv<T, 32, 32>(third.W1, kInMsg, sm.v3, t);
-            if (lead) {
-                sm.v0[o] = p;
-                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + o] = p;
-            }
-            gsync(g);
-            push_rows(ws.pe + ((l + 1) & 1) * S * kH, sm.v0, gr, i, t);
+            const T p = wmv<T, 32>(nW1h, sm.t, lane);
+            if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
+            push_rows(ws.pe + ((l + 1) & 1) * S * kH, p, gr, i, tm);
         } else {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            // fitting: h^M in v3 -> dE/dh^M in v0 (v1 scratch for the fit hidden layer)
-            fit_fwd_bwd(third, sm.v3, sm.v1, sm.v0, sm.v0, owned, ws.e_atom + i, sm.s4, t, g);
-            msg_backward_atom(msg, upd, gr, ws, sm, l, i, true, t, g);
+            // fitting: h^M -> dE/dh^M
+            const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
+                                  lead ? ws.e_atom + i : nullptr, lane);
+            msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, true, tm);
         }
-        gsync(g);
+        __syncwarp();
     }
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
-// `nxt` is message layer l+1 (its W1h^T maps the gathered adjoints).
-template <typename T>
-__device__ void msg_bwd_body(const DevMlp<T>& msg, const DevMlp<T>& upd, const DevMlp<T>& nxt,
-                             const DevGraph& gr, const DevWork<T>& ws, int l, AtomSmem<T>* sms,
-                             const Grp& G) {
-    const int g = G.g, t = G.t;
-    AtomSmem<T>& sm = sms[g];
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
-    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
-        const T own = ws.dhown[static_cast<long long>(i) * kH + o];
-        const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + o];
-        gather_in(gr, ws, sm, l + 1, i, t, g);
+template <typename T, int G>
+__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr,
+                                                               DevWork<T> ws, int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    const DevMlp<T>& msg = md.msg[l];
+    const DevMlp<T>& upd = md.upd[l];
+    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
+    // W1h^(l+1)^T: rows 0..31 of msg[l+1].W1T ([in][32])
+    const T* nW1hT = sg.template mat<32, 32>(md.msg[l + 1].W1T, 32);
+    const T* uW2T = sg.template mat<32, 32>(upd.W2T, 32);
+    const T* uW1T = sg.template mat<64, 32>(upd.W1T, 32);
+    const T* mW2T = sg.template mat<32, 32>(msg.W2T, 32);
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    T w1b[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
+    const T mb2 = msg.b2[lane];
+    sg.wait();
+    __syncthreads();
+    pdl_wait();
+    const T* Dn = ws.d + ((l + 1) & 1) * ws.slots * kH;
+    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
+        const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + lane];
+        sm.t[lane] = gather_in(Dn, ws, gr, i, tm, sm);
+        __syncwarp();
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
-        const T dh = own + bmv<T, 32, 32>(nxt.W1T, 32, sm.v1, t);
-        if (lead) {
-            sm.v0[o] = dh;
-            sm.v2[o] = zu;
-        }
-        gsync(g);
-        msg_backward_atom(msg, upd, gr, ws, sm, l, i, false, t, g);
-        gsync(g);
+        const T dh = own + wmv<T, 32>(nW1hT, sm.t, lane);
+        __syncwarp();
+        msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, false, tm);
+        __syncwarp();
     }
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
-template <typename T>
-__device__ void embed_bwd_body(const DevMlp<T>& emb, const DevMlp<T>& msg0, const DevGraph& gr,
-                               const DevWork<T>& ws, AtomSmem<T>* sms, const Grp& G) {
-    const int g = G.g, t = G.t;
-    AtomSmem<T>& sm = sms[g];
-    const int o = bmv_out<32>(t);
-    const bool lead = bmv_lead<32>(t);
-    for (int i = G.gid; i < gr.n_active; i += G.ngroups) {
-        const T own = ws.dhown[static_cast<long long>(i) * kH + o];
-        const T z1 = ws.ez1[static_cast<long long>(i) * kH + o];
-        gather_in(gr, ws, sm, 0, i, t, g);
-        const T dh = own + bmv<T, 32, 32>(msg0.W1T, 32, sm.v1, t);
-        if (lead) sm.v0[o] = dh;
-        gsync(g);
-        const T dz1 = bmv<T, 32, 32>(emb.W2T, 32, sm.v0, t) * (T(1) - z1 * z1);
-        if (lead) sm.v2[o] = dz1;
-        gsync(g);
-        const T dd = bmv<T, 32, 32>(emb.W1T, 32, sm.v2, t);
-        if (lead) sm.v3[o] = dd;
-        gsync(g);
-        const int start = gr.row_start[i], cnt = gr.nnei[i];
-        for (int q = t; q < cnt; q += kAT) {
-            const long long e = start + q;
+template <typename T, int G>
+__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr,
+                                                                 DevWork<T> ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
+    const T* m0W1hT = sg.template mat<32, 32>(md.msg[0].W1T, 32);
+    const T* eW2T = sg.template mat<32, 32>(md.embed.W2T, 32);
+    const T* eW1T = sg.template mat<32, 32>(md.embed.W1T, 32);
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    sg.wait();
+    __syncthreads();
+    pdl_wait();
+    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
+        const T z1 = ws.ez1[static_cast<long long>(i) * kH + lane];
+        sm.t[lane] = gather_in(ws.d, ws, gr, i, tm, sm);
+        __syncwarp();
+        const T dh = own + wmv<T, 32>(m0W1hT, sm.t, lane);
+        sm.x[lane] = dh;
+        __syncwarp();
+        const T dz1 = wmv<T, 32>(eW2T, sm.x, lane) * (T(1) - z1 * z1);
+        sm.y[lane] = dz1;
+        __syncwarp();
+        const T dd = wmv<T, 32>(eW1T, sm.y, lane);
+        sm.t[lane] = dd;
+        __syncwarp();
+        const int start = gr.row_start[i] + tm.w;
+        const int mloc = tm.local(gr.nnei[i]);
+        for (int q = lane; q < mloc; q += 32) {
+            const long long e = start + static_cast<long long>(G) * q;
             const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-            const T* dv = sm.v3 + gr.ety[e] * kK;
+            const T* dv = sm.t + gr.ety[e] * kK;
             T acc = dv[0] * d0.x;
             acc += dv[1] * d0.y;
             acc += dv[2] * d0.z;
@@ -651,27 +753,46 @@ __device__ void embed_bwd_body(const DevMlp<T>& emb, const DevMlp<T>& msg0, cons
             ws.g[e] = gv;
             ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
         }
-        gsync(g);
+        __syncwarp();
     }
 }
 
+// Warp-per-atom range for the force kernel: warp-global index and stride.
+struct WarpPos {
+    int lane, first, stride;
+    __device__ WarpPos()
+        : lane(threadIdx.x & 31),
+          first(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)),
+          stride(gridDim.x * (blockDim.x >> 5)) {}
+};
+
 // ---------------------------------------------------------------------------
-// Forces (gather form), per-atom energy, virial, and the velocity-Verlet tail
-// of the device MD loop; accumulates this thread's E, W, W_ab into acc[11].
+// Forces (gather form, warp per atom), per-atom energy, virial, and the
+// velocity-Verlet tail of the device MD loop.
 //   F_i = sum_{e in out(i)} u_e g_e - sum_{e' in in(i)} u_e' g_e'
 //       = sum_q u_q (g_q + grev_q)            (symmetric list: u_rev(e) = -u_e)
 //   W   = -sum_e g_e r_e ;  W_ab = -sum_e g_e dr_a u_b
+// CTA partials of (E, W, W_ab) in a fixed order, then the last CTA to finish
+// reduces all CTAs' partials in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __restrict__ forces,
-                           double* __restrict__ per_atom, const MdFuse& mf, AtomSmem<T>* sms,
-                           double (&acc)[11], const Grp& G) {
-    const int g = G.g, t = G.t, lane = t & 31, w = t >> 5;
-    AtomSmem<T>& sm = sms[g];
-    for (int i = G.gid; i < gr.n; i += G.ngroups) {
+__global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
+                                                     double* __restrict__ forces,
+                                                     double* __restrict__ per_atom,
+                                                     double* __restrict__ out, MdFuse mf) {
+    __shared__ double s_part[kForceCTA / 32][12];
+    __shared__ bool s_last;
+    pdl_launch_dependents();
+    pdl_wait();
+    const WarpPos wp;
+    const int lane = wp.lane, wc = threadIdx.x >> 5;
+    double acc[11];
+#pragma unroll
+    for (int q = 0; q < 11; ++q) acc[q] = 0.0;
+    for (int i = wp.first; i < gr.n; i += wp.stride) {
         // MD state of atom i, loaded early (independent of the edge loads)
         double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0;
-        if (mf.mode && t == 0) {
+        if (mf.mode && lane == 0) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 vv[a] = mf.v[3 * i + a];
@@ -681,7 +802,7 @@ __device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __r
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
         const int start = gr.row_start[i], cnt = gr.nnei[i];
-        for (int q = t; q < cnt; q += kAT) {
+        for (int q = lane; q < cnt; q += 32) {
             const int e = start + q;
             const T gg = ws.g[e];
             const T gm = gr.sym ? ws.grev[e] : T(0);
@@ -703,7 +824,7 @@ __device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __r
         }
         if (!gr.sym) {  // generic CSR: the pushed g of each in-edge, its own geometry
             const int is = gr.in_start[i], ic = gr.in_cnt[i];
-            for (int q = t; q < ic; q += kAT) {
+            for (int q = lane; q < ic; q += 32) {
                 const int e = gr.in_edge[is + q];
                 const T gg = ws.grev[is + q];
                 T x, y, z;
@@ -717,24 +838,16 @@ __device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __r
         fy = warp_sum(fy);
         fz = warp_sum(fz);
         if (lane == 0) {
-            sm.f[w][0] = fx;
-            sm.f[w][1] = fy;
-            sm.f[w][2] = fz;
-        }
-        gsync(g);
-        if (t == 0) {
-            double f3[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) f3[a] = ((sm.f[0][a] + sm.f[1][a]) + sm.f[2][a]) + sm.f[3][a];
-            forces[3 * i] = f3[0];
-            forces[3 * i + 1] = f3[1];
-            forces[3 * i + 2] = f3[2];
+            const double f3[3] = {fx, fy, fz};
+            forces[3 * i] = fx;
+            forces[3 * i + 1] = fy;
+            forces[3 * i + 2] = fz;
             const double ei = ws.e_atom[i];
             if (per_atom) per_atom[i] = ei;
             acc[0] += ei;
             if (mf.mode) {
                 const double s = mf.half / mi;
-                const bool finite = isfinite(f3[0]) && isfinite(f3[1]) && isfinite(f3[2]);
+                const bool finite = isfinite(fx) && isfinite(fy) && isfinite(fz);
                 if (!finite) atomicOr(ws.err, kErrNonFinite);
                 double x3[3];
 #pragma unroll
@@ -751,38 +864,28 @@ __device__ void force_body(const DevGraph& gr, const DevWork<T>& ws, double* __r
                     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, ws.err);
             }
         }
-        gsync(g);
     }
-}
-
-// CTA partials of (E, W, W_ab) in a fixed order, then the last CTA to finish
-// reduces all CTAs' partials in a fixed order into out[0..10] (deterministic).
-template <typename T>
-__device__ void reduce_energy_virial(double (&acc)[11], const DevWork<T>& ws,
-                                     double* __restrict__ out, double (*s_part)[12], bool* s_last) {
-    const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < 11; ++q) acc[q] = warp_sum(acc[q]);
-    __syncthreads();
     if (lane == 0)
 #pragma unroll
         for (int q = 0; q < 11; ++q) s_part[wc][q] = acc[q];
     __syncthreads();
     if (threadIdx.x < 11) {
         double v = 0.0;
-        for (int q = 0; q < kCTA / 32; ++q) v += s_part[q][threadIdx.x];
+        for (int q = 0; q < kForceCTA / 32; ++q) v += s_part[q][threadIdx.x];
         ws.partial[blockIdx.x * 16 + threadIdx.x] = v;
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
-    if (*s_last) {
+    if (s_last) {
         __threadfence();
         double v[11];
 #pragma unroll
         for (int q = 0; q < 11; ++q) v[q] = 0.0;
-        for (unsigned b = threadIdx.x; b < gridDim.x; b += kCTA)
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += kForceCTA)
 #pragma unroll
             for (int q = 0; q < 11; ++q) v[q] += __ldcg(ws.partial + b * 16 + q);
 #pragma unroll
@@ -794,88 +897,11 @@ __device__ void reduce_energy_virial(double (&acc)[11], const DevWork<T>& ws,
         __syncthreads();
         if (threadIdx.x < 11) {
             double tot = 0.0;
-            for (int q = 0; q < kCTA / 32; ++q) tot += s_part[q][threadIdx.x];
+            for (int q = 0; q < kForceCTA / 32; ++q) tot += s_part[q][threadIdx.x];
             out[threadIdx.x] = tot;
         }
-        if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / step
+        if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / graph replay
     }
-    __syncthreads();
-}
-
-// ---------------------------------------------------------------------------
-// Standalone kernels (one phase each; weights staged per launch)
-// ---------------------------------------------------------------------------
-template <typename T, bool FUSE_FIT>
-__global__ __launch_bounds__(kCTA, 1) void k_embed(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                   int* __restrict__ rev, MdFuse mf) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
-    const DevMlp<T> second =
-        FUSE_FIT ? sg.mlp(md.fit, kInFit, 1) : sg.mlp(md.msg[0], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    embed_body<T, FUSE_FIT>(md, emb, second, gr, ws, rev, mf,
-                            sg.template scratch<AtomSmem<T>>(), Grp());
-}
-
-template <typename T, bool LAST>
-__global__ __launch_bounds__(kCTA, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                     int l) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
-    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
-    const DevMlp<T> third = LAST ? sg.mlp(md.fit, kInFit, 1) : sg.mlp(md.msg[l + 1], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    msg_fwd_body<T, LAST>(msg, upd, third, gr, ws, l, sg.template scratch<AtomSmem<T>>(), Grp());
-}
-
-template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws,
-                                                     int l) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> msg = sg.mlp(md.msg[l], kInMsg, kH);
-    const DevMlp<T> upd = sg.mlp(md.upd[l], kInUpd, kH);
-    const DevMlp<T> nxt = sg.mlp(md.msg[l + 1], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    msg_bwd_body<T>(msg, upd, nxt, gr, ws, l, sg.template scratch<AtomSmem<T>>(), Grp());
-}
-
-template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr, DevWork<T> ws) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_launch_dependents();
-    Stager<T> sg{reinterpret_cast<T*>(smem_raw), 0};
-    const DevMlp<T> emb = sg.mlp(md.embed, kInEmbed, kH);
-    const DevMlp<T> msg0 = sg.mlp(md.msg[0], kInMsg, kH);
-    __syncthreads();
-    pdl_wait();
-    embed_bwd_body<T>(emb, msg0, gr, ws, sg.template scratch<AtomSmem<T>>(), Grp());
-}
-
-template <typename T>
-__global__ __launch_bounds__(kCTA, 1) void k_force(DevGraph gr, DevWork<T> ws,
-                                                   double* __restrict__ forces,
-                                                   double* __restrict__ per_atom,
-                                                   double* __restrict__ out, MdFuse mf) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double s_part[kCTA / 32][12];
-    __shared__ bool s_last;
-    pdl_launch_dependents();
-    pdl_wait();
-    double acc[11];
-#pragma unroll
-    for (int q = 0; q < 11; ++q) acc[q] = 0.0;
-    force_body<T>(gr, ws, forces, per_atom, mf, reinterpret_cast<AtomSmem<T>*>(smem_raw), acc,
-                  Grp());
-    reduce_energy_virial<T>(acc, ws, out, s_part, &s_last);
 }
 
 // ---------------------------------------------------------------------------
@@ -907,83 +933,150 @@ __global__ void k_dd_ghost_sums(DevGraph gr, const T* __restrict__ d, T* __restr
 // ---------------------------------------------------------------------------
 // launch
 // ---------------------------------------------------------------------------
-static int net_grid(int n) {
-    const int want = (n + kG - 1) / kG;
-    const int cap = num_sms() * 2;  // grid-stride beyond two CTAs per SM
+// Staged weight elements per kernel (must follow the kernels' staging order).
+enum class Phase { EmbedFit, Embed, MsgFwd, MsgFwdLast, MsgBwd, EmbedBwd };
+template <typename T>
+static int staged_elems(Phase p) {
+    const int m32 = mat_elems<T>(32, 32), m64 = mat_elems<T>(32, 64), t64 = mat_elems<T>(64, 32);
+    switch (p) {
+        case Phase::EmbedFit: return 6 * m32;
+        case Phase::Embed: return 3 * m32;
+        case Phase::MsgFwd: return 3 * m32 + m64;
+        case Phase::MsgFwdLast: return 6 * m32 + m64 + t64;
+        case Phase::MsgBwd: return 3 * m32 + t64;
+        case Phase::EmbedBwd: return 3 * m32;
+    }
+    return 0;
+}
+
+// Launch shape: team size G (warps per atom) from the system size — the
+// largest of 4, 2, 1 that keeps every atom's team resident at 16 warps per SM —
+// then enough teams per CTA that the atoms fill every SM, grid-stride beyond
+// two CTAs per SM.
+struct NetShape {
+    int G, warps, grid;
+};
+static NetShape net_shape(int n) {
+    const int sms = num_sms();
+    const int G = (4 * n <= kMaxWarps * sms) ? 4 : (2 * n <= kMaxWarps * sms ? 2 : 1);
+    const int max_teams = kMaxWarps / G;
+    int teams = (n + sms - 1) / sms;
+    teams = teams < 1 ? 1 : (teams > max_teams ? max_teams : teams);
+    if (G == 1 && teams < 2) teams = 2;
+    int grid = (n + teams - 1) / teams;
+    if (grid > 2 * sms) grid = 2 * sms;
+    return {G, teams * G, grid < 1 ? 1 : grid};
+}
+
+template <typename T, typename... Params, typename... Args>
+static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, cudaStream_t st,
+                       Args... args) {
+    const size_t smem = static_cast<size_t>(staged_elems<T>(p)) * sizeof(T) + 16 +
+                        static_cast<size_t>(sh.warps) * sizeof(WarpSmem<T>);
+    launch_pdl(kernel, dim3(sh.grid), dim3(32 * sh.warps), smem, st, args...);
+}
+
+static int force_grid(int n) {
+    const int want = (n + kForceCTA / 32 - 1) / (kForceCTA / 32);
+    const int cap = num_sms() * 8;
     return want < 1 ? 1 : (want < cap ? want : cap);
 }
 
-template <typename T>
-static size_t smem_bytes(int weight_elems) {
-    return static_cast<size_t>(weight_elems) * sizeof(T) + 16 + kG * sizeof(AtomSmem<T>);
-}
+constexpr int kMaxSmem = 200 * 1024;
 
-// Launch with the staged weights + the groups' AtomSmem in dynamic shared memory
-// (the > 48 KB opt-in is set by net_configure() when a context is created, never
-// during stream capture).
-template <typename T, typename... Params, typename... Args>
-static void launch_staged(void (*kernel)(Params...), int grid, int smem_elems, cudaStream_t st,
-                          Args... args) {
-    launch_pdl(kernel, dim3(grid), dim3(kCTA), smem_bytes<T>(smem_elems), st, args...);
-}
+// The network phases for one element type and team size.
+template <typename T, int G>
+struct Net {
+    static cudaError_t configure() {
+        const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        cudaError_t e = cudaSuccess;
+        for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_embed<T, G, false>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, true>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, false>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_bwd<T, G>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_embed_bwd<T, G>, a, kMaxSmem)})
+            if (r != cudaSuccess) e = r;
+        return e;
+    }
+    static void embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                      const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
+        if (md.n_msg == 0)
+            launch_net<T>(k_embed<T, G, true>, Phase::EmbedFit, sh, st, md, gr, ws, rev, mf);
+        else
+            launch_net<T>(k_embed<T, G, false>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
+    }
+    static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                        const DevWork<T>& ws, int l, cudaStream_t st) {
+        if (l == md.n_msg - 1)
+            launch_net<T>(k_msg_fwd<T, G, true>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
+        else
+            launch_net<T>(k_msg_fwd<T, G, false>, Phase::MsgFwd, sh, st, md, gr, ws, l);
+    }
+    static void msg_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                        const DevWork<T>& ws, int l, cudaStream_t st) {
+        launch_net<T>(k_msg_bwd<T, G>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+    }
+    static void embed_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                          const DevWork<T>& ws, cudaStream_t st) {
+        launch_net<T>(k_embed_bwd<T, G>, Phase::EmbedBwd, sh, st, md, gr, ws);
+    }
+    static int network(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                       const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
+                       const MdFuse& mf) {
+        const int M = md.n_msg;
+        embed(sh, md, gr, ws, rev, mf, st);
+        mk(M == 0 ? "embed_fit" : "embed", st);
+        if (M == 0) return 1;
+        for (int l = 0; l < M; ++l) {
+            msg_fwd(sh, md, gr, ws, l, st);
+            mk(l == M - 1 ? "msg_fwd_last" : "msg_fwd", st);
+        }
+        for (int l = M - 2; l >= 0; --l) {
+            msg_bwd(sh, md, gr, ws, l, st);
+            mk("msg_bwd", st);
+        }
+        embed_bwd(sh, md, gr, ws, st);
+        mk("embed_bwd", st);
+        return 2 + M + (M - 1);
+    }
+    static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                         const DevWork<T>& ws, int phase, int l, cudaStream_t st) {
+        const MdFuse none{};
+        switch (phase) {
+            case 0: embed(sh, md, gr, ws, nullptr, none, st); break;
+            case 2: msg_fwd(sh, md, gr, ws, l, st); break;
+            case 4: msg_bwd(sh, md, gr, ws, l, st); break;
+            case 5: embed_bwd(sh, md, gr, ws, st); break;
+        }
+    }
+};
 
-constexpr int kMaxSmem = 224 * 1024;
-
-template <typename T>
-static cudaError_t configure_t() {
-    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+// Per device: allow the staged-weight kernels > 48 KB of dynamic shared memory
+// (set when a context is created, never during stream capture).
+cudaError_t net_configure() {
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, true>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_embed<T, false>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_msg_fwd<T, true>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_msg_fwd<T, false>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_msg_bwd<T>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_embed_bwd<T>, a, kMaxSmem),
-                          cudaFuncSetAttribute(k_force<T>, a, kMaxSmem)})
+    for (cudaError_t r : {Net<float, 1>::configure(), Net<float, 2>::configure(),
+                          Net<float, 4>::configure(), Net<double, 1>::configure(),
+                          Net<double, 2>::configure(), Net<double, 4>::configure()})
         if (r != cudaSuccess) e = r;
     return e;
-}
-// Per device: allow the staged-weight kernels up to 224 KB of dynamic smem.
-cudaError_t net_configure() {
-    const cudaError_t a = configure_t<float>();
-    const cudaError_t b = configure_t<double>();
-    return a != cudaSuccess ? a : b;
 }
 
 template <typename T>
 int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws,
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
-    const int nb = net_grid(gr.n);
-    const int M = md.n_msg;
-    const int e_emb = mlp_elems(kInEmbed, kH), e_fit = mlp_elems(kInFit, 1);
-    const int e_msg = mlp_elems(kInMsg, kH), e_upd = mlp_elems(kInUpd, kH);
-    int launches = 0;
-    if (M == 0) {
-        launch_staged<T>(k_embed<T, true>, nb, e_emb + e_fit, st, md, gr, ws, rev, mf);
-        mk("embed_fit", st);
-        ++launches;
-    } else {
-        launch_staged<T>(k_embed<T, false>, nb, e_emb + e_msg, st, md, gr, ws, rev, mf);
-        mk("embed", st);
-        for (int l = 0; l < M; ++l) {
-            if (l == M - 1) {
-                launch_staged<T>(k_msg_fwd<T, true>, nb, e_msg + e_upd + e_fit, st, md, gr, ws, l);
-                mk("msg_fwd_last", st);
-            } else {
-                launch_staged<T>(k_msg_fwd<T, false>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
-                mk("msg_fwd", st);
-            }
-        }
-        for (int l = M - 2; l >= 0; --l) {
-            launch_staged<T>(k_msg_bwd<T>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
-            mk("msg_bwd", st);
-        }
-        launch_staged<T>(k_embed_bwd<T>, nb, e_emb + e_msg, st, md, gr, ws);
-        mk("embed_bwd", st);
-        launches += 2 + M + (M - 1);
-    }
-    launch_staged<T>(k_force<T>, nb, 0, st, gr, ws, forces, per_atom, out, mf);
+    const NetShape sh = net_shape(gr.n_active);
+    int launches;
+    if (sh.G == 4)
+        launches = Net<T, 4>::network(sh, md, gr, ws, rev, st, mk, mf);
+    else if (sh.G == 2)
+        launches = Net<T, 2>::network(sh, md, gr, ws, rev, st, mk, mf);
+    else
+        launches = Net<T, 1>::network(sh, md, gr, ws, rev, st, mk, mf);
+    launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
+               per_atom, out, mf);
     mk("force", st);
     return launches + 1;
 }
@@ -995,47 +1088,30 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st) {
-    const int nb = net_grid(gr.n_active);
-    const int M = md.n_msg;
-    const int e_emb = mlp_elems(kInEmbed, kH), e_fit = mlp_elems(kInFit, 1);
-    const int e_msg = mlp_elems(kInMsg, kH), e_upd = mlp_elems(kInUpd, kH);
+    const NetShape sh = net_shape(gr.n_active);
     const int ng = gr.n - gr.n_active;
-    const MdFuse none{};
     switch (phase) {
-        case 0:
-            if (M == 0)
-                launch_staged<T>(k_embed<T, true>, nb, e_emb + e_fit, st, md, gr, ws,
-                                 static_cast<int*>(nullptr), none);
-            else
-                launch_staged<T>(k_embed<T, false>, nb, e_emb + e_msg, st, md, gr, ws,
-                                 static_cast<int*>(nullptr), none);
-            break;
         case 1:
             if (ng > 0)
                 k_dd_push_ghosts<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
                     gr, ws.p_atom, ws.pe + (l & 1) * ws.slots * kH);
-            break;
-        case 2:
-            if (l == M - 1)
-                launch_staged<T>(k_msg_fwd<T, true>, nb, e_msg + e_upd + e_fit, st, md, gr, ws, l);
-            else
-                launch_staged<T>(k_msg_fwd<T, false>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
             break;
         case 3:
             if (ng > 0)
                 k_dd_ghost_sums<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
                     gr, ws.d + (l & 1) * ws.slots * kH, s_ghost);
             break;
-        case 4:
-            launch_staged<T>(k_msg_bwd<T>, nb, 2 * e_msg + e_upd, st, md, gr, ws, l);
-            break;
-        case 5:
-            launch_staged<T>(k_embed_bwd<T>, nb, e_emb + e_msg, st, md, gr, ws);
-            break;
         case 6:
-            launch_staged<T>(k_force<T>, net_grid(gr.n), 0, st, gr, ws, forces,
-                             static_cast<double*>(nullptr), out, none);
+            launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws,
+                       forces, static_cast<double*>(nullptr), out, MdFuse{});
             break;
+        default:
+            if (sh.G == 4)
+                Net<T, 4>::dd_phase(sh, md, gr, ws, phase, l, st);
+            else if (sh.G == 2)
+                Net<T, 2>::dd_phase(sh, md, gr, ws, phase, l, st);
+            else
+                Net<T, 1>::dd_phase(sh, md, gr, ws, phase, l, st);
     }
 }
 template void launch_dd_phase<float>(const DevModel<float>&, const DevGraph&,

@@ -213,7 +213,11 @@ class GpuEngine:
         self.prec = precision
         self.dtype = torch.float64 if int(precision) == 1 else torch.float32
         stream = torch.cuda.current_stream(torch.device("cuda", ctx.device))
-        check(lib().hmdp_set_stream(ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
+        # torch's default stream has handle 0, which hmdp_set_stream reads as "the
+        # context's own stream"; name the legacy default stream (cudaStreamLegacy
+        # = 1) explicitly so the phases and the torch halo copies share one stream
+        handle = stream.cuda_stream or 1
+        check(lib().hmdp_set_stream(ctx.handle, ctypes.c_void_p(handle)))
 
     def setup(self, plan: RankPlan):
         L = lib()
