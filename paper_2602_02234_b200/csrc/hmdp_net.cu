@@ -51,7 +51,7 @@ namespace hmdp {
 int num_sms();  // hmdp_nbr.cu
 
 constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
-constexpr int kForceCTA = 256;
+constexpr int kForceCTA = 128;  // small CTAs: every SM gets atoms in small systems
 // edges per unrolled batch (row loads in flight per lane; fewer for FP64 registers)
 template <typename T>
 constexpr int kU = sizeof(T) == 4 ? 8 : 4;
@@ -74,7 +74,7 @@ struct WarpSmem {
     alignas(16) T y[64];
     alignas(16) T t[32];
     alignas(16) T ed[32][12];  // staged edge scalars: (s, s', -, -, b or b'[8])
-    alignas(16) T red[2][32];  // team-sum partials (double-buffered)
+    alignas(16) T red[2][64];  // team-sum partials (double-buffered)
     T reds[2];
     int emir[32];  // staged mirror slots
     int ety[32];   // staged neighbour types
@@ -210,9 +210,84 @@ struct Team {
         T dummy = T(0);
         return sum(v, dummy, sm);
     }
+    // two per-lane values summed with one barrier
+    template <typename T>
+    __device__ __forceinline__ void sum2(T& v0, T& v1, WarpSmem<T>& sm) {
+        if constexpr (G > 1) {
+            sm.red[rb][lane] = v0;
+            sm.red[rb][32 + lane] = v1;
+            sync();
+            const WarpSmem<T>* b = &sm - w;
+            T a0 = b[0].red[rb][lane], a1 = b[0].red[rb][32 + lane];
+#pragma unroll
+            for (int q = 1; q < G; ++q) {
+                a0 += b[q].red[rb][lane];
+                a1 += b[q].red[rb][32 + lane];
+            }
+            v0 = a0;
+            v1 = a1;
+            rb ^= 1;
+        }
+    }
     // number of this warp's local edges among cnt
     __device__ __forceinline__ int local(int cnt) const { return (cnt - w + G - 1) / G; }
 };
+
+// Team mat-vec: sum_{k<NIN} W[row][k] x[k] with the inputs split over the
+// team's warps (warp w: inputs [w NIN/G, (w+1) NIN/G)) and the partials summed
+// in a fixed order — one copy of the weight traffic per team, not per warp.
+template <typename T, int NIN, int G>
+__device__ __forceinline__ T twmv(const T* W, const T* x, int row, Team<G>& tm,
+                                  WarpSmem<T>& sm) {
+    if constexpr (G == 1) {
+        return wmv<T, NIN>(W, x, row);
+    } else {
+        constexpr int KC = NIN / G;
+        static_assert(KC % 4 == 0, "bad team split");
+        const T* wr = W + row * pad_ld<T>(NIN) + tm.w * KC;
+        const T* xr = x + tm.w * KC;
+        T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+        for (int k = 0; k < KC; k += 4) {
+            const V4<T> wv = ld4c(wr + k), xv = ld4c(xr + k);
+            a0 += wv.x * xv.x;
+            a1 += wv.y * xv.y;
+            a2 += wv.z * xv.z;
+            a3 += wv.w * xv.w;
+        }
+        return tm.sum((a0 + a1) + (a2 + a3), sm);
+    }
+}
+// Two rows of the same matrix (e.g. both halves of a 64-row transposed layer).
+template <typename T, int NIN, int G>
+__device__ __forceinline__ void twmv2(const T* W, const T* x, int row0, int row1, T& y0, T& y1,
+                                      Team<G>& tm, WarpSmem<T>& sm) {
+    if constexpr (G == 1) {
+        y0 = wmv<T, NIN>(W, x, row0);
+        y1 = wmv<T, NIN>(W, x, row1);
+    } else {
+        constexpr int KC = NIN / G;
+        const T* w0 = W + row0 * pad_ld<T>(NIN) + tm.w * KC;
+        const T* w1 = W + row1 * pad_ld<T>(NIN) + tm.w * KC;
+        const T* xr = x + tm.w * KC;
+        T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
+#pragma unroll
+        for (int k = 0; k < KC; k += 4) {
+            const V4<T> xv = ld4c(xr + k), u = ld4c(w0 + k), v = ld4c(w1 + k);
+            a0 += u.x * xv.x;
+            a1 += u.y * xv.y;
+            a0 += u.z * xv.z;
+            a1 += u.w * xv.w;
+            b0 += v.x * xv.x;
+            b1 += v.y * xv.y;
+            b0 += v.z * xv.z;
+            b1 += v.w * xv.w;
+        }
+        y0 = a0 + a1;
+        y1 = b0 + b1;
+        tm.sum2(y0, y1, sm);
+    }
+}
 
 // Push the per-lane value P (channel lane) into the rows dst[in_edge[..]] of
 // i's in-edges (the out-slots whose consumer reads P_i); slots split over the team.
@@ -258,16 +333,18 @@ __device__ __forceinline__ T gather_in(const T* D, const DevWork<T>& ws, const D
 // Fitting net forward + backward on h (shared, channel-indexed): writes e_i for
 // owned atoms (0 for ghosts; e_out may be null), returns dE/dh[lane] (0 for
 // ghosts).  inference.cpp:288-311.  tmp: 32 elements of shared scratch.
-template <typename T>
+template <typename T, int G>
 __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2, T fb2,
-                                      const T* h_s, T* tmp, bool owned, double* e_out, int lane) {
-    const T zf = d_tanh(wmv<T, 32>(fW1, h_s, lane) + fb1);
+                                      const T* h_s, T* tmp, bool owned, double* e_out,
+                                      Team<G>& tm, WarpSmem<T>& sm) {
+    const int lane = tm.lane;
+    const T zf = d_tanh(twmv<T, 32>(fW1, h_s, lane, tm, sm) + fb1);
     // linear head 32 -> 1 and its adjoint (dout = 1)
     const T e = warp_sum(fw2 * zf) + fb2;
     if (e_out && lane == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
     tmp[lane] = (fw2 * T(1)) * (T(1) - zf * zf);
     __syncwarp();
-    const T dh = wmv<T, 32>(fW1T, tmp, lane);
+    const T dh = twmv<T, 32>(fW1T, tmp, lane, tm, sm);
     __syncwarp();
     return owned ? dh : T(0);
 }
@@ -397,25 +474,25 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed(DevModel<T> md, Dev
         if (lead && lane < nd) ws.desc[static_cast<long long>(i) * 32 + lane] = desc;
         __syncwarp();
         // embedding forward nd (zero-padded to 32) -> 32 (tanh) -> 32
-        const T z1 = d_tanh(wmv<T, 32>(eW1, sm.x, lane) + eb1);
+        const T z1 = d_tanh(twmv<T, 32>(eW1, sm.x, lane, tm, sm) + eb1);
         if (lead) ws.ez1[static_cast<long long>(i) * kH + lane] = z1;
         sm.y[lane] = z1;
         __syncwarp();
-        const T h0 = wmv<T, 32>(eW2, sm.y, lane) + eb2;
+        const T h0 = twmv<T, 32>(eW2, sm.y, lane, tm, sm) + eb2;
         if (lead) ws.h[static_cast<long long>(i) * kH + lane] = h0;
         sm.x[lane] = h0;
         __syncwarp();
         if constexpr (FUSE_FIT) {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
             const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.x, sm.t, owned,
-                                  lead ? ws.e_atom + i : nullptr, lane);
+                                  lead ? ws.e_atom + i : nullptr, tm, sm);
             sm.y[lane] = dh;
             __syncwarp();
             // embedding backward: linear layer 2 (W2^T), tanh layer 1 (W1^T, padded)
-            const T dz1 = wmv<T, 32>(eW2T, sm.y, lane) * (T(1) - z1 * z1);
+            const T dz1 = twmv<T, 32>(eW2T, sm.y, lane, tm, sm) * (T(1) - z1 * z1);
             sm.t[lane] = dz1;
             __syncwarp();
-            const T dd = wmv<T, 32>(eW1T, sm.t, lane);
+            const T dd = twmv<T, 32>(eW1T, sm.t, lane, tm, sm);
             sm.x[lane] = dd;
             __syncwarp();
             for (int q = lane; q < mloc; q += 32) {
@@ -435,7 +512,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed(DevModel<T> md, Dev
             }
         } else {
             // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
-            const T p = wmv<T, 32>(W1h, sm.x, lane);
+            const T p = twmv<T, 32>(W1h, sm.x, lane, tm, sm);
             if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
             push_rows(ws.pe, p, gr, i, tm);
         }
@@ -453,22 +530,22 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
                                                   T mb2, const T (&w1b)[kK], const DevGraph& gr,
                                                   const DevWork<T>& ws, WarpSmem<T>& sm, int l,
                                                   int i, T dh, T zu, bool first_g,
-                                                  const Team<G>& tm) {
+                                                  Team<G>& tm) {
     const int lane = tm.lane;
     const long long S = ws.slots;
     // update MLP backward (64 -> 32 tanh -> 32)
     sm.t[lane] = dh;
     __syncwarp();
-    const T dz = wmv<T, 32>(uW2T, sm.t, lane) * (T(1) - zu * zu);
+    const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
     sm.y[lane] = dz;
     __syncwarp();
-    const T din_h = wmv<T, 32>(uW1T, sm.y, lane);       // input rows 0..31: h
-    const T dmsum = wmv<T, 32>(uW1T, sm.y, lane + 32);  // input rows 32..63: msum
+    T din_h, dmsum;  // input rows 0..31 (h) and 32..63 (msum)
+    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, dmsum, tm, sm);
     if (tm.w == 0)
         ws.dhown[static_cast<long long>(i) * kH + lane] = dh + din_h;  // residual + update
     sm.x[lane] = dmsum;
     __syncwarp();
-    const T v = wmv<T, 32>(mW2T, sm.x, lane);  // v = W2^T dmsum
+    const T v = twmv<T, 32>(mW2T, sm.x, lane, tm, sm);  // v = W2^T dmsum
     const T c0 = warp_sum(dmsum * mb2);
     const T* Z = ws.z + l * S * kH;
     T* D = ws.d + (l & 1) * S * kH;
@@ -640,27 +717,27 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_fwd(DevModel<T> md, D
         sm.t[lane] = acc;
         __syncwarp();
         // msum = W2 (sum_e s_e z_e) + (sum_e s_e) b2  -> second half of the update input
-        const T msum = wmv<T, 32>(mW2, sm.t, lane) + ssum * mb2;
+        const T msum = twmv<T, 32>(mW2, sm.t, lane, tm, sm) + ssum * mb2;
         sm.x[kH + lane] = msum;
         __syncwarp();
         // update MLP on [h_i, msum] (64 -> 32 tanh -> 32), residual
-        const T zu = d_tanh(wmv<T, 64>(uW1, sm.x, lane) + ub1);
+        const T zu = d_tanh(twmv<T, 64>(uW1, sm.x, lane, tm, sm) + ub1);
         if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
         sm.y[lane] = zu;
         __syncwarp();
-        const T hn = hi + (wmv<T, 32>(uW2, sm.y, lane) + ub2);
+        const T hn = hi + (twmv<T, 32>(uW2, sm.y, lane, tm, sm) + ub2);
         if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
         sm.t[lane] = hn;
         __syncwarp();
         if constexpr (!LAST) {
-            const T p = wmv<T, 32>(nW1h, sm.t, lane);
+            const T p = twmv<T, 32>(nW1h, sm.t, lane, tm, sm);
             if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
             push_rows(ws.pe + ((l + 1) & 1) * S * kH, p, gr, i, tm);
         } else {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
             // fitting: h^M -> dE/dh^M
             const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
-                                  lead ? ws.e_atom + i : nullptr, lane);
+                                  lead ? ws.e_atom + i : nullptr, tm, sm);
             msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, true, tm);
         }
         __syncwarp();
@@ -698,7 +775,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_bwd(DevModel<T> md, D
         sm.t[lane] = gather_in(Dn, ws, gr, i, tm, sm);
         __syncwarp();
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
-        const T dh = own + wmv<T, 32>(nW1hT, sm.t, lane);
+        const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
         msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, false, tm);
         __syncwarp();
@@ -726,13 +803,13 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed_bwd(DevModel<T> md,
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + lane];
         sm.t[lane] = gather_in(ws.d, ws, gr, i, tm, sm);
         __syncwarp();
-        const T dh = own + wmv<T, 32>(m0W1hT, sm.t, lane);
+        const T dh = own + twmv<T, 32>(m0W1hT, sm.t, lane, tm, sm);
         sm.x[lane] = dh;
         __syncwarp();
-        const T dz1 = wmv<T, 32>(eW2T, sm.x, lane) * (T(1) - z1 * z1);
+        const T dz1 = twmv<T, 32>(eW2T, sm.x, lane, tm, sm) * (T(1) - z1 * z1);
         sm.y[lane] = dz1;
         __syncwarp();
-        const T dd = wmv<T, 32>(eW1T, sm.y, lane);
+        const T dd = twmv<T, 32>(eW1T, sm.y, lane, tm, sm);
         sm.t[lane] = dd;
         __syncwarp();
         const int start = gr.row_start[i] + tm.w;
@@ -978,7 +1055,7 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
 
 static int force_grid(int n) {
     const int want = (n + kForceCTA / 32 - 1) / (kForceCTA / 32);
-    const int cap = num_sms() * 8;
+    const int cap = num_sms() * 16;
     return want < 1 ? 1 : (want < cap ? want : cap);
 }
 
