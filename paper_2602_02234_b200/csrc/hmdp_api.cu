@@ -39,6 +39,7 @@ template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t);
 cudaError_t net_configure();
+void launch_reduce_partials(const double*, int, double*, cudaStream_t);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
 
@@ -239,6 +240,9 @@ struct hmdp_ctx {
     // per-kernel timing (hmdp_profile): event k is recorded after kernel k
     bool prof = false;
     int pcount = 0;
+    // the device MD loop whose binning the cell lists currently hold (a primed
+    // MD chunk continues from it); any other binning clears it
+    const void* cells_owner = nullptr;
     std::vector<cudaEvent_t> pev;
     std::vector<std::string> pname;
 
@@ -409,6 +413,7 @@ struct hmdp_ctx {
                    const int* d_types = nullptr) {
         CellGrid cg = grid(box, rc, n);
         ensure_edges(static_cast<long long>(n) * cap);
+        cells_owner = nullptr;
         ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
         mark("memset_cells", st);
         launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
@@ -496,13 +501,15 @@ struct hmdp_md {
     int precision = HMDP_FP32;
     double dt = 0.001, box[3] = {0, 0, 0};
     DBuf x, v, f, m, types, energy;
+    DBuf xs, vs;          // completed-step snapshot (what hmdp_md_get returns)
+    bool primed = false;  // working (x, v) already carry the next step's opening kick
     int steps_per_graph = 1;
     std::map<int, cudaGraphExec_t> graphs;
     cudaStream_t graph_stream = nullptr;
     bool graph_prof = false;
     ~hmdp_md() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-        for (DBuf* b : {&x, &v, &f, &m, &types, &energy}) b->release();
+        for (DBuf* b : {&x, &v, &f, &m, &types, &energy, &xs, &vs}) b->release();
     }
 };
 
@@ -970,16 +977,20 @@ int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
 // Device MD loop
 // ---------------------------------------------------------------------------
 namespace {
-void md_enqueue_steps(hmdp_md* md, int steps, cudaStream_t st) {
-    // chunk = [kick+drift+bin] then per step [search, network..., force+kicks(+drift+bin)];
-    // the last step of the chunk closes with the second half kick only, so the
-    // state between chunks is a complete velocity-Verlet step.
+void md_enqueue_steps(hmdp_md* md, int steps, bool primed, cudaStream_t st) {
+    // Every step is [search, network..., force + closing kick + next step's
+    // opening kick + drift + binning]; the completed step's (x, v) go to the
+    // snapshot buffers.  Only the first chunk after hmdp_md_create starts with
+    // the opening kick + drift + binning kernel (velocity Verlet,
+    // integrators.cpp:32-47, split at the force evaluation).
     hmdp_ctx* ctx = md->ctx;
     const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
     MdFuse mf = ctx->zeroing(cg);
     mf.x = md->x.as<double>();
     mf.v = md->v.as<double>();
     mf.m = md->m.as<double>();
+    mf.xs = md->xs.as<double>();
+    mf.vs = md->vs.as<double>();
     mf.half = 0.5 * md->dt;
     mf.dt = md->dt;
     mf.cg = cg;
@@ -987,13 +998,15 @@ void md_enqueue_steps(hmdp_md* md, int steps, cudaStream_t st) {
     mf.cell_of = ctx->cell_of.as<int>();
     ctx->pcount = 0;
     ctx->mark("step_begin", st);
-    launch_vv_kick_drift_bin(md->n, mf, md->f.as<double>(), ctx->err.as<unsigned>(), st);
-    ctx->mark("vv_kick_drift_bin", st);
+    if (!primed) {
+        launch_vv_kick_drift_bin(md->n, mf, md->f.as<double>(), ctx->err.as<unsigned>(), st);
+        ctx->mark("vv_kick_drift_bin", st);
+    }
     const DevGraph gr = ctx->periodic_graph(md->n, md->types.as<int>());
     const long long slots = static_cast<long long>(md->n) * ctx->cap;
+    mf.mode = 2;
     for (int s = 0; s < steps; ++s) {
         ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st, md->types.as<int>());
-        mf.mode = s + 1 < steps ? 2 : 1;
         if (md->precision == HMDP_FP64)
             ctx->network<double>(gr, slots, md->f.as<double>(), nullptr, st, ctx->rev.as<int>(), mf);
         else
@@ -1026,6 +1039,8 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         md->m.ensure(n * sizeof(double));
         md->types.ensure(n * sizeof(int));
         md->energy.ensure(sizeof(double));
+        md->xs.ensure(3 * n * sizeof(double));
+        md->vs.ensure(3 * n * sizeof(double));
         cudaStream_t st = ctx->st();
         ck(cudaMemcpyAsync(md->x.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(md->v.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
@@ -1059,6 +1074,10 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         else
             ctx->work<float>(n, slots);
         ctx->grid(box, ctx->model.rc, n);
+        ck(cudaMemcpyAsync(md->xs.p, md->x.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st),
+           "D2D");
+        ck(cudaMemcpyAsync(md->vs.p, md->v.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st),
+           "D2D");
         ck(cudaStreamSynchronize(st), "sync");
         *out = md.release();
     });
@@ -1066,7 +1085,8 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
 
 namespace {
 cudaGraphExec_t md_graph(hmdp_md* md, int chunk, cudaStream_t st) {
-    auto it = md->graphs.find(chunk);
+    const int key = 2 * chunk + (md->primed ? 1 : 0);
+    auto it = md->graphs.find(key);
     if (it != md->graphs.end() && md->graph_stream == st && md->graph_prof == md->ctx->prof)
         return it->second;
     if (md->graph_stream != st || md->graph_prof != md->ctx->prof) {
@@ -1077,22 +1097,33 @@ cudaGraphExec_t md_graph(hmdp_md* md, int chunk, cudaStream_t st) {
     }
     cudaGraph_t graph;
     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-    md_enqueue_steps(md, chunk, st);
+    md_enqueue_steps(md, chunk, md->primed, st);
     ck(cudaStreamEndCapture(st, &graph), "end capture");
     cudaGraphExec_t exec;
     ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
     cudaGraphDestroy(graph);
-    md->graphs[chunk] = exec;
+    md->graphs[key] = exec;
     return exec;
 }
 void md_launch(hmdp_md* md, int steps) {
     hmdp_ctx* ctx = md->ctx;
     set_device(ctx);
     cudaStream_t st = ctx->st();
+    if (md->primed && ctx->cells_owner != md && steps > 0) {
+        // another operation re-binned the cell lists: bin this loop's (drifted)
+        // positions again before continuing
+        const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
+        ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
+           "memset cells");
+        launch_cell_bin(md->n, md->x.as<double>(), cg, ctx->cell_count.as<int>(),
+                        ctx->members.as<int>(), ctx->cell_of.as<int>(), ctx->err.as<unsigned>(), st);
+    }
     int left = steps;
     while (left > 0) {
         const int chunk = std::min(left, md->steps_per_graph);
         ck(cudaGraphLaunch(md_graph(md, chunk, st), st), "graph launch");
+        md->primed = true;
+        ctx->cells_owner = md;
         left -= chunk;
     }
 }
@@ -1119,10 +1150,19 @@ int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* e
         set_device(md->ctx);
         cudaStream_t st = md->ctx->st();
         const size_t b = 3 * static_cast<size_t>(md->n) * sizeof(double);
-        if (xyz) ck(cudaMemcpyAsync(xyz, md->x.p, b, cudaMemcpyDeviceToHost, st), "D2H");
-        if (vel) ck(cudaMemcpyAsync(vel, md->v.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (xyz) ck(cudaMemcpyAsync(xyz, md->xs.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (vel) ck(cudaMemcpyAsync(vel, md->vs.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         if (forces) ck(cudaMemcpyAsync(forces, md->f.p, b, cudaMemcpyDeviceToHost, st), "D2H");
-        if (epot) ck(cudaMemcpyAsync(epot, md->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        if (epot) {
+            // (E, W) of the last step: the force kernel leaves per-CTA partials in MD
+            if (md->primed) {
+                launch_reduce_partials(md->ctx->partial.as<double>(), md->n,
+                                       md->ctx->out.as<double>(), st);
+                ck(cudaGetLastError(), "reduce launch");
+            }
+            ck(cudaMemcpyAsync(epot, md->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st),
+               "D2H");
+        }
         ck(cudaStreamSynchronize(st), "sync");
     });
 }

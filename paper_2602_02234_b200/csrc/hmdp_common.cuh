@@ -94,7 +94,12 @@ __device__ __forceinline__ T edge_len(const double* dr3, T& x, T& y, T& z) {
 
 // FP64 helpers with explicit rounding (no FMA contraction) for the bit-exact
 // neighbour test: minimum_image (box.hpp:24-31) and norm2 (vec3.hpp:57-70).
+// d - L * nearbyint(d / L) (box.hpp:27).  For |d| <= L/2 the rounded quotient
+// has magnitude <= 0.5, which rounds (half to even) to zero: the result is d
+// itself (+ 0.0 reproduces the +0 the full expression gives for d = -0), so the
+// FP64 division is only paid by the pairs that actually wrap.
 __device__ __forceinline__ double min_image1(double d, double L) {
+    if (fabs(d) <= 0.5 * L) return __dadd_rn(d, 0.0);
     return __dsub_rn(d, __dmul_rn(L, rint(__ddiv_rn(d, L))));
 }
 __device__ __forceinline__ double norm2_rn(double x, double y, double z) {

@@ -128,6 +128,8 @@ struct CellGrid {
 //   mode 1: second half kick            v += F * (dt/2)/m
 //   mode 2: second half kick, then the next step's first half kick, drift and
 //           cell binning:  v += F*(dt/2)/m; v += F*(dt/2)/m; x += v*dt; bin(x)
+// The device MD loop runs every step in mode 2 (the opening kick of the next
+// step is fused into this one) and writes the completed step to (xs, vs).
 // (integrators.cpp:32-47, with the finite-force check of :12-18 on F).
 // zero_cells (embed kernel): cell counts to clear once the search consumed them.
 struct MdFuse {
@@ -141,6 +143,8 @@ struct MdFuse {
     int* members = nullptr;
     int* cell_of = nullptr;
     int n_cells_zero = 0;  // > 0: embed kernel zeroes cell_count[0..n)
+    double* xs = nullptr;  // nullable: completed-step snapshot (x, v after the
+    double* vs = nullptr;  // closing kick), what hmdp_md_get returns
 };
 
 }  // namespace hmdp

@@ -852,6 +852,9 @@ struct WarpPos {
 // CTA partials of (E, W, W_ab) in a fixed order, then the last CTA to finish
 // reduces all CTAs' partials in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void reduce_partials(const double* partial, unsigned nb, double* out,
+                                                double (*s_part)[12]);
+
 template <typename T>
 __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                                                      double* __restrict__ forces,
@@ -868,7 +871,8 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
     for (int q = 0; q < 11; ++q) acc[q] = 0.0;
     for (int i = wp.first; i < gr.n; i += wp.stride) {
         // MD state of atom i, loaded early (independent of the edge loads)
-        double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0;
+        double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0, ei = 0.0;
+        if (lane == 0) ei = ws.e_atom[i];
         if (mf.mode && lane == 0) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -919,7 +923,6 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
             forces[3 * i] = fx;
             forces[3 * i + 1] = fy;
             forces[3 * i + 2] = fz;
-            const double ei = ws.e_atom[i];
             if (per_atom) per_atom[i] = ei;
             acc[0] += ei;
             if (mf.mode) {
@@ -930,6 +933,10 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     double va = __dadd_rn(vv[a], __dmul_rn(f3[a], s));  // closing kick
+                    if (mf.vs) {  // completed step: the state hmdp_md_get returns
+                        mf.vs[3 * i + a] = va;
+                        mf.xs[3 * i + a] = xv[a];
+                    }
                     if (mf.mode == 2) {
                         va = __dadd_rn(va, __dmul_rn(f3[a], s));  // next step's opening kick
                         x3[a] = __dadd_rn(xv[a], __dmul_rn(va, mf.dt));
@@ -953,32 +960,49 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
         for (int q = 0; q < kForceCTA / 32; ++q) v += s_part[q][threadIdx.x];
         ws.partial[blockIdx.x * 16 + threadIdx.x] = v;
     }
+    // device MD: the (E, W) totals are reduced on demand (hmdp_md_get ->
+    // k_reduce_partials); a single evaluation reduces here, in the last CTA
+    if (mf.mode) return;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(ws.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
     if (s_last) {
         __threadfence();
-        double v[11];
-#pragma unroll
-        for (int q = 0; q < 11; ++q) v[q] = 0.0;
-        for (unsigned b = threadIdx.x; b < gridDim.x; b += kForceCTA)
-#pragma unroll
-            for (int q = 0; q < 11; ++q) v[q] += __ldcg(ws.partial + b * 16 + q);
-#pragma unroll
-        for (int q = 0; q < 11; ++q) v[q] = warp_sum(v[q]);
-        __syncthreads();
-        if (lane == 0)
-#pragma unroll
-            for (int q = 0; q < 11; ++q) s_part[wc][q] = v[q];
-        __syncthreads();
-        if (threadIdx.x < 11) {
-            double tot = 0.0;
-            for (int q = 0; q < kForceCTA / 32; ++q) tot += s_part[q][threadIdx.x];
-            out[threadIdx.x] = tot;
-        }
+        reduce_partials(ws.partial, gridDim.x, out, s_part);
         if (threadIdx.x == 0) *ws.ticket = 0u;  // re-arm for the next launch / graph replay
     }
+}
+
+// Fixed-order sum of nb CTA partials (E, W, W_ab) into out[0..10], by one CTA of
+// kForceCTA threads.
+__device__ __forceinline__ void reduce_partials(const double* partial, unsigned nb, double* out,
+                                                double (*s_part)[12]) {
+    const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+    double v[11];
+#pragma unroll
+    for (int q = 0; q < 11; ++q) v[q] = 0.0;
+    for (unsigned b = threadIdx.x; b < nb; b += kForceCTA)
+#pragma unroll
+        for (int q = 0; q < 11; ++q) v[q] += __ldcg(partial + b * 16 + q);
+#pragma unroll
+    for (int q = 0; q < 11; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 11; ++q) s_part[wc][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 11) {
+        double tot = 0.0;
+        for (int q = 0; q < kForceCTA / 32; ++q) tot += s_part[q][threadIdx.x];
+        out[threadIdx.x] = tot;
+    }
+}
+
+__global__ __launch_bounds__(kForceCTA) void k_reduce_partials(const double* partial, int nb,
+                                                               double* out) {
+    __shared__ double s_part[kForceCTA / 32][12];
+    reduce_partials(partial, nb, out, s_part);
 }
 
 // ---------------------------------------------------------------------------
@@ -1053,7 +1077,7 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
     launch_pdl(kernel, dim3(sh.grid), dim3(32 * sh.warps), smem, st, args...);
 }
 
-static int force_grid(int n) {
+int force_grid(int n) {
     const int want = (n + kForceCTA / 32 - 1) / (kForceCTA / 32);
     const int cap = num_sms() * 16;
     return want < 1 ? 1 : (want < cap ? want : cap);
@@ -1156,6 +1180,11 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
                per_atom, out, mf);
     mk("force", st);
     return launches + 1;
+}
+
+// Device MD: (E, W, W_ab) of the last step from the force kernel's CTA partials.
+void launch_reduce_partials(const double* partial, int n, double* out, cudaStream_t st) {
+    k_reduce_partials<<<1, kForceCTA, 0, st>>>(partial, force_grid(n), out);
 }
 
 // One phase of a domain-decomposed evaluation (the caller exchanges halo rows
