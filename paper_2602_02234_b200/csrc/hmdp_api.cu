@@ -39,6 +39,7 @@ template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t);
 cudaError_t net_configure();
+cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
@@ -308,7 +309,7 @@ struct hmdp_ctx {
         cursor.ensure(na * sizeof(int));
         e_atom.ensure(na * sizeof(double));
         forces.ensure(na * 3 * sizeof(double));
-        const size_t nb = std::max<size_t>(na, 4096);  // >= atom_grid(n) CTAs
+        const size_t nb = std::max<size_t>(na, 4096);  // >= force_grid(n) CTAs
         partial.ensure(nb * 16 * sizeof(double));
         if (!ticket.p) {
             ticket.ensure(sizeof(unsigned));
@@ -616,6 +617,7 @@ int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, i
         ck(cudaSetDevice(device), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
         ck(net_configure(), "kernel smem configuration");
+        ck(nbr_configure(), "kernel smem configuration");
         if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
         if (has_model) {
             ctx->wf.upload(ctx->model, ctx->stream);

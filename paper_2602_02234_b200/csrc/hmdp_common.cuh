@@ -210,89 +210,84 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
 }
 
 // ---------------------------------------------------------------------------
-// Neighbour search body for one 128-thread group (named barrier `bar`).
-// The deduplicated 27 neighbouring cells' member lists form one candidate index
-// space spread over the group (about two candidates per thread at the paper
-// densities); every j with FP64 minimum-image |dr|^2 <= rc^2
-// (neighborlist.cpp:91-93) survives; survivors are ranked ascending (the
-// reference's sorted full pair list, neighborlist.cpp:104-111) and written with
-// their FP64 edge_dr (inference.cpp:474-485) and neighbour type.
+// Neighbour search body, one warp per atom.  The deduplicated 27 neighbouring
+// cells' member lists form one candidate index space enumerated 32 lanes at a
+// time; every j with FP64 minimum-image |dr|^2 <= rc^2 (neighborlist.cpp:91-93,
+// box.hpp:27, no FMA contraction) survives a ballot compaction into the warp's
+// shared list; survivors are ranked ascending (the reference's sorted full pair
+// list, neighborlist.cpp:104-111) and written with their FP64 edge_dr
+// (inference.cpp:474-485) and neighbour type.
 // ---------------------------------------------------------------------------
 struct NbrSmem {
-    int cand[kCandMax];
-    int cell[32];
-    int off[33];
-    int wcnt[4];
+    int cand[kCandMax];  // this warp's surviving candidates
+    int cnt;
 };
 
-__device__ __forceinline__ void group_bar(int bar) {
-    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(kAT) : "memory");
-}
-
-__device__ __forceinline__ void nbr_search_atom(int i, const double* pos,
-                                                const CellGrid& cg, const int* cell_count,
-                                                const int* members,
+// G warps (a "team", named barrier `bar`) search one atom: warp w takes the
+// candidate blocks q in [32 (w + G k), 32 (w + G k) + 32); each warp compacts its
+// survivors into its own list, and ranks them against the whole team's lists.
+template <int G>
+__device__ __forceinline__ void nbr_search_team(int i, const double* pos, const CellGrid& cg,
+                                                const int* cell_count, const int* members,
                                                 const int* cell_of, double range2, int cap,
                                                 int* __restrict__ nnei, int* __restrict__ row_start,
                                                 int* __restrict__ nbr, double* __restrict__ dr,
-                                                const int* __restrict__ types, int* __restrict__ ety,
-                                                unsigned* err, NbrSmem& sm, int t, int bar) {
-    const int lane = t & 31, w = t >> 5;
+                                                const int* __restrict__ types,
+                                                int* __restrict__ ety, unsigned* err,
+                                                NbrSmem* team_sm, int w, int lane, int bar) {
+    NbrSmem& sm = team_sm[w];
     const double L0 = cg.L[0], L1 = cg.L[1], L2 = cg.L[2];
     const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
-    if (w == 0) {
-        const int ci = cell_of[i];
-        const int cx = ci % cg.nc[0], cy = (ci / cg.nc[0]) % cg.nc[1], cz = ci / (cg.nc[0] * cg.nc[1]);
-        int nid = -1;
-        if (lane < 27) {
-            const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
-            const int x = ((cx + dx) % cg.nc[0] + cg.nc[0]) % cg.nc[0];
-            const int y = ((cy + dy) % cg.nc[1] + cg.nc[1]) % cg.nc[1];
-            const int z = ((cz + dz) % cg.nc[2] + cg.nc[2]) % cg.nc[2];
-            nid = (z * cg.nc[1] + y) * cg.nc[0] + x;
-        }
-        bool unique = lane < 27;
-        for (int q = 0; q < 27; ++q) {
-            const int other = __shfl_sync(FULL_MASK, nid, q);
-            if (q < lane && other == nid) unique = false;
-        }
-        int cnt = 0;
-        if (unique) {
-            cnt = cell_count[nid];
-            cnt = cnt < cg.ccap ? cnt : cg.ccap;
-        }
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL_MASK, incl, o);
-            if (lane >= o) incl += v;
-        }
-        sm.cell[lane] = nid;
-        sm.off[lane + 1] = incl;
-        if (lane == 0) sm.off[0] = 0;
+    const int ci = cell_of[i];
+    const int cx = ci % cg.nc[0], cy = (ci / cg.nc[0]) % cg.nc[1], cz = ci / (cg.nc[0] * cg.nc[1]);
+    int nid = -1;
+    if (lane < 27) {
+        const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+        const int x = ((cx + dx) % cg.nc[0] + cg.nc[0]) % cg.nc[0];
+        const int y = ((cy + dy) % cg.nc[1] + cg.nc[1]) % cg.nc[1];
+        const int z = ((cz + dz) % cg.nc[2] + cg.nc[2]) % cg.nc[2];
+        nid = (z * cg.nc[1] + y) * cg.nc[0] + x;
     }
-    group_bar(bar);
-    const int ncand = sm.off[27];
+    bool unique = lane < 27;
+    for (int q = 0; q < 27; ++q) {
+        const int other = __shfl_sync(FULL_MASK, nid, q);
+        if (q < lane && other == nid) unique = false;
+    }
+    int cnt = 0;
+    if (unique) {
+        cnt = cell_count[nid];
+        cnt = cnt < cg.ccap ? cnt : cg.ccap;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int off = incl - cnt;  // exclusive offset of lane's cell
+    const int base = nid * cg.ccap;
+    const int ncand = __shfl_sync(FULL_MASK, incl, 31);
+    constexpr int U = G >= 4 ? 2 : 4;  // candidate blocks per warp per pass
     int total = 0;
-    for (int q0 = 0; q0 < ncand; q0 += 2 * kAT) {
-        int jr[2];
-        bool pass[2];
+    for (int b0 = w; 32 * b0 < ncand; b0 += G * U) {
+        int jr[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {  // candidate indices: independent loads
-            const int q = q0 + u * kAT + t;
-            jr[u] = -1;
-            if (q < ncand) {
-                int lo = 0, hi = 26;  // cell slot owning candidate q
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (sm.off[mid] <= q) lo = mid;
-                    else hi = mid - 1;
-                }
-                jr[u] = members[sm.cell[lo] * cg.ccap + (q - sm.off[lo])];
+        for (int u = 0; u < U; ++u) {  // candidate q -> (cell slot, member): independent loads
+            const int q = 32 * (b0 + G * u) + lane;
+            int lo = 0;  // largest cell slot whose offset <= q (always a non-empty cell)
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int mid = lo + step;
+                const int om = __shfl_sync(FULL_MASK, off, mid & 31);
+                if (mid < 27 && om <= q) lo = mid;
             }
+            const int ob = __shfl_sync(FULL_MASK, off, lo);
+            const int bb = __shfl_sync(FULL_MASK, base, lo);
+            jr[u] = q < ncand ? members[bb + (q - ob)] : -1;
         }
+        bool pass[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {  // FP64 pair test, no FMA contraction
+        for (int u = 0; u < U; ++u) {  // FP64 pair test, no FMA contraction
             pass[u] = false;
             const int j = jr[u];
             if (j >= 0 && j != i) {
@@ -303,29 +298,36 @@ __device__ __forceinline__ void nbr_search_atom(int i, const double* pos,
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {  // group-wide compaction
+        for (int u = 0; u < U; ++u) {  // warp compaction
             const unsigned bal = __ballot_sync(FULL_MASK, pass[u]);
-            if (lane == 0) sm.wcnt[w] = __popc(bal);
-            group_bar(bar);
-            int off = total;
-            for (int q = 0; q < w; ++q) off += sm.wcnt[q];
             if (pass[u]) {
-                const int idx = off + __popc(bal & ((1u << lane) - 1u));
+                const int idx = total + __popc(bal & ((1u << lane) - 1u));
                 if (idx < kCandMax) sm.cand[idx] = jr[u];
             }
-            total += ((sm.wcnt[0] + sm.wcnt[1]) + sm.wcnt[2]) + sm.wcnt[3];
-            group_bar(bar);
+            total += __popc(bal);
         }
     }
-    int m = total;
-    if (m > cap || m > kCandMax) {
-        if (t == 0) atomicOr(err, kErrNbrOverflow);
-        m = cap < kCandMax ? cap : kCandMax;
-    }
-    for (int q = t; q < m; q += kAT) {
+    if (lane == 0) sm.cnt = total;
+    if constexpr (G > 1)
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");
+    else
+        __syncwarp();
+    int m = 0;
+#pragma unroll
+    for (int q = 0; q < G; ++q) m += team_sm[q].cnt;
+    const bool over = m > cap || total > kCandMax;
+    if (over && w == 0 && lane == 0) atomicOr(err, kErrNbrOverflow);
+    const int mine = total < kCandMax ? total : kCandMax;
+    for (int q = lane; q < mine; q += 32) {
         const int v = sm.cand[q];
         int rank = 0;
-        for (int p = 0; p < m; ++p) rank += sm.cand[p] < v;
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+            const NbrSmem& o = team_sm[t];
+            const int c = o.cnt < kCandMax ? o.cnt : kCandMax;
+            for (int p = 0; p < c; ++p) rank += o.cand[p] < v;
+        }
+        if (rank >= cap) continue;  // overflow: flagged above, the caller re-runs
         const long long slot = static_cast<long long>(i) * cap + rank;
         nbr[slot] = v;
         if (ety) ety[slot] = types[v];
@@ -333,11 +335,15 @@ __device__ __forceinline__ void nbr_search_atom(int i, const double* pos,
         dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
         dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
     }
-    if (t == 0) {
-        nnei[i] = m;
+    if (w == 0 && lane == 0) {
+        nnei[i] = m < cap ? m : cap;
         row_start[i] = i * cap;
     }
-    group_bar(bar);
+    // the lists are reused by the team's next atom
+    if constexpr (G > 1)
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");
+    else
+        __syncwarp();
 }
 
 // Opening of a device-MD chunk for atom i: first half kick + drift + binning

@@ -22,19 +22,26 @@ __global__ void k_cell_bin(int n, const double* __restrict__ pos, CellGrid cg,
     bin_atom(i, pos + 3 * i, cg, cell_count, members, cell_of, err);
 }
 
-// One 128-thread CTA per atom (grid-stride over atoms).
-__global__ __launch_bounds__(kAT) void k_nbr_search(
+// G warps per atom (G = 4 / 2 / 1 by system size, as the network kernels), 16
+// warps per CTA, grid-stride over atoms.
+constexpr int kSearchCTA = 512;
+template <int G>
+__global__ __launch_bounds__(kSearchCTA) void k_nbr_search(
     int n, const double* __restrict__ pos, CellGrid cg, const int* __restrict__ cell_count,
     const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
     int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
     double* __restrict__ dr, const int* __restrict__ types, int* __restrict__ ety,
     unsigned* err) {
-    __shared__ NbrSmem sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    NbrSmem* sm = reinterpret_cast<NbrSmem*>(smem_raw);
     pdl_launch_dependents();
     pdl_wait();
-    for (int i = blockIdx.x; i < n; i += gridDim.x)
-        nbr_search_atom(i, pos, cg, cell_count, members, cell_of, range2, cap, nnei, row_start, nbr,
-                        dr, types, ety, err, sm, threadIdx.x, 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tpc = (blockDim.x >> 5) / G, team = warp / G, w = warp % G;
+    const int nt = gridDim.x * tpc;
+    for (int i = blockIdx.x * tpc + team; i < n; i += nt)
+        nbr_search_team<G>(i, pos, cg, cell_count, members, cell_of, range2, cap, nnei, row_start,
+                           nbr, dr, types, ety, err, sm + team * G, w, lane, 1 + team);
 }
 
 // CSR offsets -> (row_start, nnei)
@@ -169,11 +176,6 @@ int num_sms() {
     }
     return sms_cached;
 }
-int atom_grid(int n) {
-    // grid-stride over atoms: enough CTAs to fill every SM several times
-    const int g = num_sms() * 12;
-    return n < g ? (n > 0 ? n : 1) : g;
-}
 
 void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_count, int* members,
                      int* cell_of, unsigned* err, cudaStream_t st) {
@@ -183,8 +185,32 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
                        unsigned* err, cudaStream_t st) {
-    launch_pdl(k_nbr_search, dim3(atom_grid(n)), dim3(kAT), 0, st, n, pos, cg, cell_count, members,
-               cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety, err);
+    const int sms = num_sms();
+    const int G = (4 * n <= 16 * sms) ? 4 : (2 * n <= 16 * sms ? 2 : 1);
+    // warps per CTA: enough teams per CTA that the atoms fill every SM
+    int teams = (n + sms - 1) / sms;
+    teams = teams < 1 ? 1 : (teams > 16 / G ? 16 / G : teams);
+    const int threads = 32 * G * teams;
+    int grid = (n + teams - 1) / teams;
+    grid = grid < 8 * sms ? grid : 8 * sms;
+    const size_t smem = static_cast<size_t>(G * teams) * sizeof(NbrSmem);
+    auto args = [&](auto kernel) {
+        launch_pdl(kernel, dim3(grid > 0 ? grid : 1), dim3(threads), smem, st, n, pos, cg,
+                   cell_count, members, cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety,
+                   err);
+    };
+    if (G == 4) args(k_nbr_search<4>);
+    else if (G == 2) args(k_nbr_search<2>);
+    else args(k_nbr_search<1>);
+}
+cudaError_t nbr_configure() {
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {cudaFuncSetAttribute(k_nbr_search<1>, a, 16 * sizeof(NbrSmem)),
+                          cudaFuncSetAttribute(k_nbr_search<2>, a, 16 * sizeof(NbrSmem)),
+                          cudaFuncSetAttribute(k_nbr_search<4>, a, 16 * sizeof(NbrSmem))})
+        if (r != cudaSuccess) e = r;
+    return e;
 }
 void launch_edge_meta(int ne, const int* nbr, const int* types, int* ety, const int* in_edge,
                       int* inv_pos, cudaStream_t st) {
