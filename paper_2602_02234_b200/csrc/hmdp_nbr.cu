@@ -166,6 +166,8 @@ __global__ void k_vv_kick_drift_bin(int n, MdFuse mf, const double* __restrict__
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+int team_override();  // hmdp_net.cu
+
 int num_sms() {
     static thread_local int dev_cached = -1, sms_cached = 148;
     int dev = 0;
@@ -186,7 +188,8 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
                        unsigned* err, cudaStream_t st) {
     const int sms = num_sms();
-    const int G = (4 * n <= 16 * sms) ? 4 : (2 * n <= 16 * sms ? 2 : 1);
+    int G = (4 * n <= 16 * sms) ? 4 : (2 * n <= 16 * sms ? 2 : 1);
+    if (team_override()) G = team_override();
     // warps per CTA: enough teams per CTA that the atoms fill every SM
     int teams = (n + sms - 1) / sms;
     teams = teams < 1 ? 1 : (teams > 16 / G ? 16 / G : teams);

@@ -44,6 +44,8 @@
 //   k_embed_bwd    embedding + descriptor adjoint             :355-370
 //   k_force        force / virial (gather form) + E, W sums   :288-298, :372-387
 //                  [+ velocity Verlet tail, src/integrators.cpp:32-47]
+#include <cstdlib>
+
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -1057,9 +1059,18 @@ static int staged_elems(Phase p) {
 struct NetShape {
     int G, warps, grid;
 };
+int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments)
+    static const int v = [] {
+        const char* e = std::getenv("HMDP_TEAM");
+        const int t = e ? std::atoi(e) : 0;
+        return (t == 1 || t == 2 || t == 4) ? t : 0;
+    }();
+    return v;
+}
 static NetShape net_shape(int n) {
     const int sms = num_sms();
-    const int G = (4 * n <= kMaxWarps * sms) ? 4 : (2 * n <= kMaxWarps * sms ? 2 : 1);
+    int G = (4 * n <= kMaxWarps * sms) ? 4 : (2 * n <= kMaxWarps * sms ? 2 : 1);
+    if (team_override()) G = team_override();
     const int max_teams = kMaxWarps / G;
     int teams = (n + sms - 1) / sms;
     teams = teams < 1 ? 1 : (teams > max_teams ? max_teams : teams);
