@@ -11,6 +11,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -29,6 +30,13 @@ PROFILE_NAME = {
 
 def short(name):
     return name.replace("void ", "").split("(")[0].replace("hmdp::", "")
+
+
+def profile_name(name):
+    """kernel symbol (team-size template argument dropped) -> hmdp_profile marker"""
+    base = re.sub(r"<([124])>$", "", name)  # k_nbr_search<G>
+    base = re.sub(r"<(float|double), [124]", r"<\1", base)  # k_*<T, G, ...>
+    return PROFILE_NAME.get(base)
 
 
 def launches(path):
@@ -96,7 +104,8 @@ def main():
     recs = raw(rep)
     traffic = {}
     with open(os.path.join(out, "kernels.md"), "w") as f:
-        f.write(f"# ncu --set full ({model} {system}), key metrics per kernel\n\n")
+        f.write(f"# ncu --set full --cache-control none ({model} {system}), key metrics per "
+                f"kernel (one MD step inside the graph loop, L2 state as in the loop)\n\n")
         for d in recs:
             name = short(d.get("Kernel Name", ("?", ""))[0])
             f.write(f"## {name}\n\n| metric | value | unit |\n|---|---|---|\n")
@@ -105,8 +114,8 @@ def main():
                     f.write(f"| {k} | {d[k][0]} | {d[k][1]} |\n")
             f.write("\n")
             rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
-            if rd is not None and wr is not None and name in PROFILE_NAME:
-                traffic[PROFILE_NAME[name]] = rd + wr
+            if rd is not None and wr is not None and profile_name(name):
+                traffic[profile_name(name)] = rd + wr
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     allt = json.load(open(tpath)) if os.path.exists(tpath) else {}
     allt.setdefault(model, {})[system] = traffic
