@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+    common += os.environ.get("HMDP_NVCC_DEFS", "").split()  # tuning experiments, e.g. -DX=2
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".", "_") + ".o")
         cmd = [nvcc(), *common, *ARCH, "-lineinfo", "-c", os.path.join(CSRC, src), "-o", obj]

@@ -53,6 +53,12 @@ namespace hmdp {
 int num_sms();  // hmdp_nbr.cu
 
 constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
+// Resident CTAs per SM the register budget is sized for: 2 (64 registers) for the
+// 1-warp teams of large systems — more atoms in flight; 1 (128 registers) for
+// the 2/4-warp teams of small systems, whose chains would spill at 64 (measured:
+// DPA2 2PTC +11 %, DPA3 2PTC +2 %, DPA3 1YRF -33 % if forced to 2).
+template <int G>
+constexpr int kNetMinCTAs = G == 1 ? 2 : 1;
 constexpr int kForceCTA = 128;  // small CTAs: every SM gets atoms in small systems
 // edges per unrolled batch (row loads in flight per lane; fewer for FP64 registers)
 template <typename T>
@@ -358,7 +364,7 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // edge, which is the in-edge array of the symmetric graph (in_edge == rev).
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool FUSE_FIT>
-__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -622,7 +628,7 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool LAST>
-__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_fwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -748,7 +754,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_fwd(DevModel<T> md, D
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
 template <typename T, int G>
-__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -786,7 +792,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, 1) void k_msg_bwd(DevModel<T> md, D
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T, int G>
-__global__ __launch_bounds__(kMaxWarps * 32, 1) void k_embed_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
