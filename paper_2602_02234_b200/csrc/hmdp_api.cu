@@ -172,6 +172,69 @@ struct WeightSet {
             order.push_back(&m.update[l]);
         }
         for (size_t q = 0; q < order.size(); ++q) push_mlp(*order[q], q == 0 ? kH : 0);
+        // Per-kernel shared-memory images (hmdp_net.cu Stage order, rows padded by
+        // 16 bytes): mat(mlp q, array a, rows, cols, leading dimension)
+        enum { W1 = 0, W1T = 1, W2 = 3, W2T = 4 };
+        const int padc = 16 / static_cast<int>(sizeof(T));
+        auto mat = [&](size_t q, int a, int rows, int cols, int ld) {
+            const size_t src = offs[6 * q + a];
+            for (int r = 0; r < rows; ++r) {
+                for (int c = 0; c < cols; ++c) {
+                    const T v = host[src + static_cast<size_t>(r) * ld + c];
+                    host.push_back(v);
+                }
+                for (int c = 0; c < padc; ++c) host.push_back(T(0));
+            }
+        };
+        const size_t E = 0, F = 1;
+        auto Mq = [](size_t l) { return 2 + 2 * l; };
+        auto Uq = [](size_t l) { return 3 + 2 * l; };
+        const size_t M = m.message.size();
+        const int kin = kH + kK;
+        std::vector<size_t> img;  // image start offsets, in the order below
+        auto begin = [&] {
+            align();
+            img.push_back(host.size());
+        };
+        begin();  // embedding / embed_fit
+        mat(E, W1, 32, 32, 32);
+        mat(E, W2, 32, 32, 32);
+        if (M == 0) {
+            mat(F, W1, 32, 32, 32);
+            mat(F, W1T, 32, 32, 32);
+            mat(E, W2T, 32, 32, 32);
+            mat(E, W1T, 32, 32, 32);
+        } else {
+            mat(Mq(0), W1, 32, 32, kin);
+        }
+        for (size_t l = 0; l < M; ++l) {  // message layer forward
+            begin();
+            mat(Mq(l), W2, 32, 32, 32);
+            mat(Uq(l), W1, 32, 64, 64);
+            mat(Uq(l), W2, 32, 32, 32);
+            if (l + 1 == M) {
+                mat(F, W1, 32, 32, 32);
+                mat(F, W1T, 32, 32, 32);
+                mat(Uq(l), W2T, 32, 32, 32);
+                mat(Uq(l), W1T, 64, 32, 32);
+                mat(Mq(l), W2T, 32, 32, 32);
+            } else {
+                mat(Mq(l + 1), W1, 32, 32, kin);
+            }
+        }
+        for (size_t l = 0; l + 1 < M; ++l) {  // message layer backward
+            begin();
+            mat(Mq(l + 1), W1T, 32, 32, 32);
+            mat(Uq(l), W2T, 32, 32, 32);
+            mat(Uq(l), W1T, 64, 32, 32);
+            mat(Mq(l), W2T, 32, 32, 32);
+        }
+        if (M > 0) {  // embedding backward
+            begin();
+            mat(Mq(0), W1T, 32, 32, 32);
+            mat(E, W2T, 32, 32, 32);
+            mat(E, W1T, 32, 32, 32);
+        }
         align();
         buf.ensure(host.size() * sizeof(T));
         ck(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, st),
@@ -196,6 +259,11 @@ struct WeightSet {
             dev.msg[l] = next_mlp();
             dev.upd[l] = next_mlp();
         }
+        size_t k = 0;
+        dev.img_embed = base + img[k++];
+        for (size_t l = 0; l < M; ++l) dev.img_fwd[l] = base + img[k++];
+        for (size_t l = 0; l + 1 < M; ++l) dev.img_bwd[l] = base + img[k++];
+        dev.img_embed_bwd = M > 0 ? base + img[k++] : nullptr;
         for (int k = 0; k < kK; ++k) dev.mu[k] = static_cast<T>(m.centers[k]);
         const T width = static_cast<T>(m.width);
         dev.rc = static_cast<T>(m.rc);
@@ -444,6 +512,7 @@ struct hmdp_ctx {
         gr.n = n;
         gr.n_active = n;
         gr.sym = 1;
+        gr.ell = cap;
         gr.row_start = row_start.as<int>();
         gr.nnei = nnei.as<int>();
         gr.nbr = nbr.as<int>();

@@ -43,6 +43,15 @@ struct DevModel {
     T invw2;    // T(1)/(width*width)        (inference.cpp:174)
     int n_types;
     int n_msg;
+    // Shared-memory images of the matrices each network kernel stages, laid out
+    // exactly as in shared memory (rows padded by 16 bytes), one bulk copy each
+    // (hmdp_net.cu, Smem::load): embedding (or embed_fit when n_msg == 0), message
+    // layer forward (the fused last-layer layout at n_msg - 1), message layer
+    // backward (l < n_msg - 1), embedding backward.
+    const T* img_embed;
+    const T* img_fwd[kMaxMsg];
+    const T* img_bwd[kMaxMsg];
+    const T* img_embed_bwd;
 };
 
 // Directed edge graph of one evaluation.  Out-edges of atom i occupy slots
@@ -62,6 +71,7 @@ struct DevGraph {
     int n;
     int n_active;  // atoms [0, n_active) run the network; the rest are halo ghosts
     int sym;       // 1: in-edge array aliases the out-slots (rev), see above
+    int ell;       // > 0: ELL rows, row_start[i] = i * ell (periodic path); 0: general CSR
     const int* row_start;
     const int* nnei;
     const int* nbr;

@@ -52,6 +52,24 @@ namespace hmdp {
 
 int num_sms();  // hmdp_nbr.cu
 
+// Dev-only stage timing (build with HMDP_NVCC_DEFS=-DHMDP_TPROBE): lane 0 of every
+// warp adds the clock64 cycles spent between consecutive TP(k) marks.
+#ifdef HMDP_TPROBE
+__device__ unsigned long long g_tprobe[32];
+#define TP_START long long tp_last_ = clock64()
+#define TP(k)                                                       \
+    do {                                                            \
+        if ((threadIdx.x & 31) == 0) {                              \
+            const long long t_ = clock64();                         \
+            atomicAdd(&g_tprobe[k], (unsigned long long)(t_ - tp_last_)); \
+            tp_last_ = t_;                                          \
+        }                                                           \
+    } while (0)
+#else
+#define TP_START
+#define TP(k)
+#endif
+
 constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
 // Resident CTAs per SM the register budget is sized for: 2 (64 registers) for the
 // 1-warp teams of large systems — more atoms in flight; 1 (128 registers) for
@@ -89,32 +107,54 @@ struct WarpSmem {
 };
 
 // Bump allocator over the dynamic shared memory: staged matrices, then the
-// warps' scratch.  Matrices are copied with cp.async (16 bytes per request, no
-// register round trip), so every request of every matrix is in flight at once;
-// wait() completes them (followed by the kernel's __syncthreads).
+// warps' scratch.  view() only assigns the layout; load() fills it with ONE bulk
+// copy (TMA engine, cp.async.bulk) of the kernel's pre-laid-out weight image
+// (DevModel::img_*, built at upload in exactly this order), completed on an
+// mbarrier — no per-thread copy loop.
 template <typename T>
 struct Smem {
+    T* base;
     T* cur;
-    // rows x cols block of src (leading dimension src_ld), copied by the whole
-    // CTA into rows of stride pad_ld(cols); src rows must be 16-byte aligned
+    __device__ explicit Smem(T* b) : base(b), cur(b) {}
     template <int R, int C>
-    __device__ const T* mat(const T* src, int src_ld) {
+    __device__ const T* view() {
         T* dst = cur;
-        constexpr int V = 16 / sizeof(T);  // elements per request
-        constexpr int RV = C / V;          // requests per row
-        constexpr int ld = pad_ld<T>(C);
-        static_assert(C % V == 0, "row not a multiple of 16 bytes");
-        for (int q = threadIdx.x; q < R * RV; q += blockDim.x) {
-            const int r = q / RV, v = q % RV;
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + r * ld + v * V));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
-                         "l"(src + static_cast<long long>(r) * src_ld + v * V)
-                         : "memory");
-        }
-        cur += R * ld;
+        cur += R * pad_ld<T>(C);
         return dst;
     }
-    __device__ static void wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+    // thread 0: arm the mbarrier and issue the copy; callers then __syncthreads()
+    // (publishes the mbarrier init) and wait()
+    __device__ void load(const T* img, unsigned long long* mbar) const {
+        if (threadIdx.x != 0) return;
+        const unsigned bytes = static_cast<unsigned>((cur - base) * sizeof(T));
+        const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                     : "memory");
+        constexpr unsigned kChunk = 32768;
+        for (unsigned off = 0; off < bytes; off += kChunk) {
+            const unsigned n = bytes - off < kChunk ? bytes - off : kChunk;
+            const unsigned dst = static_cast<unsigned>(
+                __cvta_generic_to_shared(reinterpret_cast<char*>(base) + off));
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(dst),
+                "l"(reinterpret_cast<const char*>(img) + off), "r"(n), "r"(mb)
+                : "memory");
+        }
+    }
+    __device__ static void wait(unsigned long long* mbar) {
+        const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+        unsigned done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(mb)
+                : "memory");
+    }
     __device__ WarpSmem<T>& warp_scratch() const {
         const size_t a = (reinterpret_cast<size_t>(cur) + 15) & ~size_t(15);
         return reinterpret_cast<WarpSmem<T>*>(a)[threadIdx.x >> 5];
@@ -369,18 +409,20 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
                                                              MdFuse mf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
-    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
-    const T* eW1 = sg.template mat<32, 32>(md.embed.W1, 32);
-    const T* eW2 = sg.template mat<32, 32>(md.embed.W2, 32);
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
+    const T* eW1 = sg.template view<32, 32>();
+    const T* eW2 = sg.template view<32, 32>();
     const T *W1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *eW2T = nullptr, *eW1T = nullptr;
     if constexpr (FUSE_FIT) {
-        fW1 = sg.template mat<32, 32>(md.fit.W1, 32);
-        fW1T = sg.template mat<32, 32>(md.fit.W1T, 32);
-        eW2T = sg.template mat<32, 32>(md.embed.W2T, 32);
-        eW1T = sg.template mat<32, 32>(md.embed.W1T, 32);
-    } else {
-        W1h = sg.template mat<32, 32>(md.msg[0].W1, kInMsg);
+        fW1 = sg.template view<32, 32>();
+        fW1T = sg.template view<32, 32>();
+        eW2T = sg.template view<32, 32>();
+        eW1T = sg.template view<32, 32>();
+} else {
+        W1h = sg.template view<32, 32>();
     }
+    sg.load(md.img_embed, &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
     const int lane = tm.lane;
@@ -389,8 +431,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
     const T fb1 = FUSE_FIT ? md.fit.b1[lane] : T(0), fw2 = FUSE_FIT ? md.fit.W2[lane] : T(0);
     const T fb2 = FUSE_FIT ? md.fit.b2[0] : T(0);
     const int nd = md.n_types * kK;
-    sg.wait();
-    __syncthreads();
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
     pdl_wait();
     // this step's neighbour search is complete: clear the cell counts for the
     // binning fused into the force kernel (device MD) / keep the zero invariant
@@ -478,6 +520,10 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
             __syncwarp();
         }
         desc = tm.sum(desc, sm);
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
         sm.x[lane] = lane < nd ? desc : T(0);
         if (lead && lane < nd) ws.desc[static_cast<long long>(i) * 32 + lane] = desc;
         __syncwarp();
@@ -526,19 +572,110 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
         }
         __syncwarp();
     }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
+
+// ---------------------------------------------------------------------------
+// Atom prologue.  On the periodic (ELL) graph atom i's slots are
+// [i*ell, i*ell + ell), so a warp can issue its first batch of edge loads before
+// the neighbour count arrives — every per-atom kernel then waits for ONE memory
+// round trip before computing, instead of count -> rows -> ... chains.  Loads past
+// the count read valid (ELL padding) memory and are never used.
+// ---------------------------------------------------------------------------
+template <int G>
+struct AtomRow {
+    long long e0;  // this warp's first slot: local edge k is e0 + G k
+    int room;      // local slots addressable before the count is known
+    int cnt;       // neighbour count (valid after finish())
+    const int* nnei;
+    int i;
+    __device__ __forceinline__ AtomRow(const DevGraph& gr, int i_, const Team<G>& tm)
+        : nnei(gr.nnei), i(i_) {
+        if (gr.ell) {
+            e0 = static_cast<long long>(i) * gr.ell + tm.w;
+            room = tm.local(gr.ell);
+            cnt = -1;
+        } else {
+            e0 = gr.row_start[i] + tm.w;
+            cnt = gr.nnei[i];
+            room = tm.local(cnt);
+        }
+    }
+    __device__ __forceinline__ int finish(const Team<G>& tm) {
+        if (cnt < 0) cnt = nnei[i];
+        return tm.local(cnt);  // this warp's local edges
+    }
+};
+
+// First batch of a warp's backward edge loop, loaded early (lane = local edge
+// for the scalars, lane = channel for the z rows).
+template <typename T>
+struct BwdPre {
+    T zr[8];
+    T s, ds;
+    V4<T> d0, d1;
+    int mir;
+};
+template <typename T, int G>
+__device__ __forceinline__ void bwd_prefetch(BwdPre<T>& p, const T* Z, const DevWork<T>& ws,
+                                             const DevGraph& gr, long long e0, int room,
+                                             int lane) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        if (u < room) p.zr[u] = Z[(e0 + static_cast<long long>(G) * u) * kH + lane];
+    if (lane < room) {
+        const long long e = e0 + static_cast<long long>(G) * lane;
+        p.s = ws.es[e];
+        p.ds = ws.eds[e];
+        p.d0 = ld4c(ws.edb + 8 * e);
+        p.d1 = ld4c(ws.edb + 8 * e + 4);
+        p.mir = gr.inv_pos[e];
+    }
+}
+
+// Sum of the pushed adjoint rows in i's mirror slots (fixed order), symmetric
+// ELL graph: the in-slots are the atom's own out-slots, so the first batch is
+// loaded speculatively (see AtomRow).  General graphs use gather_in.
+template <typename T, int G>
+struct GatherPre {
+    static constexpr int B = 2 * kU<T>;
+    T r[B];
+    __device__ __forceinline__ void load(const T* D, long long e0, int room, int lane) {
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (u < room) r[u] = D[(e0 + static_cast<long long>(G) * u) * kH + lane];
+    }
+    __device__ __forceinline__ T sum(const T* D, long long e0, int ic, int lane) const {
+        T acc = T(0);
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (u < ic) acc += r[u];
+        for (int k0 = B; k0 < ic; k0 += B) {
+            T q[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                if (k0 + u < ic) q[u] = D[(e0 + static_cast<long long>(G) * (k0 + u)) * kH + lane];
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                if (k0 + u < ic) acc += q[u];
+        }
+        return acc;
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Message-layer backward for atom i, given dE/dh^{l+1}_i (dh, lane = channel)
 // and the update hidden activation zu.  Pushes dz_e to e's mirror slot and
-// accumulates dE/dr_e into g (this warp's share of the edges).
+// accumulates dE/dr_e into g (this warp's share of the edges).  `pre` holds the
+// first batch of the edge loop, loaded before the atom's mat-vecs.
 // ---------------------------------------------------------------------------
 template <typename T, int G>
 __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, const T* mW2T,
                                                   T mb2, const T (&w1b)[kK], const DevGraph& gr,
                                                   const DevWork<T>& ws, WarpSmem<T>& sm, int l,
                                                   int i, T dh, T zu, bool first_g,
-                                                  Team<G>& tm) {
+                                                  Team<G>& tm, BwdPre<T>& pre, long long e0,
+                                                  int mloc) {
     const int lane = tm.lane;
     const long long S = ws.slots;
     // update MLP backward (64 -> 32 tanh -> 32)
@@ -557,30 +694,22 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
     const T c0 = warp_sum(dmsum * mb2);
     const T* Z = ws.z + l * S * kH;
     T* D = ws.d + (l & 1) * S * kH;
-    const int start = gr.row_start[i] + tm.w;
-    const int mloc = tm.local(gr.nnei[i]);
     for (int base = 0; base < mloc; base += 32) {
         const int m = min(32, mloc - base);
-        const long long e0 = start + static_cast<long long>(G) * base;  // local edge k: e0 + G k
-        const T* zrow = Z + e0 * kH + lane;
-        // the first batch of z rows is in flight during the scalar staging;
-        // each batch's compute overlaps the next batch's loads
-        T zr[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (u < m) zr[u] = zrow[u * G * kH];
-        // lane u stages edge u's scalars (one memory round trip for the batch)
+        const long long eb = e0 + static_cast<long long>(G) * base;  // local edge k: eb + G k
+        const T* zrow = Z + eb * kH + lane;
+        if (base > 0) bwd_prefetch<T, G>(pre, Z, ws, gr, eb, m, lane);
+        // lane u stages edge u's scalars; the edge loop reads them as broadcasts
         if (lane < m) {
-            const long long e = e0 + G * lane;
             T* row = sm.ed[lane];
-            row[0] = ws.es[e];
-            row[1] = ws.eds[e];
-            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-            st4(row + 4, d0.x, d0.y, d0.z, d0.w);
-            st4(row + 8, d1.x, d1.y, d1.z, d1.w);
-            sm.emir[lane] = gr.inv_pos[e];
+            row[0] = pre.s;
+            row[1] = pre.ds;
+            st4(row + 4, pre.d0.x, pre.d0.y, pre.d0.z, pre.d0.w);
+            st4(row + 8, pre.d1.x, pre.d1.y, pre.d1.z, pre.d1.w);
+            sm.emir[lane] = pre.mir;
         }
         __syncwarp();
+        T* zr = pre.zr;
         for (int u0 = 0; u0 < m; u0 += 8) {
             const int mu = min(8, m - u0);
             T zn[8];
@@ -613,7 +742,7 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
             const T tot = reduce8(term, lane);
             if ((lane & 3) == 0 && (lane >> 2) < mu) {
                 const int u = u0 + (lane >> 2);
-                const long long e = e0 + static_cast<long long>(G) * u;
+                const long long e = eb + static_cast<long long>(G) * u;
                 ws.g[e] = (first_g ? T(0) : ws.g[e]) + (tot + sm.ed[u][1] * c0);
             }
 #pragma unroll
@@ -631,24 +760,27 @@ template <typename T, int G, bool LAST>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    TP_START;
     pdl_launch_dependents();
     const DevMlp<T>& msg = md.msg[l];
     const DevMlp<T>& upd = md.upd[l];
-    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
-    const T* mW2 = sg.template mat<32, 32>(msg.W2, 32);
-    const T* uW1 = sg.template mat<32, 64>(upd.W1, 64);
-    const T* uW2 = sg.template mat<32, 32>(upd.W2, 32);
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
+    const T* mW2 = sg.template view<32, 32>();
+    const T* uW1 = sg.template view<32, 64>();
+    const T* uW2 = sg.template view<32, 32>();
     const T *nW1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *uW2T = nullptr, *uW1T = nullptr,
             *mW2T = nullptr;
     if constexpr (LAST) {
-        fW1 = sg.template mat<32, 32>(md.fit.W1, 32);
-        fW1T = sg.template mat<32, 32>(md.fit.W1T, 32);
-        uW2T = sg.template mat<32, 32>(upd.W2T, 32);
-        uW1T = sg.template mat<64, 32>(upd.W1T, 32);
-        mW2T = sg.template mat<32, 32>(msg.W2T, 32);
-    } else {
-        nW1h = sg.template mat<32, 32>(md.msg[l + 1].W1, kInMsg);
+        fW1 = sg.template view<32, 32>();
+        fW1T = sg.template view<32, 32>();
+        uW2T = sg.template view<32, 32>();
+        uW1T = sg.template view<64, 32>();
+        mW2T = sg.template view<32, 32>();
+} else {
+        nW1h = sg.template view<32, 32>();
     }
+    sg.load(md.img_fwd[l], &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
     const int lane = tm.lane;
@@ -659,36 +791,59 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     const T mb1 = msg.b1[lane], mb2 = msg.b2[lane], ub1 = upd.b1[lane], ub2 = upd.b2[lane];
     const T fb1 = LAST ? md.fit.b1[lane] : T(0), fw2 = LAST ? md.fit.W2[lane] : T(0);
     const T fb2 = LAST ? md.fit.b2[0] : T(0);
-    sg.wait();
-    __syncthreads();
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
+    TP(0);
     pdl_wait();
+    TP(1);
     const int n = gr.n;
     const long long S = ws.slots;
     const T* Pin = ws.pe + (l & 1) * S * kH;
     T* Z = ws.z + l * S * kH;
     for (int i = tm.first; i < gr.n_active; i += tm.stride) {
-        const int start = gr.row_start[i] + tm.w;
-        const int mloc = tm.local(gr.nnei[i]);
+        AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
+        // first batch: P rows (lane = channel) and edge scalars (lane = local edge)
+        T pr[kU<T>];
+#pragma unroll
+        for (int u = 0; u < kU<T>; ++u)
+            if (u < ar.room) pr[u] = Pin[(ar.e0 + static_cast<long long>(G) * u) * kH + lane];
+        T es_l = T(0);
+        V4<T> b0_l{}, bb_l{};
+        if (lane < ar.room) {
+            const long long e = ar.e0 + static_cast<long long>(G) * lane;
+            es_l = ws.es[e];
+            b0_l = ld4c(ws.eb + 8 * e);
+            bb_l = ld4c(ws.eb + 8 * e + 4);
+        }
+        // push targets of P^{l+1} (symmetric graph: the atom's own reverse slots)
+        int push_idx = 0;
+        if (!LAST && gr.sym && lane < ar.room)
+            push_idx = gr.in_edge[ar.e0 + static_cast<long long>(G) * lane];
+        const int mloc = ar.finish(tm);
         sm.x[lane] = hi;
+        TP(2);
         T acc = T(0), ssum = T(0);
         for (int base = 0; base < mloc; base += 32) {
             const int m = min(32, mloc - base);
-            const long long e0 = start + static_cast<long long>(G) * base;  // local k: e0 + G k
+            const long long e0 = ar.e0 + static_cast<long long>(G) * base;  // local k: e0 + G k
             const T* prow = Pin + e0 * kH + lane;
-            // the first batch of P rows is in flight during the scalar staging;
-            // each batch's compute overlaps the next batch's loads
-            T pr[kU<T>];
+            if (base > 0) {
 #pragma unroll
-            for (int u = 0; u < kU<T>; ++u)
-                if (u < m) pr[u] = prow[u * G * kH];
+                for (int u = 0; u < kU<T>; ++u)
+                    if (u < m) pr[u] = prow[u * G * kH];
+                if (lane < m) {
+                    const long long e = e0 + G * lane;
+                    es_l = ws.es[e];
+                    b0_l = ld4c(ws.eb + 8 * e);
+                    bb_l = ld4c(ws.eb + 8 * e + 4);
+                }
+            }
             if (lane < m) {
-                const long long e = e0 + G * lane;
                 T* row = sm.ed[lane];
-                row[0] = ws.es[e];
-                const V4<T> b0 = ld4c(ws.eb + 8 * e), bb = ld4c(ws.eb + 8 * e + 4);
-                st4(row + 4, b0.x, b0.y, b0.z, b0.w);
-                st4(row + 8, bb.x, bb.y, bb.z, bb.w);
+                row[0] = es_l;
+                st4(row + 4, b0_l.x, b0_l.y, b0_l.z, b0_l.w);
+                st4(row + 8, bb_l.x, bb_l.y, bb_l.z, bb_l.w);
             }
             __syncwarp();
             for (int u0 = 0; u0 < m; u0 += kU<T>) {
@@ -721,7 +876,17 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
             }
             __syncwarp();
         }
+        // LAST: the backward edge loop's first batch (z rows just written by this
+        // warp) is loaded now, under the atom-level mat-vecs below
+        TP(3);
+        BwdPre<T> pre;
+        if constexpr (LAST) bwd_prefetch<T, G>(pre, Z, ws, gr, ar.e0, min(mloc, 32), lane);
         acc = tm.sum(acc, ssum, sm);
+        TP(4);
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
         sm.t[lane] = acc;
         __syncwarp();
         // msum = W2 (sum_e s_e z_e) + (sum_e s_e) b2  -> second half of the update input
@@ -737,19 +902,40 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
         sm.t[lane] = hn;
         __syncwarp();
+        TP(5);
         if constexpr (!LAST) {
             const T p = twmv<T, 32>(nW1h, sm.t, lane, tm, sm);
             if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
-            push_rows(ws.pe + ((l + 1) & 1) * S * kH, p, gr, i, tm);
+            T* dst = ws.pe + ((l + 1) & 1) * S * kH;
+            if (gr.sym) {  // in-slots == out-slots: push_idx holds the first 32 targets
+                for (int k0 = 0; k0 < mloc; k0 += 32) {
+                    const int kk = min(32, mloc - k0);
+                    if (k0 > 0)
+                        push_idx = lane < kk ? gr.in_edge[ar.e0 + static_cast<long long>(G) *
+                                                                       (k0 + lane)]
+                                             : 0;
+                    for (int k = 0; k < kk; ++k) {
+                        const long long slot = __shfl_sync(FULL_MASK, push_idx, k);
+                        dst[slot * kH + lane] = p;
+                    }
+                }
+            } else {
+                push_rows(dst, p, gr, i, tm);
+            }
+            TP(6);
         } else {
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
             // fitting: h^M -> dE/dh^M
             const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
                                   lead ? ws.e_atom + i : nullptr, tm, sm);
-            msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, true, tm);
+            TP(7);
+            msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, true, tm, pre,
+                              ar.e0, mloc);
+            TP(8);
         }
         __syncwarp();
     }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
@@ -760,12 +946,14 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
     pdl_launch_dependents();
     const DevMlp<T>& msg = md.msg[l];
     const DevMlp<T>& upd = md.upd[l];
-    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
     // W1h^(l+1)^T: rows 0..31 of msg[l+1].W1T ([in][32])
-    const T* nW1hT = sg.template mat<32, 32>(md.msg[l + 1].W1T, 32);
-    const T* uW2T = sg.template mat<32, 32>(upd.W2T, 32);
-    const T* uW1T = sg.template mat<64, 32>(upd.W1T, 32);
-    const T* mW2T = sg.template mat<32, 32>(msg.W2T, 32);
+    const T* nW1hT = sg.template view<32, 32>();
+    const T* uW2T = sg.template view<32, 32>();
+    const T* uW1T = sg.template view<64, 32>();
+    const T* mW2T = sg.template view<32, 32>();
+    sg.load(md.img_bwd[l], &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
     const int lane = tm.lane;
@@ -773,21 +961,43 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
     const T mb2 = msg.b2[lane];
-    sg.wait();
-    __syncthreads();
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
     pdl_wait();
     const T* Dn = ws.d + ((l + 1) & 1) * ws.slots * kH;
+    const T* Z = ws.z + l * ws.slots * kH;
     for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        AtomRow<G> ar(gr, i, tm);
+        // one round trip: own adjoint, update activations, the pushed adjoint rows
+        // and the backward edge loop's first batch
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
         const T zu = ws.uz1[(static_cast<long long>(l) * gr.n + i) * kH + lane];
-        sm.t[lane] = gather_in(Dn, ws, gr, i, tm, sm);
+        GatherPre<T, G> gp;
+        if (gr.sym) gp.load(Dn, ar.e0, ar.room, lane);
+        BwdPre<T> pre;
+        bwd_prefetch<T, G>(pre, Z, ws, gr, ar.e0, min(ar.room, 32), lane);
+        const int mloc = ar.finish(tm);
+        T sv;
+        if (gr.sym) {
+            sv = tm.sum(gp.sum(Dn, ar.e0, mloc, lane), sm);
+            if (ws.s_remote) sv += ws.s_remote[static_cast<long long>(i) * kH + lane];
+        } else {
+            sv = gather_in(Dn, ws, gr, i, tm, sm);
+        }
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
+        sm.t[lane] = sv;
         __syncwarp();
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, false, tm);
+        msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, false, tm, pre,
+                          ar.e0, mloc);
         __syncwarp();
     }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
@@ -796,20 +1006,49 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
-    Smem<T> sg{reinterpret_cast<T*>(smem_raw)};
-    const T* m0W1hT = sg.template mat<32, 32>(md.msg[0].W1T, 32);
-    const T* eW2T = sg.template mat<32, 32>(md.embed.W2T, 32);
-    const T* eW1T = sg.template mat<32, 32>(md.embed.W1T, 32);
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
+    const T* m0W1hT = sg.template view<32, 32>();
+    const T* eW2T = sg.template view<32, 32>();
+    const T* eW1T = sg.template view<32, 32>();
+    sg.load(md.img_embed_bwd, &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
     const int lane = tm.lane;
-    sg.wait();
-    __syncthreads();
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
     pdl_wait();
     for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+        AtomRow<G> ar(gr, i, tm);
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + lane];
-        sm.t[lane] = gather_in(ws.d, ws, gr, i, tm, sm);
+        GatherPre<T, G> gp;
+        if (gr.sym) gp.load(ws.d, ar.e0, ar.room, lane);
+        // first batch of the per-edge descriptor adjoint (lane = local edge)
+        V4<T> d0_l{}, d1_l{};
+        T g_l = T(0);
+        int ty_l = 0, mir_l = 0;
+        if (lane < ar.room) {
+            const long long e = ar.e0 + static_cast<long long>(G) * lane;
+            d0_l = ld4c(ws.edb + 8 * e);
+            d1_l = ld4c(ws.edb + 8 * e + 4);
+            g_l = ws.g[e];
+            ty_l = gr.ety[e];
+            mir_l = gr.inv_pos[e];
+        }
+        const int mloc = ar.finish(tm);
+        T sv;
+        if (gr.sym) {
+            sv = tm.sum(gp.sum(ws.d, ar.e0, mloc, lane), sm);
+            if (ws.s_remote) sv += ws.s_remote[static_cast<long long>(i) * kH + lane];
+        } else {
+            sv = gather_in(ws.d, ws, gr, i, tm, sm);
+        }
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
+        sm.t[lane] = sv;
         __syncwarp();
         const T dh = own + twmv<T, 32>(m0W1hT, sm.t, lane, tm, sm);
         sm.x[lane] = dh;
@@ -820,26 +1059,31 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
         const T dd = twmv<T, 32>(eW1T, sm.y, lane, tm, sm);
         sm.t[lane] = dd;
         __syncwarp();
-        const int start = gr.row_start[i] + tm.w;
-        const int mloc = tm.local(gr.nnei[i]);
         for (int q = lane; q < mloc; q += 32) {
-            const long long e = start + static_cast<long long>(G) * q;
-            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-            const T* dv = sm.t + gr.ety[e] * kK;
-            T acc = dv[0] * d0.x;
-            acc += dv[1] * d0.y;
-            acc += dv[2] * d0.z;
-            acc += dv[3] * d0.w;
-            acc += dv[4] * d1.x;
-            acc += dv[5] * d1.y;
-            acc += dv[6] * d1.z;
-            acc += dv[7] * d1.w;
-            const T gv = ws.g[e] + acc;
+            const long long e = ar.e0 + static_cast<long long>(G) * q;
+            if (q >= 32) {
+                d0_l = ld4c(ws.edb + 8 * e);
+                d1_l = ld4c(ws.edb + 8 * e + 4);
+                g_l = ws.g[e];
+                ty_l = gr.ety[e];
+                mir_l = gr.inv_pos[e];
+            }
+            const T* dv = sm.t + ty_l * kK;
+            T acc = dv[0] * d0_l.x;
+            acc += dv[1] * d0_l.y;
+            acc += dv[2] * d0_l.z;
+            acc += dv[3] * d0_l.w;
+            acc += dv[4] * d1_l.x;
+            acc += dv[5] * d1_l.y;
+            acc += dv[6] * d1_l.z;
+            acc += dv[7] * d1_l.w;
+            const T gv = g_l + acc;
             ws.g[e] = gv;
-            ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
+            ws.grev[mir_l] = gv;  // mirror for the force gather
         }
         __syncwarp();
     }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
 
 // Warp-per-atom range for the force kernel: warp-global index and stride.
@@ -1251,3 +1495,15 @@ template int launch_network<double>(const DevModel<double>&, const DevGraph&,
                                     cudaStream_t, const Marker&, const MdFuse&);
 
 }  // namespace hmdp
+
+#ifdef HMDP_TPROBE
+extern "C" int hmdp_debug_tprobe(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, hmdp::g_tprobe, sizeof(hmdp::g_tprobe));
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(hmdp::g_tprobe, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
