@@ -152,6 +152,19 @@ int hmdp_check(hmdp_ctx* ctx);
 int hmdp_kernels_per_eval(const hmdp_ctx* ctx);
 
 /* ---------------------------------------------------------------------------
+ * NNPot-style group provider (the paper's Fig. 2 coupling):
+ * the DP model runs on the atoms listed in group[n_group] (sorted, duplicate-
+ * free indices into the n_total-atom periodic system, e.g. Topology::groups
+ * ["protein"]); their NN forces are ADDED into forces_accum[3 n_total] (other
+ * atoms untouched), the NN energy is returned.  Classical terms — including
+ * every cross-group interaction — stay with the caller.  Positions are gathered
+ * on the device; equivalent to hmdp_compute on the extracted group.
+ * ------------------------------------------------------------------------- */
+int hmdp_compute_group(hmdp_ctx* ctx, int n_total, const double* xyz, const int* types,
+                       const int* group, int n_group, const double* box, int precision,
+                       double* energy, double* forces_accum, double* virial9, double* virial);
+
+/* ---------------------------------------------------------------------------
  * Device MD loop: velocity Verlet (integrators.cpp:32-47) with the finite-force
  * check (integrators.cpp:12-18) and the NN force provider, neighbour list
  * rebuilt every step (skin 0, as build_input_periodic), all on the device and

@@ -11,6 +11,9 @@
 //   halomd::nn::descriptors(model, input)                        -> hmdp::halomd::descriptors(model, input)
 //   halomd::nn::switch_value / switch_derivative                 -> hmdp::halomd::switch_value / switch_derivative
 //   ForceFunction (integrators.hpp:35)                           -> hmdp::halomd::force_function(model, types, prec)
+//   NNPot hybrid coupling (no reference code):
+//     plan_group_preprocessing(topo, "protein")                  -> hmdp::halomd::plan_group_preprocessing(topo, name)
+//     nn_force_provider(state, topo', plan, model)               -> hmdp::halomd::nn_force_provider(state, plan, model, prec)
 //
 // Semantics follow the reference: same argument meaning, energies for owned
 // atoms only, forces for every input atom, std::invalid_argument /
@@ -26,8 +29,10 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hmdp.h"
@@ -210,6 +215,108 @@ std::function<double(State&)> force_function(const NnModel& model, std::vector<i
         }
         return e;
     };
+}
+
+// ---------------------------------------------------------------------------
+// NNPot-style hybrid coupling (SPEC.md:375-383 plan_group_preprocessing,
+// :411-419 nn_force_provider; the paper's Fig. 2).  The reference declares the
+// contract but ships no code; these follow it on the caller's own Topology /
+// State types (topology.hpp, state.hpp).
+// ---------------------------------------------------------------------------
+
+// Everything plan_group_preprocessing removed or added, so it can be undone.
+template <class Topology>
+struct NnGroupPlan {
+    std::string group;
+    std::vector<int> atoms;  // sorted, duplicate-free (Topology::groups)
+    std::vector<typename decltype(Topology::bonds)::value_type> removed_bonds;
+    std::vector<typename decltype(Topology::angles)::value_type> removed_angles;
+    std::vector<typename decltype(Topology::dihedrals)::value_type> removed_dihedrals;
+    std::vector<std::pair<int, int>> added_exclusions;  // i < j, previously not excluded
+};
+
+// Removes every bonded term whose atoms all lie in the group and excludes every
+// in-group pair (symmetrically); cross-group terms and pairs are untouched.  An
+// empty group is a no-op.  Throws std::invalid_argument for an unknown group.
+template <class Topology>
+NnGroupPlan<Topology> plan_group_preprocessing(Topology& topo, const std::string& group) {
+    auto it = topo.groups.find(group);
+    if (it == topo.groups.end()) throw std::invalid_argument("unknown atom group: " + group);
+    NnGroupPlan<Topology> plan;
+    plan.group = group;
+    plan.atoms = it->second;
+    if (plan.atoms.empty()) return plan;
+    std::vector<char> in(static_cast<std::size_t>(topo.n_atoms), 0);
+    for (int a : plan.atoms) in[static_cast<std::size_t>(a)] = 1;
+    auto split = [](auto& terms, auto& removed, auto inside) {
+        auto keep = terms.begin();
+        for (auto t = terms.begin(); t != terms.end(); ++t) {
+            if (inside(*t)) removed.push_back(*t);
+            else *keep++ = *t;
+        }
+        terms.erase(keep, terms.end());
+    };
+    split(topo.bonds, plan.removed_bonds, [&](const auto& b) { return in[b.i] && in[b.j]; });
+    split(topo.angles, plan.removed_angles,
+          [&](const auto& a) { return in[a.i] && in[a.j] && in[a.k]; });
+    split(topo.dihedrals, plan.removed_dihedrals,
+          [&](const auto& d) { return in[d.i] && in[d.j] && in[d.k] && in[d.l]; });
+    for (std::size_t p = 0; p < plan.atoms.size(); ++p)
+        for (std::size_t q = p + 1; q < plan.atoms.size(); ++q) {
+            const int i = plan.atoms[p], j = plan.atoms[q];
+            if (!topo.excluded(i, j)) {
+                topo.add_exclusion(i, j);
+                plan.added_exclusions.emplace_back(i, j);
+            }
+        }
+    return plan;
+}
+
+// Reverts plan_group_preprocessing (bonded terms re-appended, added exclusions
+// dropped).
+template <class Topology>
+void undo_group_preprocessing(Topology& topo, const NnGroupPlan<Topology>& plan) {
+    topo.bonds.insert(topo.bonds.end(), plan.removed_bonds.begin(), plan.removed_bonds.end());
+    topo.angles.insert(topo.angles.end(), plan.removed_angles.begin(), plan.removed_angles.end());
+    topo.dihedrals.insert(topo.dihedrals.end(), plan.removed_dihedrals.begin(),
+                          plan.removed_dihedrals.end());
+    for (const auto& [i, j] : plan.added_exclusions) {
+        auto drop = [&](int a, int b) {
+            auto& v = topo.exclusions[static_cast<std::size_t>(a)];
+            v.erase(std::remove(v.begin(), v.end(), b), v.end());
+        };
+        drop(i, j);
+        drop(j, i);
+    }
+}
+
+// The coupling layer: extracts the group's positions (on the device), runs the DP
+// model on them, ADDS the group's NN forces into state.forces and returns the NN
+// energy.  The caller's classical force field supplies everything else, including
+// every cross-group interaction.
+template <class State, class Topology, class NnModel, class ToJson>
+double nn_force_provider(State& state, const std::vector<int>& type_of,
+                         const NnGroupPlan<Topology>& plan, const NnModel& model, int prec,
+                         ToJson&& to_json, int device = 0) {
+    hmdp_ctx* c = ContextCache::get().ctx(to_json(model), device);
+    std::lock_guard<std::mutex> lk(ContextCache::get().lock());
+    const int n = static_cast<int>(state.positions.size());
+    if (static_cast<int>(type_of.size()) != n)
+        throw std::invalid_argument("positions/types/global_index size mismatch");
+    if (static_cast<int>(state.forces.size()) != n) state.forces.resize(n);
+    const std::vector<double> x = flat3(state.positions);
+    std::vector<double> f = flat3(state.forces);
+    const double b[3] = {state.box.lengths.x, state.box.lengths.y, state.box.lengths.z};
+    double e = 0.0;
+    check(hmdp_compute_group(c, n, x.data(), type_of.data(), plan.atoms.data(),
+                             static_cast<int>(plan.atoms.size()), b,
+                             prec == 1 ? HMDP_FP64 : HMDP_FP32, &e, f.data(), nullptr, nullptr));
+    for (int i = 0; i < n; ++i) {
+        state.forces[i].x = f[3 * i];
+        state.forces[i].y = f[3 * i + 1];
+        state.forces[i].z = f[3 * i + 2];
+    }
+    return e;
 }
 
 }  // namespace hmdp::halomd

@@ -63,6 +63,8 @@ SIGNATURES = {
     "hmdp_peak_fp32": (_c_int, [_c_int, _c_int, _vp]),
     "hmdp_md_get": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "hmdp_md_destroy": (_c_int, [_vp]),
+    "hmdp_compute_group": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _vp, _c_int, _vp, _vp,
+                                    _vp, _vp]),
     "hmdp_make_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_int, _c_int, _c_int,
                                        ctypes.c_uint64, _vp, _c_long]),
     "hmdp_synthetic_system": (_c_int, [_c_int, _c_double, _c_double, ctypes.c_uint64, _c_double,

@@ -34,6 +34,7 @@ template <typename T>
 int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, double*, double*,
                    double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cudaStream_t);
+void launch_gather_group(int, const int*, const double*, const int*, double*, int*, cudaStream_t);
 double probe_fp32_tflops(int ms);
 template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
@@ -300,6 +301,7 @@ struct hmdp_ctx {
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // domain decomposition (hmdp_dd_*): local graph + halo row buffers
     DBuf dd_patom, dd_sremote, dd_sghost;
+    DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
     DevGraph dd_gr{};
     int dd_prec = -1;
     long long dd_slots = 1;
@@ -352,7 +354,7 @@ struct hmdp_ctx {
                         &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
-                        &dd_sremote, &dd_sghost})
+                        &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -757,6 +759,73 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
             }
             hmdp_ctx::raise_bits(bits);
             copy_outputs(ctx, n, energy, per_atom, forces, virial9, virial);
+            return;
+        }
+        fail(HMDP_RUNTIME_ERROR, "neighbour capacity did not converge");
+    });
+}
+
+int hmdp_compute_group(hmdp_ctx* ctx, int n_total, const double* xyz, const int* types,
+                       const int* group, int n_group, const double* box, int precision,
+                       double* energy, double* forces_accum, double* virial9, double* virial) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!ctx) fail(HMDP_INVALID_ARGUMENT, "null context");
+        if (n_total < 0 || n_group < 0 || n_group > n_total)
+            fail(HMDP_INVALID_ARGUMENT, "group size out of range");
+        if (!energy || !forces_accum || !box || (n_group > 0 && (!xyz || !types || !group)))
+            fail(HMDP_INVALID_ARGUMENT, "required pointer is NULL");
+        // Topology::validate: groups are sorted and duplicate-free, indices in range
+        for (int k = 0; k < n_group; ++k) {
+            if (group[k] < 0 || group[k] >= n_total)
+                fail(HMDP_INVALID_ARGUMENT, "group member out of range");
+            if (k > 0 && group[k] <= group[k - 1])
+                fail(HMDP_INVALID_ARGUMENT, "group must be sorted and duplicate-free");
+        }
+        set_device(ctx);
+        if (n_group == 0) {
+            ctx->grid(box, ctx->model.rc, 0);
+            zero_outputs(0, energy, nullptr, nullptr, virial9, virial);
+            return;
+        }
+        for (int k = 0; k < n_group; ++k)
+            if (types[group[k]] < 0 || types[group[k]] >= ctx->model.n_types)
+                fail(HMDP_INVALID_ARGUMENT, "atom type " + std::to_string(types[group[k]]) +
+                                                " of atom " + std::to_string(group[k]) +
+                                                " out of range for the model");
+        ctx->ensure_atoms(n_group);
+        cudaStream_t st = ctx->st();
+        ctx->grp_xyz.ensure(3 * static_cast<size_t>(n_total) * sizeof(double));
+        ctx->grp_types.ensure(static_cast<size_t>(n_total) * sizeof(int));
+        ctx->grp_idx.ensure(static_cast<size_t>(n_group) * sizeof(int));
+        ck(cudaMemcpyAsync(ctx->grp_xyz.p, xyz, 3 * static_cast<size_t>(n_total) * sizeof(double),
+                           cudaMemcpyHostToDevice, st),
+           "xyz H2D");
+        ck(cudaMemcpyAsync(ctx->grp_types.p, types, static_cast<size_t>(n_total) * sizeof(int),
+                           cudaMemcpyHostToDevice, st),
+           "types H2D");
+        ck(cudaMemcpyAsync(ctx->grp_idx.p, group, static_cast<size_t>(n_group) * sizeof(int),
+                           cudaMemcpyHostToDevice, st),
+           "group H2D");
+        // group-local positions (the NNPot extraction), on the device
+        launch_gather_group(n_group, ctx->grp_idx.as<int>(), ctx->grp_xyz.as<double>(),
+                            ctx->grp_types.as<int>(), ctx->pos.as<double>(), ctx->types.as<int>(), st);
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            ctx->last_launches =
+                enqueue_periodic(ctx, n_group, ctx->pos.as<double>(), ctx->types.as<int>(), box,
+                                 precision, ctx->forces.as<double>(), nullptr, st);
+            ck(cudaGetLastError(), "kernel launch");
+            const unsigned bits = ctx->take_err();
+            if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
+                ctx->grow_for(bits);
+                continue;
+            }
+            hmdp_ctx::raise_bits(bits);
+            std::vector<double> fg(3 * static_cast<size_t>(n_group));
+            copy_outputs(ctx, n_group, energy, nullptr, fg.data(), virial9, virial);
+            // scatter back into the global force array
+            for (int k = 0; k < n_group; ++k)
+                for (int a = 0; a < 3; ++a) forces_accum[3 * group[k] + a] += fg[3 * k + a];
             return;
         }
         fail(HMDP_RUNTIME_ERROR, "neighbour capacity did not converge");

@@ -163,6 +163,19 @@ __global__ void k_vv_kick_drift_bin(int n, MdFuse mf, const double* __restrict__
     vv_kick_drift_bin_atom(i, mf, f, err);
 }
 
+// NNPot extraction: group-local positions and types.
+__global__ void k_gather_group(int ng, const int* __restrict__ idx, const double* __restrict__ xyz,
+                               const int* __restrict__ types, double* __restrict__ pos_out,
+                               int* __restrict__ types_out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const int j = idx[k];
+    pos_out[3 * k] = xyz[3 * j];
+    pos_out[3 * k + 1] = xyz[3 * j + 1];
+    pos_out[3 * k + 2] = xyz[3 * j + 2];
+    types_out[k] = types[j];
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -240,6 +253,11 @@ void launch_descriptors_f64(const DevModel<double>& md, const DevGraph& gr, doub
 void launch_vv_kick_drift_bin(int n, const MdFuse& mf, const double* f, unsigned* err,
                               cudaStream_t st) {
     k_vv_kick_drift_bin<<<(n + 127) / 128, 128, 0, st>>>(n, mf, f, err);
+}
+
+void launch_gather_group(int ng, const int* idx, const double* xyz, const int* types,
+                         double* pos_out, int* types_out, cudaStream_t st) {
+    k_gather_group<<<(ng + 127) / 128, 128, 0, st>>>(ng, idx, xyz, types, pos_out, types_out);
 }
 
 }  // namespace hmdp

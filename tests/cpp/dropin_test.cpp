@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "halomd/forcefield.hpp"
 #include "halomd/integrators.hpp"
+#include "halomd/neighborlist.hpp"
 #include "halomd/nn/inference.hpp"
 #include "halomd/nn/model.hpp"
 #include "halomd/synthetic.hpp"
@@ -108,6 +110,87 @@ int main() {
         for (std::size_t k = 0; k < d_ref[i].size(); ++k) dd = std::max(dd, std::fabs(d_ref[i][k] - d_our[i][k]));
     EXPECT(dd < 1e-12, "descriptors differ by %.3e", dd);
     EXPECT(hmdp::halomd::switch_value(0.57, 0.6) == nn::switch_value(0.57, 0.6), "switch_value");
+
+    // NNPot hybrid coupling on the reference's own
+    // Topology/State: group preprocessing, the group provider against the reference
+    // evaluate() on the extracted group, and hybrid velocity-Verlet steps with the
+    // reference's classical force field on the preprocessed topology.
+    {
+        Topology t2 = topo;
+        auto plan = hmdp::halomd::plan_group_preprocessing(t2, "protein");
+        const auto& grp = topo.groups.at("protein");
+        const int ng = static_cast<int>(grp.size());
+        std::vector<char> in(n, 0);
+        for (int a : grp) in[a] = 1;
+        bool ok = true;
+        for (const auto& b : t2.bonds) ok &= !(in[b.i] && in[b.j]);
+        for (const auto& a : t2.angles) ok &= !(in[a.i] && in[a.j] && in[a.k]);
+        for (const auto& d : t2.dihedrals) ok &= !(in[d.i] && in[d.j] && in[d.k] && in[d.l]);
+        EXPECT(ok, "in-group bonded term survived preprocessing");
+        EXPECT(t2.bonds.size() + plan.removed_bonds.size() == topo.bonds.size(), "bond bookkeeping");
+        bool excl = true;
+        for (int p2 = 0; p2 < ng && excl; ++p2)
+            for (int q = p2 + 1; q < ng; ++q) excl &= t2.excluded(grp[p2], grp[q]);
+        EXPECT(excl, "in-group pair not excluded");
+        t2.validate();
+
+        auto model = nn::make_model(nn::ModelFamily::message_passing, 3, 0.6, 2, 8, 32, 1);
+        State s = st;
+        s.forces.assign(n, Vec3{});
+        const double e_nn = hmdp::halomd::nn_force_provider(s, topo.type_of, plan, model, 1, to_json);
+        std::vector<Vec3> gpos;
+        std::vector<int> gty, ggi;
+        for (int k = 0; k < ng; ++k) {
+            gpos.push_back(st.positions[grp[k]]);
+            gty.push_back(topo.type_of[grp[k]]);
+            ggi.push_back(k);
+        }
+        auto gin = nn::build_input_periodic(gpos, gty, ggi, st.box, 0.6);
+        auto gref = nn::evaluate(model, gin, Precision::fp64);
+        EXPECT(std::fabs(e_nn - gref.energy) <= 1e-11 * std::fabs(gref.energy),
+               "group energy %.12f vs %.12f", e_nn, gref.energy);
+        double dfg = 0, other = 0;
+        Vec3 sum{};
+        for (int k = 0; k < ng; ++k) {
+            dfg = std::max(dfg, std::sqrt(norm2(s.forces[grp[k]] - gref.forces[k])));
+            sum = sum + s.forces[grp[k]];
+        }
+        for (int i = 0; i < n; ++i)
+            if (!in[i]) other = std::max(other, std::sqrt(norm2(s.forces[i])));
+        EXPECT(dfg <= 1e-10 * rms(gref.forces), "group forces differ %.3e", dfg);
+        EXPECT(other == 0.0, "NN provider touched a non-group atom");
+        EXPECT(std::sqrt(norm2(sum)) <= 1e-8 * rms(gref.forces) * ng, "group NN forces sum %.3e",
+               std::sqrt(norm2(sum)));
+
+        // hybrid MD: classical(topo') + NN(protein); energy stays finite and the
+        // hybrid potential equals classical + NN
+        ForceFieldParams ffp;
+        ffp.lj.sigma = {0.33, 0.30};
+        ffp.lj.epsilon = {0.40, 0.50};
+        ffp.rc = 0.7;
+        ffp.coulomb.rc = 0.7;
+        double last_cl = 0, last_nn = 0;
+        ForceFunction hybrid = [&](State& x) {
+            auto nl = build_neighbor_list(x, t2, 0.7, 0.0);
+            const EnergyReport rep = compute_classical(x, t2, nl, ffp);
+            last_cl = rep.total_potential();
+            last_nn = hmdp::halomd::nn_force_provider(x, topo.type_of, plan, model, 1, to_json);
+            return last_cl + last_nn;
+        };
+        State h = st;
+        const double e0 = hybrid(h);
+        EXPECT(std::fabs(e0 - (last_cl + last_nn)) == 0.0, "hybrid energy composition");
+        for (int k = 0; k < 5; ++k) velocity_verlet_step(h, hybrid, 0.001, topo.mass);
+        bool finite = true;
+        for (int i = 0; i < n; ++i) finite &= std::isfinite(h.positions[i].x + h.forces[i].x);
+        EXPECT(finite, "hybrid MD produced non-finite state");
+
+        hmdp::halomd::undo_group_preprocessing(t2, plan);
+        EXPECT(t2.bonds.size() == topo.bonds.size() && t2.angles.size() == topo.angles.size() &&
+                   t2.dihedrals.size() == topo.dihedrals.size(),
+               "undo did not restore bonded terms");
+        EXPECT(t2.exclusions == topo.exclusions, "undo did not restore exclusions");
+    }
     std::printf(fails ? "DROPIN FAIL (%d)\n" : "DROPIN PASS\n", fails);
     return fails ? 1 : 0;
 }
