@@ -67,7 +67,7 @@ int hmdp_destroy(hmdp_ctx* ctx);
 /* Host-only model check (no device work): model_from_json + validate. */
 int hmdp_model_validate(const char* model_json, size_t len);
 
-/* Model facts: family (0 embed_fit, 1 message_passing), depth, rc, n_types,
+/* Model facts: family (0 embed_fit, 1 message_passing, 2 se_a, 3 repformer), depth, rc, n_types,
  * hidden, n_basis; receptive radius = depth * rc (model.hpp:51-52). */
 int hmdp_model_info(const hmdp_ctx* ctx, int* family, int* depth, double* rc, int* n_types,
                     int* hidden, int* n_basis);
@@ -236,6 +236,16 @@ int hmdp_peak_fp32(int device, int ms, double* tflops);
  * ------------------------------------------------------------------------- */
 long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_basis,
                           int hidden, uint64_t seed, char* buf, long cap);
+/* DeePMD-style families (no reference function; SURVEY.md §8(a')):
+ * family 2 = se_a (smooth env matrix, per-neighbour-type embedding, G^T R R^T G,
+ * fitting; depth 1), family 3 = repformer (se_a descriptor + depth-1 repformer
+ * layers with gated neighbour self-attention).  Same Rng / MLP init as
+ * hmdp_make_model_json; the JSON carries "family":"se_a"|"repformer".
+ * Every compute entry point accepts these models except hmdp_descriptors, the
+ * domain-decomposition phases, the per-stage outputs of hmdp_compute_csr, and
+ * (repformer) hmdp_compute_csr itself. */
+long hmdp_make_dp_model_json(int family, int depth, double rc, double rc_smooth, int n_types,
+                             int axis, uint64_t seed, char* buf, long cap);
 int hmdp_synthetic_system(int n, double density, double fraction_grouped, uint64_t seed,
                           double temperature, double* xyz, int* types, double* masses,
                           double* vel, double* box);

@@ -6,13 +6,13 @@ package is the host-side mirror of the reference's C++ NN force-provider API
 """
 from .nn import (ForceProvider, ModelFamily, NnCounters, NnInput, NnModel, NnOutput, Precision,
                  SimBox, build_input_periodic, context_for, Context, descriptors, evaluate,
-                 load_model, make_model, model_from_json, model_to_json, save_model,
+                 load_model, make_dp_model, make_model, model_from_json, model_to_json, save_model,
                  switch_derivative, switch_value)
 from .synthetic import PAPER_SYSTEMS, generate_synthetic_system, replicate
 
 __all__ = [
     "ForceProvider", "ModelFamily", "NnCounters", "NnInput", "NnModel", "NnOutput", "Precision",
     "SimBox", "build_input_periodic", "context_for", "Context", "descriptors", "evaluate",
-    "load_model", "make_model", "model_from_json", "model_to_json", "save_model",
+    "load_model", "make_dp_model", "make_model", "model_from_json", "model_to_json", "save_model",
     "switch_derivative", "switch_value", "PAPER_SYSTEMS", "generate_synthetic_system", "replicate",
 ]

@@ -67,6 +67,8 @@ SIGNATURES = {
                                     _vp, _vp]),
     "hmdp_make_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_int, _c_int, _c_int,
                                        ctypes.c_uint64, _vp, _c_long]),
+    "hmdp_make_dp_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_double, _c_int, _c_int,
+                                          ctypes.c_uint64, _vp, _c_long]),
     "hmdp_synthetic_system": (_c_int, [_c_int, _c_double, _c_double, ctypes.c_uint64, _c_double,
                                        _vp, _vp, _vp, _vp, _vp]),
 }

@@ -40,6 +40,9 @@ template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t);
 cudaError_t net_configure();
+template <typename T>
+int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWork<T>&, double*,
+              double*, double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
@@ -279,6 +282,96 @@ struct WeightSet {
     }
 };
 
+// Weights of the DeePMD-style families for one precision (hmdp_dp.cu): every
+// linear layer as W [out][in], W^T [in][out] and b.
+template <typename T>
+struct DpWeightSet {
+    DBuf buf;
+    DevDp<T> dev{};
+
+    void upload(const Model& m, cudaStream_t st) {
+        std::vector<T> host;
+        std::vector<size_t> offs;
+        auto push = [&](const std::vector<double>& v) {
+            while (host.size() % 32) host.push_back(T(0));
+            offs.push_back(host.size());
+            for (double x : v) host.push_back(static_cast<T>(x));
+        };
+        auto push_lin = [&](const std::vector<double>& w, const std::vector<double>& b, int out,
+                            int in) {
+            std::vector<double> t(w.size());
+            for (int o = 0; o < out; ++o)
+                for (int i = 0; i < in; ++i) t[static_cast<size_t>(i) * out + o] = w[o * in + i];
+            push(w);
+            push(t);
+            push(b);
+        };
+        auto push_mlp_layer = [&](const Mlp& p, int l) {
+            push_lin(p.weights[l], p.biases[l], p.sizes[l + 1], p.sizes[l]);
+        };
+        for (const Mlp& e : m.embeds) {
+            push(e.weights[0]);  // [32][1]
+            push(e.biases[0]);
+            push_mlp_layer(e, 1);
+        }
+        push_mlp_layer(m.fitting, 0);
+        push_mlp_layer(m.fitting, 1);
+        if (m.family == kRepformer) {
+            push_mlp_layer(m.g1map, 0);
+            push_mlp_layer(m.g1map, 1);
+            for (const RfLayer& L : m.rf) {
+                for (const Mlp* p : {&L.q, &L.k, &L.v, &L.o, &L.c}) push_mlp_layer(*p, 0);
+                push_mlp_layer(L.update, 0);
+                push_mlp_layer(L.update, 1);
+            }
+        }
+        while (host.size() % 32) host.push_back(T(0));
+        buf.ensure(host.size() * sizeof(T));
+        ck(cudaMemcpyAsync(buf.p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, st),
+           "weights H2D");
+        ck(cudaStreamSynchronize(st), "weights sync");
+        const T* base = buf.as<T>();
+        size_t q = 0;
+        auto next = [&]() { return base + offs[q++]; };
+        auto lin = [&]() {
+            DevLin<T> d;
+            d.W = next();
+            d.WT = next();
+            d.b = next();
+            return d;
+        };
+        dev = DevDp<T>{};
+        dev.family = m.family;
+        dev.rc = static_cast<T>(m.rc);
+        dev.rcs = static_cast<T>(m.rcs);
+        dev.inv_nnorm = static_cast<T>(1.0 / m.nnorm);
+        dev.n_types = m.n_types;
+        dev.n_layers = static_cast<int>(m.rf.size());
+        for (int t = 0; t < m.n_types; ++t) {
+            dev.emb_w1[t] = next();
+            dev.emb_b1[t] = next();
+            dev.emb2[t] = lin();
+            dev.ebias[t] = static_cast<T>(m.ebias[t]);
+        }
+        dev.fit1 = lin();
+        dev.fit2 = lin();
+        if (m.family == kRepformer) {
+            dev.map1 = lin();
+            dev.map2 = lin();
+            for (size_t l = 0; l < m.rf.size(); ++l) {
+                DevDpLayer<T>& L = dev.L[l];
+                L.q = lin();
+                L.k = lin();
+                L.v = lin();
+                L.o = lin();
+                L.c = lin();
+                L.u1 = lin();
+                L.u2 = lin();
+            }
+        }
+    }
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -291,6 +384,8 @@ struct hmdp_ctx {
     cudaStream_t stream = nullptr;
     WeightSet<float> wf;
     WeightSet<double> wd;
+    DpWeightSet<float> pf;  // DeePMD-style families (model.is_dp())
+    DpWeightSet<double> pd;
     int cap = 64;      // per-atom neighbour capacity (ELL)
     int ccap = 32;     // per-cell member capacity
     // atom / edge / cell buffers
@@ -299,6 +394,9 @@ struct hmdp_ctx {
     // network workspace
     DBuf er, es, eds, eb, edb, g, grev, zb, db, pe, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
+    // DeePMD-style families: vector edge gradients and the repformer workspace
+    DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
+        rf_Ts, rf_stat, rf_dob, rf_aux, rf_dconv, rf_dg1;
     // domain decomposition (hmdp_dd_*): local graph + halo row buffers
     DBuf dd_patom, dd_sremote, dd_sghost;
     DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
@@ -354,10 +452,14 @@ struct hmdp_ctx {
                         &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
-                        &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx})
+                        &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
+                        &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
+                        &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_dconv, &rf_dg1})
             b->release();
         wf.buf.release();
         wd.buf.release();
+        pf.buf.release();
+        pd.buf.release();
         pin.release();
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -529,10 +631,68 @@ struct hmdp_ctx {
         return gr;
     }
 
+    // Workspace of the DeePMD-style families (hmdp_dp.cu) on top of DevWork.
+    template <typename T>
+    DevDpWork<T> dp_work(int n, long long slots, DevWork<T>& w) {
+        const size_t na = static_cast<size_t>(std::max(n, 1));
+        const size_t s = static_cast<size_t>(std::max<long long>(slots, 1));
+        gv.ensure(s * 4 * sizeof(T));
+        gvrev.ensure(s * 4 * sizeof(T));
+        w.gv = gv.as<T>();
+        w.gvrev = gvrev.as<T>();
+        DevDpWork<T> d{};
+        if (model.family != kRepformer) return d;
+        const size_t L = model.rf.size();
+        rf_env.ensure(s * 8 * sizeof(T));
+        rf_g2.ensure((L + 1) * s * 32 * sizeof(T));
+        rf_qkv.ensure(s * 96 * sizeof(T));
+        rf_dg2.ensure(s * 32 * sizeof(T));
+        rf_dwh.ensure(s * 4 * sizeof(T));
+        rf_g1.ensure((L + 1) * na * 32 * sizeof(T));
+        rf_P.ensure(L * na * 32 * sizeof(T));
+        rf_uz.ensure(L * na * 32 * sizeof(T));
+        rf_mz.ensure(na * 32 * sizeof(T));
+        rf_D.ensure(na * 128 * sizeof(T));
+        rf_A.ensure(na * 128 * sizeof(T));
+        rf_Ts.ensure(L * na * 96 * sizeof(T));
+        rf_stat.ensure(L * s * 2 * sizeof(T));
+        rf_dob.ensure(s * 32 * sizeof(T));
+        rf_aux.ensure(s * 2 * sizeof(T));
+        rf_dconv.ensure(2 * na * 32 * sizeof(T));
+        rf_dg1.ensure(na * 32 * sizeof(T));
+        d.env = rf_env.as<T>();
+        d.g2 = rf_g2.as<T>();
+        d.qkv = rf_qkv.as<T>();
+        d.dg2 = rf_dg2.as<T>();
+        d.dwh = rf_dwh.as<T>();
+        d.g1 = rf_g1.as<T>();
+        d.P = rf_P.as<T>();
+        d.uz = rf_uz.as<T>();
+        d.mz = rf_mz.as<T>();
+        d.D = rf_D.as<T>();
+        d.A = rf_A.as<T>();
+        d.Ts = rf_Ts.as<T>();
+        d.stat = rf_stat.as<T>();
+        d.dob = rf_dob.as<T>();
+        d.aux = rf_aux.as<T>();
+        d.dconv = rf_dconv.as<T>();
+        d.dg1 = rf_dg1.as<T>();
+        return d;
+    }
+
     template <typename T>
     int network(const DevGraph& gr, long long slots, double* d_forces, double* d_per_atom,
                 cudaStream_t st, int* d_rev, const MdFuse& mf) {
         DevWork<T> w = work<T>(gr.n, slots);
+        if (model.is_dp()) {
+            const DevDpWork<T> d = dp_work<T>(gr.n, slots, w);
+            if constexpr (sizeof(T) == 4)
+                return launch_dp<float>(pf.dev, gr, w, d, d_forces, d_per_atom, out.as<double>(),
+                                        d_rev, st, marker(), mf);
+            else
+                return launch_dp<double>(pd.dev, gr, w, d, d_forces, d_per_atom, out.as<double>(),
+                                         d_rev, st, marker(), mf);
+        }
         if constexpr (sizeof(T) == 4)
             return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, out.as<double>(),
                                          d_rev, st, marker(), mf);
@@ -690,7 +850,10 @@ int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, i
         ck(net_configure(), "kernel smem configuration");
         ck(nbr_configure(), "kernel smem configuration");
         if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
-        if (has_model) {
+        if (has_model && ctx->model.is_dp()) {
+            ctx->pf.upload(ctx->model, ctx->stream);
+            ctx->pd.upload(ctx->model, ctx->stream);
+        } else if (has_model) {
             ctx->wf.upload(ctx->model, ctx->stream);
             ctx->wd.upload(ctx->model, ctx->stream);
         }
@@ -854,6 +1017,13 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
             if (nbr[e] < 0 || nbr[e] >= n)
                 fail(HMDP_INVALID_ARGUMENT, "NnInput edge neighbor out of range");
         check_types(n, types, ctx->model.n_types);
+        if (ctx->model.is_dp() && (desc || h || edge_g))
+            fail(HMDP_INVALID_ARGUMENT,
+                 "per-stage outputs are only available for the embed_fit / message_passing families");
+        if (ctx->model.family == kRepformer)
+            fail(HMDP_INVALID_ARGUMENT,
+                 "repformer runs on the periodic entry points (hmdp_compute, hmdp_compute_device, "
+                 "hmdp_md_*): its neighbour gathers need the symmetric list");
         // receptive-field check before compute (inference.cpp:188-193)
         const double needed = ctx->model.receptive_radius();
         if (!skip_coverage_check && coverage_radius < needed - 1e-12) {
@@ -1007,6 +1177,8 @@ int hmdp_descriptors(hmdp_ctx* ctx, int n, const int* types, const int* offset, 
             if (nbr[e] < 0 || nbr[e] >= n)
                 fail(HMDP_INVALID_ARGUMENT, "NnInput edge neighbor out of range");
         check_types(n, types, ctx->model.n_types);
+        if (ctx->model.is_dp())
+            fail(HMDP_INVALID_ARGUMENT, "descriptors() is defined for the halomd radial basis only");
         if (n == 0) return;
         set_device(ctx);
         ctx->ensure_atoms(n);
@@ -1108,6 +1280,10 @@ int hmdp_check(hmdp_ctx* ctx) {
 
 int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
     if (!ctx) return -1;
+    if (ctx->model.is_dp()) {  // bin + search + hmdp_dp.cu launches
+        const int L = static_cast<int>(ctx->model.rf.size());
+        return 2 + (ctx->model.family == kSeA ? 2 : 2 * L + 2);
+    }
     const int M = static_cast<int>(ctx->model.message.size());
     // bin + search + (embed_fit | embed + M fwd + (M-1) bwd + embed_bwd) + force
     return 2 + (M == 0 ? 1 : 2 + 2 * M - 1) + 1;
@@ -1357,6 +1533,9 @@ int hmdp_dd_setup(hmdp_ctx* ctx, int n_loc, int n_own, const int* offset, const 
                   const double* dr, const int* types, int precision) {
     return guarded([&] {
         need_model(ctx);
+        if (ctx->model.is_dp())
+            fail(HMDP_INVALID_ARGUMENT,
+                 "domain decomposition is implemented for the embed_fit / message_passing families");
         if (n_loc < 1 || n_own < 0 || n_own > n_loc || !offset || !types)
             fail(HMDP_INVALID_ARGUMENT, "bad arguments");
         const int ne = offset[n_loc];
@@ -1485,6 +1664,17 @@ long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_b
     const int code = guarded([&] {
         if (family != 0 && family != 1) fail(HMDP_INVALID_ARGUMENT, "family must be 0 or 1");
         s = model_to_json(make_model(family, depth, rc, n_types, n_basis, hidden, seed));
+    });
+    if (code) return -code;
+    if (buf && cap > static_cast<long>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<long>(s.size());
+}
+
+long hmdp_make_dp_model_json(int family, int depth, double rc, double rc_smooth, int n_types,
+                             int axis, uint64_t seed, char* buf, long cap) {
+    std::string s;
+    const int code = guarded([&] {
+        s = model_to_json(make_dp_model(family, depth, rc, rc_smooth, n_types, axis, seed));
     });
     if (code) return -code;
     if (buf && cap > static_cast<long>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);

@@ -115,6 +115,63 @@ struct DevWork {
     double* out;  // [16]: E, W, W9[9]
     long long slots;  // edge-slot capacity of the per-edge arrays
     unsigned* err;
+    // DeePMD-style families: dE/d(edge_dr) as a vector per edge slot ([slot][4],
+    // xyz + pad) and its mirror copy pushed by the edge's source (gv of rev(e) at
+    // slot e); the force kernel gathers both when gv != nullptr.
+    T* gv;
+    T* gvrev;
+};
+
+// ---------------------------------------------------------------------------
+// DeePMD-style families (se_a, repformer, hmdp_dp.cu).
+// Linear layer y = W x + b with W row-major [out][in] and its transpose.
+template <typename T>
+struct DevLin {
+    const T* W;   // [out][in]
+    const T* WT;  // [in][out]
+    const T* b;   // [out]
+};
+
+template <typename T>
+struct DevDpLayer {
+    DevLin<T> q, k, v, o, c;   // [32][32] each
+    DevLin<T> u1, u2;          // update MLP [32 + 4*32 -> 32 -> 32]
+};
+
+template <typename T>
+struct DevDp {
+    T rc, rcs, inv_nnorm;
+    int n_types, n_layers, family;  // family: kSeA / kRepformer
+    T ebias[kMaxTypes];
+    // per neighbour type embedding [1 -> 32 -> 32]: w1/b1 [32], layer 2 as DevLin
+    const T* emb_w1[kMaxTypes];
+    const T* emb_b1[kMaxTypes];
+    DevLin<T> emb2[kMaxTypes];
+    DevLin<T> fit1, fit2;  // fitting [in -> 32 -> 1]
+    DevLin<T> map1, map2;  // repformer g1 map [128 -> 32 -> 32]
+    DevDpLayer<T> L[kMaxMsg];
+};
+
+// Per-evaluation workspace of the repformer kernels (per edge slot / per atom).
+template <typename T>
+struct DevDpWork {
+    T* env;    // [slot][8]: s, w, h0, h1, h2, dsw, r, type (as T)
+    T* g2;     // [L+1][slot][32] edge channel g2 per layer (g2^{l+1} = after attention l)
+    T* qkv;    // [slot][96] q, k, v of the current layer
+    T* dg2;    // [slot][32] adjoint of g2 (in place, layer by layer)
+    T* dwh;    // [slot][4]  accumulated dE/dw, dE/dh (from every layer)
+    T* g1;     // [L+1][n][32]
+    T* P;      // [L][n][32] neighbour projections P^l = Wc g1^l + bc
+    T* uz;     // [L][n][32] update MLP hidden activations
+    T* mz;     // [n][32] g1 map hidden activations
+    T* D;      // [n][128] descriptor
+    T* A;      // [n][128] R^T G / nnorm (4 x 32)
+    T* Ts;     // [L][n][96] h^T g2 / nnorm per layer (3 x 32)
+    T* stat;   // [L][slot][2] softmax row max and normaliser per layer
+    T* dob;    // [slot][32] attention output adjoint do_e = Wo^T dg2hat_e
+    T* aux;    // [slot][2] row sums S_e = sum_f a_ef da_ef
+    T* dconv;  // [2][n][32] adjoint of conv_i / nnorm (double-buffered by layer)
+    T* dg1;    // [n][32] adjoint of g1 (residual part) of the current layer
 };
 
 // Optional per-kernel timing hook: called after every kernel launch with the

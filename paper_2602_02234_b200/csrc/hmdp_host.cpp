@@ -327,7 +327,47 @@ int Mlp::act_size() const {
     return s;
 }
 
+namespace {
+void validate_dp(const Model& m) {
+    // DeePMD-style families (no reference function).
+    auto shape = [](const Mlp& p, std::vector<int> want, const char* name) {
+        if (p.sizes != want)
+            throw std::invalid_argument(std::string("unsupported ") + name +
+                                        " MLP shape for this model family");
+    };
+    if (m.rc <= 0.0) throw std::invalid_argument("rc_model must be positive");
+    if (!(m.rcs >= 0.0 && m.rcs < m.rc))
+        throw std::invalid_argument("rc_smooth must satisfy 0 <= rc_smooth < rc_model");
+    if (m.n_types < 1) throw std::invalid_argument("n_types must be >= 1");
+    if (m.n_types > kMaxTypes) throw std::invalid_argument("unsupported n_types (kernels take <= 4)");
+    if (m.hidden != kH) throw std::invalid_argument("unsupported hidden width (kernels take H=32)");
+    if (m.axis != kAxis) throw std::invalid_argument("unsupported axis neurons (kernels take 4)");
+    if (!(m.nnorm > 0.0)) throw std::invalid_argument("nnorm must be positive");
+    if (static_cast<int>(m.embeds.size()) != m.n_types)
+        throw std::invalid_argument("one embedding net per neighbour type required");
+    for (const Mlp& e : m.embeds) shape(e, {1, kH, kH}, "embedding");
+    if (static_cast<int>(m.ebias.size()) != m.n_types)
+        throw std::invalid_argument("energy_bias must have n_types entries");
+    const int nd = m.axis * kH;
+    if (m.family == kSeA) {
+        shape(m.fitting, {nd, kH, 1}, "fitting");
+        if (!m.rf.empty()) throw std::invalid_argument("se_a model cannot carry repformer layers");
+        return;
+    }
+    if (m.rf.empty()) throw std::invalid_argument("repformer needs depth >= 2 (one layer or more)");
+    shape(m.g1map, {nd, kH, kH}, "g1map");
+    shape(m.fitting, {kH, kH, 1}, "fitting");
+    if (static_cast<int>(m.rf.size()) > kMaxMsg)
+        throw std::invalid_argument("unsupported depth (kernels take <= 9)");
+    for (const RfLayer& l : m.rf) {
+        for (const Mlp* p : {&l.q, &l.k, &l.v, &l.o, &l.c}) shape(*p, {kH, kH}, "attention");
+        shape(l.update, {kH + nd, kH, kH}, "update");
+    }
+}
+}  // namespace
+
 void Model::validate() const {
+    if (is_dp()) return validate_dp(*this);
     // NnModel::validate, model.cpp:30-48 (same messages).
     if (rc <= 0.0) throw std::invalid_argument("rc_model must be positive");
     if (n_types < 1) throw std::invalid_argument("n_types must be >= 1");
@@ -367,6 +407,32 @@ void Model::validate() const {
 
 void Model::counters(int n, int n_owned, long long ne, int real_bytes,
                      std::uint64_t out[2]) const {
+    if (is_dp()) {
+        // Algorithmic count in the reference's convention (forward + 2x forward
+        // for the reverse pass, inference.cpp:389-402), written out for the
+        // DeePMD-style operators: env matrix, embedding, R^T G, G^T R R^T G,
+        // fitting; repformer: q/k/v/o projections, attention over the n_e^2
+        // neighbour pairs of each atom (n_e = ne / n), conv, grrg, update.
+        const double H = kH, nd = axis * kH;
+        const double m2 = n > 0 ? static_cast<double>(ne) * ne / n : 0.0;
+        double fl = 0.0, act = 0.0;
+        fl += ne * (30.0 + 3.0 * embeds[0].forward_flops() + 3.0 * 2 * 4 * H);
+        fl += n * 3.0 * (2.0 * axis * 4 * H);
+        fl += n_owned * 3.0 * fitting.forward_flops();
+        act += static_cast<double>(ne) * (8 + 2 * H) + n * (nd + fitting.act_size());
+        if (family == kRepformer) {
+            fl += n * 3.0 * g1map.forward_flops();
+            for (const RfLayer& l : rf) {
+                fl += ne * 3.0 * (4.0 * l.q.forward_flops() + 6 * H);
+                fl += m2 * 3.0 * (4.0 * H + 12);
+                fl += n * 3.0 * (l.c.forward_flops() + 2.0 * 3 * axis * H + l.update.forward_flops());
+                act += static_cast<double>(ne) * 5 * H + m2 + n * (nd + 2 * H + l.update.act_size());
+            }
+        }
+        out[0] = static_cast<std::uint64_t>(fl);
+        out[1] = static_cast<std::uint64_t>(act) * static_cast<std::uint64_t>(real_bytes);
+        return;
+    }
     // inference.cpp:389-414
     const std::uint64_t K = n_basis(), H = hidden;
     std::uint64_t fl = 0, act = 0;
@@ -402,11 +468,48 @@ Model model_from_json(const std::string& text) {
     Model m;
     const JVal& fam = j.at("family");
     if (fam.kind == JVal::Str && fam.str == "embed_fit")
-        m.family = 0;
+        m.family = kEmbedFit;
     else if (fam.kind == JVal::Str && fam.str == "message_passing")
-        m.family = 1;
+        m.family = kMessagePassing;
+    else if (fam.kind == JVal::Str && fam.str == "se_a")
+        m.family = kSeA;
+    else if (fam.kind == JVal::Str && fam.str == "repformer")
+        m.family = kRepformer;
     else
         throw std::invalid_argument("unknown model family '" + fam.str + "'");
+    if (m.is_dp()) {
+        m.rc = j.at("rc_model").as_num();
+        m.rcs = j.at("rc_smooth").as_num();
+        m.n_types = j.at("n_types").as_int();
+        m.hidden = j.at("hidden").as_int();
+        m.axis = j.at("axis").as_int();
+        m.nnorm = j.at("nnorm").as_num();
+        if (const JVal* s = j.find("seed"); s && s->kind == JVal::Num)
+            m.seed = static_cast<std::uint64_t>(s->num);
+        const JVal& em = j.at("embeddings");
+        if (em.kind != JVal::Arr) throw std::invalid_argument("model JSON: embeddings must be an array");
+        for (const auto& e : em.arr) m.embeds.push_back(mlp_from(e));
+        m.ebias = j.at("energy_bias").as_vec();
+        m.fitting = mlp_from(j.at("fitting"));
+        if (m.family == kRepformer) {
+            m.g1map = mlp_from(j.at("g1map"));
+            const JVal& layers = j.at("layers");
+            if (layers.kind != JVal::Arr)
+                throw std::invalid_argument("model JSON: layers must be an array");
+            for (const auto& jl : layers.arr) {
+                RfLayer l;
+                l.q = mlp_from(jl.at("q"));
+                l.k = mlp_from(jl.at("k"));
+                l.v = mlp_from(jl.at("v"));
+                l.o = mlp_from(jl.at("o"));
+                l.c = mlp_from(jl.at("c"));
+                l.update = mlp_from(jl.at("update"));
+                m.rf.push_back(std::move(l));
+            }
+        }
+        m.validate();
+        return m;
+    }
     m.rc = j.at("rc_model").as_num();
     m.n_types = j.at("n_types").as_int();
     m.hidden = j.at("hidden").as_int();
@@ -426,7 +529,58 @@ Model model_from_json(const std::string& text) {
     return m;
 }
 
+namespace {
+std::string dp_to_json(const Model& m) {
+    std::string o;
+    o.reserve(400000);
+    o += "{\"format\":\"halomd-model\",\"version\":1,\"family\":\"";
+    o += m.family == kSeA ? "se_a" : "repformer";
+    o += "\",\"rc_model\":";
+    put_num(o, m.rc);
+    o += ",\"rc_smooth\":";
+    put_num(o, m.rcs);
+    o += ",\"n_types\":" + std::to_string(m.n_types);
+    o += ",\"hidden\":" + std::to_string(m.hidden);
+    o += ",\"axis\":" + std::to_string(m.axis);
+    o += ",\"nnorm\":";
+    put_num(o, m.nnorm);
+    o += ",\"seed\":" + std::to_string(m.seed);
+    o += ",\"embeddings\":[";
+    for (std::size_t t = 0; t < m.embeds.size(); ++t) {
+        if (t) o += ',';
+        put_mlp(o, m.embeds[t]);
+    }
+    o += "],\"energy_bias\":";
+    put_vec(o, m.ebias);
+    o += ",\"fitting\":";
+    put_mlp(o, m.fitting);
+    if (m.family == kRepformer) {
+        o += ",\"g1map\":";
+        put_mlp(o, m.g1map);
+        o += ",\"layers\":[";
+        for (std::size_t l = 0; l < m.rf.size(); ++l) {
+            if (l) o += ',';
+            const RfLayer& L = m.rf[l];
+            const std::pair<const char*, const Mlp*> parts[] = {{"q", &L.q}, {"k", &L.k},
+                                                                {"v", &L.v}, {"o", &L.o},
+                                                                {"c", &L.c}, {"update", &L.update}};
+            o += '{';
+            for (int p = 0; p < 6; ++p) {
+                if (p) o += ',';
+                o += std::string("\"") + parts[p].first + "\":";
+                put_mlp(o, *parts[p].second);
+            }
+            o += '}';
+        }
+        o += ']';
+    }
+    o += '}';
+    return o;
+}
+}  // namespace
+
 std::string model_to_json(const Model& m) {
+    if (m.is_dp()) return dp_to_json(m);
     std::string o;
     o.reserve(400000);
     o += "{\"format\":\"halomd-model\",\"version\":1,\"family\":\"";
@@ -479,6 +633,43 @@ Model make_model(int family, int depth, double rc, int n_types, int n_basis, int
     for (int l = 1; l < depth; ++l) {
         m.message.push_back(random_mlp({hidden + n_basis, hidden, hidden}, rng));
         m.update.push_back(random_mlp({2 * hidden, hidden, hidden}, rng));
+    }
+    m.validate();
+    return m;
+}
+
+Model make_dp_model(int family, int depth, double rc, double rcs, int n_types, int axis,
+                    std::uint64_t seed) {
+    if (family != kSeA && family != kRepformer)
+        throw std::invalid_argument("make_dp_model: family must be se_a or repformer");
+    if (depth < 1) throw std::invalid_argument("depth must be >= 1");
+    if (family == kSeA && depth != 1) throw std::invalid_argument("se_a has depth 1 by construction");
+    Model m;
+    m.family = family;
+    m.rc = rc;
+    m.rcs = rcs;
+    m.n_types = n_types;
+    m.hidden = kH;
+    m.axis = axis;
+    m.nnorm = 32.0;
+    m.seed = seed;
+    Rng rng(seed);
+    for (int t = 0; t < n_types; ++t) m.embeds.push_back(random_mlp({1, kH, kH}, rng));
+    const int nd = axis * kH;
+    m.fitting = random_mlp({family == kSeA ? nd : kH, kH, 1}, rng);
+    for (int t = 0; t < n_types; ++t) m.ebias.push_back(rng.uniform(-1.0, 1.0));
+    if (family == kRepformer) {
+        m.g1map = random_mlp({nd, kH, kH}, rng);
+        for (int l = 1; l < depth; ++l) {
+            RfLayer L;
+            L.q = random_mlp({kH, kH}, rng);
+            L.k = random_mlp({kH, kH}, rng);
+            L.v = random_mlp({kH, kH}, rng);
+            L.o = random_mlp({kH, kH}, rng);
+            L.c = random_mlp({kH, kH}, rng);
+            L.update = random_mlp({kH + nd, kH, kH}, rng);
+            m.rf.push_back(std::move(L));
+        }
     }
     m.validate();
     return m;

@@ -1135,6 +1135,39 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
         const int start = gr.row_start[i], cnt = gr.nnei[i];
+        if (ws.gv) {  // DeePMD-style families: vector dE/d(edge_dr) (hmdp_dp.cu)
+            //   F_i = sum_q (gv_q - gv_rev(q));  W_ab = -sum_q dr_a gv_b
+            for (int q = lane; q < cnt; q += 32) {
+                const int e = start + q;
+                const V4<T> g = ld4c(ws.gv + 4ll * e);
+                const double* d = gr.dr + 3ll * e;
+                const double g3[3] = {static_cast<double>(g.x), static_cast<double>(g.y),
+                                      static_cast<double>(g.z)};
+                fx += g3[0];
+                fy += g3[1];
+                fz += g3[2];
+                if (gr.sym) {
+                    const V4<T> m = ld4c(ws.gvrev + 4ll * e);
+                    fx -= static_cast<double>(m.x);
+                    fy -= static_cast<double>(m.y);
+                    fz -= static_cast<double>(m.z);
+                }
+                acc[1] -= d[0] * g3[0] + d[1] * g3[1] + d[2] * g3[2];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) acc[2 + 3 * a + b] -= d[a] * g3[b];
+            }
+            if (!gr.sym) {
+                const int is = gr.in_start[i], ic = gr.in_cnt[i];
+                for (int q = lane; q < ic; q += 32) {
+                    const V4<T> m = ld4c(ws.gvrev + 4ll * (is + q));
+                    fx -= static_cast<double>(m.x);
+                    fy -= static_cast<double>(m.y);
+                    fz -= static_cast<double>(m.z);
+                }
+            }
+        } else {
         for (int q = lane; q < cnt; q += 32) {
             const int e = start + q;
             const T gg = ws.g[e];
@@ -1166,6 +1199,7 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                 fy -= static_cast<double>((y / r) * gg);
                 fz -= static_cast<double>((z / r) * gg);
             }
+        }
         }
         fx = warp_sum(fx);
         fy = warp_sum(fy);
@@ -1442,6 +1476,18 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
     mk("force", st);
     return launches + 1;
 }
+
+// Force kernel alone (the DeePMD-style families' last phase, hmdp_dp.cu).
+template <typename T>
+void launch_force(const DevGraph& gr, const DevWork<T>& ws, double* forces, double* per_atom,
+                  double* out, cudaStream_t st, const MdFuse& mf) {
+    launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
+               per_atom, out, mf);
+}
+template void launch_force<float>(const DevGraph&, const DevWork<float>&, double*, double*,
+                                  double*, cudaStream_t, const MdFuse&);
+template void launch_force<double>(const DevGraph&, const DevWork<double>&, double*, double*,
+                                   double*, cudaStream_t, const MdFuse&);
 
 // Device MD: (E, W, W_ab) of the last step from the force kernel's CTA partials.
 void launch_reduce_partials(const double* partial, int n, double* out, cudaStream_t st) {

@@ -28,10 +28,15 @@ from ._lib import check, lib, ptr
 
 
 class ModelFamily(enum.IntEnum):
-    """model.hpp:9 ``enum class ModelFamily { embed_fit, message_passing }``."""
+    """model.hpp:9 ``enum class ModelFamily { embed_fit, message_passing }``, plus the
+    DeePMD-style families of the north star that have no reference function
+    (SURVEY.md §8(a')): ``se_a`` (smooth env matrix, G^T R R^T G) and
+    ``repformer`` (DPA2-style gated neighbour self-attention)."""
 
     embed_fit = 0
     message_passing = 1
+    se_a = 2
+    repformer = 3
 
 
 class Precision(enum.IntEnum):
@@ -57,7 +62,10 @@ class NnModel:
     # model.hpp fields
     @property
     def family(self) -> ModelFamily:
-        return ModelFamily.embed_fit if self._d["family"] == "embed_fit" else ModelFamily.message_passing
+        return ModelFamily[self._d["family"]]
+
+    def is_dp(self) -> bool:
+        return self.family >= ModelFamily.se_a
 
     @property
     def rc_model(self) -> float:
@@ -84,18 +92,28 @@ class NnModel:
         return float(self._d["basis"]["width"])
 
     def depth(self) -> int:
-        return 1 + len(self._d["layers"])
+        return 1 + len(self._d.get("layers", []))
 
     def receptive_radius(self) -> float:
         return self.depth() * self.rc_model
 
     def descriptor_dim(self) -> int:
+        if self.is_dp():
+            return int(self._d["axis"]) * self.hidden
         return self.n_types * len(self.basis_centers)
 
     def n_params(self) -> int:
         def mlp(m):
             return sum(len(w) for w in m["weights"]) + sum(len(b) for b in m["biases"])
 
+        if self.is_dp():
+            n = sum(mlp(e) for e in self._d["embeddings"]) + mlp(self._d["fitting"])
+            n += len(self._d["energy_bias"])
+            if "g1map" in self._d:
+                n += mlp(self._d["g1map"])
+            for layer in self._d.get("layers", []):
+                n += sum(mlp(v) for v in layer.values())
+            return n
         n = mlp(self._d["embedding"]) + mlp(self._d["fitting"])
         for layer in self._d["layers"]:
             n += mlp(layer["message"]) + mlp(layer["update"])
@@ -119,6 +137,21 @@ def make_model(family: ModelFamily, depth: int, rc_model: float, n_types: int, n
         check(-need)
     buf = ctypes.create_string_buffer(need + 1)
     L.hmdp_make_model_json(*args, buf, need + 1)
+    return NnModel(buf.value.decode())
+
+
+def make_dp_model(family: ModelFamily, depth: int, rc_model: float = 0.6, rc_smooth: float = 0.3,
+                  n_types: int = 2, seed: int = 1, axis: int = 4) -> NnModel:
+    """Random-init DeePMD-style model (se_a: depth 1; repformer: depth - 1 layers),
+    same Rng / MLP init as make_model.  No reference function (parity unpinned)."""
+    L = lib()
+    args = (int(family), int(depth), float(rc_model), float(rc_smooth), int(n_types), int(axis),
+            ctypes.c_uint64(seed))
+    need = L.hmdp_make_dp_model_json(*args, None, 0)
+    if need < 0:
+        check(-need)
+    buf = ctypes.create_string_buffer(need + 1)
+    L.hmdp_make_dp_model_json(*args, buf, need + 1)
     return NnModel(buf.value.decode())
 
 
