@@ -37,7 +37,18 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-MODELS = {"dpa2": (0, 1), "dpa3": (1, 3)}
+# name -> (family, depth): the reference's two toy families (DPA2 / DPA3 analogs)
+# and the DeePMD-style families of the north star (no reference function,
+# DESIGN.md §11): se_a (smooth env matrix, G^T R R^T G) and a 2-layer repformer
+# (DPA2-style gated neighbour self-attention).
+MODELS = {"dpa2": (0, 1), "dpa3": (1, 3), "se_a": (2, 1), "repformer": (3, 3)}
+
+
+def make_bench_model(P, name):
+    fam, depth = MODELS[name]
+    if fam >= 2:
+        return P.make_dp_model(P.ModelFamily(fam), depth, 0.6, 0.3, 2, 1)
+    return P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
 SYSTEMS = {"1YRF": 582, "1UBQ": 1231, "3LZM": 2643, "2PTC": 4114}
 METRIC = "DPA2/DPA3 force-eval steps/s & ns/day at 1/2/4/8 B200 vs CPU ref; %roofline"
 
@@ -71,7 +82,31 @@ def mlp_flops(sizes):
     return sum(2 * a * b + 4 * b for a, b in zip(sizes[:-1], sizes[1:]))
 
 
-def kernel_flops(model_dict, n, n_owned, ne):
+def dp_kernel_flops(d, n, ne, m2):
+    """Algorithmic FLOPs per kernel of the DeePMD-style families (hmdp_dp.cu), in
+    the reference counter's convention (forward, reverse = 2x forward): env
+    matrix 30/edge, per-edge embedding MLP, R^T G (8H/edge), G^T R R^T G, MLPs by
+    mlp_flops; repformer attention 4H+5 per neighbour pair (m2 = sum_i n_i^2)."""
+    H = d["hidden"]
+    ax = d["axis"]
+    fe = mlp_flops(d["embeddings"][0]["sizes"])
+    ff = mlp_flops(d["fitting"]["sizes"])
+    desc = ne * (30 + fe + 8 * H) + n * (2 * ax * 4 * H)
+    if d["family"] == "se_a":
+        return {"sea": 3 * desc + 3 * n * ff}
+    fmap = mlp_flops(d["g1map"]["sizes"])
+    lay = d["layers"][0]
+    fq = mlp_flops(lay["q"]["sizes"])
+    fu = mlp_flops(lay["update"]["sizes"])
+    fwd = ne * (4 * fq + 6 * H) + m2 * (4 * H + 5) + n * (fq + 2 * 3 * ax * H + fu)
+    emb = desc + n * fmap
+    return {"rf_embed": emb, "rf_fwd": fwd, "rf_top": 3 * fwd + 3 * n * ff, "rf_bwd": 2 * fwd,
+            "rf_embed_bwd": 2 * emb}
+
+
+def kernel_flops(model_dict, n, n_owned, ne, m2=0):
+    if model_dict["family"] in ("se_a", "repformer"):
+        return dp_kernel_flops(model_dict, n, ne, m2)
     H = model_dict["hidden"]
     K = len(model_dict["basis"]["centers"])
     fe = mlp_flops(model_dict["embedding"]["sizes"])
@@ -164,6 +199,30 @@ def reference_md(model_name, system, steps, warmup, precision, threads, replicas
     s = P.generate_synthetic_system(SYSTEMS[system])
     if tuple(replicas) != (1, 1, 1):
         s = P.replicate(s, replicas)
+    if fam >= 2:
+        # no reference implementation exists for the DeePMD-style families: the
+        # FP64 oracle (torch autograd on the host cores) is the CPU path
+        import torch
+
+        from oracle import dpfamily as DF
+
+        torch.set_num_threads(threads)
+        m = make_bench_model(P, model_name).as_dict()
+        x, v = s.positions.copy(), s.velocities.copy()
+        half, dt = 0.0005, 0.001
+
+        def force(x):
+            return DF.evaluate(m, s.types, *O.neighbors(x, s.box, 0.6))["forces"]
+
+        f = force(x)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            v += f * (half / s.masses[:, None])
+            x += v * dt
+            f = force(x)
+            v += f * (half / s.masses[:, None])
+        wall = time.perf_counter() - t0
+        return steps / wall, wall, "port"
     if O.ref_available():
         rm = O.RefModel(O.ref_model_json(fam, depth))
         kind = "reference"
@@ -243,9 +302,8 @@ def run_ours(args, rank, world, local_rank, dist):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     L = lib()
-    fam, depth = MODELS[args.model]
     prec = P.Precision[args.precision]
-    model = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
+    model = make_bench_model(P, args.model)
     s = P.generate_synthetic_system(SYSTEMS[args.system])
     reps = tuple(int(v) for v in args.replicas.split(","))
     if reps != (1, 1, 1):
@@ -255,6 +313,7 @@ def run_ours(args, rank, world, local_rank, dist):
     check(L.hmdp_set_stream(ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
     inp = P.build_input_periodic(s.positions, s.types, np.arange(n), s.box, 0.6, device=local_rank)
     ne = int(inp.edge_offset[-1])
+    m2 = int(np.sum(np.diff(inp.edge_offset).astype(np.int64) ** 2))
     # per MD step: search + network + force (the cell binning and both velocity-Verlet
     # halves are fused into the force kernel; kernels_per_eval counts the binning)
     per_step_kernels = ctx.kernels_per_eval() - 1
@@ -335,7 +394,7 @@ def run_ours(args, rank, world, local_rank, dist):
     if sampler:
         clocks = sampler.stop()
     kern_ms = {k: sums[k] / counts[k] for k in sums}
-    kflops = kernel_flops(model.as_dict(), n, n, ne)
+    kflops = kernel_flops(model.as_dict(), n, n, ne, m2)
     # FLOP-carrying kernels; the dominant one is the slowest of them
     cands = {k: v for k, v in kern_ms.items() if k in kflops}
     dom = max(cands, key=cands.get)
@@ -394,14 +453,19 @@ def run_ours(args, rank, world, local_rank, dist):
     if world == 1 and not args.no_cpu_baseline:
         threads = cpu_count()
         # bounded sample: ~cpu_seconds of wall on all host threads
-        per_step = 0.2 if args.model == "dpa3" else 0.012
+        per_step = {"dpa3": 0.2, "dpa2": 0.012, "se_a": 0.03, "repformer": 0.06}[args.model]
         per_step *= n / 582
         steps_cpu = max(2, int(args.cpu_seconds / per_step))
         sps, cwall, kind = reference_md(args.model, args.system, steps_cpu, 1, args.precision,
                                         threads, reps)
-        cpu = {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind,
-               "sample": f"{steps_cpu} MD steps x {threads} concurrent replicas of the same "
-                         f"{n}-atom box, {args.precision}, {cwall:.1f} s wall"}
+        if MODELS[args.model][0] >= 2:
+            sample = (f"{steps_cpu} MD steps of one {n}-atom box through the FP64 torch oracle "
+                      f"(no reference implementation of this family), {threads} threads, "
+                      f"{cwall:.1f} s wall")
+        else:
+            sample = (f"{steps_cpu} MD steps x {threads} concurrent replicas of the same "
+                      f"{n}-atom box, {args.precision}, {cwall:.1f} s wall")
+        cpu = {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind, "sample": sample}
 
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K,
@@ -455,9 +519,8 @@ def run_dd(args, rank, world, local_rank, dist):
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    fam, depth = MODELS[args.model]
     prec = P.Precision[args.precision]
-    model = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
+    model = make_bench_model(P, args.model)
     base = P.generate_synthetic_system(SYSTEMS[args.system])
     dims = dd.rank_grid(world)
     s = P.replicate(base, dims)

@@ -40,6 +40,7 @@ template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t);
 cudaError_t net_configure();
+cudaError_t dp_configure();
 template <typename T>
 int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWork<T>&, double*,
               double*, double*, int*, cudaStream_t, const Marker&, const MdFuse&);
@@ -396,7 +397,7 @@ struct hmdp_ctx {
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // DeePMD-style families: vector edge gradients and the repformer workspace
     DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
-        rf_Ts, rf_stat, rf_dob, rf_aux, rf_dconv, rf_dg1;
+        rf_Ts, rf_stat, rf_dob, rf_aux, rf_tmp, rf_dconv, rf_dg1;
     // domain decomposition (hmdp_dd_*): local graph + halo row buffers
     DBuf dd_patom, dd_sremote, dd_sghost;
     DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
@@ -454,7 +455,7 @@ struct hmdp_ctx {
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
                         &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
-                        &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_dconv, &rf_dg1})
+                        &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -658,6 +659,7 @@ struct hmdp_ctx {
         rf_stat.ensure(L * s * 2 * sizeof(T));
         rf_dob.ensure(s * 32 * sizeof(T));
         rf_aux.ensure(s * 2 * sizeof(T));
+        rf_tmp.ensure(s * 96 * sizeof(T));
         rf_dconv.ensure(2 * na * 32 * sizeof(T));
         rf_dg1.ensure(na * 32 * sizeof(T));
         d.env = rf_env.as<T>();
@@ -675,6 +677,7 @@ struct hmdp_ctx {
         d.stat = rf_stat.as<T>();
         d.dob = rf_dob.as<T>();
         d.aux = rf_aux.as<T>();
+        d.tmp = rf_tmp.as<T>();
         d.dconv = rf_dconv.as<T>();
         d.dg1 = rf_dg1.as<T>();
         return d;
@@ -849,6 +852,7 @@ int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, i
         ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
         ck(net_configure(), "kernel smem configuration");
         ck(nbr_configure(), "kernel smem configuration");
+        ck(dp_configure(), "kernel smem configuration");
         if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
         if (has_model && ctx->model.is_dp()) {
             ctx->pf.upload(ctx->model, ctx->stream);

@@ -170,8 +170,10 @@ struct DevDpWork {
     T* stat;   // [L][slot][2] softmax row max and normaliser per layer
     T* dob;    // [slot][32] attention output adjoint do_e = Wo^T dg2hat_e
     T* aux;    // [slot][2] row sums S_e = sum_f a_ef da_ef
+    T* tmp;    // [slot][96] attention output o_e (forward); dq, dk, dv (backward)
     T* dconv;  // [2][n][32] adjoint of conv_i / nnorm (double-buffered by layer)
     T* dg1;    // [n][32] adjoint of g1 (residual part) of the current layer
+    int smem_rows;  // 1: per-atom q/k/v and do rows live in shared memory (ELL cap <= 64)
 };
 
 // Optional per-kernel timing hook: called after every kernel launch with the

@@ -455,17 +455,132 @@ __global__ __launch_bounds__(kDpCTA) void k_sea(DevDp<T> md, DevGraph gr, DevWor
 }
 
 // ---------------------------------------------------------------------------
-// repformer: embedding + descriptor + g1 map + P^0 (one warp per atom).
+// repformer: ONE ATOM PER CTA (a team of 4 warps, 128 threads), grid-stride.
+//   * per-edge 32x32 projections (q, k, v, o and their transposes): warp w takes
+//     the atom's edges q = w, w+4, ...; lane c keeps row c of the matrix in
+//     registers and reads the edge's input row at a uniform address (broadcast);
+//   * attention: a QUAD of lanes per edge row (lane 4r + p holds channels
+//     8p..8p+7 of row r), 32 rows per pass; the q.k and do.v dot products are
+//     8 FMAs + 2 quad shuffles; the loop over the atom's neighbours f keeps an
+//     online softmax (running max / sum); the backward runs a row pass
+//     (dq, row-side dw/dh) and a column pass (dk, dv, column-side dw/dh);
+//   * atom-level vectors (conv, grrg, update MLP, fitting, g1 map) by warp 0
+//     from per-warp partials summed in a fixed order in shared memory.
 // ---------------------------------------------------------------------------
+constexpr int kRfT = 128;
+constexpr double kInvSqrt32 = 0.17677669529663688;  // 1 / sqrt(32)
+
 template <typename T>
-__global__ __launch_bounds__(kDpCTA) void k_rf_embed(DevDp<T> md, DevGraph gr, DevWork<T> ws,
-                                                     DevDpWork<T> dw, int* __restrict__ rev,
-                                                     MdFuse mf) {
-    __shared__ DpWarpSmem s_w[kDpWarps];
+struct RfSmem {
+    T x[160];       // MLP input staging (warp 0)
+    T red[4][128];  // per-warp partial sums
+    T bc[128];      // values broadcast to the team (dconv + dT, dA)
+};
+
+// out_q = [res_q] + b + W x_q over the atom's cnt edge rows (warp w: q = w, w+4,
+// ...), W [32][32] row-major (lane c holds row c); rows of 32 at `in + q*ld_in`,
+// `out + q*ld_out` (local row index q; shared or global memory); ADD accumulates
+// into out instead of a residual.  Two rows per iteration (loads in flight).
+template <typename T, bool ADD>
+__device__ __forceinline__ void proj(const T* __restrict__ W, const T* __restrict__ b,
+                                     const T* in, int ld_in, const T* res, int ld_res, T* out,
+                                     int ld_out, int cnt) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T wr[32];
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+        const V4<T> v = ld4(W + lane * 32 + k);
+        wr[k] = v.x;
+        wr[k + 1] = v.y;
+        wr[k + 2] = v.z;
+        wr[k + 3] = v.w;
+    }
+    const T bb = b ? __ldg(b + lane) : T(0);
+#pragma unroll 1
+    for (int q = w; q < cnt; q += 8) {
+        const bool two = q + 4 < cnt;
+        const T* x = in + (long long)q * ld_in;
+        const T* y = in + (long long)(two ? q + 4 : q) * ld_in;
+        T a0 = bb, a1 = T(0), c0 = bb, c1 = T(0);
+#pragma unroll
+        for (int k = 0; k < 32; k += 8) {
+            const V4<T> u = ld4c(x + k), v = ld4c(x + k + 4);
+            const V4<T> u2 = ld4c(y + k), v2 = ld4c(y + k + 4);
+            a0 += wr[k] * u.x + wr[k + 1] * u.y + wr[k + 2] * u.z + wr[k + 3] * u.w;
+            a1 += wr[k + 4] * v.x + wr[k + 5] * v.y + wr[k + 6] * v.z + wr[k + 7] * v.w;
+            c0 += wr[k] * u2.x + wr[k + 1] * u2.y + wr[k + 2] * u2.z + wr[k + 3] * u2.w;
+            c1 += wr[k + 4] * v2.x + wr[k + 5] * v2.y + wr[k + 6] * v2.z + wr[k + 7] * v2.w;
+        }
+        T* o = out + (long long)q * ld_out + lane;
+        if (ADD) *o += a0 + a1;
+        else *o = (res ? res[(long long)q * ld_res + lane] : T(0)) + a0 + a1;
+        if (two) {
+            T* o2 = out + (long long)(q + 4) * ld_out + lane;
+            if (ADD) *o2 += c0 + c1;
+            else *o2 = (res ? res[(long long)(q + 4) * ld_res + lane] : T(0)) + c0 + c1;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T quad_sum(T v) {
+    v += __shfl_xor_sync(FULL_MASK, v, 1);
+    return v + __shfl_xor_sync(FULL_MASK, v, 2);
+}
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, T (&x)[8]) {
+    const V4<T> a = ld4c(p), b = ld4c(p + 4);
+    x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const T (&x)[8]) {
+    st4(p, x[0], x[1], x[2], x[3]);
+    st4(p + 4, x[4], x[5], x[6], x[7]);
+}
+template <typename T>
+__device__ __forceinline__ T dot8(const T (&a)[8], const T* p) {
+    const V4<T> u = ld4c(p), v = ld4c(p + 4);
+    return (a[0] * u.x + a[1] * u.y + a[2] * u.z + a[3] * u.w) +
+           (a[4] * v.x + a[5] * v.y + a[6] * v.z + a[7] * v.w);
+}
+
+// Per-atom q/k/v and attention-output-adjoint rows: in the CTA's dynamic shared
+// memory when the ELL capacity fits (kRfSmemRows rows: 64 x 128 values), else
+// in the global per-slot scratch (capacity grown for dense clusters).
+constexpr int kRfSmemRows = 64;
+template <typename T>
+__device__ __forceinline__ T* rf_smem_rows() {
+    extern __shared__ __align__(16) unsigned char rf_dyn[];
+    return reinterpret_cast<T*>(rf_dyn);
+}
+template <typename T>
+__device__ __forceinline__ T* rf_rows_qkv(const DevDpWork<T>& dw, int start) {
+    return dw.smem_rows ? rf_smem_rows<T>() : dw.qkv + 96ll * start;
+}
+template <typename T>
+__device__ __forceinline__ T* rf_rows_dob(const DevDpWork<T>& dw, int start) {
+    return dw.smem_rows ? rf_smem_rows<T>() + 96 * kRfSmemRows : dw.dob + 32ll * start;
+}
+
+// Per-edge env row: s, w, h0, h1 | h2, dsw, r, type.
+template <typename T>
+struct EnvRow {
+    T s, w, h0, h1, h2;
+};
+template <typename T>
+__device__ __forceinline__ EnvRow<T> env_row(const T* env, long long e) {
+    const V4<T> a = ld4c(env + 8 * e);
+    return {a.x, a.y, a.z, a.w, env[8 * e + 4]};
+}
+
+// embedding + descriptor + g1 map + P^0, one atom per CTA
+template <typename T>
+__global__ __launch_bounds__(kRfT) void k_rf_embed(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+                                                   DevDpWork<T> dw, int* __restrict__ rev,
+                                                   MdFuse mf) {
+    __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
-    const WarpIdx wi;
-    const int lane = wi.lane;
-    DpWarpSmem& sm = s_w[wi.wid];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     T w1[kMaxTypes], b1[kMaxTypes], b2[kMaxTypes];
 #pragma unroll
     for (int t = 0; t < kMaxTypes; ++t) {
@@ -473,13 +588,12 @@ __global__ __launch_bounds__(kDpCTA) void k_rf_embed(DevDp<T> md, DevGraph gr, D
         b1[t] = t < md.n_types ? md.emb_b1[t][lane] : T(0);
         b2[t] = t < md.n_types ? md.emb2[t].b[lane] : T(0);
     }
-    const long long S = ws.slots;
     pdl_wait();
     zero_cells(mf);
-    for (int i = wi.first; i < gr.n_active; i += wi.stride) {
+    for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
-        T A[4] = {T(0), T(0), T(0), T(0)};
-        for (int base = 0; base < cnt; base += 32) {
+        // env rows + mirror slots (warp w: edge chunks 32 w + 128 k)
+        for (int base = 32 * w; base < cnt; base += kRfT) {
             const int m = min(32, cnt - base);
             const int e = start + base + lane;
             int j = 0;
@@ -487,16 +601,9 @@ __global__ __launch_bounds__(kDpCTA) void k_rf_embed(DevDp<T> md, DevGraph gr, D
                 j = gr.nbr[e];
                 const Env<T> v = dp_env<T>(gr.dr + 3ll * e, md.rc, md.rcs);
                 if (!(v.r > T(0))) atomicOr(ws.err, kErrZeroEdge);
-                const int t = gr.ety[e];
-                sm.s[lane] = v.s;
-                sm.R[lane][0] = v.s;
-                sm.R[lane][1] = v.s * v.ux;
-                sm.R[lane][2] = v.s * v.uy;
-                sm.R[lane][3] = v.s * v.uz;
-                sm.t[lane] = t;
                 T* en = dw.env + 8ll * e;
                 st4(en, v.s, v.sw, v.s * v.ux, v.s * v.uy);
-                st4(en + 4, v.s * v.uz, v.dsw, v.r, static_cast<T>(t));
+                st4(en + 4, v.s * v.uz, v.dsw, v.r, static_cast<T>(gr.ety[e]));
             }
             if (rev) {
                 const int f = find_rev(i, j, m, gr);
@@ -505,413 +612,421 @@ __global__ __launch_bounds__(kDpCTA) void k_rf_embed(DevDp<T> md, DevGraph gr, D
                     if (f < 0) atomicOr(ws.err, kErrAsymmetric);
                 }
             }
-            __syncwarp();
-            for (int u = 0; u < m; ++u) {
-                const int t = sm.t[u];
-                const T s = static_cast<T>(sm.s[u]);
-                T z = T(0), bb = T(0);
-                const T* W2T = md.emb2[0].WT;
+        }
+        __syncthreads();
+        // embedding G_e (lane = channel) and R^T G partials
+        T A[4] = {T(0), T(0), T(0), T(0)};
+        for (int q = w; q < cnt; q += 4) {
+            const long long e = start + q;
+            const V4<T> a = ld4c(dw.env + 8 * e), b = ld4c(dw.env + 8 * e + 4);
+            const int t = static_cast<int>(b.w);
+            T z = T(0), bb = T(0);
+            const T* W2T = md.emb2[0].WT;
 #pragma unroll
-                for (int tt = 0; tt < kMaxTypes; ++tt)
-                    if (tt == t) {
-                        z = d_tanh(w1[tt] * s + b1[tt]);
-                        bb = b2[tt];
-                        W2T = md.emb2[tt].WT;
-                    }
-                T G = bb;
+            for (int tt = 0; tt < kMaxTypes; ++tt)
+                if (tt == t) {
+                    z = d_tanh(w1[tt] * a.x + b1[tt]);
+                    bb = b2[tt];
+                    W2T = md.emb2[tt].WT;
+                }
+            T G0 = bb, G1 = T(0);
 #pragma unroll 8
-                for (int o = 0; o < 32; ++o) G += __ldg(W2T + o * 32 + lane) * shfl(z, o);
-                dw.g2[(long long)(start + base + u) * 32 + lane] = G;
+            for (int o = 0; o < 32; o += 2) {
+                G0 += __ldg(W2T + o * 32 + lane) * shfl(z, o);
+                G1 += __ldg(W2T + (o + 1) * 32 + lane) * shfl(z, o + 1);
+            }
+            const T G = G0 + G1;
+            dw.g2[32 * e + lane] = G;
+            A[0] += a.x * G;
+            A[1] += a.z * G;
+            A[2] += a.w * G;
+            A[3] += b.x * G;
+        }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) A[c] += static_cast<T>(sm.R[u][c]) * G;
+        for (int c = 0; c < 4; ++c) sm.red[w][32 * c + lane] = A[c];
+        __syncthreads();
+        if (w == 0) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                A[c] = ((sm.red[0][32 * c + lane] + sm.red[1][32 * c + lane]) +
+                        sm.red[2][32 * c + lane]) + sm.red[3][32 * c + lane];
+                A[c] *= md.inv_nnorm;
+                dw.A[128ll * i + 32 * c + lane] = A[c];
+            }
+            T Dv[4];
+            gram4(A, Dv);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                sm.x[a * 32 + lane] = Dv[a];
+                dw.D[128ll * i + 32 * a + lane] = Dv[a];
             }
             __syncwarp();
+            T m0 = md.map1.b[lane], m1 = T(0);
+            for (int k = 0; k < 128; k += 2) {
+                m0 += __ldg(md.map1.WT + k * 32 + lane) * sm.x[k];
+                m1 += __ldg(md.map1.WT + (k + 1) * 32 + lane) * sm.x[k + 1];
+            }
+            const T mz = d_tanh(m0 + m1);
+            const T g1 = cmv(md.map2.WT, md.map2.b, mz);
+            dw.mz[32ll * i + lane] = mz;
+            dw.g1[32ll * i + lane] = g1;
+            dw.P[32ll * i + lane] = cmv(md.L[0].c.WT, md.L[0].c.b, g1);
         }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            A[c] *= md.inv_nnorm;
-            dw.A[128ll * i + 32 * c + lane] = A[c];
-        }
-        T Dv[4];
-        gram4(A, Dv);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            sm.x[a * 32 + lane] = Dv[a];
-            dw.D[128ll * i + 32 * a + lane] = Dv[a];
-        }
-        __syncwarp();
-        T xs_t = T(0);
-        (void)xs_t;
-        // g1 map [128 -> 32 -> 32]
-        T mz = md.map1.b[lane];
-        for (int k = 0; k < 128; ++k) mz += __ldg(md.map1.WT + k * 32 + lane) * static_cast<T>(sm.x[k]);
-        mz = d_tanh(mz);
-        const T g1 = cmv(md.map2.WT, md.map2.b, mz);
-        dw.mz[32ll * i + lane] = mz;
-        dw.g1[32ll * i + lane] = g1;
-        dw.P[32ll * i + lane] = cmv(md.L[0].c.WT, md.L[0].c.b, g1);
-        __syncwarp();
+        __syncthreads();
     }
-    (void)S;
 }
 
-// ---------------------------------------------------------------------------
-// repformer layer pieces (device functions, one warp per atom i)
-// ---------------------------------------------------------------------------
-constexpr double kInvSqrt32 = 0.17677669529663688;  // 1 / sqrt(32)
-
-// q, k, v of every edge of atom i from g2^l (lane = row).
-template <typename T>
-__device__ __forceinline__ void rf_qkv(const DevDpLayer<T>& L, const T* g2l, T* qkv, int start,
-                                       int cnt) {
-    const int lane = threadIdx.x & 31;
-    for (int rb = 0; rb < cnt; rb += 32) {
-        if (rb + lane < cnt) {
-            const long long e = start + rb + lane;
-            T x[32], y[32];
-            load_row(g2l + 32 * e, x);
-            rmv(L.q.W, L.q.b, x, y);
-            store_row(qkv + 96 * e, y);
-            rmv(L.k.W, L.k.b, x, y);
-            store_row(qkv + 96 * e + 32, y);
-            rmv(L.v.W, L.v.b, x, y);
-            store_row(qkv + 96 * e + 64, y);
-        }
-    }
-    __syncwarp();
-}
-
-// Layer l forward for atom i: attention (lane = row), conv / grrg / update
-// (lane = channel).  Returns g1^{l+1}_i (lane = channel).
+// Layer l forward for the CTA's atom i; returns g1^{l+1}_i in warp 0 (lane = channel).
 template <typename T>
 __device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
-                          long long S, int n, int l, int i, DpWarpSmem& sm) {
-    const int lane = threadIdx.x & 31;
+                          long long S, int n, int l, int i, RfSmem<T>& sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const DevDpLayer<T>& L = md.L[l];
     const int start = gr.row_start[i], cnt = gr.nnei[i];
     const T* g2l = dw.g2 + (long long)l * S * 32;
     T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
-    rf_qkv(L, g2l, dw.qkv, start, cnt);
+    T* Q = rf_rows_qkv(dw, start);
+    T* TMP = dw.tmp + 96ll * start;
+    proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
+    proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
+    proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+    __syncthreads();
+    // attention, a quad per row
     const T sh = static_cast<T>(kShift), isq = static_cast<T>(kInvSqrt32);
+    const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
     for (int rb = 0; rb < cnt; rb += 32) {
-        const bool valid = rb + lane < cnt;
-        const long long e = start + rb + (valid ? lane : 0);
-        T q[32], o[32];
-        load_row(dw.qkv + 96 * e, q);
-        const V4<T> en0 = ld4c(dw.env + 8 * e), en1 = ld4c(dw.env + 8 * e + 4);
-        const T we = en0.y, he0 = en0.z, he1 = en0.w, he2 = en1.x;
+        const int r = rb + rq;
+        const bool valid = r < cnt;
+        const long long e = start + (valid ? r : 0);
+        T q[8], o[8];
+        ld8(Q + 96 * (valid ? r : 0) + 8 * p, q);
+        const EnvRow<T> er = env_row(dw.env, e);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) o[c] = T(0);
+        for (int c = 0; c < 8; ++c) o[c] = T(0);
         T mx = T(-1e30), Z = T(0);
+#pragma unroll 2
         for (int f = 0; f < cnt; ++f) {
             const long long ef = start + f;
-            const T lam = dot32(q, dw.qkv + 96 * ef + 32) * isq;
-            const V4<T> fn0 = ld4c(dw.env + 8 * ef), fn1 = ld4c(dw.env + 8 * ef + 4);
-            const T ww = we * fn0.y;
-            const T gam = he0 * fn0.z + he1 * fn0.w + he2 * fn1.x;
+            const T lam = quad_sum(dot8(q, Q + 96 * f + 32 + 8 * p)) * isq;
+            const EnvRow<T> fr = env_row(dw.env, ef);
+            const T ww = er.w * fr.w;
+            const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
             const T lt = (lam + sh) * ww - sh;
             if (lt > mx) {
                 const T sc = d_exp(mx - lt);
                 Z *= sc;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) o[c] *= sc;
+                for (int c = 0; c < 8; ++c) o[c] *= sc;
                 mx = lt;
             }
-            const T p = d_exp(lt - mx);
-            Z += p;
-            const T coef = p * ww * gam;
-            const T* vf = dw.qkv + 96 * ef + 64;
+            const T pe = d_exp(lt - mx);
+            Z += pe;
+            const T coef = pe * ww * gam;
+            T v[8];
+            ld8(Q + 96 * f + 64 + 8 * p, v);
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const V4<T> vv = ld4c(vf + c);
-                o[c] += coef * vv.x;
-                o[c + 1] += coef * vv.y;
-                o[c + 2] += coef * vv.z;
-                o[c + 3] += coef * vv.w;
-            }
+            for (int c = 0; c < 8; ++c) o[c] += coef * v[c];
         }
         if (valid) {
             const T iz = T(1) / Z;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] *= iz;
-            T g[32], y[32];
-            load_row(g2l + 32 * e, g);
-            rmv(L.o.W, L.o.b, o, y);
-#pragma unroll
-            for (int c = 0; c < 32; ++c) y[c] += g[c];
-            store_row(g2n + 32 * e, y);
-            T* st = dw.stat + ((long long)l * S + e) * 2;
-            st[0] = mx;
-            st[1] = Z;
+            for (int c = 0; c < 8; ++c) o[c] *= iz;
+            st8(TMP + 96 * r + 8 * p, o);
+            if (p == 0) {
+                T* st = dw.stat + ((long long)l * S + e) * 2;
+                st[0] = mx;
+                st[1] = Z;
+            }
         }
     }
-    __syncwarp();
-    // conv, T (lane = channel)
+    __syncthreads();
+    // g2hat = g2 + Wo o + bo
+    proj<T, false>(L.o.W, L.o.b, TMP, 96, g2l + 32ll * start, 32, g2n + 32ll * start, 32, cnt);
+    __syncthreads();
+    // conv and T partials (lane = channel), summed over warps in a fixed order
     const T* Pl = dw.P + (long long)l * n * 32;
     T conv = T(0), T3[3] = {T(0), T(0), T(0)};
-    for (int q = 0; q < cnt; ++q) {
-        const long long e = start + q;
+    for (int q2 = w; q2 < cnt; q2 += 4) {
+        const long long e = start + q2;
         const T gh = g2n[32 * e + lane];
-        const int j = gr.nbr[e];
-        const T pj = Pl[32ll * j + lane];
-        const V4<T> en0 = ld4c(dw.env + 8 * e);
-        const T h2 = dw.env[8 * e + 4];
-        conv += en0.y * gh * pj;
-        T3[0] += en0.z * gh;
-        T3[1] += en0.w * gh;
-        T3[2] += h2 * gh;
+        const T pj = Pl[32ll * gr.nbr[e] + lane];
+        const EnvRow<T> er = env_row(dw.env, e);
+        conv += er.w * gh * pj;
+        T3[0] += er.h0 * gh;
+        T3[1] += er.h1 * gh;
+        T3[2] += er.h2 * gh;
     }
-    conv *= md.inv_nnorm;
+    sm.red[w][lane] = conv;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        T3[c] *= md.inv_nnorm;
-        dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane] = T3[c];
+    for (int c = 0; c < 3; ++c) sm.red[w][32 + 32 * c + lane] = T3[c];
+    __syncthreads();
+    T g1 = T(0);
+    if (w == 0) {
+        auto tot = [&](int k) {
+            return ((sm.red[0][k] + sm.red[1][k]) + sm.red[2][k]) + sm.red[3][k];
+        };
+        conv = tot(lane) * md.inv_nnorm;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T3[c] = tot(32 + 32 * c + lane) * md.inv_nnorm;
+            dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane] = T3[c];
+        }
+        T gr4[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            T v = T(0);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v += shfl(T3[c], a) * T3[c];
+            gr4[a] = v;
+        }
+        sm.x[lane] = conv;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) sm.x[32 + 32 * a + lane] = gr4[a];
+        __syncwarp();
+        T u0 = L.u1.b[lane], u1 = T(0);
+        for (int k = 0; k < 160; k += 2) {
+            u0 += __ldg(L.u1.WT + k * 32 + lane) * sm.x[k];
+            u1 += __ldg(L.u1.WT + (k + 1) * 32 + lane) * sm.x[k + 1];
+        }
+        const T uz = d_tanh(u0 + u1);
+        dw.uz[((long long)l * n + i) * 32 + lane] = uz;
+        g1 = dw.g1[((long long)l * n + i) * 32 + lane] + cmv(L.u2.WT, L.u2.b, uz);
+        dw.g1[((long long)(l + 1) * n + i) * 32 + lane] = g1;
     }
-    T gr4[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        T v = T(0);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v += shfl(T3[c], a) * T3[c];
-        gr4[a] = v;
-    }
-    __syncwarp();
-    sm.x[lane] = conv;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) sm.x[32 + 32 * a + lane] = gr4[a];
-    __syncwarp();
-    T uz = L.u1.b[lane];
-    for (int k = 0; k < 160; ++k) uz += __ldg(L.u1.WT + k * 32 + lane) * static_cast<T>(sm.x[k]);
-    uz = d_tanh(uz);
-    __syncwarp();
-    dw.uz[((long long)l * n + i) * 32 + lane] = uz;
-    const T g1 = dw.g1[((long long)l * n + i) * 32 + lane] + cmv(L.u2.WT, L.u2.b, uz);
-    dw.g1[((long long)(l + 1) * n + i) * 32 + lane] = g1;
     return g1;
 }
 
-// Layer l backward, atom-local part: update MLP, grrg and conv adjoints, the
-// per-edge adjoints of g2hat, and the attention backward (row + column pass).
-// dg1_out: adjoint of g1^{l+1}_i (lane = channel).  top: no g2 adjoint from above.
-// Writes dconv (scaled by 1/nnorm) for the neighbours' P gather, the residual
-// part of dg1^l (dw.dg1), dg2 (adjoint of g2^l) and accumulates dwh.
+// Layer l backward for the CTA's atom i.  dg1_out (warp 0, lane = channel): the
+// adjoint of g1^{l+1}_i.  top: no g2 adjoint from above.  Writes dconv (scaled by
+// 1/nnorm) for the neighbours' P gather, the residual part of dg1^l (dw.dg1),
+// dg2 (adjoint of g2^l), and accumulates dwh.
 template <typename T>
 __device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
                              long long S, int n, int l, int i, T dg1_out, bool top,
-                             DpWarpSmem& sm) {
-    const int lane = threadIdx.x & 31;
+                             RfSmem<T>& sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const DevDpLayer<T>& L = md.L[l];
     const int start = gr.row_start[i], cnt = gr.nnei[i];
     const T* g2l = dw.g2 + (long long)l * S * 32;
     const T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
-    // update MLP backward
-    const T uz = dw.uz[((long long)l * n + i) * 32 + lane];
-    T du = T(0);
+    if (w == 0) {
+        // update MLP backward -> dconv, dgrrg -> dT
+        const T uz = dw.uz[((long long)l * n + i) * 32 + lane];
+        T du = T(0);
 #pragma unroll 8
-    for (int c = 0; c < 32; ++c) du += __ldg(L.u2.W + c * 32 + lane) * shfl(dg1_out, c);
-    du *= (T(1) - uz * uz);
-    T dx[5] = {T(0), T(0), T(0), T(0), T(0)};
-    for (int o = 0; o < 32; ++o) {
-        const T d_o = shfl(du, o);
+        for (int c = 0; c < 32; ++c) du += __ldg(L.u2.W + c * 32 + lane) * shfl(dg1_out, c);
+        du *= (T(1) - uz * uz);
+        T dx[5] = {T(0), T(0), T(0), T(0), T(0)};
+        for (int o = 0; o < 32; ++o) {
+            const T d_o = shfl(du, o);
 #pragma unroll
-        for (int jj = 0; jj < 5; ++jj) dx[jj] += __ldg(L.u1.W + o * 160 + 32 * jj + lane) * d_o;
+            for (int jj = 0; jj < 5; ++jj) dx[jj] += __ldg(L.u1.W + o * 160 + 32 * jj + lane) * d_o;
+        }
+        const T dconv = dx[0] * md.inv_nnorm;
+        T T3[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) T3[c] = dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane];
+        const T dgr[4] = {dx[1], dx[2], dx[3], dx[4]};
+        T dT[3];
+        gram4_bwd<T, 3>(T3, dgr, dT);
+        sm.bc[lane] = dconv;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sm.bc[32 + 32 * c + lane] = dT[c] * md.inv_nnorm;
+        dw.dconv[((long long)(l & 1) * n + i) * 32 + lane] = dconv;
+        dw.dg1[32ll * i + lane] = dg1_out;
     }
-    const T dconv = dx[0] * md.inv_nnorm;
-    T T3[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) T3[c] = dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane];
-    const T dgr[4] = {dx[1], dx[2], dx[3], dx[4]};
-    T dT[3];
-    gram4_bwd<T, 3>(T3, dgr, dT);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) dT[c] *= md.inv_nnorm;
-    dw.dconv[((long long)(l & 1) * n + i) * 32 + lane] = dconv;
-    dw.dg1[32ll * i + lane] = dg1_out;
+    __syncthreads();
     // per-edge adjoints of g2hat (lane = channel)
-    const T* Pl = dw.P + (long long)l * n * 32;
-    for (int q = 0; q < cnt; ++q) {
-        const long long e = start + q;
-        const T gh = g2n[32 * e + lane];
-        const int j = gr.nbr[e];
-        const T pj = Pl[32ll * j + lane];
-        const V4<T> en0 = ld4c(dw.env + 8 * e);
-        const T h2 = dw.env[8 * e + 4];
-        T d = top ? T(0) : dw.dg2[32 * e + lane];
-        d += en0.y * dconv * pj + en0.z * dT[0] + en0.w * dT[1] + h2 * dT[2];
-        dw.dg2[32 * e + lane] = d;
-        const T a0 = warp_sum(dconv * gh * pj);
-        const T a1 = warp_sum(dT[0] * gh);
-        const T a2 = warp_sum(dT[1] * gh);
-        const T a3 = warp_sum(dT[2] * gh);
-        if (lane == 0) {
-            T* p = dw.dwh + 4 * e;
-            if (top) {
-                st4(p, a0, a1, a2, a3);
-            } else {
-                const V4<T> old = ld4c(p);
-                st4(p, old.x + a0, old.y + a1, old.z + a2, old.w + a3);
+    {
+        const T dconv = sm.bc[lane], dT0 = sm.bc[32 + lane], dT1 = sm.bc[64 + lane],
+                dT2 = sm.bc[96 + lane];
+        const T* Pl = dw.P + (long long)l * n * 32;
+        for (int q = w; q < cnt; q += 4) {
+            const long long e = start + q;
+            const T gh = g2n[32 * e + lane];
+            const T pj = Pl[32ll * gr.nbr[e] + lane];
+            const EnvRow<T> er = env_row(dw.env, e);
+            T d = top ? T(0) : dw.dg2[32 * e + lane];
+            d += er.w * dconv * pj + er.h0 * dT0 + er.h1 * dT1 + er.h2 * dT2;
+            dw.dg2[32 * e + lane] = d;
+            const T a0 = warp_sum(dconv * gh * pj);
+            const T a1 = warp_sum(dT0 * gh);
+            const T a2 = warp_sum(dT1 * gh);
+            const T a3 = warp_sum(dT2 * gh);
+            if (lane == 0) {
+                T* pw = dw.dwh + 4 * e;
+                if (top) {
+                    st4(pw, a0, a1, a2, a3);
+                } else {
+                    const V4<T> old = ld4c(pw);
+                    st4(pw, old.x + a0, old.y + a1, old.z + a2, old.w + a3);
+                }
             }
         }
     }
-    __syncwarp();
-    // attention backward
-    rf_qkv(L, g2l, dw.qkv, start, cnt);
+    __syncthreads();
+    // q, k, v (recomputed) and do = Wo^T dg2hat
+    T* Q = rf_rows_qkv(dw, start);
+    T* DOB = rf_rows_dob(dw, start);
+    T* TMP = dw.tmp + 96ll * start;
+    T* DG2 = dw.dg2 + 32ll * start;
+    proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
+    proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
+    proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+    proj<T, false>(L.o.WT, nullptr, DG2, 32, nullptr, 0, DOB, 32, cnt);
+    __syncthreads();
     const T sh = static_cast<T>(kShift), isq = static_cast<T>(kInvSqrt32);
-    // row pass (lane = e): do_e, S_e, dq_e, row-side dw/dh; dg2_e += Wq^T dq_e
+    const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
+    // row pass (quad per row e): S_e, dq_e, row-side dw/dh
     for (int rb = 0; rb < cnt; rb += 32) {
-        const bool valid = rb + lane < cnt;
-        const long long e = start + rb + (valid ? lane : 0);
-        T x[32], dov[32];
-        load_row(dw.dg2 + 32 * e, x);
-        rmv(L.o.WT, static_cast<const T*>(nullptr), x, dov);
-        if (valid) store_row(dw.dob + 32 * e, dov);
+        const int r = rb + rq;
+        const bool valid = r < cnt;
+        const long long e = start + (valid ? r : 0);
+        T q[8], dov[8];
+        ld8(Q + 96 * (valid ? r : 0) + 8 * p, q);
+        ld8(DOB + 32 * (valid ? r : 0) + 8 * p, dov);
         const T* st = dw.stat + ((long long)l * S + e) * 2;
         const T mx = st[0], iz = T(1) / st[1];
-        T q[32];
-        load_row(dw.qkv + 96 * e, q);
-        const V4<T> en0 = ld4c(dw.env + 8 * e), en1 = ld4c(dw.env + 8 * e + 4);
-        const T we = en0.y, he0 = en0.z, he1 = en0.w, he2 = en1.x;
+        const EnvRow<T> er = env_row(dw.env, e);
         T Ssum = T(0);
+#pragma unroll 2
         for (int f = 0; f < cnt; ++f) {
             const long long ef = start + f;
-            const T lam = dot32(q, dw.qkv + 96 * ef + 32) * isq;
-            const V4<T> fn0 = ld4c(dw.env + 8 * ef), fn1 = ld4c(dw.env + 8 * ef + 4);
-            const T ww = we * fn0.y;
-            const T gam = he0 * fn0.z + he1 * fn0.w + he2 * fn1.x;
+            const T lam = quad_sum(dot8(q, Q + 96 * f + 32 + 8 * p)) * isq;
+            const T db = quad_sum(dot8(dov, Q + 96 * f + 64 + 8 * p));
+            const EnvRow<T> fr = env_row(dw.env, ef);
+            const T ww = er.w * fr.w;
+            const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
             const T al = d_exp((lam + sh) * ww - sh - mx) * iz;
-            const T db = dot32(dov, dw.qkv + 96 * ef + 64);
             Ssum += al * db * ww * gam;
         }
-        T dq[32];
+        T dq[8];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dq[c] = T(0);
+        for (int c = 0; c < 8; ++c) dq[c] = T(0);
         T dwe = T(0), dh0 = T(0), dh1 = T(0), dh2 = T(0);
+#pragma unroll 2
         for (int f = 0; f < cnt; ++f) {
             const long long ef = start + f;
-            const T* kf = dw.qkv + 96 * ef + 32;
-            const T lam = dot32(q, kf) * isq;
-            const V4<T> fn0 = ld4c(dw.env + 8 * ef), fn1 = ld4c(dw.env + 8 * ef + 4);
-            const T wf = fn0.y, ww = we * wf;
-            const T gam = he0 * fn0.z + he1 * fn0.w + he2 * fn1.x;
+            const T* kf = Q + 96 * f + 32 + 8 * p;
+            const T lam = quad_sum(dot8(q, kf)) * isq;
+            const T db = quad_sum(dot8(dov, Q + 96 * f + 64 + 8 * p));
+            const EnvRow<T> fr = env_row(dw.env, ef);
+            const T ww = er.w * fr.w;
+            const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
             const T al = d_exp((lam + sh) * ww - sh - mx) * iz;
-            const T db = dot32(dov, dw.qkv + 96 * ef + 64);
             const T da = db * ww * gam;
             const T dlt = al * (da - Ssum);
             const T dlam = dlt * ww * isq;
+            T k[8];
+            ld8(kf, k);
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const V4<T> kv = ld4c(kf + c);
-                dq[c] += dlam * kv.x;
-                dq[c + 1] += dlam * kv.y;
-                dq[c + 2] += dlam * kv.z;
-                dq[c + 3] += dlam * kv.w;
-            }
+            for (int c = 0; c < 8; ++c) dq[c] += dlam * k[c];
             const T dww = db * al * gam + dlt * (lam + sh);
             const T dgam = db * al * ww;
-            dwe += dww * wf;
-            dh0 += dgam * fn0.z;
-            dh1 += dgam * fn0.w;
-            dh2 += dgam * fn1.x;
+            dwe += dww * fr.w;
+            dh0 += dgam * fr.h0;
+            dh1 += dgam * fr.h1;
+            dh2 += dgam * fr.h2;
         }
-        T y[32];
-        rmv(L.q.WT, static_cast<const T*>(nullptr), dq, y);
         if (valid) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) y[c] += x[c];
-            store_row(dw.dg2 + 32 * e, y);
-            dw.aux[2 * e] = Ssum;
-            T* p = dw.dwh + 4 * e;
-            const V4<T> old = ld4c(p);
-            st4(p, old.x + dwe, old.y + dh0, old.z + dh1, old.w + dh2);
+            st8(TMP + 96 * r + 8 * p, dq);
+            if (p == 0) {
+                dw.aux[2 * e] = Ssum;
+                T* pw = dw.dwh + 4 * e;
+                const V4<T> old = ld4c(pw);
+                st4(pw, old.x + dwe, old.y + dh0, old.z + dh1, old.w + dh2);
+            }
         }
     }
-    __syncwarp();
-    // column pass (lane = f): dk_f, dv_f, column-side dw/dh; dg2_f += Wk^T dk_f + Wv^T dv_f
+    __syncthreads();
+    // column pass (quad per column f): dk_f, dv_f, column-side dw/dh
     for (int rb = 0; rb < cnt; rb += 32) {
-        const bool valid = rb + lane < cnt;
-        const long long f = start + rb + (valid ? lane : 0);
-        T k[32], v[32], dk[32], dv[32];
-        load_row(dw.qkv + 96 * f + 32, k);
-        load_row(dw.qkv + 96 * f + 64, v);
+        const int r = rb + rq;
+        const bool valid = r < cnt;
+        const long long f = start + (valid ? r : 0);
+        T k[8], v[8], dk[8], dv[8];
+        const int rl = valid ? r : 0;
+        ld8(Q + 96 * rl + 32 + 8 * p, k);
+        ld8(Q + 96 * rl + 64 + 8 * p, v);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dk[c] = dv[c] = T(0);
-        const V4<T> fn0 = ld4c(dw.env + 8 * f), fn1 = ld4c(dw.env + 8 * f + 4);
-        const T wf = fn0.y, hf0 = fn0.z, hf1 = fn0.w, hf2 = fn1.x;
+        for (int c = 0; c < 8; ++c) dk[c] = dv[c] = T(0);
+        const EnvRow<T> fr = env_row(dw.env, f);
         T dwf = T(0), dh0 = T(0), dh1 = T(0), dh2 = T(0);
-        for (int r = 0; r < cnt; ++r) {
-            const long long e = start + r;
-            const T* qe = dw.qkv + 96 * e;
-            const T* de = dw.dob + 32 * e;
-            const T lam = dot32(k, qe) * isq;
-            const T db = dot32(v, de);
-            const V4<T> en0 = ld4c(dw.env + 8 * e), en1 = ld4c(dw.env + 8 * e + 4);
-            const T we = en0.y, ww = we * wf;
-            const T gam = en0.z * hf0 + en0.w * hf1 + en1.x * hf2;
+#pragma unroll 2
+        for (int r2 = 0; r2 < cnt; ++r2) {
+            const long long e = start + r2;
+            const T* qe = Q + 96 * r2 + 8 * p;
+            const T* de = DOB + 32 * r2 + 8 * p;
+            const T lam = quad_sum(dot8(k, qe)) * isq;
+            const T db = quad_sum(dot8(v, de));
+            const EnvRow<T> er = env_row(dw.env, e);
+            const T ww = er.w * fr.w;
+            const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
             const T* st = dw.stat + ((long long)l * S + e) * 2;
             const T al = d_exp((lam + sh) * ww - sh - st[0]) / st[1];
             const T da = db * ww * gam;
             const T dlt = al * (da - dw.aux[2 * e]);
             const T dlam = dlt * ww * isq;
             const T bet = al * ww * gam;
+            T qv[8], dv8[8];
+            ld8(qe, qv);
+            ld8(de, dv8);
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                const V4<T> qv = ld4c(qe + c);
-                const V4<T> dv4 = ld4c(de + c);
-                dk[c] += dlam * qv.x;
-                dk[c + 1] += dlam * qv.y;
-                dk[c + 2] += dlam * qv.z;
-                dk[c + 3] += dlam * qv.w;
-                dv[c] += bet * dv4.x;
-                dv[c + 1] += bet * dv4.y;
-                dv[c + 2] += bet * dv4.z;
-                dv[c + 3] += bet * dv4.w;
+            for (int c = 0; c < 8; ++c) {
+                dk[c] += dlam * qv[c];
+                dv[c] += bet * dv8[c];
             }
             const T dww = db * al * gam + dlt * (lam + sh);
             const T dgam = db * al * ww;
-            dwf += dww * we;
-            dh0 += dgam * en0.z;
-            dh1 += dgam * en0.w;
-            dh2 += dgam * en1.x;
+            dwf += dww * er.w;
+            dh0 += dgam * er.h0;
+            dh1 += dgam * er.h1;
+            dh2 += dgam * er.h2;
         }
-        T y[32];
-        rmv(L.k.WT, static_cast<const T*>(nullptr), dk, y);
-        T y2[32];
-        rmv(L.v.WT, static_cast<const T*>(nullptr), dv, y2);
         if (valid) {
-            T x[32];
-            load_row(dw.dg2 + 32 * f, x);
-#pragma unroll
-            for (int c = 0; c < 32; ++c) x[c] += y[c] + y2[c];
-            store_row(dw.dg2 + 32 * f, x);
-            T* p = dw.dwh + 4 * f;
-            const V4<T> old = ld4c(p);
-            st4(p, old.x + dwf, old.y + dh0, old.z + dh1, old.w + dh2);
+            st8(TMP + 96 * r + 32 + 8 * p, dk);
+            st8(TMP + 96 * r + 64 + 8 * p, dv);
+            if (p == 0) {
+                T* pw = dw.dwh + 4 * f;
+                const V4<T> old = ld4c(pw);
+                st4(pw, old.x + dwf, old.y + dh0, old.z + dh1, old.w + dh2);
+            }
         }
     }
-    __syncwarp();
+    __syncthreads();
+    // dg2 = dg2hat + Wq^T dq + Wk^T dk + Wv^T dv
+    proj<T, true>(L.q.WT, nullptr, TMP, 96, nullptr, 0, DG2, 32, cnt);
+    proj<T, true>(L.k.WT, nullptr, TMP + 32, 96, nullptr, 0, DG2, 32, cnt);
+    proj<T, true>(L.v.WT, nullptr, TMP + 64, 96, nullptr, 0, DG2, 32, cnt);
+    __syncthreads();
 }
 
-// Gather of the neighbour-projection adjoint for atom j and layer l:
-// dP_j = sum_{q in out(j)} w_q g2hat^l_{rev q} * dconv^l_{nbr q}, returns
-// dg1^l_j = dg1(residual) + Wc^T dP_j (lane = channel).
+// dg1^l_j = dg1(residual) + Wc^T dP_j with dP_j = sum_{q in out(j)} w_q g2hat^l_{rev q}
+// * dconv^l_{nbr q}; per-warp partials, warp 0 returns the result (lane = channel).
 template <typename T>
 __device__ __forceinline__ T rf_gather_dg1(const DevDp<T>& md, const DevGraph& gr,
                                            const DevDpWork<T>& dw, long long S, int n, int l,
-                                           int j) {
-    const int lane = threadIdx.x & 31;
+                                           int j, RfSmem<T>& sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int start = gr.row_start[j], cnt = gr.nnei[j];
     const T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
     const T* dcv = dw.dconv + (long long)(l & 1) * n * 32;
     T dP = T(0);
-    for (int q = 0; q < cnt; ++q) {
+    for (int q = w; q < cnt; q += 4) {
         const long long e = start + q;
-        const int mir = gr.inv_pos[e];
-        const int i = gr.nbr[e];
-        dP += dw.env[8ll * mir + 1] * g2n[32ll * mir + lane] * dcv[32ll * i + lane];
+        const long long mir = gr.inv_pos[e];
+        dP += dw.env[8 * mir + 1] * g2n[32 * mir + lane] * dcv[32ll * gr.nbr[e] + lane];
     }
-    T acc = dw.dg1[32ll * j + lane];
+    sm.red[w][lane] = dP;
+    __syncthreads();
+    T acc = T(0);
+    if (w == 0) {
+        dP = ((sm.red[0][lane] + sm.red[1][lane]) + sm.red[2][lane]) + sm.red[3][lane];
+        acc = dw.dg1[32ll * j + lane];
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) acc += __ldg(md.L[l].c.W + k * 32 + lane) * shfl(dP, k);
+        for (int k = 0; k < 32; ++k) acc += __ldg(md.L[l].c.W + k * 32 + lane) * shfl(dP, k);
+    }
+    __syncthreads();
     return acc;
 }
 
@@ -932,60 +1047,58 @@ __device__ __forceinline__ T rf_fit(const DevDp<T>& md, const DevGraph& gr, cons
 
 // Layer l forward (l < L - 1): g1^{l+1}, P^{l+1}.
 template <typename T>
-__global__ __launch_bounds__(kDpCTA) void k_rf_fwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
-                                                   DevDpWork<T> dw, int l) {
-    __shared__ DpWarpSmem s_w[kDpWarps];
+__global__ __launch_bounds__(kRfT) void k_rf_fwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+                                                 DevDpWork<T> dw, int l) {
+    __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
-    const WarpIdx wi;
     pdl_wait();
     const int n = gr.n;
-    for (int i = wi.first; i < gr.n_active; i += wi.stride) {
-        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, s_w[wi.wid]);
-        dw.P[((long long)(l + 1) * n + i) * 32 + wi.lane] = cmv(md.L[l + 1].c.WT, md.L[l + 1].c.b, g1);
-        __syncwarp();
+    for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
+        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, sm);
+        if (threadIdx.x < 32)
+            dw.P[((long long)(l + 1) * n + i) * 32 + threadIdx.x] =
+                cmv(md.L[l + 1].c.WT, md.L[l + 1].c.b, g1);
+        __syncthreads();
     }
 }
 
 // Top layer forward + fitting + top layer backward (atom-local part).
 template <typename T>
-__global__ __launch_bounds__(kDpCTA) void k_rf_top(DevDp<T> md, DevGraph gr, DevWork<T> ws,
-                                                   DevDpWork<T> dw) {
-    __shared__ DpWarpSmem s_w[kDpWarps];
+__global__ __launch_bounds__(kRfT) void k_rf_top(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+                                                 DevDpWork<T> dw) {
+    __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
-    const WarpIdx wi;
     pdl_wait();
     const int n = gr.n, l = md.n_layers - 1;
-    for (int i = wi.first; i < gr.n_active; i += wi.stride) {
-        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, s_w[wi.wid]);
-        const T dg1 = rf_fit(md, gr, ws, i, g1);
-        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, true, s_w[wi.wid]);
+    for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
+        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, sm);
+        T dg1 = T(0);
+        if (threadIdx.x < 32) dg1 = rf_fit(md, gr, ws, i, g1);
+        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, true, sm);
     }
 }
 
 // Gather for layer l + 1, then layer l backward.
 template <typename T>
-__global__ __launch_bounds__(kDpCTA) void k_rf_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
-                                                   DevDpWork<T> dw, int l) {
-    __shared__ DpWarpSmem s_w[kDpWarps];
+__global__ __launch_bounds__(kRfT) void k_rf_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+                                                 DevDpWork<T> dw, int l) {
+    __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
-    const WarpIdx wi;
     pdl_wait();
     const int n = gr.n;
-    for (int i = wi.first; i < gr.n_active; i += wi.stride) {
-        const T dg1 = rf_gather_dg1(md, gr, dw, ws.slots, n, l + 1, i);
-        __syncwarp();
-        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, false, s_w[wi.wid]);
+    for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
+        const T dg1 = rf_gather_dg1(md, gr, dw, ws.slots, n, l + 1, i, sm);
+        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, false, sm);
     }
 }
 
 // Gather for layer 0, g1 map + descriptor + embedding backward -> dE/d(edge_dr).
 template <typename T>
-__global__ __launch_bounds__(kDpCTA) void k_rf_embed_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
-                                                         DevDpWork<T> dw) {
-    __shared__ DpWarpSmem s_w[kDpWarps];
+__global__ __launch_bounds__(kRfT) void k_rf_embed_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+                                                       DevDpWork<T> dw) {
+    __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
-    const WarpIdx wi;
-    const int lane = wi.lane;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     T w1[kMaxTypes], b1[kMaxTypes];
 #pragma unroll
     for (int t = 0; t < kMaxTypes; ++t) {
@@ -994,47 +1107,53 @@ __global__ __launch_bounds__(kDpCTA) void k_rf_embed_bwd(DevDp<T> md, DevGraph g
     }
     pdl_wait();
     const int n = gr.n;
-    for (int i = wi.first; i < gr.n_active; i += wi.stride) {
+    for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
         const int start = gr.row_start[i], cnt = gr.nnei[i];
-        const T dg1 = rf_gather_dg1(md, gr, dw, ws.slots, n, 0, i);
-        // g1 map backward
-        const T mz = dw.mz[32ll * i + lane];
-        T dm = T(0);
+        const T dg1 = rf_gather_dg1(md, gr, dw, ws.slots, n, 0, i, sm);
+        if (w == 0) {
+            // g1 map backward -> dD -> dA (broadcast to the team)
+            const T mz = dw.mz[32ll * i + lane];
+            T dm = T(0);
 #pragma unroll 8
-        for (int c = 0; c < 32; ++c) dm += __ldg(md.map2.W + c * 32 + lane) * shfl(dg1, c);
-        dm *= (T(1) - mz * mz);
-        T dD[4] = {T(0), T(0), T(0), T(0)};
-        for (int o = 0; o < 32; ++o) {
-            const T d_o = shfl(dm, o);
+            for (int c = 0; c < 32; ++c) dm += __ldg(md.map2.W + c * 32 + lane) * shfl(dg1, c);
+            dm *= (T(1) - mz * mz);
+            T dD[4] = {T(0), T(0), T(0), T(0)};
+            for (int o = 0; o < 32; ++o) {
+                const T d_o = shfl(dm, o);
 #pragma unroll
-            for (int a = 0; a < 4; ++a) dD[a] += __ldg(md.map1.W + o * 128 + a * 32 + lane) * d_o;
+                for (int a = 0; a < 4; ++a) dD[a] += __ldg(md.map1.W + o * 128 + a * 32 + lane) * d_o;
+            }
+            T A[4], dA[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) A[c] = dw.A[128ll * i + 32 * c + lane];
+            gram4_bwd<T, 4>(A, dD, dA);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm.bc[32 * c + lane] = dA[c] * md.inv_nnorm;
         }
-        T A[4], dA[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) A[c] = dw.A[128ll * i + 32 * c + lane];
-        gram4_bwd<T, 4>(A, dD, dA);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dA[c] *= md.inv_nnorm;
-        for (int q = 0; q < cnt; ++q) {
+        __syncthreads();
+        const T dA0 = sm.bc[lane], dA1 = sm.bc[32 + lane], dA2 = sm.bc[64 + lane],
+                dA3 = sm.bc[96 + lane];
+        for (int q = w; q < cnt; q += 4) {
             const long long e = start + q;
-            const V4<T> en0 = ld4c(dw.env + 8 * e), en1 = ld4c(dw.env + 8 * e + 4);
-            const T s = en0.x;
-            const int t = static_cast<int>(en1.w);
+            const V4<T> a = ld4c(dw.env + 8 * e), b = ld4c(dw.env + 8 * e + 4);
+            const T s = a.x;
+            const int t = static_cast<int>(b.w);
             const T G = dw.g2[32 * e + lane];
-            const T dG = dw.dg2[32 * e + lane] + dA[0] * s + dA[1] * en0.z + dA[2] * en0.w +
-                         dA[3] * en1.x;
-            const T dR0 = warp_sum(dA[0] * G), dR1 = warp_sum(dA[1] * G),
-                    dR2 = warp_sum(dA[2] * G), dR3 = warp_sum(dA[3] * G);
+            const T dG = dw.dg2[32 * e + lane] + dA0 * s + dA1 * a.z + dA2 * a.w + dA3 * b.x;
+            const T dR0 = warp_sum(dA0 * G), dR1 = warp_sum(dA1 * G), dR2 = warp_sum(dA2 * G),
+                    dR3 = warp_sum(dA3 * G);
             T ds = T(0);
 #pragma unroll
             for (int tt = 0; tt < kMaxTypes; ++tt)
                 if (tt == t) {
                     const T z = d_tanh(w1[tt] * s + b1[tt]);
-                    T dz = T(0);
+                    T dz0 = T(0), dz1 = T(0);
 #pragma unroll 8
-                    for (int b = 0; b < 32; ++b) dz += __ldg(md.emb2[tt].W + b * 32 + lane) * shfl(dG, b);
-                    dz *= (T(1) - z * z);
-                    ds = warp_sum(w1[tt] * dz);
+                    for (int bq = 0; bq < 32; bq += 2) {
+                        dz0 += __ldg(md.emb2[tt].W + bq * 32 + lane) * shfl(dG, bq);
+                        dz1 += __ldg(md.emb2[tt].W + (bq + 1) * 32 + lane) * shfl(dG, bq + 1);
+                    }
+                    ds = warp_sum(w1[tt] * (dz0 + dz1) * (T(1) - z * z));
                 }
             if (lane == 0) {
                 const V4<T> wh = ld4c(dw.dwh + 4 * e);
@@ -1046,9 +1165,25 @@ __global__ __launch_bounds__(kDpCTA) void k_rf_embed_bwd(DevDp<T> md, DevGraph g
                 st4(ws.gvrev + 4ll * gr.inv_pos[e], g[0], g[1], g[2], T(0));
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
-    (void)s_w;
+}
+
+template <typename T>
+cudaError_t rf_configure() {
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    const int bytes = kRfSmemRows * 128 * sizeof(T);
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {cudaFuncSetAttribute(k_rf_fwd<T>, a, bytes),
+                          cudaFuncSetAttribute(k_rf_top<T>, a, bytes),
+                          cudaFuncSetAttribute(k_rf_bwd<T>, a, bytes)})
+        if (r != cudaSuccess) e = r;
+    return e;
+}
+
+int rf_grid(int n) {
+    const int cap = num_sms() * 4;
+    return n < 1 ? 1 : (n < cap ? n : cap);
 }
 
 int dp_grid(int n) {
@@ -1058,6 +1193,12 @@ int dp_grid(int n) {
 }
 
 }  // namespace
+
+// Per device: allow the repformer kernels their shared-memory rows (FP64 > 48 KB).
+cudaError_t dp_configure() {
+    const cudaError_t a = rf_configure<float>(), b = rf_configure<double>();
+    return a != cudaSuccess ? a : b;
+}
 
 // Launches the whole DeePMD-style network + forces; returns the kernel count.
 template <typename T>
@@ -1076,19 +1217,23 @@ int launch_dp(const DevDp<T>& md, const DevGraph& gr, const DevWork<T>& ws,
     DevGraph g2 = gr;
     if (rev) g2.inv_pos = rev;
     const int L = md.n_layers;
-    launch_pdl(k_rf_embed<T>, grid, block, 0, st, md, gr, ws, dw, rev, mf);
+    const dim3 rgrid(rf_grid(gr.n_active)), rblock(kRfT);
+    DevDpWork<T> dws = dw;
+    dws.smem_rows = gr.ell > 0 && gr.ell <= kRfSmemRows;
+    const size_t rsm = dws.smem_rows ? size_t(kRfSmemRows) * 128 * sizeof(T) : 0;
+    launch_pdl(k_rf_embed<T>, rgrid, rblock, 0, st, md, gr, ws, dw, rev, mf);
     mk("rf_embed", st);
     for (int l = 0; l + 1 < L; ++l) {
-        launch_pdl(k_rf_fwd<T>, grid, block, 0, st, md, g2, ws, dw, l);
+        launch_pdl(k_rf_fwd<T>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
         mk("rf_fwd", st);
     }
-    launch_pdl(k_rf_top<T>, grid, block, 0, st, md, g2, ws, dw);
+    launch_pdl(k_rf_top<T>, rgrid, rblock, rsm, st, md, g2, ws, dws);
     mk("rf_top", st);
     for (int l = L - 2; l >= 0; --l) {
-        launch_pdl(k_rf_bwd<T>, grid, block, 0, st, md, g2, ws, dw, l);
+        launch_pdl(k_rf_bwd<T>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
         mk("rf_bwd", st);
     }
-    launch_pdl(k_rf_embed_bwd<T>, grid, block, 0, st, md, g2, ws, dw);
+    launch_pdl(k_rf_embed_bwd<T>, rgrid, rblock, 0, st, md, g2, ws, dw);
     mk("rf_embed_bwd", st);
     launch_force<T>(g2, ws, forces, per_atom, out, st, mf);
     mk("force", st);
