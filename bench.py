@@ -40,8 +40,9 @@ sys.path.insert(0, ROOT)
 # name -> (family, depth): the reference's two toy families (DPA2 / DPA3 analogs)
 # and the DeePMD-style families of the north star (no reference function,
 # DESIGN.md §11): se_a (smooth env matrix, G^T R R^T G) and a 2-layer repformer
-# (DPA2-style gated neighbour self-attention).
-MODELS = {"dpa2": (0, 1), "dpa3": (1, 3), "se_a": (2, 1), "repformer": (3, 3)}
+# (DPA2-style gated neighbour self-attention), 2-layer repflow (DPA3-style
+# edge/angle message passing).
+MODELS = {"dpa2": (0, 1), "dpa3": (1, 3), "se_a": (2, 1), "repformer": (3, 3), "repflow": (4, 3)}
 
 
 def make_bench_model(P, name):
@@ -96,16 +97,19 @@ def dp_kernel_flops(d, n, ne, m2):
         return {"sea": 3 * desc + 3 * n * ff}
     fmap = mlp_flops(d["g1map"]["sizes"])
     lay = d["layers"][0]
-    fq = mlp_flops(lay["q"]["sizes"])
+    fq = mlp_flops(lay["v"]["sizes"])
     fu = mlp_flops(lay["update"]["sizes"])
-    fwd = ne * (4 * fq + 6 * H) + m2 * (4 * H + 5) + n * (fq + 2 * 3 * ax * H + fu)
+    if d["family"] == "repflow":  # v, o projections; per angle pair 3 + 4H (tanh counted once)
+        fwd = ne * (2 * fq + 6 * H) + m2 * (3 + 4 * H) + n * (fq + 2 * 3 * ax * H + fu)
+    else:
+        fwd = ne * (4 * fq + 6 * H) + m2 * (4 * H + 5) + n * (fq + 2 * 3 * ax * H + fu)
     emb = desc + n * fmap
     return {"rf_embed": emb, "rf_fwd": fwd, "rf_top": 3 * fwd + 3 * n * ff, "rf_bwd": 2 * fwd,
             "rf_embed_bwd": 2 * emb}
 
 
 def kernel_flops(model_dict, n, n_owned, ne, m2=0):
-    if model_dict["family"] in ("se_a", "repformer"):
+    if model_dict["family"] in ("se_a", "repformer", "repflow"):
         return dp_kernel_flops(model_dict, n, ne, m2)
     H = model_dict["hidden"]
     K = len(model_dict["basis"]["centers"])
@@ -453,7 +457,8 @@ def run_ours(args, rank, world, local_rank, dist):
     if world == 1 and not args.no_cpu_baseline:
         threads = cpu_count()
         # bounded sample: ~cpu_seconds of wall on all host threads
-        per_step = {"dpa3": 0.2, "dpa2": 0.012, "se_a": 0.03, "repformer": 0.06}[args.model]
+        per_step = {"dpa3": 0.2, "dpa2": 0.012, "se_a": 0.03, "repformer": 0.06,
+                    "repflow": 0.06}[args.model]
         per_step *= n / 582
         steps_cpu = max(2, int(args.cpu_seconds / per_step))
         sps, cwall, kind = reference_md(args.model, args.system, steps_cpu, 1, args.precision,

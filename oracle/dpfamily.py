@@ -42,6 +42,14 @@ function, hmdp_dp.cu):
       grrg_i = T_i[:, :axis]^T T_i                        [axis, 32]
       g1_i <- g1_i + upd([conv_i, grrg_i])               MLP [32 + axis*32, 32, 32]
     e_i = fit(g1_i) + ebias[t_i]                         MLP [32, 32, 1]
+  repflow (family "repflow", DPA3-style; depth = 1 + n_layers): as repformer, with
+  the attention replaced by an edge/angle message over the angle neighbours
+  A(i) = {e : r_e < rca} (omega_e = DeePMD switch between rcas and rca):
+      c_ef   = u_e . u_f                              (cos of the angle j-i-k, f != e)
+      z_ef   = tanh(wa c_ef + ba)                     elementwise, MLP [1, 32] "angle"
+      v_f    = Wv g2_f + bv
+      m_e    = (1/anorm) sum_{f in A(i), f != e} omega_e omega_f z_ef * v_f
+      g2_e  <- g2_e + Wo m_e + bo
 """
 from __future__ import annotations
 
@@ -124,7 +132,7 @@ def energy_terms(model: dict, types, offset, nbr, dr_edges):
     ebias = torch.tensor(model["energy_bias"], dtype=torch.float64)[ty]
     if fam == "se_a":
         return _mlp(model["fitting"], D)[:, 0] + ebias, stages
-    if fam != "repformer":
+    if fam not in ("repformer", "repflow"):
         raise ValueError(f"dpfamily oracle: unknown family {fam}")
     g1 = _mlp(model["g1map"], D)
     g2 = G
@@ -133,15 +141,44 @@ def energy_terms(model: dict, types, offset, nbr, dr_edges):
     gate = torch.einsum("nec,nfc->nef", h, h)
     neg = torch.where(mask[:, None, :] > 0, torch.zeros_like(ww), torch.full_like(ww, -1e30))
     stages["g1"] = [g1]
+    if fam == "repflow":
+        # angle neighbours (r < rca) as a padded sub-list of each atom's edges
+        rca, rcas = float(model["rc_angle"]), float(model["rc_angle_smooth"])
+        anorm = float(model["anorm"])
+        rn = r.detach().numpy()
+        sel = [np.nonzero((slot_np[i] >= 0) & (rn[i] < rca))[0] for i in range(n)]
+        ma = max(max((len(x) for x in sel), default=0), 1)
+        aidx = np.zeros((n, ma), dtype=np.int64)
+        amask_np = np.zeros((n, ma))
+        for i, x in enumerate(sel):
+            aidx[i, : len(x)] = x
+            amask_np[i, : len(x)] = 1.0
+        aidx_t = torch.from_numpy(aidx)
+        amask = torch.from_numpy(amask_np)
+        ra = torch.gather(r, 1, aidx_t)
+        da = torch.gather(d, 1, aidx_t[..., None].expand(-1, -1, 3))
+        om = smooth_switch(ra, rca, rcas) * amask
+        ua = da / ra[..., None]
+        cos = torch.einsum("nec,nfc->nef", ua, ua)
+        pair = om[:, :, None] * om[:, None, :] * (1.0 - torch.eye(ma, dtype=torch.float64)) / anorm
     for layer in model["layers"]:
-        q = _mlp(layer["q"], g2)
-        k = _mlp(layer["k"], g2)
-        v = _mlp(layer["v"], g2)
-        lg = torch.einsum("nec,nfc->nef", q, k) / math.sqrt(32.0)
-        lg = (lg + SHIFT) * ww - SHIFT + neg
-        a = torch.softmax(lg, dim=-1)
-        b = a * ww * gate
-        o = torch.einsum("nef,nfc->nec", b, v)
+        if fam == "repformer":
+            q = _mlp(layer["q"], g2)
+            k = _mlp(layer["k"], g2)
+            v = _mlp(layer["v"], g2)
+            lg = torch.einsum("nec,nfc->nef", q, k) / math.sqrt(32.0)
+            lg = (lg + SHIFT) * ww - SHIFT + neg
+            a = torch.softmax(lg, dim=-1)
+            b = a * ww * gate
+            o = torch.einsum("nef,nfc->nec", b, v)
+        else:
+            v = _mlp(layer["v"], g2)
+            va = torch.gather(v, 1, aidx_t[..., None].expand(-1, -1, 32))
+            z = _mlp(layer["angle"], cos[..., None])  # [n, ma, ma, 32] (linear, then tanh)
+            z = torch.tanh(z)
+            oa = torch.einsum("nef,nefc,nfc->nec", pair, z, va)
+            o = torch.zeros(n, idx.shape[1], 32, dtype=torch.float64)
+            o = o.scatter_add(1, aidx_t[..., None].expand(-1, -1, 32), oa * amask[..., None])
         g2 = g2 + _mlp(layer["o"], o) * mask[..., None]
         P = _mlp(layer["c"], g1)  # [n, 32]
         Pn = P[idx.clamp(min=0)]

@@ -317,11 +317,19 @@ struct DpWeightSet {
         }
         push_mlp_layer(m.fitting, 0);
         push_mlp_layer(m.fitting, 1);
-        if (m.family == kRepformer) {
+        const bool flow = m.family == kRepflow;
+        if (m.family >= kRepformer) {
             push_mlp_layer(m.g1map, 0);
             push_mlp_layer(m.g1map, 1);
             for (const RfLayer& L : m.rf) {
-                for (const Mlp* p : {&L.q, &L.k, &L.v, &L.o, &L.c}) push_mlp_layer(*p, 0);
+                if (flow) {
+                    push(L.angle.weights[0]);  // [32][1]
+                    push(L.angle.biases[0]);
+                } else {
+                    push_mlp_layer(L.q, 0);
+                    push_mlp_layer(L.k, 0);
+                }
+                for (const Mlp* p : {&L.v, &L.o, &L.c}) push_mlp_layer(*p, 0);
                 push_mlp_layer(L.update, 0);
                 push_mlp_layer(L.update, 1);
             }
@@ -356,13 +364,21 @@ struct DpWeightSet {
         }
         dev.fit1 = lin();
         dev.fit2 = lin();
-        if (m.family == kRepformer) {
+        dev.rca = static_cast<T>(m.rca);
+        dev.rcas = static_cast<T>(m.rcas);
+        dev.inv_anorm = static_cast<T>(1.0 / m.anorm);
+        if (m.family >= kRepformer) {
             dev.map1 = lin();
             dev.map2 = lin();
             for (size_t l = 0; l < m.rf.size(); ++l) {
                 DevDpLayer<T>& L = dev.L[l];
-                L.q = lin();
-                L.k = lin();
+                if (flow) {
+                    L.aw = next();
+                    L.ab = next();
+                } else {
+                    L.q = lin();
+                    L.k = lin();
+                }
                 L.v = lin();
                 L.o = lin();
                 L.c = lin();
@@ -397,7 +413,7 @@ struct hmdp_ctx {
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // DeePMD-style families: vector edge gradients and the repformer workspace
     DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
-        rf_Ts, rf_stat, rf_dob, rf_aux, rf_tmp, rf_dconv, rf_dg1;
+        rf_Ts, rf_stat, rf_dob, rf_aux, rf_tmp, rf_dconv, rf_dg1, rf_envA, rf_dua;
     // domain decomposition (hmdp_dd_*): local graph + halo row buffers
     DBuf dd_patom, dd_sremote, dd_sghost;
     DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
@@ -455,7 +471,8 @@ struct hmdp_ctx {
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
                         &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
-                        &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1})
+                        &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1,
+                        &rf_envA, &rf_dua})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -642,7 +659,7 @@ struct hmdp_ctx {
         w.gv = gv.as<T>();
         w.gvrev = gvrev.as<T>();
         DevDpWork<T> d{};
-        if (model.family != kRepformer) return d;
+        if (model.family < kRepformer) return d;
         const size_t L = model.rf.size();
         rf_env.ensure(s * 8 * sizeof(T));
         rf_g2.ensure((L + 1) * s * 32 * sizeof(T));
@@ -660,6 +677,12 @@ struct hmdp_ctx {
         rf_dob.ensure(s * 32 * sizeof(T));
         rf_aux.ensure(s * 2 * sizeof(T));
         rf_tmp.ensure(s * 96 * sizeof(T));
+        if (model.family == kRepflow) {
+            rf_envA.ensure(s * 8 * sizeof(T));
+            rf_dua.ensure(s * 4 * sizeof(T));
+            d.envA = rf_envA.as<T>();
+            d.dua = rf_dua.as<T>();
+        }
         rf_dconv.ensure(2 * na * 32 * sizeof(T));
         rf_dg1.ensure(na * 32 * sizeof(T));
         d.env = rf_env.as<T>();
@@ -1024,7 +1047,7 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
         if (ctx->model.is_dp() && (desc || h || edge_g))
             fail(HMDP_INVALID_ARGUMENT,
                  "per-stage outputs are only available for the embed_fit / message_passing families");
-        if (ctx->model.family == kRepformer)
+        if (ctx->model.family >= kRepformer)
             fail(HMDP_INVALID_ARGUMENT,
                  "repformer runs on the periodic entry points (hmdp_compute, hmdp_compute_device, "
                  "hmdp_md_*): its neighbour gathers need the symmetric list");
@@ -1286,7 +1309,7 @@ int hmdp_kernels_per_eval(const hmdp_ctx* ctx) {
     if (!ctx) return -1;
     if (ctx->model.is_dp()) {  // bin + search + hmdp_dp.cu launches
         const int L = static_cast<int>(ctx->model.rf.size());
-        return 2 + (ctx->model.family == kSeA ? 2 : 2 * L + 2);
+        return 2 + (ctx->model.family == kSeA ? 2 : 2 * L + 2);  // repformer / repflow
     }
     const int M = static_cast<int>(ctx->model.message.size());
     // bin + search + (embed_fit | embed + M fwd + (M-1) bwd + embed_bwd) + force

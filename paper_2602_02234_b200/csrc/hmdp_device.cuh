@@ -134,14 +134,17 @@ struct DevLin {
 
 template <typename T>
 struct DevDpLayer {
-    DevLin<T> q, k, v, o, c;   // [32][32] each
+    DevLin<T> q, k, v, o, c;   // [32][32] each (repflow: no q, k)
+    const T* aw;               // repflow angle embedding z = tanh(aw c + ab), [32] each
+    const T* ab;
     DevLin<T> u1, u2;          // update MLP [32 + 4*32 -> 32 -> 32]
 };
 
 template <typename T>
 struct DevDp {
     T rc, rcs, inv_nnorm;
-    int n_types, n_layers, family;  // family: kSeA / kRepformer
+    T rca, rcas, inv_anorm;         // repflow angle neighbours
+    int n_types, n_layers, family;  // family: kSeA / kRepformer / kRepflow
     T ebias[kMaxTypes];
     // per neighbour type embedding [1 -> 32 -> 32]: w1/b1 [32], layer 2 as DevLin
     const T* emb_w1[kMaxTypes];
@@ -174,6 +177,8 @@ struct DevDpWork {
     T* dconv;  // [2][n][32] adjoint of conv_i / nnorm (double-buffered by layer)
     T* dg1;    // [n][32] adjoint of g1 (residual part) of the current layer
     int smem_rows;  // 1: per-atom q/k/v and do rows live in shared memory (ELL cap <= 64)
+    T* envA;   // repflow [slot][8]: omega, omega', u_x, u_y, u_z
+    T* dua;    // repflow [slot][4]: dE/domega, dE/du (accumulated over layers)
 };
 
 // Optional per-kernel timing hook: called after every kernel launch with the

@@ -475,7 +475,29 @@ struct RfSmem {
     T x[160];       // MLP input staging (warp 0)
     T red[4][128];  // per-warp partial sums
     T bc[128];      // values broadcast to the team (dconv + dT, dA)
+    int alist[256];  // repflow: local rows of the angle neighbours (r < rca), ascending
+    int na;
 };
+
+// repflow: the atom's angle-neighbour rows (omega > 0, i.e. r < rca) in ascending
+// order, by warp 0 with a ballot per 32 rows.  Ends with a CTA barrier.
+template <typename T>
+__device__ __forceinline__ void rf_angle_list(const DevDpWork<T>& dw, int start, int cnt,
+                                              RfSmem<T>& sm) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int na = 0;
+        for (int base = 0; base < cnt; base += 32) {
+            const int r = base + lane;
+            const bool in = r < cnt && dw.envA[8ll * (start + r)] > T(0);
+            const unsigned b = __ballot_sync(FULL_MASK, in);
+            if (in) sm.alist[na + __popc(b & ((1u << lane) - 1u))] = r;
+            na += __popc(b);
+        }
+        if (lane == 0) sm.na = na;
+    }
+    __syncthreads();
+}
 
 // out_q = [res_q] + b + W x_q over the atom's cnt edge rows (warp w: q = w, w+4,
 // ...), W [32][32] row-major (lane c holds row c); rows of 32 at `in + q*ld_in`,
@@ -604,6 +626,12 @@ __global__ __launch_bounds__(kRfT) void k_rf_embed(DevDp<T> md, DevGraph gr, Dev
                 T* en = dw.env + 8ll * e;
                 st4(en, v.s, v.sw, v.s * v.ux, v.s * v.uy);
                 st4(en + 4, v.s * v.uz, v.dsw, v.r, static_cast<T>(gr.ety[e]));
+                if (md.family == kRepflow) {  // angle switch omega(r) on [rcas, rca)
+                    const Env<T> a = dp_env<T>(gr.dr + 3ll * e, md.rca, md.rcas);
+                    T* ea = dw.envA + 8ll * e;
+                    st4(ea, a.sw, a.dsw, v.ux, v.uy);
+                    st4(ea + 4, v.uz, T(0), T(0), T(0));
+                }
             }
             if (rev) {
                 const int f = find_rev(i, j, m, gr);
@@ -676,22 +704,19 @@ __global__ __launch_bounds__(kRfT) void k_rf_embed(DevDp<T> md, DevGraph gr, Dev
     }
 }
 
-// Layer l forward for the CTA's atom i; returns g1^{l+1}_i in warp 0 (lane = channel).
+// Gated, switched neighbour self-attention of one atom (forward), a quad per
+// row: o_e = sum_f softmax_f(l_ef) w_e w_f (h_e . h_f) v_f into TMP rows; the
+// row max / normaliser go to dw.stat for the backward.
 template <typename T>
-__device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
-                          long long S, int n, int l, int i, RfSmem<T>& sm) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const DevDpLayer<T>& L = md.L[l];
-    const int start = gr.row_start[i], cnt = gr.nnei[i];
-    const T* g2l = dw.g2 + (long long)l * S * 32;
-    T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
-    T* Q = rf_rows_qkv(dw, start);
-    T* TMP = dw.tmp + 96ll * start;
-    proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
-    proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
-    proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+__device__ void rf_attn_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+                            T* Q, T* TMP, long long S, int l, int start, int cnt) {
+    proj<T, false>(L.q.W, L.q.b, dw.g2 + (long long)l * S * 32 + 32ll * start, 32, nullptr, 0, Q,
+                   96, cnt);
+    proj<T, false>(L.k.W, L.k.b, dw.g2 + (long long)l * S * 32 + 32ll * start, 32, nullptr, 0,
+                   Q + 32, 96, cnt);
+    proj<T, false>(L.v.W, L.v.b, dw.g2 + (long long)l * S * 32 + 32ll * start, 32, nullptr, 0,
+                   Q + 64, 96, cnt);
     __syncthreads();
-    // attention, a quad per row
     const T sh = static_cast<T>(kShift), isq = static_cast<T>(kInvSqrt32);
     const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
     for (int rb = 0; rb < cnt; rb += 32) {
@@ -738,6 +763,65 @@ __device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWor
                 st[1] = Z;
             }
         }
+    }
+}
+
+// repflow edge/angle message of one atom (forward), a quad per row:
+// m_e = (1/anorm) sum_{f in A(i), f != e} omega_e omega_f tanh(aw c_ef + ab) * v_f
+// into TMP rows (zero for rows outside A(i)).  v rows are in Q + 64.
+template <typename T>
+__device__ void rf_angle_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+                             const T* Q, T* TMP, int start, int cnt, const RfSmem<T>& sm) {
+    const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
+    T aw[8], ab[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        aw[c] = L.aw[8 * p + c];
+        ab[c] = L.ab[8 * p + c];
+    }
+    const int na = sm.na;
+    for (int rb = 0; rb < cnt; rb += 32) {
+        const int r = rb + rq;
+        if (r >= cnt) continue;
+        const V4<T> ea = ld4c(dw.envA + 8ll * (start + r));
+        T m[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) m[c] = T(0);
+        if (ea.x > T(0)) {
+            const T ux = ea.z, uy = ea.w, uz = dw.envA[8ll * (start + r) + 4];
+            for (int a = 0; a < na; ++a) {
+                const int f = sm.alist[a];
+                if (f == r) continue;
+                const V4<T> fa = ld4c(dw.envA + 8ll * (start + f));
+                const T cs = ux * fa.z + uy * fa.w + uz * dw.envA[8ll * (start + f) + 4];
+                const T coef = ea.x * fa.x * md.inv_anorm;
+                T v[8];
+                ld8(Q + 96 * f + 64 + 8 * p, v);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) m[c] += coef * d_tanh(aw[c] * cs + ab[c]) * v[c];
+            }
+        }
+        st8(TMP + 96 * r + 8 * p, m);
+    }
+}
+
+// Layer l forward for the CTA's atom i; returns g1^{l+1}_i in warp 0 (lane = channel).
+template <typename T>
+__device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
+                          long long S, int n, int l, int i, RfSmem<T>& sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const DevDpLayer<T>& L = md.L[l];
+    const int start = gr.row_start[i], cnt = gr.nnei[i];
+    const T* g2l = dw.g2 + (long long)l * S * 32;
+    T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
+    T* Q = rf_rows_qkv(dw, start);
+    T* TMP = dw.tmp + 96ll * start;
+    if (md.family == kRepflow) {
+        proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+        rf_angle_list(dw, start, cnt, sm);
+        rf_angle_fwd(md, L, dw, Q, TMP, start, cnt, sm);
+    } else {
+        rf_attn_fwd(md, L, dw, Q, TMP, S, l, start, cnt);
     }
     __syncthreads();
     // g2hat = g2 + Wo o + bo
@@ -796,80 +880,14 @@ __device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWor
     return g1;
 }
 
-// Layer l backward for the CTA's atom i.  dg1_out (warp 0, lane = channel): the
-// adjoint of g1^{l+1}_i.  top: no g2 adjoint from above.  Writes dconv (scaled by
-// 1/nnorm) for the neighbours' P gather, the residual part of dg1^l (dw.dg1),
-// dg2 (adjoint of g2^l), and accumulates dwh.
+// Attention backward of one atom: q/k/v recomputed, do = Wo^T dg2hat, row pass
+// (S_e, dq_e, row-side dw/dh), column pass (dk_f, dv_f, column-side dw/dh), then
+// dg2 = dg2hat + Wq^T dq + Wk^T dk + Wv^T dv.
 template <typename T>
-__device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
-                             long long S, int n, int l, int i, T dg1_out, bool top,
-                             RfSmem<T>& sm) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const DevDpLayer<T>& L = md.L[l];
-    const int start = gr.row_start[i], cnt = gr.nnei[i];
-    const T* g2l = dw.g2 + (long long)l * S * 32;
-    const T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
-    if (w == 0) {
-        // update MLP backward -> dconv, dgrrg -> dT
-        const T uz = dw.uz[((long long)l * n + i) * 32 + lane];
-        T du = T(0);
-#pragma unroll 8
-        for (int c = 0; c < 32; ++c) du += __ldg(L.u2.W + c * 32 + lane) * shfl(dg1_out, c);
-        du *= (T(1) - uz * uz);
-        T dx[5] = {T(0), T(0), T(0), T(0), T(0)};
-        for (int o = 0; o < 32; ++o) {
-            const T d_o = shfl(du, o);
-#pragma unroll
-            for (int jj = 0; jj < 5; ++jj) dx[jj] += __ldg(L.u1.W + o * 160 + 32 * jj + lane) * d_o;
-        }
-        const T dconv = dx[0] * md.inv_nnorm;
-        T T3[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) T3[c] = dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane];
-        const T dgr[4] = {dx[1], dx[2], dx[3], dx[4]};
-        T dT[3];
-        gram4_bwd<T, 3>(T3, dgr, dT);
-        sm.bc[lane] = dconv;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) sm.bc[32 + 32 * c + lane] = dT[c] * md.inv_nnorm;
-        dw.dconv[((long long)(l & 1) * n + i) * 32 + lane] = dconv;
-        dw.dg1[32ll * i + lane] = dg1_out;
-    }
-    __syncthreads();
-    // per-edge adjoints of g2hat (lane = channel)
-    {
-        const T dconv = sm.bc[lane], dT0 = sm.bc[32 + lane], dT1 = sm.bc[64 + lane],
-                dT2 = sm.bc[96 + lane];
-        const T* Pl = dw.P + (long long)l * n * 32;
-        for (int q = w; q < cnt; q += 4) {
-            const long long e = start + q;
-            const T gh = g2n[32 * e + lane];
-            const T pj = Pl[32ll * gr.nbr[e] + lane];
-            const EnvRow<T> er = env_row(dw.env, e);
-            T d = top ? T(0) : dw.dg2[32 * e + lane];
-            d += er.w * dconv * pj + er.h0 * dT0 + er.h1 * dT1 + er.h2 * dT2;
-            dw.dg2[32 * e + lane] = d;
-            const T a0 = warp_sum(dconv * gh * pj);
-            const T a1 = warp_sum(dT0 * gh);
-            const T a2 = warp_sum(dT1 * gh);
-            const T a3 = warp_sum(dT2 * gh);
-            if (lane == 0) {
-                T* pw = dw.dwh + 4 * e;
-                if (top) {
-                    st4(pw, a0, a1, a2, a3);
-                } else {
-                    const V4<T> old = ld4c(pw);
-                    st4(pw, old.x + a0, old.y + a1, old.z + a2, old.w + a3);
-                }
-            }
-        }
-    }
-    __syncthreads();
+__device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+                            const T* g2l, T* Q, T* DOB, T* TMP, T* DG2, long long S, int l,
+                            int start, int cnt) {
     // q, k, v (recomputed) and do = Wo^T dg2hat
-    T* Q = rf_rows_qkv(dw, start);
-    T* DOB = rf_rows_dob(dw, start);
-    T* TMP = dw.tmp + 96ll * start;
-    T* DG2 = dw.dg2 + 32ll * start;
     proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
     proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
     proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
@@ -999,6 +1017,170 @@ __device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDp
     proj<T, true>(L.k.WT, nullptr, TMP + 32, 96, nullptr, 0, DG2, 32, cnt);
     proj<T, true>(L.v.WT, nullptr, TMP + 64, 96, nullptr, 0, DG2, 32, cnt);
     __syncthreads();
+}
+
+// repflow angle-message backward of one atom (v rows in Q + 64, dm = Wo^T dg2hat
+// rows in DOB), one pass over rows e (a quad per row) that also takes the terms
+// of every m_f that depend on row e (c_ef = c_fe, v_e):
+//   dv_e  = sum_f coef z_ef dm_f,                coef = omega_e omega_f / anorm
+//   dE/dc = coef sum_c (dm_e v_f + dm_f v_e) (1 - z^2) aw   -> dE/du_e += dE/dc u_f
+//   dE/domega_e = sum_f omega_f / anorm sum_c (dm_e v_f + dm_f v_e) z
+// dv rows go to TMP + 64 (zero outside A(i)); (domega, du) accumulate into dua.
+template <typename T>
+__device__ void rf_angle_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+                             const T* Q, const T* DOB, T* TMP, int start, int cnt, bool top,
+                             const RfSmem<T>& sm) {
+    const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
+    T aw[8], ab[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        aw[c] = L.aw[8 * p + c];
+        ab[c] = L.ab[8 * p + c];
+    }
+    const int na = sm.na;
+    for (int rb = 0; rb < cnt; rb += 32) {
+        const int r = rb + rq;
+        const bool valid = r < cnt;
+        const int rl = valid ? r : 0;
+        const long long e = start + rl;
+        const V4<T> ea = ld4c(dw.envA + 8 * e);
+        const T ux = ea.z, uy = ea.w, uz = dw.envA[8 * e + 4];
+        T dv[8], ve[8], dme[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dv[c] = T(0);
+        ld8(Q + 96 * rl + 64 + 8 * p, ve);
+        ld8(DOB + 32 * rl + 8 * p, dme);
+        T dom = T(0), du0 = T(0), du1 = T(0), du2 = T(0);
+        if (valid && ea.x > T(0)) {
+            for (int a = 0; a < na; ++a) {
+                const int f = sm.alist[a];
+                if (f == r) continue;
+                const V4<T> fa = ld4c(dw.envA + 8ll * (start + f));
+                const T fz = dw.envA[8ll * (start + f) + 4];
+                const T cs = ux * fa.z + uy * fa.w + uz * fz;
+                const T coef = ea.x * fa.x * md.inv_anorm;
+                T vf[8], dmf[8];
+                ld8(Q + 96 * f + 64 + 8 * p, vf);
+                ld8(DOB + 32 * f + 8 * p, dmf);
+                T sdc = T(0), sz = T(0);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const T z = d_tanh(aw[c] * cs + ab[c]);
+                    const T t = dme[c] * vf[c] + dmf[c] * ve[c];
+                    sdc += t * (T(1) - z * z) * aw[c];
+                    sz += t * z;
+                    dv[c] += coef * z * dmf[c];
+                }
+                const T dc = coef * sdc;
+                du0 += dc * fa.z;
+                du1 += dc * fa.w;
+                du2 += dc * fz;
+                dom += fa.x * md.inv_anorm * sz;
+            }
+        }
+        dom = quad_sum(dom);
+        du0 = quad_sum(du0);
+        du1 = quad_sum(du1);
+        du2 = quad_sum(du2);
+        if (valid) {
+            st8(TMP + 96 * r + 64 + 8 * p, dv);
+            if (p == 0) {
+                T* pa = dw.dua + 4 * e;
+                if (top) {
+                    st4(pa, dom, du0, du1, du2);
+                } else {
+                    const V4<T> old = ld4c(pa);
+                    st4(pa, old.x + dom, old.y + du0, old.z + du1, old.w + du2);
+                }
+            }
+        }
+    }
+}
+
+// Layer l backward for the CTA's atom i.  dg1_out (warp 0, lane = channel): the
+// adjoint of g1^{l+1}_i.  top: no g2 adjoint from above.  Writes dconv (scaled by
+// 1/nnorm) for the neighbours' P gather, the residual part of dg1^l (dw.dg1),
+// dg2 (adjoint of g2^l), and accumulates dwh.
+template <typename T>
+__device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
+                             long long S, int n, int l, int i, T dg1_out, bool top,
+                             RfSmem<T>& sm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const DevDpLayer<T>& L = md.L[l];
+    const int start = gr.row_start[i], cnt = gr.nnei[i];
+    const T* g2l = dw.g2 + (long long)l * S * 32;
+    const T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
+    if (w == 0) {
+        // update MLP backward -> dconv, dgrrg -> dT
+        const T uz = dw.uz[((long long)l * n + i) * 32 + lane];
+        T du = T(0);
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) du += __ldg(L.u2.W + c * 32 + lane) * shfl(dg1_out, c);
+        du *= (T(1) - uz * uz);
+        T dx[5] = {T(0), T(0), T(0), T(0), T(0)};
+        for (int o = 0; o < 32; ++o) {
+            const T d_o = shfl(du, o);
+#pragma unroll
+            for (int jj = 0; jj < 5; ++jj) dx[jj] += __ldg(L.u1.W + o * 160 + 32 * jj + lane) * d_o;
+        }
+        const T dconv = dx[0] * md.inv_nnorm;
+        T T3[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) T3[c] = dw.Ts[((long long)l * n + i) * 96 + 32 * c + lane];
+        const T dgr[4] = {dx[1], dx[2], dx[3], dx[4]};
+        T dT[3];
+        gram4_bwd<T, 3>(T3, dgr, dT);
+        sm.bc[lane] = dconv;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sm.bc[32 + 32 * c + lane] = dT[c] * md.inv_nnorm;
+        dw.dconv[((long long)(l & 1) * n + i) * 32 + lane] = dconv;
+        dw.dg1[32ll * i + lane] = dg1_out;
+    }
+    __syncthreads();
+    // per-edge adjoints of g2hat (lane = channel)
+    {
+        const T dconv = sm.bc[lane], dT0 = sm.bc[32 + lane], dT1 = sm.bc[64 + lane],
+                dT2 = sm.bc[96 + lane];
+        const T* Pl = dw.P + (long long)l * n * 32;
+        for (int q = w; q < cnt; q += 4) {
+            const long long e = start + q;
+            const T gh = g2n[32 * e + lane];
+            const T pj = Pl[32ll * gr.nbr[e] + lane];
+            const EnvRow<T> er = env_row(dw.env, e);
+            T d = top ? T(0) : dw.dg2[32 * e + lane];
+            d += er.w * dconv * pj + er.h0 * dT0 + er.h1 * dT1 + er.h2 * dT2;
+            dw.dg2[32 * e + lane] = d;
+            const T a0 = warp_sum(dconv * gh * pj);
+            const T a1 = warp_sum(dT0 * gh);
+            const T a2 = warp_sum(dT1 * gh);
+            const T a3 = warp_sum(dT2 * gh);
+            if (lane == 0) {
+                T* pw = dw.dwh + 4 * e;
+                if (top) {
+                    st4(pw, a0, a1, a2, a3);
+                } else {
+                    const V4<T> old = ld4c(pw);
+                    st4(pw, old.x + a0, old.y + a1, old.z + a2, old.w + a3);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    T* Q = rf_rows_qkv(dw, start);
+    T* DOB = rf_rows_dob(dw, start);
+    T* TMP = dw.tmp + 96ll * start;
+    T* DG2 = dw.dg2 + 32ll * start;
+    if (md.family == kRepflow) {
+        proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+        proj<T, false>(L.o.WT, nullptr, DG2, 32, nullptr, 0, DOB, 32, cnt);
+        rf_angle_list(dw, start, cnt, sm);
+        rf_angle_bwd(md, L, dw, Q, DOB, TMP, start, cnt, top, sm);
+        __syncthreads();
+        proj<T, true>(L.v.WT, nullptr, TMP + 64, 96, nullptr, 0, DG2, 32, cnt);
+        __syncthreads();
+    } else {
+        rf_attn_bwd(md, L, dw, g2l, Q, DOB, TMP, DG2, S, l, start, cnt);
+    }
 }
 
 // dg1^l_j = dg1(residual) + Wc^T dP_j with dP_j = sum_{q in out(j)} w_q g2hat^l_{rev q}
@@ -1161,6 +1343,16 @@ __global__ __launch_bounds__(kRfT) void k_rf_embed_bwd(DevDp<T> md, DevGraph gr,
                 const Env<T> v = dp_env<T>(d, md.rc, md.rcs);
                 T g[3];
                 dp_gvec(v, d, ds + dR0, dR1 + wh.y, dR2 + wh.z, dR3 + wh.w, wh.x, g);
+                if (md.family == kRepflow) {
+                    // omega(r) and u = d / r:  + dE/domega omega' u + (du - (du.u) u) / r
+                    const V4<T> ea = ld4c(dw.envA + 8 * e), da = ld4c(dw.dua + 4 * e);
+                    const T dot = da.y * v.ux + da.z * v.uy + da.w * v.uz;
+                    const T rad = da.x * ea.y - dot / v.r;
+                    const T ir = T(1) / v.r;
+                    g[0] += rad * v.ux + da.y * ir;
+                    g[1] += rad * v.uy + da.z * ir;
+                    g[2] += rad * v.uz + da.w * ir;
+                }
                 st4(ws.gv + 4 * e, g[0], g[1], g[2], T(0));
                 st4(ws.gvrev + 4ll * gr.inv_pos[e], g[0], g[1], g[2], T(0));
             }
@@ -1181,8 +1373,8 @@ cudaError_t rf_configure() {
     return e;
 }
 
-int rf_grid(int n) {
-    const int cap = num_sms() * 4;
+int rf_grid(int n) {  // one atom per CTA; as many CTAs as fit (the scheduler queues the rest)
+    const int cap = num_sms() * 16;
     return n < 1 ? 1 : (n < cap ? n : cap);
 }
 

@@ -359,8 +359,18 @@ void validate_dp(const Model& m) {
     shape(m.fitting, {kH, kH, 1}, "fitting");
     if (static_cast<int>(m.rf.size()) > kMaxMsg)
         throw std::invalid_argument("unsupported depth (kernels take <= 9)");
+    if (m.family == kRepflow) {
+        if (!(m.rcas >= 0.0 && m.rcas < m.rca && m.rca <= m.rc))
+            throw std::invalid_argument("repflow needs 0 <= rc_angle_smooth < rc_angle <= rc_model");
+        if (!(m.anorm > 0.0)) throw std::invalid_argument("anorm must be positive");
+    }
     for (const RfLayer& l : m.rf) {
-        for (const Mlp* p : {&l.q, &l.k, &l.v, &l.o, &l.c}) shape(*p, {kH, kH}, "attention");
+        if (m.family == kRepflow) {
+            shape(l.angle, {1, kH}, "angle");
+            for (const Mlp* p : {&l.v, &l.o, &l.c}) shape(*p, {kH, kH}, "edge");
+        } else {
+            for (const Mlp* p : {&l.q, &l.k, &l.v, &l.o, &l.c}) shape(*p, {kH, kH}, "attention");
+        }
         shape(l.update, {kH + nd, kH, kH}, "update");
     }
 }
@@ -420,7 +430,7 @@ void Model::counters(int n, int n_owned, long long ne, int real_bytes,
         fl += n * 3.0 * (2.0 * axis * 4 * H);
         fl += n_owned * 3.0 * fitting.forward_flops();
         act += static_cast<double>(ne) * (8 + 2 * H) + n * (nd + fitting.act_size());
-        if (family == kRepformer) {
+        if (family >= kRepformer) {
             fl += n * 3.0 * g1map.forward_flops();
             for (const RfLayer& l : rf) {
                 fl += ne * 3.0 * (4.0 * l.q.forward_flops() + 6 * H);
@@ -475,6 +485,8 @@ Model model_from_json(const std::string& text) {
         m.family = kSeA;
     else if (fam.kind == JVal::Str && fam.str == "repformer")
         m.family = kRepformer;
+    else if (fam.kind == JVal::Str && fam.str == "repflow")
+        m.family = kRepflow;
     else
         throw std::invalid_argument("unknown model family '" + fam.str + "'");
     if (m.is_dp()) {
@@ -491,15 +503,24 @@ Model model_from_json(const std::string& text) {
         for (const auto& e : em.arr) m.embeds.push_back(mlp_from(e));
         m.ebias = j.at("energy_bias").as_vec();
         m.fitting = mlp_from(j.at("fitting"));
-        if (m.family == kRepformer) {
+        if (m.family == kRepflow) {
+            m.rca = j.at("rc_angle").as_num();
+            m.rcas = j.at("rc_angle_smooth").as_num();
+            m.anorm = j.at("anorm").as_num();
+        }
+        if (m.family >= kRepformer) {
             m.g1map = mlp_from(j.at("g1map"));
             const JVal& layers = j.at("layers");
             if (layers.kind != JVal::Arr)
                 throw std::invalid_argument("model JSON: layers must be an array");
             for (const auto& jl : layers.arr) {
                 RfLayer l;
-                l.q = mlp_from(jl.at("q"));
-                l.k = mlp_from(jl.at("k"));
+                if (m.family == kRepflow) {
+                    l.angle = mlp_from(jl.at("angle"));
+                } else {
+                    l.q = mlp_from(jl.at("q"));
+                    l.k = mlp_from(jl.at("k"));
+                }
                 l.v = mlp_from(jl.at("v"));
                 l.o = mlp_from(jl.at("o"));
                 l.c = mlp_from(jl.at("c"));
@@ -534,7 +555,7 @@ std::string dp_to_json(const Model& m) {
     std::string o;
     o.reserve(400000);
     o += "{\"format\":\"halomd-model\",\"version\":1,\"family\":\"";
-    o += m.family == kSeA ? "se_a" : "repformer";
+    o += m.family == kSeA ? "se_a" : (m.family == kRepformer ? "repformer" : "repflow");
     o += "\",\"rc_model\":";
     put_num(o, m.rc);
     o += ",\"rc_smooth\":";
@@ -554,19 +575,31 @@ std::string dp_to_json(const Model& m) {
     put_vec(o, m.ebias);
     o += ",\"fitting\":";
     put_mlp(o, m.fitting);
-    if (m.family == kRepformer) {
+    if (m.family == kRepflow) {
+        o += ",\"rc_angle\":";
+        put_num(o, m.rca);
+        o += ",\"rc_angle_smooth\":";
+        put_num(o, m.rcas);
+        o += ",\"anorm\":";
+        put_num(o, m.anorm);
+    }
+    if (m.family >= kRepformer) {
         o += ",\"g1map\":";
         put_mlp(o, m.g1map);
         o += ",\"layers\":[";
         for (std::size_t l = 0; l < m.rf.size(); ++l) {
             if (l) o += ',';
             const RfLayer& L = m.rf[l];
-            const std::pair<const char*, const Mlp*> parts[] = {{"q", &L.q}, {"k", &L.k},
-                                                                {"v", &L.v}, {"o", &L.o},
-                                                                {"c", &L.c}, {"update", &L.update}};
+            const bool flow = m.family == kRepflow;
+            const std::pair<const char*, const Mlp*> parts[] = {
+                {flow ? "angle" : "q", flow ? &L.angle : &L.q}, {"k", &L.k}, {"v", &L.v},
+                {"o", &L.o}, {"c", &L.c}, {"update", &L.update}};
             o += '{';
+            bool first = true;
             for (int p = 0; p < 6; ++p) {
-                if (p) o += ',';
+                if (flow && p == 1) continue;
+                if (!first) o += ',';
+                first = false;
                 o += std::string("\"") + parts[p].first + "\":";
                 put_mlp(o, *parts[p].second);
             }
@@ -640,8 +673,8 @@ Model make_model(int family, int depth, double rc, int n_types, int n_basis, int
 
 Model make_dp_model(int family, int depth, double rc, double rcs, int n_types, int axis,
                     std::uint64_t seed) {
-    if (family != kSeA && family != kRepformer)
-        throw std::invalid_argument("make_dp_model: family must be se_a or repformer");
+    if (family != kSeA && family != kRepformer && family != kRepflow)
+        throw std::invalid_argument("make_dp_model: family must be se_a, repformer or repflow");
     if (depth < 1) throw std::invalid_argument("depth must be >= 1");
     if (family == kSeA && depth != 1) throw std::invalid_argument("se_a has depth 1 by construction");
     Model m;
@@ -658,12 +691,16 @@ Model make_dp_model(int family, int depth, double rc, double rcs, int n_types, i
     const int nd = axis * kH;
     m.fitting = random_mlp({family == kSeA ? nd : kH, kH, 1}, rng);
     for (int t = 0; t < n_types; ++t) m.ebias.push_back(rng.uniform(-1.0, 1.0));
-    if (family == kRepformer) {
+    if (family >= kRepformer) {
         m.g1map = random_mlp({nd, kH, kH}, rng);
         for (int l = 1; l < depth; ++l) {
             RfLayer L;
-            L.q = random_mlp({kH, kH}, rng);
-            L.k = random_mlp({kH, kH}, rng);
+            if (family == kRepflow) {
+                L.angle = random_mlp({1, kH}, rng);
+            } else {
+                L.q = random_mlp({kH, kH}, rng);
+                L.k = random_mlp({kH, kH}, rng);
+            }
             L.v = random_mlp({kH, kH}, rng);
             L.o = random_mlp({kH, kH}, rng);
             L.c = random_mlp({kH, kH}, rng);

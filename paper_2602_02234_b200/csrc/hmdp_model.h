@@ -28,13 +28,15 @@ struct Mlp {
 // One repformer layer of the DeePMD-style "repformer" family:
 // attention projections q, k, v, o and the neighbour projection c are single
 // linear layers [32, 32] (Mlp with one layer); update is [32 + axis*32, 32, 32].
+// repflow layers carry `angle` [1, 32] (the elementwise angle embedding) instead
+// of q and k.
 struct RfLayer {
-    Mlp q, k, v, o, c, update;
+    Mlp q, k, v, o, c, update, angle;
 };
 
 // Model families: the reference's two (model.hpp:9) plus the DeePMD-style
 // families of the north star that have no reference function (SURVEY §8(a')).
-enum Family : int { kEmbedFit = 0, kMessagePassing = 1, kSeA = 2, kRepformer = 3 };
+enum Family : int { kEmbedFit = 0, kMessagePassing = 1, kSeA = 2, kRepformer = 3, kRepflow = 4 };
 
 struct Model {
     int family = 0;  // Family
@@ -56,6 +58,8 @@ struct Model {
     std::vector<double> ebias;
     Mlp g1map;
     std::vector<RfLayer> rf;
+    // repflow: angle neighbours r < rca, switch onset rcas, angle normaliser anorm
+    double rca = 0.4, rcas = 0.2, anorm = 8.0;
 
     bool is_dp() const { return family >= kSeA; }
     int n_basis() const { return static_cast<int>(centers.size()); }

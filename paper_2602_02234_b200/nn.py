@@ -31,12 +31,14 @@ class ModelFamily(enum.IntEnum):
     """model.hpp:9 ``enum class ModelFamily { embed_fit, message_passing }``, plus the
     DeePMD-style families of the north star that have no reference function
     (SURVEY.md §8(a')): ``se_a`` (smooth env matrix, G^T R R^T G) and
-    ``repformer`` (DPA2-style gated neighbour self-attention)."""
+    ``repformer`` (DPA2-style gated neighbour self-attention) and ``repflow``
+    (DPA3-style edge/angle message passing)."""
 
     embed_fit = 0
     message_passing = 1
     se_a = 2
     repformer = 3
+    repflow = 4
 
 
 class Precision(enum.IntEnum):
@@ -142,7 +144,7 @@ def make_model(family: ModelFamily, depth: int, rc_model: float, n_types: int, n
 
 def make_dp_model(family: ModelFamily, depth: int, rc_model: float = 0.6, rc_smooth: float = 0.3,
                   n_types: int = 2, seed: int = 1, axis: int = 4) -> NnModel:
-    """Random-init DeePMD-style model (se_a: depth 1; repformer: depth - 1 layers),
+    """Random-init DeePMD-style model (se_a: depth 1; repformer / repflow: depth - 1 layers),
     same Rng / MLP init as make_model.  No reference function (parity unpinned)."""
     L = lib()
     args = (int(family), int(depth), float(rc_model), float(rc_smooth), int(n_types), int(axis),

@@ -15,8 +15,9 @@ import paper_2602_02234_b200 as P
 from oracle import dpfamily as DF
 from conftest import E_TOL, F_TOL, rms
 
-FAMS = [(P.ModelFamily.se_a, 1), (P.ModelFamily.repformer, 2), (P.ModelFamily.repformer, 3)]
-IDS = ["se_a", "repformer_d2", "repformer_d3"]
+FAMS = [(P.ModelFamily.se_a, 1), (P.ModelFamily.repformer, 2), (P.ModelFamily.repformer, 3),
+        (P.ModelFamily.repflow, 2), (P.ModelFamily.repflow, 3)]
+IDS = ["se_a", "repformer_d2", "repformer_d3", "repflow_d2", "repflow_d3"]
 
 
 def _system(n, seed=7):
@@ -123,10 +124,11 @@ def test_oracle_rotation_permutation_invariance(fam, depth, small):
     assert np.abs(per["forces"] - out["forces"][perm]).max() < 1e-10 * rms(out["forces"])
 
 
-def test_oracle_smooth_at_cutoff():
+@pytest.mark.parametrize("fam", [P.ModelFamily.repformer, P.ModelFamily.repflow])
+def test_oracle_smooth_at_cutoff(fam):
     """Energy is continuous as a neighbour crosses rc (the switch and the gated,
-    switched attention both vanish there)."""
-    d = P.make_dp_model(P.ModelFamily.repformer, 2).as_dict()
+    switched attention / angle messages all vanish there)."""
+    d = P.make_dp_model(fam, 2).as_dict()
     types = [0, 1, 1]
     base = np.array([[0.0, 0.0, 0.0], [0.25, 0.1, 0.0]])
 
@@ -138,6 +140,9 @@ def test_oracle_smooth_at_cutoff():
 
     inside, outside = energy(0.6 - 1e-7), energy(0.6 + 1e-7)
     assert abs(inside - outside) < 1e-6
+    if fam == P.ModelFamily.repflow:  # and as it crosses the angle cutoff
+        ra = d["rc_angle"]
+        assert abs(energy(ra - 1e-7) - energy(ra + 1e-7)) < 1e-6
 
 
 def test_counters_and_launches_cpu():
@@ -204,12 +209,13 @@ def test_gpu_se_a_csr_path_with_ghosts_free_list():
                     edge_offset=off, edge_neighbor=nbr, edge_dr=dr)
     out = P.evaluate(m, inp, P.Precision.fp64)
     _check(out, ref, 1e-11, 1e-9)
-    with pytest.raises(ValueError):
-        P.evaluate(P.make_dp_model(P.ModelFamily.repformer, 2), inp, P.Precision.fp64)
+    for fam in (P.ModelFamily.repformer, P.ModelFamily.repflow):
+        with pytest.raises(ValueError):
+            P.evaluate(P.make_dp_model(fam, 2), inp, P.Precision.fp64)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fam,depth", FAMS[:2], ids=IDS[:2])
+@pytest.mark.parametrize("fam,depth", FAMS[:2] + FAMS[3:4], ids=IDS[:2] + IDS[3:4])
 def test_gpu_md_loop(fam, depth):
     """Device MD with a DeePMD-style model: state after 6 steps matches a host
     velocity-Verlet loop driven by the FP64 oracle."""
