@@ -152,59 +152,7 @@ __device__ __forceinline__ T cmv(const T* __restrict__ WT, const T* __restrict__
     for (int k = 0; k < 32; ++k) acc += __ldg(WT + k * 32 + lane) * shfl(x, k);
     return acc;
 }
-// Lane = channel mat-vec with x in shared memory (nin inputs, WT [nin][32]).
-template <typename T>
-__device__ __forceinline__ T cmv_s(const T* __restrict__ WT, const T* __restrict__ b,
-                                   const T* xs, int nin) {
-    const int lane = threadIdx.x & 31;
-    T acc = b ? __ldg(b + lane) : T(0);
-#pragma unroll 8
-    for (int k = 0; k < nin; ++k) acc += __ldg(WT + k * 32 + lane) * xs[k];
-    return acc;
-}
 
-// Lane = row mat-vec: y = W x (+ b), W [32][32] row-major read at uniform
-// addresses (broadcast), x and y in registers.
-template <typename T>
-__device__ __forceinline__ void rmv(const T* __restrict__ W, const T* __restrict__ b,
-                                    const T (&x)[32], T (&y)[32]) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-        T acc = b ? __ldg(b + c) : T(0);
-#pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-            const V4<T> w = ld4(W + c * 32 + k);
-            acc += w.x * x[k] + w.y * x[k + 1] + w.z * x[k + 2] + w.w * x[k + 3];
-        }
-        y[c] = acc;
-    }
-}
-template <typename T>
-__device__ __forceinline__ void load_row(const T* p, T (&x)[32]) {  // coherent (same-kernel data)
-#pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-        const V4<T> v = ld4c(p + k);
-        x[k] = v.x;
-        x[k + 1] = v.y;
-        x[k + 2] = v.z;
-        x[k + 3] = v.w;
-    }
-}
-template <typename T>
-__device__ __forceinline__ void store_row(T* p, const T (&x)[32]) {
-#pragma unroll
-    for (int k = 0; k < 32; k += 4) st4(p + k, x[k], x[k + 1], x[k + 2], x[k + 3]);
-}
-template <typename T>
-__device__ __forceinline__ T dot32(const T (&a)[32], const T* p) {  // a . row p (coherent)
-    T acc = T(0);
-#pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-        const V4<T> v = ld4c(p + k);
-        acc += a[k] * v.x + a[k + 1] * v.y + a[k + 2] * v.z + a[k + 3] * v.w;
-    }
-    return acc;
-}
 
 // A (lane b holds A[c][b], c < 4) -> D[a][b] = sum_c A[c][a] A[c][b], a < 4.
 template <typename T>
@@ -236,6 +184,7 @@ __device__ __forceinline__ void gram4_bwd(const T (&A)[NC], const T (&dD)[4], T 
             if (lane == a) dA[c] += x;
         }
 }
+
 
 struct DpWarpSmem {
     double s[32];
@@ -886,11 +835,14 @@ __device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWor
 template <typename T>
 __device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
                             const T* g2l, T* Q, T* DOB, T* TMP, T* DG2, long long S, int l,
-                            int start, int cnt) {
-    // q, k, v (recomputed) and do = Wo^T dg2hat
-    proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
-    proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
-    proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+                            int start, int cnt, bool have_qkv) {
+    // q, k, v (recomputed unless the forward of this layer just left them in Q)
+    // and do = Wo^T dg2hat
+    if (!have_qkv) {
+        proj<T, false>(L.q.W, L.q.b, g2l + 32ll * start, 32, nullptr, 0, Q, 96, cnt);
+        proj<T, false>(L.k.W, L.k.b, g2l + 32ll * start, 32, nullptr, 0, Q + 32, 96, cnt);
+        proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+    }
     proj<T, false>(L.o.WT, nullptr, DG2, 32, nullptr, 0, DOB, 32, cnt);
     __syncthreads();
     const T sh = static_cast<T>(kShift), isq = static_cast<T>(kInvSqrt32);
@@ -1171,15 +1123,17 @@ __device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDp
     T* TMP = dw.tmp + 96ll * start;
     T* DG2 = dw.dg2 + 32ll * start;
     if (md.family == kRepflow) {
-        proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
+        if (!top)  // the top kernel's forward left v in Q + 64 (and the angle list)
+            proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
         proj<T, false>(L.o.WT, nullptr, DG2, 32, nullptr, 0, DOB, 32, cnt);
-        rf_angle_list(dw, start, cnt, sm);
+        if (!top) rf_angle_list(dw, start, cnt, sm);
+        else __syncthreads();
         rf_angle_bwd(md, L, dw, Q, DOB, TMP, start, cnt, top, sm);
         __syncthreads();
         proj<T, true>(L.v.WT, nullptr, TMP + 64, 96, nullptr, 0, DG2, 32, cnt);
         __syncthreads();
     } else {
-        rf_attn_bwd(md, L, dw, g2l, Q, DOB, TMP, DG2, S, l, start, cnt);
+        rf_attn_bwd(md, L, dw, g2l, Q, DOB, TMP, DG2, S, l, start, cnt, top);
     }
 }
 
@@ -1373,16 +1327,17 @@ cudaError_t rf_configure() {
     return e;
 }
 
+int dp_grid(int n) {  // one warp per atom (se_a)
+    const int want = (n + kDpWarps - 1) / kDpWarps;
+    const int cap = num_sms() * 8;
+    return want < 1 ? 1 : (want < cap ? want : cap);
+}
+
 int rf_grid(int n) {  // one atom per CTA; as many CTAs as fit (the scheduler queues the rest)
     const int cap = num_sms() * 16;
     return n < 1 ? 1 : (n < cap ? n : cap);
 }
 
-int dp_grid(int n) {
-    const int want = (n + kDpWarps - 1) / kDpWarps;
-    const int cap = num_sms() * 8;
-    return want < 1 ? 1 : (want < cap ? want : cap);
-}
 
 }  // namespace
 
@@ -1397,9 +1352,9 @@ template <typename T>
 int launch_dp(const DevDp<T>& md, const DevGraph& gr, const DevWork<T>& ws,
               const DevDpWork<T>& dw, double* forces, double* per_atom, double* out, int* rev,
               cudaStream_t st, const Marker& mk, const MdFuse& mf) {
-    const dim3 grid(dp_grid(gr.n_active)), block(kDpCTA);
+    const dim3 block(kDpCTA);
     if (md.family == kSeA) {
-        launch_pdl(k_sea<T>, grid, block, 0, st, md, gr, ws, rev, mf);
+        launch_pdl(k_sea<T>, dim3(dp_grid(gr.n_active)), block, 0, st, md, gr, ws, rev, mf);
         mk("sea", st);
         launch_force<T>(gr, ws, forces, per_atom, out, st, mf);
         mk("force", st);
