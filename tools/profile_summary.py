@@ -25,11 +25,16 @@ PROFILE_NAME = {
     "k_msg_fwd<float, 0>": "msg_fwd", "k_msg_fwd<float, 1>": "msg_fwd_last",
     "k_msg_bwd<float>": "msg_bwd", "k_embed_bwd<float>": "embed_bwd", "k_force<float>": "force",
     "k_nbr_search": "nbr_search",
+    "k_sea<float>": "sea", "k_rf_embed<float>": "rf_embed", "k_rf_fwd<float>": "rf_fwd",
+    "k_rf_top<float>": "rf_top", "k_rf_bwd<float>": "rf_bwd", "k_rf_embed_bwd<float>": "rf_embed_bwd",
 }
 
 
 def short(name):
-    return name.replace("void ", "").split("(")[0].replace("hmdp::", "")
+    base = (name.replace("void ", "").replace("(anonymous namespace)::", "")
+            .replace("<unnamed>::", "").split("(")[0])
+    head, sep, args = base.partition("<")
+    return head.split("::")[-1] + sep + args
 
 
 def profile_name(name):
