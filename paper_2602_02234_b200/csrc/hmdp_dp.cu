@@ -858,22 +858,14 @@ __device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const De
         const T* st = dw.stat + ((long long)l * S + e) * 2;
         const T mx = st[0], iz = T(1) / st[1];
         const EnvRow<T> er = env_row(dw.env, e);
-        T Ssum = T(0);
-#pragma unroll 2
-        for (int f = 0; f < cnt; ++f) {
-            const long long ef = start + f;
-            const T lam = quad_sum(dot8(q, Q + 96 * f + 32 + 8 * p)) * isq;
-            const T db = quad_sum(dot8(dov, Q + 96 * f + 64 + 8 * p));
-            const EnvRow<T> fr = env_row(dw.env, ef);
-            const T ww = er.w * fr.w;
-            const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
-            const T al = d_exp((lam + sh) * ww - sh - mx) * iz;
-            Ssum += al * db * ww * gam;
-        }
-        T dq[8];
+        // one pass: with dlt_ef = a_ef (da_ef - S_e), every S_e-dependent sum splits
+        // into two S_e-free sums combined after the loop
+        //   dq_e  = isq (sum a da ww k_f - S_e sum a ww k_f)
+        //   dw_e += sum db a gam w_f + sum a da (lam+sh) w_f - S_e sum a (lam+sh) w_f
+        T Ssum = T(0), k1[8], k2[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) dq[c] = T(0);
-        T dwe = T(0), dh0 = T(0), dh1 = T(0), dh2 = T(0);
+        for (int c = 0; c < 8; ++c) k1[c] = k2[c] = T(0);
+        T dwe = T(0), dwa = T(0), dwb = T(0), dh0 = T(0), dh1 = T(0), dh2 = T(0);
 #pragma unroll 2
         for (int f = 0; f < cnt; ++f) {
             const long long ef = start + f;
@@ -885,19 +877,28 @@ __device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const De
             const T gam = er.h0 * fr.h0 + er.h1 * fr.h1 + er.h2 * fr.h2;
             const T al = d_exp((lam + sh) * ww - sh - mx) * iz;
             const T da = db * ww * gam;
-            const T dlt = al * (da - Ssum);
-            const T dlam = dlt * ww * isq;
+            Ssum += al * da;
+            const T aw = al * ww, ada = aw * da;
             T k[8];
             ld8(kf, k);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) dq[c] += dlam * k[c];
-            const T dww = db * al * gam + dlt * (lam + sh);
-            const T dgam = db * al * ww;
-            dwe += dww * fr.w;
+            for (int c = 0; c < 8; ++c) {
+                k1[c] += ada * k[c];
+                k2[c] += aw * k[c];
+            }
+            const T lw = (lam + sh) * fr.w;
+            dwe += db * al * gam * fr.w;
+            dwa += al * da * lw;
+            dwb += al * lw;
+            const T dgam = db * aw;
             dh0 += dgam * fr.h0;
             dh1 += dgam * fr.h1;
             dh2 += dgam * fr.h2;
         }
+        T dq[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dq[c] = isq * (k1[c] - Ssum * k2[c]);
+        dwe += dwa - Ssum * dwb;
         if (valid) {
             st8(TMP + 96 * r + 8 * p, dq);
             if (p == 0) {
