@@ -417,6 +417,12 @@ __global__ __launch_bounds__(kDpCTA) void k_sea(DevDp<T> md, DevGraph gr, DevWor
 //     from per-warp partials summed in a fixed order in shared memory.
 // ---------------------------------------------------------------------------
 constexpr int kRfT = 128;
+// Resident CTAs per SM the register budget targets for the lighter kernels (embed,
+// forward layers, embed backward): 6 in FP32 (<= 80 registers, 24 warps per SM for
+// these latency-bound atom teams), 2 in FP64.  The top / backward layer kernels keep
+// the compiler's choice (128 registers): forcing 80 spills and measured slower.
+template <typename T>
+constexpr int kRfMinB = sizeof(T) == 4 ? 6 : 2;
 constexpr double kInvSqrt32 = 0.17677669529663688;  // 1 / sqrt(32)
 
 template <typename T>
@@ -546,7 +552,7 @@ __device__ __forceinline__ EnvRow<T> env_row(const T* env, long long e) {
 
 // embedding + descriptor + g1 map + P^0, one atom per CTA
 template <typename T>
-__global__ __launch_bounds__(kRfT) void k_rf_embed(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_embed(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                    DevDpWork<T> dw, int* __restrict__ rev,
                                                    MdFuse mf) {
     __shared__ RfSmem<T> sm;
@@ -1184,7 +1190,7 @@ __device__ __forceinline__ T rf_fit(const DevDp<T>& md, const DevGraph& gr, cons
 
 // Layer l forward (l < L - 1): g1^{l+1}, P^{l+1}.
 template <typename T>
-__global__ __launch_bounds__(kRfT) void k_rf_fwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_fwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                  DevDpWork<T> dw, int l) {
     __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
@@ -1231,7 +1237,7 @@ __global__ __launch_bounds__(kRfT) void k_rf_bwd(DevDp<T> md, DevGraph gr, DevWo
 
 // Gather for layer 0, g1 map + descriptor + embedding backward -> dE/d(edge_dr).
 template <typename T>
-__global__ __launch_bounds__(kRfT) void k_rf_embed_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
+__global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_embed_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                        DevDpWork<T> dw) {
     __shared__ RfSmem<T> sm;
     pdl_launch_dependents();
