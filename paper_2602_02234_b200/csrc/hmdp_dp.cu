@@ -331,7 +331,9 @@ __global__ __launch_bounds__(kDpCTA) void k_sea(DevDp<T> md, DevGraph gr, DevWor
 #pragma unroll
         for (int c = 0; c < 4; ++c) sm.zs[0][c][lane] = dA[c];
         __syncwarp();
-        T V[kMaxTypes][4], c0[kMaxTypes][4];
+        // V_t[c][o] = sum_b W2_t[b][o] dA[c][b] (lane o) into zs[t][c][o]; c0_t[c]
+        T c0[kMaxTypes][4];
+        T V[kMaxTypes][4];
 #pragma unroll
         for (int t = 0; t < kMaxTypes; ++t) {
 #pragma unroll
@@ -349,46 +351,49 @@ __global__ __launch_bounds__(kDpCTA) void k_sea(DevDp<T> md, DevGraph gr, DevWor
             }
         }
         __syncwarp();
-        // pass 2: per-edge adjoints -> dE/d(edge_dr)
+#pragma unroll
+        for (int t = 0; t < kMaxTypes; ++t)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm.zs[t][c][lane] = V[t][c];
+        __syncwarp();
+        // pass 2: per-edge adjoints -> dE/d(edge_dr), LANE = EDGE: each lane runs the
+        // 32 channels of its own edge (no cross-lane reductions)
+        //   z_o = tanh(w1_o s + b1_o), dR_c = sum_o V[c][o] z_o + c0[c],
+        //   ds = sum_o w1_o (sum_c R_c V[c][o]) (1 - z_o^2)
         for (int base = 0; base < cnt; base += 32) {
             const int m = min(32, cnt - base);
             const int e = start + base + lane;
             Env<T> v{};
+            T mdR[4] = {T(0), T(0), T(0), T(0)}, mds = T(0);
             if (lane < m) {
                 v = dp_env<T>(gr.dr + 3ll * e, md.rc, md.rcs);
-                sm.s[lane] = v.s;
-                sm.R[lane][0] = v.s;
-                sm.R[lane][1] = v.s * v.ux;
-                sm.R[lane][2] = v.s * v.uy;
-                sm.R[lane][3] = v.s * v.uz;
-                sm.t[lane] = gr.ety[e];
-            }
-            __syncwarp();
-            T mdR[4] = {T(0), T(0), T(0), T(0)}, mds = T(0);
-            for (int u = 0; u < m; ++u) {
-                const int t = sm.t[u];
-                const T s = static_cast<T>(sm.s[u]);
-                const T R0 = static_cast<T>(sm.R[u][0]), R1 = static_cast<T>(sm.R[u][1]),
-                        R2 = static_cast<T>(sm.R[u][2]), R3 = static_cast<T>(sm.R[u][3]);
+                const int t = gr.ety[e];
+                const T sv = v.s, R1 = v.s * v.ux, R2 = v.s * v.uy, R3 = v.s * v.uz;
+                const T* w1t = md.emb_w1[0];
+                const T* b1t = md.emb_b1[0];
 #pragma unroll
                 for (int tt = 0; tt < kMaxTypes; ++tt)
                     if (tt == t) {
-                        const T z = d_tanh(w1[tt] * s + b1[tt]);
-                        const T dz = (R0 * V[tt][0] + R1 * V[tt][1] + R2 * V[tt][2] + R3 * V[tt][3]) *
-                                     (T(1) - z * z);
-                        const T p0 = warp_sum(V[tt][0] * z) + c0[tt][0];
-                        const T p1 = warp_sum(V[tt][1] * z) + c0[tt][1];
-                        const T p2 = warp_sum(V[tt][2] * z) + c0[tt][2];
-                        const T p3 = warp_sum(V[tt][3] * z) + c0[tt][3];
-                        const T ds = warp_sum(w1[tt] * dz);
-                        if (lane == u) {
-                            mdR[0] = p0;
-                            mdR[1] = p1;
-                            mdR[2] = p2;
-                            mdR[3] = p3;
-                            mds = ds;
-                        }
+                        w1t = md.emb_w1[tt];
+                        b1t = md.emb_b1[tt];
+                        mdR[0] = c0[tt][0];
+                        mdR[1] = c0[tt][1];
+                        mdR[2] = c0[tt][2];
+                        mdR[3] = c0[tt][3];
                     }
+                const double* Vt = &sm.zs[t][0][0];
+#pragma unroll 4
+                for (int o = 0; o < 32; ++o) {
+                    const T w = __ldg(w1t + o);
+                    const T z = d_tanh(w * sv + __ldg(b1t + o));
+                    const T v0 = static_cast<T>(Vt[o]), v1 = static_cast<T>(Vt[32 + o]),
+                            v2 = static_cast<T>(Vt[64 + o]), v3 = static_cast<T>(Vt[96 + o]);
+                    mdR[0] += v0 * z;
+                    mdR[1] += v1 * z;
+                    mdR[2] += v2 * z;
+                    mdR[3] += v3 * z;
+                    mds += w * (sv * v0 + R1 * v1 + R2 * v2 + R3 * v3) * (T(1) - z * z);
+                }
             }
             if (lane < m) {
                 T g[3];
