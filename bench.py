@@ -66,8 +66,10 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--mode", choices=["dd", "replicas"], default="dd",
-                    help="N>1: domain decomposition (default) or independent replica boxes")
+    ap.add_argument("--mode", choices=["dd", "replicas"], default="replicas",
+                    help="N>1: independent replica boxes per GPU (default; weak scaling, no "
+                         "data-path collective) or spatial domain decomposition of one "
+                         "replicated box (host-orchestrated, DESIGN.md §6)")
     return ap.parse_args()
 
 
