@@ -244,3 +244,61 @@ def test_gpu_md_loop(fam, depth):
     assert np.abs(x_dev - x).max() < 1e-10
     assert np.abs(v_dev - v).max() < 1e-8
     assert e_dev == pytest.approx(e, rel=1e-10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam,depth", FAMS[:2] + FAMS[3:4], ids=IDS[:2] + IDS[3:4])
+def test_gpu_group_provider(fam, depth):
+    """NNPot hybrid coupling (hmdp_compute_group) with a DeePMD-style model equals
+    the model on the extracted group and leaves the other atoms alone."""
+    from paper_2602_02234_b200.hybrid import (nn_force_provider, plan_group_preprocessing,
+                                              synthetic_topology)
+
+    s = P.generate_synthetic_system(582)
+    _, plan = plan_group_preprocessing(synthetic_topology(582), "protein")
+    m = P.make_dp_model(fam, depth)
+    ctx = P.Context(m)
+    f = np.zeros((582, 3))
+    e = nn_force_provider(ctx, s.positions, s.types, s.box, plan, f, P.Precision.fp64)
+    g = plan.atoms
+    off, nbr, dr = O.neighbors(s.positions[g], s.box, 0.6)
+    ref = DF.evaluate(m.as_dict(), s.types[g], off, nbr, dr)
+    assert e == pytest.approx(ref["energy"], rel=1e-11)
+    assert np.abs(f[g] - ref["forces"]).max() < 1e-9 * rms(ref["forces"])
+    assert not np.any(f[np.setdiff1d(np.arange(582), g)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam,depth", [(P.ModelFamily.se_a, 1), (P.ModelFamily.repflow, 2)])
+def test_gpu_four_types(fam, depth):
+    s, off, nbr, dr = _system(582)
+    types = (np.arange(582) * 7) % 4
+    m = P.make_dp_model(fam, depth, n_types=4, seed=5)
+    ref = DF.evaluate(m.as_dict(), types, off, nbr, dr)
+    out = P.Context(m).compute(s.positions, types, s.box, P.Precision.fp64)
+    _check(out, ref, 1e-11, 1e-9)
+    with pytest.raises(ValueError):
+        P.Context(m).compute(s.positions, np.full(582, 4), s.box, P.Precision.fp64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam,depth", [(P.ModelFamily.se_a, 1), (P.ModelFamily.repformer, 2),
+                                       (P.ModelFamily.repflow, 2)])
+def test_gpu_nve_energy_conservation(fam, depth):
+    """Smooth potentials conserve energy: 400 FP64 velocity-Verlet steps of 0.5 fs
+    on the device keep E_kin + E_pot within a small drift."""
+    from paper_2602_02234_b200.md import DeviceMD
+
+    s = P.generate_synthetic_system(582, temperature=300.0)
+    m = P.make_dp_model(fam, depth)
+    md = DeviceMD(P.Context(m), s.positions, s.velocities, s.masses, s.types, s.box,
+                  dt_ps=0.0005, precision=P.Precision.fp64, steps_per_graph=50)
+
+    def etot():
+        x, v, f, ep = md.state()
+        return ep + 0.5 * float(np.sum(s.masses[:, None] * v * v))
+
+    e0 = etot()
+    ke0 = 0.5 * float(np.sum(s.masses[:, None] * s.velocities ** 2))
+    md.run(400)
+    assert abs(etot() - e0) < 2e-3 * ke0
