@@ -46,6 +46,7 @@ int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWo
               double*, double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
+void launch_stage_in(int, const double*, const int*, double*, int*, cudaStream_t);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
 
@@ -125,7 +126,8 @@ struct PinnedBuf {
         if (p) cudaFreeHost(p);
         p = nullptr;
         bytes = 0;
-        ck(cudaMallocHost(&p, std::max<size_t>(need, 4096)), "cudaMallocHost");
+        // mapped: kernels address it directly (UVA), e.g. hmdp_compute's graph path
+        ck(cudaHostAlloc(&p, std::max<size_t>(need, 4096), cudaHostAllocMapped), "cudaHostAlloc");
         bytes = std::max<size_t>(need, 4096);
     }
     void release() {
@@ -735,24 +737,29 @@ struct hmdp_ctx {
         return d;
     }
 
+    // hmdp_compute's graph path: (E, W, W9, err) to this host-mapped block instead of `out`
+    double* out_override = nullptr;
+
     template <typename T>
     int network(const DevGraph& gr, long long slots, double* d_forces, double* d_per_atom,
                 cudaStream_t st, int* d_rev, const MdFuse& mf) {
         DevWork<T> w = work<T>(gr.n, slots);
+        w.export_err = out_override != nullptr;
+        double* const o = out_override ? out_override : out.as<double>();
         if (model.is_dp()) {
             const DevDpWork<T> d = dp_work<T>(gr.n, slots, w);
             if constexpr (sizeof(T) == 4)
-                return launch_dp<float>(pf.dev, gr, w, d, d_forces, d_per_atom, out.as<double>(),
-                                        d_rev, st, marker(), mf);
+                return launch_dp<float>(pf.dev, gr, w, d, d_forces, d_per_atom, o, d_rev, st,
+                                        marker(), mf);
             else
-                return launch_dp<double>(pd.dev, gr, w, d, d_forces, d_per_atom, out.as<double>(),
-                                         d_rev, st, marker(), mf);
+                return launch_dp<double>(pd.dev, gr, w, d, d_forces, d_per_atom, o, d_rev, st,
+                                         marker(), mf);
         }
         if constexpr (sizeof(T) == 4)
-            return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, out.as<double>(),
+            return launch_network<float>(wf.dev, gr, w, d_forces, d_per_atom, o,
                                          d_rev, st, marker(), mf);
         else
-            return launch_network<double>(wd.dev, gr, w, d_forces, d_per_atom, out.as<double>(),
+            return launch_network<double>(wd.dev, gr, w, d_forces, d_per_atom, o,
                                           d_rev, st, marker(), mf);
     }
 
@@ -972,8 +979,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
             ck(cudaGraphLaunch(ctx->cgraph.exec, st), "graph launch");
             ck(cudaStreamSynchronize(st), "sync");
             const double* hp = static_cast<const double*>(ctx->pin.p);
-            unsigned bits = 0;
-            std::memcpy(&bits, hp + 12, sizeof(unsigned));
+            const unsigned bits = static_cast<unsigned>(hp[12]);
             ctx->last_launches = ctx->cgraph.launches;
             if (!(bits & (kErrNbrOverflow | kErrCellOverflow))) {
                 hmdp_ctx::raise_bits(bits);
@@ -1010,35 +1016,40 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 double* hp = static_cast<double*>(ctx->pin.p);
                 char* hin = static_cast<char*>(ctx->pin_in.p);
                 cudaGraph_t g = nullptr;
-                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-                cudaMemcpyAsync(ctx->pos.p, hin, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st);
-                cudaMemcpyAsync(ctx->types.p, hin + 3 * n * sizeof(double), n * sizeof(int),
-                                cudaMemcpyHostToDevice, st);
-                const int launches =
-                    enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(), box,
-                                     precision, ctx->forces.as<double>(), ctx->e_atom.as<double>(), st);
-                cudaMemcpyAsync(hp, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st);
-                cudaMemcpyAsync(hp + 12, ctx->err.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
-                cudaMemsetAsync(ctx->err.p, 0, sizeof(unsigned), st);
-                cudaMemcpyAsync(hp + 16, ctx->forces.p, 3 * n * sizeof(double),
-                                cudaMemcpyDeviceToHost, st);
-                cudaMemcpyAsync(hp + 16 + 3 * n, ctx->e_atom.p, n * sizeof(double),
-                                cudaMemcpyDeviceToHost, st);
-                const cudaError_t ce = cudaStreamEndCapture(st, &g);
-                if (ce == cudaSuccess && g) {
-                    cudaGraphExec_t ex = nullptr;
-                    if (cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
-                        ctx->cgraph.exec = ex;
-                        ctx->cgraph.n = n;
-                        ctx->cgraph.prec = precision;
-                        ctx->cgraph.cap = ctx->cap;
-                        ctx->cgraph.ccap = ctx->ccap;
-                        ctx->cgraph.st = st;
-                        ctx->cgraph.gen = g_alloc_gen;
-                        ctx->cgraph.launches = launches;
-                        for (int a = 0; a < 3; ++a) ctx->cgraph.box[a] = box[a];
+                // inputs staged in by one kernel from host-mapped memory; the force
+                // kernel writes forces, per-atom energies, (E, W, W9) and the error
+                // word straight into the host-mapped output block: no copy nodes
+                try {
+                    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+                    launch_stage_in(n, reinterpret_cast<const double*>(hin),
+                                    reinterpret_cast<const int*>(hin + 3 * n * sizeof(double)),
+                                    ctx->pos.as<double>(), ctx->types.as<int>(), st);
+                    ctx->out_override = hp;
+                    const int launches =
+                        1 + enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
+                                             box, precision, hp + 16, hp + 16 + 3 * n, st);
+                    ctx->out_override = nullptr;
+                    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+                    if (ce == cudaSuccess && g) {
+                        cudaGraphExec_t ex = nullptr;
+                        if (cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+                            ctx->cgraph.exec = ex;
+                            ctx->cgraph.n = n;
+                            ctx->cgraph.prec = precision;
+                            ctx->cgraph.cap = ctx->cap;
+                            ctx->cgraph.ccap = ctx->ccap;
+                            ctx->cgraph.st = st;
+                            ctx->cgraph.gen = g_alloc_gen;
+                            ctx->cgraph.launches = launches;
+                            for (int a = 0; a < 3; ++a) ctx->cgraph.box[a] = box[a];
+                        }
+                        cudaGraphDestroy(g);
                     }
-                    cudaGraphDestroy(g);
+                } catch (...) {  // the result above stands; stay on the direct path
+                    ctx->out_override = nullptr;
+                    cudaGraph_t gg = nullptr;
+                    cudaStreamEndCapture(st, &gg);
+                    if (gg) cudaGraphDestroy(gg);
                 }
                 if (!ctx->cgraph.exec) ctx->cgraph.disabled = true;
                 cudaGetLastError();  // a failed capture leaves the direct path in place
