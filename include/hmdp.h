@@ -210,6 +210,28 @@ int hmdp_dd_buffer(hmdp_ctx* ctx, int kind, void** dptr);
 int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* virial);
 
 /* ---------------------------------------------------------------------------
+ * Device-resident domain decomposition on the global index space (hmdp_gdd.cu).
+ * Every rank holds all n positions (replicated; all ranks integrate all atoms
+ * with the same all-reduced forces) and runs the network for the atoms its region
+ * of the dims[0] x dims[1] x dims[2] rank grid owns; plans are built on the device
+ * each step (no host work, fixed sizes: the whole step is capturable in a CUDA
+ * graph together with the caller's collectives).  The caller binds device buffers
+ * (kind 0 positions [n][3] f64, 1 P rows [n][32] T, 2 halo sums [n][32] T,
+ * 3 forces [n][3] f64, 4 out[16] f64 = (E, W, W9), 5 velocities, 6 masses) and
+ * runs, on the context's stream, with a SUM all-reduce of the named buffer at "|":
+ *   10 ; 0 ; for l < depth-1: |1| 1(l) 2(l) ;
+ *   for l = depth-2 .. 0: 3(l) |2| then 4(l-1) or 5 ; 6 |3| |4| ; 7(dt)
+ * (phase 8(dt) = the initial opening kick + drift).  Same results as the
+ * single-domain evaluation up to the summation order of halo partials.
+ * Replaces: the SPEC's halo_inference, per-layer rc halo.
+ * ------------------------------------------------------------------------- */
+int hmdp_gdd_setup(hmdp_ctx* ctx, int n, const int* types, const double* box, const int* dims,
+                   int rank, int precision);
+int hmdp_gdd_bind(hmdp_ctx* ctx, int kind, void* dptr);
+int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt);
+int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts3); /* owned, halo, searched (syncs) */
+
+/* ---------------------------------------------------------------------------
  * Measurement hooks.
  * hmdp_set_stream: run the context's work on an external cudaStream_t (e.g. the
  *   caller's current stream) instead of its own (NULL restores it).

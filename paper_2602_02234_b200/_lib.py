@@ -67,6 +67,10 @@ SIGNATURES = {
                                     _vp, _vp]),
     "hmdp_make_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_int, _c_int, _c_int,
                                        ctypes.c_uint64, _vp, _c_long]),
+    "hmdp_gdd_setup": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int]),
+    "hmdp_gdd_bind": (_c_int, [_vp, _c_int, _vp]),
+    "hmdp_gdd_phase": (_c_int, [_vp, _c_int, _c_int, _c_double]),
+    "hmdp_gdd_counts": (_c_int, [_vp, _vp]),
     "hmdp_make_dp_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_double, _c_int, _c_int,
                                           ctypes.c_uint64, _vp, _c_long]),
     "hmdp_synthetic_system": (_c_int, [_c_int, _c_double, _c_double, ctypes.c_uint64, _c_double,

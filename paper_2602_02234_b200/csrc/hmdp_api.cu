@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -26,7 +27,7 @@ namespace hmdp {
 void launch_cell_bin(int, const double*, const CellGrid&, int*, int*, int*, unsigned*, cudaStream_t);
 void launch_nbr_search(int, const double*, const CellGrid&, const int*, const int*, const int*,
                        double, int, int*, int*, int*, double*, const int*, int*, unsigned*,
-                       cudaStream_t);
+                       cudaStream_t, const int* = nullptr, const int* = nullptr);
 void launch_edge_meta(int, const int*, const int*, int*, const int*, int*, cudaStream_t);
 void launch_csr_rows(int, const int*, int*, int*, cudaStream_t);
 void launch_in_edges(int, int, const int*, int*, int*, int*, int*, cudaStream_t);
@@ -38,7 +39,7 @@ void launch_gather_group(int, const int*, const double*, const int*, double*, in
 double probe_fp32_tflops(int ms);
 template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
-                     double*, cudaStream_t);
+                     double*, cudaStream_t, int* = nullptr);
 cudaError_t net_configure();
 cudaError_t dp_configure();
 template <typename T>
@@ -47,6 +48,23 @@ int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWo
 cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
 void launch_stage_in(int, const double*, const int*, double*, int*, cudaStream_t);
+struct GddGeom {
+    int d[3];
+    double L[3];
+    int rank;
+    double halo;
+};
+void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t);
+void launch_gdd_rev(const DevGraph&, int, int*, cudaStream_t);
+template <typename T>
+void launch_gdd_zero(const DevGraph&, int, const unsigned char*, T*, long long, T*, T*, double*,
+                     cudaStream_t);
+template <typename T>
+void launch_gdd_push_halo(const DevGraph&, int, const T*, T*, const int*, const int*, cudaStream_t);
+template <typename T>
+void launch_gdd_halo_sums(const DevGraph&, int, const T*, T*, const int*, const int*, cudaStream_t);
+void launch_gdd_integrate(int, const double*, double*, double*, const double*, double, int, unsigned*,
+                          cudaStream_t);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
 
@@ -424,6 +442,20 @@ struct hmdp_ctx {
         rf_Ts, rf_stat, rf_dob, rf_aux, rf_tmp, rf_dconv, rf_dg1, rf_envA, rf_dua;
     // domain decomposition (hmdp_dd_*): local graph + halo row buffers
     DBuf dd_patom, dd_sremote, dd_sghost;
+    // global-index device DD (hmdp_gdd_*): roles, lists, counts + caller-bound buffers
+    struct Gdd {
+        int n = 0, prec = -1, n_est = 0;
+        GddGeom geom{};
+        DBuf role, lists, counts;
+        double box[3] = {0, 0, 0};
+        double* pos = nullptr;   // [n][3] replicated positions
+        void* p_atom = nullptr;  // [n][32] T, P rows exchange (sum all-reduce)
+        void* sghost = nullptr;  // [n][32] T, halo partial sums exchange -> s_remote
+        double* forces = nullptr;  // [n][3] partial forces exchange
+        double* out = nullptr;     // [16] (E, W, W9) partials exchange
+        double* vel = nullptr;
+        double* mass = nullptr;
+    } gdd;
     DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
     DevGraph dd_gr{};
     int dd_prec = -1;
@@ -498,7 +530,7 @@ struct hmdp_ctx {
                         &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
-                        &dd_sremote, &dd_sghost, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
+                        &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
                         &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1,
                         &rf_envA, &rf_dua})
@@ -1787,6 +1819,180 @@ int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* viria
         if (energy) *energy = h[0];
         if (virial) *virial = h[1];
         if (virial9) std::memcpy(virial9, h + 2, 9 * sizeof(double));
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Global-index device domain decomposition (hmdp_gdd.cu)
+// ---------------------------------------------------------------------------
+namespace {
+DevGraph gdd_graph(hmdp_ctx* ctx, int list) {  // list 0 owned, 1 halo, 2 searched
+    DevGraph gr = ctx->periodic_graph(ctx->gdd.n, ctx->types.as<int>());
+    gr.n_active = ctx->gdd.n_est;  // launch sizing only; the loop bound is *alist_n
+    gr.alist = ctx->gdd.lists.as<int>() + static_cast<size_t>(list) * ctx->gdd.n;
+    gr.alist_n = ctx->gdd.counts.as<int>() + list;
+    return gr;
+}
+}  // namespace
+
+int hmdp_gdd_setup(hmdp_ctx* ctx, int n, const int* types, const double* box, const int* dims,
+                   int rank, int precision) {
+    return guarded([&] {
+        need_model(ctx);
+        if (ctx->model.is_dp())
+            fail(HMDP_INVALID_ARGUMENT,
+                 "domain decomposition is implemented for the embed_fit / message_passing families");
+        if (n < 1 || !types || !box || !dims) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        const int world = dims[0] * dims[1] * dims[2];
+        if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || rank < 0 || rank >= world)
+            fail(HMDP_INVALID_ARGUMENT, "bad rank grid");
+        check_types(n, types, ctx->model.n_types);
+        set_device(ctx);
+        auto& g = ctx->gdd;
+        g.n = n;
+        g.prec = precision;
+        g.n_est = std::min(n, std::max(1, static_cast<int>(1.3 * n / world) + 32));
+        for (int a = 0; a < 3; ++a) {
+            g.geom.d[a] = dims[a];
+            g.geom.L[a] = box[a];
+            g.box[a] = box[a];
+        }
+        g.geom.rank = rank;
+        g.geom.halo = ctx->model.rc;
+        ctx->ensure_atoms(n);
+        ctx->ensure_edges(static_cast<long long>(n) * ctx->cap);
+        ctx->grid(box, ctx->model.rc, n);  // geometry checks + cell buffers
+        g.role.ensure(n);
+        g.lists.ensure(3 * static_cast<size_t>(n) * sizeof(int));
+        g.counts.ensure(4 * sizeof(int));
+        cudaStream_t st = ctx->st();
+        ck(cudaMemcpyAsync(ctx->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        const long long slots = static_cast<long long>(n) * ctx->cap;
+        if (precision == HMDP_FP64)
+            ctx->work<double>(n, slots);
+        else
+            ctx->work<float>(n, slots);
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int hmdp_gdd_bind(hmdp_ctx* ctx, int kind, void* dptr) {
+    if (!ctx) return HMDP_INVALID_ARGUMENT;
+    auto& g = ctx->gdd;
+    switch (kind) {
+        case 0: g.pos = static_cast<double*>(dptr); break;
+        case 1: g.p_atom = dptr; break;
+        case 2: g.sghost = dptr; break;
+        case 3: g.forces = static_cast<double*>(dptr); break;
+        case 4: g.out = static_cast<double*>(dptr); break;
+        case 5: g.vel = static_cast<double*>(dptr); break;
+        case 6: g.mass = static_cast<double*>(dptr); break;
+        default: return HMDP_INVALID_ARGUMENT;
+    }
+    return HMDP_OK;
+}
+
+int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
+    return guarded([&] {
+        need_model(ctx);
+        auto& g = ctx->gdd;
+        if (g.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
+        if (!g.pos || !g.p_atom || !g.sghost || !g.forces || !g.out)
+            fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_bind: buffers 0-4 must be bound");
+        const int M = ctx->n_msg(), n = g.n;
+        if ((phase >= 1 && phase <= 4) && (layer < 0 || layer >= std::max(M, 1)))
+            fail(HMDP_INVALID_ARGUMENT, "layer out of range");
+        set_device(ctx);
+        cudaStream_t st = ctx->st();
+        const long long slots = static_cast<long long>(n) * ctx->cap;
+        const size_t tb = g.prec == HMDP_FP64 ? sizeof(double) : sizeof(float);
+        const size_t rows = static_cast<size_t>(n) * kH * tb;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            DevWork<T> w = ctx->work<T>(n, slots);
+            w.p_atom = static_cast<T*>(g.p_atom);
+            w.s_remote = static_cast<T*>(g.sghost);
+            const DevModel<T>& md = [&]() -> const DevModel<T>& {
+                if constexpr (sizeof(T) == 8) return ctx->wd.dev;
+                else return ctx->wf.dev;
+            }();
+            const DevGraph own = gdd_graph(ctx, 0);
+            switch (phase) {
+                case 10: {  // roles, neighbour list of owned + halo atoms, mirrors, zeroing
+                    ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
+                    launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), g.lists.as<int>(),
+                                     g.counts.as<int>(), st);
+                    const CellGrid cg = ctx->grid(g.box, ctx->model.rc, n);
+                    ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
+                       "memset cells");
+                    launch_cell_bin(n, g.pos, cg, ctx->cell_count.as<int>(), ctx->members.as<int>(),
+                                    ctx->cell_of.as<int>(), ctx->err.as<unsigned>(), st);
+                    ck(cudaMemsetAsync(ctx->nnei.p, 0, n * sizeof(int), st), "memset nnei");
+                    const DevGraph srch = gdd_graph(ctx, 2);
+                    launch_nbr_search(std::min(n, 2 * g.n_est), g.pos, cg, ctx->cell_count.as<int>(),
+                                      ctx->members.as<int>(), ctx->cell_of.as<int>(),
+                                      ctx->model.rc * ctx->model.rc, ctx->cap, ctx->nnei.as<int>(),
+                                      ctx->row_start.as<int>(), ctx->nbr.as<int>(),
+                                      ctx->dr.as<double>(), ctx->types.as<int>(), ctx->ety.as<int>(),
+                                      ctx->err.as<unsigned>(), st, srch.alist, srch.alist_n);
+                    ctx->cells_owner = nullptr;
+                    launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
+                    launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
+                                       M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
+                    break;
+                }
+                case 0:
+                    ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
+                    launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st);
+                    break;
+                case 1:
+                    launch_gdd_push_halo<T>(own, g.n_est, static_cast<const T*>(g.p_atom),
+                                            w.pe + (layer & 1) * slots * kH,
+                                            g.lists.as<int>() + n, g.counts.as<int>() + 1, st);
+                    break;
+                case 2:
+                    if (layer < M - 1) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
+                    launch_dd_phase<T>(md, own, w, 2, layer, nullptr, g.forces, g.out, st);
+                    break;
+                case 3:
+                    ck(cudaMemsetAsync(g.sghost, 0, rows, st), "memset");
+                    launch_gdd_halo_sums<T>(own, g.n_est, w.d + (layer & 1) * slots * kH,
+                                            static_cast<T*>(g.sghost), g.lists.as<int>() + n,
+                                            g.counts.as<int>() + 1, st);
+                    break;
+                case 4:
+                case 5:
+                    launch_dd_phase<T>(md, own, w, phase, layer, nullptr, g.forces, g.out, st);
+                    break;
+                case 6:  // forces of every row (halo rows: partials), (E, W, W9) partials
+                    launch_dd_phase<T>(md, own, w, 6, 0, nullptr, g.forces, g.out, st);
+                    break;
+                case 7:  // velocity Verlet on all atoms from the all-reduced forces
+                case 8:  // the initial opening kick + drift only
+                    if (!g.vel || !g.mass) fail(HMDP_INVALID_ARGUMENT, "bind velocities and masses");
+                    launch_gdd_integrate(n, g.forces, g.pos, g.vel, g.mass, dt, phase == 8 ? 1 : 0,
+                                         ctx->err.as<unsigned>(), st);
+                    break;
+                default:
+                    fail(HMDP_INVALID_ARGUMENT, "unknown phase");
+            }
+        };
+        if (g.prec == HMDP_FP64)
+            run(double{});
+        else
+            run(float{});
+        ck(cudaGetLastError(), "kernel launch");
+    });
+}
+
+int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts) {
+    return guarded([&] {
+        if (!ctx || !counts) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(ctx);
+        ck(cudaMemcpyAsync(counts, ctx->gdd.counts.p, 3 * sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->st()),
+           "D2H");
+        ck(cudaStreamSynchronize(ctx->st()), "sync");
     });
 }
 

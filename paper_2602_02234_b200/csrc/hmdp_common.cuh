@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "hmdp_device.cuh"
@@ -183,6 +184,44 @@ __device__ __forceinline__ void bin_atom(int i, const double* x3, const CellGrid
 }
 
 
+// rev(e) for the lanes' edges (lane l < m holds edge (i -> j_l)): the slot of i
+// in nbr(j_l), found with 8 neighbour-list rows in flight per lane and a ballot;
+// lists longer than 32 fall back to a binary search (lists are sorted).
+__device__ __forceinline__ int find_rev(int i, int j, int m, const DevGraph& gr) {
+    const int lane = threadIdx.x & 31;
+    const int rs_l = lane < m ? gr.row_start[j] : 0;
+    const int nn_l = lane < m ? gr.nnei[j] : 0;
+    int found = -1;
+    for (int q0 = 0; q0 < m; q0 += 8) {
+        int val[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int rsq = __shfl_sync(FULL_MASK, rs_l, (q0 + u) & 31);
+            const int nnq = __shfl_sync(FULL_MASK, nn_l, (q0 + u) & 31);
+            val[u] = (q0 + u < m && lane < nnq) ? gr.nbr[rsq + lane] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const unsigned bal = __ballot_sync(FULL_MASK, val[u] == i);
+            if (lane == q0 + u && bal) found = rs_l + __ffs(bal) - 1;
+        }
+    }
+    if (lane < m && found < 0 && nn_l > 32) {
+        int lo = rs_l, hi = rs_l + nn_l - 1;
+        while (lo <= hi) {
+            const int mid = (lo + hi) >> 1;
+            const int vv = gr.nbr[mid];
+            if (vv == i) {
+                found = mid;
+                break;
+            }
+            if (vv < i) lo = mid + 1;
+            else hi = mid - 1;
+        }
+    }
+    return found;
+}
+
 // Programmatic dependent launch (PDL): a kernel lets its successor start
 // launching right away (the successor's CTAs take SMs as ours retire and stage
 // their weights), and waits for its predecessor's results before touching them.
@@ -205,7 +244,8 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool no_pdl = std::getenv("HMDP_NO_PDL") != nullptr;  // A/B experiments
+    cfg.numAttrs = no_pdl ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
 }
 

@@ -83,6 +83,10 @@ struct DevGraph {
     const int* inv_pos;  // [edge slot] -> in-position (mirror slot)
     const int* types;
     const unsigned char* is_ghost;  // nullable
+    // nullable: run the network only for the atoms alist[0 .. *alist_n) (global-index
+    // domain decomposition, hmdp_gdd_*: this rank's owned atoms); else [0, n_active)
+    const int* alist;
+    const int* alist_n;
 };
 
 // Per-evaluation device workspace (element type T for the network tensors).

@@ -100,44 +100,6 @@ __device__ __forceinline__ void dp_gvec(const Env<T>& v, const double* d, T dEds
     g[2] = radial * v.uz + q * dh2;
 }
 
-// rev(e) for the lanes' edges (lane l < m holds edge (i -> j_l)): the slot of i
-// in nbr(j_l), found with 8 neighbour-list rows in flight per lane and a ballot;
-// lists longer than 32 fall back to a binary search (lists are sorted).
-__device__ __forceinline__ int find_rev(int i, int j, int m, const DevGraph& gr) {
-    const int lane = threadIdx.x & 31;
-    const int rs_l = lane < m ? gr.row_start[j] : 0;
-    const int nn_l = lane < m ? gr.nnei[j] : 0;
-    int found = -1;
-    for (int q0 = 0; q0 < m; q0 += 8) {
-        int val[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int rsq = __shfl_sync(FULL_MASK, rs_l, (q0 + u) & 31);
-            const int nnq = __shfl_sync(FULL_MASK, nn_l, (q0 + u) & 31);
-            val[u] = (q0 + u < m && lane < nnq) ? gr.nbr[rsq + lane] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const unsigned bal = __ballot_sync(FULL_MASK, val[u] == i);
-            if (lane == q0 + u && bal) found = rs_l + __ffs(bal) - 1;
-        }
-    }
-    if (lane < m && found < 0 && nn_l > 32) {
-        int lo = rs_l, hi = rs_l + nn_l - 1;
-        while (lo <= hi) {
-            const int mid = (lo + hi) >> 1;
-            const int vv = gr.nbr[mid];
-            if (vv == i) {
-                found = mid;
-                break;
-            }
-            if (vv < i) lo = mid + 1;
-            else hi = mid - 1;
-        }
-    }
-    return found;
-}
-
 template <typename T>
 __device__ __forceinline__ T shfl(T v, int src) {
     return __shfl_sync(FULL_MASK, v, src);

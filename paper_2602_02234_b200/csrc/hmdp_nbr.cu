@@ -31,7 +31,7 @@ __global__ __launch_bounds__(kSearchCTA) void k_nbr_search(
     const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
     int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
     double* __restrict__ dr, const int* __restrict__ types, int* __restrict__ ety,
-    unsigned* err) {
+    unsigned* err, const int* __restrict__ alist, const int* __restrict__ alist_n) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NbrSmem* sm = reinterpret_cast<NbrSmem*>(smem_raw);
     pdl_launch_dependents();
@@ -39,9 +39,12 @@ __global__ __launch_bounds__(kSearchCTA) void k_nbr_search(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tpc = (blockDim.x >> 5) / G, team = warp / G, w = warp % G;
     const int nt = gridDim.x * tpc;
-    for (int i = blockIdx.x * tpc + team; i < n; i += nt)
-        nbr_search_team<G>(i, pos, cg, cell_count, members, cell_of, range2, cap, nnei, row_start,
-                           nbr, dr, types, ety, err, sm + team * G, w, lane, 1 + team);
+    // alist (global-index domain decomposition): only this rank's owned + halo atoms
+    const int n_run = alist ? *alist_n : n;
+    for (int k = blockIdx.x * tpc + team; k < n_run; k += nt)
+        nbr_search_team<G>(alist ? alist[k] : k, pos, cg, cell_count, members, cell_of, range2,
+                           cap, nnei, row_start, nbr, dr, types, ety, err, sm + team * G, w, lane,
+                           1 + team);
 }
 
 // CSR offsets -> (row_start, nnei)
@@ -199,7 +202,7 @@ void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_cou
 void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* cell_count,
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
-                       unsigned* err, cudaStream_t st) {
+                       unsigned* err, cudaStream_t st, const int* alist, const int* alist_n) {
     const int sms = num_sms();
     int G = (4 * n <= 16 * sms) ? 4 : (2 * n <= 16 * sms ? 2 : 1);
     if (team_override()) G = team_override();
@@ -213,7 +216,7 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
     auto args = [&](auto kernel) {
         launch_pdl(kernel, dim3(grid > 0 ? grid : 1), dim3(threads), smem, st, n, pos, cg,
                    cell_count, members, cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety,
-                   err);
+                   err, alist, alist_n);
     };
     if (G == 4) args(k_nbr_search<4>);
     else if (G == 2) args(k_nbr_search<2>);

@@ -440,7 +440,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
          c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
     T(*sb)[12] = sm.ed;
-    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int i = gr.alist ? gr.alist[k_at] : k_at;
         const int start = gr.row_start[i] + tm.w, cnt = gr.nnei[i];
         const int mloc = tm.local(cnt);
         T desc = T(0);  // lane q < nd accumulates descriptor component q
@@ -800,7 +802,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     const long long S = ws.slots;
     const T* Pin = ws.pe + (l & 1) * S * kH;
     T* Z = ws.z + l * S * kH;
-    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int i = gr.alist ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
         // first batch: P rows (lane = channel) and edge scalars (lane = local edge)
@@ -966,7 +970,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
     pdl_wait();
     const T* Dn = ws.d + ((l + 1) & 1) * ws.slots * kH;
     const T* Z = ws.z + l * ws.slots * kH;
-    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int i = gr.alist ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         // one round trip: own adjoint, update activations, the pushed adjoint rows
         // and the backward edge loop's first batch
@@ -1018,7 +1024,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
     pdl_wait();
-    for (int i = tm.first; i < gr.n_active; i += tm.stride) {
+    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int i = gr.alist ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + lane];
@@ -1443,10 +1451,10 @@ struct Net {
         return 2 + M + (M - 1);
     }
     static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                         const DevWork<T>& ws, int phase, int l, cudaStream_t st) {
+                         const DevWork<T>& ws, int phase, int l, cudaStream_t st, int* rev) {
         const MdFuse none{};
         switch (phase) {
-            case 0: embed(sh, md, gr, ws, nullptr, none, st); break;
+            case 0: embed(sh, md, gr, ws, rev, none, st); break;
             case 2: msg_fwd(sh, md, gr, ws, l, st); break;
             case 4: msg_bwd(sh, md, gr, ws, l, st); break;
             case 5: embed_bwd(sh, md, gr, ws, st); break;
@@ -1520,7 +1528,7 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 // 5 embedding backward, 6 forces.
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
-                     int l, T* s_ghost, double* forces, double* out, cudaStream_t st) {
+                     int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
     const NetShape sh = net_shape(gr.n_active);
     const int ng = gr.n - gr.n_active;
     switch (phase) {
@@ -1540,19 +1548,19 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
             break;
         default:
             if (sh.G == 4)
-                Net<T, 4>::dd_phase(sh, md, gr, ws, phase, l, st);
+                Net<T, 4>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
             else if (sh.G == 2)
-                Net<T, 2>::dd_phase(sh, md, gr, ws, phase, l, st);
+                Net<T, 2>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
             else
-                Net<T, 1>::dd_phase(sh, md, gr, ws, phase, l, st);
+                Net<T, 1>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
     }
 }
 template void launch_dd_phase<float>(const DevModel<float>&, const DevGraph&,
                                      const DevWork<float>&, int, int, float*, double*, double*,
-                                     cudaStream_t);
+                                     cudaStream_t, int*);
 template void launch_dd_phase<double>(const DevModel<double>&, const DevGraph&,
                                       const DevWork<double>&, int, int, double*, double*, double*,
-                                      cudaStream_t);
+                                      cudaStream_t, int*);
 template int launch_network<float>(const DevModel<float>&, const DevGraph&, const DevWork<float>&,
                                    double*, double*, double*, int*, cudaStream_t, const Marker&,
                                    const MdFuse&);

@@ -371,3 +371,131 @@ def evaluate_local(engines, plans, depth: int):
         fr = fr.cpu().numpy() if hasattr(fr, "cpu") else np.asarray(fr)
         F[r] = fr[: plans[r].n_own]
     return E, F, W, W9.reshape(3, 3)
+
+
+# ---------------------------------------------------------------------------
+# Device-resident domain decomposition on the global index space (hmdp_gdd_*):
+# plans built on the device every step, exchanges as SUM all-reduces of fixed-size
+# global-index buffers -> one CUDA graph per step (collectives included).
+# ---------------------------------------------------------------------------
+class DeviceDD:
+    """One rank's device-resident DD engine.  Every rank holds all n positions and
+    velocities (replicated: all ranks integrate all atoms with the same all-reduced
+    forces) and evaluates the network for the atoms its region owns.
+
+    ``program(kind)`` is a generator over the phase program; it yields every
+    tensor that must be SUM all-reduced across ranks before it continues
+    (``run_dist`` does that with torch.distributed / NCCL, ``run_local`` for
+    ranks simulated in one process)."""
+
+    def __init__(self, ctx, n, types, box, dims, rank, precision, masses=None):
+        import torch
+
+        from .nn import Precision
+
+        self.ctx, self.n, self.rank = ctx, int(n), int(rank)
+        self.dims = tuple(int(d) for d in dims)
+        self.depth = ctx.model.depth()
+        self.prec = precision
+        dev = torch.device("cuda", ctx.device)
+        T = torch.float64 if precision == Precision.fp64 else torch.float32
+        self.pos = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.vel = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.mass = torch.ones(n, dtype=torch.float64, device=dev)
+        self.p = torch.zeros((n, 32), dtype=T, device=dev)
+        self.sg = torch.zeros((n, 32), dtype=T, device=dev)
+        self.f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.out = torch.zeros(16, dtype=torch.float64, device=dev)
+        t = np.ascontiguousarray(types, dtype=np.int32)
+        b = np.ascontiguousarray(box, dtype=np.float64)
+        d = np.ascontiguousarray(self.dims, dtype=np.int32)
+        L = lib()
+        # the context runs on torch's current stream, so the phases and the all-reduces
+        # (torch ops / NCCL) are stream-ordered; torch's default stream is the legacy
+        # NULL stream, passed as cudaStreamLegacy (NULL would select the context's own)
+        sid = torch.cuda.current_stream(dev).cuda_stream
+        check(L.hmdp_set_stream(ctx.handle, ctypes.c_void_p(sid if sid else 1)))
+        check(L.hmdp_gdd_setup(ctx.handle, self.n, ptr(t), ptr(b), ptr(d), self.rank,
+                               int(precision)))
+        for kind, ten in enumerate([self.pos, self.p, self.sg, self.f, self.out, self.vel,
+                                    self.mass]):
+            check(L.hmdp_gdd_bind(ctx.handle, kind, ctypes.c_void_p(ten.data_ptr())))
+        if masses is not None:
+            self.mass.copy_(torch.as_tensor(np.asarray(masses, dtype=np.float64)))
+
+    def load(self, positions, velocities=None):
+        import torch
+
+        self.pos.copy_(torch.as_tensor(np.asarray(positions, dtype=np.float64).reshape(-1, 3)))
+        if velocities is not None:
+            self.vel.copy_(torch.as_tensor(np.asarray(velocities, dtype=np.float64).reshape(-1, 3)))
+
+    def _ph(self, phase, layer=0, dt=0.0):
+        check(lib().hmdp_gdd_phase(self.ctx.handle, phase, layer, float(dt)))
+
+    def program(self, kind="eval", dt=0.001):
+        """kind: 'eval' (one force evaluation), 'md' (evaluation + velocity Verlet
+        closing kick, next opening kick, drift), 'open' (the initial opening kick +
+        drift from the current forces)."""
+        if kind == "open":
+            self._ph(8, 0, dt)
+            return
+        M = self.depth - 1
+        self._ph(10)
+        self._ph(0)
+        for l in range(M):
+            yield self.p
+            self._ph(1, l)
+            self._ph(2, l)
+        for l in range(M - 1, -1, -1):
+            self._ph(3, l)
+            yield self.sg
+            if l > 0:
+                self._ph(4, l - 1)
+            else:
+                self._ph(5)
+        self._ph(6)
+        yield self.f
+        yield self.out
+        if kind == "md":
+            self._ph(7, 0, dt)
+
+    def counts(self):
+        c = np.zeros(3, dtype=np.int32)
+        check(lib().hmdp_gdd_counts(self.ctx.handle, ptr(c)))
+        return tuple(int(v) for v in c)
+
+    def result(self):
+        o = self.out.cpu().numpy()
+        return float(o[0]), self.f.cpu().numpy(), float(o[1]), o[2:11].reshape(3, 3)
+
+
+def run_dist(engine: DeviceDD, kind="eval", dt=0.001, group=None):
+    """One rank's program with NCCL SUM all-reduces (torch.distributed) on the
+    current stream — capturable in a CUDA graph."""
+    import torch.distributed as td
+
+    for ten in engine.program(kind, dt):
+        td.all_reduce(ten, group=group)
+
+
+def run_local(engines, kind="eval", dt=0.001):
+    """Ranks simulated in one process: lockstep programs, the all-reduce is a sum of
+    the ranks' buffers in rank order written back to every rank."""
+    progs = [e.program(kind, dt) for e in engines]
+    while True:
+        bufs = []
+        for p in progs:  # every rank advances to its next collective (or its end)
+            try:
+                bufs.append(next(p))
+            except StopIteration:
+                pass
+        if not bufs:
+            return
+        if len(bufs) != len(progs):
+            raise RuntimeError("ranks disagree on the number of collectives")
+        tot = bufs[0].clone()
+        for b in bufs[1:]:
+            tot += b
+        for b in bufs:
+            b.copy_(tot)
