@@ -66,10 +66,11 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--mode", choices=["dd", "replicas"], default="replicas",
-                    help="N>1: independent replica boxes per GPU (default; weak scaling, no "
-                         "data-path collective) or spatial domain decomposition of one "
-                         "replicated box (host-orchestrated, DESIGN.md §6)")
+    ap.add_argument("--mode", choices=["dd", "dd-host", "replicas"], default="dd",
+                    help="N>1: device-resident spatial domain decomposition of the box "
+                         "replicated over the rank grid (default; one CUDA graph per MD step "
+                         "with the NCCL halo all-reduces inside), the host-orchestrated DD "
+                         "(dd-host), or independent replica boxes (replicas)")
     return ap.parse_args()
 
 
@@ -509,6 +510,117 @@ def run_ours(args, rank, world, local_rank, dist):
     print(json.dumps(line), flush=True)
 
 
+def run_gdd(args, rank, world, local_rank, dist):
+    """N > 1, --mode dd (default DD path): device-resident domain decomposition
+    (hmdp_gdd_*).  Global box = the per-rank box replicated over the rank grid (one
+    box per GPU, weak scaling); every step = roles + neighbour list of this rank's
+    owned + halo atoms, the network over its owned atoms, and the per-layer halo
+    exchanges as fixed-size SUM all-reduces (NCCL) — the whole MD step (velocity
+    Verlet on the replicated positions included) captured in ONE CUDA graph per
+    rank, collectives inside.  value = world * steps / max-over-ranks time."""
+    import numpy as np
+    import torch
+
+    import paper_2602_02234_b200 as P
+    from paper_2602_02234_b200 import dd
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    prec = P.Precision[args.precision]
+    model = make_bench_model(P, args.model)
+    if model.is_dp():
+        raise SystemExit("--mode dd: the DeePMD-style families run replicas only (DESIGN.md §11)")
+    base = P.generate_synthetic_system(SYSTEMS[args.system])
+    dims = dd.rank_grid(world)
+    s = P.replicate(base, dims)
+    n = s.n_atoms
+    eng = dd.DeviceDD(P.Context(model, device=local_rank, max_atoms=n), n, s.types, s.box, dims,
+                      rank, prec, masses=s.masses)
+    eng.load(s.positions, s.velocities)
+    use_graph = dist.get_backend() == "nccl" and not os.environ.get("BENCH_DD_NOGRAPH")
+    dd.run_dist(eng, "eval")
+    torch.cuda.synchronize(dev)
+    E = float(eng.out[0])  # energy of the initial configuration (extensivity check)
+    dd.run_dist(eng, "open", 0.001)
+    for _ in range(max(args.warmup, 3)):
+        dd.run_dist(eng, "md", 0.001)
+    torch.cuda.synchronize(dev)
+    g = None
+    if use_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                dd.run_dist(eng, "md", 0.001)
+            g.replay()
+        except Exception as exc:  # symmetric on every rank: all fall back to direct launches
+            print(f"rank {rank}: graph capture failed ({exc}); direct launches", file=sys.stderr)
+            g = None
+            torch.cuda.synchronize(dev)
+    # halo share: the same step's collectives timed alone (events, non-graph)
+    torch.cuda.synchronize(dev)
+    K = args.steps
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        if g is not None:
+            g.replay()
+        else:
+            dd.run_dist(eng, "md", 0.001)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t_ms = e0.elapsed_time(e1)
+    ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bufs = [eng.p, eng.p, eng.sg, eng.sg, eng.f, eng.out][: 2 * (model.depth() - 1) + 2]
+    ca.record(stream)
+    for _ in range(20):
+        for b in bufs:
+            dist.all_reduce(b)
+    cb.record(stream)
+    torch.cuda.synchronize(dev)
+    halo_ms = ca.elapsed_time(cb) / 20
+    tt = torch.tensor([t_ms, halo_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms, halo_ms = float(tt[0]), float(tt[1])
+    value = world * K / (t_ms * 1e-3)
+    counts = eng.counts()
+    from paper_2602_02234_b200._lib import check, lib
+
+    check(lib().hmdp_check(eng.ctx.handle))
+    if rank != 0:
+        return
+    e_single = P.Context(model, device=local_rank).compute(base.positions, base.types, base.box,
+                                                           P.Precision.fp64).energy
+    line = {
+        "metric": METRIC, "value": value, "unit": f"steps/s ({args.system}-box equivalents)",
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
+        "config": {"workload": f"{args.model.upper()} domain-decomposed MD step, {args.system} "
+                               f"box replicated {dims} (one box per GPU)",
+                   "model": args.model, "system": args.system, "atoms_total": n,
+                   "rank_grid": list(dims), "precision": args.precision,
+                   "parallelism": f"device-resident spatial DD x{world}: owner/halo lists on the "
+                                  f"device, per-layer rc-halo exchange as SUM all-reduces (NCCL), "
+                                  f"replicated velocity Verlet",
+                   "graph": "one CUDA graph per MD step incl. NCCL" if g is not None else "none",
+                   "rank0_owned": counts[0], "rank0_halo": counts[1]},
+        "ns_per_day_per_box": ns_per_day(value / world),
+        "halo": {"ms_per_step": halo_ms, "rounds_per_step": len(bufs),
+                 "share": halo_ms / (t_ms / K)},
+        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * world,
+                        "rel_diff": abs(E - e_single * world) / abs(e_single * world)},
+        "gpu_launches": None,
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0, "note": "device-resident MD loop"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_dd(args, rank, world, local_rank, dist):
     """N > 1: domain-decomposed force evaluation (weak scaling).  The global box
     is the per-rank box replicated over the rank grid (1x1x1, 2x1x1, 2x2x1,
@@ -627,6 +739,8 @@ def main():
             local_rank = local_rank % max(1, torch.cuda.device_count())
     try:
         if world > 1 and args.mode == "dd":
+            run_gdd(args, rank, world, local_rank, dist)
+        elif world > 1 and args.mode == "dd-host":
             run_dd(args, rank, world, local_rank, dist)
         else:
             run_ours(args, rank, world, local_rank, dist)
