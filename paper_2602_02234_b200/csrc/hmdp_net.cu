@@ -403,7 +403,7 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // backward chain.  rev (periodic path): computes the reverse slot of every
 // edge, which is the in-edge array of the symmetric graph (in_edge == rev).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool FUSE_FIT>
+template <typename T, int G, bool FUSE_FIT, bool LIST = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
@@ -440,9 +440,10 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
          c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
     T(*sb)[12] = sm.ed;
-    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
+    const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
-        const int i = gr.alist ? gr.alist[k_at] : k_at;
+        const int i = LIST ? gr.alist[k_at] : k_at;
         const int start = gr.row_start[i] + tm.w, cnt = gr.nnei[i];
         const int mloc = tm.local(cnt);
         T desc = T(0);  // lane q < nd accumulates descriptor component q
@@ -758,7 +759,7 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
 // Message layer l forward; LAST fuses the fitting net and the top layer's
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool LAST>
+template <typename T, int G, bool LAST, bool LIST = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -802,9 +803,10 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     const long long S = ws.slots;
     const T* Pin = ws.pe + (l & 1) * S * kH;
     T* Z = ws.z + l * S * kH;
-    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
+    const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
-        const int i = gr.alist ? gr.alist[k_at] : k_at;
+        const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
         // first batch: P rows (lane = channel) and edge scalars (lane = local edge)
@@ -943,7 +945,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
-template <typename T, int G>
+template <typename T, int G, bool LIST = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -970,9 +972,10 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
     pdl_wait();
     const T* Dn = ws.d + ((l + 1) & 1) * ws.slots * kH;
     const T* Z = ws.z + l * ws.slots * kH;
-    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
+    const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
-        const int i = gr.alist ? gr.alist[k_at] : k_at;
+        const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         // one round trip: own adjoint, update activations, the pushed adjoint rows
         // and the backward edge loop's first batch
@@ -1007,7 +1010,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
-template <typename T, int G>
+template <typename T, int G, bool LIST = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1024,9 +1027,10 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
     pdl_wait();
-    const int n_run = gr.alist ? *gr.alist_n : gr.n_active;
+    // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
+    const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
-        const int i = gr.alist ? gr.alist[k_at] : k_at;
+        const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(i) * kH + lane];
@@ -1395,41 +1399,41 @@ int force_grid(int n) {
 constexpr int kMaxSmem = 200 * 1024;
 
 // The network phases for one element type and team size.
-template <typename T, int G>
+template <typename T, int G, bool LIST = false>
 struct Net {
     static cudaError_t configure() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
-        for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_embed<T, G, false>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_fwd<T, G, true>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_fwd<T, G, false>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_bwd<T, G>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_embed_bwd<T, G>, a, kMaxSmem)})
+        for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_embed<T, G, false, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_bwd<T, G, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_embed_bwd<T, G, LIST>, a, kMaxSmem)})
             if (r != cudaSuccess) e = r;
         return e;
     }
     static void embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                       const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
         if (md.n_msg == 0)
-            launch_net<T>(k_embed<T, G, true>, Phase::EmbedFit, sh, st, md, gr, ws, rev, mf);
+            launch_net<T>(k_embed<T, G, true, LIST>, Phase::EmbedFit, sh, st, md, gr, ws, rev, mf);
         else
-            launch_net<T>(k_embed<T, G, false>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
+            launch_net<T>(k_embed<T, G, false, LIST>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
     }
     static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                         const DevWork<T>& ws, int l, cudaStream_t st) {
         if (l == md.n_msg - 1)
-            launch_net<T>(k_msg_fwd<T, G, true>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_fwd<T, G, true, LIST>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
         else
-            launch_net<T>(k_msg_fwd<T, G, false>, Phase::MsgFwd, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_fwd<T, G, false, LIST>, Phase::MsgFwd, sh, st, md, gr, ws, l);
     }
     static void msg_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                         const DevWork<T>& ws, int l, cudaStream_t st) {
-        launch_net<T>(k_msg_bwd<T, G>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+        launch_net<T>(k_msg_bwd<T, G, LIST>, Phase::MsgBwd, sh, st, md, gr, ws, l);
     }
     static void embed_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                           const DevWork<T>& ws, cudaStream_t st) {
-        launch_net<T>(k_embed_bwd<T, G>, Phase::EmbedBwd, sh, st, md, gr, ws);
+        launch_net<T>(k_embed_bwd<T, G, LIST>, Phase::EmbedBwd, sh, st, md, gr, ws);
     }
     static int network(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                        const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
@@ -1468,7 +1472,10 @@ cudaError_t net_configure() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {Net<float, 1>::configure(), Net<float, 2>::configure(),
                           Net<float, 4>::configure(), Net<double, 1>::configure(),
-                          Net<double, 2>::configure(), Net<double, 4>::configure()})
+                          Net<double, 2>::configure(), Net<double, 4>::configure(),
+                          Net<float, 1, true>::configure(), Net<float, 2, true>::configure(),
+                          Net<float, 4, true>::configure(), Net<double, 1, true>::configure(),
+                          Net<double, 2, true>::configure(), Net<double, 4, true>::configure()})
         if (r != cudaSuccess) e = r;
     return e;
 }
@@ -1547,7 +1554,14 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
                        forces, static_cast<double*>(nullptr), out, MdFuse{});
             break;
         default:
-            if (sh.G == 4)
+            if (gr.alist) {  // global-index DD: the owned-atom list variants
+                if (sh.G == 4)
+                    Net<T, 4, true>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
+                else if (sh.G == 2)
+                    Net<T, 2, true>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
+                else
+                    Net<T, 1, true>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
+            } else if (sh.G == 4)
                 Net<T, 4>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
             else if (sh.G == 2)
                 Net<T, 2>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
