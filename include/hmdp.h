@@ -232,6 +232,30 @@ int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt);
 int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts3); /* owned, halo, searched (syncs) */
 
 /* ---------------------------------------------------------------------------
+ * Classical force field on the device: the reference's
+ * compute_classical (forcefield.cpp:265-279) — harmonic bonds, angles, periodic
+ * dihedrals, potential-shifted LJ (Lorentz-Berthelot), Coulomb cutoff_shifted (0)
+ * or reaction_field (1) — over the device cell-list pairs within max(rc_lj,
+ * rc_coulomb) minus the exclusions (excl_offset[n+1] / excl: each atom's sorted
+ * list).  bonds[2 nb] + bond_params[2 nb] = (k_b, r0); angles[3 na] (j = vertex) +
+ * angle_params[2 na] = (k_a, theta0); dihedrals[4 nd] + dihedral_params[3 nd] =
+ * (k_d, phase, multiplicity).  energies[3] = (bonded, lj, coulomb); forces[3n]
+ * are SET (as compute_classical zeroes first); virial = sum r.F over all terms;
+ * collinear = angles evaluated with the clamped derivative.
+ * precision: HMDP_FP32 / HMDP_FP64 arithmetic as the reference's Precision.
+ * ------------------------------------------------------------------------- */
+typedef struct hmdp_ff hmdp_ff;
+int hmdp_ff_create(int device, int n, const int* types, const double* charges, int n_types,
+                   const double* sigma, const double* epsilon, int coulomb_scheme,
+                   double rc_coulomb, double eps_rf, double rc_lj, const int* excl_offset,
+                   const int* excl, int n_bonds, const int* bonds, const double* bond_params,
+                   int n_angles, const int* angles, const double* angle_params, int n_dihedrals,
+                   const int* dihedrals, const double* dihedral_params, hmdp_ff** out);
+int hmdp_ff_compute(hmdp_ff* ff, const double* xyz, const double* box, int precision,
+                    double* energies, double* forces, double* virial, int* collinear);
+int hmdp_ff_destroy(hmdp_ff* ff);
+
+/* ---------------------------------------------------------------------------
  * Measurement hooks.
  * hmdp_set_stream: run the context's work on an external cudaStream_t (e.g. the
  *   caller's current stream) instead of its own (NULL restores it).

@@ -90,6 +90,11 @@ def ref():
         L.ref_evaluate_periodic.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp,
                                             _vp, _vp, _vp]
         L.ref_descriptors.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.ref_synthetic_topology.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_uint64] + [_vp] * 10
+        L.ref_classical.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                    _vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_int, _vp, _vp, _vp, _vp]
         L.ref_switch_value.restype = ctypes.c_double
         L.ref_switch_value.argtypes = [ctypes.c_double, ctypes.c_double]
         L.ref_switch_derivative.restype = ctypes.c_double
@@ -298,3 +303,51 @@ def ref_md(model: RefModel, pos, vel, types, masses, box, dt_ps=0.001, prec="fp3
     wall = L.ref_md_run(model.h, x.shape[0], _p(x), _p(v), _p(t), _p(m), _p(b), float(dt_ps),
                         0 if prec == "fp64" else 1, int(steps), int(threads), ctypes.byref(ep))
     return wall, x, v, ep.value
+
+
+# ---- classical force field of the reference (forcefield.cpp) ----------------
+LJ_SIGMA = (0.33, 0.30)  # SyntheticParams defaults (synthetic.hpp:30-33)
+LJ_EPS = (0.40, 0.50)
+
+
+def ref_synthetic_topology(n, density=33.4, fraction=0.35, seed=7) -> dict:
+    """The synthetic system's topology (synthetic.cpp:36-130) as flat arrays."""
+    L = ref()
+    c = np.zeros(4, dtype=np.int32)
+    _rcheck(L.ref_synthetic_topology(n, density, fraction, seed, _p(c), *([None] * 9)))
+    nb, na, nd, ne = (int(v) for v in c)
+    t = {"charges": np.zeros(n), "excl_offset": np.zeros(n + 1, dtype=np.int32),
+         "excl": np.zeros(max(ne, 1), dtype=np.int32), "bonds": np.zeros((max(nb, 1), 2), dtype=np.int32),
+         "bond_params": np.zeros((max(nb, 1), 2)), "angles": np.zeros((max(na, 1), 3), dtype=np.int32),
+         "angle_params": np.zeros((max(na, 1), 2)), "dihedrals": np.zeros((max(nd, 1), 4), dtype=np.int32),
+         "dihedral_params": np.zeros((max(nd, 1), 3))}
+    _rcheck(L.ref_synthetic_topology(n, density, fraction, seed, _p(c), _p(t["charges"]),
+                                     _p(t["excl_offset"]), _p(t["excl"]), _p(t["bonds"]),
+                                     _p(t["bond_params"]), _p(t["angles"]), _p(t["angle_params"]),
+                                     _p(t["dihedrals"]), _p(t["dihedral_params"])))
+    t["excl"] = t["excl"][:ne]
+    for k, m in (("bonds", nb), ("bond_params", nb), ("angles", na), ("angle_params", na),
+                 ("dihedrals", nd), ("dihedral_params", nd)):
+        t[k] = t[k][:m]
+    return t
+
+
+def ref_classical(pos, n, scheme=0, rc_c=0.7, eps_rf=78.0, rc_lj=0.7, fp64=True, density=33.4,
+                  fraction=0.35, seed=7):
+    """compute_classical (forcefield.cpp:265-279) on the synthetic topology."""
+    L = ref()
+    x = np.ascontiguousarray(pos, dtype=np.float64)
+    sig = np.asarray(LJ_SIGMA)
+    eps = np.asarray(LJ_EPS)
+    e = np.zeros(3)
+    f = np.zeros((n, 3))
+    w = np.zeros(1)
+    c = np.zeros(1, dtype=np.int32)
+    _rcheck(L.ref_classical(n, density, fraction, seed, _p(x), _p(sig), _p(eps), scheme, rc_c,
+                            eps_rf, rc_lj, int(fp64), _p(e), _p(f), _p(w), _p(c)))
+    return {"energies": e, "forces": f, "virial": float(w[0]), "collinear": int(c[0])}
+
+
+def _rcheck(code):
+    if code:
+        raise OracleError(code, ref().ref_last_error().decode())

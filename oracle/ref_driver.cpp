@@ -22,7 +22,9 @@
 #include <thread>
 #include <vector>
 
+#include "halomd/forcefield.hpp"
 #include "halomd/integrators.hpp"
+#include "halomd/neighborlist.hpp"
 #include "halomd/nn/inference.hpp"
 #include "halomd/nn/model.hpp"
 #include "halomd/synthetic.hpp"
@@ -84,6 +86,88 @@ int ref_synthetic(int n, double density, double fraction, uint64_t seed, double 
             masses[i] = topo.mass[i];
         }
         for (int a = 0; a < 3; ++a) box[a] = st.box.lengths[a];
+    });
+}
+
+// ---- classical force field (forcefield.cpp) on the synthetic topology -------
+// The synthetic system's topology (synthetic.cpp:36-130) exported as flat arrays
+// (call with NULL arrays to get the counts: counts[0..3] = bonds, angles,
+// dihedrals, exclusion entries).
+int ref_synthetic_topology(int n, double density, double fraction, uint64_t seed, int* counts,
+                           double* charges, int* excl_offset, int* excl, int* bonds,
+                           double* bond_p, int* angles, double* angle_p, int* dih, double* dih_p) {
+    return guarded([&] {
+        SyntheticParams p;
+        p.n_atoms = n;
+        p.density = density;
+        p.fraction_grouped = fraction;
+        p.seed = seed;
+        auto [topo, st] = generate_synthetic_system(p);
+        (void)st;
+        long ne = 0;
+        for (const auto& e : topo.exclusions) ne += static_cast<long>(e.size());
+        counts[0] = static_cast<int>(topo.bonds.size());
+        counts[1] = static_cast<int>(topo.angles.size());
+        counts[2] = static_cast<int>(topo.dihedrals.size());
+        counts[3] = static_cast<int>(ne);
+        if (!charges) return;
+        int k = 0;
+        excl_offset[0] = 0;
+        for (int i = 0; i < n; ++i) {
+            charges[i] = topo.charge[i];
+            for (int j : topo.exclusions[i]) excl[k++] = j;
+            excl_offset[i + 1] = k;
+        }
+        for (size_t t = 0; t < topo.bonds.size(); ++t) {
+            const auto& b = topo.bonds[t];
+            bonds[2 * t] = b.i, bonds[2 * t + 1] = b.j;
+            bond_p[2 * t] = b.k_b, bond_p[2 * t + 1] = b.r0;
+        }
+        for (size_t t = 0; t < topo.angles.size(); ++t) {
+            const auto& a = topo.angles[t];
+            angles[3 * t] = a.i, angles[3 * t + 1] = a.j, angles[3 * t + 2] = a.k;
+            angle_p[2 * t] = a.k_a, angle_p[2 * t + 1] = a.theta0;
+        }
+        for (size_t t = 0; t < topo.dihedrals.size(); ++t) {
+            const auto& d = topo.dihedrals[t];
+            dih[4 * t] = d.i, dih[4 * t + 1] = d.j, dih[4 * t + 2] = d.k, dih[4 * t + 3] = d.l;
+            dih_p[3 * t] = d.k_d, dih_p[3 * t + 1] = d.phase, dih_p[3 * t + 2] = d.multiplicity;
+        }
+    });
+}
+
+// compute_classical (forcefield.cpp:265-279) on the synthetic topology with the
+// given positions; pair list = build_neighbor_list(.., rc, skin 0, half).
+int ref_classical(int n, double density, double fraction, uint64_t seed, const double* xyz,
+                  const double* sigma, const double* eps, int scheme, double rc_c, double eps_rf,
+                  double rc_lj, int fp64, double* energies, double* forces, double* virial,
+                  int* collinear) {
+    return guarded([&] {
+        SyntheticParams p;
+        p.n_atoms = n;
+        p.density = density;
+        p.fraction_grouped = fraction;
+        p.seed = seed;
+        auto [topo, st] = generate_synthetic_system(p);
+        for (int i = 0; i < n; ++i) st.positions[i] = Vec3{xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+        ForceFieldParams ffp;
+        ffp.lj.sigma = {sigma[0], sigma[1]};
+        ffp.lj.epsilon = {eps[0], eps[1]};
+        ffp.rc = rc_lj;
+        ffp.coulomb.rc = rc_c;
+        ffp.coulomb.eps_rf = eps_rf;
+        ffp.coulomb.scheme = scheme ? CoulombScheme::reaction_field : CoulombScheme::cutoff_shifted;
+        auto nl = build_neighbor_list(st, topo, std::max(rc_c, rc_lj), 0.0);
+        ForceDiagnostics diag;
+        const EnergyReport rep = compute_classical(st, topo, nl, ffp, &diag,
+                                                   fp64 ? Precision::fp64 : Precision::fp32);
+        energies[0] = rep.bonded;
+        energies[1] = rep.lj;
+        energies[2] = rep.coulomb;
+        for (int i = 0; i < n; ++i)
+            for (int a = 0; a < 3; ++a) forces[3 * i + a] = st.forces[i][a];
+        *virial = diag.virial;
+        *collinear = diag.collinear_angles;
     });
 }
 

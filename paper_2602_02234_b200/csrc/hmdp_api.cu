@@ -55,6 +55,30 @@ struct GddGeom {
     double halo;
 };
 void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t);
+struct FfDev {
+    int n, n_types, scheme;
+    double rc_lj, rc_c, k_rf, c_rf, fpre;
+    const double* sigma;
+    const double* eps;
+    const double* q;
+    const int* type;
+    const int* exo;
+    const int* exc;
+    int nb, na, nd;
+    const int* bi;
+    const double* bp;
+    const int* ai;
+    const double* ap;
+    const int* di;
+    const double* dp;
+    const int* aso;
+    const int* asl;
+    double L[3];
+};
+int ff_grid(int);
+template <typename T>
+void launch_ff(const FfDev&, const DevGraph&, const double*, double*, double*, double*, double*,
+               int*, double*, unsigned*, cudaStream_t);
 void launch_gdd_rev(const DevGraph&, int, int*, cudaStream_t);
 template <typename T>
 void launch_gdd_zero(const DevGraph&, int, const unsigned char*, T*, long long, T*, T*, double*,
@@ -1994,6 +2018,199 @@ int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts) {
            "D2H");
         ck(cudaStreamSynchronize(ctx->st()), "sync");
     });
+}
+
+// ---------------------------------------------------------------------------
+// Classical force field on the device (hmdp_ff.cu; forcefield.cpp)
+// ---------------------------------------------------------------------------
+struct hmdp_ff {
+    hmdp_ctx* geo = nullptr;  // geometry-only context: device neighbour list
+    int n = 0;
+    FfDev dev{};
+    DBuf buf_i, buf_d, pos, F, part, contrib, term, out, coll;
+    PinnedBuf pin;
+    ~hmdp_ff() {
+        for (DBuf* b : {&buf_i, &buf_d, &pos, &F, &part, &contrib, &term, &out, &coll}) b->release();
+        pin.release();
+        delete geo;
+    }
+};
+
+int hmdp_ff_create(int device, int n, const int* types, const double* charges, int n_types,
+                   const double* sigma, const double* epsilon, int coulomb_scheme,
+                   double rc_coulomb, double eps_rf, double rc_lj, const int* excl_offset,
+                   const int* excl, int n_bonds, const int* bonds, const double* bond_params,
+                   int n_angles, const int* angles, const double* angle_params, int n_dihedrals,
+                   const int* dihedrals, const double* dihedral_params, hmdp_ff** out) {
+    if (!out) return HMDP_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded([&] {
+        if (n < 1 || !types || !charges || !sigma || !epsilon || n_types < 1 || !excl_offset)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        if (coulomb_scheme != 0 && coulomb_scheme != 1)
+            fail(HMDP_INVALID_ARGUMENT, "coulomb scheme must be 0 (cutoff_shifted) or 1 (reaction_field)");
+        if (!(rc_lj > 0.0) || !(rc_coulomb > 0.0)) fail(HMDP_INVALID_ARGUMENT, "cutoffs must be positive");
+        for (int i = 0; i < n; ++i)
+            if (types[i] < 0 || types[i] >= n_types)
+                fail(HMDP_INVALID_ARGUMENT, "atom type out of range");
+        const int ne = excl_offset[n];
+        for (int i = 0; i < n; ++i)
+            for (int k = excl_offset[i]; k < excl_offset[i + 1]; ++k)
+                if (excl[k] < 0 || excl[k] >= n || (k > excl_offset[i] && excl[k] <= excl[k - 1]))
+                    fail(HMDP_INVALID_ARGUMENT, "exclusion lists must be sorted, in range");
+        auto check_idx = [&](const int* a, int cnt, int per) {
+            for (int q = 0; q < cnt * per; ++q)
+                if (a[q] < 0 || a[q] >= n) fail(HMDP_INVALID_ARGUMENT, "bonded term index out of range");
+        };
+        check_idx(bonds, n_bonds, 2);
+        check_idx(angles, n_angles, 3);
+        check_idx(dihedrals, n_dihedrals, 4);
+        auto ff = std::make_unique<hmdp_ff>();
+        hmdp_ctx* g = nullptr;
+        const int code = hmdp_create(nullptr, 0, device, n, 0, &g);
+        if (code) fail(code, hmdp_last_error());
+        ff->geo = g;
+        ff->n = n;
+        set_device(g);
+        // atom -> contribution slots (bonds 2, angles 3, dihedrals 4 per term), slot order
+        std::vector<std::vector<int>> slots(n);
+        int s = 0;
+        for (int t = 0; t < n_bonds; ++t)
+            for (int a = 0; a < 2; ++a) slots[bonds[2 * t + a]].push_back(s++);
+        for (int t = 0; t < n_angles; ++t)
+            for (int a = 0; a < 3; ++a) slots[angles[3 * t + a]].push_back(s++);
+        for (int t = 0; t < n_dihedrals; ++t)
+            for (int a = 0; a < 4; ++a) slots[dihedrals[4 * t + a]].push_back(s++);
+        std::vector<int> ivec, aso(n + 1, 0), asl;
+        for (int i = 0; i < n; ++i) {
+            aso[i + 1] = aso[i] + static_cast<int>(slots[i].size());
+            asl.insert(asl.end(), slots[i].begin(), slots[i].end());
+        }
+        std::vector<size_t> io;
+        auto pushi = [&](const int* p, size_t cnt) {
+            io.push_back(ivec.size());
+            ivec.insert(ivec.end(), p, p + cnt);
+            while (ivec.size() % 4) ivec.push_back(0);
+        };
+        pushi(types, n);
+        pushi(excl_offset, n + 1);
+        pushi(excl ? excl : excl_offset, excl ? ne : 0);
+        pushi(bonds ? bonds : excl_offset, 2 * static_cast<size_t>(n_bonds));
+        pushi(angles ? angles : excl_offset, 3 * static_cast<size_t>(n_angles));
+        pushi(dihedrals ? dihedrals : excl_offset, 4 * static_cast<size_t>(n_dihedrals));
+        pushi(aso.data(), aso.size());
+        pushi(asl.empty() ? aso.data() : asl.data(), asl.size());
+        std::vector<double> dvec;
+        std::vector<size_t> dof;
+        auto pushd = [&](const double* p, size_t cnt) {
+            dof.push_back(dvec.size());
+            if (p) dvec.insert(dvec.end(), p, p + cnt);
+            while (dvec.size() % 2 || dvec.size() == dof.back()) dvec.push_back(0.0);
+        };
+        pushd(sigma, n_types);
+        pushd(epsilon, n_types);
+        pushd(charges, n);
+        pushd(bond_params, 2 * static_cast<size_t>(n_bonds));
+        pushd(angle_params, 2 * static_cast<size_t>(n_angles));
+        pushd(dihedral_params, 3 * static_cast<size_t>(n_dihedrals));
+        ff->buf_i.ensure(ivec.size() * sizeof(int));
+        ff->buf_d.ensure(dvec.size() * sizeof(double));
+        ck(cudaMemcpy(ff->buf_i.p, ivec.data(), ivec.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(ff->buf_d.p, dvec.data(), dvec.size() * sizeof(double), cudaMemcpyHostToDevice),
+           "H2D");
+        const int* bi = ff->buf_i.as<int>();
+        const double* bd = ff->buf_d.as<double>();
+        FfDev& f = ff->dev;
+        f.n = n;
+        f.n_types = n_types;
+        f.scheme = coulomb_scheme;
+        f.rc_lj = rc_lj;
+        f.rc_c = rc_coulomb;
+        f.k_rf = (eps_rf - 1.0) / ((2.0 * eps_rf + 1.0) * rc_coulomb * rc_coulomb * rc_coulomb);
+        f.c_rf = 1.0 / rc_coulomb + f.k_rf * rc_coulomb * rc_coulomb;
+        f.fpre = 138.935458;  // units::coulomb_prefactor (units.hpp:13)
+        f.type = bi + io[0];
+        f.exo = bi + io[1];
+        f.exc = bi + io[2];
+        f.bi = bi + io[3];
+        f.ai = bi + io[4];
+        f.di = bi + io[5];
+        f.aso = bi + io[6];
+        f.asl = bi + io[7];
+        f.sigma = bd + dof[0];
+        f.eps = bd + dof[1];
+        f.q = bd + dof[2];
+        f.bp = bd + dof[3];
+        f.ap = bd + dof[4];
+        f.dp = bd + dof[5];
+        f.nb = n_bonds;
+        f.na = n_angles;
+        f.nd = n_dihedrals;
+        const int nt = n_bonds + n_angles + n_dihedrals;
+        ff->pos.ensure(3 * static_cast<size_t>(n) * sizeof(double));
+        ff->F.ensure(3 * static_cast<size_t>(n) * sizeof(double));
+        ff->part.ensure(3 * static_cast<size_t>(ff_grid(n)) * sizeof(double));
+        ff->contrib.ensure(3 * static_cast<size_t>(std::max(s, 1)) * sizeof(double));
+        ff->term.ensure(2 * static_cast<size_t>(std::max(nt, 1)) * sizeof(double));
+        ff->out.ensure(8 * sizeof(double));
+        ff->coll.ensure(sizeof(int));
+        *out = ff.release();
+    });
+}
+
+int hmdp_ff_compute(hmdp_ff* ff, const double* xyz, const double* box, int precision,
+                    double* energies, double* forces, double* virial, int* collinear) {
+    return guarded([&] {
+        if (!ff || !xyz || !box || !energies || !forces) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        hmdp_ctx* g = ff->geo;
+        set_device(g);
+        const int n = ff->n;
+        const double rc = std::max(ff->dev.rc_lj, ff->dev.rc_c);
+        cudaStream_t st = g->st();
+        ck(cudaMemcpyAsync(ff->pos.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        FfDev f = ff->dev;
+        for (int a = 0; a < 3; ++a) f.L[a] = box[a];
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            g->ensure_atoms(n);
+            g->neighbors(n, ff->pos.as<double>(), box, rc, st, nullptr);
+            const DevGraph gr = g->periodic_graph(n, nullptr);
+            ck(cudaMemsetAsync(ff->coll.p, 0, sizeof(int), st), "memset");
+            if (precision == HMDP_FP64)
+                launch_ff<double>(f, gr, ff->pos.as<double>(), ff->F.as<double>(), ff->part.as<double>(),
+                                  ff->contrib.as<double>(), ff->term.as<double>(), ff->coll.as<int>(),
+                                  ff->out.as<double>(), g->err.as<unsigned>(), st);
+            else
+                launch_ff<float>(f, gr, ff->pos.as<double>(), ff->F.as<double>(), ff->part.as<double>(),
+                                 ff->contrib.as<double>(), ff->term.as<double>(), ff->coll.as<int>(),
+                                 ff->out.as<double>(), g->err.as<unsigned>(), st);
+            ck(cudaGetLastError(), "kernel launch");
+            const unsigned bits = g->take_err();
+            if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
+                g->grow_for(bits);
+                continue;
+            }
+            if (bits & kErrZeroEdge)
+                fail(HMDP_RUNTIME_ERROR, "pair distance below overlap threshold (blow-up)");
+            hmdp_ctx::raise_bits(bits);
+            double h[8];
+            int c = 0;
+            ck(cudaMemcpy(h, ff->out.p, 4 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(&c, ff->coll.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(forces, ff->F.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            energies[0] = h[0];
+            energies[1] = h[1];
+            energies[2] = h[2];
+            if (virial) *virial = h[3];
+            if (collinear) *collinear = c;
+            return;
+        }
+        fail(HMDP_RUNTIME_ERROR, "neighbour capacity did not converge");
+    });
+}
+
+int hmdp_ff_destroy(hmdp_ff* ff) {
+    delete ff;
+    return HMDP_OK;
 }
 
 long hmdp_make_model_json(int family, int depth, double rc, int n_types, int n_basis, int hidden,
