@@ -255,6 +255,20 @@ int hmdp_ff_compute(hmdp_ff* ff, const double* xyz, const double* box, int preci
                     double* energies, double* forces, double* virial, int* collinear);
 int hmdp_ff_destroy(hmdp_ff* ff);
 
+/* Hybrid device MD (the paper's NNPot coupling): every step the
+ * classical force field (ff) on all n atoms + the DP model (ctx) on the sorted
+ * group[n_group], forces summed, velocity Verlet on all atoms — captured as one CUDA
+ * graph per steps_per_graph steps.  energies[4] = (bonded, lj, coulomb, nn) of the
+ * last evaluated configuration. */
+typedef struct hmdp_hmd hmdp_hmd;
+int hmdp_hybrid_create(hmdp_ctx* ctx, hmdp_ff* ff, int n, const int* group, int n_group,
+                       const double* xyz, const double* vel, const double* masses, const int* types,
+                       const double* box, double dt_ps, int precision, int steps_per_graph,
+                       hmdp_hmd** out);
+int hmdp_hybrid_run(hmdp_hmd* h, int steps);
+int hmdp_hybrid_get(hmdp_hmd* h, double* xyz, double* vel, double* forces, double* energies);
+int hmdp_hybrid_destroy(hmdp_hmd* h);
+
 /* ---------------------------------------------------------------------------
  * Measurement hooks.
  * hmdp_set_stream: run the context's work on an external cudaStream_t (e.g. the

@@ -76,6 +76,11 @@ SIGNATURES = {
                                 _c_int, _vp, _vp, ctypes.POINTER(_vp)]),
     "hmdp_ff_compute": (_c_int, [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp]),
     "hmdp_ff_destroy": (_c_int, [_vp]),
+    "hmdp_hybrid_create": (_c_int, [_vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_double,
+                                    _c_int, _c_int, ctypes.POINTER(_vp)]),
+    "hmdp_hybrid_run": (_c_int, [_vp, _c_int]),
+    "hmdp_hybrid_get": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "hmdp_hybrid_destroy": (_c_int, [_vp]),
     "hmdp_make_dp_model_json": (_c_long, [_c_int, _c_int, _c_double, _c_double, _c_int, _c_int,
                                           ctypes.c_uint64, _vp, _c_long]),
     "hmdp_synthetic_system": (_c_int, [_c_int, _c_double, _c_double, ctypes.c_uint64, _c_double,

@@ -76,6 +76,7 @@ struct FfDev {
     double L[3];
 };
 int ff_grid(int);
+void launch_scatter_add3(int, const int*, const double*, double*, cudaStream_t);
 template <typename T>
 void launch_ff(const FfDev&, const DevGraph&, const double*, double*, double*, double*, double*,
                int*, double*, unsigned*, cudaStream_t);
@@ -2210,6 +2211,189 @@ int hmdp_ff_compute(hmdp_ff* ff, const double* xyz, const double* box, int preci
 
 int hmdp_ff_destroy(hmdp_ff* ff) {
     delete ff;
+    return HMDP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Hybrid device MD: classical force field on every atom + DP model on one group
+// (NNPot coupling), velocity Verlet, CUDA-graph captured.
+// ---------------------------------------------------------------------------
+struct hmdp_hmd {
+    hmdp_ctx* ctx = nullptr;
+    hmdp_ff* ff = nullptr;
+    int n = 0, ng = 0, precision = HMDP_FP64, steps_per_graph = 1;
+    double dt = 0.001, box[3] = {0, 0, 0};
+    DBuf x, v, m, types, grp, F;
+    std::map<int, cudaGraphExec_t> graphs;
+    cudaStream_t gst = nullptr;
+    ~hmdp_hmd() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+        for (DBuf* b : {&x, &v, &m, &types, &grp, &F}) b->release();
+    }
+};
+
+namespace {
+// forces at the current positions: classical (all atoms, SET) + DP (group, ADDED)
+void hmd_forces(hmdp_hmd* h, cudaStream_t st) {
+    hmdp_ff* ff = h->ff;
+    hmdp_ctx* g = ff->geo;
+    FfDev f = ff->dev;
+    for (int a = 0; a < 3; ++a) f.L[a] = h->box[a];
+    const double rcf = std::max(f.rc_lj, f.rc_c);
+    g->neighbors(h->n, h->x.as<double>(), h->box, rcf, st, nullptr);
+    const DevGraph gr = g->periodic_graph(h->n, nullptr);
+    ck(cudaMemsetAsync(ff->coll.p, 0, sizeof(int), st), "memset");
+    if (h->precision == HMDP_FP64)
+        launch_ff<double>(f, gr, h->x.as<double>(), h->F.as<double>(), ff->part.as<double>(),
+                          ff->contrib.as<double>(), ff->term.as<double>(), ff->coll.as<int>(),
+                          ff->out.as<double>(), g->err.as<unsigned>(), st);
+    else
+        launch_ff<float>(f, gr, h->x.as<double>(), h->F.as<double>(), ff->part.as<double>(),
+                         ff->contrib.as<double>(), ff->term.as<double>(), ff->coll.as<int>(),
+                         ff->out.as<double>(), g->err.as<unsigned>(), st);
+    hmdp_ctx* c = h->ctx;
+    launch_gather_group(h->ng, h->grp.as<int>(), h->x.as<double>(), h->types.as<int>(),
+                        c->pos.as<double>(), c->types.as<int>(), st);
+    enqueue_periodic(c, h->ng, c->pos.as<double>(), c->types.as<int>(), h->box, h->precision,
+                     c->forces.as<double>(), nullptr, st);
+    launch_scatter_add3(h->ng, h->grp.as<int>(), c->forces.as<double>(), h->F.as<double>(), st);
+}
+void hmd_check(hmdp_hmd* h) {
+    const unsigned a = h->ff->geo->take_err(), b = h->ctx->take_err();
+    if (a & kErrZeroEdge) fail(HMDP_RUNTIME_ERROR, "pair distance below overlap threshold (blow-up)");
+    hmdp_ctx::raise_bits(a | b);
+}
+}  // namespace
+
+int hmdp_hybrid_create(hmdp_ctx* ctx, hmdp_ff* ff, int n, const int* group, int n_group,
+                       const double* xyz, const double* vel, const double* masses, const int* types,
+                       const double* box, double dt_ps, int precision, int steps_per_graph,
+                       hmdp_hmd** out) {
+    if (!out) return HMDP_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded([&] {
+        need_model(ctx);
+        if (!ff || ff->n != n || n_group < 1 || n_group > n || !group || !xyz || !vel || !masses ||
+            !types || !box)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        for (int k = 0; k < n_group; ++k)
+            if (group[k] < 0 || group[k] >= n || (k > 0 && group[k] <= group[k - 1]))
+                fail(HMDP_INVALID_ARGUMENT, "group must be sorted, duplicate-free, in range");
+        for (int k = 0; k < n_group; ++k)
+            if (types[group[k]] < 0 || types[group[k]] >= ctx->model.n_types)
+                fail(HMDP_INVALID_ARGUMENT, "atom type out of range for the model");
+        set_device(ctx);
+        auto h = std::make_unique<hmdp_hmd>();
+        h->ctx = ctx;
+        h->ff = ff;
+        h->n = n;
+        h->ng = n_group;
+        h->precision = precision;
+        h->dt = dt_ps;
+        h->steps_per_graph = std::max(1, steps_per_graph);
+        std::memcpy(h->box, box, sizeof h->box);
+        h->x.ensure(3 * n * sizeof(double));
+        h->v.ensure(3 * n * sizeof(double));
+        h->m.ensure(n * sizeof(double));
+        h->types.ensure(n * sizeof(int));
+        h->grp.ensure(n_group * sizeof(int));
+        h->F.ensure(3 * n * sizeof(double));
+        cudaStream_t st = ctx->st();
+        ck(hmdp_set_stream(ff->geo, st) == HMDP_OK ? cudaSuccess : cudaErrorInvalidValue, "stream");
+        ck(cudaMemcpyAsync(h->x.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(h->v.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(h->m.p, masses, n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(h->types.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(h->grp.p, group, n_group * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        ctx->ensure_atoms(n_group);
+        ff->geo->ensure_atoms(n);
+        // initial forces, sizing every buffer (capacity growth happens here, never in a graph)
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            hmd_forces(h.get(), st);
+            const unsigned a = ff->geo->take_err(), b = ctx->take_err();
+            if ((a | b) & (kErrNbrOverflow | kErrCellOverflow)) {
+                ff->geo->grow_for(a);
+                ctx->grow_for(b);
+                continue;
+            }
+            if (a & kErrZeroEdge) fail(HMDP_RUNTIME_ERROR, "pair distance below overlap threshold (blow-up)");
+            hmdp_ctx::raise_bits(a | b);
+            break;
+        }
+        // headroom for the dynamics (as hmdp_md_create), then the opening kick + drift
+        for (hmdp_ctx* c : {ctx, ff->geo}) c->cap = std::min(256, c->cap + c->cap / 2);
+        hmd_forces(h.get(), st);
+        hmd_check(h.get());
+        launch_gdd_integrate(n, h->F.as<double>(), h->x.as<double>(), h->v.as<double>(),
+                             h->m.as<double>(), dt_ps, 1, ctx->err.as<unsigned>(), st);
+        ck(cudaStreamSynchronize(st), "sync");
+        *out = h.release();
+    });
+}
+
+int hmdp_hybrid_run(hmdp_hmd* h, int steps) {
+    return guarded([&] {
+        if (!h || steps < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(h->ctx);
+        cudaStream_t st = h->ctx->st();
+        if (h->gst != st) {
+            for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+            h->graphs.clear();
+            h->gst = st;
+        }
+        int left = steps;
+        while (left > 0) {
+            const int chunk = std::min(left, h->steps_per_graph);
+            auto it = h->graphs.find(chunk);
+            if (it == h->graphs.end()) {
+                cudaGraph_t gph;
+                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+                for (int k = 0; k < chunk; ++k) {
+                    hmd_forces(h, st);
+                    launch_gdd_integrate(h->n, h->F.as<double>(), h->x.as<double>(),
+                                         h->v.as<double>(), h->m.as<double>(), h->dt, 0,
+                                         h->ctx->err.as<unsigned>(), st);
+                }
+                ck(cudaStreamEndCapture(st, &gph), "end capture");
+                cudaGraphExec_t ex;
+                ck(cudaGraphInstantiate(&ex, gph, 0), "instantiate");
+                cudaGraphDestroy(gph);
+                it = h->graphs.emplace(chunk, ex).first;
+            }
+            ck(cudaGraphLaunch(it->second, st), "graph launch");
+            left -= chunk;
+        }
+        hmd_check(h);
+    });
+}
+
+// State after the last run: positions / velocities are the next step's drifted
+// positions and half-kicked velocities (velocity Verlet split as the device MD
+// loop); forces and energies of the last evaluated configuration.
+int hmdp_hybrid_get(hmdp_hmd* h, double* xyz, double* vel, double* forces, double* energies) {
+    return guarded([&] {
+        if (!h) fail(HMDP_INVALID_ARGUMENT, "null hybrid");
+        set_device(h->ctx);
+        cudaStream_t st = h->ctx->st();
+        const size_t b = 3 * static_cast<size_t>(h->n) * sizeof(double);
+        if (xyz) ck(cudaMemcpyAsync(xyz, h->x.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (vel) ck(cudaMemcpyAsync(vel, h->v.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        if (forces) ck(cudaMemcpyAsync(forces, h->F.p, b, cudaMemcpyDeviceToHost, st), "D2H");
+        double e4[4] = {0, 0, 0, 0}, enn = 0.0;
+        ck(cudaMemcpyAsync(e4, h->ff->out.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(&enn, h->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (energies) {
+            energies[0] = e4[0];
+            energies[1] = e4[1];
+            energies[2] = e4[2];
+            energies[3] = enn;
+        }
+    });
+}
+
+int hmdp_hybrid_destroy(hmdp_hmd* h) {
+    delete h;
     return HMDP_OK;
 }
 

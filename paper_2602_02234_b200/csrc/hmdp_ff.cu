@@ -295,6 +295,19 @@ __global__ void k_ff_reduce(int nblk, const double* __restrict__ part, int nt,
     }
 }
 
+// dst[group[k]] += src[k] (the NNPot scatter of group forces)
+__global__ void k_scatter_add3(int ng, const int* __restrict__ grp, const double* __restrict__ src,
+                               double* __restrict__ dst) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const int i = grp[k];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dst[3 * i + a] += src[3 * k + a];
+}
+void launch_scatter_add3(int ng, const int* grp, const double* src, double* dst, cudaStream_t st) {
+    if (ng > 0) k_scatter_add3<<<(ng + 127) / 128, 128, 0, st>>>(ng, grp, src, dst);
+}
+
 int ff_grid(int n) {
     const int want = (n + kFfCTA / 32 - 1) / (kFfCTA / 32);
     return want < 1 ? 1 : (want > 4096 ? 4096 : want);

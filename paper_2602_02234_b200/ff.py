@@ -84,3 +84,50 @@ class ClassicalFF:
             self.close()
         except Exception:
             pass
+
+
+class HybridMD:
+    """Hybrid device MD (include/hmdp.h hmdp_hybrid_*): classical force field on every
+    atom + the DP model on one sorted atom group (the paper's NNPot coupling,
+    SPEC.md:411-419), summed forces, velocity Verlet, one CUDA graph per
+    ``steps_per_graph`` steps."""
+
+    def __init__(self, ctx, ff: ClassicalFF, group, positions, velocities, masses, types, box,
+                 dt_ps=0.001, precision: Precision = Precision.fp64, steps_per_graph: int = 10):
+        g = np.ascontiguousarray(group, dtype=np.int32)
+        x = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+        v = np.ascontiguousarray(velocities, dtype=np.float64).reshape(-1, 3)
+        m = np.ascontiguousarray(masses, dtype=np.float64)
+        t = np.ascontiguousarray(types, dtype=np.int32)
+        b = _box3(box)
+        self.n = x.shape[0]
+        self.ctx, self.ff = ctx, ff  # keep both alive
+        h = ctypes.c_void_p()
+        check(lib().hmdp_hybrid_create(ctx.handle, ff.handle, self.n, ptr(g), g.shape[0], ptr(x),
+                                       ptr(v), ptr(m), ptr(t), ptr(b), float(dt_ps), int(precision),
+                                       int(steps_per_graph), ctypes.byref(h)))
+        self.handle = h
+
+    def run(self, steps: int) -> None:
+        check(lib().hmdp_hybrid_run(self.handle, int(steps)))
+
+    def state(self):
+        """(x, v, F, energies[bonded, lj, coulomb, nn]); x / v are the next step's
+        drifted positions and half-kicked velocities (velocity Verlet split)."""
+        x = np.zeros((self.n, 3))
+        v = np.zeros((self.n, 3))
+        f = np.zeros((self.n, 3))
+        e = np.zeros(4)
+        check(lib().hmdp_hybrid_get(self.handle, ptr(x), ptr(v), ptr(f), ptr(e)))
+        return x, v, f, e
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().hmdp_hybrid_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
