@@ -426,9 +426,9 @@ __device__ __forceinline__ void rf_angle_list(const DevDpWork<T>& dw, int start,
 // `out + q*ld_out` (local row index q; shared or global memory); ADD accumulates
 // into out instead of a residual.  Two rows per iteration (loads in flight).
 template <typename T, bool ADD>
-__device__ __forceinline__ void proj(const T* __restrict__ W, const T* __restrict__ b,
-                                     const T* in, int ld_in, const T* res, int ld_res, T* out,
-                                     int ld_out, int cnt) {
+__device__ __forceinline__ void proj_simt(const T* __restrict__ W, const T* __restrict__ b,
+                                          const T* in, int ld_in, const T* res, int ld_res, T* out,
+                                          int ld_out, int cnt) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     T wr[32];
 #pragma unroll
@@ -464,6 +464,93 @@ __device__ __forceinline__ void proj(const T* __restrict__ W, const T* __restric
             else *o2 = (res ? res[(long long)(q + 4) * ld_res + lane] : T(0)) + c0 + c1;
         }
     }
+}
+
+// ---- tensor-core projection (FP32 path): mma.sync m16n8k8 TF32 with the 3-pass
+// hi/lo split (x = hi + lo, x*y ~ hi*hi + hi*lo + lo*hi), which keeps FP32-level
+// accuracy (single-pass TF32 fails the force tolerance).  Warp w
+// owns output channels 8w..8w+7 for every 16-row tile of the atom's edge rows.
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <bool ADD>
+__device__ __forceinline__ void proj_tc(const float* __restrict__ W, const float* __restrict__ b,
+                                        const float* in, int ld_in, const float* res, int ld_res,
+                                        float* out, int ld_out, int cnt) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    // B[k][n] = W[n][k] for this warp's 8 output channels, all four k-steps, split
+    uint32_t bh[4][2], bl[4][2];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        tf32_split(__ldg(W + (8 * w + g) * 32 + 8 * kk + t), bh[kk][0], bl[kk][0]);
+        tf32_split(__ldg(W + (8 * w + g) * 32 + 8 * kk + t + 4), bh[kk][1], bl[kk][1]);
+    }
+    const int col = 8 * w + 2 * t;
+    const float bias0 = b ? __ldg(b + col) : 0.f, bias1 = b ? __ldg(b + col + 1) : 0.f;
+    for (int m0 = 0; m0 < cnt; m0 += 16) {
+        const int r0 = m0 + g, r1 = r0 + 8;
+        const bool v0 = r0 < cnt, v1 = r1 < cnt;
+        const float* x0 = in + (long long)(v0 ? r0 : 0) * ld_in;
+        const float* x1 = in + (long long)(v1 ? r1 : 0) * ld_in;
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const int k0 = 8 * kk + t;
+            const float a[4] = {v0 ? x0[k0] : 0.f, v1 ? x1[k0] : 0.f, v0 ? x0[k0 + 4] : 0.f,
+                                v1 ? x1[k0 + 4] : 0.f};
+            uint32_t ah[4], al[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tf32_split(a[q], ah[q], al[q]);
+            mma_tf32(c, al, bh[kk][0], bh[kk][1]);
+            mma_tf32(c, ah, bl[kk][0], bl[kk][1]);
+            mma_tf32(c, ah, bh[kk][0], bh[kk][1]);
+        }
+        if (v0) {
+            float* o = out + (long long)r0 * ld_out + col;
+            if (ADD) {
+                o[0] += c[0];
+                o[1] += c[1];
+            } else {
+                const float* rr = res ? res + (long long)r0 * ld_res + col : nullptr;
+                o[0] = (rr ? rr[0] : 0.f) + bias0 + c[0];
+                o[1] = (rr ? rr[1] : 0.f) + bias1 + c[1];
+            }
+        }
+        if (v1) {
+            float* o = out + (long long)r1 * ld_out + col;
+            if (ADD) {
+                o[0] += c[2];
+                o[1] += c[3];
+            } else {
+                const float* rr = res ? res + (long long)r1 * ld_res + col : nullptr;
+                o[0] = (rr ? rr[0] : 0.f) + bias0 + c[2];
+                o[1] = (rr ? rr[1] : 0.f) + bias1 + c[3];
+            }
+        }
+    }
+}
+
+// out_q = [res_q] + b + W x_q over the atom's edge rows: tensor cores (3xTF32) in
+// FP32, SIMT in FP64 (the FP64 check mode).
+template <typename T, bool ADD>
+__device__ __forceinline__ void proj(const T* __restrict__ W, const T* __restrict__ b,
+                                     const T* in, int ld_in, const T* res, int ld_res, T* out,
+                                     int ld_out, int cnt) {
+    if constexpr (sizeof(T) == 4)
+        proj_tc<ADD>(W, b, in, ld_in, res, ld_res, out, ld_out, cnt);
+    else
+        proj_simt<T, ADD>(W, b, in, ld_in, res, ld_res, out, ld_out, cnt);
 }
 
 template <typename T>
