@@ -41,6 +41,8 @@ def profile_name(name):
     """kernel symbol (team-size template argument dropped) -> hmdp_profile marker"""
     base = re.sub(r"<([124])>$", "", name)  # k_nbr_search<G>
     base = re.sub(r"<(float|double), [124]", r"<\1", base)  # k_*<T, G, ...>
+    if base.startswith(("k_embed<", "k_msg_fwd<", "k_msg_bwd<", "k_embed_bwd<")):
+        base = re.sub(r", [01]>$", ">", base)  # the LIST (atom-list) template argument
     return PROFILE_NAME.get(base)
 
 
