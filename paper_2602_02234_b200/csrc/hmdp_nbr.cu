@@ -204,7 +204,9 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
                        unsigned* err, cudaStream_t st, const int* alist, const int* alist_n) {
     const int sms = num_sms();
-    int G = (4 * n <= 16 * sms) ? 4 : (2 * n <= 16 * sms ? 2 : 1);
+    // team size by system size (measured with the network kernels):
+    // 4 warps per atom up to 4 atoms per SM, 2 up to ~20 per SM, then 1
+    int G = (4 * n <= 16 * sms) ? 4 : (n <= 20 * sms ? 2 : 1);
     if (team_override()) G = team_override();
     // warps per CTA: enough teams per CTA that the atoms fill every SM
     int teams = (n + sms - 1) / sms;

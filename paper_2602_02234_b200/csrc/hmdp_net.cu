@@ -1369,9 +1369,15 @@ int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments
     }();
     return v;
 }
-static NetShape net_shape(int n) {
+// Team size by system size and model (measured on B200): 4 warps per
+// atom up to 4 atoms per SM (1YRF); 2 warps per atom for the message-passing model
+// up to ~40 atoms per SM (1UBQ 7.5k -> 11.4k, 3LZM 6.8k -> 8.1k steps/s vs 1 warp;
+// 2PTC on par, warm L2 6.3k vs 3.9k) and for embed_fit up to ~10 atoms per SM
+// (1UBQ 24.2k -> 28.9k; 3LZM and 2PTC prefer 1 warp); 1 warp beyond.
+static NetShape net_shape(int n, int n_msg) {
     const int sms = num_sms();
-    int G = (4 * n <= kMaxWarps * sms) ? 4 : (2 * n <= kMaxWarps * sms ? 2 : 1);
+    const int two_upto = (n_msg > 0 ? 40 : 10) * sms;
+    int G = (4 * n <= kMaxWarps * sms) ? 4 : (n <= two_upto ? 2 : 1);
     if (team_override()) G = team_override();
     const int max_teams = kMaxWarps / G;
     int teams = (n + sms - 1) / sms;
@@ -1484,7 +1490,7 @@ template <typename T>
 int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws,
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
-    const NetShape sh = net_shape(gr.n_active);
+    const NetShape sh = net_shape(gr.n_active, md.n_msg);
     int launches;
     if (sh.G == 4)
         launches = Net<T, 4>::network(sh, md, gr, ws, rev, st, mk, mf);
@@ -1536,7 +1542,7 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
-    const NetShape sh = net_shape(gr.n_active);
+    const NetShape sh = net_shape(gr.n_active, md.n_msg);
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:
