@@ -86,3 +86,31 @@ def test_device_dd_md_matches_device_md(golden_models):
     # next step's drifted positions: x(t + dt) = x(t) + dt v(t + dt/2)
     v_half = engs[0].vel.cpu().numpy()
     assert np.abs(x - 0.001 * v_half - x_ref).max() < 1e-10
+
+
+def test_device_dd_fp32_within_tolerance(golden_models):
+    from paper_2602_02234_b200.dd import DeviceDD, run_local
+
+    s = P.generate_synthetic_system(2643)
+    m = P.model_from_json(golden_models["dpa3"])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    engs = [DeviceDD(P.Context(m, max_atoms=2643), 2643, s.types, s.box, (2, 2, 1), r,
+                     P.Precision.fp32) for r in range(4)]
+    for e in engs:
+        e.load(s.positions)
+    run_local(engs)
+    E, F, W, W9 = engs[3].result()
+    assert abs(E - ref.energy) <= E_TOL * abs(ref.energy)
+    assert np.abs(F - ref.forces).max() <= F_TOL * rms(ref.forces)
+
+
+def test_device_dd_rejects_deepmd_families_and_bad_grids(golden_models):
+    from paper_2602_02234_b200.dd import DeviceDD
+
+    s = P.generate_synthetic_system(582)
+    with pytest.raises(ValueError):
+        DeviceDD(P.Context(P.make_dp_model(P.ModelFamily.se_a, 1)), 582, s.types, s.box,
+                 (2, 1, 1), 0, P.Precision.fp32)
+    m = P.model_from_json(golden_models["dpa3"])
+    with pytest.raises(ValueError):
+        DeviceDD(P.Context(m), 582, s.types, s.box, (2, 1, 1), 2, P.Precision.fp32)
