@@ -11,9 +11,11 @@ kick -- one CUDA graph per step.
   value      steps/s over all ranks (N independent replica boxes = weak scaling),
              each timed step bracketed by CUDA events on the launching stream,
              L2 flushed (256 MiB write) before every step outside the events.
-  e2e        the same MD through the host-buffer C-ABI call (ForceProvider ->
-             hmdp_compute): pinned H2D positions/types + D2H forces/energy every
-             step, host integration, timed with CUDA events around the loop.
+  e2e        the same MD through the host-buffer C-ABI call: a C++ caller runs the
+             reference's velocity_verlet_step on host arrays with hmdp_compute as
+             its force function (csrc/hmdp_caller_md.cpp), so every step carries
+             the H2D of positions/types and the D2H of forces/energy; timed with
+             CUDA events around the loop.
   roofline   dominant kernel from per-kernel CUDA events (hmdp_profile) in the
              same graph-per-step loop; achieved = reference-counter FLOPs of that
              kernel / its mean duration; peak = FP32 FFMA throughput measured
@@ -299,7 +301,7 @@ def run_ours(args, rank, world, local_rank, dist):
     import torch
 
     import paper_2602_02234_b200 as P
-    from paper_2602_02234_b200._lib import check, lib
+    from paper_2602_02234_b200._lib import check, lib, ptr
     from paper_2602_02234_b200.md import DeviceMD
 
     torch.cuda.set_device(local_rank)
@@ -422,27 +424,27 @@ def run_ours(args, rank, world, local_rank, dist):
         except Exception:
             mp = {}
 
-    # ---- e2e: host-buffer C-ABI provider, host integration ----
+    # ---- e2e: host-buffer C-ABI provider driven by a C++ caller running the
+    # reference's velocity_verlet_step (csrc/hmdp_caller_md.cpp) ----
     KE = min(K, 300)
     prov_ctx = P.Context(model, device=local_rank, max_atoms=n)
     check(L.hmdp_set_stream(prov_ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
-    xh = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
-    th = torch.empty((n,), dtype=torch.int32, pin_memory=True).numpy()
-    xh[:] = s.positions
-    th[:] = s.types
-    vh = s.velocities.copy()
-    inv_m = (0.0005 / s.masses)[:, None]
-    out = prov_ctx.compute(xh, th, s.box, prec)
-    fh = out.forces
-    for _ in range(5):
-        prov_ctx.compute(xh, th, s.box, prec)
+    caller = ctypes.CDLL(os.path.join(ROOT, "paper_2602_02234_b200", "lib", "libhmdp_caller.so"))
+    vv = caller.hmdp_caller_velocity_verlet
+    vv.restype = ctypes.c_int
+    xh = np.ascontiguousarray(s.positions, dtype=np.float64).copy()
+    th = np.ascontiguousarray(s.types, dtype=np.int32)
+    vh = np.ascontiguousarray(s.velocities, dtype=np.float64).copy()
+    mh = np.ascontiguousarray(s.masses, dtype=np.float64)
+    bh = np.ascontiguousarray(s.box, dtype=np.float64)
+    out = prov_ctx.compute(xh, th, bh, prec)
+    fh = np.ascontiguousarray(out.forces).copy()
+    eh = ctypes.c_double()
+    vv_args = (prov_ctx.handle, ctypes.c_int(n), ptr(xh), ptr(vh), ptr(fh), ptr(th), ptr(bh),
+               ptr(mh), ctypes.c_double(0.001), None, ctypes.c_int(int(prec)), ctypes.byref(eh))
+    check(vv(*vv_args[:9], ctypes.c_int(5), *vv_args[10:]))  # warm-up (graph captured)
     e0.record(stream)
-    for _ in range(KE):
-        vh += fh * inv_m
-        xh += vh * 0.001
-        out = prov_ctx.compute(xh, th, s.box, prec)
-        fh = out.forces
-        vh += fh * inv_m
+    check(vv(*vv_args[:9], ctypes.c_int(KE), *vv_args[10:]))
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1)
@@ -452,7 +454,7 @@ def run_ours(args, rank, world, local_rank, dist):
         e2e_ms = float(tt.item())
     e2e_value = world * KE / (e2e_ms * 1e-3)
     h2d = xh.nbytes + th.nbytes
-    d2h = out.forces.nbytes + 11 * 8
+    d2h = fh.nbytes + 11 * 8
 
     if rank != 0:
         return
@@ -501,8 +503,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "gpu_launches": per_step_kernels * K,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "ForceProvider -> hmdp_compute (pinned host xyz/types in, forces/E out), "
-                        "host velocity Verlet"},
+                "path": "C++ caller: reference velocity_verlet_step on host arrays, force "
+                        "function = hmdp_compute (host xyz/types in, forces/E out)"},
         "cpu_baseline": cpu,
         "clocks": clocks if sampler else None,
         "wall_s_timed_region": wall,

@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.join(ROOT, "include", "hmdp.h"))
     deps.append(os.path.abspath(__file__))
     if not force and not _stale(LIB, deps):
+        _build_caller(force)
         return LIB
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
@@ -62,7 +63,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
+    _build_caller(True)
     return LIB
+
+
+CALLER = os.path.join(LIBDIR, "libhmdp_caller.so")
+
+
+def _build_caller(force: bool) -> None:
+    """bench.py's e2e caller (csrc/hmdp_caller_md.cpp): a host C++ MD loop over libhmdp."""
+    src = os.path.join(CSRC, "hmdp_caller_md.cpp")
+    if not force and not _stale(CALLER, [src, os.path.join(ROOT, "include", "hmdp.h")]):
+        return
+    tmp = CALLER + ".tmp"
+    subprocess.run(["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-I",
+                    os.path.join(ROOT, "include"), src, "-o", tmp, "-L", LIBDIR, "-lhmdp",
+                    "-Wl,-rpath,$ORIGIN"], check=True)
+    os.replace(tmp, CALLER)
 
 
 if __name__ == "__main__":

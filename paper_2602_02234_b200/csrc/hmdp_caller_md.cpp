@@ -1,0 +1,45 @@
+// hmdp_caller_md.cpp — the reference's MD call site over the drop-in, as a caller
+// would compile it: velocity_verlet_step (integrators.cpp:32-47, with
+// check_finite_forces :12-18) on HOST buffers, the force function being the C-ABI's
+// host-buffer hmdp_compute (= build_input_periodic + evaluate every step, rebuild
+// every step as the reference's ForceFunction does).  Not part of the product
+// library: bench.py's e2e leg times it, so the end-to-end number carries a C++
+// caller's host work (as the reference's own loop does) instead of numpy's.
+#include <cmath>
+
+#include "hmdp.h"
+
+extern "C" {
+
+// Runs `steps` velocity-Verlet steps in place on x/v (n x 3, FP64), forces f in/out
+// (f holds the forces of the current x on entry, as the reference's State does).
+// Returns an hmdp status; HMDP_RUNTIME_ERROR on a non-finite force (message in
+// hmdp_last_error() is the library's when the failure came from hmdp_compute).
+int hmdp_caller_velocity_verlet(hmdp_ctx* ctx, int n, double* x, double* v, double* f,
+                                const int* types, const double* box, const double* masses,
+                                double dt, int steps, int precision, double* energy) {
+    const double half = 0.5 * dt;
+    for (int s = 0; s < steps; ++s) {
+        for (int k = 0; k < 3 * n; ++k)
+            if (!std::isfinite(f[k])) return HMDP_RUNTIME_ERROR;
+        for (int i = 0; i < n; ++i) {
+            const double c = half / masses[i];
+            for (int a = 0; a < 3; ++a) {
+                v[3 * i + a] += f[3 * i + a] * c;
+                x[3 * i + a] += v[3 * i + a] * dt;
+            }
+        }
+        const int rc = hmdp_compute(ctx, n, x, types, box, precision, energy, nullptr, f,
+                                    nullptr, nullptr);
+        if (rc != HMDP_OK) return rc;
+        for (int k = 0; k < 3 * n; ++k)
+            if (!std::isfinite(f[k])) return HMDP_RUNTIME_ERROR;
+        for (int i = 0; i < n; ++i) {
+            const double c = half / masses[i];
+            for (int a = 0; a < 3; ++a) v[3 * i + a] += f[3 * i + a] * c;
+        }
+    }
+    return HMDP_OK;
+}
+
+}  // extern "C"

@@ -100,3 +100,39 @@ def test_md_after_host_compute_keeps_cells_consistent(golden_models):
     x, v, f, e = md.state()
     hx, *_ = host_md(json.loads(golden_models["dpa2"]), s, 4)
     assert np.abs(x - hx).max() < 1e-10
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_caller_velocity_verlet_matches_device_md(prec, golden_models):
+    """bench.py's e2e leg: the reference's velocity_verlet_step in C++ over host
+    buffers with hmdp_compute as the force function (csrc/hmdp_caller_md.cpp)
+    follows the same trajectory as the fused device MD loop."""
+    import ctypes
+    import os
+
+    from paper_2602_02234_b200._lib import LIB_PATH, check, ptr
+
+    caller = ctypes.CDLL(os.path.join(os.path.dirname(LIB_PATH), "libhmdp_caller.so"))
+    s = P.generate_synthetic_system(582)
+    m = P.model_from_json(golden_models["dpa3"])
+    pr = P.Precision[prec]
+    md = DeviceMD(P.Context(m), s.positions, s.velocities, s.masses, s.types, s.box,
+                  precision=pr, steps_per_graph=4)
+    md.run(8)
+    dx, dv, df, de = md.state()
+    ctx = P.Context(m, max_atoms=582)
+    x = s.positions.copy()
+    v = s.velocities.copy()
+    t = s.types.astype(np.int32)
+    mass = np.ascontiguousarray(s.masses, dtype=np.float64)
+    box = np.ascontiguousarray(s.box, dtype=np.float64)
+    f = np.ascontiguousarray(ctx.compute(x, t, box, pr).forces).copy()
+    e = ctypes.c_double()
+    check(caller.hmdp_caller_velocity_verlet(ctx.handle, ctypes.c_int(582), ptr(x), ptr(v), ptr(f),
+                                             ptr(t), ptr(box), ptr(mass), ctypes.c_double(0.001),
+                                             ctypes.c_int(8), ctypes.c_int(int(pr)),
+                                             ctypes.byref(e)))
+    tol = 1e-12 if prec == "fp64" else 1e-9
+    assert np.abs(x - dx).max() < tol
+    assert np.abs(v - dv).max() < 1e3 * tol
+    assert e.value == pytest.approx(de, rel=1e-12 if prec == "fp64" else 1e-6)
