@@ -114,3 +114,81 @@ def test_device_dd_rejects_deepmd_families_and_bad_grids(golden_models):
     m = P.model_from_json(golden_models["dpa3"])
     with pytest.raises(ValueError):
         DeviceDD(P.Context(m), 582, s.types, s.box, (2, 1, 1), 2, P.Precision.fp32)
+
+
+def _dist_worker(rank, world, port, model_json, q):
+    """One rank of a real torch.distributed job (gloo: NCCL refuses two ranks on
+    one GPU, and the pool has one) running run_dist, the program bench.py captures."""
+    import os
+    import sys
+
+    import torch
+    import torch.distributed as tdist
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2602_02234_b200 as PP
+        from paper_2602_02234_b200.dd import DeviceDD, run_dist
+
+        s = PP.generate_synthetic_system(1231, temperature=300.0)
+        m = PP.model_from_json(model_json)
+        eng = DeviceDD(PP.Context(m, max_atoms=1231), 1231, s.types, s.box, (world, 1, 1), rank,
+                       PP.Precision.fp64, masses=s.masses)
+        eng.load(s.positions, s.velocities)
+        run_dist(eng, "eval")
+        torch.cuda.synchronize()
+        E, F, W, W9 = eng.result()
+        run_dist(eng, "open", 0.001)
+        for _ in range(3):
+            run_dist(eng, "md", 0.001)
+        torch.cuda.synchronize()
+        q.put((rank, E, F, W9, eng.pos.cpu().numpy(), eng.vel.cpu().numpy()))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+def test_device_dd_two_processes_match_single_domain(mname, golden_models):
+    """run_dist in two processes (torch.distributed, gloo over the GPU tensors)
+    equals the single-domain evaluation and the in-process simulated ranks' MD."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2602_02234_b200.dd import DeviceDD, run_local
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, golden_models[mname], q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s = P.generate_synthetic_system(1231, temperature=300.0)
+    m = P.model_from_json(golden_models[mname])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    engs = [DeviceDD(P.Context(m, max_atoms=1231), 1231, s.types, s.box, (2, 1, 1), r,
+                     P.Precision.fp64, masses=s.masses) for r in range(2)]
+    for e in engs:
+        e.load(s.positions, s.velocities)
+    run_local(engs, "eval")
+    run_local(engs, "open", 0.001)
+    for _ in range(3):
+        run_local(engs, "md", 0.001)
+    x_loc = engs[0].pos.cpu().numpy()
+    for rank, E, F, W9, x, v in res:
+        assert E == pytest.approx(ref.energy, rel=1e-12)
+        assert np.abs(F - ref.forces).max() < 1e-10 * np.abs(ref.forces).max()
+        assert np.abs(W9 - ref.virial_tensor).max() < 1e-9 * max(1.0, np.abs(W9).max())
+        assert np.abs(x - x_loc).max() < 1e-12
+    assert np.array_equal(res[0][4], res[1][4])  # replicated positions agree bitwise
