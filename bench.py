@@ -547,7 +547,9 @@ def run_gdd(args, rank, world, local_rank, dist):
     E = float(eng.out[0])  # energy of the initial configuration (extensivity check)
     dd.run_dist(eng, "open", 0.001)
     for _ in range(max(args.warmup, 3)):
+        l0 = eng.launches()
         dd.run_dist(eng, "md", 0.001)
+        per_step_kernels = eng.launches() - l0
     torch.cuda.synchronize(dev)
     g = None
     if use_graph:
@@ -576,7 +578,7 @@ def run_gdd(args, rank, world, local_rank, dist):
     dist.barrier()
     t_ms = e0.elapsed_time(e1)
     ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    bufs = [eng.p, eng.p, eng.sg, eng.sg, eng.f, eng.out][: 2 * (model.depth() - 1) + 2]
+    bufs = [eng.p, eng.p, eng.sg, eng.sg, eng.fo][: 2 * (model.depth() - 1) + 1]
     ca.record(stream)
     for _ in range(20):
         for b in bufs:
@@ -584,10 +586,35 @@ def run_gdd(args, rank, world, local_rank, dist):
     cb.record(stream)
     torch.cuda.synchronize(dev)
     halo_ms = ca.elapsed_time(cb) / 20
-    tt = torch.tensor([t_ms, halo_ms], dtype=torch.float64, device=dev)
+    # e2e: every step the positions come in from pinned host memory and the step's
+    # result (positions, forces, E/W) goes back to pinned host memory, read by the host
+    KE = min(K, 300)
+    x_h = torch.empty_like(eng.pos, device="cpu").pin_memory()
+    fo_h = torch.empty_like(eng.fo, device="cpu").pin_memory()
+    x_h.copy_(eng.pos)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    e_host = 0.0
+    for _ in range(KE):
+        eng.pos.copy_(x_h, non_blocking=True)
+        if g is not None:
+            g.replay()
+        else:
+            dd.run_dist(eng, "md", 0.001)
+        x_h.copy_(eng.pos, non_blocking=True)
+        fo_h.copy_(eng.fo, non_blocking=True)
+        stream.synchronize()
+        e_host += float(fo_h[3 * n])  # the host reads the step's energy
+    eb.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = ea.elapsed_time(eb)
+    tt = torch.tensor([t_ms, halo_ms, e2e_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t_ms, halo_ms = float(tt[0]), float(tt[1])
+    t_ms, halo_ms, e2e_ms = float(tt[0]), float(tt[1]), float(tt[2])
     value = world * K / (t_ms * 1e-3)
+    e2e_value = world * KE / (e2e_ms * 1e-3)
     counts = eng.counts()
     from paper_2602_02234_b200._lib import check, lib
 
@@ -616,9 +643,12 @@ def run_gdd(args, rank, world, local_rank, dist):
                  "share": halo_ms / (t_ms / K)},
         "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * world,
                         "rel_diff": abs(E - e_single * world) / abs(e_single * world)},
-        "gpu_launches": None,
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0, "note": "device-resident MD loop"},
+        "gpu_launches": per_step_kernels * K,
+        "e2e": {"value": e2e_value, "unit": "steps/s",
+                "h2d_bytes_per_step": int(x_h.numel() * 8),
+                "d2h_bytes_per_step": int((x_h.numel() + fo_h.numel()) * 8),
+                "path": "per step and rank: positions H2D from pinned host memory, the "
+                        "captured DD step, positions + forces + (E, W) D2H, host sync"},
     }
     print(json.dumps(line), flush=True)
 

@@ -230,6 +230,8 @@ int hmdp_gdd_setup(hmdp_ctx* ctx, int n, const int* types, const double* box, co
 int hmdp_gdd_bind(hmdp_ctx* ctx, int kind, void* dptr);
 int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt);
 int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts3); /* owned, halo, searched (syncs) */
+/* Kernels enqueued by hmdp_gdd_phase on this context so far (launch accounting). */
+int hmdp_gdd_launches(const hmdp_ctx* ctx, long long* launches);
 
 /* ---------------------------------------------------------------------------
  * Classical force field on the device: the reference's

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hmdp_gdd_bind": (_c_int, [_vp, _c_int, _vp]),
     "hmdp_gdd_phase": (_c_int, [_vp, _c_int, _c_int, _c_double]),
     "hmdp_gdd_counts": (_c_int, [_vp, _vp]),
+    "hmdp_gdd_launches": (_c_int, [_vp, _vp]),
     "hmdp_ff_create": (_c_int, [_c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_double,
                                 _c_double, _c_double, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp,
                                 _c_int, _vp, _vp, ctypes.POINTER(_vp)]),

@@ -470,6 +470,7 @@ struct hmdp_ctx {
     // global-index device DD (hmdp_gdd_*): roles, lists, counts + caller-bound buffers
     struct Gdd {
         int n = 0, prec = -1, n_est = 0;
+        long long launches = 0;  // kernels enqueued by hmdp_gdd_phase so far
         GddGeom geom{};
         DBuf role, lists, counts;
         double box[3] = {0, 0, 0};
@@ -1964,39 +1965,47 @@ int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
                     launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
                     launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
                                        M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
+                    g.launches += 6;  // roles, bin, search, rev, zero, zero_energy
                     break;
                 }
                 case 0:
                     ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
                     launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st);
+                    g.launches += 1;
                     break;
                 case 1:
                     launch_gdd_push_halo<T>(own, g.n_est, static_cast<const T*>(g.p_atom),
                                             w.pe + (layer & 1) * slots * kH,
                                             g.lists.as<int>() + n, g.counts.as<int>() + 1, st);
+                    g.launches += 1;
                     break;
                 case 2:
                     if (layer < M - 1) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
                     launch_dd_phase<T>(md, own, w, 2, layer, nullptr, g.forces, g.out, st);
+                    g.launches += 1;
                     break;
                 case 3:
                     ck(cudaMemsetAsync(g.sghost, 0, rows, st), "memset");
                     launch_gdd_halo_sums<T>(own, g.n_est, w.d + (layer & 1) * slots * kH,
                                             static_cast<T*>(g.sghost), g.lists.as<int>() + n,
                                             g.counts.as<int>() + 1, st);
+                    g.launches += 1;
                     break;
                 case 4:
                 case 5:
                     launch_dd_phase<T>(md, own, w, phase, layer, nullptr, g.forces, g.out, st);
+                    g.launches += 1;
                     break;
                 case 6:  // forces of every row (halo rows: partials), (E, W, W9) partials
                     launch_dd_phase<T>(md, own, w, 6, 0, nullptr, g.forces, g.out, st);
+                    g.launches += 1;
                     break;
                 case 7:  // velocity Verlet on all atoms from the all-reduced forces
                 case 8:  // the initial opening kick + drift only
                     if (!g.vel || !g.mass) fail(HMDP_INVALID_ARGUMENT, "bind velocities and masses");
                     launch_gdd_integrate(n, g.forces, g.pos, g.vel, g.mass, dt, phase == 8 ? 1 : 0,
                                          ctx->err.as<unsigned>(), st);
+                    g.launches += 1;
                     break;
                 default:
                     fail(HMDP_INVALID_ARGUMENT, "unknown phase");
@@ -2008,6 +2017,12 @@ int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
             run(float{});
         ck(cudaGetLastError(), "kernel launch");
     });
+}
+
+int hmdp_gdd_launches(const hmdp_ctx* ctx, long long* launches) {
+    if (!ctx || !launches) return HMDP_INVALID_ARGUMENT;
+    *launches = ctx->gdd.launches;
+    return HMDP_OK;
 }
 
 int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts) {

@@ -404,8 +404,10 @@ class DeviceDD:
         self.mass = torch.ones(n, dtype=torch.float64, device=dev)
         self.p = torch.zeros((n, 32), dtype=T, device=dev)
         self.sg = torch.zeros((n, 32), dtype=T, device=dev)
-        self.f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
-        self.out = torch.zeros(16, dtype=torch.float64, device=dev)
+        # forces and the (E, W, W9) totals share one buffer: one all-reduce for both
+        self.fo = torch.zeros(3 * n + 16, dtype=torch.float64, device=dev)
+        self.f = self.fo[:3 * n].view(n, 3)
+        self.out = self.fo[3 * n:]
         t = np.ascontiguousarray(types, dtype=np.int32)
         b = np.ascontiguousarray(box, dtype=np.float64)
         d = np.ascontiguousarray(self.dims, dtype=np.int32)
@@ -455,10 +457,15 @@ class DeviceDD:
             else:
                 self._ph(5)
         self._ph(6)
-        yield self.f
-        yield self.out
+        yield self.fo  # forces + (E, W, W9)
         if kind == "md":
             self._ph(7, 0, dt)
+
+    def launches(self):
+        """Kernels this rank's phases have enqueued so far (hmdp_gdd_launches)."""
+        v = ctypes.c_longlong()
+        check(lib().hmdp_gdd_launches(self.ctx.handle, ctypes.byref(v)))
+        return int(v.value)
 
     def counts(self):
         c = np.zeros(3, dtype=np.int32)

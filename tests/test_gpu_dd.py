@@ -78,8 +78,11 @@ def test_device_dd_md_matches_device_md(golden_models):
         e.load(s.positions, s.velocities)
     run_local(engs, "eval")
     run_local(engs, "open", 0.001)  # the device MD loop's first chunk: opening kick + drift
-    for _ in range(5):
+    for step in range(5):
+        l0 = engs[0].launches()
         run_local(engs, "md", 0.001)
+        # roles/bin/search/rev/zero x2, embed, (push, fwd) x2, (sums, bwd) x2, force, integrate
+        assert engs[0].launches() - l0 == 17
     x = engs[0].pos.cpu().numpy()
     assert np.abs(x - engs[1].pos.cpu().numpy()).max() == 0.0  # replicated state
     # DeviceMD's state is the completed step (x(t), v(t)); the DD engines hold the
