@@ -406,7 +406,11 @@ def run_ours(args, rank, world, local_rank, dist):
     kflops = kernel_flops(model.as_dict(), n, n, ne, m2)
     # FLOP-carrying kernels; the dominant one is the slowest of them
     cands = {k: v for k, v in kern_ms.items() if k in kflops}
-    dom = max(cands, key=cands.get)
+    # the slowest; kernels within 3 % of it count as tied (msg_fwd_last and msg_bwd run
+    # equally long at 1YRF) and the tie goes to the one carrying more FLOPs, so the
+    # reported kernel does not flip between runs
+    tmax = max(cands.values())
+    dom = max((k for k in cands if cands[k] >= 0.97 * tmax), key=lambda k: kflops[k])
     peak = ctypes.c_double()
     check(L.hmdp_peak_fp32(local_rank, 200, ctypes.byref(peak)))
     achieved = kflops[dom] / (kern_ms[dom] * 1e-3) / 1e12
@@ -498,7 +502,9 @@ def run_ours(args, rank, world, local_rank, dist):
                      "mean_launch_us": kern_ms[dom] * 1e3,
                      "peak_kind": "measured FP32 FFMA (SIMT) throughput, hmdp_peak_fp32; the "
                                   "kernels run FP32 FMA, not tensor cores",
-                     "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None},
+                     "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None,
+                     "frac_per_kernel": {k: kflops[k] / (cands[k] * 1e-3) / 1e12 / peak.value
+                                         for k in sorted(cands, key=lambda k: -cands[k])}},
         "kernels_us": {k: v * 1e3 for k, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},
         "gpu_launches": per_step_kernels * K,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
