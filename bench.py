@@ -413,6 +413,8 @@ def run_ours(args, rank, world, local_rank, dist):
     dom = max((k for k in cands if cands[k] >= 0.97 * tmax), key=lambda k: kflops[k])
     peak = ctypes.c_double()
     check(L.hmdp_peak_fp32(local_rank, 200, ctypes.byref(peak)))
+    peak_tc = ctypes.c_double()  # 3xTF32 mma.sync: the DeePMD-family projections' pipe
+    check(L.hmdp_peak_tf32x3(local_rank, 200, ctypes.byref(peak_tc)))
     achieved = kflops[dom] / (kern_ms[dom] * 1e-3) / 1e12
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -503,6 +505,7 @@ def run_ours(args, rank, world, local_rank, dist):
                      "peak_kind": "measured FP32 FFMA (SIMT) throughput, hmdp_peak_fp32; the "
                                   "kernels run FP32 FMA, not tensor cores",
                      "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None,
+                     "peak_tf32x3_tflops": peak_tc.value,
                      "frac_per_kernel": {k: kflops[k] / (cands[k] * 1e-3) / 1e12 / peak.value
                                          for k in sorted(cands, key=lambda k: -cands[k])}},
         "kernels_us": {k: v * 1e3 for k, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},

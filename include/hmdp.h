@@ -281,12 +281,16 @@ int hmdp_hybrid_destroy(hmdp_hmd* h);
  *   hmdp_profile_name(i) the i-th kernel's name.
  * hmdp_peak_fp32: measured FP32 FFMA throughput of the device (TFLOP/s), the
  *   roofline denominator for the SIMT kernels.
+ * hmdp_peak_tf32x3: measured FP32-accurate 3xTF32 mma.sync throughput (TFLOP/s,
+ *   each hi/lo triple of m16n8k8 MMAs counted as one product), the denominator for
+ *   the tensor-core projections of the DeePMD-style families.
  * ------------------------------------------------------------------------- */
 int hmdp_set_stream(hmdp_ctx* ctx, void* stream);
 int hmdp_profile(hmdp_ctx* ctx, int enable);
 int hmdp_profile_read(hmdp_ctx* ctx, float* ms, int cap, int* count);
 const char* hmdp_profile_name(const hmdp_ctx* ctx, int i);
 int hmdp_peak_fp32(int device, int ms, double* tflops);
+int hmdp_peak_tf32x3(int device, int ms, double* tflops);
 
 /* ---------------------------------------------------------------------------
  * Host fixtures (no device work).

@@ -37,6 +37,7 @@ int launch_network(const DevModel<T>&, const DevGraph&, const DevWork<T>&, doubl
 void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cudaStream_t);
 void launch_gather_group(int, const int*, const double*, const int*, double*, int*, cudaStream_t);
 double probe_fp32_tflops(int ms);
+double probe_tf32x3_tflops(int ms);
 template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t, int* = nullptr);
@@ -1716,6 +1717,14 @@ int hmdp_peak_fp32(int device, int ms, double* tflops) {
         if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
         ck(cudaSetDevice(device), "cudaSetDevice");
         *tflops = probe_fp32_tflops(ms);
+    });
+}
+
+int hmdp_peak_tf32x3(int device, int ms, double* tflops) {
+    return guarded([&] {
+        if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        *tflops = probe_tf32x3_tflops(ms);
     });
 }
 

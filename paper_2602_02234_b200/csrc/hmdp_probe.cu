@@ -1,7 +1,12 @@
-// hmdp_probe.cu — measured FP32 FFMA throughput (the roofline denominator of
-// the SIMT kernels).  16 independent FMA chains per thread, 8 x 256-thread CTAs
-// per SM; timed with CUDA events.
+// hmdp_probe.cu — measured peaks for the roofline denominators:
+//   FP32 FFMA throughput (the SIMT kernels): 16 independent FMA chains per thread,
+//   8 x 256-thread CTAs per SM;
+//   3xTF32 mma.sync throughput (the DeePMD-family projections, hmdp_dp.cu proj_tc):
+//   m16n8k8 TF32 MMAs in hi/lo triples, 8 independent accumulators per warp.
+// Timed with CUDA events.
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 #include <algorithm>
 #include <stdexcept>
@@ -57,6 +62,72 @@ double probe_fp32_tflops(int ms) {
     cudaEventDestroy(e1);
     cudaFree(out);
     const double flops = 2.0 * grid * block * static_cast<double>(iters) * 8 * 16;
+    return flops / (best * 1e-3) / 1e12;
+}
+
+__global__ __launch_bounds__(256) void k_tf32x3_probe(float* out, int iters) {
+    const uint32_t x = __float_as_uint(1.0f + threadIdx.x * 1e-6f);
+    uint32_t ah[4] = {x, x ^ 1u, x ^ 2u, x ^ 3u}, al[4] = {x >> 9, x >> 10, x >> 11, x >> 12};
+    const uint32_t bh0 = x ^ 4u, bh1 = x ^ 5u, bl0 = x >> 13, bl1 = x >> 14;
+    float c[8][4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k][0] = c[k][1] = c[k][2] = c[k][3] = 0.f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+                const uint32_t* a = pass == 2 ? ah : (pass == 0 ? al : ah);
+                const uint32_t b0 = pass == 1 ? bl0 : bh0, b1 = pass == 1 ? bl1 : bh1;
+                asm volatile(
+                    "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+                    "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                    : "+f"(c[k][0]), "+f"(c[k][1]), "+f"(c[k][2]), "+f"(c[k][3])
+                    : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+            }
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+    if (s == 1234.5f) out[blockIdx.x] = s;
+}
+
+// FP32-accurate (3xTF32) GEMM throughput: every hi/lo triple counts as ONE
+// m16n8k8 product (2 * 16 * 8 * 8 flop); the raw TF32 MMA rate is 3x this.
+double probe_tf32x3_tflops(int ms) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = sms * 4, block = 256;
+    float* out = nullptr;
+    if (cudaMalloc(&out, grid * sizeof(float)) != cudaSuccess) throw std::runtime_error("probe alloc");
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto run = [&](int iters) {
+        cudaEventRecord(e0);
+        k_tf32x3_probe<<<grid, block>>>(out, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        return static_cast<double>(t);
+    };
+    run(16);  // warm-up
+    int iters = 64;
+    double t = run(iters);
+    while (t < ms * 0.5 && iters < (1 << 22)) {
+        iters *= 2;
+        t = run(iters);
+    }
+    double best = 1e30;
+    for (int r = 0; r < 5; ++r) best = std::min(best, run(iters));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double warps = static_cast<double>(grid) * (block / 32);
+    const double flops = 2.0 * 16 * 8 * 8 * warps * static_cast<double>(iters) * 8;
     return flops / (best * 1e-3) / 1e12;
 }
 
