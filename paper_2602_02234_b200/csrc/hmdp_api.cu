@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -134,8 +135,9 @@ int guarded(F&& f) {
 
 // Grow-only device allocation.
 // Incremented on every device (re)allocation: a captured graph whose buffers may
-// have moved is stale when the generation changed since its capture.
-unsigned long long g_alloc_gen = 0;
+// have moved is stale when the generation changed since its capture.  Process-wide
+// (contexts on other threads bump it too: at worst a spurious re-capture), atomic.
+std::atomic<unsigned long long> g_alloc_gen{0};
 
 struct DBuf {
     void* p = nullptr;
@@ -501,7 +503,7 @@ struct hmdp_ctx {
         bool disabled = false;  // a capture failed once: stay on the direct path
         bool matches(int n_, int prec_, const double* b, int cap_, int ccap_, cudaStream_t st_) const {
             return exec && n == n_ && prec == prec_ && cap == cap_ && ccap == ccap_ && st == st_ &&
-                   gen == g_alloc_gen && box[0] == b[0] && box[1] == b[1] && box[2] == b[2];
+                   gen == g_alloc_gen.load() && box[0] == b[0] && box[1] == b[1] && box[2] == b[2];
         }
         void reset() {
             if (exec) cudaGraphExecDestroy(exec);
@@ -1098,7 +1100,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                             ctx->cgraph.cap = ctx->cap;
                             ctx->cgraph.ccap = ctx->ccap;
                             ctx->cgraph.st = st;
-                            ctx->cgraph.gen = g_alloc_gen;
+                            ctx->cgraph.gen = g_alloc_gen.load();
                             ctx->cgraph.launches = launches;
                             for (int a = 0; a < 3; ++a) ctx->cgraph.box[a] = box[a];
                         }
