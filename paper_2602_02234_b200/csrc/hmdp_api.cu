@@ -2252,9 +2252,16 @@ struct hmdp_hmd {
     DBuf x, v, m, types, grp, F;
     std::map<int, cudaGraphExec_t> graphs;
     cudaStream_t gst = nullptr;
+    // the DP branch runs beside the classical branch (fork / join by events; inside
+    // a captured graph the two become parallel branches)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~hmdp_hmd() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
         for (DBuf* b : {&x, &v, &m, &types, &grp, &F}) b->release();
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
     }
 };
 
@@ -2266,6 +2273,17 @@ void hmd_forces(hmdp_hmd* h, cudaStream_t st) {
     FfDev f = ff->dev;
     for (int a = 0; a < 3; ++a) f.L[a] = h->box[a];
     const double rcf = std::max(f.rc_lj, f.rc_c);
+    // DP branch (group gather, network, group forces) on the side stream: it reads
+    // the positions and writes only the DP context's buffers
+    hmdp_ctx* c = h->ctx;
+    ck(cudaEventRecord(h->ev_fork, st), "fork");
+    ck(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "fork wait");
+    launch_gather_group(h->ng, h->grp.as<int>(), h->x.as<double>(), h->types.as<int>(),
+                        c->pos.as<double>(), c->types.as<int>(), h->side);
+    enqueue_periodic(c, h->ng, c->pos.as<double>(), c->types.as<int>(), h->box, h->precision,
+                     c->forces.as<double>(), nullptr, h->side);
+    ck(cudaEventRecord(h->ev_join, h->side), "join");
+    // classical branch (all atoms, SETs F) on the caller's stream
     g->neighbors(h->n, h->x.as<double>(), h->box, rcf, st, nullptr);
     const DevGraph gr = g->periodic_graph(h->n, nullptr);
     ck(cudaMemsetAsync(ff->coll.p, 0, sizeof(int), st), "memset");
@@ -2277,11 +2295,7 @@ void hmd_forces(hmdp_hmd* h, cudaStream_t st) {
         launch_ff<float>(f, gr, h->x.as<double>(), h->F.as<double>(), ff->part.as<double>(),
                          ff->contrib.as<double>(), ff->term.as<double>(), ff->coll.as<int>(),
                          ff->out.as<double>(), g->err.as<unsigned>(), st);
-    hmdp_ctx* c = h->ctx;
-    launch_gather_group(h->ng, h->grp.as<int>(), h->x.as<double>(), h->types.as<int>(),
-                        c->pos.as<double>(), c->types.as<int>(), st);
-    enqueue_periodic(c, h->ng, c->pos.as<double>(), c->types.as<int>(), h->box, h->precision,
-                     c->forces.as<double>(), nullptr, st);
+    ck(cudaStreamWaitEvent(st, h->ev_join, 0), "join wait");
     launch_scatter_add3(h->ng, h->grp.as<int>(), c->forces.as<double>(), h->F.as<double>(), st);
 }
 void hmd_check(hmdp_hmd* h) {
@@ -2326,6 +2340,9 @@ int hmdp_hybrid_create(hmdp_ctx* ctx, hmdp_ff* ff, int n, const int* group, int 
         h->F.ensure(3 * n * sizeof(double));
         cudaStream_t st = ctx->st();
         ck(hmdp_set_stream(ff->geo, st) == HMDP_OK ? cudaSuccess : cudaErrorInvalidValue, "stream");
+        ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "side stream");
+        ck(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming), "event");
         ck(cudaMemcpyAsync(h->x.p, xyz, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(h->v.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
         ck(cudaMemcpyAsync(h->m.p, masses, n * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
