@@ -115,7 +115,9 @@ def energy_terms(model: dict, types, offset, nbr, dr_edges):
     mask = (idx >= 0).to(torch.float64)  # [n, m]
     safe_slot = slot.clamp(min=0)
     far = torch.tensor([2.0 * rc, 0.0, 0.0], dtype=torch.float64)
-    d = torch.where((slot >= 0)[..., None], dr_edges[safe_slot], far)  # [n, m, 3]
+    # (no edges at all: gather from a one-row stand-in, every slot is padding)
+    src = dr_edges if dr_edges.shape[0] > 0 else far[None, :]
+    d = torch.where((slot >= 0)[..., None], src[safe_slot], far)  # [n, m, 3]
     r = torch.sqrt((d * d).sum(-1))
     w = smooth_switch(r, rc, rcs) * mask
     s = w / r
@@ -203,8 +205,11 @@ def evaluate(model, types, offset, nbr, dr, want_stages: bool = False):
     dr_t = torch.tensor(np.asarray(dr, dtype=np.float64).reshape(-1, 3), requires_grad=True)
     e_atom, stages = energy_terms(model, types, offset, nbr, dr_t)
     E = e_atom.sum()
-    (g,) = torch.autograd.grad(E, dr_t)
-    g = g.numpy()
+    if E.requires_grad:
+        (g,) = torch.autograd.grad(E, dr_t)
+        g = g.numpy()
+    else:  # no edges: nothing depends on the geometry
+        g = np.zeros((0, 3))
     src = np.repeat(np.arange(n), np.diff(offset))
     F = np.zeros((n, 3))
     np.add.at(F, src, g)

@@ -302,3 +302,37 @@ def test_gpu_nve_energy_conservation(fam, depth):
     ke0 = 0.5 * float(np.sum(s.masses[:, None] * s.velocities ** 2))
     md.run(400)
     assert abs(etot() - e0) < 2e-3 * ke0
+
+
+def _sparse_system():
+    """A pair, an isolated atom and a triplet in a 3 nm box: rows with 0, 1 and 2
+    neighbours (empty softmax / angle lists, single-column attention)."""
+    box = np.array([3.0, 3.0, 3.0])
+    pos = np.array([[0.5, 0.5, 0.5], [0.8, 0.5, 0.5], [2.0, 2.0, 2.0],
+                    [1.5, 0.4, 2.4], [1.5, 0.75, 2.4], [1.5, 0.6, 2.1]])
+    types = np.array([0, 1, 0, 1, 0, 1], dtype=np.int32)
+    return pos, types, box
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam,depth", FAMS, ids=IDS)
+def test_gpu_sparse_rows_and_tiny_systems(fam, depth):
+    pos, types, box = _sparse_system()
+    off, nbr, dr = O.neighbors(pos, box, 0.6)
+    assert list(np.diff(off)) == [1, 1, 0, 2, 2, 2]
+    m = P.make_dp_model(fam, depth)
+    ref = DF.evaluate(m.as_dict(), types, off, nbr, dr)
+    ctx = P.Context(m, device=0)
+    out = ctx.compute(pos, types, box, P.Precision.fp64, per_atom=True)
+    _check(out, ref, 1e-11, 1e-9)
+    assert np.abs(out.per_atom_energy - ref["per_atom"]).max() < 1e-10
+    _check(ctx.compute(pos, types, box, P.Precision.fp32), ref, E_TOL, F_TOL)
+    # one isolated atom: energy = the fitting of an empty environment, no force
+    one = ctx.compute(pos[2:3], types[2:3], box, P.Precision.fp64, per_atom=True)
+    r1 = DF.evaluate(m.as_dict(), types[2:3], np.array([0, 0]), np.zeros(0, dtype=np.int32),
+                     np.zeros((0, 3)))
+    assert one.energy == pytest.approx(r1["energy"], rel=1e-12, abs=1e-12)
+    assert np.abs(one.forces).max() == 0.0
+    # no atoms: zero outputs
+    zero = ctx.compute(np.zeros((0, 3)), np.zeros(0, dtype=np.int32), box)
+    assert zero.energy == 0.0 and zero.forces.shape == (0, 3)
