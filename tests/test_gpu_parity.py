@@ -232,3 +232,28 @@ def test_receptive_field_exactness(golden_models):
     x[far] += [0.01, 0.0, 0.0]
     pert = ctx.compute(x, s.types, s.box, P.Precision.fp64, per_atom=True)
     assert pert.per_atom_energy[0] == base.per_atom_energy[0]
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+def test_sparse_rows_isolated_atom(mname, golden_models):
+    """Rows with 0, 1 and 2 neighbours (a pair, an isolated atom, a triplet) and a
+    single isolated atom, against the oracle; message passing over empty rows."""
+    box = np.array([3.0, 3.0, 3.0])
+    pos = np.array([[0.5, 0.5, 0.5], [0.8, 0.5, 0.5], [2.0, 2.0, 2.0],
+                    [1.5, 0.4, 2.4], [1.5, 0.75, 2.4], [1.5, 0.6, 2.1]])
+    types = np.array([0, 1, 0, 1, 0, 1], dtype=np.int32)
+    md = json.loads(golden_models[mname])
+    ctx = P.context_for(model(golden_models, mname))
+    off, nbr, dr = O.neighbors(pos, box, 0.6)
+    assert list(np.diff(off)) == [1, 1, 0, 2, 2, 2]
+    for prec in ("fp32", "fp64"):
+        ref = O.evaluate(md, types, off, nbr, dr, prec=prec)
+        out = ctx.compute(pos, types, box, P.Precision[prec], per_atom=True)
+        assert out.energy == pytest.approx(ref["energy"], rel=1e-6 if prec == "fp32" else 1e-12)
+        assert np.abs(out.forces - ref["forces"]).max() <= 1e-4 * rms(ref["forces"])
+        assert np.abs(out.per_atom_energy - ref["per_atom"]).max() < 1e-5
+    one = ctx.compute(pos[2:3], types[2:3], box, P.Precision.fp64)
+    r1 = O.evaluate(md, types[2:3], np.array([0, 0], dtype=np.int32), np.zeros(0, dtype=np.int32),
+                    np.zeros((0, 3)))
+    assert one.energy == pytest.approx(r1["energy"], rel=1e-12)
+    assert np.abs(one.forces).max() == 0.0
