@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--strong", action="store_true",
+                    help="--mode dd: split ONE box over the ranks (strong scaling, SURVEY "
+                         "§8(d) configs 3/4) instead of one box per rank")
     ap.add_argument("--mode", choices=["dd", "dd-host", "replicas"], default="dd",
                     help="N>1: device-resident spatial domain decomposition of the box "
                          "replicated over the rank grid (default; one CUDA graph per MD step "
@@ -545,7 +548,8 @@ def run_gdd(args, rank, world, local_rank, dist):
         raise SystemExit("--mode dd: the DeePMD-style families run replicas only (DESIGN.md §11)")
     base = P.generate_synthetic_system(SYSTEMS[args.system])
     dims = dd.rank_grid(world)
-    s = P.replicate(base, dims)
+    s = base if args.strong else P.replicate(base, dims)
+    boxes = 1 if args.strong else world
     n = s.n_atoms
     eng = dd.DeviceDD(P.Context(model, device=local_rank, max_atoms=n), n, s.types, s.box, dims,
                       rank, prec, masses=s.masses)
@@ -622,8 +626,8 @@ def run_gdd(args, rank, world, local_rank, dist):
     tt = torch.tensor([t_ms, halo_ms, e2e_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms, halo_ms, e2e_ms = float(tt[0]), float(tt[1]), float(tt[2])
-    value = world * K / (t_ms * 1e-3)
-    e2e_value = world * KE / (e2e_ms * 1e-3)
+    value = boxes * K / (t_ms * 1e-3)
+    e2e_value = boxes * KE / (e2e_ms * 1e-3)
     counts = eng.counts()
     from paper_2602_02234_b200._lib import check, lib
 
@@ -635,11 +639,13 @@ def run_gdd(args, rank, world, local_rank, dist):
     line = {
         "metric": METRIC, "value": value, "unit": f"steps/s ({args.system}-box equivalents)",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
-        "config": {"workload": f"{args.model.upper()} domain-decomposed MD step, {args.system} "
-                               f"box replicated {dims} (one box per GPU)",
+        "config": {"workload": f"{args.model.upper()} domain-decomposed MD step, " + (
+                       f"one {args.system} box split over {dims}" if args.strong else
+                       f"{args.system} box replicated {dims} (one box per GPU)"),
                    "model": args.model, "system": args.system, "atoms_total": n,
                    "rank_grid": list(dims), "precision": args.precision,
                    "parallelism": f"device-resident spatial DD x{world}: owner/halo lists on the "
@@ -647,11 +653,11 @@ def run_gdd(args, rank, world, local_rank, dist):
                                   f"replicated velocity Verlet",
                    "graph": "one CUDA graph per MD step incl. NCCL" if g is not None else "none",
                    "rank0_owned": counts[0], "rank0_halo": counts[1]},
-        "ns_per_day_per_box": ns_per_day(value / world),
+        "ns_per_day_per_box": ns_per_day(value / boxes),
         "halo": {"ms_per_step": halo_ms, "rounds_per_step": len(bufs),
                  "share": halo_ms / (t_ms / K)},
-        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * world,
-                        "rel_diff": abs(E - e_single * world) / abs(e_single * world)},
+        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * boxes,
+                        "rel_diff": abs(E - e_single * boxes) / abs(e_single * boxes)},
         "gpu_launches": per_step_kernels * K,
         "e2e": {"value": e2e_value, "unit": "steps/s",
                 "h2d_bytes_per_step": int(x_h.numel() * 8),
