@@ -49,7 +49,8 @@ int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWo
               double*, double*, int*, cudaStream_t, const Marker&, const MdFuse&);
 cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
-void launch_stage_in(int, const double*, const int*, double*, int*, cudaStream_t);
+void launch_stage_bin(int, const double*, const int*, double*, int*, const CellGrid&, int*, int*,
+                      int*, unsigned*, cudaStream_t);
 struct GddGeom {
     int d[3];
     double L[3];
@@ -511,6 +512,10 @@ struct hmdp_ctx {
         }
     } cgraph;
     PinnedBuf pin_in;
+    // set while capturing hmdp_compute's graph: neighbors() stages these host-mapped
+    // inputs into the device position / type arrays as it bins them
+    const double* stage_hx = nullptr;
+    const int* stage_ht = nullptr;
     int last_launches = 0;
     cudaStream_t user_stream = nullptr;  // hmdp_set_stream; NULL = own stream
     // per-kernel timing (hmdp_profile): event k is recorded after kernel k
@@ -699,8 +704,13 @@ struct hmdp_ctx {
         cells_owner = nullptr;
         ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
         mark("memset_cells", st);
-        launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
-                        err.as<unsigned>(), st);
+        if (stage_hx)  // graph path: inputs staged from host-mapped memory by the binning
+            launch_stage_bin(n, stage_hx, stage_ht, const_cast<double*>(d_pos),
+                             const_cast<int*>(d_types), cg, cell_count.as<int>(),
+                             members.as<int>(), cell_of.as<int>(), err.as<unsigned>(), st);
+        else
+            launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(),
+                            cell_of.as<int>(), err.as<unsigned>(), st);
         mark("cell_bin", st);
         search(n, d_pos, cg, rc, st, d_types);
     }
@@ -1082,14 +1092,15 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 // word straight into the host-mapped output block: no copy nodes
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-                    launch_stage_in(n, reinterpret_cast<const double*>(hin),
-                                    reinterpret_cast<const int*>(hin + 3 * n * sizeof(double)),
-                                    ctx->pos.as<double>(), ctx->types.as<int>(), st);
+                    ctx->stage_hx = reinterpret_cast<const double*>(hin);
+                    ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
                     ctx->out_override = hp;
                     const int launches =
-                        1 + enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
-                                             box, precision, hp + 16, hp + 16 + 3 * n, st);
+                        enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
+                                         box, precision, hp + 16, hp + 16 + 3 * n, st);
                     ctx->out_override = nullptr;
+                    ctx->stage_hx = nullptr;
+                    ctx->stage_ht = nullptr;
                     const cudaError_t ce = cudaStreamEndCapture(st, &g);
                     if (ce == cudaSuccess && g) {
                         cudaGraphExec_t ex = nullptr;
@@ -1108,6 +1119,8 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     }
                 } catch (...) {  // the result above stands; stay on the direct path
                     ctx->out_override = nullptr;
+                    ctx->stage_hx = nullptr;
+                    ctx->stage_ht = nullptr;
                     cudaGraph_t gg = nullptr;
                     cudaStreamEndCapture(st, &gg);
                     if (gg) cudaGraphDestroy(gg);

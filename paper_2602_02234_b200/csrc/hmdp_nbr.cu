@@ -22,6 +22,23 @@ __global__ void k_cell_bin(int n, const double* __restrict__ pos, CellGrid cg,
     bin_atom(i, pos + 3 * i, cg, cell_count, members, cell_of, err);
 }
 
+// hmdp_compute's graph path: stage one atom's inputs from host-mapped memory into
+// the device arrays and bin it — one kernel where a stage-in kernel and the binning
+// were two (-4 µs per DPA3 1YRF call, tools/ab_e2e.sh).
+__global__ void k_stage_bin(int n, const double* __restrict__ hx, const int* __restrict__ ht,
+                            double* __restrict__ pos, int* __restrict__ types, CellGrid cg,
+                            int* __restrict__ cell_count, int* __restrict__ members,
+                            int* __restrict__ cell_of, unsigned* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x3[3] = {hx[3 * i], hx[3 * i + 1], hx[3 * i + 2]};
+    types[i] = ht[i];
+    pos[3 * i] = x3[0];
+    pos[3 * i + 1] = x3[1];
+    pos[3 * i + 2] = x3[2];
+    bin_atom(i, x3, cg, cell_count, members, cell_of, err);
+}
+
 // G warps per atom (G = 4 / 2 / 1 by system size, as the network kernels), 16
 // warps per CTA, grid-stride over atoms.
 constexpr int kSearchCTA = 512;
@@ -198,6 +215,12 @@ int num_sms() {
 void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_count, int* members,
                      int* cell_of, unsigned* err, cudaStream_t st) {
     k_cell_bin<<<(n + 127) / 128, 128, 0, st>>>(n, pos, cg, cell_count, members, cell_of, err);
+}
+void launch_stage_bin(int n, const double* hx, const int* ht, double* pos, int* types,
+                      const CellGrid& cg, int* cell_count, int* members, int* cell_of,
+                      unsigned* err, cudaStream_t st) {
+    k_stage_bin<<<(n + 127) / 128, 128, 0, st>>>(n, hx, ht, pos, types, cg, cell_count, members,
+                                                 cell_of, err);
 }
 void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* cell_count,
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,

@@ -1504,20 +1504,6 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
     return launches + 1;
 }
 
-// Inputs of hmdp_compute's graph path: positions and types from host-mapped
-// pinned memory into the device buffers (one kernel instead of two copy nodes).
-__global__ void k_stage_in(int n, const double* __restrict__ hx, const int* __restrict__ ht,
-                           double* __restrict__ x, int* __restrict__ t) {
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 4 * n; q += gridDim.x * blockDim.x) {
-        if (q < 3 * n) x[q] = hx[q];
-        else t[q - 3 * n] = ht[q - 3 * n];
-    }
-}
-void launch_stage_in(int n, const double* hx, const int* ht, double* x, int* t, cudaStream_t st) {
-    const int blocks = (4 * n + 255) / 256;
-    k_stage_in<<<blocks < 1 ? 1 : (blocks > 256 ? 256 : blocks), 256, 0, st>>>(n, hx, ht, x, t);
-}
-
 // Force kernel alone (the DeePMD-style families' last phase, hmdp_dp.cu).
 template <typename T>
 void launch_force(const DevGraph& gr, const DevWork<T>& ws, double* forces, double* per_atom,
