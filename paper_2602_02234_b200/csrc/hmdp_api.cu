@@ -524,6 +524,11 @@ struct hmdp_ctx {
     // the device MD loop whose binning the cell lists currently hold (a primed
     // MD chunk continues from it); any other binning clears it
     const void* cells_owner = nullptr;
+    // cell counts are all zero (the network kernels clear them after the search):
+    // hmdp_compute's graph then needs no memset node; skip_cell_memset is set while
+    // that graph is captured
+    bool cells_zero = false;
+    bool skip_cell_memset = false;
     std::vector<cudaEvent_t> pev;
     std::vector<std::string> pname;
 
@@ -702,8 +707,11 @@ struct hmdp_ctx {
         CellGrid cg = grid(box, rc, n);
         ensure_edges(static_cast<long long>(n) * cap);
         cells_owner = nullptr;
-        ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
-        mark("memset_cells", st);
+        if (!skip_cell_memset) {
+            ck(cudaMemsetAsync(cell_count.p, 0, ncells(cg) * sizeof(int), st), "memset cells");
+            mark("memset_cells", st);
+        }
+        cells_zero = false;
         if (stage_hx)  // graph path: inputs staged from host-mapped memory by the binning
             launch_stage_bin(n, stage_hx, stage_ht, const_cast<double*>(d_pos),
                              const_cast<int*>(d_types), cg, cell_count.as<int>(),
@@ -911,6 +919,7 @@ int enqueue_periodic(hmdp_ctx* ctx, int n, const double* d_xyz, const int* d_typ
         precision == HMDP_FP64
             ? ctx->network<double>(gr, slots, d_forces, d_per_atom, st, ctx->rev.as<int>(), mf)
             : ctx->network<float>(gr, slots, d_forces, d_per_atom, st, ctx->rev.as<int>(), mf);
+    ctx->cells_zero = true;  // the network's first kernel cleared them (MdFuse zeroing)
     return 2 + net;  // bin + search + network kernels (+ one memset node)
 }
 
@@ -1047,7 +1056,14 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
             std::memcpy(ctx->pin_in.p, xyz, 3 * n * sizeof(double));
             std::memcpy(static_cast<char*>(ctx->pin_in.p) + 3 * n * sizeof(double), types,
                         n * sizeof(int));
+            if (!ctx->cells_zero) {  // another operation left binned cells behind
+                const CellGrid cg = ctx->grid(box, ctx->model.rc, n);
+                ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
+                   "memset cells");
+            }
             ck(cudaGraphLaunch(ctx->cgraph.exec, st), "graph launch");
+            ctx->cells_zero = true;
+            ctx->cells_owner = nullptr;
             ck(cudaStreamSynchronize(st), "sync");
             const double* hp = static_cast<const double*>(ctx->pin.p);
             const unsigned bits = static_cast<unsigned>(hp[12]);
@@ -1092,6 +1108,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 // word straight into the host-mapped output block: no copy nodes
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+                    ctx->skip_cell_memset = true;  // cleared by this call's network
                     ctx->stage_hx = reinterpret_cast<const double*>(hin);
                     ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
                     ctx->out_override = hp;
@@ -1101,6 +1118,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     ctx->out_override = nullptr;
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
+                    ctx->skip_cell_memset = false;
                     const cudaError_t ce = cudaStreamEndCapture(st, &g);
                     if (ce == cudaSuccess && g) {
                         cudaGraphExec_t ex = nullptr;
@@ -1121,6 +1139,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     ctx->out_override = nullptr;
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
+                    ctx->skip_cell_memset = false;
                     cudaGraph_t gg = nullptr;
                     cudaStreamEndCapture(st, &gg);
                     if (gg) cudaGraphDestroy(gg);
@@ -1637,6 +1656,7 @@ void md_launch(hmdp_md* md, int steps) {
         const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
         ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
            "memset cells");
+        ctx->cells_zero = false;
         launch_cell_bin(md->n, md->x.as<double>(), cg, ctx->cell_count.as<int>(),
                         ctx->members.as<int>(), ctx->cell_of.as<int>(), ctx->err.as<unsigned>(), st);
     }
@@ -1646,6 +1666,7 @@ void md_launch(hmdp_md* md, int steps) {
         ck(cudaGraphLaunch(md_graph(md, chunk, st), st), "graph launch");
         md->primed = true;
         ctx->cells_owner = md;
+        ctx->cells_zero = false;  // the force kernel bins the next step's positions
         left -= chunk;
     }
 }
@@ -1975,6 +1996,7 @@ int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
                     const CellGrid cg = ctx->grid(g.box, ctx->model.rc, n);
                     ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
                        "memset cells");
+                    ctx->cells_zero = false;
                     launch_cell_bin(n, g.pos, cg, ctx->cell_count.as<int>(), ctx->members.as<int>(),
                                     ctx->cell_of.as<int>(), ctx->err.as<unsigned>(), st);
                     ck(cudaMemsetAsync(ctx->nnei.p, 0, n * sizeof(int), st), "memset nnei");

@@ -136,3 +136,41 @@ def test_caller_velocity_verlet_matches_device_md(prec, golden_models):
     assert np.abs(x - dx).max() < tol
     assert np.abs(v - dv).max() < 1e3 * tol
     assert e.value == pytest.approx(de, rel=1e-12 if prec == "fp64" else 1e-6)
+
+
+def test_cached_compute_graph_after_other_binning(golden_models):
+    """hmdp_compute's cached graph carries no cell-count memset (the network clears
+    the counts after the search); operations that leave binned cells behind (an MD
+    chunk, a neighbour-list build) must be followed by a clear before the replay."""
+    s = P.generate_synthetic_system(582)
+    m = P.model_from_json(golden_models["dpa3"])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp32)
+    ctx = P.Context(m)
+    for _ in range(3):  # direct path, capture, replay
+        out = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+        assert np.array_equal(out.forces, ref.forces)
+    md = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box,
+                  precision=P.Precision.fp32, steps_per_graph=2)
+    for _ in range(2):  # the first round may reallocate (graph re-captured), the second
+        md.run(4)       # replays the cached graph over the MD loop's binned cells
+        for _ in range(2):
+            out = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+            assert np.array_equal(out.forces, ref.forces) and out.energy == ref.energy
+    # a neighbour-list build on the same context bins without a network
+    import ctypes
+
+    from paper_2602_02234_b200._lib import check, lib, ptr
+
+    x = np.ascontiguousarray(s.positions)
+    box = np.ascontiguousarray(s.box, dtype=np.float64)
+    off = np.zeros(583, dtype=np.int32)
+    nbr = np.zeros(40000, dtype=np.int32)
+    dr = np.zeros((40000, 3))
+    ne = ctypes.c_int()
+    for _ in range(2):
+        check(lib().hmdp_build_neighbors(ctx.handle, 582, ptr(x), ptr(box), 0.6, 40000,
+                                         ptr(off), ptr(nbr), ptr(dr), ctypes.byref(ne)))
+        assert 0 < ne.value <= 40000
+        for _ in range(2):
+            out = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+            assert np.array_equal(out.forces, ref.forces) and out.energy == ref.energy
