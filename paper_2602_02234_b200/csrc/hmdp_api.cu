@@ -512,6 +512,7 @@ struct hmdp_ctx {
         }
     } cgraph;
     PinnedBuf pin_in;
+    DBuf cg_out;  // device output block of the hmdp_compute graph (copied D2H in-graph)
     // set while capturing hmdp_compute's graph: neighbors() stages these host-mapped
     // inputs into the device position / type arrays as it bins them
     const double* stage_hx = nullptr;
@@ -572,7 +573,7 @@ struct hmdp_ctx {
                         &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
                         &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1,
-                        &rf_envA, &rf_dua})
+                        &rf_envA, &rf_dua, &cg_out})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -1103,19 +1104,37 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 double* hp = static_cast<double*>(ctx->pin.p);
                 char* hin = static_cast<char*>(ctx->pin_in.p);
                 cudaGraph_t g = nullptr;
-                // inputs staged in by one kernel from host-mapped memory; the force
-                // kernel writes forces, per-atom energies, (E, W, W9) and the error
-                // word straight into the host-mapped output block: no copy nodes
+                // inputs staged in from host-mapped memory by the binning kernel; the
+                // force kernel writes forces, per-atom energies, (E, W, W9) and the
+                // error word straight into the host-mapped output block for small
+                // systems, and into one device block that a single D2H copy node
+                // moves for large ones: the copy node costs ~4 us flat, the force
+                // kernel's scattered 8-byte PCIe writes grow with n (measured per
+                // call: 582 atoms 60.7 vs 64.5 us, 4114 atoms 92 vs 85 us; crossover
+                // near 1900 atoms).  HMDP_CGRAPH_MAPPED_OUT=0/1 pins it for A/B.
+                static const int mapped_env = [] {
+                    const char* e = std::getenv("HMDP_CGRAPH_MAPPED_OUT");
+                    return e ? std::atoi(e) : -1;
+                }();
+                const bool mapped_out = mapped_env >= 0 ? mapped_env != 0 : n < 2048;
+                double* dst = hp;
+                if (!mapped_out) {
+                    ctx->cg_out.ensure(out_bytes);
+                    dst = ctx->cg_out.as<double>();
+                }
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
                     ctx->skip_cell_memset = true;  // cleared by this call's network
                     ctx->stage_hx = reinterpret_cast<const double*>(hin);
                     ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
-                    ctx->out_override = hp;
+                    ctx->out_override = dst;
                     const int launches =
                         enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
-                                         box, precision, hp + 16, hp + 16 + 3 * n, st);
+                                         box, precision, dst + 16, dst + 16 + 3 * n, st);
                     ctx->out_override = nullptr;
+                    if (!mapped_out)
+                        ck(cudaMemcpyAsync(hp, dst, out_bytes, cudaMemcpyDeviceToHost, st),
+                           "out D2H");
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
                     ctx->skip_cell_memset = false;

@@ -257,3 +257,22 @@ def test_sparse_rows_isolated_atom(mname, golden_models):
                     np.zeros((0, 3)))
     assert one.energy == pytest.approx(r1["energy"], rel=1e-12)
     assert np.abs(one.forces).max() == 0.0
+
+
+@pytest.mark.parametrize("n", [582, 2643])
+def test_cached_graph_replays_match_direct_path(n, golden_models):
+    """hmdp_compute's cached graph (second call captures, later calls replay; outputs
+    through host-mapped memory below 2048 atoms, a D2H copy node above) returns
+    exactly what the direct path returned, per-atom energies included."""
+    s = P.generate_synthetic_system(n)
+    m = model(golden_models, "dpa3")
+    ctx = P.Context(m)
+    first = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32, per_atom=True)
+    for _ in range(4):
+        out = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32, per_atom=True)
+        assert out.energy == first.energy and out.virial == first.virial
+        assert np.array_equal(out.forces, first.forces)
+        assert np.array_equal(out.per_atom_energy, first.per_atom_energy)
+        assert np.array_equal(out.virial_tensor, first.virial_tensor)
+    ref = O.evaluate(json.loads(golden_models["dpa3"]), s.types, *O.neighbors(s.positions, s.box, 0.6))
+    assert_close(out, ref, "fp32", f"graph replay {n}")
