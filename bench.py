@@ -785,9 +785,12 @@ def main():
 
             local_rank = local_rank % max(1, torch.cuda.device_count())
     try:
-        if world > 1 and args.mode == "dd":
+        # the DeePMD-style families have no domain decomposition: their
+        # N > 1 line is N independent replicas
+        dd_ok = args.model in ("dpa2", "dpa3")
+        if world > 1 and args.mode == "dd" and dd_ok:
             run_gdd(args, rank, world, local_rank, dist)
-        elif world > 1 and args.mode == "dd-host":
+        elif world > 1 and args.mode == "dd-host" and dd_ok:
             run_dd(args, rank, world, local_rank, dist)
         else:
             run_ours(args, rank, world, local_rank, dist)
