@@ -1,6 +1,6 @@
 """Long NVE run on the device MD loop: total-energy drift of the DPA2 / DPA3 analogs
 in FP32 and FP64 (velocity Verlet, dt = 1 fs, neighbour list rebuilt every step).
-usage: python tools/nve_drift.py [dpa3|dpa2] [steps] [fp32|fp64]"""
+usage: python tools/nve_drift.py [dpa3|dpa2|se_a|repformer|repflow] [steps] [fp32|fp64]"""
 import json
 import os
 import sys
@@ -15,8 +15,12 @@ from paper_2602_02234_b200.md import DeviceMD
 name = sys.argv[1] if len(sys.argv) > 1 else "dpa3"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
 prec = P.Precision[sys.argv[3] if len(sys.argv) > 3 else "fp32"]
-fam, depth = {"dpa3": (1, 3), "dpa2": (0, 1)}[name]
-m = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
+fam, depth = {"dpa3": (1, 3), "dpa2": (0, 1), "se_a": (2, 1), "repformer": (3, 3),
+              "repflow": (4, 3)}[name]
+if fam >= 2:  # DeePMD-style families
+    m = P.make_dp_model(P.ModelFamily(fam), depth)
+else:
+    m = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1)
 s = P.generate_synthetic_system(582, temperature=300.0)
 md = DeviceMD(P.Context(m), s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
               steps_per_graph=100)
