@@ -81,7 +81,6 @@ constexpr int kForceCTA = 128;  // small CTAs: every SM gets atoms in small syst
 // edges per unrolled batch (row loads in flight per lane; fewer for FP64 registers)
 template <typename T>
 constexpr int kU = sizeof(T) == 4 ? 8 : 4;
-constexpr int kInMsg = kH + kK;
 
 // Staged matrices: rows padded by 16 bytes (row stride in elements).
 template <typename T>
