@@ -151,6 +151,11 @@ struct DBuf {
         bytes = 0;
         const size_t want = std::max<size_t>(need, 256);
         ck(cudaMalloc(&p, want), "cudaMalloc");
+        // zero once: the batched row prefetches read slots past an atom's last
+        // neighbour (values discarded); zeroed memory keeps compute-sanitizer's
+        // initcheck clean.  Allocation is setup / growth only, never in a hot loop.
+        ck(cudaMemset(p, 0, want), "cudaMemset");
+        ck(cudaDeviceSynchronize(), "sync");
         bytes = want;
     }
     void release() {
