@@ -1,5 +1,6 @@
 """Small workload for compute-sanitizer: every family once through hmdp_compute (FP32 and
-FP64; direct path, graph capture, replay), a few device MD steps, a device-DD evaluation."""
+FP64; direct path, graph capture, replay), a few device MD steps, a device-DD evaluation,
+hybrid device MD (classical force field + DP group)."""
 import os
 import sys
 
@@ -32,3 +33,27 @@ for e in engs:
     e.load(s.positions)
 run_local(engs)
 print("dd", engs[0].result()[0])
+
+# classical force field + hybrid device MD (DP on the protein group)
+import oracle as O  # noqa: E402  (topology fixture only)
+from paper_2602_02234_b200.ff import ClassicalFF, HybridMD  # noqa: E402
+from paper_2602_02234_b200.hybrid import plan_group_preprocessing, synthetic_topology  # noqa: E402
+
+n = 582
+sh = P.generate_synthetic_system(n, temperature=300.0)
+t = O.ref_synthetic_topology(n)
+topo2, plan = plan_group_preprocessing(synthetic_topology(n), "protein")
+eo = np.zeros(n + 1, dtype=np.int32)
+ex = []
+for i in range(n):
+    ex += topo2.exclusions[i]
+    eo[i + 1] = len(ex)
+kept = set(map(tuple, topo2.bonds))
+kb = [k for k, b in enumerate(map(tuple, t["bonds"])) if b in kept]
+ff = ClassicalFF(sh.types, t["charges"], O.LJ_SIGMA, O.LJ_EPS, eo, np.array(ex), t["bonds"][kb],
+                 t["bond_params"][kb], coulomb_scheme=1)
+hm = HybridMD(P.Context(models[1], max_atoms=n), ff, plan.atoms, sh.positions, sh.velocities,
+              sh.masses, sh.types, sh.box, dt_ps=0.001, precision=P.Precision.fp32,
+              steps_per_graph=2)
+hm.run(4)
+print("hybrid", hm.state()[3])
