@@ -597,7 +597,9 @@ def run_gdd(args, rank, world, local_rank, dist):
     dist.barrier()
     t_ms = e0.elapsed_time(e1)
     ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    bufs = [eng.p, eng.p, eng.sg, eng.sg, eng.fo][: 2 * (model.depth() - 1) + 1]
+    # same sizes as the step's collectives, on scratch copies (the engine's state stays intact)
+    M = model.depth() - 1  # P^l forward rounds, halo-sum backward rounds, then forces + (E, W)
+    bufs = [b.clone() for b in [eng.p] * M + [eng.sg] * M + [eng.fo]]
     ca.record(stream)
     for _ in range(20):
         for b in bufs:
