@@ -276,3 +276,25 @@ def test_cached_graph_replays_match_direct_path(n, golden_models):
         assert np.array_equal(out.virial_tensor, first.virial_tensor)
     ref = O.evaluate(json.loads(golden_models["dpa3"]), s.types, *O.neighbors(s.positions, s.box, 0.6))
     assert_close(out, ref, "fp32", f"graph replay {n}")
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_random_models_and_systems(case):
+    """Random model seeds and systems (tools/parity_sweep.py runs hundreds): FP64 to the
+    oracle's precision; FP32 forces <= 1e-4 of the RMS force and the energy <= 1e-6 of
+    sum |e_i| (random models can make |E| small by cancellation)."""
+    rng = np.random.default_rng(100 + case)
+    fam, depth = [(0, 1), (1, 3)][case % 2]
+    n = int(rng.integers(100, 800))
+    s = P.generate_synthetic_system(n, seed=int(rng.integers(1, 10_000)))
+    m = P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, int(rng.integers(1, 1000)))
+    ref = O.evaluate(json.loads(m.to_json()), s.types, *O.neighbors(s.positions, s.box, 0.6))
+    ctx = P.Context(m, max_atoms=n)
+    scale_f = rms(ref["forces"])
+    scale_e = float(np.abs(ref["per_atom"]).sum())
+    o64 = ctx.compute(s.positions, s.types, s.box, P.Precision.fp64)
+    assert abs(o64.energy - ref["energy"]) <= 1e-12 * scale_e
+    assert np.abs(o64.forces - ref["forces"]).max() <= 1e-10 * scale_f
+    o32 = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+    assert abs(o32.energy - ref["energy"]) <= 1e-6 * scale_e
+    assert np.abs(o32.forces - ref["forces"]).max() <= F_TOL * scale_f
