@@ -33,6 +33,10 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.exists("/root/reference/proj/src/nn/inference.cpp"):
         targets += ["ref", "dropin"]
+        # the exact-signature drop-in program needs the product's libhalomd_nn_b200.so
+        lib = os.path.join(os.path.dirname(HERE), "paper_2602_02234_b200", "lib", "libhalomd_nn_b200.so")
+        if os.path.exists(lib):
+            targets.append("dropin_exact")
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
@@ -279,6 +283,17 @@ def ref_evaluate_csr(model: RefModel, pos, types, offset, nbr, dr, is_ghost=None
         raise OracleError(code, L.ref_last_error().decode())
     return dict(energy=e.value, per_atom=pa, forces=f, virial=w.value, flops=fl.value,
                 act_bytes=ab.value)
+
+
+def ref_descriptors(model: RefModel, pos, types, offset, nbr, dr, nd=16):
+    x = np.ascontiguousarray(pos, dtype=np.float64)
+    t = np.ascontiguousarray(types, dtype=np.int32)
+    out = np.zeros((t.shape[0], nd))
+    _rcheck(ref().ref_descriptors(model.h, t.shape[0], _p(x), _p(t),
+                                  _p(np.ascontiguousarray(offset, dtype=np.int32)),
+                                  _p(np.ascontiguousarray(nbr, dtype=np.int32)),
+                                  _p(np.ascontiguousarray(dr, dtype=np.float64)), _p(out)))
+    return out
 
 
 def ref_bench(model: RefModel, pos, types, box, prec="fp32", steps=1, threads=1) -> float:

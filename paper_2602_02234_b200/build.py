@@ -45,10 +45,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.abspath(__file__))
     if not force and not _stale(LIB, deps):
         _build_caller(force)
+        _build_dropin(force)
         return LIB
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
     common += os.environ.get("HMDP_NVCC_DEFS", "").split()  # tuning experiments, e.g. -DX=2
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".", "_") + ".o")
         cmd = [nvcc(), *common, *ARCH, "-lineinfo", "-c", os.path.join(CSRC, src), "-o", obj]
@@ -56,18 +58,47 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd += ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units compile independently: run them side by side
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c, capture_output=not verbose), cmds)):
+            if r.returncode:
+                sys.stderr.write((r.stderr or b"").decode(errors="replace"))
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     tmp = LIB + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
     _build_caller(True)
+    _build_dropin(True)
     return LIB
 
 
 CALLER = os.path.join(LIBDIR, "libhmdp_caller.so")
+DROPIN = os.path.join(LIBDIR, "libhalomd_nn_b200.so")
+REF_INCLUDE = os.environ.get("HMDP_REF_INCLUDE", "/root/reference/proj/include")
+
+
+def _build_dropin(force: bool) -> None:
+    """libhalomd_nn_b200.so: halomd::nn::{build_input_periodic, evaluate, descriptors,
+    switch_value, switch_derivative, NnInput::check/n_owned} with the reference's exact
+    signatures (csrc/halomd_nn_b200.cpp), compiled against the reference's own headers.
+    Built only where the reference tree exists (this container); the .so travels to
+    the GPU box with the snapshot."""
+    src = os.path.join(CSRC, "halomd_nn_b200.cpp")
+    if not os.path.exists(os.path.join(REF_INCLUDE, "halomd", "nn", "inference.hpp")):
+        return
+    if not force and not _stale(DROPIN, [src, LIB, os.path.join(ROOT, "include", "hmdp.h")]):
+        return
+    tmp = DROPIN + ".tmp"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-include", "stdexcept",
+                    "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"), src, "-o", tmp,
+                    "-L", LIBDIR, "-lhmdp", "-Wl,-rpath,$ORIGIN"], check=True)
+    os.replace(tmp, DROPIN)
 
 
 def _build_caller(force: bool) -> None:

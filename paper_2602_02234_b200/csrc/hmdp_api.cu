@@ -16,6 +16,8 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <vector>
 
@@ -113,6 +115,13 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(HMDP_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Synchronous copy on a context's (non-blocking) stream: ordered after that stream's
+// kernels, and never on the legacy default stream.
+cudaError_t copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+}
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -140,11 +149,35 @@ int guarded(F&& f) {
 // (contexts on other threads bump it too: at worst a spurious re-capture), atomic.
 std::atomic<unsigned long long> g_alloc_gen{0};
 
+// Graph capture vs device (re)allocation.  cudaFree synchronises the device, which
+// is illegal while ANY stream of the device is capturing, whatever the capture mode
+// -- so one context growing its buffers while another context (on another thread)
+// captures its step graph invalidated that capture.  Captures hold this lock shared
+// (any number run concurrently); allocation and release hold it exclusively.
+// t_capturing guards against self-deadlock: allocating inside one's own capture is
+// a bug (cudaMalloc is not capturable) and fails loudly instead.
+std::shared_mutex g_capture_mu;
+thread_local int t_capturing = 0;
+
+struct CaptureGuard {
+    std::shared_lock<std::shared_mutex> lk;
+    CaptureGuard() : lk(g_capture_mu) { ++t_capturing; }
+    ~CaptureGuard() { --t_capturing; }
+    CaptureGuard(const CaptureGuard&) = delete;
+    CaptureGuard& operator=(const CaptureGuard&) = delete;
+};
+
+std::unique_lock<std::shared_mutex> alloc_lock() {
+    if (t_capturing) fail(HMDP_CUDA_ERROR, "internal error: device allocation during graph capture");
+    return std::unique_lock<std::shared_mutex>(g_capture_mu);
+}
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
     void ensure(size_t need) {
         if (need <= bytes) return;
+        auto lk = alloc_lock();
         ++g_alloc_gen;
         if (p) cudaFree(p);
         p = nullptr;
@@ -154,12 +187,15 @@ struct DBuf {
         // zero once: the batched row prefetches read slots past an atom's last
         // neighbour (values discarded); zeroed memory keeps compute-sanitizer's
         // initcheck clean.  Allocation is setup / growth only, never in a hot loop.
-        ck(cudaMemset(p, 0, want), "cudaMemset");
-        ck(cudaDeviceSynchronize(), "sync");
+        // Zeroed on this thread's own stream (no device-wide sync, no legacy stream).
+        ck(cudaMemsetAsync(p, 0, want, cudaStreamPerThread), "cudaMemsetAsync");
+        ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
         bytes = want;
     }
-    void release() {
-        if (p) cudaFree(p);
+    void release() {  // no capture check: runs in destructors
+        if (!p) return;
+        std::unique_lock<std::shared_mutex> lk(g_capture_mu);
+        cudaFree(p);
         p = nullptr;
         bytes = 0;
     }
@@ -174,6 +210,7 @@ struct PinnedBuf {
     size_t bytes = 0;
     void ensure(size_t need) {
         if (need <= bytes) return;
+        auto lk = alloc_lock();
         ++g_alloc_gen;
         if (p) cudaFreeHost(p);
         p = nullptr;
@@ -183,7 +220,9 @@ struct PinnedBuf {
         bytes = std::max<size_t>(need, 4096);
     }
     void release() {
-        if (p) cudaFreeHost(p);
+        if (!p) return;
+        std::unique_lock<std::shared_mutex> lk(g_capture_mu);
+        cudaFreeHost(p);
         p = nullptr;
         bytes = 0;
     }
@@ -523,6 +562,10 @@ struct hmdp_ctx {
     const double* stage_hx = nullptr;
     const int* stage_ht = nullptr;
     int last_launches = 0;
+    // set while a device MD loop enqueues its steps: the force kernel's per-CTA
+    // (E, W, W9) partials go to the loop's own block, so another operation on this
+    // context cannot overwrite the energy hmdp_md_get reports
+    double* partial_override = nullptr;
     cudaStream_t user_stream = nullptr;  // hmdp_set_stream; NULL = own stream
     // per-kernel timing (hmdp_profile): event k is recorded after kernel k
     bool prof = false;
@@ -669,7 +712,7 @@ struct hmdp_ctx {
         w.dhown = dhown.as<T>();
         w.e_atom = e_atom.as<double>();
         w.forces = forces.as<double>();
-        w.partial = partial.as<double>();
+        w.partial = partial_override ? partial_override : partial.as<double>();
         w.ticket = ticket.as<unsigned>();
         w.out = out.as<double>();
         w.slots = static_cast<long long>(s);
@@ -824,13 +867,15 @@ struct hmdp_ctx {
 
     // hmdp_compute's graph path: (E, W, W9, err) to this host-mapped block instead of `out`
     double* out_override = nullptr;
+    // hybrid MD: the DP branch's (E, W, W9) to the hybrid's own block (no error export)
+    double* energy_out = nullptr;
 
     template <typename T>
     int network(const DevGraph& gr, long long slots, double* d_forces, double* d_per_atom,
                 cudaStream_t st, int* d_rev, const MdFuse& mf) {
         DevWork<T> w = work<T>(gr.n, slots);
         w.export_err = out_override != nullptr;
-        double* const o = out_override ? out_override : out.as<double>();
+        double* const o = out_override ? out_override : energy_out ? energy_out : out.as<double>();
         if (model.is_dp()) {
             const DevDpWork<T> d = dp_work<T>(gr.n, slots, w);
             if constexpr (sizeof(T) == 4)
@@ -879,16 +924,22 @@ struct hmdp_md {
     int n = 0;
     int precision = HMDP_FP32;
     double dt = 0.001, box[3] = {0, 0, 0};
-    DBuf x, v, f, m, types, energy;
+    DBuf x, v, f, m, types, energy;  // energy: [16] (E, W, W9) of the last evaluated step
+    DBuf partial;         // this loop's force-kernel CTA partials (hmdp_ctx::partial_override)
     DBuf xs, vs;          // completed-step snapshot (what hmdp_md_get returns)
     bool primed = false;  // working (x, v) already carry the next step's opening kick
     int steps_per_graph = 1;
     std::map<int, cudaGraphExec_t> graphs;
+    // what the cached graphs baked in: the stream, profiling marks, the context's
+    // capacities and the process-wide allocation generation (any re-allocation of a
+    // context buffer may have moved what the graphs address)
     cudaStream_t graph_stream = nullptr;
     bool graph_prof = false;
+    unsigned long long graph_gen = 0;
+    int graph_cap = 0, graph_ccap = 0;
     ~hmdp_md() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-        for (DBuf* b : {&x, &v, &f, &m, &types, &energy, &xs, &vs}) b->release();
+        for (DBuf* b : {&x, &v, &f, &m, &types, &energy, &partial, &xs, &vs}) b->release();
     }
 };
 
@@ -1127,6 +1178,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     ctx->cg_out.ensure(out_bytes);
                     dst = ctx->cg_out.as<double>();
                 }
+                CaptureGuard cguard;
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
                     ctx->skip_cell_memset = true;  // cleared by this call's network
@@ -1342,10 +1394,10 @@ int hmdp_compute_csr(hmdp_ctx* ctx, int n, const int* types, const unsigned char
         auto fetch = [&](const DBuf& b, size_t count, std::vector<double>& dst) {
             dst.resize(count);
             if (f64) {
-                ck(cudaMemcpy(dst.data(), b.p, count * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+                ck(copy_sync(dst.data(), b.p, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
             } else {
                 std::vector<float> tmp(count);
-                ck(cudaMemcpy(tmp.data(), b.p, count * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+                ck(copy_sync(tmp.data(), b.p, count * sizeof(float), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
                 for (size_t q = 0; q < count; ++q) dst[q] = tmp[q];
             }
         };
@@ -1395,12 +1447,12 @@ int hmdp_build_neighbors(hmdp_ctx* ctx, int n, const double* xyz, const double* 
         // restore the zero-cell-count invariant (no network kernel ran to clear them)
         ck(cudaMemsetAsync(ctx->cell_count.p, 0, ctx->cell_count.bytes, st), "memset cells");
         std::vector<int> cnt(n);
-        ck(cudaMemcpy(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        ck(copy_sync(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
         const size_t slots = static_cast<size_t>(n) * ctx->cap;
         std::vector<int> enbr(slots);
         std::vector<double> edr(slots * 3);
-        ck(cudaMemcpy(enbr.data(), ctx->nbr.p, slots * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
-        ck(cudaMemcpy(edr.data(), ctx->dr.p, slots * 3 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        ck(copy_sync(enbr.data(), ctx->nbr.p, slots * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
+        ck(copy_sync(edr.data(), ctx->dr.p, slots * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
         offset[0] = 0;
         for (int i = 0; i < n; ++i) offset[i + 1] = offset[i] + cnt[i];
         *n_edges = offset[n];
@@ -1570,6 +1622,11 @@ void md_enqueue_steps(hmdp_md* md, int steps, bool primed, cudaStream_t st) {
     const DevGraph gr = ctx->periodic_graph(md->n, md->types.as<int>());
     const long long slots = static_cast<long long>(md->n) * ctx->cap;
     mf.mode = 2;
+    struct PartialScope {  // the loop's own CTA-partials block while its steps enqueue
+        hmdp_ctx* c;
+        PartialScope(hmdp_ctx* c_, double* p) : c(c_) { c->partial_override = p; }
+        ~PartialScope() { c->partial_override = nullptr; }
+    } pscope(ctx, md->partial.as<double>());
     for (int s = 0; s < steps; ++s) {
         ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st, md->types.as<int>());
         if (md->precision == HMDP_FP64)
@@ -1603,7 +1660,8 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         md->f.ensure(3 * n * sizeof(double));
         md->m.ensure(n * sizeof(double));
         md->types.ensure(n * sizeof(int));
-        md->energy.ensure(sizeof(double));
+        md->energy.ensure(16 * sizeof(double));
+        md->partial.ensure(std::max<size_t>(n, 4096) * 16 * sizeof(double));
         md->xs.ensure(3 * n * sizeof(double));
         md->vs.ensure(3 * n * sizeof(double));
         cudaStream_t st = ctx->st();
@@ -1616,7 +1674,8 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         for (int attempt = 0; attempt < 8; ++attempt) {
             enqueue_periodic(ctx, n, md->x.as<double>(), md->types.as<int>(), box, precision,
                              md->f.as<double>(), nullptr, st);
-            ck(cudaMemcpyAsync(md->energy.p, ctx->out.p, sizeof(double), cudaMemcpyDeviceToDevice, st),
+            ck(cudaMemcpyAsync(md->energy.p, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToDevice,
+                               st),
                "D2D");
             const unsigned bits = ctx->take_err();
             if (bits & (kErrNbrOverflow | kErrCellOverflow)) {
@@ -1628,7 +1687,7 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
         }
         // headroom: degree fluctuates during dynamics; ELL capacity >= 1.5x current max
         std::vector<int> cnt(n);
-        ck(cudaMemcpy(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+        ck(copy_sync(cnt.data(), ctx->nnei.p, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
         const int maxdeg = *std::max_element(cnt.begin(), cnt.end());
         const int want = std::min(256, std::max(ctx->cap, (3 * maxdeg / 2 + 7) / 8 * 8));
         if (want > ctx->cap) ctx->cap = want;
@@ -1651,19 +1710,35 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
 namespace {
 cudaGraphExec_t md_graph(hmdp_md* md, int chunk, cudaStream_t st) {
     const int key = 2 * chunk + (md->primed ? 1 : 0);
+    const hmdp_ctx* ctx = md->ctx;
+    const bool valid = md->graph_stream == st && md->graph_prof == ctx->prof &&
+                       md->graph_gen == g_alloc_gen.load() && md->graph_cap == ctx->cap &&
+                       md->graph_ccap == ctx->ccap;
     auto it = md->graphs.find(key);
-    if (it != md->graphs.end() && md->graph_stream == st && md->graph_prof == md->ctx->prof)
-        return it->second;
-    if (md->graph_stream != st || md->graph_prof != md->ctx->prof) {
+    if (it != md->graphs.end() && valid) return it->second;
+    if (!valid) {
         for (auto& kv : md->graphs) cudaGraphExecDestroy(kv.second);
         md->graphs.clear();
         md->graph_stream = st;
-        md->graph_prof = md->ctx->prof;
+        md->graph_prof = ctx->prof;
+        md->graph_gen = g_alloc_gen.load();
+        md->graph_cap = ctx->cap;
+        md->graph_ccap = ctx->ccap;
     }
-    cudaGraph_t graph;
-    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-    md_enqueue_steps(md, chunk, md->primed, st);
-    ck(cudaStreamEndCapture(st, &graph), "end capture");
+    cudaGraph_t graph = nullptr;
+    {
+        CaptureGuard cguard;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            md_enqueue_steps(md, chunk, md->primed, st);
+        } catch (...) {
+            cudaGraph_t gg = nullptr;
+            cudaStreamEndCapture(st, &gg);
+            if (gg) cudaGraphDestroy(gg);
+            throw;
+        }
+        ck(cudaStreamEndCapture(st, &graph), "end capture");
+    }
     cudaGraphExec_t exec;
     ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
     cudaGraphDestroy(graph);
@@ -1721,16 +1796,17 @@ int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* e
         if (vel) ck(cudaMemcpyAsync(vel, md->vs.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         if (forces) ck(cudaMemcpyAsync(forces, md->f.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         if (epot) {
-            // (E, W) of the last step: the force kernel leaves per-CTA partials in MD
+            // (E, W) of the last step: the force kernel leaves per-CTA partials in
+            // this loop's own block in MD (before the first step: the create energy)
             if (md->primed) {
-                launch_reduce_partials(md->ctx->partial.as<double>(), md->n,
-                                       md->ctx->out.as<double>(), st);
+                launch_reduce_partials(md->partial.as<double>(), md->n, md->energy.as<double>(), st);
                 ck(cudaGetLastError(), "reduce launch");
             }
-            ck(cudaMemcpyAsync(epot, md->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st),
-               "D2H");
+            ck(cudaMemcpyAsync(epot, md->energy.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         }
         ck(cudaStreamSynchronize(st), "sync");
+        // errors latched by hmdp_md_enqueue'd steps (include/hmdp.h)
+        hmdp_ctx::raise_bits(md->ctx->take_err());
     });
 }
 
@@ -1910,7 +1986,7 @@ int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* viria
         set_device(ctx);
         hmdp_ctx::raise_bits(ctx->take_err());
         double h[16];
-        ck(cudaMemcpy(h, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        ck(copy_sync(h, ctx->out.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
         if (energy) *energy = h[0];
         if (virial) *virial = h[1];
         if (virial9) std::memcpy(virial9, h + 2, 9 * sizeof(double));
@@ -2201,8 +2277,8 @@ int hmdp_ff_create(int device, int n, const int* types, const double* charges, i
         pushd(dihedral_params, 3 * static_cast<size_t>(n_dihedrals));
         ff->buf_i.ensure(ivec.size() * sizeof(int));
         ff->buf_d.ensure(dvec.size() * sizeof(double));
-        ck(cudaMemcpy(ff->buf_i.p, ivec.data(), ivec.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D");
-        ck(cudaMemcpy(ff->buf_d.p, dvec.data(), dvec.size() * sizeof(double), cudaMemcpyHostToDevice),
+        ck(copy_sync(ff->buf_i.p, ivec.data(), ivec.size() * sizeof(int), cudaMemcpyHostToDevice, ff->geo->st()), "H2D");
+        ck(copy_sync(ff->buf_d.p, dvec.data(), dvec.size() * sizeof(double), cudaMemcpyHostToDevice, ff->geo->st()),
            "H2D");
         const int* bi = ff->buf_i.as<int>();
         const double* bd = ff->buf_d.as<double>();
@@ -2280,9 +2356,9 @@ int hmdp_ff_compute(hmdp_ff* ff, const double* xyz, const double* box, int preci
             hmdp_ctx::raise_bits(bits);
             double h[8];
             int c = 0;
-            ck(cudaMemcpy(h, ff->out.p, 4 * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
-            ck(cudaMemcpy(&c, ff->coll.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
-            ck(cudaMemcpy(forces, ff->F.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            ck(copy_sync(h, ff->out.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(copy_sync(&c, ff->coll.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(copy_sync(forces, ff->F.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
             energies[0] = h[0];
             energies[1] = h[1];
             energies[2] = h[2];
@@ -2309,15 +2385,18 @@ struct hmdp_hmd {
     int n = 0, ng = 0, precision = HMDP_FP64, steps_per_graph = 1;
     double dt = 0.001, box[3] = {0, 0, 0};
     DBuf x, v, m, types, grp, F;
+    DBuf enn;  // [16] (E, W, W9) of the DP branch's last evaluation
     std::map<int, cudaGraphExec_t> graphs;
     cudaStream_t gst = nullptr;
+    unsigned long long ggen = 0;  // allocation generation + capacities the graphs baked in
+    int gcap[4] = {0, 0, 0, 0};
     // the DP branch runs beside the classical branch (fork / join by events; inside
     // a captured graph the two become parallel branches)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~hmdp_hmd() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-        for (DBuf* b : {&x, &v, &m, &types, &grp, &F}) b->release();
+        for (DBuf* b : {&x, &v, &m, &types, &grp, &F, &enn}) b->release();
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
@@ -2339,8 +2418,15 @@ void hmd_forces(hmdp_hmd* h, cudaStream_t st) {
     ck(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "fork wait");
     launch_gather_group(h->ng, h->grp.as<int>(), h->x.as<double>(), h->types.as<int>(),
                         c->pos.as<double>(), c->types.as<int>(), h->side);
-    enqueue_periodic(c, h->ng, c->pos.as<double>(), c->types.as<int>(), h->box, h->precision,
-                     c->forces.as<double>(), nullptr, h->side);
+    c->energy_out = h->enn.as<double>();
+    try {
+        enqueue_periodic(c, h->ng, c->pos.as<double>(), c->types.as<int>(), h->box, h->precision,
+                         c->forces.as<double>(), nullptr, h->side);
+    } catch (...) {
+        c->energy_out = nullptr;
+        throw;
+    }
+    c->energy_out = nullptr;
     ck(cudaEventRecord(h->ev_join, h->side), "join");
     // classical branch (all atoms, SETs F) on the caller's stream
     g->neighbors(h->n, h->x.as<double>(), h->box, rcf, st, nullptr);
@@ -2397,6 +2483,7 @@ int hmdp_hybrid_create(hmdp_ctx* ctx, hmdp_ff* ff, int n, const int* group, int 
         h->types.ensure(n * sizeof(int));
         h->grp.ensure(n_group * sizeof(int));
         h->F.ensure(3 * n * sizeof(double));
+        h->enn.ensure(16 * sizeof(double));
         cudaStream_t st = ctx->st();
         ck(hmdp_set_stream(ff->geo, st) == HMDP_OK ? cudaSuccess : cudaErrorInvalidValue, "stream");
         ck(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "side stream");
@@ -2438,25 +2525,38 @@ int hmdp_hybrid_run(hmdp_hmd* h, int steps) {
         if (!h || steps < 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
         set_device(h->ctx);
         cudaStream_t st = h->ctx->st();
-        if (h->gst != st) {
+        const int caps[4] = {h->ctx->cap, h->ctx->ccap, h->ff->geo->cap, h->ff->geo->ccap};
+        if (h->gst != st || h->ggen != g_alloc_gen.load() || std::memcmp(caps, h->gcap, sizeof caps)) {
             for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
             h->graphs.clear();
             h->gst = st;
+            h->ggen = g_alloc_gen.load();
+            std::memcpy(h->gcap, caps, sizeof caps);
         }
         int left = steps;
         while (left > 0) {
             const int chunk = std::min(left, h->steps_per_graph);
             auto it = h->graphs.find(chunk);
             if (it == h->graphs.end()) {
-                cudaGraph_t gph;
-                ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-                for (int k = 0; k < chunk; ++k) {
-                    hmd_forces(h, st);
-                    launch_gdd_integrate(h->n, h->F.as<double>(), h->x.as<double>(),
-                                         h->v.as<double>(), h->m.as<double>(), h->dt, 0,
-                                         h->ctx->err.as<unsigned>(), st);
+                cudaGraph_t gph = nullptr;
+                {
+                    CaptureGuard cguard;
+                    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+                    try {
+                        for (int k = 0; k < chunk; ++k) {
+                            hmd_forces(h, st);
+                            launch_gdd_integrate(h->n, h->F.as<double>(), h->x.as<double>(),
+                                                 h->v.as<double>(), h->m.as<double>(), h->dt, 0,
+                                                 h->ctx->err.as<unsigned>(), st);
+                        }
+                    } catch (...) {
+                        cudaGraph_t gg = nullptr;
+                        cudaStreamEndCapture(st, &gg);
+                        if (gg) cudaGraphDestroy(gg);
+                        throw;
+                    }
+                    ck(cudaStreamEndCapture(st, &gph), "end capture");
                 }
-                ck(cudaStreamEndCapture(st, &gph), "end capture");
                 cudaGraphExec_t ex;
                 ck(cudaGraphInstantiate(&ex, gph, 0), "instantiate");
                 cudaGraphDestroy(gph);
@@ -2483,7 +2583,7 @@ int hmdp_hybrid_get(hmdp_hmd* h, double* xyz, double* vel, double* forces, doubl
         if (forces) ck(cudaMemcpyAsync(forces, h->F.p, b, cudaMemcpyDeviceToHost, st), "D2H");
         double e4[4] = {0, 0, 0, 0}, enn = 0.0;
         ck(cudaMemcpyAsync(e4, h->ff->out.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaMemcpyAsync(&enn, h->ctx->out.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(&enn, h->enn.p, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
         if (energies) {
             energies[0] = e4[0];

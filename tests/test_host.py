@@ -97,3 +97,23 @@ def test_replicate_box():
     r = P.replicate(s, (2, 1, 1))
     assert r.n_atoms == 128 and np.allclose(r.box, s.box * [2, 1, 1])
     assert np.array_equal(r.positions[64:], s.positions + [s.box[0], 0, 0])
+
+
+DROPIN = os.path.join(ROOT, "paper_2602_02234_b200", "lib", "libhalomd_nn_b200.so")
+REF_INFERENCE_O = os.path.join(ROOT, "oracle", "_ref", "obj", "nn_inference.o")
+
+
+@pytest.mark.skipif(not (os.path.exists(DROPIN) and os.path.exists(REF_INFERENCE_O)),
+                    reason="exact-signature drop-in is built only where the reference tree exists")
+def test_exact_dropin_exports_reference_symbols():
+    """libhalomd_nn_b200.so defines every public symbol the reference's inference.o
+    defines (same mangled names = same signatures; evaluate_with_weight_grads is the
+    undeclared training hook, not part of inference.hpp), so it links in its place."""
+    def defined(path, dynamic):
+        flag = "-D " if dynamic else ""
+        out = os.popen(f"nm {flag}--defined-only {path}").read()
+        return {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+
+    ref = {s for s in defined(REF_INFERENCE_O, False) if "weight_grads" not in s}
+    ours = defined(DROPIN, True)
+    assert len(ref) == 7 and ref <= ours, sorted(ref - ours)
