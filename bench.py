@@ -1,12 +1,14 @@
 #!/usr/bin/env python
 """bench.py — DP force-evaluation MD throughput on B200 (contract in the task brief).
 
-Workload (BASELINE.json configs[1]): DPA3 analog (make_model(message_passing, 3,
-0.6, 2, 8, 32, seed 1)) on the synthetic 1YRF-shaped protein-in-water box
-(582 atoms, generate_synthetic_system seed 7), velocity-Verlet MD at dt = 1 fs,
-neighbour list rebuilt every step (skin 0, as build_input_periodic), each step =
-kick+drift, cell-list neighbour search, full DP energy/force/virial evaluation,
-kick -- one CUDA graph per step.
+Workload (BASELINE.json configs[4], the north-star target box, the largest paper
+box): DPA3 analog (make_model(message_passing, 3, 0.6, 2, 8, 32, seed 1)) on the
+synthetic 2PTC-shaped protein-in-water box (4114 atoms, generate_synthetic_system
+seed 7), velocity-Verlet MD at dt = 1 fs, neighbour list rebuilt every step (skin 0,
+as build_input_periodic), each step = kick+drift, cell-list neighbour search, full
+DP energy/force/virial evaluation, kick -- one CUDA graph per step.  The DPA2 analog
+(embed_fit, depth 1) on the same box is measured the same way in the same run and
+reported under "models": {"dpa2": {...}} with its own roofline / e2e / cpu_baseline.
 
   value      steps/s over all ranks (N independent replica boxes = weak scaling),
              each timed step bracketed by CUDA events on the launching stream,
@@ -63,7 +65,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", choices=list(MODELS), default="dpa3")
-    ap.add_argument("--system", choices=list(SYSTEMS), default="1YRF")
+    ap.add_argument("--system", choices=list(SYSTEMS), default="2PTC")
+    ap.add_argument("--also", type=str, default="dpa2",
+                    help="further models measured on the same system, reported under "
+                         "\"models\" in the same JSON line ('' = none)")
     ap.add_argument("--replicas", type=str, default="1,1,1", help="periodic replication per rank")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -133,9 +138,10 @@ def kernel_flops(model_dict, n, n_owned, ne, m2=0):
     fu = [mlp_flops(l["update"]["sizes"]) for l in layers]
     out["embed"] = ne * (20 + 10 * K) + n * fe
     out["msg_fwd"] = sum(ne * fm[l] + n * fu[l] for l in range(M - 1)) / max(M - 1, 1)
-    out["msg_fwd_last"] = ne * fm[-1] + n * fu[-1] + 3 * n_owned * ff
     bwd = [ne * (2 * fm[l] + 6 * H + 3 * K) + n * (2 * fu[l] + 2 * H) for l in range(M)]
-    out["msg_bwd_top"] = bwd[-1]
+    # the LAST kernel runs the top layer forward, the fitting net (fwd + bwd) and the
+    # top layer's backward
+    out["msg_fwd_last"] = ne * fm[-1] + n * fu[-1] + 3 * n_owned * ff + bwd[-1]
     out["msg_bwd"] = sum(bwd[:-1]) / max(M - 1, 1)
     out["embed_bwd"] = 2 * n * fe
     return out
@@ -199,25 +205,50 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# Workload identity shared by both arms (the driver compares the config dicts)
+# ---------------------------------------------------------------------------
+def workload_config(args, model_name, world):
+    n = SYSTEMS[args.system]
+    reps = tuple(int(v) for v in args.replicas.split(","))
+    n_rep = reps[0] * reps[1] * reps[2]
+    return {"workload": f"{model_name.upper()} velocity-Verlet MD step on the {args.system}-shaped "
+                        f"box (dt 1 fs, neighbour list rebuilt every step, E+F+W every step)",
+            "model": model_name, "system": args.system, "atoms": n * n_rep,
+            "replicas_per_rank": list(reps), "precision": args.precision,
+            "parallelism": f"replicas x{world}"}
+
+
+def replicate_np(x, t, m, v, box, reps):
+    """Periodic replica box, numpy only (the reference arm must not load libhmdp)."""
+    import numpy as np
+
+    rx, ry, rz = reps
+    sh = np.array([(i, j, k) for k in range(rz) for j in range(ry) for i in range(rx)], float) * box
+    r = sh.shape[0]
+    return ((x[None] + sh[:, None]).reshape(-1, 3), np.tile(t, r), np.tile(m, r),
+            np.tile(v, (r, 1)), box * np.array(reps, float))
+
+
+# ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref): P concurrent replicas of the same MD workload
 # ---------------------------------------------------------------------------
 def reference_md(model_name, system, steps, warmup, precision, threads, replicas=(1, 1, 1)):
     import numpy as np
 
     import oracle as O
-    import paper_2602_02234_b200 as P
 
     fam, depth = MODELS[model_name]
-    s = P.generate_synthetic_system(SYSTEMS[system])
-    if tuple(replicas) != (1, 1, 1):
-        s = P.replicate(s, replicas)
     if fam >= 2:
         # no reference implementation exists for the DeePMD-style families: the
         # FP64 oracle (torch autograd on the host cores) is the CPU path
         import torch
 
+        import paper_2602_02234_b200 as P
         from oracle import dpfamily as DF
 
+        s = P.generate_synthetic_system(SYSTEMS[system])
+        if tuple(replicas) != (1, 1, 1):
+            s = P.replicate(s, replicas)
         torch.set_num_threads(threads)
         m = make_bench_model(P, model_name).as_dict()
         x, v = s.positions.copy(), s.velocities.copy()
@@ -235,28 +266,17 @@ def reference_md(model_name, system, steps, warmup, precision, threads, replicas
             v += f * (half / s.masses[:, None])
         wall = time.perf_counter() - t0
         return steps / wall, wall, "port"
+    # the reference's own generator and model (oracle/_ref): libhmdp is never loaded here
+    x, t, m, v, box = O.ref_synthetic(SYSTEMS[system])
+    if tuple(replicas) != (1, 1, 1):
+        x, t, m, v, box = replicate_np(x, t, m, v, box, replicas)
     if O.ref_available():
         rm = O.RefModel(O.ref_model_json(fam, depth))
-        kind = "reference"
         if warmup:
-            O.ref_md(rm, s.positions, s.velocities, s.types, s.masses, s.box, prec=precision,
-                     steps=warmup, threads=threads)
-        wall, x, v, ep = O.ref_md(rm, s.positions, s.velocities, s.types, s.masses, s.box,
-                                  prec=precision, steps=steps, threads=threads)
-        return steps * threads / wall, wall, kind
-    # fallback: the plain-C restatement, one thread (a scalar port)
-    m = json.loads(P.make_model(P.ModelFamily(fam), depth, 0.6, 2, 8, 32, 1).to_json())
-    x, v = s.positions.copy(), s.velocities.copy()
-    half, dt = 0.0005, 0.001
-    f = O.evaluate(m, s.types, *O.neighbors(x, s.box, 0.6), prec=precision)["forces"]
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        v += f * (half / s.masses[:, None])
-        x += v * dt
-        f = O.evaluate(m, s.types, *O.neighbors(x, s.box, 0.6), prec=precision)["forces"]
-        v += f * (half / s.masses[:, None])
-    wall = time.perf_counter() - t0
-    return steps / wall, wall, "port"
+            O.ref_md(rm, x, v, t, m, box, prec=precision, steps=warmup, threads=threads)
+        wall, _, _, _ = O.ref_md(rm, x, v, t, m, box, prec=precision, steps=steps, threads=threads)
+        return steps * threads / wall, wall, "reference"
+    raise SystemExit("reference arm needs oracle/_ref (built from /root/reference by build())")
 
 
 def cpu_count():
@@ -266,44 +286,65 @@ def cpu_count():
         return os.cpu_count() or 1
 
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
+def reference_line(args, model_name, world, budget_s):
     threads = cpu_count()
     # bounded sample: calibrate the per-step cost on a few steps, then time as many of
-    # the K requested steps as fit in ~60 s of wall (the whole run stays within minutes
-    # for any K; the rate, not the step count, is the measurement)
-    cal = min(args.steps, 5)
-    _, wall0, _ = reference_md(args.model, args.system, cal, 0, args.precision, threads)
-    timed = max(cal, min(args.steps, int(60.0 / max(wall0 / cal, 1e-6))))
-    sps, wall, kind = reference_md(args.model, args.system, timed, min(args.warmup, 5),
-                                   args.precision, threads)
-    n = SYSTEMS[args.system]
-    sample = (f"{args.model} {args.system} ({n} atoms) velocity-Verlet MD, {timed} timed "
-              f"steps per replica (of the {args.steps} requested; ~60 s cap) x {threads} "
+    # the K requested steps as fit in ~budget_s of wall (the whole run stays within
+    # minutes for any K; the rate, not the step count, is the measurement)
+    reps = tuple(int(v) for v in args.replicas.split(","))
+    cal = min(args.steps, 2)
+    _, wall0, _ = reference_md(model_name, args.system, cal, 0, args.precision, threads, reps)
+    timed = max(cal, min(args.steps, int(budget_s / max(wall0 / cal, 1e-6))))
+    sps, wall, kind = reference_md(model_name, args.system, timed, min(args.warmup, 1),
+                                   args.precision, threads, reps)
+    cfg = workload_config(args, model_name, world)
+    sample = (f"{model_name} {args.system} ({cfg['atoms']} atoms) velocity-Verlet MD, {timed} timed "
+              f"steps per replica (of the {args.steps} requested; ~{budget_s:.0f} s cap) x {threads} "
               f"concurrent replicas (one per host thread), {args.precision}")
-    line = {
+    return {
         "metric": METRIC, "value": sps, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / sps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
-        "config": {"workload": f"{args.model.upper()} MD step loop on {args.system}-shaped box",
-                   "model": args.model, "system": args.system, "atoms": n,
-                   "precision": args.precision},
+        "config": cfg,
         "impl": "reference",
         "ns_per_day": ns_per_day(sps),
         "cpu_baseline": {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": sps, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    line = reference_line(args, args.model, world, 45.0)
+    extra = [m for m in args.also.split(",") if m and m != args.model]
+    if extra:
+        line["models"] = {m: reference_line(args, m, world, 30.0) for m in extra}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank, dist):
+SHARES = os.path.join(ROOT, "profiles", "round2", "launch_shares.json")
+
+
+def ncu_shares(model_name, system):
+    """Per-kernel share of one MD step from the committed ncu launch list of this bench
+    workload (tools/launch_shares.py; serialised, so only the SHARES are used)."""
+    try:
+        return json.load(open(SHARES))[model_name][system]
+    except Exception:
+        return None
+
+
+def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with_cpu):
+    """One model on the bench system: the timed device MD loop (headline value), the
+    per-kernel roofline, the warm-L2 context figure, the host-buffer e2e leg and the
+    CPU baseline.  Returns the JSON fields of that model's line (rank 0)."""
     import ctypes
 
     import numpy as np
@@ -313,15 +354,10 @@ def run_ours(args, rank, world, local_rank, dist):
     from paper_2602_02234_b200._lib import check, lib, ptr
     from paper_2602_02234_b200.md import DeviceMD
 
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    # one explicit (non-default) stream carries everything: torch's L2 flush and
-    # CUDA events, and every libhmdp launch (hmdp_set_stream)
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
     L = lib()
     prec = P.Precision[args.precision]
-    model = make_bench_model(P, args.model)
+    model = make_bench_model(P, model_name)
     s = P.generate_synthetic_system(SYSTEMS[args.system])
     reps = tuple(int(v) for v in args.replicas.split(","))
     if reps != (1, 1, 1):
@@ -337,12 +373,10 @@ def run_ours(args, rank, world, local_rank, dist):
     per_step_kernels = ctx.kernels_per_eval() - 1
 
     sampler = ClockSampler(local_rank) if rank == 0 else None
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-
     md = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
                   steps_per_graph=1)
     enqueue = L.hmdp_md_enqueue
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 3)):
         check(enqueue(md.handle, 1))
     torch.cuda.synchronize(dev)
     check(L.hmdp_check(ctx.handle))
@@ -367,32 +401,37 @@ def run_ours(args, rank, world, local_rank, dist):
     wall = time.perf_counter() - wall0
     if dist:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    t_ms = float(sum(step_ms))
-    check(L.hmdp_check(ctx.handle))
+    t_ms = float(sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
+    check(L.hmdp_md_get(md.handle, None, None, None, None))  # latched device errors
     if dist:
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     value = world * K / (t_ms * 1e-3)
+    ms_step = t_ms / K
 
-    # ---- warm-L2 multi-step graph (context, not the headline) ----
+    # ---- warm-L2 multi-step graph (context, not the headline): 100 steps per graph
+    # launch, no flush; warmed up before timing so graph capture and clock ramp are
+    # outside the events ----
     md_warm = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
                        steps_per_graph=100)
-    check(enqueue(md_warm.handle, 100))
+    check(enqueue(md_warm.handle, 300))
+    torch.cuda.synchronize(dev)
+    KW = 2000
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    check(enqueue(md_warm.handle, 1000))
+    check(enqueue(md_warm.handle, KW))
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    warm_sps = 1000 / (e0.elapsed_time(e1) * 1e-3)
+    warm_sps = KW / (e0.elapsed_time(e1) * 1e-3)
     md_warm.close()
 
-    # ---- per-kernel timing (events inside the per-step graph) -> roofline ----
+    # ---- per-kernel event timing (an event node after every kernel inside the step
+    # graph: breaks the PDL overlap, so these are upper bounds on kernel time) ----
     check(L.hmdp_profile(ctx.handle, 1))
     md_prof = DeviceMD(ctx, s.positions, s.velocities, s.masses, s.types, s.box, 0.001, prec,
                        steps_per_graph=1)
-    KP = min(K, 200)
+    KP = min(K, 100)
     sums: dict[str, float] = {}
     counts: dict[str, int] = {}
     buf = (ctypes.c_float * 64)()
@@ -411,13 +450,19 @@ def run_ours(args, rank, world, local_rank, dist):
     md_prof.close()
     if sampler:
         clocks = sampler.stop()
-    kern_ms = {k: sums[k] / counts[k] for k in sums}
+    event_ms = {k: sums[k] / counts[k] for k in sums}
     kflops = kernel_flops(model.as_dict(), n, n, ne, m2)
-    # FLOP-carrying kernels; the dominant one is the slowest of them
+    # per-kernel duration inside the timed loop = its ncu share of the step x the live
+    # ms_per_step (PDL overlap intact); the event-timed durations are the fallback
+    shares = ncu_shares(model_name, args.system) if reps == (1, 1, 1) else None
+    if shares and all(k in shares for k in kflops if k in event_ms):
+        kern_ms = {k: shares[k] * ms_step for k in shares}
+        dur_src = (f"ncu launch-list share of the step ({os.path.relpath(SHARES, ROOT)}) x the "
+                   f"live ms_per_step")
+    else:
+        kern_ms = event_ms
+        dur_src = "CUDA events around every kernel in the step graph (PDL broken: upper bound)"
     cands = {k: v for k, v in kern_ms.items() if k in kflops}
-    # the slowest; kernels within 3 % of it count as tied (msg_fwd_last and msg_bwd run
-    # equally long at 1YRF) and the tie goes to the one carrying more FLOPs, so the
-    # reported kernel does not flip between runs
     tmax = max(cands.values())
     dom = max((k for k in cands if cands[k] >= 0.97 * tmax), key=lambda k: kflops[k])
     peak = ctypes.c_double()
@@ -426,16 +471,18 @@ def run_ours(args, rank, world, local_rank, dist):
     check(L.hmdp_peak_tf32x3(local_rank, 200, ctypes.byref(peak_tc)))
     achieved = kflops[dom] / (kern_ms[dom] * 1e-3) / 1e12
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tfile = os.path.join(ROOT, "profiles", "round2", "ncu_traffic.json")
+    if not os.path.exists(tfile):
+        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.model, {}).get(args.system, {}).get(dom)
+            traffic = json.load(open(tfile)).get(model_name, {}).get(args.system, {}).get(dom)
         except Exception:
             traffic = None
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(
-            os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as f:
+    mp = {}
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
         try:
-            mp = json.load(f)
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
             mp = {}
 
@@ -458,6 +505,7 @@ def run_ours(args, rank, world, local_rank, dist):
     vv_args = (prov_ctx.handle, ctypes.c_int(n), ptr(xh), ptr(vh), ptr(fh), ptr(th), ptr(bh),
                ptr(mh), ctypes.c_double(0.001), None, ctypes.c_int(int(prec)), ctypes.byref(eh))
     check(vv(*vv_args[:9], ctypes.c_int(5), *vv_args[10:]))  # warm-up (graph captured)
+    torch.cuda.synchronize(dev)
     e0.record(stream)
     check(vv(*vv_args[:9], ctypes.c_int(KE), *vv_args[10:]))
     e1.record(stream)
@@ -470,63 +518,89 @@ def run_ours(args, rank, world, local_rank, dist):
     e2e_value = world * KE / (e2e_ms * 1e-3)
     h2d = xh.nbytes + th.nbytes
     d2h = fh.nbytes + 11 * 8
+    prov_ctx.close()
+    md.close()
+    ctx.close()
 
     if rank != 0:
-        return
+        return None
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if with_cpu:
         threads = cpu_count()
         # bounded sample: ~cpu_seconds of wall on all host threads
         per_step = {"dpa3": 0.2, "dpa2": 0.012, "se_a": 0.03, "repformer": 0.06,
-                    "repflow": 0.06}[args.model]
+                    "repflow": 0.06}[model_name]
         per_step *= n / 582
         steps_cpu = max(2, int(args.cpu_seconds / per_step))
-        sps, cwall, kind = reference_md(args.model, args.system, steps_cpu, 1, args.precision,
+        sps, cwall, kind = reference_md(model_name, args.system, steps_cpu, 1, args.precision,
                                         threads, reps)
-        if MODELS[args.model][0] >= 2:
+        if MODELS[model_name][0] >= 2:
             sample = (f"{steps_cpu} MD steps of one {n}-atom box through the FP64 torch oracle "
                       f"(no reference implementation of this family), {threads} threads, "
                       f"{cwall:.1f} s wall")
         else:
             sample = (f"{steps_cpu} MD steps x {threads} concurrent replicas of the same "
-                      f"{n}-atom box, {args.precision}, {cwall:.1f} s wall")
+                      f"{n}-atom box (the reference compiled from its sources), "
+                      f"{args.precision}, {cwall:.1f} s wall")
         cpu = {"value": sps, "unit": "steps/s", "cores": threads, "kind": kind, "sample": sample}
 
-    line = {
+    return {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": t_ms / K, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
-        "config": {"workload": f"{args.model.upper()} MD step loop on {args.system}-shaped box "
-                               f"(graph per step, nbr rebuild every step)",
-                   "model": args.model, "system": args.system, "atoms": n, "edges": ne,
-                   "replicas_per_rank": list(reps), "precision": args.precision,
-                   "parallelism": f"replicas x{world}",
-                   "l2": "flushed (256 MiB write) before every timed step, outside the events"},
+        "config": workload_config(args, model_name, world),
+        "workload_detail": {"edges": ne, "graph": "one CUDA graph launch per MD step",
+                            "l2": "flushed (256 MiB write) before every timed step, outside "
+                                  "the events"},
         "ns_per_day": ns_per_day(value),
         "warm_l2_graph100": {"steps_per_s": warm_sps, "ns_per_day": ns_per_day(warm_sps),
-                             "note": "100 steps per graph, L2 not flushed, 1 rank"},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak.value,
+                             "note": f"{KW} steps in 100-step graphs after a 300-step warm-up, "
+                                     f"L2 not flushed, 1 rank"},
+        "roofline": {"bound": "fp32-simt", "achieved": achieved, "peak": peak.value,
                      "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
                      "kernel": dom, "flops_per_launch": kflops[dom],
-                     "mean_launch_us": kern_ms[dom] * 1e3,
-                     "peak_kind": "measured FP32 FFMA (SIMT) throughput, hmdp_peak_fp32; the "
-                                  "kernels run FP32 FMA, not tensor cores",
+                     "mean_launch_us": kern_ms[dom] * 1e3, "duration_source": dur_src,
+                     "peak_kind": "measured FP32 FFMA (SIMT) throughput on this GPU "
+                                  "(hmdp_peak_fp32): the parity-mode kernels run FP32 FMA",
                      "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None,
                      "peak_tf32x3_tflops": peak_tc.value,
                      "frac_per_kernel": {k: kflops[k] / (cands[k] * 1e-3) / 1e12 / peak.value
                                          for k in sorted(cands, key=lambda k: -cands[k])}},
         "kernels_us": {k: v * 1e3 for k, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},
+        "kernels_event_us": {k: v * 1e3 for k, v in sorted(event_ms.items(), key=lambda kv: -kv[1])},
         "gpu_launches": per_step_kernels * K,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "C++ caller: reference velocity_verlet_step on host arrays, force "
-                        "function = hmdp_compute (host xyz/types in, forces/E out)"},
+                "path": "C++ caller: velocity_verlet_step (integrators.cpp:32-47) on host arrays, "
+                        "force function = hmdp_compute (host xyz/types in, forces/E out)"},
         "cpu_baseline": cpu,
         "clocks": clocks if sampler else None,
         "wall_s_timed_region": wall,
     }
+
+
+def run_ours(args, rank, world, local_rank, dist):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # one explicit (non-default) stream carries everything: torch's L2 flush and
+    # CUDA events, and every libhmdp launch (hmdp_set_stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    with_cpu = world == 1 and not args.no_cpu_baseline
+    line = measure(args, args.model, rank, world, local_rank, dist, stream, flush, with_cpu)
+    extra = [m for m in args.also.split(",") if m and m != args.model]
+    models = {}
+    for m in extra:
+        models[m] = measure(args, m, rank, world, local_rank, dist, stream, flush, with_cpu)
+    if rank != 0:
+        return
+    if models:
+        line["models"] = models
     print(json.dumps(line), flush=True)
 
 

@@ -5,7 +5,9 @@ usage: python tools/profile_summary.py <tag> <launches.csv> <full.ncu-rep> [mode
 Writes
   profiles/<tag>/launches.md      per-kernel share of the step (ncu launch list)
   profiles/<tag>/kernels.md       key --set full metrics per kernel
-  profiles/ncu_traffic.json       DRAM bytes per launch per kernel (read by bench.py)
+  profiles/round2/ncu_traffic.json    DRAM bytes per launch per kernel (read by bench.py)
+  profiles/round2/launch_shares.json  per-kernel share of the MD step (read by bench.py:
+                                      kernel time = share x live ms_per_step)
 """
 import csv
 import io
@@ -123,7 +125,18 @@ def main():
             rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
             if rd is not None and wr is not None and profile_name(name):
                 traffic[profile_name(name)] = rd + wr
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    shares = {}
+    nl = max(1, min(len(v) for v in agg.values()))
+    for k, v in agg.items():
+        pn = profile_name(k)
+        if pn:
+            shares[pn] = shares.get(pn, 0.0) + sum(v) / tot
+    spath = os.path.join(ROOT, "profiles", "round2", "launch_shares.json")
+    os.makedirs(os.path.dirname(spath), exist_ok=True)
+    alls = json.load(open(spath)) if os.path.exists(spath) else {}
+    alls.setdefault(model, {})[system] = shares
+    json.dump(alls, open(spath, "w"), indent=1, sort_keys=True)
+    tpath = os.path.join(ROOT, "profiles", "round2", "ncu_traffic.json")
     allt = json.load(open(tpath)) if os.path.exists(tpath) else {}
     allt.setdefault(model, {})[system] = traffic
     json.dump(allt, open(tpath, "w"), indent=1, sort_keys=True)
