@@ -508,7 +508,7 @@ struct hmdp_ctx {
     DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev, ety, inv_pos;
     DBuf offset, in_start, in_cnt, cursor, in_edge;
     // network workspace
-    DBuf er, es, eds, eb, edb, g, grev, zb, db, pe, desc, ez1, h, uz1, dhown;
+    DBuf er, es, eds, eb, edb, g, grev, zb, db, pa, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // DeePMD-style families: vector edge gradients and the repformer workspace
     DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
@@ -615,7 +615,7 @@ struct hmdp_ctx {
         cudaSetDevice(device);
         for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
                         &nbr, &dr, &rev, &ety, &inv_pos, &offset, &in_start, &in_cnt, &cursor,
-                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pe, &desc,
+                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
                         &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
@@ -685,9 +685,9 @@ struct hmdp_ctx {
         g.ensure(s * sizeof(T));
         grev.ensure(s * sizeof(T));
         if (M > 0) {
-            zb.ensure(M * s * kH * sizeof(T));
+            zb.ensure(M * s * kH * sizeof(T));  // z_e of every layer (hmdp_net.cu kRecomputeZ)
             db.ensure(2 * s * kH * sizeof(T));
-            pe.ensure(2 * s * kH * sizeof(T));
+            pa.ensure(M * na * kH * sizeof(T));
         }
         desc.ensure(na * 32 * sizeof(T));
         ez1.ensure(na * kH * sizeof(T));
@@ -704,7 +704,7 @@ struct hmdp_ctx {
         w.grev = grev.as<T>();
         w.z = zb.as<T>();
         w.d = db.as<T>();
-        w.pe = pe.as<T>();
+        w.pa = pa.as<T>();
         w.desc = desc.as<T>();
         w.ez1 = ez1.as<T>();
         w.h = h.as<T>();
@@ -2121,7 +2121,7 @@ int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
                     break;
                 case 1:
                     launch_gdd_push_halo<T>(own, g.n_est, static_cast<const T*>(g.p_atom),
-                                            w.pe + (layer & 1) * slots * kH,
+                                            w.pa + static_cast<long long>(layer) * own.n * kH,
                                             g.lists.as<int>() + n, g.counts.as<int>() + 1, st);
                     g.launches += 1;
                     break;

@@ -100,9 +100,11 @@ struct DevWork {
     T* edb;   // [slot][8] b_k'
     T* g;     // dE/dr
     T* grev;  // [in-position] g of the edge mirrored there (pushed by its source)
-    T* z;     // [M][slot][32] message hidden (tanh) activations z_e
+    T* z;     // [slot][32] message hidden (tanh) activations z_e of the LAST layer (the
+              // lower layers recompute z_e in their backward from pa and b_e)
     T* d;     // [2][in-position][32] pushed adjoints dz_e (double-buffered by layer)
-    T* pe;    // [2][slot][32] pushed neighbour projections P_j = W1h h_j, per out-slot
+    T* pa;    // [M][n][32] per-atom neighbour projections P^l_i = W1h^l h^l_i, gathered
+              // by the edges' sources (nbr index); L2-resident at every paper size
     // domain decomposition (nullable otherwise)
     T* p_atom;    // [n][32] per-atom P of the layer just produced (sent to ghost copies)
     T* s_remote;  // [n][32] adjoint partial sums received from ghost copies elsewhere

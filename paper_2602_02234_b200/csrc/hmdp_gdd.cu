@@ -128,22 +128,18 @@ __global__ void k_gdd_zero_energy(int n, const unsigned char* __restrict__ role,
     if (i < n && role[i] != 1) e_atom[i] = 0.0;
 }
 
-// Halo atoms push the P rows received from their owners into their in-edge slots.
+// Halo atoms take the P rows received from their owners into the layer's per-atom
+// P rows (gathered by the owned sources' edges).
 template <typename T>
-__global__ void k_gdd_push_halo(DevGraph gr, const T* __restrict__ p_atom, T* __restrict__ pe,
+__global__ void k_gdd_push_halo(DevGraph gr, const T* __restrict__ p_atom, T* __restrict__ pa,
                                 const int* __restrict__ hlist, const int* __restrict__ hcount) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int nh = *hcount;
     for (int k = warp; k < nh; k += nw) {
-        const int i = hlist[k];
-        const T v = p_atom[static_cast<long long>(i) * kH + lane];
-        const int start = gr.row_start[i], cnt = gr.nnei[i];
-        for (int q = 0; q < cnt; ++q) {
-            const int m = gr.inv_pos[start + q];
-            if (m >= 0) pe[static_cast<long long>(m) * kH + lane] = v;
-        }
+        const long long i = hlist[k];
+        pa[i * kH + lane] = p_atom[i * kH + lane];
     }
 }
 

@@ -71,6 +71,12 @@ __device__ unsigned long long g_tprobe[32];
 #endif
 
 constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
+// Message layers: store every layer's z_e rows (false) or only the LAST layer's and
+// recompute z_e = tanh(W1b b_e + b1 + P^l_j) in the lower layers' backward (true:
+// a tanh + 8 FMAs per edge channel instead of a 128-byte row that spills to HBM at
+// 2PTC).  Measured on B200 (DPA3 2PTC, FP32): recompute made k_msg_bwd 31.7 -> 52.4
+// us (step 152 -> 177 us) -- the kernel is issue/latency-bound, not HBM-bound.
+constexpr bool kRecomputeZ = false;
 // Resident CTAs per SM the register budget is sized for: 2 (64 registers) for the
 // 1-warp teams of large systems — more atoms in flight; 1 (128 registers) for
 // the 2/4-warp teams of small systems, whose chains would spill at 64 (measured:
@@ -98,11 +104,12 @@ struct WarpSmem {
     alignas(16) T x[64];
     alignas(16) T y[64];
     alignas(16) T t[32];
-    alignas(16) T ed[32][12];  // staged edge scalars: (s, s', -, -, b or b'[8])
+    alignas(16) T ed[32][kRecomputeZ ? 20 : 12];  // edge scalars: (s, s', -, -, b or b'[8], [b[8]])
     alignas(16) T red[2][64];  // team-sum partials (double-buffered)
     T reds[2];
     int emir[32];  // staged mirror slots
     int ety[32];   // staged neighbour types
+    int enb[32];   // staged neighbour indices (P_j row gathers)
 };
 
 // Bump allocator over the dynamic shared memory: staged matrices, then the
@@ -336,23 +343,6 @@ __device__ __forceinline__ void twmv2(const T* W, const T* x, int row0, int row1
     }
 }
 
-// Push the per-lane value P (channel lane) into the rows dst[in_edge[..]] of
-// i's in-edges (the out-slots whose consumer reads P_i); slots split over the team.
-template <typename T, int G>
-__device__ __forceinline__ void push_rows(T* dst, T p, const DevGraph& gr, int i,
-                                          const Team<G>& tm) {
-    const int is = gr.in_start[i] + tm.w;
-    const int ic = tm.local(gr.in_cnt[i]);
-    for (int k0 = 0; k0 < ic; k0 += 32) {
-        const int kk = min(32, ic - k0);
-        const int idx = tm.lane < kk ? gr.in_edge[is + G * (k0 + tm.lane)] : 0;
-        for (int k = 0; k < kk; ++k) {
-            const long long slot = __shfl_sync(FULL_MASK, idx, k);
-            dst[slot * kH + tm.lane] = p;
-        }
-    }
-}
-
 // Sum of the pushed adjoint rows in i's mirror slots (+ remote partials in
 // domain decomposition), lane = channel, fixed order.
 template <typename T, int G>
@@ -438,7 +428,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mf.n_cells_zero;
          c += gridDim.x * blockDim.x)
         mf.cell_count[c] = 0;
-    T(*sb)[12] = sm.ed;
+    auto sb = sm.ed;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
@@ -567,10 +557,13 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
                 ws.grev[gr.inv_pos[e]] = acc;  // mirror for the force gather
             }
         } else {
-            // P^0 = W1h^(0) h^0, pushed into the out-slots of i's in-edges
+            // P^0 = W1h^(0) h^0, one row per atom (L2-resident; gathered by the
+            // sources of i's in-edges in the message layer)
             const T p = twmv<T, 32>(W1h, sm.x, lane, tm, sm);
-            if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
-            push_rows(ws.pe, p, gr, i, tm);
+            if (lead) {
+                ws.pa[static_cast<long long>(i) * kH + lane] = p;
+                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
+            }
         }
         __syncwarp();
     }
@@ -610,21 +603,27 @@ struct AtomRow {
 };
 
 // First batch of a warp's backward edge loop, loaded early (lane = local edge
-// for the scalars, lane = channel for the z rows).
+// for the scalars, lane = channel for the rows).  Stored mode: the rows are z_e,
+// written by the layer's forward.  RECOMP mode: nothing per edge is stored by the
+// forward; the rows are the gathered P^l_j and z_e = tanh(W1b b_e + b1 + P^l_j) is
+// recomputed in the edge loop (kRecomputeZ, defined with the team constants).
 template <typename T>
 struct BwdPre {
-    T zr[8];
+    T zr[8];  // z rows (stored mode) or P^l_j rows (RECOMP)
     T s, ds;
     V4<T> d0, d1;
-    int mir;
+    V4<T> b0, b1;  // RECOMP: basis b_e
+    int mir, nb;
 };
-template <typename T, int G>
+template <typename T, int G, bool RECOMP>
 __device__ __forceinline__ void bwd_prefetch(BwdPre<T>& p, const T* Z, const DevWork<T>& ws,
                                              const DevGraph& gr, long long e0, int room,
                                              int lane) {
+    if constexpr (!RECOMP) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-        if (u < room) p.zr[u] = Z[(e0 + static_cast<long long>(G) * u) * kH + lane];
+        for (int u = 0; u < 8; ++u)
+            if (u < room) p.zr[u] = Z[(e0 + static_cast<long long>(G) * u) * kH + lane];
+    }
     if (lane < room) {
         const long long e = e0 + static_cast<long long>(G) * lane;
         p.s = ws.es[e];
@@ -632,6 +631,18 @@ __device__ __forceinline__ void bwd_prefetch(BwdPre<T>& p, const T* Z, const Dev
         p.d0 = ld4c(ws.edb + 8 * e);
         p.d1 = ld4c(ws.edb + 8 * e + 4);
         p.mir = gr.inv_pos[e];
+        if constexpr (RECOMP) {
+            p.b0 = ld4c(ws.eb + 8 * e);
+            p.b1 = ld4c(ws.eb + 8 * e + 4);
+            p.nb = min(max(gr.nbr[e], 0), gr.n - 1);  // ELL padding: any valid row
+        }
+    }
+    if constexpr (RECOMP) {  // Z = P^l rows [n][32]
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = __shfl_sync(FULL_MASK, p.nb, u);
+            if (u < room) p.zr[u] = Z[static_cast<long long>(j) * kH + lane];
+        }
     }
 }
 
@@ -671,9 +682,9 @@ struct GatherPre {
 // accumulates dE/dr_e into g (this warp's share of the edges).  `pre` holds the
 // first batch of the edge loop, loaded before the atom's mat-vecs.
 // ---------------------------------------------------------------------------
-template <typename T, int G>
+template <typename T, int G, bool RECOMP>
 __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, const T* mW2T,
-                                                  T mb2, const T (&w1b)[kK], const DevGraph& gr,
+                                                  T mb1, T mb2, const T (&w1b)[kK], const DevGraph& gr,
                                                   const DevWork<T>& ws, WarpSmem<T>& sm, int l,
                                                   int i, T dh, T zu, bool first_g,
                                                   Team<G>& tm, BwdPre<T>& pre, long long e0,
@@ -694,13 +705,15 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
     __syncwarp();
     const T v = twmv<T, 32>(mW2T, sm.x, lane, tm, sm);  // v = W2^T dmsum
     const T c0 = warp_sum(dmsum * mb2);
-    const T* Z = ws.z + l * S * kH;
+    // stored z rows (LAST layer) or this layer's P rows (RECOMP)
+    const T* Z = RECOMP ? ws.pa + static_cast<long long>(l) * gr.n * kH
+                        : ws.z + (kRecomputeZ ? 0 : static_cast<long long>(l) * S * kH);
     T* D = ws.d + (l & 1) * S * kH;
     for (int base = 0; base < mloc; base += 32) {
         const int m = min(32, mloc - base);
         const long long eb = e0 + static_cast<long long>(G) * base;  // local edge k: eb + G k
         const T* zrow = Z + eb * kH + lane;
-        if (base > 0) bwd_prefetch<T, G>(pre, Z, ws, gr, eb, m, lane);
+        if (base > 0) bwd_prefetch<T, G, RECOMP>(pre, Z, ws, gr, eb, m, lane);
         // lane u stages edge u's scalars; the edge loop reads them as broadcasts
         if (lane < m) {
             T* row = sm.ed[lane];
@@ -708,6 +721,11 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
             row[1] = pre.ds;
             st4(row + 4, pre.d0.x, pre.d0.y, pre.d0.z, pre.d0.w);
             st4(row + 8, pre.d1.x, pre.d1.y, pre.d1.z, pre.d1.w);
+            if constexpr (RECOMP) {
+                st4(row + 12, pre.b0.x, pre.b0.y, pre.b0.z, pre.b0.w);
+                st4(row + 16, pre.b1.x, pre.b1.y, pre.b1.z, pre.b1.w);
+                sm.enb[lane] = pre.nb;
+            }
             sm.emir[lane] = pre.mir;
         }
         __syncwarp();
@@ -717,7 +735,9 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
             T zn[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (u0 + 8 + u < m) zn[u] = zrow[(u0 + 8 + u) * G * kH];
+                if (u0 + 8 + u < m)
+                    zn[u] = RECOMP ? Z[static_cast<long long>(sm.enb[u0 + 8 + u]) * kH + lane]
+                                   : zrow[(u0 + 8 + u) * G * kH];
             T term[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -734,7 +754,22 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
                     wv += w1b[5] * d1.y;
                     wv += w1b[6] * d1.z;
                     wv += w1b[7] * d1.w;
-                    const T z = zr[u];
+                    T z;
+                    if constexpr (RECOMP) {  // z_e = tanh(W1b b_e + b1 + P^l_j), as the forward
+                        const V4<T> b0 = ld4c(row + 12), bb = ld4c(row + 16);
+                        T a = mb1;
+                        a += w1b[0] * b0.x;
+                        a += w1b[1] * b0.y;
+                        a += w1b[2] * b0.z;
+                        a += w1b[3] * b0.w;
+                        a += w1b[4] * bb.x;
+                        a += w1b[5] * bb.y;
+                        a += w1b[6] * bb.z;
+                        a += w1b[7] * bb.w;
+                        z = d_tanh(a + zr[u]);
+                    } else {
+                        z = zr[u];
+                    }
                     const T d = s * v * (T(1) - z * z);
                     D[static_cast<long long>(sm.emir[u0 + u]) * kH + lane] = d;
                     term[u] = ds * v * z + d * wv;
@@ -799,32 +834,36 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     pdl_wait();
     TP(1);
     const int n = gr.n;
-    const long long S = ws.slots;
-    const T* Pin = ws.pe + (l & 1) * S * kH;
-    T* Z = ws.z + l * S * kH;
+    // P^l_j rows: one per atom, gathered by neighbour index (the [n][32] array stays
+    // in L2 at every paper size; per-edge pushed copies would not)
+    const T* Pl = ws.pa + static_cast<long long>(l) * n * kH;
+    // z_e rows of this layer (read back by the layer's backward); with kRecomputeZ only
+    // the LAST layer's are stored (the lower layers' backward recomputes them)
+    T* Z = ws.z + (kRecomputeZ ? 0 : static_cast<long long>(l) * ws.slots * kH);
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
-        // first batch: P rows (lane = channel) and edge scalars (lane = local edge)
-        T pr[kU<T>];
-#pragma unroll
-        for (int u = 0; u < kU<T>; ++u)
-            if (u < ar.room) pr[u] = Pin[(ar.e0 + static_cast<long long>(G) * u) * kH + lane];
+        // first batch: edge scalars and neighbour indices (lane = local edge; on the
+        // ELL graph issued before the count arrives), then the P rows they select
         T es_l = T(0);
         V4<T> b0_l{}, bb_l{};
+        int nb_l = 0;
         if (lane < ar.room) {
             const long long e = ar.e0 + static_cast<long long>(G) * lane;
             es_l = ws.es[e];
             b0_l = ld4c(ws.eb + 8 * e);
             bb_l = ld4c(ws.eb + 8 * e + 4);
+            nb_l = min(max(gr.nbr[e], 0), n - 1);  // padding slots: any valid row
         }
-        // push targets of P^{l+1} (symmetric graph: the atom's own reverse slots)
-        int push_idx = 0;
-        if (!LAST && gr.sym && lane < ar.room)
-            push_idx = gr.in_edge[ar.e0 + static_cast<long long>(G) * lane];
+        T pr[kU<T>];
+#pragma unroll
+        for (int u = 0; u < kU<T>; ++u) {
+            const int j = __shfl_sync(FULL_MASK, nb_l, u);
+            if (u < ar.room) pr[u] = Pl[static_cast<long long>(j) * kH + lane];
+        }
         const int mloc = ar.finish(tm);
         sm.x[lane] = hi;
         TP(2);
@@ -832,16 +871,18 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         for (int base = 0; base < mloc; base += 32) {
             const int m = min(32, mloc - base);
             const long long e0 = ar.e0 + static_cast<long long>(G) * base;  // local k: e0 + G k
-            const T* prow = Pin + e0 * kH + lane;
             if (base > 0) {
-#pragma unroll
-                for (int u = 0; u < kU<T>; ++u)
-                    if (u < m) pr[u] = prow[u * G * kH];
                 if (lane < m) {
                     const long long e = e0 + G * lane;
                     es_l = ws.es[e];
                     b0_l = ld4c(ws.eb + 8 * e);
                     bb_l = ld4c(ws.eb + 8 * e + 4);
+                    nb_l = gr.nbr[e];
+                }
+#pragma unroll
+                for (int u = 0; u < kU<T>; ++u) {
+                    const int j = __shfl_sync(FULL_MASK, nb_l, u);
+                    if (u < m) pr[u] = Pl[static_cast<long long>(j) * kH + lane];
                 }
             }
             if (lane < m) {
@@ -849,13 +890,15 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
                 row[0] = es_l;
                 st4(row + 4, b0_l.x, b0_l.y, b0_l.z, b0_l.w);
                 st4(row + 8, bb_l.x, bb_l.y, bb_l.z, bb_l.w);
+                sm.enb[lane] = nb_l;
             }
             __syncwarp();
             for (int u0 = 0; u0 < m; u0 += kU<T>) {
                 T pn[kU<T>];
 #pragma unroll
                 for (int u = 0; u < kU<T>; ++u)
-                    if (u0 + kU<T> + u < m) pn[u] = prow[(u0 + kU<T> + u) * G * kH];
+                    if (u0 + kU<T> + u < m)
+                        pn[u] = Pl[static_cast<long long>(sm.enb[u0 + kU<T> + u]) * kH + lane];
 #pragma unroll
                 for (int u = 0; u < kU<T>; ++u) {
                     if (u0 + u >= m) break;
@@ -872,7 +915,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
                     a += w1b[6] * bb.z;
                     a += w1b[7] * bb.w;
                     const T z = d_tanh(a + pr[u]);
-                    Z[(e0 + static_cast<long long>(G) * (u0 + u)) * kH + lane] = z;
+                    if (LAST || !kRecomputeZ)
+                        Z[(e0 + static_cast<long long>(G) * (u0 + u)) * kH + lane] = z;
                     acc += s * z;
                     ssum += s;
                 }
@@ -885,7 +929,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         // warp) is loaded now, under the atom-level mat-vecs below
         TP(3);
         BwdPre<T> pre;
-        if constexpr (LAST) bwd_prefetch<T, G>(pre, Z, ws, gr, ar.e0, min(mloc, 32), lane);
+        if constexpr (LAST) bwd_prefetch<T, G, false>(pre, Z, ws, gr, ar.e0, min(mloc, 32), lane);
         acc = tm.sum(acc, ssum, sm);
         TP(4);
         if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
@@ -909,23 +953,11 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         __syncwarp();
         TP(5);
         if constexpr (!LAST) {
+            // P^{l+1}_i, one row per atom
             const T p = twmv<T, 32>(nW1h, sm.t, lane, tm, sm);
-            if (lead && ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
-            T* dst = ws.pe + ((l + 1) & 1) * S * kH;
-            if (gr.sym) {  // in-slots == out-slots: push_idx holds the first 32 targets
-                for (int k0 = 0; k0 < mloc; k0 += 32) {
-                    const int kk = min(32, mloc - k0);
-                    if (k0 > 0)
-                        push_idx = lane < kk ? gr.in_edge[ar.e0 + static_cast<long long>(G) *
-                                                                       (k0 + lane)]
-                                             : 0;
-                    for (int k = 0; k < kk; ++k) {
-                        const long long slot = __shfl_sync(FULL_MASK, push_idx, k);
-                        dst[slot * kH + lane] = p;
-                    }
-                }
-            } else {
-                push_rows(dst, p, gr, i, tm);
+            if (lead) {
+                ws.pa[(static_cast<long long>(l + 1) * n + i) * kH + lane] = p;
+                if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
             }
             TP(6);
         } else {
@@ -934,8 +966,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
             const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
                                   lead ? ws.e_atom + i : nullptr, tm, sm);
             TP(7);
-            msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, true, tm, pre,
-                              ar.e0, mloc);
+            msg_backward_warp<T, G, false>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i, dh,
+                                           zu, true, tm, pre, ar.e0, mloc);
             TP(8);
         }
         __syncwarp();
@@ -965,12 +997,14 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
     T w1b[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
-    const T mb2 = msg.b2[lane];
+    const T mb1 = msg.b1[lane], mb2 = msg.b2[lane];
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
     pdl_wait();
     const T* Dn = ws.d + ((l + 1) & 1) * ws.slots * kH;
-    const T* Z = ws.z + l * ws.slots * kH;
+    // kRecomputeZ: z_e recomputed from P^l_j; else the rows the forward stored
+    const T* Pl = kRecomputeZ ? ws.pa + static_cast<long long>(l) * gr.n * kH
+                              : ws.z + static_cast<long long>(l) * ws.slots * kH;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
@@ -983,7 +1017,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
         GatherPre<T, G> gp;
         if (gr.sym) gp.load(Dn, ar.e0, ar.room, lane);
         BwdPre<T> pre;
-        bwd_prefetch<T, G>(pre, Z, ws, gr, ar.e0, min(ar.room, 32), lane);
+        bwd_prefetch<T, G, kRecomputeZ>(pre, Pl, ws, gr, ar.e0, min(ar.room, 32), lane);
         const int mloc = ar.finish(tm);
         T sv;
         if (gr.sym) {
@@ -1001,8 +1035,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        msg_backward_warp(uW2T, uW1T, mW2T, mb2, w1b, gr, ws, sm, l, i, dh, zu, false, tm, pre,
-                          ar.e0, mloc);
+        msg_backward_warp<T, G, kRecomputeZ>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i, dh,
+                                             zu, false, tm, pre, ar.e0, mloc);
         __syncwarp();
     }
     if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
@@ -1311,16 +1345,14 @@ __global__ __launch_bounds__(kForceCTA) void k_reduce_partials(const double* par
 // ---------------------------------------------------------------------------
 // Domain-decomposition helpers (halo ghosts are atoms [n_active, n)).
 // ---------------------------------------------------------------------------
-// Push the received per-atom projections P of halo ghosts into their in-edge
-// slots (what the owner would have pushed had the ghost been local).
+// The received per-atom projections P of halo ghosts into the layer's P rows
+// (what the owner would have written had the ghost been local).
 template <typename T>
-__global__ void k_dd_push_ghosts(DevGraph gr, const T* __restrict__ p_atom, T* __restrict__ pe) {
+__global__ void k_dd_ghost_p(DevGraph gr, const T* __restrict__ p_atom, T* __restrict__ pa) {
     const int i = gr.n_active + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (i >= gr.n) return;
-    const T v = p_atom[static_cast<long long>(i) * kH + lane];
-    const int is = gr.in_start[i], ic = gr.in_cnt[i];
-    for (int k = 0; k < ic; ++k) pe[static_cast<long long>(gr.in_edge[is + k]) * kH + lane] = v;
+    pa[static_cast<long long>(i) * kH + lane] = p_atom[static_cast<long long>(i) * kH + lane];
 }
 // Partial dE/dh adjoint sums collected at halo ghosts (sent back to the owners).
 template <typename T>
@@ -1373,12 +1405,15 @@ int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments
 // up to ~40 atoms per SM (1UBQ 7.5k -> 11.4k, 3LZM 6.8k -> 8.1k steps/s vs 1 warp;
 // 2PTC on par, warm L2 6.3k vs 3.9k) and for embed_fit up to ~10 atoms per SM
 // (1UBQ 24.2k -> 28.9k; 3LZM and 2PTC prefer 1 warp); 1 warp beyond.
-static NetShape net_shape(int n, int n_msg) {
+// FP64 (the oracle-of-record mode) caps a CTA at 8 warps: its per-warp scratch and
+// staged matrices are twice as large and 16 warps would not fit in shared memory.
+static NetShape net_shape(int n, int n_msg, int elem_bytes) {
     const int sms = num_sms();
     const int two_upto = (n_msg > 0 ? 40 : 10) * sms;
+    const int max_warps = elem_bytes > 4 ? kMaxWarps / 2 : kMaxWarps;
     int G = (4 * n <= kMaxWarps * sms) ? 4 : (n <= two_upto ? 2 : 1);
     if (team_override()) G = team_override();
-    const int max_teams = kMaxWarps / G;
+    const int max_teams = max_warps / G;
     int teams = (n + sms - 1) / sms;
     teams = teams < 1 ? 1 : (teams > max_teams ? max_teams : teams);
     if (G == 1 && teams < 2) teams = 2;
@@ -1489,7 +1524,7 @@ template <typename T>
 int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws,
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
-    const NetShape sh = net_shape(gr.n_active, md.n_msg);
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)));
     int launches;
     if (sh.G == 4)
         launches = Net<T, 4>::network(sh, md, gr, ws, rev, st, mk, mf);
@@ -1521,19 +1556,19 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 }
 
 // One phase of a domain-decomposed evaluation (the caller exchanges halo rows
-// between phases).  Phases: 0 embed, 1 push ghost P (into parity `l`), 2 message
+// between phases).  Phases: 0 embed, 1 ghost P rows (into layer `l`), 2 message
 // layer l forward, 3 ghost adjoint sums of layer l, 4 message layer l backward,
 // 5 embedding backward, 6 forces.
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
-    const NetShape sh = net_shape(gr.n_active, md.n_msg);
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)));
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:
             if (ng > 0)
-                k_dd_push_ghosts<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
-                    gr, ws.p_atom, ws.pe + (l & 1) * ws.slots * kH);
+                k_dd_ghost_p<T><<<(ng * 32 + 255) / 256, 256, 0, st>>>(
+                    gr, ws.p_atom, ws.pa + static_cast<long long>(l) * gr.n * kH);
             break;
         case 3:
             if (ng > 0)
