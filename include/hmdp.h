@@ -234,6 +234,57 @@ int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts3); /* owned, halo, searched (sync
 int hmdp_gdd_launches(const hmdp_ctx* ctx, long long* launches);
 
 /* ---------------------------------------------------------------------------
+ * Halo-exchange mode of the device DD (the multi-GPU engine; SPEC.md:474-524
+ * message kinds ghost_positions / ghost_forces, per-layer rc halo).
+ * Nothing is replicated: each rank integrates only the atoms its region owns, and
+ * every step moves exactly the halo with point-to-point rounds to every peer:
+ *   POS (x, v of owned atoms within rc of the peer's region; migration included),
+ *   P^l per message layer (P rows of owned atoms near the peer),
+ *   SUMS^l per layer (dE/dh partial sums at halo atoms -> their owners),
+ *   FORCES (partial forces at halo atoms -> their owners), OUT ((E, W, W9) partials,
+ *   summed in rank order on every rank).
+ * Each round packs one fixed-capacity packet per peer on the device (capacity
+ * planned once from the initial geometry, x1.5 + 64 rows headroom; overflow latches
+ * an error), so a whole MD step -- collectives included -- is one CUDA graph.
+ * Transports: NCCL (grouped ncclSend/ncclRecv on the context's stream; libnccl is
+ * loaded at run time), an in-process hub (simulated ranks = contexts on one GPU,
+ * one host thread each), or a caller callback (e.g. gloo in tests).
+ *   hmdp_gdd_set_mode(ctx, 1) after hmdp_gdd_setup, bind buffers 0 (positions),
+ *   3 (forces), 4 (out[16]) and, for MD, 5 (velocities) and 6 (masses), load the
+ *   positions, then hmdp_gdd_plan (capacity; syncs) and hmdp_gdd_step per step.
+ * ------------------------------------------------------------------------- */
+typedef struct hmdp_gdd_hub hmdp_gdd_hub;
+/* Caller transport: move, for every peer q != rank, the first `bytes` of
+ * send + q*stride (device) to peer q's recv + rank*stride (device); return 0 on
+ * success.  Called with the context's stream synchronized. */
+typedef int (*hmdp_gdd_exchange_fn)(void* user, int round, const void* send, void* recv,
+                                    size_t stride, size_t bytes);
+int hmdp_gdd_set_mode(hmdp_ctx* ctx, int mode); /* 0 all-reduce (replicated), 1 halo */
+/* NCCL transport: 128-byte ncclUniqueId (generated on rank 0 by hmdp_nccl_unique_id
+ * and broadcast by the caller), world size and this rank (= DD rank). */
+int hmdp_nccl_unique_id(void* id128);
+int hmdp_gdd_attach_nccl(hmdp_ctx* ctx, const void* id128, int world, int rank);
+int hmdp_gdd_hub_create(int world, hmdp_gdd_hub** out);
+int hmdp_gdd_hub_destroy(hmdp_gdd_hub* hub);
+int hmdp_gdd_attach_hub(hmdp_ctx* ctx, hmdp_gdd_hub* hub);
+int hmdp_gdd_attach_callback(hmdp_ctx* ctx, hmdp_gdd_exchange_fn fn, void* user);
+/* Packet capacity from the loaded positions; marks every atom current (syncs). */
+int hmdp_gdd_plan(hmdp_ctx* ctx);
+/* One step on the context's stream: kind 0 evaluation (E, F, W into the bound
+ * buffers), 1 MD step (evaluation + closing kick + next opening kick + drift of
+ * the owned atoms), 2 the initial opening kick + drift only.  Capturable with the
+ * NCCL transport. */
+int hmdp_gdd_step(hmdp_ctx* ctx, int kind, double dt);
+/* Halo statistics of the last step (syncs): out[0] packet rows capacity C,
+ * out[1] rounds per step, out[2] useful halo bytes sent by this rank per step
+ * (rows x row bytes over every round), out[3] bytes actually transferred per step
+ * (fixed-capacity packets), out[4] peers. */
+int hmdp_gdd_halo_stats(hmdp_ctx* ctx, long long* out5);
+/* Roles of the last step (syncs): out[n] = 1 owned here, 2 halo, 0 neither; the
+ * forces of the owned rows are this rank's share of the global result. */
+int hmdp_gdd_roles(hmdp_ctx* ctx, unsigned char* out);
+
+/* ---------------------------------------------------------------------------
  * Classical force field on the device: the reference's
  * compute_classical (forcefield.cpp:265-279) — harmonic bonds, angles, periodic
  * dihedrals, potential-shifted LJ (Lorentz-Berthelot), Coulomb cutoff_shifted (0)

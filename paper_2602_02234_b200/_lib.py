@@ -73,6 +73,17 @@ SIGNATURES = {
     "hmdp_gdd_phase": (_c_int, [_vp, _c_int, _c_int, _c_double]),
     "hmdp_gdd_counts": (_c_int, [_vp, _vp]),
     "hmdp_gdd_launches": (_c_int, [_vp, _vp]),
+    "hmdp_gdd_set_mode": (_c_int, [_vp, _c_int]),
+    "hmdp_nccl_unique_id": (_c_int, [_vp]),
+    "hmdp_gdd_attach_nccl": (_c_int, [_vp, _vp, _c_int, _c_int]),
+    "hmdp_gdd_hub_create": (_c_int, [_c_int, ctypes.POINTER(_vp)]),
+    "hmdp_gdd_hub_destroy": (_c_int, [_vp]),
+    "hmdp_gdd_attach_hub": (_c_int, [_vp, _vp]),
+    "hmdp_gdd_attach_callback": (_c_int, [_vp, _vp, _vp]),
+    "hmdp_gdd_plan": (_c_int, [_vp]),
+    "hmdp_gdd_step": (_c_int, [_vp, _c_int, _c_double]),
+    "hmdp_gdd_halo_stats": (_c_int, [_vp, _vp]),
+    "hmdp_gdd_roles": (_c_int, [_vp, _vp]),
     "hmdp_ff_create": (_c_int, [_c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_double,
                                 _c_double, _c_double, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp,
                                 _c_int, _vp, _vp, ctypes.POINTER(_vp)]),

@@ -7,11 +7,14 @@
 // the host-pointer entry points.  There is no CPU fallback: every compute
 // entry point fails with HMDP_CUDA_ERROR when no device is usable.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -59,7 +62,24 @@ struct GddGeom {
     int rank;
     double halo;
 };
-void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t);
+void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t,
+                      const int* = nullptr, const int* = nullptr);
+void launch_gdd_send_lists(const int*, const int*, int, const double*, const GddGeom&, int, int, int,
+                           int*, int*, unsigned*, cudaStream_t);
+template <typename E>
+void launch_gdd_pack(int, int, const int*, const int*, int, const E*, int, const E*, int, char*,
+                     size_t, cudaStream_t);
+template <typename E>
+void launch_gdd_unpack_copy(int, int, int, const char*, size_t, E*, int, E*, int, int*, const int*,
+                            cudaStream_t);
+template <typename E>
+void launch_gdd_unpack_add(int, int, int, const char*, size_t, E*, int, cudaStream_t);
+void launch_gdd_tick(int*, cudaStream_t);
+void launch_gdd_stamp_all(int, int*, const int*, cudaStream_t);
+void launch_gdd_out_pack(int, int, const double*, char*, size_t, cudaStream_t);
+void launch_gdd_sum_out(int, int, const char*, size_t, double*, cudaStream_t);
+void launch_cell_bin_list(const int*, const int*, int, const double*, const CellGrid&, int*, int*,
+                          int*, unsigned*, cudaStream_t);
 struct FfDev {
     int n, n_types, scheme;
     double rc_lj, rc_c, k_rf, c_rf, fpre;
@@ -94,7 +114,7 @@ void launch_gdd_push_halo(const DevGraph&, int, const T*, T*, const int*, const 
 template <typename T>
 void launch_gdd_halo_sums(const DevGraph&, int, const T*, T*, const int*, const int*, cudaStream_t);
 void launch_gdd_integrate(int, const double*, double*, double*, const double*, double, int, unsigned*,
-                          cudaStream_t);
+                          cudaStream_t, const int* = nullptr, const int* = nullptr);
 void launch_descriptors_f64(const DevModel<double>&, const DevGraph&, double*, cudaStream_t);
 }  // namespace hmdp
 
@@ -227,6 +247,52 @@ struct PinnedBuf {
         bytes = 0;
     }
 };
+
+// NCCL, loaded at run time (the library is a dependency of the multi-GPU
+// transport only; a process that already loaded torch's libnccl.so.2 shares it).
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](auto& fp, const char* name) {
+            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+            if (!fp) a.why = std::string("missing NCCL symbol ") + name;
+        };
+        sym(a.GetUniqueId, "ncclGetUniqueId");
+        sym(a.CommInitRank, "ncclCommInitRank");
+        sym(a.CommDestroy, "ncclCommDestroy");
+        sym(a.Send, "ncclSend");
+        sym(a.Recv, "ncclRecv");
+        sym(a.GroupStart, "ncclGroupStart");
+        sym(a.GroupEnd, "ncclGroupEnd");
+        sym(a.GetErrorString, "ncclGetErrorString");
+        a.ok = a.why.empty();
+        return a;
+    }();
+    if (!api.ok) fail(HMDP_CUDA_ERROR, api.why);
+    return api;
+}
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(HMDP_CUDA_ERROR, std::string(what) + ": " + nccl_api().GetErrorString(r));
+}
 
 // Flattened weights for one precision: per MLP {W1, W1T, b1, W2, W2T, b2}.
 template <typename T>
@@ -529,6 +595,18 @@ struct hmdp_ctx {
         double* out = nullptr;     // [16] (E, W, W9) partials exchange
         double* vel = nullptr;
         double* mass = nullptr;
+        // halo-exchange mode (hmdp_gdd_set_mode 1): point-to-point rounds with every
+        // peer instead of all-reduces of replicated global buffers
+        int mode = 0, world = 1, C = 0;
+        size_t stride = 0;  // bytes per peer slot of the packet buffers
+        DBuf stamp, cur, flist, fcnt, rlist, rcnt, spk, rpk, sremote, hsum, outs;
+        int transport = 0;  // 0 none (world 1), 1 NCCL, 2 in-process hub, 3 caller callback
+        void* comm = nullptr;  // ncclComm_t
+        struct hmdp_gdd_hub* hub = nullptr;
+        cudaEvent_t ev_packed = nullptr, ev_done = nullptr;
+        hmdp_gdd_exchange_fn cb = nullptr;
+        void* cb_user = nullptr;
+        long long rounds = 0;  // halo rounds enqueued so far
     } gdd;
     DBuf grp_xyz, grp_types, grp_idx;  // hmdp_compute_group: the full system + member list
     DevGraph dd_gr{};
@@ -618,7 +696,9 @@ struct hmdp_ctx {
                         &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
-                        &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
+                        &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &gdd.stamp,
+                        &gdd.cur, &gdd.flist, &gdd.fcnt, &gdd.rlist, &gdd.rcnt, &gdd.spk, &gdd.rpk,
+                        &gdd.sremote, &gdd.hsum, &gdd.outs, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
                         &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1,
                         &rf_envA, &rf_dua, &cg_out})
@@ -631,6 +711,9 @@ struct hmdp_ctx {
         pin_in.release();
         cgraph.reset();
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
+        if (gdd.ev_packed) cudaEventDestroy(gdd.ev_packed);
+        if (gdd.ev_done) cudaEventDestroy(gdd.ev_done);
+        if (gdd.comm) nccl_api().CommDestroy(static_cast<ncclComm_t>(gdd.comm));
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -2063,106 +2146,194 @@ int hmdp_gdd_bind(hmdp_ctx* ctx, int kind, void* dptr) {
     return HMDP_OK;
 }
 
-int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
-    return guarded([&] {
-        need_model(ctx);
-        auto& g = ctx->gdd;
-        if (g.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
-        if (!g.pos || !g.p_atom || !g.sghost || !g.forces || !g.out)
-            fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_bind: buffers 0-4 must be bound");
-        const int M = ctx->n_msg(), n = g.n;
-        if ((phase >= 1 && phase <= 4) && (layer < 0 || layer >= std::max(M, 1)))
-            fail(HMDP_INVALID_ARGUMENT, "layer out of range");
-        set_device(ctx);
-        cudaStream_t st = ctx->st();
-        const long long slots = static_cast<long long>(n) * ctx->cap;
-        const size_t tb = g.prec == HMDP_FP64 ? sizeof(double) : sizeof(float);
-        const size_t rows = static_cast<size_t>(n) * kH * tb;
-        auto run = [&](auto tag) {
-            using T = decltype(tag);
-            DevWork<T> w = ctx->work<T>(n, slots);
-            w.p_atom = static_cast<T*>(g.p_atom);
-            w.s_remote = static_cast<T*>(g.sghost);
-            const DevModel<T>& md = [&]() -> const DevModel<T>& {
-                if constexpr (sizeof(T) == 8) return ctx->wd.dev;
-                else return ctx->wf.dev;
-            }();
-            const DevGraph own = gdd_graph(ctx, 0);
-            switch (phase) {
-                case 10: {  // roles, neighbour list of owned + halo atoms, mirrors, zeroing
-                    ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
-                    launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), g.lists.as<int>(),
-                                     g.counts.as<int>(), st);
-                    const CellGrid cg = ctx->grid(g.box, ctx->model.rc, n);
-                    ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
-                       "memset cells");
-                    ctx->cells_zero = false;
+namespace {
+// One phase of the device DD on the context's stream (throws; hmdp_gdd_phase and
+// hmdp_gdd_step wrap it).  Phases 0-10 are shared by both modes; 19-28 belong to
+// the halo-exchange mode (hmdp.h).
+void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
+    need_model(ctx);
+    auto& g = ctx->gdd;
+    if (g.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
+    const bool halo = g.mode == 1;
+    if (!g.pos || !g.forces || !g.out || (!halo && (!g.p_atom || !g.sghost)))
+        fail(HMDP_INVALID_ARGUMENT, halo ? "hmdp_gdd_bind: buffers 0, 3, 4 must be bound"
+                                         : "hmdp_gdd_bind: buffers 0-4 must be bound");
+    const int M = ctx->n_msg(), n = g.n;
+    if (((phase >= 1 && phase <= 4) || phase == 22 || phase == 23) &&
+        (layer < 0 || layer >= std::max(M, 1)))
+        fail(HMDP_INVALID_ARGUMENT, "layer out of range");
+    if (halo && phase >= 20 && phase <= 28 && g.C <= 0)
+        fail(HMDP_INVALID_ARGUMENT, "halo mode: hmdp_gdd_plan not called");
+    set_device(ctx);
+    cudaStream_t st = ctx->st();
+    const long long slots = static_cast<long long>(n) * ctx->cap;
+    const size_t tb = g.prec == HMDP_FP64 ? sizeof(double) : sizeof(float);
+    const size_t rows = static_cast<size_t>(n) * kH * tb;
+    unsigned* err = ctx->err.as<unsigned>();
+    char* spk = g.spk.as<char>();
+    char* rpk = g.rpk.as<char>();
+    const int W = g.world, R = g.geom.rank, C = g.C;
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        DevWork<T> w = ctx->work<T>(n, slots);
+        w.p_atom = halo ? nullptr : static_cast<T*>(g.p_atom);
+        w.s_remote = halo ? g.sremote.as<T>() : static_cast<T*>(g.sghost);
+        T* hsum = halo ? g.hsum.as<T>() : static_cast<T*>(g.sghost);
+        const DevModel<T>& md = [&]() -> const DevModel<T>& {
+            if constexpr (sizeof(T) == 8) return ctx->wd.dev;
+            else return ctx->wf.dev;
+        }();
+        const DevGraph own = gdd_graph(ctx, 0);
+        int* lists = g.lists.as<int>();
+        int* counts = g.counts.as<int>();
+        switch (phase) {
+            case 10: {  // roles, neighbour list of owned + halo atoms, mirrors, zeroing
+                ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
+                launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), lists, counts, st,
+                                 halo ? g.stamp.as<int>() : nullptr, halo ? g.cur.as<int>() : nullptr);
+                const CellGrid cg = ctx->grid(g.box, ctx->model.rc, n);
+                ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
+                   "memset cells");
+                ctx->cells_zero = false;
+                if (halo)  // only the current rows (owned + halo); the rest are stale
+                    launch_cell_bin_list(lists + 2 * static_cast<size_t>(n), counts + 2,
+                                         std::min(n, 2 * g.n_est), g.pos, cg,
+                                         ctx->cell_count.as<int>(), ctx->members.as<int>(),
+                                         ctx->cell_of.as<int>(), err, st);
+                else
                     launch_cell_bin(n, g.pos, cg, ctx->cell_count.as<int>(), ctx->members.as<int>(),
-                                    ctx->cell_of.as<int>(), ctx->err.as<unsigned>(), st);
-                    ck(cudaMemsetAsync(ctx->nnei.p, 0, n * sizeof(int), st), "memset nnei");
-                    const DevGraph srch = gdd_graph(ctx, 2);
-                    launch_nbr_search(std::min(n, 2 * g.n_est), g.pos, cg, ctx->cell_count.as<int>(),
-                                      ctx->members.as<int>(), ctx->cell_of.as<int>(),
-                                      ctx->model.rc * ctx->model.rc, ctx->cap, ctx->nnei.as<int>(),
-                                      ctx->row_start.as<int>(), ctx->nbr.as<int>(),
-                                      ctx->dr.as<double>(), ctx->types.as<int>(), ctx->ety.as<int>(),
-                                      ctx->err.as<unsigned>(), st, srch.alist, srch.alist_n);
-                    ctx->cells_owner = nullptr;
-                    launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
-                    launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
-                                       M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
-                    g.launches += 6;  // roles, bin, search, rev, zero, zero_energy
-                    break;
+                                    ctx->cell_of.as<int>(), err, st);
+                ck(cudaMemsetAsync(ctx->nnei.p, 0, n * sizeof(int), st), "memset nnei");
+                const DevGraph srch = gdd_graph(ctx, 2);
+                launch_nbr_search(std::min(n, 2 * g.n_est), g.pos, cg, ctx->cell_count.as<int>(),
+                                  ctx->members.as<int>(), ctx->cell_of.as<int>(),
+                                  ctx->model.rc * ctx->model.rc, ctx->cap, ctx->nnei.as<int>(),
+                                  ctx->row_start.as<int>(), ctx->nbr.as<int>(),
+                                  ctx->dr.as<double>(), ctx->types.as<int>(), ctx->ety.as<int>(),
+                                  err, st, srch.alist, srch.alist_n);
+                ctx->cells_owner = nullptr;
+                launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
+                launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
+                                   M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
+                g.launches += 6;  // roles, bin, search, rev, zero, zero_energy
+                if (halo) {  // this step's send lists: owned -> peers' halos, halo -> owners
+                    ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
+                    ck(cudaMemsetAsync(g.rcnt.p, 0, W * sizeof(int), st), "memset");
+                    launch_gdd_send_lists(lists, counts, g.n_est, g.pos, g.geom, W, 0, C,
+                                          g.flist.as<int>(), g.fcnt.as<int>(), err, st);
+                    launch_gdd_send_lists(lists + n, counts + 1, g.n_est, g.pos, g.geom, W, 1, C,
+                                          g.rlist.as<int>(), g.rcnt.as<int>(), err, st);
+                    g.launches += 2;
                 }
-                case 0:
-                    ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
-                    launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st);
-                    g.launches += 1;
-                    break;
-                case 1:
-                    launch_gdd_push_halo<T>(own, g.n_est, static_cast<const T*>(g.p_atom),
-                                            w.pa + static_cast<long long>(layer) * own.n * kH,
-                                            g.lists.as<int>() + n, g.counts.as<int>() + 1, st);
-                    g.launches += 1;
-                    break;
-                case 2:
-                    if (layer < M - 1) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
-                    launch_dd_phase<T>(md, own, w, 2, layer, nullptr, g.forces, g.out, st);
-                    g.launches += 1;
-                    break;
-                case 3:
-                    ck(cudaMemsetAsync(g.sghost, 0, rows, st), "memset");
-                    launch_gdd_halo_sums<T>(own, g.n_est, w.d + (layer & 1) * slots * kH,
-                                            static_cast<T*>(g.sghost), g.lists.as<int>() + n,
-                                            g.counts.as<int>() + 1, st);
-                    g.launches += 1;
-                    break;
-                case 4:
-                case 5:
-                    launch_dd_phase<T>(md, own, w, phase, layer, nullptr, g.forces, g.out, st);
-                    g.launches += 1;
-                    break;
-                case 6:  // forces of every row (halo rows: partials), (E, W, W9) partials
-                    launch_dd_phase<T>(md, own, w, 6, 0, nullptr, g.forces, g.out, st);
-                    g.launches += 1;
-                    break;
-                case 7:  // velocity Verlet on all atoms from the all-reduced forces
-                case 8:  // the initial opening kick + drift only
-                    if (!g.vel || !g.mass) fail(HMDP_INVALID_ARGUMENT, "bind velocities and masses");
-                    launch_gdd_integrate(n, g.forces, g.pos, g.vel, g.mass, dt, phase == 8 ? 1 : 0,
-                                         ctx->err.as<unsigned>(), st);
-                    g.launches += 1;
-                    break;
-                default:
-                    fail(HMDP_INVALID_ARGUMENT, "unknown phase");
+                break;
             }
-        };
-        if (g.prec == HMDP_FP64)
-            run(double{});
-        else
-            run(float{});
-        ck(cudaGetLastError(), "kernel launch");
-    });
+            case 0:
+                if (!halo) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
+                launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st);
+                g.launches += 1;
+                break;
+            case 1:
+                launch_gdd_push_halo<T>(own, g.n_est, static_cast<const T*>(g.p_atom),
+                                        w.pa + static_cast<long long>(layer) * own.n * kH,
+                                        lists + n, counts + 1, st);
+                g.launches += 1;
+                break;
+            case 2:
+                if (!halo && layer < M - 1) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
+                launch_dd_phase<T>(md, own, w, 2, layer, nullptr, g.forces, g.out, st);
+                g.launches += 1;
+                break;
+            case 3:
+                ck(cudaMemsetAsync(hsum, 0, rows, st), "memset");
+                launch_gdd_halo_sums<T>(own, g.n_est, w.d + (layer & 1) * slots * kH, hsum,
+                                        lists + n, counts + 1, st);
+                g.launches += 1;
+                break;
+            case 4:
+            case 5:
+                launch_dd_phase<T>(md, own, w, phase, layer, nullptr, g.forces, g.out, st);
+                g.launches += 1;
+                break;
+            case 6:  // forces of every row (halo rows: partials), (E, W, W9) partials
+                launch_dd_phase<T>(md, own, w, 6, 0, nullptr, g.forces, g.out, st);
+                g.launches += 1;
+                break;
+            case 7:  // velocity Verlet (halo mode: owned atoms only)
+            case 8:  // the initial opening kick + drift only
+                if (!g.vel || !g.mass) fail(HMDP_INVALID_ARGUMENT, "bind velocities and masses");
+                launch_gdd_integrate(n, g.forces, g.pos, g.vel, g.mass, dt, phase == 8 ? 1 : 0, err,
+                                     st, halo ? lists : nullptr, halo ? counts : nullptr);
+                g.launches += 1;
+                break;
+            // ---- halo-exchange mode ----
+            case 20:  // POS send lists (owned after the drift, near each peer) + pack (x, v)
+                launch_gdd_tick(g.cur.as<int>(), st);
+                ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
+                launch_gdd_send_lists(lists, counts, g.n_est, g.pos, g.geom, W, 0, C,
+                                      g.flist.as<int>(), g.fcnt.as<int>(), err, st);
+                launch_gdd_pack<double>(W, R, g.flist.as<int>(), g.fcnt.as<int>(), C, g.pos, 3,
+                                        g.vel, g.vel ? 3 : 0, spk, g.stride, st);
+                g.launches += 3;
+                break;
+            case 21:  // unpack POS: received atoms become current for this step
+                launch_gdd_unpack_copy<double>(W, R, C, rpk, g.stride, g.pos, 3, g.vel,
+                                               g.vel ? 3 : 0, g.stamp.as<int>(), g.cur.as<int>(),
+                                               st);
+                g.launches += 1;
+                break;
+            case 22:  // pack P^l rows of owned atoms near each peer
+                launch_gdd_pack<T>(W, R, g.flist.as<int>(), g.fcnt.as<int>(), C,
+                                   w.pa + static_cast<long long>(layer) * n * kH, kH,
+                                   static_cast<const T*>(nullptr), 0, spk, g.stride, st);
+                g.launches += 1;
+                break;
+            case 23:  // unpack P^l rows of halo atoms
+                launch_gdd_unpack_copy<T>(W, R, C, rpk, g.stride,
+                                          w.pa + static_cast<long long>(layer) * n * kH, kH,
+                                          static_cast<T*>(nullptr), 0, nullptr, nullptr, st);
+                g.launches += 1;
+                break;
+            case 24:  // pack the halo atoms' partial dE/dh sums by owner
+                launch_gdd_pack<T>(W, R, g.rlist.as<int>(), g.rcnt.as<int>(), C, hsum, kH,
+                                   static_cast<const T*>(nullptr), 0, spk, g.stride, st);
+                g.launches += 1;
+                break;
+            case 25:  // owners: s_remote = sum over peers (rank order)
+                ck(cudaMemsetAsync(g.sremote.p, 0, rows, st), "memset");
+                launch_gdd_unpack_add<T>(W, R, C, rpk, g.stride, g.sremote.as<T>(), kH, st);
+                g.launches += W - 1;
+                break;
+            case 26:  // pack the halo atoms' partial forces by owner
+                launch_gdd_pack<double>(W, R, g.rlist.as<int>(), g.rcnt.as<int>(), C, g.forces, 3,
+                                        static_cast<const double*>(nullptr), 0, spk, g.stride, st);
+                g.launches += 1;
+                break;
+            case 27:  // owners add the received partial forces (rank order)
+                launch_gdd_unpack_add<double>(W, R, C, rpk, g.stride, g.forces, 3, st);
+                g.launches += W - 1;
+                break;
+            case 28:  // (E, W, W9) partials: this rank's into every peer's packet slot
+                launch_gdd_out_pack(W, R, g.out, spk, g.stride, st);
+                g.launches += 1;
+                break;
+            case 29:  // totals = sum over ranks in rank order, identical on every rank
+                launch_gdd_sum_out(W, R, rpk, g.stride, g.out, st);
+                g.launches += 1;
+                break;
+            default:
+                fail(HMDP_INVALID_ARGUMENT, "unknown phase");
+        }
+    };
+    if (g.prec == HMDP_FP64)
+        run(double{});
+    else
+        run(float{});
+    ck(cudaGetLastError(), "kernel launch");
+}
+}  // namespace
+
+int hmdp_gdd_phase(hmdp_ctx* ctx, int phase, int layer, double dt) {
+    return guarded([&] { gdd_phase_impl(ctx, phase, layer, dt); });
 }
 
 int hmdp_gdd_launches(const hmdp_ctx* ctx, long long* launches) {
@@ -2179,6 +2350,299 @@ int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts) {
                            ctx->st()),
            "D2H");
         ck(cudaStreamSynchronize(ctx->st()), "sync");
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Halo-exchange mode: transports, capacity plan, the step program
+// ---------------------------------------------------------------------------
+struct hmdp_gdd_hub {
+    int world = 0;
+    std::vector<hmdp_ctx*> ctx;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long gen = 0;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const unsigned long long g0 = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g0; });
+        }
+    }
+};
+
+namespace {
+// Bytes of one round's packets: 16-byte header + C indices + C rows of W elements.
+size_t round_bytes(int C, int W, size_t esz) {
+    return 16 + static_cast<size_t>(C) * 4 + static_cast<size_t>(C) * W * esz;
+}
+
+// Move packet (rank -> q) into q's receive slot `rank`, for every peer q.
+void gdd_exchange(hmdp_ctx* ctx, int round, size_t bytes) {
+    auto& g = ctx->gdd;
+    const int W = g.world, R = g.geom.rank;
+    if (W == 1) return;
+    cudaStream_t st = ctx->st();
+    char* spk = g.spk.as<char>();
+    char* rpk = g.rpk.as<char>();
+    ++g.rounds;
+    switch (g.transport) {
+        case 1: {  // NCCL: grouped point-to-point on the context's stream (capturable)
+            NcclApi& api = nccl_api();
+            auto comm = static_cast<ncclComm_t>(g.comm);
+            nck(api.GroupStart(), "ncclGroupStart");
+            for (int q = 0; q < W; ++q) {
+                if (q == R) continue;
+                nck(api.Send(spk + q * g.stride, bytes, ncclUint8, q, comm, st), "ncclSend");
+                nck(api.Recv(rpk + q * g.stride, bytes, ncclUint8, q, comm, st), "ncclRecv");
+            }
+            nck(api.GroupEnd(), "ncclGroupEnd");
+            break;
+        }
+        case 2: {  // in-process hub: ranks are contexts on one device, one host thread each
+            hmdp_gdd_hub* hub = g.hub;
+            ck(cudaEventRecord(g.ev_packed, st), "record");
+            hub->barrier();  // every rank packed
+            for (int q = 0; q < W; ++q) {
+                if (q == R) continue;
+                hmdp_ctx* peer = hub->ctx[q];
+                ck(cudaStreamWaitEvent(st, peer->gdd.ev_packed, 0), "wait packed");
+                ck(cudaMemcpyAsync(rpk + q * g.stride, peer->gdd.spk.as<char>() + R * g.stride, bytes,
+                                   cudaMemcpyDeviceToDevice, st),
+                   "hub copy");
+            }
+            ck(cudaEventRecord(g.ev_done, st), "record");
+            hub->barrier();  // every rank issued its reads of the peers' send packets
+            for (int q = 0; q < W; ++q)  // a send packet is reused only after its readers
+                if (q != R) ck(cudaStreamWaitEvent(st, hub->ctx[q]->gdd.ev_done, 0), "wait done");
+            break;
+        }
+        case 3: {  // caller transport (e.g. gloo): synchronous
+            ck(cudaStreamSynchronize(st), "sync");
+            if (g.cb(g.cb_user, round, spk, rpk, g.stride, bytes) != 0)
+                fail(HMDP_RUNTIME_ERROR, "halo exchange callback failed");
+            break;
+        }
+        default:
+            fail(HMDP_INVALID_ARGUMENT, "halo mode with more than one rank needs a transport");
+    }
+}
+
+// One DD step in halo mode (hmdp.h): the phases of gdd_phase_impl with the
+// exchanges between them.  Rounds: POS, P^l (l < M), SUMS^l (l = M-1 .. 0),
+// FORCES, OUT.
+void gdd_step_impl(hmdp_ctx* ctx, int kind, double dt) {
+    auto& g = ctx->gdd;
+    if (g.mode != 1) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_step: halo mode only (hmdp_gdd_set_mode)");
+    if (kind == 2) {
+        gdd_phase_impl(ctx, 8, 0, dt);
+        return;
+    }
+    const int M = ctx->n_msg(), C = g.C;
+    const size_t tb = g.prec == HMDP_FP64 ? sizeof(double) : sizeof(float);
+    gdd_phase_impl(ctx, 20, 0, dt);
+    gdd_exchange(ctx, 0, round_bytes(C, g.vel ? 6 : 3, sizeof(double)));
+    gdd_phase_impl(ctx, 21, 0, dt);
+    gdd_phase_impl(ctx, 10, 0, dt);
+    gdd_phase_impl(ctx, 0, 0, dt);
+    for (int l = 0; l < M; ++l) {
+        gdd_phase_impl(ctx, 22, l, dt);
+        gdd_exchange(ctx, 1, round_bytes(C, kH, tb));
+        gdd_phase_impl(ctx, 23, l, dt);
+        gdd_phase_impl(ctx, 2, l, dt);
+    }
+    for (int l = M - 1; l >= 0; --l) {
+        gdd_phase_impl(ctx, 3, l, dt);
+        gdd_phase_impl(ctx, 24, l, dt);
+        gdd_exchange(ctx, 2, round_bytes(C, kH, tb));
+        gdd_phase_impl(ctx, 25, l, dt);
+        gdd_phase_impl(ctx, l > 0 ? 4 : 5, l > 0 ? l - 1 : 0, dt);
+    }
+    gdd_phase_impl(ctx, 6, 0, dt);
+    gdd_phase_impl(ctx, 26, 0, dt);
+    gdd_exchange(ctx, 3, round_bytes(C, 3, sizeof(double)));
+    gdd_phase_impl(ctx, 27, 0, dt);
+    gdd_phase_impl(ctx, 28, 0, dt);
+    gdd_exchange(ctx, 4, 16 * sizeof(double));
+    gdd_phase_impl(ctx, 29, 0, dt);
+    if (kind == 1) gdd_phase_impl(ctx, 7, 0, dt);
+}
+}  // namespace
+
+int hmdp_gdd_set_mode(hmdp_ctx* ctx, int mode) {
+    return guarded([&] {
+        need_model(ctx);
+        if (mode != 0 && mode != 1) fail(HMDP_INVALID_ARGUMENT, "mode must be 0 or 1");
+        if (ctx->gdd.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
+        ctx->gdd.mode = mode;
+        ctx->gdd.world = ctx->gdd.geom.d[0] * ctx->gdd.geom.d[1] * ctx->gdd.geom.d[2];
+    });
+}
+
+int hmdp_nccl_unique_id(void* id128) {
+    return guarded([&] {
+        if (!id128) fail(HMDP_INVALID_ARGUMENT, "null id");
+        ncclUniqueId id;
+        nck(nccl_api().GetUniqueId(&id), "ncclGetUniqueId");
+        static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id128, &id, sizeof id);
+    });
+}
+
+int hmdp_gdd_attach_nccl(hmdp_ctx* ctx, const void* id128, int world, int rank) {
+    return guarded([&] {
+        need_model(ctx);
+        auto& g = ctx->gdd;
+        if (!id128 || world != g.world || rank != g.geom.rank)
+            fail(HMDP_INVALID_ARGUMENT, "NCCL world/rank must match the DD rank grid");
+        set_device(ctx);
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof id);
+        ncclComm_t comm = nullptr;
+        nck(nccl_api().CommInitRank(&comm, world, id, rank), "ncclCommInitRank");
+        g.comm = comm;
+        g.transport = 1;
+    });
+}
+
+int hmdp_gdd_hub_create(int world, hmdp_gdd_hub** out) {
+    if (!out || world < 1) return HMDP_INVALID_ARGUMENT;
+    auto* h = new hmdp_gdd_hub;
+    h->world = world;
+    h->ctx.assign(world, nullptr);
+    *out = h;
+    return HMDP_OK;
+}
+
+int hmdp_gdd_hub_destroy(hmdp_gdd_hub* hub) {
+    delete hub;
+    return HMDP_OK;
+}
+
+int hmdp_gdd_attach_hub(hmdp_ctx* ctx, hmdp_gdd_hub* hub) {
+    return guarded([&] {
+        need_model(ctx);
+        auto& g = ctx->gdd;
+        if (!hub || hub->world != g.world) fail(HMDP_INVALID_ARGUMENT, "hub size != rank grid");
+        set_device(ctx);
+        if (!g.ev_packed) ck(cudaEventCreateWithFlags(&g.ev_packed, cudaEventDisableTiming), "event");
+        if (!g.ev_done) ck(cudaEventCreateWithFlags(&g.ev_done, cudaEventDisableTiming), "event");
+        hub->ctx[g.geom.rank] = ctx;
+        g.hub = hub;
+        g.transport = 2;
+    });
+}
+
+int hmdp_gdd_attach_callback(hmdp_ctx* ctx, hmdp_gdd_exchange_fn fn, void* user) {
+    if (!ctx || !fn) return HMDP_INVALID_ARGUMENT;
+    ctx->gdd.cb = fn;
+    ctx->gdd.cb_user = user;
+    ctx->gdd.transport = 3;
+    return HMDP_OK;
+}
+
+int hmdp_gdd_plan(hmdp_ctx* ctx) {
+    return guarded([&] {
+        need_model(ctx);
+        auto& g = ctx->gdd;
+        if (g.mode != 1) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_plan: halo mode only");
+        if (!g.pos) fail(HMDP_INVALID_ARGUMENT, "bind the positions first");
+        set_device(ctx);
+        cudaStream_t st = ctx->st();
+        const int n = g.n, W = g.world;
+        g.stamp.ensure(static_cast<size_t>(n) * sizeof(int));
+        g.cur.ensure(sizeof(int));
+        g.flist.ensure(static_cast<size_t>(W) * n * sizeof(int));
+        g.rlist.ensure(static_cast<size_t>(W) * n * sizeof(int));
+        g.fcnt.ensure(W * sizeof(int));
+        g.rcnt.ensure(W * sizeof(int));
+        // every rank holds the full initial configuration, so every rank can derive
+        // every rank's send counts (both directions, at capacity n) and all ranks
+        // agree on one packet capacity -- the packet layout depends on it.  This
+        // rank's own roles are computed last (they seed the first step).
+        unsigned* err = ctx->err.as<unsigned>();
+        int mx = 1;
+        for (int k = 1; k <= W; ++k) {
+            GddGeom gq = g.geom;
+            gq.rank = (g.geom.rank + k) % W;
+            ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
+            ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
+            ck(cudaMemsetAsync(g.rcnt.p, 0, W * sizeof(int), st), "memset");
+            launch_gdd_roles(n, g.pos, gq, g.role.as<unsigned char>(), g.lists.as<int>(),
+                             g.counts.as<int>(), st);
+            launch_gdd_send_lists(g.lists.as<int>(), g.counts.as<int>(), n, g.pos, gq, W, 0, n,
+                                  g.flist.as<int>(), g.fcnt.as<int>(), err, st);
+            launch_gdd_send_lists(g.lists.as<int>() + n, g.counts.as<int>() + 1, n, g.pos, gq, W,
+                                  1, n, g.rlist.as<int>(), g.rcnt.as<int>(), err, st);
+            std::vector<int> fc(W), rc(W);
+            ck(copy_sync(fc.data(), g.fcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(copy_sync(rc.data(), g.rcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+            for (int q = 0; q < W; ++q) mx = std::max({mx, fc[q], rc[q]});
+        }
+        ck(cudaMemsetAsync(g.cur.p, 0, sizeof(int), st), "memset");
+        g.C = std::min((static_cast<int>(1.5 * mx) + 64 + 31) / 32 * 32, (n + 31) / 32 * 32);
+        const size_t tb = g.prec == HMDP_FP64 ? sizeof(double) : sizeof(float);
+        g.stride = (round_bytes(g.C, kH, tb) + 255) / 256 * 256;
+        g.spk.ensure(W * g.stride);
+        g.rpk.ensure(W * g.stride);
+        g.sremote.ensure(static_cast<size_t>(n) * kH * tb);
+        g.hsum.ensure(static_cast<size_t>(n) * kH * tb);
+        launch_gdd_stamp_all(n, g.stamp.as<int>(), g.cur.as<int>(), st);  // all current at step 1
+        ck(cudaGetLastError(), "kernel launch");
+        hmdp_ctx::raise_bits(ctx->take_err());
+    });
+}
+
+int hmdp_gdd_step(hmdp_ctx* ctx, int kind, double dt) {
+    return guarded([&] { gdd_step_impl(ctx, kind, dt); });
+}
+
+int hmdp_gdd_roles(hmdp_ctx* ctx, unsigned char* out) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!out || ctx->gdd.n <= 0) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        set_device(ctx);
+        ck(copy_sync(out, ctx->gdd.role.p, ctx->gdd.n, cudaMemcpyDeviceToHost, ctx->st()), "D2H");
+    });
+}
+
+int hmdp_gdd_halo_stats(hmdp_ctx* ctx, long long* out) {
+    return guarded([&] {
+        need_model(ctx);
+        if (!out) fail(HMDP_INVALID_ARGUMENT, "null out");
+        auto& g = ctx->gdd;
+        if (g.mode != 1 || g.C <= 0) fail(HMDP_INVALID_ARGUMENT, "halo mode not planned");
+        set_device(ctx);
+        const int W = g.world, M = ctx->n_msg();
+        std::vector<int> fc(W), rc(W);
+        ck(copy_sync(fc.data(), g.fcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
+        ck(copy_sync(rc.data(), g.rcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
+        long long fwd = 0, rev = 0;
+        for (int q = 0; q < W; ++q)
+            if (q != g.geom.rank) {
+                fwd += fc[q];
+                rev += rc[q];
+            }
+        const long long tb = g.prec == HMDP_FP64 ? 8 : 4;
+        const long long pos_row = 4 + (g.vel ? 48 : 24), p_row = 4 + kH * tb, f_row = 4 + 24;
+        // POS rows use last step's owned-near lists (close to fwd); P rows fwd; SUMS,
+        // FORCES rows rev; OUT 16 doubles per peer
+        const long long useful = fwd * pos_row + M * fwd * p_row + M * rev * p_row + rev * f_row +
+                                 (W - 1) * 128;
+        const long long moved =
+            (W - 1) * static_cast<long long>(round_bytes(g.C, g.vel ? 6 : 3, 8) +
+                                             M * round_bytes(g.C, kH, tb) * 2 +
+                                             round_bytes(g.C, 3, 8) + 128);
+        out[0] = g.C;
+        out[1] = 2 + 2 * M + (W > 1 ? 1 : 0);
+        out[2] = useful;
+        out[3] = moved;
+        out[4] = W - 1;
     });
 }
 

@@ -17,6 +17,7 @@ enum : unsigned {
     kErrZeroEdge = 1u << 2,      // zero-length edge (inference.cpp:221)
     kErrAsymmetric = 1u << 3,    // reverse edge missing in a "symmetric" list
     kErrNonFinite = 1u << 4,     // non-finite force (integrators.cpp:12-18)
+    kErrHaloOverflow = 1u << 5,  // a halo-exchange packet exceeded its row capacity
 };
 
 // One two-layer MLP [in, 32, out] on the device, stored both row-major (as in

@@ -24,6 +24,18 @@
 // The collectives are the caller's (NCCL all_reduce on the bound buffers, between
 // phases, on the same stream); an in-process sum over simulated ranks exercises the
 // same phases on one GPU.
+//
+// Halo-exchange mode (the default multi-GPU engine; hmdp_api.cu "gdd halo"): the
+// same phases, but nothing is replicated and nothing is all-reduced except (E, W,
+// W9).  Each rank integrates ONLY its owned atoms; per step, point-to-point rounds
+// with every peer move exactly the halo:
+//   POS     (x, v) of owned atoms near peer q's region      -> q   (+ migration)
+//   P^l     P rows of owned atoms near q's region           -> q   (per layer)
+//   SUMS^l  dE/dh partial sums at halo atoms                 -> their owners
+//   FORCES  partial forces at halo atoms                     -> their owners
+// Ownership is re-derived every step from the received positions (owner = region
+// of the wrapped position), so an atom that drifts into a neighbour's region is
+// migrated by the POS round itself (it is near -- inside -- that region).
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -35,45 +47,199 @@ struct GddGeom {
     double halo;   // halo width (rc)
 };
 
-// roles + lists: lists[0..n) owned, lists[n..2n) halo, lists[2n..3n) searched
-// (owned + halo); counts[0..2] their lengths (zeroed by the caller each step).
-__global__ void k_gdd_roles(int n, const double* __restrict__ pos, GddGeom g,
-                            unsigned char* __restrict__ role, int* __restrict__ lists,
-                            int* __restrict__ counts) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int rc3[3] = {g.rank % g.d[0], (g.rank / g.d[0]) % g.d[1], g.rank / (g.d[0] * g.d[1])};
-    bool owned = true;
+// Wrapped coordinate (wrap_position, box.hpp:34-42, as dd.owners).
+__device__ __forceinline__ double gdd_wrap(double r, double L) {
+    r = r - L * floor(r / L);
+    return r >= L ? 0.0 : r;
+}
+// Region (rank) owning a wrapped position: its cell of the rank grid.
+__device__ __forceinline__ int gdd_owner(const double* p, const GddGeom& g) {
+    int c3[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double r = gdd_wrap(p[a], g.L[a]);
+        int c = static_cast<int>(r / g.L[a] * g.d[a]);
+        c3[a] = c < 0 ? 0 : (c > g.d[a] - 1 ? g.d[a] - 1 : c);
+    }
+    return c3[0] + g.d[0] * (c3[1] + g.d[1] * c3[2]);
+}
+// Periodic distance from a position to rank q's region, tested against the halo
+// width.  The ONE predicate for "q needs this atom": the sender's send lists and
+// the receiver's halo role both use it on bitwise-identical positions, so they
+// always agree.  The ownership test and the slab bounds may disagree at a boundary
+// by rounding: the region's own atoms are always "near".
+__device__ __forceinline__ bool gdd_near(const double* p, const GddGeom& g, int q) {
+    const int q3[3] = {q % g.d[0], (q / g.d[0]) % g.d[1], q / (g.d[0] * g.d[1])};
     double dist2 = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
+        if (g.d[a] <= 1) continue;
         const double L = g.L[a];
-        double r = pos[3 * i + a];
-        r = r - L * floor(r / L);  // wrap_position (box.hpp:34-42), as dd.owners
-        if (r >= L) r = 0.0;
-        int c = static_cast<int>(r / L * g.d[a]);
-        c = c < 0 ? 0 : (c > g.d[a] - 1 ? g.d[a] - 1 : c);
-        if (c != rc3[a]) owned = false;
-        if (g.d[a] > 1) {  // periodic distance to this rank's slab [lo, hi)
-            const double lo = L * rc3[a] / g.d[a], hi = L * (rc3[a] + 1) / g.d[a];
-            double da = 0.0;
-            if (r < lo || r >= hi) {
-                double a1 = lo - r, a2 = r - hi;
-                a1 -= L * floor(a1 / L);
-                a2 -= L * floor(a2 / L);
-                da = a1 < a2 ? a1 : a2;
-            }
-            dist2 += da * da;
+        const double r = gdd_wrap(p[a], L);
+        const double lo = L * q3[a] / g.d[a], hi = L * (q3[a] + 1) / g.d[a];
+        double da = 0.0;
+        if (r < lo || r >= hi) {  // periodic distance to the slab [lo, hi)
+            double a1 = lo - r, a2 = r - hi;
+            a1 -= L * floor(a1 / L);
+            a2 -= L * floor(a2 / L);
+            da = a1 < a2 ? a1 : a2;
         }
+        dist2 += da * da;
     }
-    // the ownership test and the slab bounds may disagree at a boundary by rounding:
-    // an owned atom is always searched
-    const bool halo = !owned && dist2 <= g.halo * g.halo * (1.0 + 1e-9) + 1e-24;
+    return dist2 <= g.halo * g.halo * (1.0 + 1e-9) + 1e-24;
+}
+
+// roles + lists: lists[0..n) owned, lists[n..2n) halo, lists[2n..3n) searched
+// (owned + halo); counts[0..2] their lengths (zeroed by the caller each step).
+// Halo-exchange mode (stamp != null): only atoms whose position is current on this
+// rank take part -- owned here last step (role 1) or received this step (stamp ==
+// *cur); every other row of the global arrays is stale.
+__global__ void k_gdd_roles(int n, const double* __restrict__ pos, GddGeom g,
+                            unsigned char* __restrict__ role, int* __restrict__ lists,
+                            int* __restrict__ counts, const int* __restrict__ stamp,
+                            const int* __restrict__ cur) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (stamp && role[i] != 1 && stamp[i] != *cur) {
+        role[i] = 0;
+        return;
+    }
+    const bool owned = gdd_owner(pos + 3 * i, g) == g.rank;
+    const bool halo = !owned && gdd_near(pos + 3 * i, g, g.rank);
     const unsigned char ro = owned ? 1 : (halo ? 2 : 0);
     role[i] = ro;
     if (owned) lists[atomicAdd(counts + 0, 1)] = i;
     if (halo) lists[n + atomicAdd(counts + 1, 1)] = i;
     if (ro) lists[2 * n + atomicAdd(counts + 2, 1)] = i;
+}
+
+// ---------------------------------------------------------------------------
+// Halo exchange (point-to-point, per peer; hmdp_gdd halo mode).  Per round every
+// rank fills one fixed-capacity packet per peer and the transport (grouped
+// ncclSend/ncclRecv, or the caller) moves packet s->r into r's receive slot s.
+// Packet (C rows, C % 4 == 0): int count, 3 pad, int gidx[C], payload[C][W] (E).
+// Lists are [world][C] global indices; counts[world].
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t gdd_pkt_bytes(int C, int W, int esz) {
+    return 16 + static_cast<size_t>(C) * 4 + static_cast<size_t>(C) * W * esz;
+}
+
+// send lists: src atoms (a list) that are near peer q's region, for every q != rank
+// (forward rounds: owned atoms -> the peers whose halo they are in), or grouped by
+// owner (reverse rounds: halo atoms -> their owners, by_owner = 1).
+__global__ void k_gdd_send_lists(const int* __restrict__ src, const int* __restrict__ src_n,
+                                 const double* __restrict__ pos, GddGeom g, int world, int by_owner,
+                                 int C, int* __restrict__ lists, int* __restrict__ counts,
+                                 unsigned* err) {
+    const int ns = *src_n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += gridDim.x * blockDim.x) {
+        const int i = src[k];
+        const double* p = pos + 3 * i;
+        if (by_owner) {
+            const int q = gdd_owner(p, g);
+            if (q == g.rank) continue;
+            const int s = atomicAdd(counts + q, 1);
+            if (s < C) lists[q * C + s] = i;
+            else atomicOr(err, kErrHaloOverflow);
+        } else {
+            for (int q = 0; q < world; ++q) {
+                if (q == g.rank || !gdd_near(p, g, q)) continue;
+                const int s = atomicAdd(counts + q, 1);
+                if (s < C) lists[q * C + s] = i;
+                else atomicOr(err, kErrHaloOverflow);
+            }
+        }
+    }
+}
+
+// pack: payload columns [0, w0) from src0 rows, [w0, w0 + w1) from src1 rows
+template <typename E>
+__global__ void k_gdd_pack(int world, int rank, const int* __restrict__ lists,
+                           const int* __restrict__ counts, int C, const E* __restrict__ src0,
+                           int w0, const E* __restrict__ src1, int w1, char* __restrict__ pkts,
+                           size_t pkt_bytes) {
+    const int q = blockIdx.y;
+    if (q == rank) return;
+    const int W = w0 + w1;
+    const int cnt = min(counts[q], C);
+    char* pk = pkts + q * pkt_bytes;
+    int* head = reinterpret_cast<int*>(pk);
+    int* gid = head + 4;
+    E* pay = reinterpret_cast<E*>(pk + 16 + static_cast<size_t>(C) * 4);
+    if (blockIdx.x == 0 && threadIdx.x == 0) head[0] = cnt;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt * W; t += gridDim.x * blockDim.x) {
+        const int k = t / W, c = t - k * W;
+        const long long i = lists[q * C + k];
+        if (c == 0) gid[k] = static_cast<int>(i);
+        pay[static_cast<size_t>(k) * W + c] = c < w0 ? src0[i * w0 + c] : src1[i * w1 + (c - w0)];
+    }
+}
+
+// unpack (copy): rows of every peer's packet into dst0/dst1 at their global index;
+// stamp (nullable) marks the received atoms current for this step
+template <typename E>
+__global__ void k_gdd_unpack_copy(int world, int rank, int C, const char* __restrict__ pkts,
+                                  size_t pkt_bytes, E* __restrict__ dst0, int w0,
+                                  E* __restrict__ dst1, int w1, int* __restrict__ stamp,
+                                  const int* __restrict__ cur) {
+    const int q = blockIdx.y;
+    if (q == rank) return;
+    const int W = w0 + w1;
+    const char* pk = pkts + q * pkt_bytes;
+    const int* head = reinterpret_cast<const int*>(pk);
+    const int* gid = head + 4;
+    const E* pay = reinterpret_cast<const E*>(pk + 16 + static_cast<size_t>(C) * 4);
+    const int cnt = min(head[0], C);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt * W; t += gridDim.x * blockDim.x) {
+        const int k = t / W, c = t - k * W;
+        const long long i = gid[k];
+        const E v = pay[static_cast<size_t>(k) * W + c];
+        if (c < w0) dst0[i * w0 + c] = v;
+        else dst1[i * w1 + (c - w0)] = v;
+        if (stamp && c == 0) stamp[i] = *cur;
+    }
+}
+
+// unpack (add): peer q's rows added into dst at their global index.  One launch per
+// peer, in rank order: an atom that is a halo atom on several peers receives their
+// partials in a fixed order (bitwise-deterministic sums, no float atomics).
+template <typename E>
+__global__ void k_gdd_unpack_add(int q, int C, const char* __restrict__ pkts, size_t pkt_bytes,
+                                 E* __restrict__ dst, int W) {
+    const char* pk = pkts + q * pkt_bytes;
+    const int* head = reinterpret_cast<const int*>(pk);
+    const int* gid = head + 4;
+    const E* pay = reinterpret_cast<const E*>(pk + 16 + static_cast<size_t>(C) * 4);
+    const int cnt = min(head[0], C);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt * W; t += gridDim.x * blockDim.x) {
+        const int k = t / W, c = t - k * W;
+        dst[static_cast<long long>(gid[k]) * W + c] += pay[static_cast<size_t>(k) * W + c];
+    }
+}
+
+__global__ void k_gdd_tick(int* cur) { *cur += 1; }
+
+// OUT round: (E, W, W9) partials into every peer's packet slot; the totals are the
+// rank-ordered sum of all ranks' partials (own partial read from `out` itself), so
+// every rank ends with bitwise the same totals.
+__global__ void k_gdd_out_pack(int world, int rank, const double* __restrict__ out,
+                               char* __restrict__ pkts, size_t stride) {
+    const int q = blockIdx.x, k = threadIdx.x;
+    if (q != rank && k < 16) reinterpret_cast<double*>(pkts + q * stride)[k] = out[k];
+}
+__global__ void k_gdd_sum_out(int world, int rank, const char* __restrict__ pkts, size_t stride,
+                              double* __restrict__ out) {
+    const int k = threadIdx.x;
+    if (k >= 11) return;
+    double s = 0.0;
+    for (int q = 0; q < world; ++q)
+        s += q == rank ? out[k] : reinterpret_cast<const double*>(pkts + q * stride)[k];
+    __syncwarp();
+    out[k] = s;
+}
+__global__ void k_gdd_stamp_all(int n, int* __restrict__ stamp, const int* __restrict__ cur) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) stamp[i] = *cur + 1;  // current for the next step
 }
 
 // Mirror slots of the searched rows (one warp per atom); rows of atoms that are
@@ -164,10 +330,16 @@ __global__ void k_gdd_halo_sums(DevGraph gr, const T* __restrict__ d, T* __restr
 // Velocity Verlet on every atom from the all-reduced forces: closing kick of this
 // step, opening kick of the next, drift (integrators.cpp:32-47, the split the
 // single-GPU device MD loop fuses into its force kernel).
+// (Halo mode: only the atoms of `list` -- this rank's owned atoms.)
 __global__ void k_gdd_integrate(int n, const double* __restrict__ f, double* __restrict__ x,
                                 double* __restrict__ v, const double* __restrict__ m, double half,
-                                double dt, int mode, unsigned* err) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                                double dt, int mode, unsigned* err, const int* __restrict__ list,
+                                const int* __restrict__ list_n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (list) {
+        if (i >= *list_n) return;
+        i = list[i];
+    }
     if (i >= n) return;
     const double s = half / m[i];
     bool finite = true;
@@ -185,8 +357,52 @@ __global__ void k_gdd_integrate(int n, const double* __restrict__ f, double* __r
 }
 
 void launch_gdd_roles(int n, const double* pos, const GddGeom& g, unsigned char* role, int* lists,
-                      int* counts, cudaStream_t st) {
-    k_gdd_roles<<<(n + 255) / 256, 256, 0, st>>>(n, pos, g, role, lists, counts);
+                      int* counts, cudaStream_t st, const int* stamp, const int* cur) {
+    k_gdd_roles<<<(n + 255) / 256, 256, 0, st>>>(n, pos, g, role, lists, counts, stamp, cur);
+}
+void launch_gdd_send_lists(const int* src, const int* src_n, int n_est, const double* pos,
+                           const GddGeom& g, int world, int by_owner, int C, int* lists,
+                           int* counts, unsigned* err, cudaStream_t st) {
+    const int blocks = (n_est + 255) / 256;
+    k_gdd_send_lists<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(src, src_n, pos, g, world, by_owner, C,
+                                                              lists, counts, err);
+}
+template <typename E>
+void launch_gdd_pack(int world, int rank, const int* lists, const int* counts, int C, const E* src0,
+                     int w0, const E* src1, int w1, char* pkts, size_t pkt_bytes, cudaStream_t st) {
+    const int work = C * (w0 + w1);
+    const int bx = (work + 255) / 256;
+    k_gdd_pack<E><<<dim3(bx < 1 ? 1 : (bx > 64 ? 64 : bx), world), 256, 0, st>>>(
+        world, rank, lists, counts, C, src0, w0, src1, w1, pkts, pkt_bytes);
+}
+template <typename E>
+void launch_gdd_unpack_copy(int world, int rank, int C, const char* pkts, size_t pkt_bytes, E* dst0,
+                            int w0, E* dst1, int w1, int* stamp, const int* cur, cudaStream_t st) {
+    const int work = C * (w0 + w1);
+    const int bx = (work + 255) / 256;
+    k_gdd_unpack_copy<E><<<dim3(bx < 1 ? 1 : (bx > 64 ? 64 : bx), world), 256, 0, st>>>(
+        world, rank, C, pkts, pkt_bytes, dst0, w0, dst1, w1, stamp, cur);
+}
+template <typename E>
+void launch_gdd_unpack_add(int world, int rank, int C, const char* pkts, size_t pkt_bytes, E* dst,
+                           int W, cudaStream_t st) {
+    const int bx = (C * W + 255) / 256;
+    for (int q = 0; q < world; ++q)
+        if (q != rank)
+            k_gdd_unpack_add<E><<<bx < 1 ? 1 : (bx > 64 ? 64 : bx), 256, 0, st>>>(q, C, pkts,
+                                                                              pkt_bytes, dst, W);
+}
+void launch_gdd_tick(int* cur, cudaStream_t st) { k_gdd_tick<<<1, 1, 0, st>>>(cur); }
+void launch_gdd_out_pack(int world, int rank, const double* out, char* pkts, size_t stride,
+                         cudaStream_t st) {
+    k_gdd_out_pack<<<world, 32, 0, st>>>(world, rank, out, pkts, stride);
+}
+void launch_gdd_sum_out(int world, int rank, const char* pkts, size_t stride, double* out,
+                        cudaStream_t st) {
+    k_gdd_sum_out<<<1, 32, 0, st>>>(world, rank, pkts, stride, out);
+}
+void launch_gdd_stamp_all(int n, int* stamp, const int* cur, cudaStream_t st) {
+    k_gdd_stamp_all<<<(n + 255) / 256, 256, 0, st>>>(n, stamp, cur);
 }
 static int warp_grid(int n_est) {
     const int blocks = (n_est * 32 + 255) / 256;
@@ -212,8 +428,10 @@ void launch_gdd_halo_sums(const DevGraph& gr, int n_est, const T* d, T* out, con
     k_gdd_halo_sums<T><<<warp_grid(n_est), 256, 0, st>>>(gr, d, out, hlist, hcount);
 }
 void launch_gdd_integrate(int n, const double* f, double* x, double* v, const double* m,
-                          double dt, int mode, unsigned* err, cudaStream_t st) {
-    k_gdd_integrate<<<(n + 255) / 256, 256, 0, st>>>(n, f, x, v, m, 0.5 * dt, dt, mode, err);
+                          double dt, int mode, unsigned* err, cudaStream_t st, const int* list,
+                          const int* list_n) {
+    k_gdd_integrate<<<(n + 255) / 256, 256, 0, st>>>(n, f, x, v, m, 0.5 * dt, dt, mode, err, list,
+                                                     list_n);
 }
 
 #define HMDP_GDD_INST(T)                                                                       \
@@ -225,5 +443,14 @@ void launch_gdd_integrate(int n, const double* f, double* x, double* v, const do
                                           const int*, cudaStream_t);
 HMDP_GDD_INST(float)
 HMDP_GDD_INST(double)
+#define HMDP_GDD_PKT_INST(E)                                                                      \
+    template void launch_gdd_pack<E>(int, int, const int*, const int*, int, const E*, int,        \
+                                     const E*, int, char*, size_t, cudaStream_t);                 \
+    template void launch_gdd_unpack_copy<E>(int, int, int, const char*, size_t, E*, int, E*, int, \
+                                            int*, const int*, cudaStream_t);                      \
+    template void launch_gdd_unpack_add<E>(int, int, int, const char*, size_t, E*, int,           \
+                                           cudaStream_t);
+HMDP_GDD_PKT_INST(float)
+HMDP_GDD_PKT_INST(double)
 
 }  // namespace hmdp

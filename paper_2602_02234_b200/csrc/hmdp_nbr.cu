@@ -212,6 +212,23 @@ int num_sms() {
     return sms_cached;
 }
 
+// Binning of a list of atoms only (halo-exchange DD: the other rows are stale).
+__global__ void k_cell_bin_list(const int* __restrict__ list, const int* __restrict__ list_n,
+                                const double* __restrict__ pos, CellGrid cg,
+                                int* __restrict__ cell_count, int* __restrict__ members,
+                                int* __restrict__ cell_of, unsigned* err) {
+    const int cnt = *list_n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const int i = list[k];
+        bin_atom(i, pos + 3 * i, cg, cell_count, members, cell_of, err);
+    }
+}
+void launch_cell_bin_list(const int* list, const int* list_n, int n_max, const double* pos,
+                          const CellGrid& cg, int* cell_count, int* members, int* cell_of,
+                          unsigned* err, cudaStream_t st) {
+    k_cell_bin_list<<<(n_max + 127) / 128, 128, 0, st>>>(list, list_n, pos, cg, cell_count,
+                                                         members, cell_of, err);
+}
 void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_count, int* members,
                      int* cell_of, unsigned* err, cudaStream_t st) {
     k_cell_bin<<<(n + 127) / 128, 128, 0, st>>>(n, pos, cg, cell_count, members, cell_of, err);

@@ -506,3 +506,188 @@ def run_local(engines, kind="eval", dt=0.001):
             tot += b
         for b in bufs:
             b.copy_(tot)
+
+
+# ---------------------------------------------------------------------------
+# Halo-exchange engine (the multi-GPU default): hmdp_gdd_* in halo mode.
+# ---------------------------------------------------------------------------
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t)
+
+
+class HaloDD:
+    """One rank's halo-exchange DD engine (include/hmdp.h, hmdp_gdd_* halo mode).
+
+    Nothing is replicated: the rank integrates only the atoms its region owns and
+    every step moves exactly the halo with point-to-point rounds to every peer
+    (POS with migration, P^l per message layer forward, dE/dh partial sums per layer
+    and partial forces back to the owners, (E, W, W9) partials).  The whole step --
+    exchanges included -- is one C++ call (``step``), capturable in a CUDA graph
+    with the NCCL transport.  Transports: ``attach_nccl`` (one GPU per rank),
+    ``attach_hub`` (ranks simulated as contexts on one GPU, one host thread each) or
+    ``attach_callback`` (a Python exchange, e.g. gloo).
+
+    Global-index buffers: only the rows of owned (and halo) atoms are current on a
+    rank; ``owned_forces`` returns this rank's share of the global result."""
+
+    def __init__(self, ctx, n, types, box, dims, rank, precision, masses=None, stream=None):
+        import torch
+
+        self.ctx, self.n, self.rank = ctx, int(n), int(rank)
+        self.dims = tuple(int(d) for d in dims)
+        self.world = self.dims[0] * self.dims[1] * self.dims[2]
+        self.depth = ctx.model.depth()
+        dev = torch.device("cuda", ctx.device)
+        self.dev = dev
+        self.pos = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.vel = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.mass = torch.ones(n, dtype=torch.float64, device=dev)
+        self.f = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.out = torch.zeros(16, dtype=torch.float64, device=dev)
+        if masses is not None:
+            self.mass.copy_(torch.as_tensor(np.asarray(masses, dtype=np.float64)))
+        L = lib()
+        if stream is not None:  # run on the caller's stream (graph capture, NCCL ordering)
+            check(L.hmdp_set_stream(ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
+        t = np.ascontiguousarray(types, dtype=np.int32)
+        b = np.ascontiguousarray(box, dtype=np.float64)
+        d = np.ascontiguousarray(self.dims, dtype=np.int32)
+        check(L.hmdp_gdd_setup(ctx.handle, self.n, ptr(t), ptr(b), ptr(d), self.rank,
+                               int(precision)))
+        check(L.hmdp_gdd_set_mode(ctx.handle, 1))
+        for kind, ten in ((0, self.pos), (3, self.f), (4, self.out), (5, self.vel),
+                          (6, self.mass)):
+            check(L.hmdp_gdd_bind(ctx.handle, kind, ctypes.c_void_p(ten.data_ptr())))
+        self._cb = None
+
+    def load(self, positions, velocities=None):
+        """Every rank loads the full initial configuration; plans the packet capacity."""
+        import torch
+
+        self.pos.copy_(torch.as_tensor(np.asarray(positions, dtype=np.float64).reshape(-1, 3)))
+        if velocities is not None:
+            self.vel.copy_(torch.as_tensor(np.asarray(velocities, dtype=np.float64).reshape(-1, 3)))
+        torch.cuda.synchronize(self.dev)
+        check(lib().hmdp_gdd_plan(self.ctx.handle))
+
+    def attach_nccl(self, unique_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(lib().hmdp_gdd_attach_nccl(self.ctx.handle, buf, self.world, self.rank))
+
+    def attach_hub(self, hub):
+        check(lib().hmdp_gdd_attach_hub(self.ctx.handle, hub))
+
+    def attach_callback(self, fn):
+        """fn(round, send_ptr, recv_ptr, stride, nbytes) -> None: move the first nbytes of
+        packet send + q*stride to peer q's recv + rank*stride (device pointers)."""
+        def trampoline(user, rnd, send, recv, stride, nbytes):
+            try:
+                fn(int(rnd), int(send), int(recv), int(stride), int(nbytes))
+                return 0
+            except Exception:  # surfaced as HMDP_RUNTIME_ERROR by the step
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._cb = EXCHANGE_FN(trampoline)  # keep alive
+        check(lib().hmdp_gdd_attach_callback(self.ctx.handle, ctypes.cast(self._cb, ctypes.c_void_p),
+                                             None))
+
+    def step(self, kind="eval", dt=0.001):
+        k = {"eval": 0, "md": 1, "open": 2}[kind]
+        check(lib().hmdp_gdd_step(self.ctx.handle, k, float(dt)))
+
+    def roles(self):
+        r = np.zeros(self.n, dtype=np.uint8)
+        check(lib().hmdp_gdd_roles(self.ctx.handle, ptr(r)))
+        return r
+
+    def owned_forces(self):
+        """(owned mask, forces [n][3] with only the owned rows meaningful)."""
+        own = self.roles() == 1
+        return own, self.f.cpu().numpy()
+
+    def sync(self):
+        c = np.zeros(3, dtype=np.int32)
+        check(lib().hmdp_gdd_counts(self.ctx.handle, ptr(c)))  # synchronizes the rank's stream
+
+    def energy_virial(self):
+        self.sync()
+        o = self.out.cpu().numpy()
+        return float(o[0]), float(o[1]), o[2:11].reshape(3, 3)
+
+    def halo_stats(self):
+        v = (ctypes.c_longlong * 5)()
+        check(lib().hmdp_gdd_halo_stats(self.ctx.handle, v))
+        return {"capacity_rows": v[0], "rounds_per_step": v[1], "halo_bytes_per_step": v[2],
+                "transferred_bytes_per_step": v[3], "peers": v[4]}
+
+    def launches(self):
+        v = ctypes.c_longlong()
+        check(lib().hmdp_gdd_launches(self.ctx.handle, ctypes.byref(v)))
+        return int(v.value)
+
+
+class Hub:
+    """In-process transport: ranks simulated as contexts on one GPU (hmdp_gdd_hub)."""
+
+    def __init__(self, world):
+        h = ctypes.c_void_p()
+        check(lib().hmdp_gdd_hub_create(int(world), ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().hmdp_gdd_hub_destroy(self.handle)
+            self.handle = None
+
+
+def run_hub(engines, kind="eval", dt=0.001, steps=1):
+    """Run `steps` steps of every simulated rank, one host thread per rank (the hub's
+    exchange points are barriers across the threads)."""
+    import threading
+
+    errs = []
+
+    def work(e):
+        try:
+            for _ in range(steps):
+                e.step(kind, dt)
+        except Exception as exc:  # re-raised below
+            errs.append(exc)
+
+    th = [threading.Thread(target=work, args=(e,)) for e in engines]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def gloo_exchange(engine: HaloDD, group=None):
+    """A callback transport over torch.distributed (gloo; tests / dry runs): the
+    packets go device -> host -> all_to_all -> host -> device."""
+    import torch
+    import torch.distributed as td
+
+    cudart = lib()  # libcudart is a dependency of libhmdp: its symbols resolve here
+    cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    W, R = engine.world, engine.rank
+
+    def fn(rnd, send, recv, stride, nbytes):
+        host = torch.empty(W * stride, dtype=torch.uint8)
+        if cudart.cudaMemcpy(ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(send), W * stride, 2):
+            raise RuntimeError("cudaMemcpy D2H failed")
+        out = torch.empty_like(host)
+        td.all_to_all_single(out, host, group=group)  # slot q of mine -> slot R of q's
+        # only the first nbytes of every slot are meaningful; slot R stays as it was
+        if cudart.cudaMemcpy(ctypes.c_void_p(recv), ctypes.c_void_p(out.data_ptr()), W * stride, 1):
+            raise RuntimeError("cudaMemcpy H2D failed")
+        # a pageable H2D cudaMemcpy may return before its DMA lands: complete it before
+        # the engine's (non-blocking) stream unpacks
+        if cudart.cudaDeviceSynchronize():
+            raise RuntimeError("cudaDeviceSynchronize failed")
+
+    engine.attach_callback(fn)

@@ -1,0 +1,172 @@
+"""Halo-exchange domain decomposition (hmdp_gdd_* halo mode, dd.HaloDD): ranks own
+disjoint regions, integrate only their own atoms and exchange exactly the halo with
+point-to-point rounds (POS with migration, P^l, dE/dh partial sums, partial forces,
+(E, W, W9)).  Ranks are simulated as contexts on cuda:0 (the in-process hub: one
+host thread per rank, the same C++ step program the NCCL transport runs), and as
+two real processes with a gloo callback transport.  Checked against the
+single-domain evaluation and the single-GPU device MD loop."""
+import numpy as np
+import pytest
+
+import paper_2602_02234_b200 as P
+from conftest import E_TOL, F_TOL, rms
+from paper_2602_02234_b200 import dd
+
+pytestmark = pytest.mark.gpu
+
+
+def _engines(m, s, dims, prec, masses=None):
+    world = dims[0] * dims[1] * dims[2]
+    hub = dd.Hub(world)
+    engs = [dd.HaloDD(P.Context(m, max_atoms=s.n_atoms), s.n_atoms, s.types, s.box, dims, r, prec,
+                      masses=masses) for r in range(world)]
+    for e in engs:
+        e.attach_hub(hub.handle)
+        e.load(s.positions, s.velocities if masses is not None else None)
+    return hub, engs
+
+
+def _assemble(engs, n):
+    F = np.full((n, 3), np.nan)
+    owned = np.zeros(n, dtype=int)
+    for e in engs:
+        own, f = e.owned_forces()
+        F[own] = f[own]
+        owned += own
+    return F, owned
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2)])
+def test_halo_dd_matches_single_domain(mname, dims, golden_models):
+    s = P.generate_synthetic_system(1231)
+    m = P.model_from_json(golden_models[mname])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    hub, engs = _engines(m, s, dims, P.Precision.fp64)
+    dd.run_hub(engs, "eval")
+    F, owned = _assemble(engs, s.n_atoms)
+    assert np.all(owned == 1)  # every atom owned by exactly one rank
+    for e in engs:  # every rank ends with the same totals (rank-ordered sum)
+        E, W, W9 = e.energy_virial()
+        assert E == pytest.approx(ref.energy, rel=1e-12)
+        assert np.abs(W9 - ref.virial_tensor).max() < 1e-9 * max(1.0, np.abs(W9).max())
+    assert np.abs(F - ref.forces).max() < 1e-10 * np.abs(ref.forces).max()
+    st = engs[0].halo_stats()
+    assert st["peers"] == len(engs) - 1 and st["halo_bytes_per_step"] > 0
+    assert st["rounds_per_step"] == 2 + 2 * (m.depth() - 1) + 1
+    hub.close()
+
+
+def test_halo_dd_fp32_within_tolerance(golden_models):
+    s = P.generate_synthetic_system(2643)
+    m = P.model_from_json(golden_models["dpa3"])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    hub, engs = _engines(m, s, (2, 2, 1), P.Precision.fp32)
+    dd.run_hub(engs, "eval")
+    F, owned = _assemble(engs, s.n_atoms)
+    E = engs[0].energy_virial()[0]
+    assert abs(E - ref.energy) <= E_TOL * abs(ref.energy)
+    assert np.abs(F - ref.forces).max() <= F_TOL * rms(ref.forces)
+    hub.close()
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+def test_halo_dd_md_matches_device_md(mname, golden_models):
+    """60 MD steps, each rank integrating only its own atoms (atoms migrate between
+    regions on the way), equal the single-GPU device MD loop in FP64."""
+    from paper_2602_02234_b200.md import DeviceMD
+
+    s = P.generate_synthetic_system(1231, temperature=300.0)
+    m = P.model_from_json(golden_models[mname])
+    md = DeviceMD(P.Context(m), s.positions, s.velocities, s.masses, s.types, s.box,
+                  precision=P.Precision.fp64, steps_per_graph=1)
+    md.run(60)
+    x_ref, v_ref, f_ref, e_ref = md.state()
+    hub, engs = _engines(m, s, (2, 2, 1), P.Precision.fp64, masses=s.masses)
+    dd.run_hub(engs, "eval")
+    dd.run_hub(engs, "open", 0.001)
+    own0 = engs[0].roles() == 1
+    dd.run_hub(engs, "md", 0.001, steps=60)
+    x = np.full((s.n_atoms, 3), np.nan)
+    v = np.full((s.n_atoms, 3), np.nan)
+    owned = np.zeros(s.n_atoms, dtype=int)
+    for e in engs:
+        own = e.roles() == 1
+        x[own] = e.pos.cpu().numpy()[own]
+        v[own] = e.vel.cpu().numpy()[own]
+        owned += own
+    assert np.all(owned == 1)
+    assert (engs[0].roles() == 1).sum() != own0.sum() or not np.array_equal(
+        engs[0].roles() == 1, own0)  # ownership changed: atoms migrated
+    # the engines hold the next step's drifted positions: x(t + dt) = x(t) + dt v(t + dt/2)
+    assert np.abs(x - 0.001 * v - x_ref).max() < 1e-10
+    assert engs[0].energy_virial()[0] == pytest.approx(e_ref, rel=1e-11)
+    hub.close()
+
+
+def _gloo_worker(rank, world, port, model_json, q):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = P.generate_synthetic_system(1231, temperature=300.0)
+        m = P.model_from_json(model_json)
+        eng = dd.HaloDD(P.Context(m, max_atoms=1231), 1231, s.types, s.box, (2, 1, 1), rank,
+                        P.Precision.fp64, masses=s.masses)
+        dd.gloo_exchange(eng)
+        eng.load(s.positions, s.velocities)
+        eng.step("eval")
+        E = eng.energy_virial()[0]
+        own, F = eng.owned_forces()
+        eng.step("open", 0.001)
+        for _ in range(3):
+            eng.step("md", 0.001)
+        torch.cuda.synchronize()
+        ownx = eng.roles() == 1
+        q.put((rank, E, own, F, ownx, eng.pos.cpu().numpy()))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+def test_halo_dd_two_processes_gloo(mname, golden_models):
+    """Two processes (torch.distributed gloo as the caller transport) run the same C++
+    step program and equal the single-domain evaluation and the hub's MD."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, golden_models[mname], q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s = P.generate_synthetic_system(1231, temperature=300.0)
+    m = P.model_from_json(golden_models[mname])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    F = np.full((1231, 3), np.nan)
+    for rank, E, own, f, ownx, x in res:
+        assert E == pytest.approx(ref.energy, rel=1e-12)
+        F[own] = f[own]
+    assert np.abs(F - ref.forces).max() < 1e-10 * np.abs(ref.forces).max()
+    hub, engs = _engines(m, s, (2, 1, 1), P.Precision.fp64, masses=s.masses)
+    dd.run_hub(engs, "eval")
+    dd.run_hub(engs, "open", 0.001)
+    dd.run_hub(engs, "md", 0.001, steps=3)
+    for (rank, E, own, f, ownx, x), e in zip(res, engs):
+        assert np.array_equal(ownx, e.roles() == 1)
+        assert np.array_equal(x[ownx], e.pos.cpu().numpy()[ownx])  # bitwise: same program
+    hub.close()
