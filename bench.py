@@ -76,11 +76,12 @@ def parse():
     ap.add_argument("--strong", action="store_true",
                     help="--mode dd: split ONE box over the ranks (strong scaling, SURVEY "
                          "§8(d) configs 3/4) instead of one box per rank")
-    ap.add_argument("--mode", choices=["dd", "dd-host", "replicas"], default="dd",
-                    help="N>1: device-resident spatial domain decomposition of the box "
-                         "replicated over the rank grid (default; one CUDA graph per MD step "
-                         "with the NCCL halo all-reduces inside), the host-orchestrated DD "
-                         "(dd-host), or independent replica boxes (replicas)")
+    ap.add_argument("--mode", choices=["dd", "dd-allreduce", "replicas"], default="dd",
+                    help="N>1: halo-exchange spatial domain decomposition of the box "
+                         "replicated over the rank grid (default; point-to-point NCCL halo "
+                         "rounds, one CUDA graph per MD step), the replicated all-reduce "
+                         "variant for tiny boxes (dd-allreduce), or independent replica "
+                         "boxes (replicas)")
     return ap.parse_args()
 
 
@@ -750,13 +751,15 @@ def run_gdd(args, rank, world, local_rank, dist):
     print(json.dumps(line), flush=True)
 
 
-def run_dd(args, rank, world, local_rank, dist):
-    """N > 1: domain-decomposed force evaluation (weak scaling).  The global box
-    is the per-rank box replicated over the rank grid (1x1x1, 2x1x1, 2x2x1,
-    2x2x2), so each GPU owns one box's worth of atoms.  A step = device neighbour
-    list of the global box, halo plans, and the DD evaluation with its NCCL halo
-    rounds (P^l forward, dE/dh partials backward, ghost forces) plus the (E, W)
-    all-reduce.  value = world * steps / max-over-ranks time (box-steps/s)."""
+def run_halo(args, rank, world, local_rank, dist):
+    """N > 1, --mode dd (default): the halo-exchange domain decomposition (dd.HaloDD,
+    hmdp_gdd_* halo mode).  Global box = the per-rank box replicated over the rank grid
+    (weak scaling, one box per GPU) or, with --strong, one box split over the ranks.
+    Every rank integrates only the atoms its region owns; each MD step moves exactly
+    the halo with point-to-point NCCL rounds to every peer (POS with migration, P^l,
+    dE/dh partial sums, partial forces, (E, W) partials) issued from C++ on the
+    step's stream, and the whole step -- NCCL included -- is one CUDA graph per rank.
+    value = boxes * steps / max-over-ranks time."""
     import numpy as np
     import torch
 
@@ -769,82 +772,152 @@ def run_dd(args, rank, world, local_rank, dist):
     torch.cuda.set_stream(stream)
     prec = P.Precision[args.precision]
     model = make_bench_model(P, args.model)
+    if model.is_dp():
+        raise SystemExit("--mode dd: the DeePMD-style families run replicas only (DESIGN.md §11)")
     base = P.generate_synthetic_system(SYSTEMS[args.system])
     dims = dd.rank_grid(world)
-    s = P.replicate(base, dims)
+    s = base if args.strong else P.replicate(base, dims)
+    boxes = 1 if args.strong else world
     n = s.n_atoms
-    eng = dd.GpuEngine(P.Context(model, device=local_rank, max_atoms=n), prec)
+    eng = dd.HaloDD(P.Context(model, device=local_rank, max_atoms=n), n, s.types, s.box, dims,
+                    rank, prec, masses=s.masses, stream=stream)
+    use_nccl = dist.get_backend() == "nccl"
+    if use_nccl:  # our own communicator: the C++ engine issues ncclSend/ncclRecv itself
+        import ctypes
 
-    class TimedTransport(dd.TorchDistTransport):
-        halo_ms = 0.0
-        rounds = 0
+        from paper_2602_02234_b200._lib import check, lib
 
-        def exchange(self, send, width, like):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            out = super().exchange(send, width, like)
-            b.record()
-            b.synchronize()
-            TimedTransport.halo_ms += a.elapsed_time(b)
-            TimedTransport.rounds += 1
-            return out
-
-    tr = TimedTransport()
-    gidx = np.arange(n)
-
-    def step():
-        inp = P.build_input_periodic(s.positions, s.types, gidx, s.box, 0.6, device=local_rank)
-        own = dd.owners(s.positions, s.box, dims)
-        plans = dd.make_plans(inp.edge_offset, inp.edge_neighbor, inp.edge_dr, s.types, own, world)
-        return dd.evaluate_dd(eng, tr, plans, rank, model.depth()), plans
-
-    for _ in range(max(args.warmup, 1)):
-        (E, F, W, W9), plans = step()
-    e_single = P.Context(model, device=local_rank).compute(base.positions, base.types, base.box,
-                                                           P.Precision.fp64).energy
-    K = args.steps
-    TimedTransport.halo_ms, TimedTransport.rounds = 0.0, 0
-    dist.barrier()
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(lib().hmdp_nccl_unique_id(uid))
+        obj = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng.attach_nccl(obj[0])
+    else:  # dry run with ranks sharing a GPU (BENCH_DD_BACKEND=gloo)
+        dd.gloo_exchange(eng)
+    eng.load(s.positions, s.velocities)
+    eng.step("eval")
+    E = eng.energy_virial()[0]  # energy of the initial configuration (extensivity check)
+    eng.step("open", 0.001)
+    for _ in range(max(args.warmup, 3)):
+        l0 = eng.launches()
+        eng.step("md", 0.001)
+        per_step_kernels = eng.launches() - l0
     torch.cuda.synchronize(dev)
+    g = None
+    if use_nccl and not os.environ.get("BENCH_DD_NOGRAPH"):
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                eng.step("md", 0.001)
+            g.replay()
+        except Exception as exc:  # symmetric on every rank: all fall back to direct launches
+            print(f"rank {rank}: graph capture failed ({exc}); direct launches", file=sys.stderr)
+            g = None
+    torch.cuda.synchronize(dev)
+    K = args.steps
+    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(K):
-        (E, F, W, W9), plans = step()
+        if g is not None:
+            g.replay()
+        else:
+            eng.step("md", 0.001)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     dist.barrier()
     t_ms = e0.elapsed_time(e1)
-    tt = torch.tensor([t_ms, TimedTransport.halo_ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t_ms, halo_ms = float(tt[0]), float(tt[1])
-    value = world * K / (t_ms * 1e-3)
+    stats = eng.halo_stats()
+    # e2e: every step the positions come in from pinned host memory and the step's
+    # result (positions, forces, (E, W)) goes back to pinned host memory, read by the host
+    KE = min(K, 300)
+    x_h = torch.empty_like(eng.pos, device="cpu").pin_memory()
+    f_h = torch.empty_like(eng.f, device="cpu").pin_memory()
+    o_h = torch.empty_like(eng.out, device="cpu").pin_memory()
+    x_h.copy_(eng.pos)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    e_host = 0.0
+    for _ in range(KE):
+        eng.pos.copy_(x_h, non_blocking=True)
+        if g is not None:
+            g.replay()
+        else:
+            eng.step("md", 0.001)
+        x_h.copy_(eng.pos, non_blocking=True)
+        f_h.copy_(eng.f, non_blocking=True)
+        o_h.copy_(eng.out, non_blocking=True)
+        stream.synchronize()
+        e_host += float(o_h[0])  # the host reads the step's energy
+    eb.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = ea.elapsed_time(eb)
+    tt = torch.tensor([t_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if use_nccl:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    else:
+        tc = tt.cpu()
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        tt = tc
+    t_ms, e2e_ms = float(tt[0]), float(tt[1])
+    value = boxes * K / (t_ms * 1e-3)
+    e2e_value = boxes * KE / (e2e_ms * 1e-3)
+    roles = eng.roles()
     if rank != 0:
         return
-    p = plans[rank]
+    e_single = P.Context(model, device=local_rank).compute(base.positions, base.types, base.box,
+                                                           P.Precision.fp64).energy
     line = {
         "metric": METRIC, "value": value, "unit": f"steps/s ({args.system}-box equivalents)",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
-        "config": {"workload": f"{args.model.upper()} domain-decomposed force evaluation, "
-                               f"{args.system} box replicated {dims} (one box per GPU)",
+        "config": {"workload": f"{args.model.upper()} domain-decomposed MD step, " + (
+                       f"one {args.system} box split over {dims}" if args.strong else
+                       f"{args.system} box replicated {dims} (one box per GPU)"),
                    "model": args.model, "system": args.system, "atoms_total": n,
                    "rank_grid": list(dims), "precision": args.precision,
-                   "parallelism": f"spatial DD x{world}, rc halo exchanged per message layer "
-                                  f"(NCCL all_to_all), E/W all-reduce",
-                   "rank0_owned": p.n_own, "rank0_ghosts": int(p.ghosts.shape[0])},
-        "ns_per_day_per_box": ns_per_day(value / world),
-        "halo": {"ms_per_step": halo_ms / K, "rounds_per_step": TimedTransport.rounds / K,
-                 "share": halo_ms / t_ms},
-        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * world,
-                        "rel_diff": abs(E - e_single * world) / abs(e_single * world)},
-        "gpu_launches": None,
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": None,
-                "d2h_bytes_per_step": None,
-                "note": "host-orchestrated DD step (host CSR + plans each step)"},
+                   "parallelism": f"spatial DD x{world}, rc-deep halo exchanged per layer with "
+                                  f"point-to-point {'NCCL' if use_nccl else 'gloo'} rounds; owners "
+                                  f"integrate their own atoms (migration every step)",
+                   "graph": "one CUDA graph per MD step incl. NCCL" if g is not None else "none",
+                   "rank0_owned": int((roles == 1).sum()), "rank0_halo": int((roles == 2).sum())},
+        "ns_per_day_per_box": ns_per_day(value / boxes),
+        "halo": {"rounds_per_step": stats["rounds_per_step"],
+                 "rank0_halo_bytes_per_step": stats["halo_bytes_per_step"],
+                 "rank0_transferred_bytes_per_step": stats["transferred_bytes_per_step"],
+                 "packet_capacity_rows": stats["capacity_rows"], "peers": stats["peers"]},
+        "extensivity": {"E_total": E, "E_single_box_x_boxes": e_single * boxes,
+                        "rel_diff": abs(E - e_single * boxes) / abs(e_single * boxes)},
+        "gpu_launches": per_step_kernels * K,
+        "e2e": {"value": e2e_value, "unit": "steps/s",
+                "h2d_bytes_per_step": int(x_h.numel() * 8),
+                "d2h_bytes_per_step": int((x_h.numel() + f_h.numel() + o_h.numel()) * 8),
+                "path": "per step and rank: positions H2D from pinned host memory, the "
+                        "captured DD step, positions + forces + (E, W) D2H, host sync"},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N
+    processes on this node (the driver's own launch sets WORLD_SIZE and skips this)."""
+    import socket
+    import subprocess
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
 
 
 def main():
@@ -852,6 +925,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, rank, world)
     dist = None
@@ -871,9 +948,9 @@ def main():
         # N > 1 line is N independent replicas
         dd_ok = args.model in ("dpa2", "dpa3")
         if world > 1 and args.mode == "dd" and dd_ok:
+            run_halo(args, rank, world, local_rank, dist)
+        elif world > 1 and args.mode == "dd-allreduce" and dd_ok:
             run_gdd(args, rank, world, local_rank, dist)
-        elif world > 1 and args.mode == "dd-host" and dd_ok:
-            run_dd(args, rank, world, local_rank, dist)
         else:
             run_ours(args, rank, world, local_rank, dist)
     finally:
