@@ -234,6 +234,20 @@ int hmdp_gdd_counts(hmdp_ctx* ctx, int* counts3); /* owned, halo, searched (sync
 int hmdp_gdd_launches(const hmdp_ctx* ctx, long long* launches);
 
 /* ---------------------------------------------------------------------------
+ * 5th-generation tensor cores (hmdp_tc.cu): a chain of up to 3 dense layers
+ * y = act(x W^T + b) (the reference's MlpT::forward, inference.cpp:87-101) on
+ * tcgen05.mma kind::tf32 with the 3xTF32 hi/lo split and FP32 accumulation in
+ * TMEM.  Host arrays: x [rows][sizes[0]], weights = W_1 [sizes[1]][sizes[0]], W_2
+ * [sizes[2]][sizes[1]], ... concatenated, biases likewise, act[l] 0 linear / 1 tanh;
+ * y [rows][sizes[n_layers]].  K % 8 == 0, K <= 64, N in {32, 64}.
+ * hmdp_peak_tcgen05_tf32: measured raw kind::tf32 MMA throughput (TFLOP/s);
+ * 3xTF32 delivers a third of it.
+ * ------------------------------------------------------------------------- */
+int hmdp_tc_mlp(int device, int rows, const float* x, int n_layers, const int* sizes,
+                const float* weights, const float* biases, const int* act, float* y);
+int hmdp_peak_tcgen05_tf32(int device, int ms, double* tflops);
+
+/* ---------------------------------------------------------------------------
  * Halo-exchange mode of the device DD (the multi-GPU engine; SPEC.md:474-524
  * message kinds ghost_positions / ghost_forces, per-layer rc halo).
  * Nothing is replicated: each rank integrates only the atoms its region owns, and

@@ -74,6 +74,8 @@ SIGNATURES = {
     "hmdp_gdd_counts": (_c_int, [_vp, _vp]),
     "hmdp_gdd_launches": (_c_int, [_vp, _vp]),
     "hmdp_gdd_set_mode": (_c_int, [_vp, _c_int]),
+    "hmdp_tc_mlp": (_c_int, [_c_int, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "hmdp_peak_tcgen05_tf32": (_c_int, [_c_int, _c_int, _vp]),
     "hmdp_nccl_unique_id": (_c_int, [_vp]),
     "hmdp_gdd_attach_nccl": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "hmdp_gdd_hub_create": (_c_int, [_c_int, ctypes.POINTER(_vp)]),

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libhmdp.so")
 
-SOURCES = ["hmdp_nbr.cu", "hmdp_net.cu", "hmdp_dp.cu", "hmdp_gdd.cu", "hmdp_ff.cu", "hmdp_api.cu", "hmdp_probe.cu", "hmdp_host.cpp"]
+SOURCES = ["hmdp_nbr.cu", "hmdp_net.cu", "hmdp_dp.cu", "hmdp_gdd.cu", "hmdp_ff.cu", "hmdp_api.cu", "hmdp_probe.cu", "hmdp_tc.cu", "hmdp_host.cpp"]
 HEADERS = ["hmdp_device.cuh", "hmdp_common.cuh", "hmdp_model.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

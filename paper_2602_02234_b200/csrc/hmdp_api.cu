@@ -44,6 +44,11 @@ void launch_vv_kick_drift_bin(int, const MdFuse&, const double*, unsigned*, cuda
 void launch_gather_group(int, const int*, const double*, const int*, double*, int*, cudaStream_t);
 double probe_fp32_tflops(int ms);
 double probe_tf32x3_tflops(int ms);
+double probe_tcgen05_tf32_tflops(int ms);
+cudaError_t tc_configure();
+void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const float* const* W,
+                     const float* const* b, const int* K, const int* N, const int* act, float* y,
+                     int ldy, cudaStream_t st);
 template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t, int* = nullptr);
@@ -1132,6 +1137,7 @@ int hmdp_create(const char* model_json, size_t len, int device, int max_atoms, i
         ck(net_configure(), "kernel smem configuration");
         ck(nbr_configure(), "kernel smem configuration");
         ck(dp_configure(), "kernel smem configuration");
+        ck(tc_configure(), "kernel smem configuration");
         if (max_neighbors > 0) ctx->cap = std::min(256, std::max(8, max_neighbors));
         if (has_model && ctx->model.is_dp()) {
             ctx->pf.upload(ctx->model, ctx->stream);
@@ -1936,6 +1942,59 @@ int hmdp_peak_fp32(int device, int ms, double* tflops) {
         if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
         ck(cudaSetDevice(device), "cudaSetDevice");
         *tflops = probe_fp32_tflops(ms);
+    });
+}
+
+int hmdp_peak_tcgen05_tf32(int device, int ms, double* tflops) {
+    return guarded([&] {
+        if (!tflops) fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        *tflops = probe_tcgen05_tf32_tflops(ms);
+    });
+}
+
+int hmdp_tc_mlp(int device, int rows, const float* x, int n_layers, const int* sizes,
+                const float* weights, const float* biases, const int* act, float* y) {
+    return guarded([&] {
+        if (rows < 0 || n_layers < 1 || n_layers > 3 || !x || !sizes || !weights || !act || !y)
+            fail(HMDP_INVALID_ARGUMENT, "bad arguments");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(tc_configure(), "kernel smem configuration");
+        size_t nw = 0, nb = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            nw += static_cast<size_t>(sizes[l]) * sizes[l + 1];
+            nb += sizes[l + 1];
+        }
+        const int K0 = sizes[0], NL = sizes[n_layers];
+        DBuf dx, dw, db, dy;
+        dx.ensure(std::max<size_t>(1, static_cast<size_t>(rows) * K0) * sizeof(float));
+        dw.ensure(nw * sizeof(float));
+        db.ensure(nb * sizeof(float));
+        dy.ensure(std::max<size_t>(1, static_cast<size_t>(rows) * NL) * sizeof(float));
+        cudaStream_t st = cudaStreamPerThread;
+        ck(cudaMemcpyAsync(dx.p, x, static_cast<size_t>(rows) * K0 * sizeof(float),
+                           cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(dw.p, weights, nw * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
+        if (biases)
+            ck(cudaMemcpyAsync(db.p, biases, nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
+        const float* W[3];
+        const float* b[3];
+        int K[3], N[3];
+        size_t ow = 0, ob = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            W[l] = dw.as<float>() + ow;
+            b[l] = biases ? db.as<float>() + ob : nullptr;
+            K[l] = sizes[l];
+            N[l] = sizes[l + 1];
+            ow += static_cast<size_t>(K[l]) * N[l];
+            ob += N[l];
+        }
+        launch_tc_chain(rows, dx.as<float>(), K0, n_layers, W, b, K, N, act, dy.as<float>(), NL, st);
+        ck(cudaGetLastError(), "tcgen05 chain launch");
+        ck(copy_sync(y, dy.p, static_cast<size_t>(rows) * NL * sizeof(float), cudaMemcpyDeviceToHost,
+                     st),
+           "D2H");
+        for (DBuf* q : {&dx, &dw, &db, &dy}) q->release();
     });
 }
 
