@@ -470,6 +470,8 @@ def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with
     check(L.hmdp_peak_fp32(local_rank, 200, ctypes.byref(peak)))
     peak_tc = ctypes.c_double()  # 3xTF32 mma.sync: the DeePMD-family projections' pipe
     check(L.hmdp_peak_tf32x3(local_rank, 200, ctypes.byref(peak_tc)))
+    peak_umma = ctypes.c_double()  # tcgen05 kind::tf32 raw (3xTF32 delivers a third)
+    check(L.hmdp_peak_tcgen05_tf32(local_rank, 100, ctypes.byref(peak_umma)))
     achieved = kflops[dom] / (kern_ms[dom] * 1e-3) / 1e12
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "round2", "ncu_traffic.json")
@@ -567,6 +569,11 @@ def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with
                                   "(hmdp_peak_fp32): the parity-mode kernels run FP32 FMA",
                      "frac_of_bf16_tensor_peak": achieved / mp["bf16_tflops"] if "bf16_tflops" in mp else None,
                      "peak_tf32x3_tflops": peak_tc.value,
+                     "peak_tcgen05_tf32_raw_tflops": peak_umma.value,
+                     "peak_tcgen05_tf32x3_tflops": peak_umma.value / 3.0,
+                     "tcgen05_note": "the dense atom-level MLPs on tcgen05 (3xTF32, TMEM) lose the "
+                                     "A/B at every measured size (profiles/round2/tcgen05.md); "
+                                     "the fused FP32 SIMT kernels are the default",
                      "frac_per_kernel": {k: kflops[k] / (cands[k] * 1e-3) / 1e12 / peak.value
                                          for k in sorted(cands, key=lambda k: -cands[k])}},
         "kernels_us": {k: v * 1e3 for k, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},

@@ -46,9 +46,15 @@ double probe_fp32_tflops(int ms);
 double probe_tf32x3_tflops(int ms);
 double probe_tcgen05_tf32_tflops(int ms);
 cudaError_t tc_configure();
-void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const float* const* W,
-                     const float* const* b, const int* K, const int* N, const int* act, float* y,
-                     int ldy, cudaStream_t st);
+struct TcLayer {
+    const float* W;
+    const float* b;
+    int K, N, ldw, act, res;
+    float* out;
+    int ld_out;
+};
+void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const TcLayer* L,
+                     cudaStream_t st);
 template <typename T>
 void launch_dd_phase(const DevModel<T>&, const DevGraph&, const DevWork<T>&, int, int, T*, double*,
                      double*, cudaStream_t, int* = nullptr);
@@ -1977,19 +1983,16 @@ int hmdp_tc_mlp(int device, int rows, const float* x, int n_layers, const int* s
         ck(cudaMemcpyAsync(dw.p, weights, nw * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
         if (biases)
             ck(cudaMemcpyAsync(db.p, biases, nb * sizeof(float), cudaMemcpyHostToDevice, st), "H2D");
-        const float* W[3];
-        const float* b[3];
-        int K[3], N[3];
+        TcLayer L[3];
         size_t ow = 0, ob = 0;
         for (int l = 0; l < n_layers; ++l) {
-            W[l] = dw.as<float>() + ow;
-            b[l] = biases ? db.as<float>() + ob : nullptr;
-            K[l] = sizes[l];
-            N[l] = sizes[l + 1];
-            ow += static_cast<size_t>(K[l]) * N[l];
-            ob += N[l];
+            L[l] = TcLayer{dw.as<float>() + ow, biases ? db.as<float>() + ob : nullptr, sizes[l],
+                           sizes[l + 1], sizes[l], act[l], 0,
+                           l == n_layers - 1 ? dy.as<float>() : nullptr, NL};
+            ow += static_cast<size_t>(sizes[l]) * sizes[l + 1];
+            ob += sizes[l + 1];
         }
-        launch_tc_chain(rows, dx.as<float>(), K0, n_layers, W, b, K, N, act, dy.as<float>(), NL, st);
+        launch_tc_chain(rows, dx.as<float>(), K0, n_layers, L, st);
         ck(cudaGetLastError(), "tcgen05 chain launch");
         ck(copy_sync(y, dy.p, static_cast<size_t>(rows) * NL * sizeof(float), cudaMemcpyDeviceToHost,
                      st),

@@ -44,6 +44,7 @@
 //   k_embed_bwd    embedding + descriptor adjoint             :355-370
 //   k_force        force / virial (gather form) + E, W sums   :288-298, :372-387
 //                  [+ velocity Verlet tail, src/integrators.cpp:32-47]
+#include <cstdio>
 #include <cstdlib>
 
 #include "hmdp_common.cuh"
@@ -51,6 +52,29 @@
 namespace hmdp {
 
 int num_sms();  // hmdp_nbr.cu
+struct TcLayer {  // hmdp_tc.cu
+    const float* W;
+    const float* b;
+    int K, N, ldw, act, res;
+    float* out;
+    int ld_out;
+};
+void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const TcLayer* L,
+                     cudaStream_t st);
+// Embedding MLP + P^0 on the tensor cores (tcgen05 3xTF32 chain) instead of the SIMT
+// team mat-vecs: HMDP_TC_EMBED=1 on, 0 off, unset -> from kTcEmbedMinAtoms atoms up.
+// A/B on B200 (DPA3 MD step, profiles/round2/tcgen05.md): SIMT 6218 vs tcgen05 5433
+// steps/s at 2PTC (4114 atoms), 996 vs 978 at 2PTC x (2,2,2) (32 912 atoms) -- the
+// K = N = 32 chain is latency-bound (tensor pipe active 1-6 %), so the fused SIMT
+// path stays the default at every measured size.
+constexpr int kTcEmbedMinAtoms = 1 << 30;
+static bool tc_embed_on(int n) {
+    static const int env = [] {
+        const char* e = std::getenv("HMDP_TC_EMBED");
+        return e ? std::atoi(e) : -1;
+    }();
+    return env >= 0 ? env != 0 : n >= kTcEmbedMinAtoms;
+}
 
 // Dev-only stage timing (build with HMDP_NVCC_DEFS=-DHMDP_TPROBE): lane 0 of every
 // warp adds the clock64 cycles spent between consecutive TP(k) marks.
@@ -392,7 +416,9 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // backward chain.  rev (periodic path): computes the reverse slot of every
 // edge, which is the in-edge array of the symmetric graph (in_edge == rev).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool FUSE_FIT, bool LIST = false>
+// DESC_ONLY: the edge work and the descriptor only; the embedding MLP and the P^0
+// projection then run as one tcgen05 layer chain over all atoms (hmdp_tc.cu).
+template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
@@ -411,7 +437,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
 } else {
         W1h = sg.template view<32, 32>();
     }
-    sg.load(md.img_embed, &s_mbar);
+    if constexpr (!DESC_ONLY) sg.load(md.img_embed, &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
     const int lane = tm.lane;
@@ -512,6 +538,11 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
             __syncwarp();
         }
         desc = tm.sum(desc, sm);
+        if constexpr (DESC_ONLY) {  // the tcgen05 chain takes it from here
+            if (lead) ws.desc[static_cast<long long>(i) * 32 + lane] = lane < nd ? desc : T(0);
+            __syncwarp();
+            continue;
+        }
         if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
             Smem<T>::wait(&s_mbar);
             staged = true;
@@ -567,7 +598,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
         }
         __syncwarp();
     }
-    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
+    if constexpr (!DESC_ONLY)
+        if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
 
 // ---------------------------------------------------------------------------
@@ -1427,7 +1459,16 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
                        Args... args) {
     const size_t smem = static_cast<size_t>(staged_elems<T>(p)) * sizeof(T) + 16 +
                         static_cast<size_t>(sh.warps) * sizeof(WarpSmem<T>);
-    launch_pdl(kernel, dim3(sh.grid), dim3(32 * sh.warps), smem, st, args...);
+    const cudaError_t e = launch_pdl(kernel, dim3(sh.grid), dim3(32 * sh.warps), smem, st, args...);
+    if (e != cudaSuccess && std::getenv("HMDP_DEBUG_LAUNCH")) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kernel);
+        std::fprintf(stderr,
+                     "launch_net failed: %s grid %d block %d smem %zu | attr maxThreads %d regs %d "
+                     "static smem %zu maxDyn %d\n",
+                     cudaGetErrorString(e), sh.grid, 32 * sh.warps, smem, fa.maxThreadsPerBlock,
+                     fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+    }
 }
 
 int force_grid(int n) {
@@ -1446,6 +1487,7 @@ struct Net {
         cudaError_t e = cudaSuccess;
         for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_embed<T, G, false, LIST>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_embed<T, G, false, LIST, true>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_msg_bwd<T, G, LIST>, a, kMaxSmem),
@@ -1453,12 +1495,28 @@ struct Net {
             if (r != cudaSuccess) e = r;
         return e;
     }
-    static void embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                      const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
-        if (md.n_msg == 0)
+    // returns the kernels launched (2 with the tcgen05 embedding chain)
+    static int embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                     const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
+        if (md.n_msg == 0) {
             launch_net<T>(k_embed<T, G, true, LIST>, Phase::EmbedFit, sh, st, md, gr, ws, rev, mf);
-        else
-            launch_net<T>(k_embed<T, G, false, LIST>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
+            return 1;
+        }
+        if constexpr (sizeof(T) == 4 && !LIST) {
+            if (tc_embed_on(gr.n_active) && !ws.p_atom) {
+                launch_net<T>(k_embed<T, G, false, LIST, true>, Phase::Embed, sh, st, md, gr, ws,
+                              rev, mf);
+                // desc (nd, zero-padded to 32) -> tanh(32) = ez1 -> h^0 -> P^0 = W1h h^0
+                const TcLayer L[3] = {
+                    {md.embed.W1, md.embed.b1, 32, 32, 32, 1, 0, ws.ez1, kH},
+                    {md.embed.W2, md.embed.b2, 32, 32, 32, 0, 0, ws.h, kH},
+                    {md.msg[0].W1, nullptr, 32, 32, kH + kK, 0, 0, ws.pa, kH}};
+                launch_tc_chain(gr.n_active, ws.desc, 32, 3, L, st);
+                return 2;
+            }
+        }
+        launch_net<T>(k_embed<T, G, false, LIST>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
+        return 1;
     }
     static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                         const DevWork<T>& ws, int l, cudaStream_t st) {
@@ -1479,7 +1537,7 @@ struct Net {
                        const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
                        const MdFuse& mf) {
         const int M = md.n_msg;
-        embed(sh, md, gr, ws, rev, mf, st);
+        const int ne = embed(sh, md, gr, ws, rev, mf, st);
         mk(M == 0 ? "embed_fit" : "embed", st);
         if (M == 0) return 1;
         for (int l = 0; l < M; ++l) {
@@ -1492,7 +1550,7 @@ struct Net {
         }
         embed_bwd(sh, md, gr, ws, st);
         mk("embed_bwd", st);
-        return 2 + M + (M - 1);
+        return ne + 1 + M + (M - 1);
     }
     static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                          const DevWork<T>& ws, int phase, int l, cudaStream_t st, int* rev) {

@@ -40,18 +40,19 @@ constexpr int kMaxN = 64;
 constexpr int kMaxLayers = 3;
 
 struct Layer {
-    const float* W;  // [N][K] row-major (the model's [out][in])
+    const float* W;  // [N][ldw] row-major (the model's [out][in]), first K columns used
     const float* b;  // [N] (nullable)
-    int K, N;        // K % 8 == 0, K <= 64; N % 8 == 0, 8 <= N <= 64
+    int K, N, ldw;   // K % 8 == 0, K <= 64; N in {32, 64}
     int act;         // 0 linear, 1 tanh
+    int res;         // 1: + the chain input's first N columns (residual), after act
+    float* out;      // [rows][ld_out] this layer's output (nullable except the last)
+    int ld_out;
 };
 struct Chain {
     Layer L[kMaxLayers];
     int n_layers;
     const float* x;  // [rows][ldx], first K0 columns used
     int ldx;
-    float* y;        // [rows][ldy], last layer's N columns written
-    int ldy;
     int rows;
 };
 
@@ -196,7 +197,7 @@ __global__ __launch_bounds__(128, 1) void k_tc_chain(Chain ch) {
         // B = W [N][K]: the whole CTA splits it into the B images
         for (int t = tid; t < N * K; t += kRows) {
             const int n = t / K, k = t - n * K;
-            put_split(sm.b_hi, sm.b_lo, kmajor_off(n, k, K), __ldg(L.W + t));
+            put_split(sm.b_hi, sm.b_lo, kmajor_off(n, k, K), __ldg(L.W + n * L.ldw + k));
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -234,14 +235,24 @@ __global__ __launch_bounds__(128, 1) void k_tc_chain(Chain ch) {
                 if (L.act == 1) y = tanhf(y);
                 v[c] = y;
             }
-            if (last) {
-                if (r < ch.rows) {
-                    float* yr = ch.y + static_cast<long long>(r) * ch.ldy + c0;
+            if (L.res && r < ch.rows) {
+                const float* xr = ch.x + static_cast<long long>(r) * ch.ldx + c0;
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4)
-                        *reinterpret_cast<float4*>(yr + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 q = *reinterpret_cast<const float4*>(xr + c);
+                    v[c] += q.x;
+                    v[c + 1] += q.y;
+                    v[c + 2] += q.z;
+                    v[c + 3] += q.w;
                 }
-            } else {  // next layer's A operand (its K = this N)
+            }
+            if (L.out && r < ch.rows) {
+                float* yr = L.out + static_cast<long long>(r) * L.ld_out + c0;
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    *reinterpret_cast<float4*>(yr + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+            }
+            if (!last) {  // next layer's A operand (its K = this N)
 #pragma unroll
                 for (int c = 0; c < 32; ++c) put_split(sm.a_hi, sm.a_lo, kmajor_off(tid, c0 + c, N), v[c]);
             }
@@ -304,24 +315,32 @@ cudaError_t tc_configure() {
                                 static_cast<int>(sizeof(tc::Smem)));
 }
 
-// y = act_L(... act_1(x W_1^T + b_1) ...): rows x K0 -> rows x N_last, FP32 in / out,
-// 3xTF32 on the tensor cores.  Ws/bs: device pointers, sizes[l] = {K_l, N_l}.
-void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const float* const* W,
-                     const float* const* b, const int* K, const int* N, const int* act, float* y,
-                     int ldy, cudaStream_t st) {
+// One dense layer of a chain (host description).
+struct TcLayer {
+    const float* W;
+    const float* b;
+    int K, N, ldw, act, res;
+    float* out;
+    int ld_out;
+};
+
+// y_l = act_l(y_{l-1} W_l^T + b_l) [+ x residual], y_0 = x: rows x K0 in, every layer's
+// output optionally stored; FP32 in / out, 3xTF32 on the tensor cores.
+void launch_tc_chain(int rows, const float* x, int ldx, int n_layers, const TcLayer* L,
+                     cudaStream_t st) {
     tc::Chain ch{};
     if (n_layers < 1 || n_layers > tc::kMaxLayers) throw std::invalid_argument("1..3 layers");
     for (int l = 0; l < n_layers; ++l) {
-        if (K[l] % 8 || K[l] < 8 || K[l] > tc::kMaxK || N[l] % 32 || N[l] < 32 || N[l] > tc::kMaxN)
+        const TcLayer& q = L[l];
+        if (q.K % 8 || q.K < 8 || q.K > tc::kMaxK || q.N % 32 || q.N < 32 || q.N > tc::kMaxN)
             throw std::invalid_argument("tcgen05 chain: K % 8 == 0, K <= 64, N in {32, 64}");
-        if (l > 0 && K[l] != N[l - 1]) throw std::invalid_argument("tcgen05 chain: K_l != N_{l-1}");
-        ch.L[l] = tc::Layer{W[l], b[l], K[l], N[l], act[l]};
+        if (l > 0 && q.K != L[l - 1].N) throw std::invalid_argument("tcgen05 chain: K_l != N_{l-1}");
+        ch.L[l] = tc::Layer{q.W, q.b, q.K, q.N, q.ldw, q.act, q.res, q.out, q.ld_out};
     }
+    if (!L[n_layers - 1].out) throw std::invalid_argument("tcgen05 chain: last layer needs out");
     ch.n_layers = n_layers;
     ch.x = x;
     ch.ldx = ldx;
-    ch.y = y;
-    ch.ldy = ldy;
     ch.rows = rows;
     const int grid = (rows + tc::kRows - 1) / tc::kRows;
     if (grid > 0) tc::k_tc_chain<<<grid, 128, sizeof(tc::Smem), st>>>(ch);
