@@ -1268,6 +1268,13 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     return e ? std::atoi(e) : -1;
                 }();
                 const bool mapped_out = mapped_env >= 0 ? mapped_env != 0 : n < 2048;
+                // inputs likewise: mapped reads by the binning kernel, or one H2D copy
+                // node per array from the pinned block (HMDP_CGRAPH_MAPPED_IN=0/1 for A/B)
+                static const int mapped_in_env = [] {
+                    const char* e = std::getenv("HMDP_CGRAPH_MAPPED_IN");
+                    return e ? std::atoi(e) : -1;
+                }();
+                const bool mapped_in = mapped_in_env >= 0 ? mapped_in_env != 0 : true;
                 double* dst = hp;
                 if (!mapped_out) {
                     ctx->cg_out.ensure(out_bytes);
@@ -1277,8 +1284,15 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
                     ctx->skip_cell_memset = true;  // cleared by this call's network
-                    ctx->stage_hx = reinterpret_cast<const double*>(hin);
-                    ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
+                    if (mapped_in) {
+                        ctx->stage_hx = reinterpret_cast<const double*>(hin);
+                        ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
+                    } else {
+                        ck(cudaMemcpyAsync(ctx->pos.p, hin, 3 * n * sizeof(double),
+                                           cudaMemcpyHostToDevice, st), "xyz H2D");
+                        ck(cudaMemcpyAsync(ctx->types.p, hin + 3 * n * sizeof(double),
+                                           n * sizeof(int), cudaMemcpyHostToDevice, st), "types H2D");
+                    }
                     ctx->out_override = dst;
                     const int launches =
                         enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
