@@ -71,6 +71,17 @@ class ContextCache {
     std::map<std::pair<std::string, int>, std::unique_ptr<hmdp_ctx, int (*)(hmdp_ctx*)>> map_;
 };
 
+// The device neighbour search is fully periodic (SimBox::periodic, box.hpp:10-13):
+// a box with an open axis is rejected instead of being silently wrapped.
+template <class SimBox>
+void require_periodic(const SimBox& box) {
+    for (int a = 0; a < 3; ++a)
+        if (!box.periodic[a])
+            throw std::invalid_argument(
+                "B200 neighbour search supports fully periodic boxes only (axis " +
+                std::to_string(a) + " is not periodic)");
+}
+
 template <class Vec3>
 std::vector<double> flat3(const std::vector<Vec3>& v) {
     std::vector<double> out(3 * v.size());
@@ -97,6 +108,7 @@ NnInput build_input_periodic(const std::vector<Vec3>& positions, const std::vect
     in.global_index = global_index;
     in.is_ghost.assign(n, 0);
     const std::vector<double> x = flat3(positions);
+    require_periodic(box);
     const double b[3] = {box.lengths.x, box.lengths.y, box.lengths.z};
     hmdp_ctx* c = ContextCache::get().ctx("", device);
     std::lock_guard<std::mutex> lk(ContextCache::get().lock());
@@ -202,6 +214,7 @@ std::function<double(State&)> force_function(const NnModel& model, std::vector<i
         if (static_cast<int>(types.size()) != n)
             throw std::invalid_argument("positions/types/global_index size mismatch");
         const std::vector<double> x = flat3(st.positions);
+        require_periodic(st.box);
         const double b[3] = {st.box.lengths.x, st.box.lengths.y, st.box.lengths.z};
         std::vector<double> f(3 * static_cast<std::size_t>(n));
         double e = 0.0;
@@ -306,6 +319,7 @@ double nn_force_provider(State& state, const std::vector<int>& type_of,
     if (static_cast<int>(state.forces.size()) != n) state.forces.resize(n);
     const std::vector<double> x = flat3(state.positions);
     std::vector<double> f = flat3(state.forces);
+    require_periodic(state.box);
     const double b[3] = {state.box.lengths.x, state.box.lengths.y, state.box.lengths.z};
     double e = 0.0;
     check(hmdp_compute_group(c, n, x.data(), type_of.data(), plan.atoms.data(),

@@ -52,6 +52,20 @@ int main() {
     EXPECT(ref_in.edge_neighbor == our_in.edge_neighbor, "edge_neighbor differs");
     EXPECT(ref_in.edge_dr == our_in.edge_dr, "edge_dr differs (must be bit-exact)");
 
+    // an open axis is rejected (the device search is fully periodic), not wrapped
+    {
+        SimBox open_box = st.box;
+        open_box.periodic[2] = false;
+        bool threw = false;
+        try {
+            hmdp::halomd::build_input_periodic<nn::NnInput>(st.positions, topo.type_of, gidx,
+                                                           open_box, 0.6);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        EXPECT(threw, "non-periodic axis must raise std::invalid_argument");
+    }
+
     for (auto fam : {nn::ModelFamily::embed_fit, nn::ModelFamily::message_passing}) {
         const int depth = fam == nn::ModelFamily::embed_fit ? 1 : 3;
         auto model = nn::make_model(fam, depth, 0.6, 2, 8, 32, 1);
