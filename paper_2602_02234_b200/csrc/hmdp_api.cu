@@ -585,7 +585,7 @@ struct hmdp_ctx {
     DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev, ety, inv_pos;
     DBuf offset, in_start, in_cnt, cursor, in_edge;
     // network workspace
-    DBuf er, es, eds, eb, edb, g, grev, zb, db, pa, desc, ez1, h, uz1, dhown;
+    DBuf er, es, eds, eb, edb, g, grev, zb, db, pa, vb, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // DeePMD-style families: vector edge gradients and the repformer workspace
     DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
@@ -704,7 +704,7 @@ struct hmdp_ctx {
         cudaSetDevice(device);
         for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
                         &nbr, &dr, &rev, &ety, &inv_pos, &offset, &in_start, &in_cnt, &cursor,
-                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &desc,
+                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &vb, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
                         &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &gdd.stamp,
@@ -782,6 +782,7 @@ struct hmdp_ctx {
             zb.ensure(M * s * kH * sizeof(T));  // z_e of every layer (hmdp_net.cu kRecomputeZ)
             db.ensure(2 * s * kH * sizeof(T));
             pa.ensure(M * na * kH * sizeof(T));
+            vb.ensure(2 * na * (kH + 1) * sizeof(T));  // pull-form v rows + c0
         }
         desc.ensure(na * 32 * sizeof(T));
         ez1.ensure(na * kH * sizeof(T));
@@ -799,6 +800,8 @@ struct hmdp_ctx {
         w.z = zb.as<T>();
         w.d = db.as<T>();
         w.pa = pa.as<T>();
+        w.vrow = M > 0 ? vb.as<T>() : nullptr;
+        w.vc0 = M > 0 ? vb.as<T>() + 2 * na * kH : nullptr;
         w.desc = desc.as<T>();
         w.ez1 = ez1.as<T>();
         w.h = h.as<T>();

@@ -101,11 +101,16 @@ struct DevWork {
     T* edb;   // [slot][8] b_k'
     T* g;     // dE/dr
     T* grev;  // [in-position] g of the edge mirrored there (pushed by its source)
-    T* z;     // [slot][32] message hidden (tanh) activations z_e of the LAST layer (the
-              // lower layers recompute z_e in their backward from pa and b_e)
-    T* d;     // [2][in-position][32] pushed adjoints dz_e (double-buffered by layer)
+    T* z;     // [M][slot][32] message hidden (tanh) activations z_e (push form: at the
+              // receiver's slot; pull-store form: at the sender's mirror slot)
+    T* d;     // [2][in-position][32] pushed adjoints dz_e (push form only)
     T* pa;    // [M][n][32] per-atom neighbour projections P^l_i = W1h^l h^l_i, gathered
               // by the edges' sources (nbr index); L2-resident at every paper size
+    // pull-form backward (symmetric graph, every atom runs the network): per-atom
+    // v^l_i = W2^T dmsum^l_i rows and c0^l_i = dmsum^l_i . b2, double-buffered by layer;
+    // the SENDER of each message gathers its receiver's row (hmdp_net.cu, k_msg_bwd_pull)
+    T* vrow;  // [2][n][32]
+    T* vc0;   // [2][n]
     // domain decomposition (nullable otherwise)
     T* p_atom;    // [n][32] per-atom P of the layer just produced (sent to ghost copies)
     T* s_remote;  // [n][32] adjoint partial sums received from ghost copies elsewhere

@@ -128,7 +128,7 @@ struct WarpSmem {
     alignas(16) T x[64];
     alignas(16) T y[64];
     alignas(16) T t[32];
-    alignas(16) T ed[32][kRecomputeZ ? 20 : 12];  // edge scalars: (s, s', -, -, b or b'[8], [b[8]])
+    alignas(16) T ed[32][20];  // edge scalars: (s, s', c0 | -, -, b or b'[8], [b[8]])
     alignas(16) T red[2][64];  // team-sum partials (double-buffered)
     T reds[2];
     int emir[32];  // staged mirror slots
@@ -185,9 +185,13 @@ struct Smem {
                 : "r"(mb)
                 : "memory");
     }
+    // The staged matrices end 16-byte aligned (rows padded to a multiple of 16
+    // bytes), so the scratch follows directly.  Pointer arithmetic from the
+    // __shared__ base (no integer round trip) keeps the shared state space visible
+    // to the compiler: LDS/STS instead of generic loads that may alias global
+    // stores and so pin the edge loops' schedule.
     __device__ WarpSmem<T>& warp_scratch() const {
-        const size_t a = (reinterpret_cast<size_t>(cur) + 15) & ~size_t(15);
-        return reinterpret_cast<WarpSmem<T>*>(a)[threadIdx.x >> 5];
+        return reinterpret_cast<WarpSmem<T>*>(cur)[threadIdx.x >> 5];
     }
 };
 
@@ -822,12 +826,165 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
 }
 
 // ---------------------------------------------------------------------------
+// Pull form of the message backward (symmetric periodic graph, every atom runs
+// the network).  The push form above has each RECEIVER i push dz_e = s_e v_i
+// (1 - z_e^2) into a per-edge row that the sender k later gathers: two 128-byte
+// rows per edge and layer that spill out of L2 at 2PTC.  Every quantity of
+// message e = (i <- k) depends only on (v_i, c0_i) of the receiver and on z_e,
+// so the SENDER can compute all of it over its own slots: it gathers the
+// receiver's per-atom row v_i (an [n][32] array that stays in L2, like the P
+// rows of the forward), sums dz_e in registers, and adds the message's dE/dr to
+// g at its own slot (the force kernel sums g_q + g_rev(q), so either end of a
+// pair may hold a term).  z_e is either stored by the forward at the sender's
+// mirror slot (PULL = 1) or recomputed by the sender from its OWN P row,
+// z_e = tanh(W1b b_e + b1 + P_k), no gather (PULL = 2).  Same function as the
+// push form; only the summation points of the per-pair terms move.
+// ---------------------------------------------------------------------------
+// Update-MLP backward of layer l for atom i (dE/dh^{l+1}_i = dh, update hidden
+// activation zu): writes dhown (residual + update input), v^l_i = W2^T dmsum and
+// c0^l_i = dmsum . b2 for the senders of i's messages.
+template <typename T, int G>
+__device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, const T* mW2T, T mb2,
+                                             const DevWork<T>& ws, WarpSmem<T>& sm, int n, int l,
+                                             int i, T dh, T zu, Team<G>& tm) {
+    const int lane = tm.lane;
+    sm.t[lane] = dh;
+    __syncwarp();
+    const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
+    sm.y[lane] = dz;
+    __syncwarp();
+    T din_h, dmsum;  // input rows 0..31 (h) and 32..63 (msum)
+    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, dmsum, tm, sm);
+    sm.x[lane] = dmsum;
+    __syncwarp();
+    const T v = twmv<T, 32>(mW2T, sm.x, lane, tm, sm);  // v = W2^T dmsum
+    const T c0 = warp_sum(dmsum * mb2);
+    if (tm.w == 0) {
+        const long long b = static_cast<long long>(l & 1) * n + i;
+        ws.dhown[static_cast<long long>(i) * kH + lane] = dh + din_h;
+        ws.vrow[b * kH + lane] = v;
+        if (lane == 0) ws.vc0[b] = c0;
+    }
+    __syncwarp();
+}
+
+// Sender-side backward of one message layer over this warp's local slots of atom
+// k (local edge q: slot e0 + G q, neighbour = the message's receiver i).  Returns
+// the warp's sum of dz_e (lane = channel); adds each message's dE/dr to g at the
+// slot (first_g: the first backward kernel to touch g overwrites it).
+//   z_e  = stored row (PULL 1) | tanh(W1b b_e + b1 + P_k) (PULL 2, pk = P_k[lane])
+//   dz_e = s_e v_i (1 - z_e^2);  dE/dr_e += s'_e (v_i . z_e + c0_i) + b'_e . (W1b^T dz_e)
+template <typename T, int G, int PULL>
+__device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T* Z, const T* V,
+                                        const T* C0, const DevGraph& gr, const DevWork<T>& ws,
+                                        WarpSmem<T>& sm, long long e0, int mloc, bool first_g,
+                                        int lane) {
+    T sdz = T(0);
+    for (int base = 0; base < mloc; base += 32) {
+        const int m = min(32, mloc - base);
+        const long long eb = e0 + static_cast<long long>(G) * base;  // local edge k: eb + G k
+        // lane u stages edge u's scalars (read as broadcasts by the edge loop)
+        if (lane < m) {
+            const long long e = eb + static_cast<long long>(G) * lane;
+            const int nb = gr.nbr[e];
+            T* row = sm.ed[lane];
+            row[0] = ws.es[e];
+            row[1] = ws.eds[e];
+            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+            st4(row + 4, d0.x, d0.y, d0.z, d0.w);
+            st4(row + 8, d1.x, d1.y, d1.z, d1.w);
+            if constexpr (PULL == 2) {
+                const V4<T> b0 = ld4c(ws.eb + 8 * e), b1 = ld4c(ws.eb + 8 * e + 4);
+                st4(row + 12, b0.x, b0.y, b0.z, b0.w);
+                st4(row + 16, b1.x, b1.y, b1.z, b1.w);
+            }
+            row[2] = C0[nb];
+            sm.enb[lane] = nb;
+        }
+        __syncwarp();
+        constexpr int U = kU<T>;
+        T vr[U], zr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (u < m) {
+                vr[u] = V[static_cast<long long>(sm.enb[u]) * kH + lane];
+                if constexpr (PULL == 1) zr[u] = Z[(eb + static_cast<long long>(G) * u) * kH + lane];
+            }
+        for (int u0 = 0; u0 < m; u0 += U) {
+            const int mu = min(U, m - u0);
+            T vn[U], zn[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u0 + U + u < m) {
+                    vn[u] = V[static_cast<long long>(sm.enb[u0 + U + u]) * kH + lane];
+                    if constexpr (PULL == 1)
+                        zn[u] = Z[(eb + static_cast<long long>(G) * (u0 + U + u)) * kH + lane];
+                }
+            T term[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                term[u] = T(0);
+                if (u < U && u < mu) {
+                    const T* row = sm.ed[u0 + u];
+                    const T s = row[0], ds = row[1];
+                    const V4<T> d0 = ld4c(row + 4), d1 = ld4c(row + 8);
+                    T wv = w1b[0] * d0.x;
+                    wv += w1b[1] * d0.y;
+                    wv += w1b[2] * d0.z;
+                    wv += w1b[3] * d0.w;
+                    wv += w1b[4] * d1.x;
+                    wv += w1b[5] * d1.y;
+                    wv += w1b[6] * d1.z;
+                    wv += w1b[7] * d1.w;
+                    T z;
+                    if constexpr (PULL == 2) {  // bit-identical to the forward's z_e
+                        const V4<T> b0 = ld4c(row + 12), bb = ld4c(row + 16);
+                        T a = mb1;
+                        a += w1b[0] * b0.x;
+                        a += w1b[1] * b0.y;
+                        a += w1b[2] * b0.z;
+                        a += w1b[3] * b0.w;
+                        a += w1b[4] * bb.x;
+                        a += w1b[5] * bb.y;
+                        a += w1b[6] * bb.z;
+                        a += w1b[7] * bb.w;
+                        z = d_tanh(a + pk);
+                    } else {
+                        z = zr[u];
+                    }
+                    const T v = vr[u];
+                    const T d = s * v * (T(1) - z * z);
+                    sdz += d;
+                    term[u] = ds * v * z + d * wv;
+                }
+            }
+            // reduce-scatter butterfly: 8 edge sums in 9 shuffles; lane 4u holds edge u
+            const T tot = reduce8(term, lane);
+            if ((lane & 3) == 0 && (lane >> 2) < mu) {
+                const int u = u0 + (lane >> 2);
+                const long long e = eb + static_cast<long long>(G) * u;
+                const T* row = sm.ed[u];
+                ws.g[e] = (first_g ? T(0) : ws.g[e]) + (tot + row[1] * row[2]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                vr[u] = vn[u];
+                if constexpr (PULL == 1) zr[u] = zn[u];
+            }
+        }
+        __syncwarp();
+    }
+    return sdz;
+}
+
+// ---------------------------------------------------------------------------
 // Message layer l forward; LAST fuses the fitting net and the top layer's
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool LAST, bool LIST = false>
+template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
+    static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TP_START;
     pdl_launch_dependents();
@@ -871,7 +1028,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     const T* Pl = ws.pa + static_cast<long long>(l) * n * kH;
     // z_e rows of this layer (read back by the layer's backward); with kRecomputeZ only
     // the LAST layer's are stored (the lower layers' backward recomputes them)
-    T* Z = ws.z + (kRecomputeZ ? 0 : static_cast<long long>(l) * ws.slots * kH);
+    T* Z = ws.z + (kRecomputeZ && PULL == 0 ? 0 : static_cast<long long>(l) * ws.slots * kH);
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
@@ -882,13 +1039,14 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         // ELL graph issued before the count arrives), then the P rows they select
         T es_l = T(0);
         V4<T> b0_l{}, bb_l{};
-        int nb_l = 0;
+        int nb_l = 0, mir_l = 0;
         if (lane < ar.room) {
             const long long e = ar.e0 + static_cast<long long>(G) * lane;
             es_l = ws.es[e];
             b0_l = ld4c(ws.eb + 8 * e);
             bb_l = ld4c(ws.eb + 8 * e + 4);
             nb_l = min(max(gr.nbr[e], 0), n - 1);  // padding slots: any valid row
+            if constexpr (PULL == 1) mir_l = gr.inv_pos[e];
         }
         T pr[kU<T>];
 #pragma unroll
@@ -910,6 +1068,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
                     b0_l = ld4c(ws.eb + 8 * e);
                     bb_l = ld4c(ws.eb + 8 * e + 4);
                     nb_l = gr.nbr[e];
+                    if constexpr (PULL == 1) mir_l = gr.inv_pos[e];
                 }
 #pragma unroll
                 for (int u = 0; u < kU<T>; ++u) {
@@ -923,6 +1082,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
                 st4(row + 4, b0_l.x, b0_l.y, b0_l.z, b0_l.w);
                 st4(row + 8, bb_l.x, bb_l.y, bb_l.z, bb_l.w);
                 sm.enb[lane] = nb_l;
+                if constexpr (PULL == 1) sm.emir[lane] = mir_l;
             }
             __syncwarp();
             for (int u0 = 0; u0 < m; u0 += kU<T>) {
@@ -947,8 +1107,11 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
                     a += w1b[6] * bb.z;
                     a += w1b[7] * bb.w;
                     const T z = d_tanh(a + pr[u]);
-                    if (LAST || !kRecomputeZ)
-                        Z[(e0 + static_cast<long long>(G) * (u0 + u)) * kH + lane] = z;
+                    if constexpr (PULL == 1)  // the sender's mirror slot (its backward reads it)
+                        Z[static_cast<long long>(sm.emir[u0 + u]) * kH + lane] = z;
+                    else if constexpr (PULL == 0)
+                        if (LAST || !kRecomputeZ)
+                            Z[(e0 + static_cast<long long>(G) * (u0 + u)) * kH + lane] = z;
                     acc += s * z;
                     ssum += s;
                 }
@@ -961,7 +1124,8 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
         // warp) is loaded now, under the atom-level mat-vecs below
         TP(3);
         BwdPre<T> pre;
-        if constexpr (LAST) bwd_prefetch<T, G, false>(pre, Z, ws, gr, ar.e0, min(mloc, 32), lane);
+        if constexpr (LAST && PULL == 0)
+            bwd_prefetch<T, G, false>(pre, Z, ws, gr, ar.e0, min(mloc, 32), lane);
         acc = tm.sum(acc, ssum, sm);
         TP(4);
         if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
@@ -998,8 +1162,11 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
             const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
                                   lead ? ws.e_atom + i : nullptr, tm, sm);
             TP(7);
-            msg_backward_warp<T, G, false>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i, dh,
-                                           zu, true, tm, pre, ar.e0, mloc);
+            if constexpr (PULL == 0)
+                msg_backward_warp<T, G, false>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i,
+                                               dh, zu, true, tm, pre, ar.e0, mloc);
+            else  // the edges' share runs at their senders (k_msg_bwd_pull / k_embed_bwd_pull)
+                upd_bwd_pull<T, G>(uW2T, uW1T, mW2T, mb2, ws, sm, n, l, i, dh, zu, tm);
             TP(8);
         }
         __syncwarp();
@@ -1157,6 +1324,136 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
             const T gv = g_l + acc;
             ws.g[e] = gv;
             ws.grev[mir_l] = gv;  // mirror for the force gather
+        }
+        __syncwarp();
+    }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
+}
+
+// Pull form, lower layers (l < M-1): the sender-side backward of layer l+1's
+// messages (gathering the receivers' v^{l+1} rows), dE/dh^{l+1}_k, then layer l's
+// update backward (v^l_k, c0^l_k for the next kernel).
+template <typename T, int G, int PULL>
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
+                                                                    DevGraph gr, DevWork<T> ws,
+                                                                    int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    const DevMlp<T>& msgn = md.msg[l + 1];  // the messages whose backward runs here
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
+    const T* nW1hT = sg.template view<32, 32>();  // W1h^(l+1)^T
+    const T* uW2T = sg.template view<32, 32>();
+    const T* uW1T = sg.template view<64, 32>();
+    const T* mW2T = sg.template view<32, 32>();
+    sg.load(md.img_bwd[l], &s_mbar);
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    T w1b[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) w1b[k] = msgn.W1T[(kH + k) * kH + lane];
+    const T mb1n = msgn.b1[lane], mb2 = md.msg[l].b2[lane];
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
+    pdl_wait();
+    const int n = gr.n;
+    const T* Z = ws.z + static_cast<long long>(l + 1) * ws.slots * kH;
+    const T* V = ws.vrow + static_cast<long long>((l + 1) & 1) * n * kH;
+    const T* C0 = ws.vc0 + static_cast<long long>((l + 1) & 1) * n;
+    const bool first_g = l == md.n_msg - 2;
+    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
+        AtomRow<G> ar(gr, k, tm);
+        const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
+        const T zu = ws.uz1[(static_cast<long long>(l) * n + k) * kH + lane];
+        const T pk = PULL == 2 ? ws.pa[(static_cast<long long>(l + 1) * n + k) * kH + lane] : T(0);
+        const int mloc = ar.finish(tm);
+        T sdz = pull_edges<T, G, PULL>(w1b, mb1n, pk, Z, V, C0, gr, ws, sm, ar.e0, mloc, first_g,
+                                       lane);
+        sdz = tm.sum(sdz, sm);
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
+        sm.t[lane] = sdz;
+        __syncwarp();
+        // dE/dh^{l+1}_k = own + W1h^(l+1)^T sum_e dz_e
+        const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
+        __syncwarp();
+        upd_bwd_pull<T, G>(uW2T, uW1T, mW2T, mb2, ws, sm, n, l, k, dh, zu, tm);
+    }
+    if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
+}
+
+// Pull form, embedding backward: the sender-side backward of layer 0's messages,
+// dE/dh^0_k, the embedding backward and the descriptor adjoint; pushes the final
+// g to the mirrors for the force gather.
+template <typename T, int G, int PULL>
+__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
+                                                                      DevGraph gr,
+                                                                      DevWork<T> ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    const DevMlp<T>& msg0 = md.msg[0];
+    Smem<T> sg(reinterpret_cast<T*>(smem_raw));
+    __shared__ unsigned long long s_mbar;
+    const T* m0W1hT = sg.template view<32, 32>();
+    const T* eW2T = sg.template view<32, 32>();
+    const T* eW1T = sg.template view<32, 32>();
+    sg.load(md.img_embed_bwd, &s_mbar);
+    WarpSmem<T>& sm = sg.warp_scratch();
+    Team<G> tm;
+    const int lane = tm.lane;
+    T w1b[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) w1b[k] = msg0.W1T[(kH + k) * kH + lane];
+    const T mb1 = msg0.b1[lane];
+    __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
+    bool staged = false;
+    pdl_wait();
+    const int n = gr.n;
+    const bool first_g = md.n_msg == 1;
+    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
+        AtomRow<G> ar(gr, k, tm);
+        const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
+        const T z1 = ws.ez1[static_cast<long long>(k) * kH + lane];
+        const T pk = PULL == 2 ? ws.pa[static_cast<long long>(k) * kH + lane] : T(0);
+        const int mloc = ar.finish(tm);
+        T sdz = pull_edges<T, G, PULL>(w1b, mb1, pk, ws.z, ws.vrow, ws.vc0, gr, ws, sm, ar.e0,
+                                       mloc, first_g, lane);
+        sdz = tm.sum(sdz, sm);
+        if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
+            Smem<T>::wait(&s_mbar);
+            staged = true;
+        }
+        sm.t[lane] = sdz;
+        __syncwarp();
+        const T dh = own + twmv<T, 32>(m0W1hT, sm.t, lane, tm, sm);
+        sm.x[lane] = dh;
+        __syncwarp();
+        const T dz1 = twmv<T, 32>(eW2T, sm.x, lane, tm, sm) * (T(1) - z1 * z1);
+        sm.y[lane] = dz1;
+        __syncwarp();
+        const T dd = twmv<T, 32>(eW1T, sm.y, lane, tm, sm);
+        sm.t[lane] = dd;
+        __syncwarp();
+        // descriptor adjoint per edge (lane = local edge), on top of the message
+        // terms this warp just wrote; then the mirror copy for the force gather
+        for (int q = lane; q < mloc; q += 32) {
+            const long long e = ar.e0 + static_cast<long long>(G) * q;
+            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+            const T* dv = sm.t + gr.ety[e] * kK;
+            T acc = dv[0] * d0.x;
+            acc += dv[1] * d0.y;
+            acc += dv[2] * d0.z;
+            acc += dv[3] * d0.w;
+            acc += dv[4] * d1.x;
+            acc += dv[5] * d1.y;
+            acc += dv[6] * d1.z;
+            acc += dv[7] * d1.w;
+            const T gv = ws.g[e] + acc;
+            ws.g[e] = gv;
+            ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
         }
         __syncwarp();
     }
@@ -1479,6 +1776,22 @@ int force_grid(int n) {
 
 constexpr int kMaxSmem = 200 * 1024;
 
+// Message backward form (see pull_edges): the pull form needs the symmetric
+// periodic graph with every atom running the network (no halo ghosts, no global
+// list, no domain-decomposition rows); everything else runs the push form.
+// HMDP_PULL=0|1|2 pins it (A/B experiments); default kPullDefault.
+constexpr int kPullDefault = 1;
+template <typename T>
+static int pull_mode(const DevGraph& gr, const DevWork<T>& ws) {
+    static const int env = [] {
+        const char* e = std::getenv("HMDP_PULL");
+        const int v = e ? std::atoi(e) : -1;
+        return (v >= 0 && v <= 2) ? v : -1;
+    }();
+    if (!gr.sym || gr.alist || gr.n_active != gr.n || ws.s_remote || ws.p_atom || !ws.vrow) return 0;
+    return env >= 0 ? env : kPullDefault;
+}
+
 // The network phases for one element type and team size.
 template <typename T, int G, bool LIST = false>
 struct Net {
@@ -1493,6 +1806,17 @@ struct Net {
                               cudaFuncSetAttribute(k_msg_bwd<T, G, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_embed_bwd<T, G, LIST>, a, kMaxSmem)})
             if (r != cudaSuccess) e = r;
+        if constexpr (!LIST) {
+            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_fwd<T, G, true, false, 1>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_msg_fwd<T, G, false, false, 1>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_msg_fwd<T, G, true, false, 2>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_msg_fwd<T, G, false, false, 2>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 2>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 2>, a, kMaxSmem)})
+                if (r != cudaSuccess) e = r;
+        }
         return e;
     }
     // returns the kernels launched (2 with the tcgen05 embedding chain)
@@ -1518,19 +1842,40 @@ struct Net {
         launch_net<T>(k_embed<T, G, false, LIST>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
         return 1;
     }
-    static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                        const DevWork<T>& ws, int l, cudaStream_t st) {
+    template <int PULL>
+    static void msg_fwd_p(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                          const DevWork<T>& ws, int l, cudaStream_t st) {
         if (l == md.n_msg - 1)
-            launch_net<T>(k_msg_fwd<T, G, true, LIST>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_fwd<T, G, true, LIST, PULL>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
         else
-            launch_net<T>(k_msg_fwd<T, G, false, LIST>, Phase::MsgFwd, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_fwd<T, G, false, LIST, PULL>, Phase::MsgFwd, sh, st, md, gr, ws, l);
+    }
+    static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                        const DevWork<T>& ws, int l, cudaStream_t st, int pull = 0) {
+        if constexpr (!LIST) {
+            if (pull == 1) return msg_fwd_p<1>(sh, md, gr, ws, l, st);
+            if (pull == 2) return msg_fwd_p<2>(sh, md, gr, ws, l, st);
+        }
+        msg_fwd_p<0>(sh, md, gr, ws, l, st);
     }
     static void msg_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                        const DevWork<T>& ws, int l, cudaStream_t st) {
+                        const DevWork<T>& ws, int l, cudaStream_t st, int pull = 0) {
+        if constexpr (!LIST) {
+            if (pull == 1)
+                return launch_net<T>(k_msg_bwd_pull<T, G, 1>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+            if (pull == 2)
+                return launch_net<T>(k_msg_bwd_pull<T, G, 2>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+        }
         launch_net<T>(k_msg_bwd<T, G, LIST>, Phase::MsgBwd, sh, st, md, gr, ws, l);
     }
     static void embed_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                          const DevWork<T>& ws, cudaStream_t st) {
+                          const DevWork<T>& ws, cudaStream_t st, int pull = 0) {
+        if constexpr (!LIST) {
+            if (pull == 1)
+                return launch_net<T>(k_embed_bwd_pull<T, G, 1>, Phase::EmbedBwd, sh, st, md, gr, ws);
+            if (pull == 2)
+                return launch_net<T>(k_embed_bwd_pull<T, G, 2>, Phase::EmbedBwd, sh, st, md, gr, ws);
+        }
         launch_net<T>(k_embed_bwd<T, G, LIST>, Phase::EmbedBwd, sh, st, md, gr, ws);
     }
     static int network(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
@@ -1540,15 +1885,16 @@ struct Net {
         const int ne = embed(sh, md, gr, ws, rev, mf, st);
         mk(M == 0 ? "embed_fit" : "embed", st);
         if (M == 0) return 1;
+        const int pull = pull_mode(gr, ws);
         for (int l = 0; l < M; ++l) {
-            msg_fwd(sh, md, gr, ws, l, st);
+            msg_fwd(sh, md, gr, ws, l, st, pull);
             mk(l == M - 1 ? "msg_fwd_last" : "msg_fwd", st);
         }
         for (int l = M - 2; l >= 0; --l) {
-            msg_bwd(sh, md, gr, ws, l, st);
+            msg_bwd(sh, md, gr, ws, l, st, pull);
             mk("msg_bwd", st);
         }
-        embed_bwd(sh, md, gr, ws, st);
+        embed_bwd(sh, md, gr, ws, st, pull);
         mk("embed_bwd", st);
         return ne + 1 + M + (M - 1);
     }
