@@ -45,6 +45,9 @@
 //   k_force        force / virial (gather form) + E, W sums   :288-298, :372-387
 //                  [+ velocity Verlet tail, src/integrators.cpp:32-47]
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 
 #include "hmdp_common.cuh"
@@ -131,6 +134,7 @@ struct WarpSmem {
     alignas(16) T ed[32][20];  // edge scalars: (s, s', c0 | -, -, b or b'[8], [b[8]])
     alignas(16) T red[2][64];  // team-sum partials (double-buffered)
     T reds[2];
+    int nxt[2];    // dynamic atom schedule: the team's next atom (lead warp's copy)
     int emir[32];  // staged mirror slots
     int ety[32];   // staged neighbour types
     int enb[32];   // staged neighbour indices (P_j row gathers)
@@ -315,6 +319,46 @@ struct Team {
     __device__ __forceinline__ int local(int cnt) const { return (cnt - w + G - 1) / G; }
 };
 
+// A team's atoms.  Static: grid-stride from tm.first (domain decomposition and
+// atom lists).  Dynamic (ws.dyn >= 0, single-domain network): every team starts
+// on its static first atom (no fetch on the critical path), then takes tickets
+// from the kernel's counter ws.actr[dyn] -- atom tm.stride + ticket -- fetched by
+// the team's lead lane one atom ahead, so the atomic's latency hides under the
+// current atom.  Teams keep taking atoms until the tickets pass the end, so the
+// grid is sized to the resident CTAs and the per-SM load evens out (28 atoms per
+// SM at 2PTC over 8 teams would otherwise leave 4 atoms on some teams and 3 on
+// others).  Which team runs an atom does not change its result.  The force
+// kernel re-arms the counters.
+template <int G, bool DYN>
+struct AtomIter {
+    unsigned* ctr;  // DYN: this launch's ticket counter
+    int pre = 0;
+    int pb = 0;
+    template <typename T>
+    __device__ explicit AtomIter(const DevWork<T>& ws) : ctr(DYN ? ws.actr + ws.dyn : nullptr) {}
+    __device__ __forceinline__ int first(const Team<G>& tm) const { return tm.first; }
+    // at the top of the atom body: the ticket of the atom after this one
+    // (none when the teams' first atoms already cover all n_run)
+    __device__ __forceinline__ void prefetch(const Team<G>& tm, int n_run) {
+        if (DYN && tm.w == 0 && tm.lane == 0)
+            pre = tm.stride >= n_run ? n_run : tm.stride + static_cast<int>(atomicAdd(ctr, 1u));
+    }
+    template <typename T>
+    __device__ __forceinline__ int next(int k, Team<G>& tm, WarpSmem<T>& sm) {
+        if constexpr (!DYN) return k + tm.stride;
+        if constexpr (G == 1) {
+            return __shfl_sync(FULL_MASK, pre, 0);
+        } else {
+            WarpSmem<T>* lead = &sm - tm.w;  // double-buffered: one barrier per atom
+            if (tm.w == 0 && tm.lane == 0) lead->nxt[pb] = pre;
+            tm.sync();
+            const int r = lead->nxt[pb];
+            pb ^= 1;
+            return r;
+        }
+    }
+};
+
 // Team mat-vec: sum_{k<NIN} W[row][k] x[k] with the inputs split over the
 // team's warps (warp w: inputs [w NIN/G, (w+1) NIN/G)) and the partials summed
 // in a fixed order — one copy of the weight traffic per team, not per warp.
@@ -422,7 +466,7 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // ---------------------------------------------------------------------------
 // DESC_ONLY: the edge work and the descriptor only; the embedding MLP and the P^0
 // projection then run as one tcgen05 layer chain over all atoms (hmdp_tc.cu).
-template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false>
+template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
@@ -461,7 +505,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevMod
     auto sb = sm.ed;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
+        at.prefetch(tm, n_run);
         const int i = LIST ? gr.alist[k_at] : k_at;
         const int start = gr.row_start[i] + tm.w, cnt = gr.nnei[i];
         const int mloc = tm.local(cnt);
@@ -981,7 +1027,7 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
 // Message layer l forward; LAST fuses the fitting net and the top layer's
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0>
+template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
@@ -1031,7 +1077,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
     T* Z = ws.z + (kRecomputeZ && PULL == 0 ? 0 : static_cast<long long>(l) * ws.slots * kH);
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
+        at.prefetch(tm, n_run);
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
@@ -1175,7 +1223,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
-template <typename T, int G, bool LIST = false>
+template <typename T, int G, bool LIST = false, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1206,7 +1254,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
                               : ws.z + static_cast<long long>(l) * ws.slots * kH;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
+        at.prefetch(tm, n_run);
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         // one round trip: own adjoint, update activations, the pushed adjoint rows
@@ -1242,7 +1292,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
-template <typename T, int G, bool LIST = false>
+template <typename T, int G, bool LIST = false, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1261,7 +1311,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
     pdl_wait();
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
+        at.prefetch(tm, n_run);
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
@@ -1333,7 +1385,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
 // Pull form, lower layers (l < M-1): the sender-side backward of layer l+1's
 // messages (gathering the receivers' v^{l+1} rows), dE/dh^{l+1}_k, then layer l's
 // update backward (v^l_k, c0^l_k for the next kernel).
-template <typename T, int G, int PULL>
+template <typename T, int G, int PULL, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
                                                                     DevGraph gr, DevWork<T> ws,
                                                                     int l) {
@@ -1362,7 +1414,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull
     const T* V = ws.vrow + static_cast<long long>((l + 1) & 1) * n * kH;
     const T* C0 = ws.vc0 + static_cast<long long>((l + 1) & 1) * n;
     const bool first_g = l == md.n_msg - 2;
-    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k = at.first(tm); k < gr.n_active; k = at.next(k, tm, sm)) {
+        at.prefetch(tm, gr.n_active);
         AtomRow<G> ar(gr, k, tm);
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T zu = ws.uz1[(static_cast<long long>(l) * n + k) * kH + lane];
@@ -1388,7 +1442,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull
 // Pull form, embedding backward: the sender-side backward of layer 0's messages,
 // dE/dh^0_k, the embedding backward and the descriptor adjoint; pushes the final
 // g to the mirrors for the force gather.
-template <typename T, int G, int PULL>
+template <typename T, int G, int PULL, bool DYN = false>
 __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
                                                                       DevGraph gr,
                                                                       DevWork<T> ws) {
@@ -1413,7 +1467,9 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd_pu
     pdl_wait();
     const int n = gr.n;
     const bool first_g = md.n_msg == 1;
-    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
+    AtomIter<G, DYN> at(ws);
+    for (int k = at.first(tm); k < gr.n_active; k = at.next(k, tm, sm)) {
+        at.prefetch(tm, gr.n_active);
         AtomRow<G> ar(gr, k, tm);
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(k) * kH + lane];
@@ -1490,6 +1546,9 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
     __shared__ bool s_last;
     pdl_launch_dependents();
     pdl_wait();
+    // every network kernel of this evaluation has completed: re-arm their
+    // dynamic atom-schedule counters for the next one
+    if (ws.actr && blockIdx.x == 0 && threadIdx.x < kAtomCounters) ws.actr[threadIdx.x] = 0u;
     const WarpPos wp;
     const int lane = wp.lane, wc = threadIdx.x >> 5;
     double acc[11];
@@ -1720,6 +1779,7 @@ static int staged_elems(Phase p) {
 // two CTAs per SM.
 struct NetShape {
     int G, warps, grid;
+    int dyn = 0;  // 1: dynamic atom schedule (grid capped at the resident CTAs)
 };
 int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments)
     static const int v = [] {
@@ -1748,7 +1808,25 @@ static NetShape net_shape(int n, int n_msg, int elem_bytes) {
     if (G == 1 && teams < 2) teams = 2;
     int grid = (n + teams - 1) / teams;
     if (grid > 2 * sms) grid = 2 * sms;
-    return {G, teams * G, grid < 1 ? 1 : grid};
+    return {G, teams * G, grid < 1 ? 1 : grid, 0};
+}
+
+// CTAs of a kernel resident per SM at a given block / shared-memory size (cached;
+// the dynamic atom schedule launches exactly that many per SM).
+static int resident_ctas(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(fn, threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    cache.emplace(key, nb);
+    return nb;
 }
 
 template <typename T, typename... Params, typename... Args>
@@ -1756,7 +1834,13 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
                        Args... args) {
     const size_t smem = static_cast<size_t>(staged_elems<T>(p)) * sizeof(T) + 16 +
                         static_cast<size_t>(sh.warps) * sizeof(WarpSmem<T>);
-    const cudaError_t e = launch_pdl(kernel, dim3(sh.grid), dim3(32 * sh.warps), smem, st, args...);
+    int grid = sh.grid;
+    if (sh.dyn) {  // dynamic atom schedule: one wave of resident CTAs
+        const int per_sm = resident_ctas(reinterpret_cast<const void*>(kernel), 32 * sh.warps, smem);
+        const int g = per_sm * num_sms();
+        grid = g < grid ? g : grid;
+    }
+    const cudaError_t e = launch_pdl(kernel, dim3(grid), dim3(32 * sh.warps), smem, st, args...);
     if (e != cudaSuccess && std::getenv("HMDP_DEBUG_LAUNCH")) {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, kernel);
@@ -1775,6 +1859,17 @@ int force_grid(int n) {
 }
 
 constexpr int kMaxSmem = 200 * 1024;
+
+// Dynamic atom schedule (AtomIter) for the single-domain network; HMDP_DYN=0|1
+// pins it (A/B experiments).
+constexpr bool kDynDefault = true;
+static bool dyn_sched_on() {
+    static const int env = [] {
+        const char* e = std::getenv("HMDP_DYN");
+        return e ? std::atoi(e) : -1;
+    }();
+    return env >= 0 ? env != 0 : kDynDefault;
+}
 
 // Message backward form (see pull_edges): the pull form needs the symmetric
 // periodic graph with every atom running the network (no halo ghosts, no global
@@ -1795,38 +1890,52 @@ static int pull_mode(const DevGraph& gr, const DevWork<T>& ws) {
 // The network phases for one element type and team size.
 template <typename T, int G, bool LIST = false>
 struct Net {
+    template <int PULL, bool DYN>
+    static cudaError_t configure_pd() {
+        const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        cudaError_t e = cudaSuccess;
+        for (cudaError_t r : {cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST, PULL, DYN>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST, PULL, DYN>, a, kMaxSmem)})
+            if (r != cudaSuccess) e = r;
+        if constexpr (PULL == 0) {
+            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd<T, G, LIST, DYN>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd<T, G, LIST, DYN>, a, kMaxSmem)})
+                if (r != cudaSuccess) e = r;
+        } else {
+            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd_pull<T, G, PULL, DYN>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, PULL, DYN>, a, kMaxSmem)})
+                if (r != cudaSuccess) e = r;
+        }
+        return e;
+    }
     static cudaError_t configure() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
         for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_embed<T, G, false, LIST>, a, kMaxSmem),
                               cudaFuncSetAttribute(k_embed<T, G, false, LIST, true>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_bwd<T, G, LIST>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_embed_bwd<T, G, LIST>, a, kMaxSmem)})
+                              configure_pd<0, false>()})
             if (r != cudaSuccess) e = r;
         if constexpr (!LIST) {
-            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_fwd<T, G, true, false, 1>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_msg_fwd<T, G, false, false, 1>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_msg_fwd<T, G, true, false, 2>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_msg_fwd<T, G, false, false, 2>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 2>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 2>, a, kMaxSmem)})
+            for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, false, false, true>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed<T, G, false, false, false, true>, a, kMaxSmem),
+                                  configure_pd<0, true>(), configure_pd<1, false>(),
+                                  configure_pd<1, true>(), configure_pd<2, false>(),
+                                  configure_pd<2, true>()})
                 if (r != cudaSuccess) e = r;
         }
         return e;
     }
     // returns the kernels launched (2 with the tcgen05 embedding chain)
+    template <bool DYN = false>
     static int embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                      const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
         if (md.n_msg == 0) {
-            launch_net<T>(k_embed<T, G, true, LIST>, Phase::EmbedFit, sh, st, md, gr, ws, rev, mf);
+            launch_net<T>(k_embed<T, G, true, LIST, false, DYN>, Phase::EmbedFit, sh, st, md, gr, ws,
+                          rev, mf);
             return 1;
         }
-        if constexpr (sizeof(T) == 4 && !LIST) {
+        if constexpr (sizeof(T) == 4 && !LIST && !DYN) {
             if (tc_embed_on(gr.n_active) && !ws.p_atom) {
                 launch_net<T>(k_embed<T, G, false, LIST, true>, Phase::Embed, sh, st, md, gr, ws,
                               rev, mf);
@@ -1839,73 +1948,95 @@ struct Net {
                 return 2;
             }
         }
-        launch_net<T>(k_embed<T, G, false, LIST>, Phase::Embed, sh, st, md, gr, ws, rev, mf);
+        launch_net<T>(k_embed<T, G, false, LIST, false, DYN>, Phase::Embed, sh, st, md, gr, ws, rev,
+                      mf);
         return 1;
     }
-    template <int PULL>
-    static void msg_fwd_p(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                          const DevWork<T>& ws, int l, cudaStream_t st) {
-        if (l == md.n_msg - 1)
-            launch_net<T>(k_msg_fwd<T, G, true, LIST, PULL>, Phase::MsgFwdLast, sh, st, md, gr, ws, l);
-        else
-            launch_net<T>(k_msg_fwd<T, G, false, LIST, PULL>, Phase::MsgFwd, sh, st, md, gr, ws, l);
-    }
+    template <int PULL, bool DYN = false>
     static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                        const DevWork<T>& ws, int l, cudaStream_t st, int pull = 0) {
-        if constexpr (!LIST) {
-            if (pull == 1) return msg_fwd_p<1>(sh, md, gr, ws, l, st);
-            if (pull == 2) return msg_fwd_p<2>(sh, md, gr, ws, l, st);
-        }
-        msg_fwd_p<0>(sh, md, gr, ws, l, st);
+                        const DevWork<T>& ws, int l, cudaStream_t st) {
+        if (l == md.n_msg - 1)
+            launch_net<T>(k_msg_fwd<T, G, true, LIST, PULL, DYN>, Phase::MsgFwdLast, sh, st, md, gr,
+                          ws, l);
+        else
+            launch_net<T>(k_msg_fwd<T, G, false, LIST, PULL, DYN>, Phase::MsgFwd, sh, st, md, gr, ws,
+                          l);
     }
+    template <int PULL, bool DYN = false>
     static void msg_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                        const DevWork<T>& ws, int l, cudaStream_t st, int pull = 0) {
-        if constexpr (!LIST) {
-            if (pull == 1)
-                return launch_net<T>(k_msg_bwd_pull<T, G, 1>, Phase::MsgBwd, sh, st, md, gr, ws, l);
-            if (pull == 2)
-                return launch_net<T>(k_msg_bwd_pull<T, G, 2>, Phase::MsgBwd, sh, st, md, gr, ws, l);
-        }
-        launch_net<T>(k_msg_bwd<T, G, LIST>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+                        const DevWork<T>& ws, int l, cudaStream_t st) {
+        if constexpr (PULL == 0)
+            launch_net<T>(k_msg_bwd<T, G, LIST, DYN>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+        else
+            launch_net<T>(k_msg_bwd_pull<T, G, PULL, DYN>, Phase::MsgBwd, sh, st, md, gr, ws, l);
     }
+    template <int PULL, bool DYN = false>
     static void embed_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
-                          const DevWork<T>& ws, cudaStream_t st, int pull = 0) {
-        if constexpr (!LIST) {
-            if (pull == 1)
-                return launch_net<T>(k_embed_bwd_pull<T, G, 1>, Phase::EmbedBwd, sh, st, md, gr, ws);
-            if (pull == 2)
-                return launch_net<T>(k_embed_bwd_pull<T, G, 2>, Phase::EmbedBwd, sh, st, md, gr, ws);
+                          const DevWork<T>& ws, cudaStream_t st) {
+        if constexpr (PULL == 0)
+            launch_net<T>(k_embed_bwd<T, G, LIST, DYN>, Phase::EmbedBwd, sh, st, md, gr, ws);
+        else
+            launch_net<T>(k_embed_bwd_pull<T, G, PULL, DYN>, Phase::EmbedBwd, sh, st, md, gr, ws);
+    }
+    // One evaluation's network kernels.  DYN: launch j takes its atoms from
+    // counter j (AtomIter; the force kernel re-arms them) on a grid of resident CTAs.
+    template <int PULL, bool DYN>
+    static int network_pd(const NetShape& sh0, const DevModel<T>& md, const DevGraph& gr,
+                          const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
+                          const MdFuse& mf) {
+        const int M = md.n_msg;
+        NetShape sh = sh0;
+        sh.dyn = DYN ? 1 : 0;
+        int slot = 0;
+        auto w_at = [&](int j) {
+            DevWork<T> w = ws;
+            w.dyn = DYN ? j : -1;
+            return w;
+        };
+        const int ne = embed<DYN>(sh, md, gr, w_at(slot++), rev, mf, st);
+        mk(M == 0 ? "embed_fit" : "embed", st);
+        if (M == 0) return 1;
+        for (int l = 0; l < M; ++l) {
+            msg_fwd<PULL, DYN>(sh, md, gr, w_at(slot++), l, st);
+            mk(l == M - 1 ? "msg_fwd_last" : "msg_fwd", st);
         }
-        launch_net<T>(k_embed_bwd<T, G, LIST>, Phase::EmbedBwd, sh, st, md, gr, ws);
+        for (int l = M - 2; l >= 0; --l) {
+            msg_bwd<PULL, DYN>(sh, md, gr, w_at(slot++), l, st);
+            mk("msg_bwd", st);
+        }
+        embed_bwd<PULL, DYN>(sh, md, gr, w_at(slot++), st);
+        mk("embed_bwd", st);
+        return ne + 1 + M + (M - 1);
     }
     static int network(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                        const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
                        const MdFuse& mf) {
-        const int M = md.n_msg;
-        const int ne = embed(sh, md, gr, ws, rev, mf, st);
-        mk(M == 0 ? "embed_fit" : "embed", st);
-        if (M == 0) return 1;
-        const int pull = pull_mode(gr, ws);
-        for (int l = 0; l < M; ++l) {
-            msg_fwd(sh, md, gr, ws, l, st, pull);
-            mk(l == M - 1 ? "msg_fwd_last" : "msg_fwd", st);
+        if constexpr (!LIST) {
+            // only when the static grid's teams do not already take one atom each
+            // (measured: DPA3 2PTC +3 %, 1UBQ +3-5 %; 1YRF, one atom per team, -2 %);
+            // the opt-in tcgen05 embedding chain runs on the static schedule
+            const bool dyn = dyn_sched_on() && ws.actr && !gr.alist &&
+                             gr.n_active > sh.grid * (sh.warps / G) &&
+                             !(sizeof(T) == 4 && tc_embed_on(gr.n_active) && !ws.p_atom);
+            switch (pull_mode(gr, ws) * 2 + (dyn ? 1 : 0)) {
+                case 1: return network_pd<0, true>(sh, md, gr, ws, rev, st, mk, mf);
+                case 2: return network_pd<1, false>(sh, md, gr, ws, rev, st, mk, mf);
+                case 3: return network_pd<1, true>(sh, md, gr, ws, rev, st, mk, mf);
+                case 4: return network_pd<2, false>(sh, md, gr, ws, rev, st, mk, mf);
+                case 5: return network_pd<2, true>(sh, md, gr, ws, rev, st, mk, mf);
+                default: break;
+            }
         }
-        for (int l = M - 2; l >= 0; --l) {
-            msg_bwd(sh, md, gr, ws, l, st, pull);
-            mk("msg_bwd", st);
-        }
-        embed_bwd(sh, md, gr, ws, st, pull);
-        mk("embed_bwd", st);
-        return ne + 1 + M + (M - 1);
+        return network_pd<0, false>(sh, md, gr, ws, rev, st, mk, mf);
     }
     static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                          const DevWork<T>& ws, int phase, int l, cudaStream_t st, int* rev) {
         const MdFuse none{};
         switch (phase) {
             case 0: embed(sh, md, gr, ws, rev, none, st); break;
-            case 2: msg_fwd(sh, md, gr, ws, l, st); break;
-            case 4: msg_bwd(sh, md, gr, ws, l, st); break;
-            case 5: embed_bwd(sh, md, gr, ws, st); break;
+            case 2: msg_fwd<0>(sh, md, gr, ws, l, st); break;
+            case 4: msg_bwd<0>(sh, md, gr, ws, l, st); break;
+            case 5: embed_bwd<0>(sh, md, gr, ws, st); break;
         }
     }
 };
