@@ -44,6 +44,7 @@
 //   k_embed_bwd    embedding + descriptor adjoint             :355-370
 //   k_force        force / virial (gather form) + E, W sums   :288-298, :372-387
 //                  [+ velocity Verlet tail, src/integrators.cpp:32-47]
+#include <algorithm>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -97,7 +98,18 @@ __device__ unsigned long long g_tprobe[32];
 #define TP(k)
 #endif
 
-constexpr int kMaxWarps = 16;  // warps per CTA (network kernels)
+// 20: measured against 16 on B200 (DPA3 FP32, flushed L2): 2PTC 6.94k -> 7.48k,
+// 3LZM 9.13k -> 10.10k, 1UBQ 12.5k -> 16.7k steps/s (1UBQ: 9 teams per CTA no
+// longer need a second wave of CTAs); 24 spills more (2PTC 7.04k).
+#ifndef HMDP_TEAM_CTA_WARPS
+#define HMDP_TEAM_CTA_WARPS 20
+#endif
+constexpr int kMaxWarps = 16;  // warps per CTA (network kernels, 1-warp teams)
+// warps per CTA of the 2- and 4-warp-team kernels (one CTA per SM: the register
+// budget per thread is 65536 / (32 x this))
+// (FP64, the parity mode, keeps 16: its registers would not fit more)
+template <typename T, int G>
+constexpr int kCtaWarps = (G == 1 || sizeof(T) > 4) ? kMaxWarps : HMDP_TEAM_CTA_WARPS;
 // Message layers: store every layer's z_e rows (false) or only the LAST layer's and
 // recompute z_e = tanh(W1b b_e + b1 + P^l_j) in the lower layers' backward (true:
 // a tanh + 8 FMAs per edge channel instead of a 128-byte row that spills to HBM at
@@ -467,7 +479,7 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // DESC_ONLY: the edge work and the descriptor only; the embedding MLP and the P^0
 // projection then run as one tcgen05 layer chain over all atoms (hmdp_tc.cu).
 template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1028,7 +1040,7 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1224,7 +1236,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_fwd(DevM
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
 template <typename T, int G, bool LIST = false, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -1293,7 +1305,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevM
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T, int G, bool LIST = false, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -1386,7 +1398,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(De
 // messages (gathering the receivers' v^{l+1} rows), dE/dh^{l+1}_k, then layer l's
 // update backward (v^l_k, c0^l_k for the next kernel).
 template <typename T, int G, int PULL, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
                                                                     DevGraph gr, DevWork<T> ws,
                                                                     int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1443,7 +1455,7 @@ __global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_msg_bwd_pull
 // dE/dh^0_k, the embedding backward and the descriptor adjoint; pushes the final
 // g to the mirrors for the force gather.
 template <typename T, int G, int PULL, bool DYN = false>
-__global__ __launch_bounds__(kMaxWarps * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
+__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
                                                                       DevGraph gr,
                                                                       DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1799,9 +1811,9 @@ int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments
 static NetShape net_shape(int n, int n_msg, int elem_bytes) {
     const int sms = num_sms();
     const int two_upto = (n_msg > 0 ? 40 : 10) * sms;
-    const int max_warps = elem_bytes > 4 ? kMaxWarps / 2 : kMaxWarps;
     int G = (4 * n <= kMaxWarps * sms) ? 4 : (n <= two_upto ? 2 : 1);
     if (team_override()) G = team_override();
+    const int max_warps = elem_bytes > 4 ? kMaxWarps / 2 : (G == 1 ? kCtaWarps<float, 1> : kCtaWarps<float, 2>);
     const int max_teams = max_warps / G;
     int teams = (n + sms - 1) / sms;
     teams = teams < 1 ? 1 : (teams > max_teams ? max_teams : teams);
@@ -1834,12 +1846,13 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
                        Args... args) {
     const size_t smem = static_cast<size_t>(staged_elems<T>(p)) * sizeof(T) + 16 +
                         static_cast<size_t>(sh.warps) * sizeof(WarpSmem<T>);
+    // at most one wave of resident CTAs: the teams grid-stride (or, dynamic
+    // schedule, take tickets) over the remaining atoms instead of a partial second
+    // wave of CTAs doubling the kernel time
     int grid = sh.grid;
-    if (sh.dyn) {  // dynamic atom schedule: one wave of resident CTAs
-        const int per_sm = resident_ctas(reinterpret_cast<const void*>(kernel), 32 * sh.warps, smem);
-        const int g = per_sm * num_sms();
-        grid = g < grid ? g : grid;
-    }
+    const int per_sm = resident_ctas(reinterpret_cast<const void*>(kernel), 32 * sh.warps, smem);
+    const int g = per_sm * num_sms();
+    grid = g < grid ? g : grid;
     const cudaError_t e = launch_pdl(kernel, dim3(grid), dim3(32 * sh.warps), smem, st, args...);
     if (e != cudaSuccess && std::getenv("HMDP_DEBUG_LAUNCH")) {
         cudaFuncAttributes fa{};
@@ -2016,7 +2029,7 @@ struct Net {
             // (measured: DPA3 2PTC +3 %, 1UBQ +3-5 %; 1YRF, one atom per team, -2 %);
             // the opt-in tcgen05 embedding chain runs on the static schedule
             const bool dyn = dyn_sched_on() && ws.actr && !gr.alist &&
-                             gr.n_active > sh.grid * (sh.warps / G) &&
+                             gr.n_active > std::min(sh.grid, num_sms()) * (sh.warps / G) &&
                              !(sizeof(T) == 4 && tc_embed_on(gr.n_active) && !ws.p_atom);
             switch (pull_mode(gr, ws) * 2 + (dyn ? 1 : 0)) {
                 case 1: return network_pd<0, true>(sh, md, gr, ws, rev, st, mk, mf);
