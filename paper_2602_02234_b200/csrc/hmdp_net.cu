@@ -1875,7 +1875,7 @@ constexpr int kMaxSmem = 200 * 1024;
 
 // Dynamic atom schedule (AtomIter) for the single-domain network; HMDP_DYN=0|1
 // pins it (A/B experiments).
-constexpr bool kDynDefault = true;
+constexpr bool kDynDefault = false;
 static bool dyn_sched_on() {
     static const int env = [] {
         const char* e = std::getenv("HMDP_DYN");
@@ -1887,17 +1887,26 @@ static bool dyn_sched_on() {
 // Message backward form (see pull_edges): the pull form needs the symmetric
 // periodic graph with every atom running the network (no halo ghosts, no global
 // list, no domain-decomposition rows); everything else runs the push form.
-// HMDP_PULL=0|1|2 pins it (A/B experiments); default kPullDefault.
-constexpr int kPullDefault = 1;
+// Stored z rows (PULL 1) while the M layers' rows fit comfortably in L2, recomputed
+// (PULL 2) beyond.  Measured on B200 (DPA3 FP32, flushed L2, steps/s):
+//              push (0)   stored z (1)   recomputed z (2)   DRAM/step (ncu, 0/1/2)
+//   2PTC        6443        7483           7343             112.5 / 23.1 / 1.6 MB
+//   2PTC x8     1114        1223           1451
+//   2PTC x64     145         164            195
+// HMDP_PULL=0|1|2 pins it (A/B experiments).
+constexpr size_t kZRowsL2Budget = 48u << 20;  // bytes of stored z rows (126 MB L2)
 template <typename T>
-static int pull_mode(const DevGraph& gr, const DevWork<T>& ws) {
+static int pull_mode(const DevGraph& gr, const DevWork<T>& ws, int n_msg) {
     static const int env = [] {
         const char* e = std::getenv("HMDP_PULL");
         const int v = e ? std::atoi(e) : -1;
         return (v >= 0 && v <= 2) ? v : -1;
     }();
     if (!gr.sym || gr.alist || gr.n_active != gr.n || ws.s_remote || ws.p_atom || !ws.vrow) return 0;
-    return env >= 0 ? env : kPullDefault;
+    if (env >= 0) return env;
+    // ~32 neighbours per atom at the paper density
+    const size_t zbytes = static_cast<size_t>(gr.n_active) * n_msg * 32 * kH * sizeof(T);
+    return zbytes > kZRowsL2Budget ? 2 : 1;
 }
 
 // The network phases for one element type and team size.
@@ -2031,7 +2040,7 @@ struct Net {
             const bool dyn = dyn_sched_on() && ws.actr && !gr.alist &&
                              gr.n_active > std::min(sh.grid, num_sms()) * (sh.warps / G) &&
                              !(sizeof(T) == 4 && tc_embed_on(gr.n_active) && !ws.p_atom);
-            switch (pull_mode(gr, ws) * 2 + (dyn ? 1 : 0)) {
+            switch (pull_mode(gr, ws, md.n_msg) * 2 + (dyn ? 1 : 0)) {
                 case 1: return network_pd<0, true>(sh, md, gr, ws, rev, st, mk, mf);
                 case 2: return network_pd<1, false>(sh, md, gr, ws, rev, st, mk, mf);
                 case 3: return network_pd<1, true>(sh, md, gr, ws, rev, st, mk, mf);

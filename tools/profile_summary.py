@@ -40,12 +40,24 @@ def short(name):
 
 
 def profile_name(name):
-    """kernel symbol (team-size template argument dropped) -> hmdp_profile marker"""
-    base = re.sub(r"<([124])>$", "", name)  # k_nbr_search<G>
-    base = re.sub(r"<(float|double), [124]", r"<\1", base)  # k_*<T, G, ...>
-    if base.startswith(("k_embed<", "k_msg_fwd<", "k_msg_bwd<", "k_embed_bwd<")):
-        base = re.sub(r", [01]>$", ">", base)  # the LIST (atom-list) template argument
-    return PROFILE_NAME.get(base)
+    """kernel symbol -> hmdp_profile marker (template arguments: T, team size, then the
+    kernel's switches, printed by ncu as 0/1)"""
+    head, _, args = name.partition("<")
+    a = [x.strip() for x in args.rstrip(">").split(",")] if args else []
+    on = lambda i: len(a) > i and a[i] in ("1", "true")
+    if head == "k_nbr_search":
+        return "nbr_search"
+    if head == "k_embed":
+        return "embed_fit" if on(2) else "embed"
+    if head == "k_msg_fwd":
+        return "msg_fwd_last" if on(2) else "msg_fwd"
+    if head in ("k_msg_bwd", "k_msg_bwd_pull"):
+        return "msg_bwd"
+    if head in ("k_embed_bwd", "k_embed_bwd_pull"):
+        return "embed_bwd"
+    if a and a[0] != "float":
+        return None
+    return PROFILE_NAME.get(f"{head}<float>")
 
 
 def launches(path):
