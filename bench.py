@@ -76,10 +76,11 @@ def parse():
     ap.add_argument("--strong", action="store_true",
                     help="--mode dd: split ONE box over the ranks (strong scaling, SURVEY "
                          "§8(d) configs 3/4) instead of one box per rank")
-    ap.add_argument("--mode", choices=["dd", "dd-allreduce", "replicas"], default="dd",
+    ap.add_argument("--mode", choices=["dd", "dd-gather", "dd-allreduce", "replicas"], default="dd",
                     help="N>1: halo-exchange spatial domain decomposition of the box "
                          "replicated over the rank grid (default; point-to-point NCCL halo "
-                         "rounds, one CUDA graph per MD step), the replicated all-reduce "
+                         "rounds, one CUDA graph per MD step), the paper's gather-to-root "
+                         "strategy on the same engine (dd-gather), the replicated all-reduce "
                          "variant for tiny boxes (dd-allreduce), or independent replica "
                          "boxes (replicas)")
     return ap.parse_args()
@@ -786,8 +787,9 @@ def run_halo(args, rank, world, local_rank, dist):
     s = base if args.strong else P.replicate(base, dims)
     boxes = 1 if args.strong else world
     n = s.n_atoms
+    strategy = "gather" if args.mode == "dd-gather" else "halo"
     eng = dd.HaloDD(P.Context(model, device=local_rank, max_atoms=n), n, s.types, s.box, dims,
-                    rank, prec, masses=s.masses, stream=stream)
+                    rank, prec, masses=s.masses, stream=stream, strategy=strategy)
     use_nccl = dist.get_backend() == "nccl"
     if use_nccl:  # our own communicator: the C++ engine issues ncclSend/ncclRecv itself
         import ctypes
@@ -889,9 +891,14 @@ def run_halo(args, rank, world, local_rank, dist):
                        f"{args.system} box replicated {dims} (one box per GPU)"),
                    "model": args.model, "system": args.system, "atoms_total": n,
                    "rank_grid": list(dims), "precision": args.precision,
-                   "parallelism": f"spatial DD x{world}, rc-deep halo exchanged per layer with "
-                                  f"point-to-point {'NCCL' if use_nccl else 'gloo'} rounds; owners "
-                                  f"integrate their own atoms (migration every step)",
+                   "parallelism": (f"spatial DD x{world}, rc-deep halo exchanged per layer with "
+                                   f"point-to-point {'NCCL' if use_nccl else 'gloo'} rounds; owners "
+                                   f"integrate their own atoms (migration every step)"
+                                   if strategy == "halo" else
+                                   f"spatial DD x{world}, gather-to-root (the paper's strategy, "
+                                   f"SPEC.md:505): owned atoms -> rank 0 over point-to-point "
+                                   f"{'NCCL' if use_nccl else 'gloo'}, one single-domain "
+                                   f"evaluation there, forces back to the owners, who integrate"),
                    "graph": "one CUDA graph per MD step incl. NCCL" if g is not None else "none",
                    "rank0_owned": int((roles == 1).sum()), "rank0_halo": int((roles == 2).sum())},
         "ns_per_day_per_box": ns_per_day(value / boxes),
@@ -954,7 +961,7 @@ def main():
         # the DeePMD-style families have no domain decomposition: their
         # N > 1 line is N independent replicas
         dd_ok = args.model in ("dpa2", "dpa3")
-        if world > 1 and args.mode == "dd" and dd_ok:
+        if world > 1 and args.mode in ("dd", "dd-gather") and dd_ok:
             run_halo(args, rank, world, local_rank, dist)
         elif world > 1 and args.mode == "dd-allreduce" and dd_ok:
             run_gdd(args, rank, world, local_rank, dist)

@@ -273,7 +273,13 @@ typedef struct hmdp_gdd_hub hmdp_gdd_hub;
  * success.  Called with the context's stream synchronized. */
 typedef int (*hmdp_gdd_exchange_fn)(void* user, int round, const void* send, void* recv,
                                     size_t stride, size_t bytes);
-int hmdp_gdd_set_mode(hmdp_ctx* ctx, int mode); /* 0 all-reduce (replicated), 1 halo */
+/* Gather-to-root mode (2; the paper's NNPot strategy, reference SPEC.md:505,
+ * nn_inference_decomposed(strategy = gather_to_root)): the same POS round (migration),
+ * then GATHER (every rank's owned positions -> rank 0), one single-domain evaluation
+ * of the whole system on rank 0, SCATTER (each owner's forces, in the order it sent
+ * its atoms) and OUT; owners integrate their atoms.  Same buffers, plan and step
+ * calls as halo mode; the comparison path for the halo-exchange engine. */
+int hmdp_gdd_set_mode(hmdp_ctx* ctx, int mode); /* 0 all-reduce, 1 halo, 2 gather-to-root */
 /* NCCL transport: 128-byte ncclUniqueId (generated on rank 0 by hmdp_nccl_unique_id
  * and broadcast by the caller), world size and this rank (= DD rank). */
 int hmdp_nccl_unique_id(void* id128);

@@ -86,6 +86,10 @@ void launch_gdd_unpack_copy(int, int, int, const char*, size_t, E*, int, E*, int
 template <typename E>
 void launch_gdd_unpack_add(int, int, int, const char*, size_t, E*, int, cudaStream_t);
 void launch_gdd_tick(int*, cudaStream_t);
+void launch_gdd_gather_list(int, int, const int*, const int*, int, int*, int*, unsigned*,
+                            cudaStream_t);
+template <typename E>
+void launch_gdd_pack_reply(int, int, int, const char*, char*, size_t, const E*, int, cudaStream_t);
 void launch_gdd_stamp_all(int, int*, const int*, cudaStream_t);
 void launch_gdd_out_pack(int, int, const double*, char*, size_t, cudaStream_t);
 void launch_gdd_sum_out(int, int, const char*, size_t, double*, cudaStream_t);
@@ -607,7 +611,9 @@ struct hmdp_ctx {
         double* vel = nullptr;
         double* mass = nullptr;
         // halo-exchange mode (hmdp_gdd_set_mode 1): point-to-point rounds with every
-        // peer instead of all-reduces of replicated global buffers
+        // peer instead of all-reduces of replicated global buffers; gather-to-root
+        // mode (2): the same POS round, then the owned atoms to rank 0, one
+        // single-domain evaluation there, forces back to the owners
         int mode = 0, world = 1, C = 0;
         size_t stride = 0;  // bytes per peer slot of the packet buffers
         DBuf stamp, cur, flist, fcnt, rlist, rcnt, spk, rpk, sremote, hsum, outs;
@@ -2236,7 +2242,7 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
     need_model(ctx);
     auto& g = ctx->gdd;
     if (g.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
-    const bool halo = g.mode == 1;
+    const bool halo = g.mode >= 1;  // halo-exchange or gather-to-root: packet rounds
     if (!g.pos || !g.forces || !g.out || (!halo && (!g.p_atom || !g.sghost)))
         fail(HMDP_INVALID_ARGUMENT, halo ? "hmdp_gdd_bind: buffers 0, 3, 4 must be bound"
                                          : "hmdp_gdd_bind: buffers 0-4 must be bound");
@@ -2244,7 +2250,7 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
     if (((phase >= 1 && phase <= 4) || phase == 22 || phase == 23) &&
         (layer < 0 || layer >= std::max(M, 1)))
         fail(HMDP_INVALID_ARGUMENT, "layer out of range");
-    if (halo && phase >= 20 && phase <= 28 && g.C <= 0)
+    if (halo && phase >= 20 && phase <= 34 && g.C <= 0)
         fail(HMDP_INVALID_ARGUMENT, "halo mode: hmdp_gdd_plan not called");
     set_device(ctx);
     cudaStream_t st = ctx->st();
@@ -2402,6 +2408,46 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 launch_gdd_sum_out(W, R, rpk, g.stride, g.out, st);
                 g.launches += 1;
                 break;
+            // ---- gather-to-root mode ----
+            case 30:  // roles only: this rank's owned list among its current atoms
+                ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
+                launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), lists, counts, st,
+                                 g.stamp.as<int>(), g.cur.as<int>());
+                g.launches += 1;
+                break;
+            case 31:  // GATHER packets: the owned atoms' positions -> rank 0
+                launch_gdd_gather_list(W, 0, lists, counts, C, g.flist.as<int>(), g.fcnt.as<int>(),
+                                       err, st);
+                launch_gdd_pack<double>(W, R, g.flist.as<int>(), g.fcnt.as<int>(), C, g.pos, 3,
+                                        static_cast<const double*>(nullptr), 0, spk, g.stride, st);
+                g.launches += 2;
+                break;
+            case 32:  // rank 0: every owner's positions in place, one single-domain
+                      // evaluation of the whole system; (E, W, W9) only from rank 0
+                launch_gdd_unpack_copy<double>(W, R, C, rpk, g.stride, g.pos, 3,
+                                               static_cast<double*>(nullptr), 0, nullptr, nullptr,
+                                               st);
+                g.launches += 1;
+                if (R == 0) {
+                    g.launches += enqueue_periodic(ctx, n, g.pos, ctx->types.as<int>(), g.box,
+                                                   g.prec, g.forces, nullptr, st);
+                    ck(cudaMemcpyAsync(g.out, ctx->out.p, 16 * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st),
+                       "D2D");
+                } else {
+                    ck(cudaMemsetAsync(g.out, 0, 16 * sizeof(double), st), "memset");
+                }
+                break;
+            case 33:  // SCATTER packets: each peer's atoms' forces, in the order it sent them
+                launch_gdd_pack_reply<double>(W, R, C, rpk, spk, g.stride, g.forces, 3, st);
+                g.launches += 1;
+                break;
+            case 34:  // owners: their atoms' forces
+                launch_gdd_unpack_copy<double>(W, R, C, rpk, g.stride, g.forces, 3,
+                                               static_cast<double*>(nullptr), 0, nullptr, nullptr,
+                                               st);
+                g.launches += 1;
+                break;
             default:
                 fail(HMDP_INVALID_ARGUMENT, "unknown phase");
         }
@@ -2520,9 +2566,27 @@ void gdd_exchange(hmdp_ctx* ctx, int round, size_t bytes) {
 // FORCES, OUT.
 void gdd_step_impl(hmdp_ctx* ctx, int kind, double dt) {
     auto& g = ctx->gdd;
-    if (g.mode != 1) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_step: halo mode only (hmdp_gdd_set_mode)");
+    if (g.mode != 1 && g.mode != 2)
+        fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_step: halo or gather mode only (hmdp_gdd_set_mode)");
     if (kind == 2) {
         gdd_phase_impl(ctx, 8, 0, dt);
+        return;
+    }
+    if (g.mode == 2) {  // gather-to-root: POS (migration), GATHER, SCATTER, OUT
+        gdd_phase_impl(ctx, 20, 0, dt);
+        gdd_exchange(ctx, 0, round_bytes(g.C, g.vel ? 6 : 3, sizeof(double)));
+        gdd_phase_impl(ctx, 21, 0, dt);
+        gdd_phase_impl(ctx, 30, 0, dt);
+        gdd_phase_impl(ctx, 31, 0, dt);
+        gdd_exchange(ctx, 5, round_bytes(g.C, 3, sizeof(double)));
+        gdd_phase_impl(ctx, 32, 0, dt);
+        gdd_phase_impl(ctx, 33, 0, dt);
+        gdd_exchange(ctx, 6, round_bytes(g.C, 3, sizeof(double)));
+        gdd_phase_impl(ctx, 34, 0, dt);
+        gdd_phase_impl(ctx, 28, 0, dt);
+        gdd_exchange(ctx, 4, 16 * sizeof(double));
+        gdd_phase_impl(ctx, 29, 0, dt);
+        if (kind == 1) gdd_phase_impl(ctx, 7, 0, dt);
         return;
     }
     const int M = ctx->n_msg(), C = g.C;
@@ -2559,7 +2623,7 @@ void gdd_step_impl(hmdp_ctx* ctx, int kind, double dt) {
 int hmdp_gdd_set_mode(hmdp_ctx* ctx, int mode) {
     return guarded([&] {
         need_model(ctx);
-        if (mode != 0 && mode != 1) fail(HMDP_INVALID_ARGUMENT, "mode must be 0 or 1");
+        if (mode < 0 || mode > 2) fail(HMDP_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
         if (ctx->gdd.prec < 0) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_setup not called");
         ctx->gdd.mode = mode;
         ctx->gdd.world = ctx->gdd.geom.d[0] * ctx->gdd.geom.d[1] * ctx->gdd.geom.d[2];
@@ -2632,7 +2696,8 @@ int hmdp_gdd_plan(hmdp_ctx* ctx) {
     return guarded([&] {
         need_model(ctx);
         auto& g = ctx->gdd;
-        if (g.mode != 1) fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_plan: halo mode only");
+        if (g.mode != 1 && g.mode != 2)
+            fail(HMDP_INVALID_ARGUMENT, "hmdp_gdd_plan: halo or gather mode only");
         if (!g.pos) fail(HMDP_INVALID_ARGUMENT, "bind the positions first");
         set_device(ctx);
         cudaStream_t st = ctx->st();
@@ -2665,6 +2730,11 @@ int hmdp_gdd_plan(hmdp_ctx* ctx) {
             ck(copy_sync(fc.data(), g.fcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
             ck(copy_sync(rc.data(), g.rcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
             for (int q = 0; q < W; ++q) mx = std::max({mx, fc[q], rc[q]});
+            if (g.mode == 2) {  // the GATHER round carries a whole region's atoms
+                int no = 0;
+                ck(copy_sync(&no, g.counts.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+                mx = std::max(mx, no);
+            }
         }
         ck(cudaMemsetAsync(g.cur.p, 0, sizeof(int), st), "memset");
         g.C = std::min((static_cast<int>(1.5 * mx) + 64 + 31) / 32 * 32, (n + 31) / 32 * 32);
@@ -2698,9 +2768,22 @@ int hmdp_gdd_halo_stats(hmdp_ctx* ctx, long long* out) {
         need_model(ctx);
         if (!out) fail(HMDP_INVALID_ARGUMENT, "null out");
         auto& g = ctx->gdd;
-        if (g.mode != 1 || g.C <= 0) fail(HMDP_INVALID_ARGUMENT, "halo mode not planned");
+        if ((g.mode != 1 && g.mode != 2) || g.C <= 0)
+            fail(HMDP_INVALID_ARGUMENT, "halo mode not planned");
         set_device(ctx);
         const int W = g.world, M = ctx->n_msg();
+        if (g.mode == 2) {  // gather-to-root: GATHER + SCATTER rows of the owned atoms
+            int own = 0;
+            ck(copy_sync(&own, g.counts.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
+            const long long rows = g.geom.rank == 0 ? g.n - own : own;
+            out[0] = g.C;
+            out[1] = W > 1 ? 4 : 0;  // POS, GATHER, SCATTER, OUT
+            out[2] = rows * (2 * (4 + 24)) + (W - 1) * 128;  // (+ the POS round's migrants)
+            out[3] = (W - 1) * static_cast<long long>(round_bytes(g.C, g.vel ? 6 : 3, 8) +
+                                                      2 * round_bytes(g.C, 3, 8) + 128);
+            out[4] = W - 1;
+            return;
+        }
         std::vector<int> fc(W), rc(W);
         ck(copy_sync(fc.data(), g.fcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");
         ck(copy_sync(rc.data(), g.rcnt.p, W * sizeof(int), cudaMemcpyDeviceToHost, ctx->st()), "D2H");

@@ -453,4 +453,62 @@ HMDP_GDD_INST(double)
 HMDP_GDD_PKT_INST(float)
 HMDP_GDD_PKT_INST(double)
 
+// ---------------------------------------------------------------------------
+// Gather-to-root mode (the paper's strategy: the group's atoms are
+// aggregated on one rank for a single inference, forces scattered back to the
+// owners).  GATHER: every rank's owned atoms -> root; SCATTER: root answers each
+// peer with the rows of the atoms that peer sent, in the same order.
+// ---------------------------------------------------------------------------
+// send lists of the GATHER round: this rank's owned list to `root`, nothing to the
+// other peers (lists are [world][C]).
+__global__ void k_gdd_gather_list(int world, int root, const int* __restrict__ owned,
+                                  const int* __restrict__ n_owned, int C, int* __restrict__ lists,
+                                  int* __restrict__ counts, unsigned* err) {
+    const int no = *n_owned;
+    if (blockIdx.x == 0 && threadIdx.x < world)
+        counts[threadIdx.x] = threadIdx.x == root ? (no < C ? no : C) : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && no > C) atomicOr(err, kErrHaloOverflow);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < no && k < C; k += gridDim.x * blockDim.x)
+        lists[root * C + k] = owned[k];
+}
+
+// reply packets: for every peer q, the rows src[gid] of the atoms listed in the
+// packet received from q (count 0 answers an empty packet)
+template <typename E>
+__global__ void k_gdd_pack_reply(int world, int rank, int C, const char* __restrict__ rpk,
+                                 char* __restrict__ spk, size_t pkt_bytes, const E* __restrict__ src,
+                                 int W) {
+    const int q = blockIdx.y;
+    if (q == rank) return;
+    const int* rhead = reinterpret_cast<const int*>(rpk + q * pkt_bytes);
+    const int* rgid = rhead + 4;
+    int* shead = reinterpret_cast<int*>(spk + q * pkt_bytes);
+    int* sgid = shead + 4;
+    E* pay = reinterpret_cast<E*>(spk + q * pkt_bytes + 16 + static_cast<size_t>(C) * 4);
+    const int cnt = min(rhead[0], C);
+    if (blockIdx.x == 0 && threadIdx.x == 0) shead[0] = cnt;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt * W; t += gridDim.x * blockDim.x) {
+        const int k = t / W, c = t - k * W;
+        const long long i = rgid[k];
+        if (c == 0) sgid[k] = static_cast<int>(i);
+        pay[static_cast<size_t>(k) * W + c] = src[i * W + c];
+    }
+}
+
+void launch_gdd_gather_list(int world, int root, const int* owned, const int* n_owned, int C,
+                            int* lists, int* counts, unsigned* err, cudaStream_t st) {
+    const int b = (C + 255) / 256;
+    k_gdd_gather_list<<<b < 1 ? 1 : (b > 64 ? 64 : b), 256, 0, st>>>(world, root, owned, n_owned,
+                                                                     C, lists, counts, err);
+}
+template <typename E>
+void launch_gdd_pack_reply(int world, int rank, int C, const char* rpk, char* spk,
+                           size_t pkt_bytes, const E* src, int W, cudaStream_t st) {
+    const int bx = (C * W + 255) / 256;
+    k_gdd_pack_reply<E><<<dim3(bx < 1 ? 1 : (bx > 64 ? 64 : bx), world), 256, 0, st>>>(
+        world, rank, C, rpk, spk, pkt_bytes, src, W);
+}
+template void launch_gdd_pack_reply<double>(int, int, int, const char*, char*, size_t,
+                                            const double*, int, cudaStream_t);
+
 }  // namespace hmdp

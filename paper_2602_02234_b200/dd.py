@@ -516,7 +516,10 @@ EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctyp
 
 
 class HaloDD:
-    """One rank's halo-exchange DD engine (include/hmdp.h, hmdp_gdd_* halo mode).
+    """One rank's halo-exchange DD engine (include/hmdp.h, hmdp_gdd_* halo mode), or,
+    with ``strategy="gather"``, the paper's gather-to-root strategy on the same
+    transports (owned atoms -> rank 0, one single-domain evaluation, forces back to
+    the owners).
 
     Nothing is replicated: the rank integrates only the atoms its region owns and
     every step moves exactly the halo with point-to-point rounds to every peer
@@ -530,9 +533,13 @@ class HaloDD:
     Global-index buffers: only the rows of owned (and halo) atoms are current on a
     rank; ``owned_forces`` returns this rank's share of the global result."""
 
-    def __init__(self, ctx, n, types, box, dims, rank, precision, masses=None, stream=None):
+    def __init__(self, ctx, n, types, box, dims, rank, precision, masses=None, stream=None,
+                 strategy="halo"):
         import torch
 
+        if strategy not in ("halo", "gather"):
+            raise ValueError("strategy must be 'halo' or 'gather'")
+        self.strategy = strategy
         self.ctx, self.n, self.rank = ctx, int(n), int(rank)
         self.dims = tuple(int(d) for d in dims)
         self.world = self.dims[0] * self.dims[1] * self.dims[2]
@@ -554,7 +561,8 @@ class HaloDD:
         d = np.ascontiguousarray(self.dims, dtype=np.int32)
         check(L.hmdp_gdd_setup(ctx.handle, self.n, ptr(t), ptr(b), ptr(d), self.rank,
                                int(precision)))
-        check(L.hmdp_gdd_set_mode(ctx.handle, 1))
+        # halo exchange (1) or the paper's gather-to-root strategy (2)
+        check(L.hmdp_gdd_set_mode(ctx.handle, 1 if strategy == "halo" else 2))
         for kind, ten in ((0, self.pos), (3, self.f), (4, self.out), (5, self.vel),
                           (6, self.mass)):
             check(L.hmdp_gdd_bind(ctx.handle, kind, ctypes.c_void_p(ten.data_ptr())))

@@ -4,7 +4,10 @@ point-to-point rounds (POS with migration, P^l, dE/dh partial sums, partial forc
 (E, W, W9)).  Ranks are simulated as contexts on cuda:0 (the in-process hub: one
 host thread per rank, the same C++ step program the NCCL transport runs), and as
 two real processes with a gloo callback transport.  Checked against the
-single-domain evaluation and the single-GPU device MD loop."""
+single-domain evaluation and the single-GPU device MD loop.
+The paper's gather-to-root strategy (strategy="gather": owned atoms to rank 0, one
+single-domain evaluation, forces back to the owners) runs on the same engine and
+transports and is held to the same checks."""
 import numpy as np
 import pytest
 
@@ -15,11 +18,11 @@ from paper_2602_02234_b200 import dd
 pytestmark = pytest.mark.gpu
 
 
-def _engines(m, s, dims, prec, masses=None):
+def _engines(m, s, dims, prec, masses=None, strategy="halo"):
     world = dims[0] * dims[1] * dims[2]
     hub = dd.Hub(world)
     engs = [dd.HaloDD(P.Context(m, max_atoms=s.n_atoms), s.n_atoms, s.types, s.box, dims, r, prec,
-                      masses=masses) for r in range(world)]
+                      masses=masses, strategy=strategy) for r in range(world)]
     for e in engs:
         e.attach_hub(hub.handle)
         e.load(s.positions, s.velocities if masses is not None else None)
@@ -169,4 +172,71 @@ def test_halo_dd_two_processes_gloo(mname, golden_models):
     for (rank, E, own, f, ownx, x), e in zip(res, engs):
         assert np.array_equal(ownx, e.roles() == 1)
         assert np.array_equal(x[ownx], e.pos.cpu().numpy()[ownx])  # bitwise: same program
+    hub.close()
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2)])
+def test_gather_to_root_matches_single_domain(mname, dims, golden_models):
+    """SPEC.md:505 gather_to_root: forces and (E, W) equal the single-domain result
+    (FP64), every atom owned by exactly one rank, 4 rounds per step."""
+    s = P.generate_synthetic_system(1231)
+    m = P.model_from_json(golden_models[mname])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    hub, engs = _engines(m, s, dims, P.Precision.fp64, strategy="gather")
+    dd.run_hub(engs, "eval")
+    F, owned = _assemble(engs, s.n_atoms)
+    assert np.all(owned == 1)
+    for e in engs:
+        E, W, W9 = e.energy_virial()
+        assert E == pytest.approx(ref.energy, rel=1e-12)
+        assert np.abs(W9 - ref.virial_tensor).max() < 1e-9 * max(1.0, np.abs(W9).max())
+    assert np.abs(F - ref.forces).max() < 1e-10 * np.abs(ref.forces).max()
+    st = [e.halo_stats() for e in engs]
+    assert all(x["rounds_per_step"] == 4 for x in st)
+    # the root receives (and answers) every other rank's atoms: its rows are their sum
+    ov = 128 * (len(engs) - 1)
+    assert st[0]["halo_bytes_per_step"] - ov == sum(x["halo_bytes_per_step"] - ov for x in st[1:])
+    hub.close()
+
+
+def test_gather_to_root_md_matches_halo_exchange(golden_models):
+    """20 MD steps with migration: gather-to-root and halo exchange give the same
+    owned positions (FP64) and energies as the single-GPU device MD loop."""
+    from paper_2602_02234_b200.md import DeviceMD
+
+    s = P.generate_synthetic_system(1231, temperature=300.0)
+    m = P.model_from_json(golden_models["dpa3"])
+    md = DeviceMD(P.Context(m), s.positions, s.velocities, s.masses, s.types, s.box,
+                  precision=P.Precision.fp64, steps_per_graph=1)
+    md.run(20)
+    x_ref, v_ref, f_ref, e_ref = md.state()
+    hub, engs = _engines(m, s, (2, 2, 1), P.Precision.fp64, masses=s.masses, strategy="gather")
+    dd.run_hub(engs, "eval")
+    dd.run_hub(engs, "open", 0.001)
+    dd.run_hub(engs, "md", 0.001, steps=20)
+    x = np.full((s.n_atoms, 3), np.nan)
+    v = np.full((s.n_atoms, 3), np.nan)
+    owned = np.zeros(s.n_atoms, dtype=int)
+    for e in engs:
+        own = e.roles() == 1
+        x[own] = e.pos.cpu().numpy()[own]
+        v[own] = e.vel.cpu().numpy()[own]
+        owned += own
+    assert np.all(owned == 1)
+    assert np.abs(x - 0.001 * v - x_ref).max() < 1e-10
+    assert engs[1].energy_virial()[0] == pytest.approx(e_ref, rel=1e-11)
+    hub.close()
+
+
+def test_gather_to_root_fp32_within_tolerance(golden_models):
+    s = P.generate_synthetic_system(2643)
+    m = P.model_from_json(golden_models["dpa3"])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    hub, engs = _engines(m, s, (2, 1, 1), P.Precision.fp32, strategy="gather")
+    dd.run_hub(engs, "eval")
+    F, owned = _assemble(engs, s.n_atoms)
+    E = engs[1].energy_virial()[0]
+    assert abs(E - ref.energy) <= E_TOL * abs(ref.energy)
+    assert np.abs(F - ref.forces).max() <= F_TOL * rms(ref.forces)
     hub.close()
