@@ -1528,18 +1528,12 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_
     if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
 
-// Warp-per-atom range for the force kernel: warp-global index and stride.
-struct WarpPos {
-    int lane, first, stride;
-    __device__ WarpPos()
-        : lane(threadIdx.x & 31),
-          first(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)),
-          stride(gridDim.x * (blockDim.x >> 5)) {}
-};
-
 // ---------------------------------------------------------------------------
-// Forces (gather form, warp per atom), per-atom energy, virial, and the
-// velocity-Verlet tail of the device MD loop.
+// Forces (gather form), per-atom energy, virial, and the velocity-Verlet tail of
+// the device MD loop.  A group of FG lanes per atom (FG = 32: one warp per atom
+// for small systems, where every SM should get atoms; FG = 8: four atoms per warp
+// for large ones -- 3-level group sums instead of 5-level warp sums, the MD tail
+// of four atoms at once, and a grid that fits one wave of resident CTAs).
 //   F_i = sum_{e in out(i)} u_e g_e - sum_{e' in in(i)} u_e' g_e'
 //       = sum_q u_q (g_q + grev_q)            (symmetric list: u_rev(e) = -u_e)
 //   W   = -sum_e g_e r_e ;  W_ab = -sum_e g_e dr_a u_b
@@ -1549,7 +1543,14 @@ struct WarpPos {
 __device__ __forceinline__ void reduce_partials(const double* partial, unsigned nb, double* out,
                                                 double (*s_part)[12]);
 
-template <typename T>
+template <int FG>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = FG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+template <typename T, int FG>
 __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                                                      double* __restrict__ forces,
                                                      double* __restrict__ per_atom,
@@ -1561,28 +1562,34 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
     // every network kernel of this evaluation has completed: re-arm their
     // dynamic atom-schedule counters for the next one
     if (ws.actr && blockIdx.x == 0 && threadIdx.x < kAtomCounters) ws.actr[threadIdx.x] = 0u;
-    const WarpPos wp;
-    const int lane = wp.lane, wc = threadIdx.x >> 5;
+    constexpr int APW = 32 / FG;  // atoms per warp
+    const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+    const int sub = lane % FG, grp = lane / FG;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + wc, nw = gridDim.x * (blockDim.x >> 5);
     double acc[11];
 #pragma unroll
     for (int q = 0; q < 11; ++q) acc[q] = 0.0;
-    for (int i = wp.first; i < gr.n; i += wp.stride) {
+    for (int base = gw * APW; base < gr.n; base += nw * APW) {  // warp-uniform trip count
+        const int i = base + grp;
+        const bool act = i < gr.n;
         // MD state of atom i, loaded early (independent of the edge loads)
         double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0, ei = 0.0;
-        if (lane == 0) ei = ws.e_atom[i];
-        if (mf.mode && lane == 0) {
+        if (act && sub == 0) {
+            ei = ws.e_atom[i];
+            if (mf.mode) {
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                vv[a] = mf.v[3 * i + a];
-                xv[a] = mf.x[3 * i + a];
+                for (int a = 0; a < 3; ++a) {
+                    vv[a] = mf.v[3 * i + a];
+                    xv[a] = mf.x[3 * i + a];
+                }
+                mi = mf.m[i];
             }
-            mi = mf.m[i];
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
-        const int start = gr.row_start[i], cnt = gr.nnei[i];
+        const int start = act ? gr.row_start[i] : 0, cnt = act ? gr.nnei[i] : 0;
         if (ws.gv) {  // DeePMD-style families: vector dE/d(edge_dr) (hmdp_dp.cu)
             //   F_i = sum_q (gv_q - gv_rev(q));  W_ab = -sum_q dr_a gv_b
-            for (int q = lane; q < cnt; q += 32) {
+            for (int q = sub; q < cnt; q += FG) {
                 const int e = start + q;
                 const V4<T> g = ld4c(ws.gv + 4ll * e);
                 const double* d = gr.dr + 3ll * e;
@@ -1603,9 +1610,9 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
 #pragma unroll
                     for (int b = 0; b < 3; ++b) acc[2 + 3 * a + b] -= d[a] * g3[b];
             }
-            if (!gr.sym) {
+            if (!gr.sym && act) {
                 const int is = gr.in_start[i], ic = gr.in_cnt[i];
-                for (int q = lane; q < ic; q += 32) {
+                for (int q = sub; q < ic; q += FG) {
                     const V4<T> m = ld4c(ws.gvrev + 4ll * (is + q));
                     fx -= static_cast<double>(m.x);
                     fy -= static_cast<double>(m.y);
@@ -1613,43 +1620,43 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                 }
             }
         } else {
-        for (int q = lane; q < cnt; q += 32) {
-            const int e = start + q;
-            const T gg = ws.g[e];
-            const T gm = gr.sym ? ws.grev[e] : T(0);
-            T x, y, z;
-            const double* d = gr.dr + 3ll * e;
-            const T r = edge_len<T>(d, x, y, z);
-            const T ux = x / r, uy = y / r, uz = z / r;
-            fx += static_cast<double>(ux * gg) + static_cast<double>(ux * gm);
-            fy += static_cast<double>(uy * gg) + static_cast<double>(uy * gm);
-            fz += static_cast<double>(uz * gg) + static_cast<double>(uz * gm);
-            acc[1] -= static_cast<double>(gg * r);
-            const double gd = static_cast<double>(gg);
-            const double u3[3] = {static_cast<double>(ux), static_cast<double>(uy),
-                                  static_cast<double>(uz)};
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) acc[2 + 3 * a + b] -= gd * d[a] * u3[b];
-        }
-        if (!gr.sym) {  // generic CSR: the pushed g of each in-edge, its own geometry
-            const int is = gr.in_start[i], ic = gr.in_cnt[i];
-            for (int q = lane; q < ic; q += 32) {
-                const int e = gr.in_edge[is + q];
-                const T gg = ws.grev[is + q];
+            for (int q = sub; q < cnt; q += FG) {
+                const int e = start + q;
+                const T gg = ws.g[e];
+                const T gm = gr.sym ? ws.grev[e] : T(0);
                 T x, y, z;
-                const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
-                fx -= static_cast<double>((x / r) * gg);
-                fy -= static_cast<double>((y / r) * gg);
-                fz -= static_cast<double>((z / r) * gg);
+                const double* d = gr.dr + 3ll * e;
+                const T r = edge_len<T>(d, x, y, z);
+                const T ux = x / r, uy = y / r, uz = z / r;
+                fx += static_cast<double>(ux * gg) + static_cast<double>(ux * gm);
+                fy += static_cast<double>(uy * gg) + static_cast<double>(uy * gm);
+                fz += static_cast<double>(uz * gg) + static_cast<double>(uz * gm);
+                acc[1] -= static_cast<double>(gg * r);
+                const double gd = static_cast<double>(gg);
+                const double u3[3] = {static_cast<double>(ux), static_cast<double>(uy),
+                                      static_cast<double>(uz)};
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) acc[2 + 3 * a + b] -= gd * d[a] * u3[b];
+            }
+            if (!gr.sym && act) {  // generic CSR: the pushed g of each in-edge, its own geometry
+                const int is = gr.in_start[i], ic = gr.in_cnt[i];
+                for (int q = sub; q < ic; q += FG) {
+                    const int e = gr.in_edge[is + q];
+                    const T gg = ws.grev[is + q];
+                    T x, y, z;
+                    const T r = edge_len<T>(gr.dr + 3ll * e, x, y, z);
+                    fx -= static_cast<double>((x / r) * gg);
+                    fy -= static_cast<double>((y / r) * gg);
+                    fz -= static_cast<double>((z / r) * gg);
+                }
             }
         }
-        }
-        fx = warp_sum(fx);
-        fy = warp_sum(fy);
-        fz = warp_sum(fz);
-        if (lane == 0) {
+        fx = group_sum<FG>(fx);
+        fy = group_sum<FG>(fy);
+        fz = group_sum<FG>(fz);
+        if (act && sub == 0) {
             const double f3[3] = {fx, fy, fz};
             forces[3 * i] = fx;
             forces[3 * i + 1] = fy;
@@ -1865,10 +1872,32 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
     }
 }
 
+// Lanes per atom of the force kernel: a warp per atom while the atoms do not fill
+// the SMs' resident warps (every SM gets atoms), 8 beyond (HMDP_FORCE_FG pins it).
+int force_fg(int n) {
+    static const int env = [] {
+        const char* e = std::getenv("HMDP_FORCE_FG");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 8 || v == 32) ? v : 0;
+    }();
+    if (env) return env;
+    return n > num_sms() * 16 ? 8 : 32;
+}
 int force_grid(int n) {
-    const int want = (n + kForceCTA / 32 - 1) / (kForceCTA / 32);
+    const int apc = (kForceCTA / 32) * (32 / force_fg(n));  // atoms per CTA
+    const int want = (n + apc - 1) / apc;
     const int cap = num_sms() * 16;
     return want < 1 ? 1 : (want < cap ? want : cap);
+}
+template <typename T>
+static void launch_force_k(const DevGraph& gr, const DevWork<T>& ws, double* forces,
+                           double* per_atom, double* out, cudaStream_t st, const MdFuse& mf) {
+    if (force_fg(gr.n) == 8)
+        launch_pdl(k_force<T, 8>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
+                   per_atom, out, mf);
+    else
+        launch_pdl(k_force<T, 32>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
+                   per_atom, out, mf);
 }
 
 constexpr int kMaxSmem = 200 * 1024;
@@ -2089,8 +2118,7 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
         launches = Net<T, 2>::network(sh, md, gr, ws, rev, st, mk, mf);
     else
         launches = Net<T, 1>::network(sh, md, gr, ws, rev, st, mk, mf);
-    launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
-               per_atom, out, mf);
+    launch_force_k<T>(gr, ws, forces, per_atom, out, st, mf);
     mk("force", st);
     return launches + 1;
 }
@@ -2099,8 +2127,7 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
 template <typename T>
 void launch_force(const DevGraph& gr, const DevWork<T>& ws, double* forces, double* per_atom,
                   double* out, cudaStream_t st, const MdFuse& mf) {
-    launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
-               per_atom, out, mf);
+    launch_force_k<T>(gr, ws, forces, per_atom, out, st, mf);
 }
 template void launch_force<float>(const DevGraph&, const DevWork<float>&, double*, double*,
                                   double*, cudaStream_t, const MdFuse&);
@@ -2133,8 +2160,7 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
                     gr, ws.d + (l & 1) * ws.slots * kH, s_ghost);
             break;
         case 6:
-            launch_pdl(k_force<T>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws,
-                       forces, static_cast<double*>(nullptr), out, MdFuse{});
+            launch_force_k<T>(gr, ws, forces, static_cast<double*>(nullptr), out, st, MdFuse{});
             break;
         default:
             if (gr.alist) {  // global-index DD: the owned-atom list variants
