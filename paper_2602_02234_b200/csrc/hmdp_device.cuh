@@ -10,8 +10,6 @@
 
 namespace hmdp {
 
-constexpr int kAtomCounters = 32;  // >= network kernels per evaluation (2 kMaxMsg + 1)
-
 // Device error word bits (latched with atomicOr, read back after each call).
 enum : unsigned {
     kErrNbrOverflow = 1u << 0,   // an atom has more neighbours than the ELL capacity
@@ -134,12 +132,6 @@ struct DevWork {
     // slot e); the force kernel gathers both when gv != nullptr.
     T* gv;
     T* gvrev;
-    // dynamic atom schedule of the network kernels (hmdp_net.cu AtomIter): one
-    // ticket counter per kernel of an evaluation (kAtomCounters, zero between
-    // evaluations: the force kernel re-arms them); dyn = this launch's counter, -1 =
-    // static grid-stride schedule
-    unsigned* actr;
-    int dyn;
     // 1: the force kernel's last CTA also exports the device error word into out[12]
     // and clears it (hmdp_compute's graph path, outputs in host-mapped memory)
     int export_err;

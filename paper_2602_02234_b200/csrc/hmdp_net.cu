@@ -107,9 +107,15 @@ __device__ unsigned long long g_tprobe[32];
 constexpr int kMaxWarps = 16;  // warps per CTA (network kernels, 1-warp teams)
 // warps per CTA of the 2- and 4-warp-team kernels (one CTA per SM: the register
 // budget per thread is 65536 / (32 x this))
-// (FP64, the parity mode, keeps 16: its registers would not fit more)
-template <typename T, int G>
-constexpr int kCtaWarps = (G == 1 || sizeof(T) > 4) ? kMaxWarps : HMDP_TEAM_CTA_WARPS;
+// (FP64, the parity mode, keeps 16: its registers would not fit more).  WIDE: a
+// second build of the FP32 2-warp-team kernels for 28-warp CTAs (72 registers),
+// taken when 14 teams per SM need fewer rounds of atoms than 10 (net_shape).
+#ifndef HMDP_WIDE_CTA_WARPS
+#define HMDP_WIDE_CTA_WARPS 28
+#endif
+template <typename T, int G, bool WIDE = false>
+constexpr int kCtaWarps = (G == 1 || sizeof(T) > 4) ? kMaxWarps
+                          : (WIDE ? HMDP_WIDE_CTA_WARPS : HMDP_TEAM_CTA_WARPS);
 // Message layers: store every layer's z_e rows (false) or only the LAST layer's and
 // recompute z_e = tanh(W1b b_e + b1 + P^l_j) in the lower layers' backward (true:
 // a tanh + 8 FMAs per edge channel instead of a 128-byte row that spills to HBM at
@@ -146,7 +152,6 @@ struct WarpSmem {
     alignas(16) T ed[32][20];  // edge scalars: (s, s', c0 | -, -, b or b'[8], [b[8]])
     alignas(16) T red[2][64];  // team-sum partials (double-buffered)
     T reds[2];
-    int nxt[2];    // dynamic atom schedule: the team's next atom (lead warp's copy)
     int emir[32];  // staged mirror slots
     int ety[32];   // staged neighbour types
     int enb[32];   // staged neighbour indices (P_j row gathers)
@@ -331,46 +336,6 @@ struct Team {
     __device__ __forceinline__ int local(int cnt) const { return (cnt - w + G - 1) / G; }
 };
 
-// A team's atoms.  Static: grid-stride from tm.first (domain decomposition and
-// atom lists).  Dynamic (ws.dyn >= 0, single-domain network): every team starts
-// on its static first atom (no fetch on the critical path), then takes tickets
-// from the kernel's counter ws.actr[dyn] -- atom tm.stride + ticket -- fetched by
-// the team's lead lane one atom ahead, so the atomic's latency hides under the
-// current atom.  Teams keep taking atoms until the tickets pass the end, so the
-// grid is sized to the resident CTAs and the per-SM load evens out (28 atoms per
-// SM at 2PTC over 8 teams would otherwise leave 4 atoms on some teams and 3 on
-// others).  Which team runs an atom does not change its result.  The force
-// kernel re-arms the counters.
-template <int G, bool DYN>
-struct AtomIter {
-    unsigned* ctr;  // DYN: this launch's ticket counter
-    int pre = 0;
-    int pb = 0;
-    template <typename T>
-    __device__ explicit AtomIter(const DevWork<T>& ws) : ctr(DYN ? ws.actr + ws.dyn : nullptr) {}
-    __device__ __forceinline__ int first(const Team<G>& tm) const { return tm.first; }
-    // at the top of the atom body: the ticket of the atom after this one
-    // (none when the teams' first atoms already cover all n_run)
-    __device__ __forceinline__ void prefetch(const Team<G>& tm, int n_run) {
-        if (DYN && tm.w == 0 && tm.lane == 0)
-            pre = tm.stride >= n_run ? n_run : tm.stride + static_cast<int>(atomicAdd(ctr, 1u));
-    }
-    template <typename T>
-    __device__ __forceinline__ int next(int k, Team<G>& tm, WarpSmem<T>& sm) {
-        if constexpr (!DYN) return k + tm.stride;
-        if constexpr (G == 1) {
-            return __shfl_sync(FULL_MASK, pre, 0);
-        } else {
-            WarpSmem<T>* lead = &sm - tm.w;  // double-buffered: one barrier per atom
-            if (tm.w == 0 && tm.lane == 0) lead->nxt[pb] = pre;
-            tm.sync();
-            const int r = lead->nxt[pb];
-            pb ^= 1;
-            return r;
-        }
-    }
-};
-
 // Team mat-vec: sum_{k<NIN} W[row][k] x[k] with the inputs split over the
 // team's warps (warp w: inputs [w NIN/G, (w+1) NIN/G)) and the partials summed
 // in a fixed order — one copy of the weight traffic per team, not per warp.
@@ -478,8 +443,8 @@ __device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2,
 // ---------------------------------------------------------------------------
 // DESC_ONLY: the edge work and the descriptor only; the embedding MLP and the P^0
 // projection then run as one tcgen05 layer chain over all atoms (hmdp_tc.cu).
-template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false, bool DYN = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
+template <typename T, int G, bool FUSE_FIT, bool LIST = false, bool DESC_ONLY = false, bool WIDE = false>
+__global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_embed(DevModel<T> md, DevGraph gr,
                                                              DevWork<T> ws, int* __restrict__ rev,
                                                              MdFuse mf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -517,9 +482,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed(
     auto sb = sm.ed;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    AtomIter<G, DYN> at(ws);
-    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
-        at.prefetch(tm, n_run);
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int i = LIST ? gr.alist[k_at] : k_at;
         const int start = gr.row_start[i] + tm.w, cnt = gr.nnei[i];
         const int mloc = tm.local(cnt);
@@ -1039,8 +1002,8 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
 // Message layer l forward; LAST fuses the fitting net and the top layer's
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
-template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool DYN = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
+template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool WIDE = false>
+__global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1089,9 +1052,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_fw
     T* Z = ws.z + (kRecomputeZ && PULL == 0 ? 0 : static_cast<long long>(l) * ws.slots * kH);
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    AtomIter<G, DYN> at(ws);
-    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
-        at.prefetch(tm, n_run);
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T hi = ws.h[(static_cast<long long>(l) * n + i) * kH + lane];
@@ -1235,7 +1196,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_fw
 }
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
-template <typename T, int G, bool LIST = false, bool DYN = false>
+template <typename T, int G, bool LIST = false>
 __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1266,9 +1227,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bw
                               : ws.z + static_cast<long long>(l) * ws.slots * kH;
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    AtomIter<G, DYN> at(ws);
-    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
-        at.prefetch(tm, n_run);
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         // one round trip: own adjoint, update activations, the pushed adjoint rows
@@ -1304,7 +1263,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bw
 }
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
-template <typename T, int G, bool LIST = false, bool DYN = false>
+template <typename T, int G, bool LIST = false>
 __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1323,9 +1282,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_
     pdl_wait();
     // LIST (global-index DD): the atoms alist[0 .. *alist_n); else [0, n_active)
     const int n_run = LIST ? *gr.alist_n : gr.n_active;
-    AtomIter<G, DYN> at(ws);
-    for (int k_at = at.first(tm); k_at < n_run; k_at = at.next(k_at, tm, sm)) {
-        at.prefetch(tm, n_run);
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int i = LIST ? gr.alist[k_at] : k_at;
         AtomRow<G> ar(gr, i, tm);
         const T own = ws.dhown[static_cast<long long>(i) * kH + lane];
@@ -1397,8 +1354,8 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_
 // Pull form, lower layers (l < M-1): the sender-side backward of layer l+1's
 // messages (gathering the receivers' v^{l+1} rows), dE/dh^{l+1}_k, then layer l's
 // update backward (v^l_k, c0^l_k for the next kernel).
-template <typename T, int G, int PULL, bool DYN = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
+template <typename T, int G, int PULL, bool WIDE = false>
+__global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
                                                                     DevGraph gr, DevWork<T> ws,
                                                                     int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1426,9 +1383,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bw
     const T* V = ws.vrow + static_cast<long long>((l + 1) & 1) * n * kH;
     const T* C0 = ws.vc0 + static_cast<long long>((l + 1) & 1) * n;
     const bool first_g = l == md.n_msg - 2;
-    AtomIter<G, DYN> at(ws);
-    for (int k = at.first(tm); k < gr.n_active; k = at.next(k, tm, sm)) {
-        at.prefetch(tm, gr.n_active);
+    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
         AtomRow<G> ar(gr, k, tm);
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T zu = ws.uz1[(static_cast<long long>(l) * n + k) * kH + lane];
@@ -1454,8 +1409,8 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bw
 // Pull form, embedding backward: the sender-side backward of layer 0's messages,
 // dE/dh^0_k, the embedding backward and the descriptor adjoint; pushes the final
 // g to the mirrors for the force gather.
-template <typename T, int G, int PULL, bool DYN = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
+template <typename T, int G, int PULL, bool WIDE = false>
+__global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
                                                                       DevGraph gr,
                                                                       DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1479,9 +1434,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_
     pdl_wait();
     const int n = gr.n;
     const bool first_g = md.n_msg == 1;
-    AtomIter<G, DYN> at(ws);
-    for (int k = at.first(tm); k < gr.n_active; k = at.next(k, tm, sm)) {
-        at.prefetch(tm, gr.n_active);
+    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
         AtomRow<G> ar(gr, k, tm);
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(k) * kH + lane];
@@ -1559,9 +1512,6 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
     __shared__ bool s_last;
     pdl_launch_dependents();
     pdl_wait();
-    // every network kernel of this evaluation has completed: re-arm their
-    // dynamic atom-schedule counters for the next one
-    if (ws.actr && blockIdx.x == 0 && threadIdx.x < kAtomCounters) ws.actr[threadIdx.x] = 0u;
     constexpr int APW = 32 / FG;  // atoms per warp
     const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
     const int sub = lane % FG, grp = lane / FG;
@@ -1798,8 +1748,15 @@ static int staged_elems(Phase p) {
 // two CTAs per SM.
 struct NetShape {
     int G, warps, grid;
-    int dyn = 0;  // 1: dynamic atom schedule (grid capped at the resident CTAs)
+    int wide = 0;  // 1: the 28-warp-CTA (WIDE) build of the 2-warp-team kernels
 };
+static bool wide_on() {  // HMDP_WIDE=0 keeps the 20-warp build (A/B experiments)
+    static const bool v = [] {
+        const char* e = std::getenv("HMDP_WIDE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+}
 int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments)
     static const int v = [] {
         const char* e = std::getenv("HMDP_TEAM");
@@ -1815,23 +1772,38 @@ int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments
 // (1UBQ 24.2k -> 28.9k; 3LZM and 2PTC prefer 1 warp); 1 warp beyond.
 // FP64 (the oracle-of-record mode) caps a CTA at 8 warps: its per-warp scratch and
 // staged matrices are twice as large and 16 warps would not fit in shared memory.
-static NetShape net_shape(int n, int n_msg, int elem_bytes) {
+static NetShape net_shape(int n, int n_msg, int elem_bytes, bool allow_wide = false) {
     const int sms = num_sms();
     const int two_upto = (n_msg > 0 ? 40 : 10) * sms;
     int G = (4 * n <= kMaxWarps * sms) ? 4 : (n <= two_upto ? 2 : 1);
     if (team_override()) G = team_override();
     const int max_warps = elem_bytes > 4 ? kMaxWarps / 2 : (G == 1 ? kCtaWarps<float, 1> : kCtaWarps<float, 2>);
-    const int max_teams = max_warps / G;
-    int teams = (n + sms - 1) / sms;
+    int max_teams = max_warps / G;
+    // Every team takes whole atoms, so a kernel runs ceil(n / teams) rounds of them:
+    // take the fewest teams per CTA that keep the fewest rounds (more registers and
+    // issue slots per warp at the same round count; 3LZM: 9 teams, 2 rounds).  For
+    // FP32 2-warp teams, the 28-warp build (WIDE, 14 teams) is taken when it needs
+    // fewer rounds than the 20-warp one (2PTC: 2 rounds instead of 3).
+    bool wide = false;
+    auto rounds = [&](int t) { return (n + sms * t - 1) / (sms * t); };
+    if (allow_wide && G == 2 && elem_bytes == 4 && n_msg > 0 && wide_on()) {
+        const int tw = kCtaWarps<float, 2, true> / 2;
+        if (rounds(tw) < rounds(max_teams)) {
+            wide = true;
+            max_teams = tw;
+        }
+    }
+    const int r = rounds(max_teams);
+    int teams = (n + sms * r - 1) / (sms * r);
     teams = teams < 1 ? 1 : (teams > max_teams ? max_teams : teams);
     if (G == 1 && teams < 2) teams = 2;
     int grid = (n + teams - 1) / teams;
     if (grid > 2 * sms) grid = 2 * sms;
-    return {G, teams * G, grid < 1 ? 1 : grid, 0};
+    return {G, teams * G, grid < 1 ? 1 : grid, wide ? 1 : 0};
 }
 
 // CTAs of a kernel resident per SM at a given block / shared-memory size (cached;
-// the dynamic atom schedule launches exactly that many per SM).
+// launches are capped at one wave of them).
 static int resident_ctas(const void* fn, int threads, size_t smem) {
     static std::mutex mu;
     static std::map<std::tuple<const void*, int, size_t>, int> cache;
@@ -1853,9 +1825,8 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
                        Args... args) {
     const size_t smem = static_cast<size_t>(staged_elems<T>(p)) * sizeof(T) + 16 +
                         static_cast<size_t>(sh.warps) * sizeof(WarpSmem<T>);
-    // at most one wave of resident CTAs: the teams grid-stride (or, dynamic
-    // schedule, take tickets) over the remaining atoms instead of a partial second
-    // wave of CTAs doubling the kernel time
+    // at most one wave of resident CTAs: the teams grid-stride over the remaining
+    // atoms instead of a partial second wave of CTAs doubling the kernel time
     int grid = sh.grid;
     const int per_sm = resident_ctas(reinterpret_cast<const void*>(kernel), 32 * sh.warps, smem);
     const int g = per_sm * num_sms();
@@ -1902,17 +1873,6 @@ static void launch_force_k(const DevGraph& gr, const DevWork<T>& ws, double* for
 
 constexpr int kMaxSmem = 200 * 1024;
 
-// Dynamic atom schedule (AtomIter) for the single-domain network; HMDP_DYN=0|1
-// pins it (A/B experiments).
-constexpr bool kDynDefault = false;
-static bool dyn_sched_on() {
-    static const int env = [] {
-        const char* e = std::getenv("HMDP_DYN");
-        return e ? std::atoi(e) : -1;
-    }();
-    return env >= 0 ? env != 0 : kDynDefault;
-}
-
 // Message backward form (see pull_edges): the pull form needs the symmetric
 // periodic graph with every atom running the network (no halo ghosts, no global
 // list, no domain-decomposition rows); everything else runs the push form.
@@ -1938,23 +1898,25 @@ static int pull_mode(const DevGraph& gr, const DevWork<T>& ws, int n_msg) {
     return zbytes > kZRowsL2Budget ? 2 : 1;
 }
 
-// The network phases for one element type and team size.
-template <typename T, int G, bool LIST = false>
+// The network phases for one element type and team size (WIDE: the 28-warp-CTA
+// build of the FP32 2-warp-team kernels, single-domain periodic path only).
+template <typename T, int G, bool LIST = false, bool WIDE = false>
 struct Net {
-    template <int PULL, bool DYN>
-    static cudaError_t configure_pd() {
+    static_assert(!WIDE || (!LIST && G == 2 && sizeof(T) == 4), "WIDE: FP32 2-warp teams only");
+    template <int PULL>
+    static cudaError_t configure_p() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
-        for (cudaError_t r : {cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST, PULL, DYN>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST, PULL, DYN>, a, kMaxSmem)})
+        for (cudaError_t r : {cudaFuncSetAttribute(k_msg_fwd<T, G, true, LIST, PULL, WIDE>, a, kMaxSmem),
+                              cudaFuncSetAttribute(k_msg_fwd<T, G, false, LIST, PULL, WIDE>, a, kMaxSmem)})
             if (r != cudaSuccess) e = r;
         if constexpr (PULL == 0) {
-            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd<T, G, LIST, DYN>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_embed_bwd<T, G, LIST, DYN>, a, kMaxSmem)})
+            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd<T, G, LIST>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd<T, G, LIST>, a, kMaxSmem)})
                 if (r != cudaSuccess) e = r;
         } else {
-            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd_pull<T, G, PULL, DYN>, a, kMaxSmem),
-                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, PULL, DYN>, a, kMaxSmem)})
+            for (cudaError_t r : {cudaFuncSetAttribute(k_msg_bwd_pull<T, G, PULL, WIDE>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, PULL, WIDE>, a, kMaxSmem)})
                 if (r != cudaSuccess) e = r;
         }
         return e;
@@ -1962,31 +1924,33 @@ struct Net {
     static cudaError_t configure() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
-        for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, LIST>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_embed<T, G, false, LIST>, a, kMaxSmem),
-                              cudaFuncSetAttribute(k_embed<T, G, false, LIST, true>, a, kMaxSmem),
-                              configure_pd<0, false>()})
-            if (r != cudaSuccess) e = r;
-        if constexpr (!LIST) {
+        if constexpr (WIDE) {
             for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, false, false, true>, a, kMaxSmem),
                                   cudaFuncSetAttribute(k_embed<T, G, false, false, false, true>, a, kMaxSmem),
-                                  configure_pd<0, true>(), configure_pd<1, false>(),
-                                  configure_pd<1, true>(), configure_pd<2, false>(),
-                                  configure_pd<2, true>()})
+                                  configure_p<1>(), configure_p<2>()})
                 if (r != cudaSuccess) e = r;
+            return e;
+        } else {
+            for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, LIST>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed<T, G, false, LIST>, a, kMaxSmem),
+                                  cudaFuncSetAttribute(k_embed<T, G, false, LIST, true>, a, kMaxSmem),
+                                  configure_p<0>()})
+                if (r != cudaSuccess) e = r;
+            if constexpr (!LIST)
+                for (cudaError_t r : {configure_p<1>(), configure_p<2>()})
+                    if (r != cudaSuccess) e = r;
+            return e;
         }
-        return e;
     }
     // returns the kernels launched (2 with the tcgen05 embedding chain)
-    template <bool DYN = false>
     static int embed(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                      const DevWork<T>& ws, int* rev, const MdFuse& mf, cudaStream_t st) {
         if (md.n_msg == 0) {
-            launch_net<T>(k_embed<T, G, true, LIST, false, DYN>, Phase::EmbedFit, sh, st, md, gr, ws,
-                          rev, mf);
+            launch_net<T>(k_embed<T, G, true, LIST, false, WIDE>, Phase::EmbedFit, sh, st, md, gr,
+                          ws, rev, mf);
             return 1;
         }
-        if constexpr (sizeof(T) == 4 && !LIST && !DYN) {
+        if constexpr (sizeof(T) == 4 && !LIST && !WIDE) {
             if (tc_embed_on(gr.n_active) && !ws.p_atom) {
                 launch_net<T>(k_embed<T, G, false, LIST, true>, Phase::Embed, sh, st, md, gr, ws,
                               rev, mf);
@@ -1999,63 +1963,54 @@ struct Net {
                 return 2;
             }
         }
-        launch_net<T>(k_embed<T, G, false, LIST, false, DYN>, Phase::Embed, sh, st, md, gr, ws, rev,
+        launch_net<T>(k_embed<T, G, false, LIST, false, WIDE>, Phase::Embed, sh, st, md, gr, ws, rev,
                       mf);
         return 1;
     }
-    template <int PULL, bool DYN = false>
+    template <int PULL>
     static void msg_fwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                         const DevWork<T>& ws, int l, cudaStream_t st) {
         if (l == md.n_msg - 1)
-            launch_net<T>(k_msg_fwd<T, G, true, LIST, PULL, DYN>, Phase::MsgFwdLast, sh, st, md, gr,
+            launch_net<T>(k_msg_fwd<T, G, true, LIST, PULL, WIDE>, Phase::MsgFwdLast, sh, st, md, gr,
                           ws, l);
         else
-            launch_net<T>(k_msg_fwd<T, G, false, LIST, PULL, DYN>, Phase::MsgFwd, sh, st, md, gr, ws,
+            launch_net<T>(k_msg_fwd<T, G, false, LIST, PULL, WIDE>, Phase::MsgFwd, sh, st, md, gr, ws,
                           l);
     }
-    template <int PULL, bool DYN = false>
+    template <int PULL>
     static void msg_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                         const DevWork<T>& ws, int l, cudaStream_t st) {
         if constexpr (PULL == 0)
-            launch_net<T>(k_msg_bwd<T, G, LIST, DYN>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_bwd<T, G, LIST>, Phase::MsgBwd, sh, st, md, gr, ws, l);
         else
-            launch_net<T>(k_msg_bwd_pull<T, G, PULL, DYN>, Phase::MsgBwd, sh, st, md, gr, ws, l);
+            launch_net<T>(k_msg_bwd_pull<T, G, PULL, WIDE>, Phase::MsgBwd, sh, st, md, gr, ws, l);
     }
-    template <int PULL, bool DYN = false>
+    template <int PULL>
     static void embed_bwd(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                           const DevWork<T>& ws, cudaStream_t st) {
         if constexpr (PULL == 0)
-            launch_net<T>(k_embed_bwd<T, G, LIST, DYN>, Phase::EmbedBwd, sh, st, md, gr, ws);
+            launch_net<T>(k_embed_bwd<T, G, LIST>, Phase::EmbedBwd, sh, st, md, gr, ws);
         else
-            launch_net<T>(k_embed_bwd_pull<T, G, PULL, DYN>, Phase::EmbedBwd, sh, st, md, gr, ws);
+            launch_net<T>(k_embed_bwd_pull<T, G, PULL, WIDE>, Phase::EmbedBwd, sh, st, md, gr, ws);
     }
-    // One evaluation's network kernels.  DYN: launch j takes its atoms from
-    // counter j (AtomIter; the force kernel re-arms them) on a grid of resident CTAs.
-    template <int PULL, bool DYN>
-    static int network_pd(const NetShape& sh0, const DevModel<T>& md, const DevGraph& gr,
-                          const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
-                          const MdFuse& mf) {
+    // One evaluation's network kernels.
+    template <int PULL>
+    static int network_p(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
+                         const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
+                         const MdFuse& mf) {
         const int M = md.n_msg;
-        NetShape sh = sh0;
-        sh.dyn = DYN ? 1 : 0;
-        int slot = 0;
-        auto w_at = [&](int j) {
-            DevWork<T> w = ws;
-            w.dyn = DYN ? j : -1;
-            return w;
-        };
-        const int ne = embed<DYN>(sh, md, gr, w_at(slot++), rev, mf, st);
+        const int ne = embed(sh, md, gr, ws, rev, mf, st);
         mk(M == 0 ? "embed_fit" : "embed", st);
         if (M == 0) return 1;
         for (int l = 0; l < M; ++l) {
-            msg_fwd<PULL, DYN>(sh, md, gr, w_at(slot++), l, st);
+            msg_fwd<PULL>(sh, md, gr, ws, l, st);
             mk(l == M - 1 ? "msg_fwd_last" : "msg_fwd", st);
         }
         for (int l = M - 2; l >= 0; --l) {
-            msg_bwd<PULL, DYN>(sh, md, gr, w_at(slot++), l, st);
+            msg_bwd<PULL>(sh, md, gr, ws, l, st);
             mk("msg_bwd", st);
         }
-        embed_bwd<PULL, DYN>(sh, md, gr, w_at(slot++), st);
+        embed_bwd<PULL>(sh, md, gr, ws, st);
         mk("embed_bwd", st);
         return ne + 1 + M + (M - 1);
     }
@@ -2063,22 +2018,14 @@ struct Net {
                        const DevWork<T>& ws, int* rev, cudaStream_t st, const Marker& mk,
                        const MdFuse& mf) {
         if constexpr (!LIST) {
-            // only when the static grid's teams do not already take one atom each
-            // (measured: DPA3 2PTC +3 %, 1UBQ +3-5 %; 1YRF, one atom per team, -2 %);
-            // the opt-in tcgen05 embedding chain runs on the static schedule
-            const bool dyn = dyn_sched_on() && ws.actr && !gr.alist &&
-                             gr.n_active > std::min(sh.grid, num_sms()) * (sh.warps / G) &&
-                             !(sizeof(T) == 4 && tc_embed_on(gr.n_active) && !ws.p_atom);
-            switch (pull_mode(gr, ws, md.n_msg) * 2 + (dyn ? 1 : 0)) {
-                case 1: return network_pd<0, true>(sh, md, gr, ws, rev, st, mk, mf);
-                case 2: return network_pd<1, false>(sh, md, gr, ws, rev, st, mk, mf);
-                case 3: return network_pd<1, true>(sh, md, gr, ws, rev, st, mk, mf);
-                case 4: return network_pd<2, false>(sh, md, gr, ws, rev, st, mk, mf);
-                case 5: return network_pd<2, true>(sh, md, gr, ws, rev, st, mk, mf);
-                default: break;
-            }
+            const int pull = pull_mode(gr, ws, md.n_msg);
+            if (pull == 1) return network_p<1>(sh, md, gr, ws, rev, st, mk, mf);
+            if (pull == 2) return network_p<2>(sh, md, gr, ws, rev, st, mk, mf);
         }
-        return network_pd<0, false>(sh, md, gr, ws, rev, st, mk, mf);
+        if constexpr (WIDE)
+            return -1;  // never: the WIDE build is chosen only on the pull-form path
+        else
+            return network_p<0>(sh, md, gr, ws, rev, st, mk, mf);
     }
     static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                          const DevWork<T>& ws, int phase, int l, cudaStream_t st, int* rev) {
@@ -2097,6 +2044,7 @@ struct Net {
 cudaError_t net_configure() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {Net<float, 1>::configure(), Net<float, 2>::configure(),
+                          Net<float, 2, false, true>::configure(),
                           Net<float, 4>::configure(), Net<double, 1>::configure(),
                           Net<double, 2>::configure(), Net<double, 4>::configure(),
                           Net<float, 1, true>::configure(), Net<float, 2, true>::configure(),
@@ -2110,8 +2058,17 @@ template <typename T>
 int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws,
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
-    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)));
+    // the WIDE build exists for the pull-form (single-domain periodic) path only
+    const bool wide_ok = sizeof(T) == 4 && !gr.alist && pull_mode(gr, ws, md.n_msg) != 0;
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), wide_ok);
     int launches;
+    if constexpr (sizeof(T) == 4)
+        if (sh.G == 2 && sh.wide) {
+            launches = Net<T, 2, false, true>::network(sh, md, gr, ws, rev, st, mk, mf);
+            launch_force_k<T>(gr, ws, forces, per_atom, out, st, mf);
+            mk("force", st);
+            return launches + 1;
+        }
     if (sh.G == 4)
         launches = Net<T, 4>::network(sh, md, gr, ws, rev, st, mk, mf);
     else if (sh.G == 2)
