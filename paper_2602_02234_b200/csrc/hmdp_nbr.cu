@@ -10,6 +10,8 @@
 //                       + CSR edge_dr                src/nn/inference.cpp:474-485
 //   k_descriptors_f64   descriptors()                src/nn/inference.cpp:430-447
 //   k_vv_kick_drift_bin velocity_verlet_step         src/integrators.cpp:12-47
+#include <cstdlib>
+
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -248,12 +250,37 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
     // 4 warps per atom up to 4 atoms per SM, 2 up to ~20 per SM, then 1
     int G = (4 * n <= 16 * sms) ? 4 : (n <= 20 * sms ? 2 : 1);
     if (team_override()) G = team_override();
-    // warps per CTA: enough teams per CTA that the atoms fill every SM
-    int teams = (n + sms - 1) / sms;
-    teams = teams < 1 ? 1 : (teams > 16 / G ? 16 / G : teams);
+    static const int g_env = [] {
+        const char* e = std::getenv("HMDP_SEARCH_G");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 1 || v == 2 || v == 4) ? v : 0;
+    }();
+    if (g_env) G = g_env;
+    // The kernel holds 32 warps per SM (64 registers): 2 CTAs of up to 16 warps.
+    // Atoms per SM m = ceil(n / sms); one round when m teams fit on the SM, and the
+    // CTAs are shaped so that every SM carries the same number of atoms (2PTC: two
+    // 14-warp CTAs per SM, 28 atoms each, instead of 258 16-warp CTAs that left 38 SMs
+    // half loaded); never more CTAs than one resident wave (3LZM had 331: a partial
+    // second wave), the teams grid-stride over the rest.
+    const int m = (n + sms - 1) / sms;
+    const int per_sm_teams = 32 / G;
+    int teams;
+    if (m <= 16 / G) {
+        teams = m < 1 ? 1 : m;  // one CTA per SM
+    } else {
+        const int round_teams = m <= per_sm_teams ? m : per_sm_teams;
+        teams = (round_teams + 1) / 2;  // two CTAs per SM
+        teams = teams > 16 / G ? 16 / G : teams;
+    }
+    static const int t_env = [] {
+        const char* e = std::getenv("HMDP_SEARCH_T");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (t_env > 0 && t_env * G <= 16) teams = t_env;
     const int threads = 32 * G * teams;
     int grid = (n + teams - 1) / teams;
-    grid = grid < 8 * sms ? grid : 8 * sms;
+    const int resident = sms * (32 / (G * teams));  // 64 registers: 32 warps per SM
+    grid = grid < resident ? grid : resident;
     const size_t smem = static_cast<size_t>(G * teams) * sizeof(NbrSmem);
     auto args = [&](auto kernel) {
         launch_pdl(kernel, dim3(grid > 0 ? grid : 1), dim3(threads), smem, st, n, pos, cg,

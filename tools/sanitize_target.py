@@ -57,3 +57,30 @@ hm = HybridMD(P.Context(models[1], max_atoms=n), ff, plan.atoms, sh.positions, s
               steps_per_graph=2)
 hm.run(4)
 print("hybrid", hm.state()[3])
+
+# round 2: the pull-form message backward at paper size (4114 atoms: 2-warp teams,
+# the 28-warp-CTA build, stored z rows) and beyond the z-row budget (32 912 atoms:
+# 1-warp teams, z recomputed); the halo-exchange and gather-to-root DD engines
+big = P.generate_synthetic_system(4114)
+ctxb = P.Context(models[1], max_atoms=4114)
+for _ in range(3):  # direct path, capture, replay
+    ob = ctxb.compute(big.positions, big.types, big.box, P.Precision.fp32)
+print("2PTC", ob.energy, flush=True)
+rep = P.replicate(big, (2, 2, 2))
+orp = P.Context(models[1], max_atoms=rep.n_atoms).compute(rep.positions, rep.types, rep.box,
+                                                          P.Precision.fp32)
+print("2PTC x8", orp.energy, flush=True)
+from paper_2602_02234_b200 import dd  # noqa: E402
+
+for strategy in ("halo", "gather"):
+    hub = dd.Hub(2)
+    he = [dd.HaloDD(P.Context(models[1], max_atoms=582), 582, sh.types, sh.box, (2, 1, 1), r,
+                    P.Precision.fp32, masses=sh.masses, strategy=strategy) for r in range(2)]
+    for e in he:
+        e.attach_hub(hub.handle)
+        e.load(sh.positions, sh.velocities)
+    dd.run_hub(he, "eval")
+    dd.run_hub(he, "open", 0.001)
+    dd.run_hub(he, "md", 0.001, steps=2)
+    print(strategy, he[0].energy_virial()[0], flush=True)
+    hub.close()
