@@ -246,9 +246,10 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
                        unsigned* err, cudaStream_t st, const int* alist, const int* alist_n) {
     const int sms = num_sms();
-    // team size by system size (measured with the network kernels):
-    // 4 warps per atom up to 4 atoms per SM, 2 up to ~20 per SM, then 1
-    int G = (4 * n <= 16 * sms) ? 4 : (n <= 20 * sms ? 2 : 1);
+    // team size by system size: 4 warps per atom up to 4 atoms per SM, 2 up to 16 per
+    // SM (one round of 2-warp teams), then 1 (measured: 3LZM, 18 atoms per SM, with 1
+    // instead of 2: DPA3 +2.2 %, DPA2 +6.7 %; 1UBQ with 1: -7 %)
+    int G = (4 * n <= 16 * sms) ? 4 : (n <= 16 * sms ? 2 : 1);
     if (team_override()) G = team_override();
     static const int g_env = [] {
         const char* e = std::getenv("HMDP_SEARCH_G");
