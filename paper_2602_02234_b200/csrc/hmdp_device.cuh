@@ -132,6 +132,9 @@ struct DevWork {
     // slot e); the force kernel gathers both when gv != nullptr.
     T* gv;
     T* gvrev;
+    // 1: the force kernel gathers the mirror g of each slot as g[inv_pos[q]] instead of
+    // reading the pushed grev[q] (the fused depth-1 network on the periodic path)
+    int gather_mirror_g;
     // 1: the force kernel's last CTA also exports the device error word into out[12]
     // and clears it (hmdp_compute's graph path, outputs in host-mapped memory)
     int export_err;

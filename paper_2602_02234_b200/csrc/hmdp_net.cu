@@ -517,18 +517,23 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 sm.ety[lane] = gr.ety[e];
             }
             if (rev) {
-                // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Lane l reads
-                // entry l of each neighbour's list (one memory latency per 8 edges);
-                // a ballot finds i.
-                const int rs_l = lane < m ? gr.row_start[j] : 0;
-                const int nn_l = lane < m ? gr.nnei[j] : 0;
+                // rev(e) = slot of i in nbr(j) (symmetric, sorted list).  Each pair is
+                // searched once, by its lower atom: the edges with j > i (a suffix of
+                // the warp's lanes, the list being sorted) find i in j's list and set
+                // both rev(e) and rev(rev(e)) = e; the others are set by their j.  Lane
+                // l reads entry l of each neighbour's list (one memory latency per 8
+                // edges); a ballot finds i.  rev is read only by later kernels.
+                const bool up = lane < m && j > i;
+                const int lo_lane = __popc(__ballot_sync(FULL_MASK, lane < m && !up));
+                const int rs_l = up ? gr.row_start[j] : 0;
+                const int nn_l = up ? gr.nnei[j] : 0;
                 int found = -1;
-                for (int q0 = 0; q0 < m; q0 += 8) {
+                for (int q0 = lo_lane; q0 < m; q0 += 8) {
                     int val[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        const int rsq = __shfl_sync(FULL_MASK, rs_l, q0 + u);
-                        const int nnq = __shfl_sync(FULL_MASK, nn_l, q0 + u);
+                        const int rsq = __shfl_sync(FULL_MASK, rs_l, (q0 + u) & 31);
+                        const int nnq = __shfl_sync(FULL_MASK, nn_l, (q0 + u) & 31);
                         val[u] = (q0 + u < m && lane < nnq) ? gr.nbr[rsq + lane] : -1;
                     }
 #pragma unroll
@@ -537,7 +542,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                         if (lane == q0 + u && bal) found = rs_l + __ffs(bal) - 1;
                     }
                 }
-                if (lane < m) {
+                if (up) {
                     if (found < 0 && nn_l > 32) {
                         int lo = rs_l, hi = rs_l + nn_l - 1;
                         while (lo <= hi) {
@@ -553,6 +558,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                     }
                     rev[e] = found;
                     if (found < 0) atomicOr(ws.err, kErrAsymmetric);
+                    else rev[found] = e;
                 }
             }
             __syncwarp();
@@ -610,7 +616,10 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 acc += dv[6] * d1.z;
                 acc += dv[7] * d1.w;
                 ws.g[e] = acc;
-                ws.grev[gr.inv_pos[e]] = acc;  // mirror for the force gather
+                // mirror for the force gather; on the periodic path the mirror slots are
+                // still being written by the pairs' lower atoms, so the force kernel
+                // gathers g[rev(q)] itself (DevWork::gather_mirror_g)
+                if (!rev) ws.grev[gr.inv_pos[e]] = acc;
             }
         } else {
             // P^0 = W1h^(0) h^0, one row per atom (L2-resident; gathered by the
@@ -1573,7 +1582,8 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
             for (int q = sub; q < cnt; q += FG) {
                 const int e = start + q;
                 const T gg = ws.g[e];
-                const T gm = gr.sym ? ws.grev[e] : T(0);
+                const T gm = gr.sym ? (ws.gather_mirror_g ? ws.g[gr.inv_pos[e]] : ws.grev[e])
+                                    : T(0);
                 T x, y, z;
                 const double* d = gr.dr + 3ll * e;
                 const T r = edge_len<T>(d, x, y, z);
@@ -2075,7 +2085,9 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
         launches = Net<T, 2>::network(sh, md, gr, ws, rev, st, mk, mf);
     else
         launches = Net<T, 1>::network(sh, md, gr, ws, rev, st, mk, mf);
-    launch_force_k<T>(gr, ws, forces, per_atom, out, st, mf);
+    DevWork<T> wf = ws;
+    wf.gather_mirror_g = (md.n_msg == 0 && rev) ? 1 : 0;  // k_embed<FUSE_FIT> pushed no mirrors
+    launch_force_k<T>(gr, wf, forces, per_atom, out, st, mf);
     mk("force", st);
     return launches + 1;
 }
