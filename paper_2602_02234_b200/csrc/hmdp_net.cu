@@ -116,6 +116,10 @@ constexpr int kMaxWarps = 16;  // warps per CTA (network kernels, 1-warp teams)
 template <typename T, int G, bool WIDE = false>
 constexpr int kCtaWarps = (G == 1 || sizeof(T) > 4) ? kMaxWarps
                           : (WIDE ? HMDP_WIDE_CTA_WARPS : HMDP_TEAM_CTA_WARPS);
+// The push-form message kernels (domain decomposition, general CSR graphs) keep
+// 16-warp CTAs: their backward holds the pushed-row batches and spills at 96
+// registers (k_msg_bwd 400 B); net_shape(push) sizes their launches.
+constexpr int kPushWarps = kMaxWarps;
 // Message layers: store every layer's z_e rows (false) or only the LAST layer's and
 // recompute z_e = tanh(W1b b_e + b1 + P^l_j) in the lower layers' backward (true:
 // a tanh + 8 FMAs per edge channel instead of a 128-byte row that spills to HBM at
@@ -1012,7 +1016,7 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
 // backward (all atom-local).
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool WIDE = false>
-__global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1206,7 +1210,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
 
 // Message layer l < M-1 backward: gather dE/dh^{l+1}, then the layer body.
 template <typename T, int G, bool LIST = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -1273,7 +1277,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_msg_bw
 
 // Embedding backward + descriptor adjoint (depth > 1); pushes g to the mirrors.
 template <typename T, int G, bool LIST = false>
-__global__ __launch_bounds__(kCtaWarps<T, G> * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
+__global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(DevModel<T> md, DevGraph gr,
                                                                  DevWork<T> ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
@@ -1782,12 +1786,14 @@ int team_override() {  // HMDP_TEAM=1|2|4 pins the team size (tuning experiments
 // (1UBQ 24.2k -> 28.9k; 3LZM and 2PTC prefer 1 warp); 1 warp beyond.
 // FP64 (the oracle-of-record mode) caps a CTA at 8 warps: its per-warp scratch and
 // staged matrices are twice as large and 16 warps would not fit in shared memory.
-static NetShape net_shape(int n, int n_msg, int elem_bytes, bool allow_wide = false) {
+static NetShape net_shape(int n, int n_msg, int elem_bytes, bool allow_wide = false,
+                          bool push = false) {
     const int sms = num_sms();
     const int two_upto = (n_msg > 0 ? 40 : 10) * sms;
     int G = (4 * n <= kMaxWarps * sms) ? 4 : (n <= two_upto ? 2 : 1);
     if (team_override()) G = team_override();
-    const int max_warps = elem_bytes > 4 ? kMaxWarps / 2 : (G == 1 ? kCtaWarps<float, 1> : kCtaWarps<float, 2>);
+    const int max_warps = elem_bytes > 4 ? kMaxWarps / 2
+                          : (G == 1 ? kCtaWarps<float, 1> : (push ? kPushWarps : kCtaWarps<float, 2>));
     int max_teams = max_warps / G;
     // Every team takes whole atoms, so a kernel runs ceil(n / teams) rounds of them:
     // take the fewest teams per CTA that keep the fewest rounds (more registers and
@@ -2069,8 +2075,10 @@ int launch_network(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& 
                    double* forces, double* per_atom, double* out, int* rev, cudaStream_t st,
                    const Marker& mk, const MdFuse& mf) {
     // the WIDE build exists for the pull-form (single-domain periodic) path only
-    const bool wide_ok = sizeof(T) == 4 && !gr.alist && pull_mode(gr, ws, md.n_msg) != 0;
-    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), wide_ok);
+    const bool pull = !gr.alist && pull_mode(gr, ws, md.n_msg) != 0;
+    const bool wide_ok = sizeof(T) == 4 && pull;
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), wide_ok,
+                                  !pull && md.n_msg > 0);
     int launches;
     if constexpr (sizeof(T) == 4)
         if (sh.G == 2 && sh.wide) {
@@ -2115,7 +2123,8 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
-    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)));
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), false,
+                                  md.n_msg > 0);
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:
