@@ -589,7 +589,7 @@ struct hmdp_ctx {
     DBuf pos, types, ghost, cell_count, members, cell_of, row_start, nnei, nbr, dr, rev, ety, inv_pos;
     DBuf offset, in_start, in_cnt, cursor, in_edge;
     // network workspace
-    DBuf er, es, eds, eb, edb, g, grev, zb, db, pa, vb, desc, ez1, h, uz1, dhown;
+    DBuf es, eds, eb, edb, g, grev, zb, db, pa, vb, desc, ez1, h, uz1, dhown;
     DBuf e_atom, forces, partial, ticket, out, err, desc64;
     // DeePMD-style families: vector edge gradients and the repformer workspace
     DBuf gv, gvrev, rf_env, rf_g2, rf_qkv, rf_dg2, rf_dwh, rf_g1, rf_P, rf_uz, rf_mz, rf_D, rf_A,
@@ -710,7 +710,7 @@ struct hmdp_ctx {
         cudaSetDevice(device);
         for (DBuf* b : {&pos, &types, &ghost, &cell_count, &members, &cell_of, &row_start, &nnei,
                         &nbr, &dr, &rev, &ety, &inv_pos, &offset, &in_start, &in_cnt, &cursor,
-                        &in_edge, &er, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &vb, &desc,
+                        &in_edge, &es, &eds, &eb, &edb, &g, &grev, &zb, &db, &pa, &vb, &desc,
                         &ez1, &h, &uz1, &dhown,
                         &e_atom, &forces, &partial, &ticket, &out, &err, &desc64, &dd_patom,
                         &dd_sremote, &dd_sghost, &gdd.role, &gdd.lists, &gdd.counts, &gdd.stamp,
@@ -777,7 +777,6 @@ struct hmdp_ctx {
         const size_t s = static_cast<size_t>(std::max<long long>(slots, 1));
         const size_t M = static_cast<size_t>(n_msg());
         const size_t Mw = std::max<size_t>(M, 1);
-        er.ensure(s * sizeof(T));
         es.ensure(s * sizeof(T));
         eds.ensure(s * sizeof(T));
         eb.ensure(s * kK * sizeof(T));
@@ -796,7 +795,6 @@ struct hmdp_ctx {
         uz1.ensure(Mw * na * kH * sizeof(T));
         dhown.ensure(na * kH * sizeof(T));
         DevWork<T> w{};
-        w.er = er.as<T>();
         w.es = es.as<T>();
         w.eds = eds.as<T>();
         w.eb = eb.as<T>();

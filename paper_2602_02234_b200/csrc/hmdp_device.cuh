@@ -94,7 +94,6 @@ struct DevGraph {
 template <typename T>
 struct DevWork {
     // per edge slot
-    T* er;    // r
     T* es;    // s(r)
     T* eds;   // s'(r)
     T* eb;    // [slot][8] b_k

@@ -509,7 +509,6 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                     b[k] = gk * s;
                     db[k] = -d * md.invw2 * gk * s + gk * ds;  // BasisT::derivatives
                 }
-                ws.er[e] = r;
                 ws.es[e] = s;
                 ws.eds[e] = ds;
                 st4(ws.eb + 8ll * e, b[0], b[1], b[2], b[3]);
