@@ -258,9 +258,11 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
 // list, neighborlist.cpp:104-111) and written with their FP64 edge_dr
 // (inference.cpp:474-485) and neighbour type.
 // ---------------------------------------------------------------------------
+constexpr int kCandDr = 64;  // survivors whose FP64 displacement is kept for the write
 struct NbrSmem {
     int cand[kCandMax];  // this warp's surviving candidates
     int cnt;
+    double cdr[kCandDr][3];  // their displacements as the pair test computed them
 };
 
 // G warps (a "team", named barrier `bar`) search one atom: warp w takes the
@@ -289,10 +291,11 @@ __device__ __forceinline__ void nbr_search_team(int i, const double* pos, const 
         nid = (z * cg.nc[1] + y) * cg.nc[0] + x;
     }
     bool unique = lane < 27;
-    for (int q = 0; q < 27; ++q) {
-        const int other = __shfl_sync(FULL_MASK, nid, q);
-        if (q < lane && other == nid) unique = false;
-    }
+    if (cg.nc[0] < 3 || cg.nc[1] < 3 || cg.nc[2] < 3)  // small grids: a cell can repeat
+        for (int q = 0; q < 27; ++q) {
+            const int other = __shfl_sync(FULL_MASK, nid, q);
+            if (q < lane && other == nid) unique = false;
+        }
     int cnt = 0;
     if (unique) {
         cnt = cell_count[nid];
@@ -325,24 +328,26 @@ __device__ __forceinline__ void nbr_search_team(int i, const double* pos, const 
             const int bb = __shfl_sync(FULL_MASK, base, lo);
             jr[u] = q < ncand ? members[bb + (q - ob)] : -1;
         }
-        bool pass[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {  // FP64 pair test, no FMA contraction
-            pass[u] = false;
+        for (int u = 0; u < U; ++u) {  // FP64 pair test (no FMA contraction) + compaction
+            bool pass = false;
+            double dx = 0.0, dy = 0.0, dz = 0.0;
             const int j = jr[u];
             if (j >= 0 && j != i) {
-                const double dx = min_image1(__dsub_rn(pos[3 * j], xi), L0);
-                const double dy = min_image1(__dsub_rn(pos[3 * j + 1], yi), L1);
-                const double dz = min_image1(__dsub_rn(pos[3 * j + 2], zi), L2);
-                pass[u] = !(norm2_rn(dx, dy, dz) > range2);
+                dx = min_image1(__dsub_rn(pos[3 * j], xi), L0);
+                dy = min_image1(__dsub_rn(pos[3 * j + 1], yi), L1);
+                dz = min_image1(__dsub_rn(pos[3 * j + 2], zi), L2);
+                pass = !(norm2_rn(dx, dy, dz) > range2);
             }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {  // warp compaction
-            const unsigned bal = __ballot_sync(FULL_MASK, pass[u]);
-            if (pass[u]) {
+            const unsigned bal = __ballot_sync(FULL_MASK, pass);
+            if (pass) {
                 const int idx = total + __popc(bal & ((1u << lane) - 1u));
-                if (idx < kCandMax) sm.cand[idx] = jr[u];
+                if (idx < kCandMax) sm.cand[idx] = j;
+                if (idx < kCandDr) {  // kept for the write below
+                    sm.cdr[idx][0] = dx;
+                    sm.cdr[idx][1] = dy;
+                    sm.cdr[idx][2] = dz;
+                }
             }
             total += __popc(bal);
         }
@@ -371,9 +376,15 @@ __device__ __forceinline__ void nbr_search_team(int i, const double* pos, const 
         const long long slot = static_cast<long long>(i) * cap + rank;
         nbr[slot] = v;
         if (ety) ety[slot] = types[v];
-        dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
-        dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
-        dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
+        if (q < kCandDr) {  // the displacement the pair test computed
+            dr[3 * slot] = sm.cdr[q][0];
+            dr[3 * slot + 1] = sm.cdr[q][1];
+            dr[3 * slot + 2] = sm.cdr[q][2];
+        } else {
+            dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
+            dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
+            dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
+        }
     }
     if (w == 0 && lane == 0) {
         nnei[i] = m < cap ? m : cap;

@@ -45,7 +45,7 @@ __global__ void k_stage_bin(int n, const double* __restrict__ hx, const int* __r
 // warps per CTA, grid-stride over atoms.
 constexpr int kSearchCTA = 512;
 template <int G>
-__global__ __launch_bounds__(kSearchCTA) void k_nbr_search(
+__global__ __launch_bounds__(kSearchCTA, 2) void k_nbr_search(
     int n, const double* __restrict__ pos, CellGrid cg, const int* __restrict__ cell_count,
     const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
     int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
