@@ -357,10 +357,43 @@ struct WeightSet {
             order.push_back(&m.update[l]);
         }
         for (size_t q = 0; q < order.size(); ++q) push_mlp(*order[q], q == 0 ? kH : 0);
+        // The message MLP's output layer folded into the update MLP (FP64, then cast):
+        // U1 [h; msum] with msum = W2 t + ssum b2 equals [U1h | U1m W2] [h; t] + ssum (U1m b2)
+        // (hmdp_net.cu header).  uf[l] = [U1h | U1m W2] (32 x 64), ufT[l] its transpose,
+        // c1 = U1m b2, pushed after the flat MLPs (offsets offs[6 * order.size() + l]).
+        std::vector<std::vector<double>> uf(m.message.size()), ufT(m.message.size());
+        for (size_t l = 0; l < m.message.size(); ++l) {
+            const std::vector<double>& U1 = m.update[l].weights[0];  // [32][64]
+            const std::vector<double>& W2 = m.message[l].weights[1];  // [32][32]
+            const std::vector<double>& b2 = m.message[l].biases[1];
+            std::vector<double> f(32 * 64), c1(32);
+            for (int o = 0; o < 32; ++o) {
+                for (int k = 0; k < 32; ++k) f[o * 64 + k] = U1[o * 64 + k];
+                for (int c = 0; c < 32; ++c) {
+                    double acc = 0.0;
+                    for (int j = 0; j < 32; ++j) acc += U1[o * 64 + 32 + j] * W2[j * 32 + c];
+                    f[o * 64 + 32 + c] = acc;
+                }
+                double bc = 0.0;
+                for (int j = 0; j < 32; ++j) bc += U1[o * 64 + 32 + j] * b2[j];
+                c1[o] = bc;
+            }
+            uf[l] = f;
+            ufT[l] = transpose(f, 32, 64);
+            push(c1);
+        }
         // Per-kernel shared-memory images (hmdp_net.cu Stage order, rows padded by
         // 16 bytes): mat(mlp q, array a, rows, cols, leading dimension)
         enum { W1 = 0, W1T = 1, W2 = 3, W2T = 4 };
         const int padc = 16 / static_cast<int>(sizeof(T));
+        // a host matrix (row-major, rows x cols) into the current image
+        auto matv = [&](const std::vector<double>& w, int rows, int cols) {
+            for (int r = 0; r < rows; ++r) {
+                for (int c = 0; c < cols; ++c)
+                    host.push_back(static_cast<T>(w[static_cast<size_t>(r) * cols + c]));
+                for (int c = 0; c < 16 / static_cast<int>(sizeof(T)); ++c) host.push_back(T(0));
+            }
+        };
         auto mat = [&](size_t q, int a, int rows, int cols, int ld) {
             const size_t src = offs[6 * q + a];
             for (int r = 0; r < rows; ++r) {
@@ -394,15 +427,13 @@ struct WeightSet {
         }
         for (size_t l = 0; l < M; ++l) {  // message layer forward
             begin();
-            mat(Mq(l), W2, 32, 32, 32);
-            mat(Uq(l), W1, 32, 64, 64);
+            matv(uf[l], 32, 64);
             mat(Uq(l), W2, 32, 32, 32);
             if (l + 1 == M) {
                 mat(F, W1, 32, 32, 32);
                 mat(F, W1T, 32, 32, 32);
                 mat(Uq(l), W2T, 32, 32, 32);
-                mat(Uq(l), W1T, 64, 32, 32);
-                mat(Mq(l), W2T, 32, 32, 32);
+                matv(ufT[l], 64, 32);
             } else {
                 mat(Mq(l + 1), W1, 32, 32, kin);
             }
@@ -411,8 +442,7 @@ struct WeightSet {
             begin();
             mat(Mq(l + 1), W1T, 32, 32, 32);
             mat(Uq(l), W2T, 32, 32, 32);
-            mat(Uq(l), W1T, 64, 32, 32);
-            mat(Mq(l), W2T, 32, 32, 32);
+            matv(ufT[l], 64, 32);
         }
         if (M > 0) {  // embedding backward
             begin();
@@ -444,6 +474,7 @@ struct WeightSet {
             dev.msg[l] = next_mlp();
             dev.upd[l] = next_mlp();
         }
+        for (size_t l = 0; l < m.message.size(); ++l) dev.uc1[l] = base + offs[q++];
         size_t k = 0;
         dev.img_embed = base + img[k++];
         for (size_t l = 0; l < M; ++l) dev.img_fwd[l] = base + img[k++];

@@ -48,8 +48,12 @@ struct DevModel {
     // exactly as in shared memory (rows padded by 16 bytes), one bulk copy each
     // (hmdp_net.cu, Smem::load): embedding (or embed_fit when n_msg == 0), message
     // layer forward (the fused last-layer layout at n_msg - 1), message layer
-    // backward (l < n_msg - 1), embedding backward.
+    // backward (l < n_msg - 1), embedding backward.  Forward: [U1h | U1m W2] (the
+    // message output layer folded into the update MLP), backward [U1h^T ; (U1m W2)^T].
     const T* img_embed;
+    // U1m b2 per message layer (the message MLP's output bias through the update
+    // MLP's msum half; W2 itself is folded into the update matrices of the images)
+    const T* uc1[kMaxMsg];
     const T* img_fwd[kMaxMsg];
     const T* img_bwd[kMaxMsg];
     const T* img_embed_bwd;

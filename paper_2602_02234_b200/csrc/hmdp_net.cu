@@ -29,8 +29,13 @@
 // Linearity of the message MLP is exploited exactly (same function, fewer FLOPs):
 //   forward   z_e = tanh(W1h h_j + W1b b_e + b1) with the per-ATOM projection
 //             P_j = W1h h_j computed once per layer instead of once per edge;
-//             msum_i = sum_e s_e (W2 z_e + b2) = W2 (sum_e s_e z_e) + (sum_e s_e) b2
-//   backward  with dmsum_i from the update MLP, v = W2^T dmsum_i, c0 = dmsum_i.b2:
+//             msum_i = sum_e s_e (W2 z_e + b2) = W2 (sum_e s_e z_e) + (sum_e s_e) b2,
+//             and msum enters the update MLP only through U1m msum, so W2 is folded
+//             into it once at upload: U1m msum = (U1m W2) t + ssum (U1m b2) with
+//             t = sum_e s_e z_e (one 64-input mat-vec [h; t] instead of two)
+//   backward  with dmsum_i from the update MLP, v = W2^T dmsum_i, c0 = dmsum_i.b2;
+//             folded likewise: v = (U1m W2)^T dz_u (the second half of the fused
+//             transposed update matrix), c0 = dz_u . (U1m b2):
 //             dsc_e = dmsum_i . mo_e = v . z_e + c0,  dz_e = s_e v (1 - z_e^2),
 //             dE/dr_e += dsc_e s'(r_e) + sum_k b'_e[k] (W1b^T dz_e)[k],
 //             dE/dh_j += W1h^T sum_{e in in(j)} dz_e  (one mat-vec per atom).
@@ -752,8 +757,8 @@ struct GatherPre {
 // first batch of the edge loop, loaded before the atom's mat-vecs.
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool RECOMP>
-__device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, const T* mW2T,
-                                                  T mb1, T mb2, const T (&w1b)[kK], const DevGraph& gr,
+__device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, T mb1, T c1,
+                                                  const T (&w1b)[kK], const DevGraph& gr,
                                                   const DevWork<T>& ws, WarpSmem<T>& sm, int l,
                                                   int i, T dh, T zu, bool first_g,
                                                   Team<G>& tm, BwdPre<T>& pre, long long e0,
@@ -766,14 +771,12 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
     const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
     sm.y[lane] = dz;
     __syncwarp();
-    T din_h, dmsum;  // input rows 0..31 (h) and 32..63 (msum)
-    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, dmsum, tm, sm);
+    // rows 0..31: dE/dh (update input); rows 32..63 (folded): v = W2^T U1m^T dz
+    T din_h, v;
+    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, v, tm, sm);
     if (tm.w == 0)
         ws.dhown[static_cast<long long>(i) * kH + lane] = dh + din_h;  // residual + update
-    sm.x[lane] = dmsum;
-    __syncwarp();
-    const T v = twmv<T, 32>(mW2T, sm.x, lane, tm, sm);  // v = W2^T dmsum
-    const T c0 = warp_sum(dmsum * mb2);
+    const T c0 = warp_sum(dz * c1);  // dmsum . b2
     // stored z rows (LAST layer) or this layer's P rows (RECOMP)
     const T* Z = RECOMP ? ws.pa + static_cast<long long>(l) * gr.n * kH
                         : ws.z + (kRecomputeZ ? 0 : static_cast<long long>(l) * S * kH);
@@ -877,7 +880,7 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
 // activation zu): writes dhown (residual + update input), v^l_i = W2^T dmsum and
 // c0^l_i = dmsum . b2 for the senders of i's messages.
 template <typename T, int G>
-__device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, const T* mW2T, T mb2,
+__device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, T c1,
                                              const DevWork<T>& ws, WarpSmem<T>& sm, int n, int l,
                                              int i, T dh, T zu, Team<G>& tm) {
     const int lane = tm.lane;
@@ -886,12 +889,10 @@ __device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, const
     const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
     sm.y[lane] = dz;
     __syncwarp();
-    T din_h, dmsum;  // input rows 0..31 (h) and 32..63 (msum)
-    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, dmsum, tm, sm);
-    sm.x[lane] = dmsum;
-    __syncwarp();
-    const T v = twmv<T, 32>(mW2T, sm.x, lane, tm, sm);  // v = W2^T dmsum
-    const T c0 = warp_sum(dmsum * mb2);
+    // rows 0..31: dE/dh (update input); rows 32..63 (folded): v = W2^T U1m^T dz
+    T din_h, v;
+    twmv2<T, 32>(uW1T, sm.y, lane, lane + 32, din_h, v, tm, sm);
+    const T c0 = warp_sum(dz * c1);  // dmsum . b2
     if (tm.w == 0) {
         const long long b = static_cast<long long>(l & 1) * n + i;
         ws.dhown[static_cast<long long>(i) * kH + lane] = dh + din_h;
@@ -1025,18 +1026,15 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
     const DevMlp<T>& upd = md.upd[l];
     Smem<T> sg(reinterpret_cast<T*>(smem_raw));
     __shared__ unsigned long long s_mbar;
-    const T* mW2 = sg.template view<32, 32>();
-    const T* uW1 = sg.template view<32, 64>();
+    const T* uW1 = sg.template view<32, 64>();  // [U1h | U1m W2] (folded)
     const T* uW2 = sg.template view<32, 32>();
-    const T *nW1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *uW2T = nullptr, *uW1T = nullptr,
-            *mW2T = nullptr;
+    const T *nW1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *uW2T = nullptr, *uW1T = nullptr;
     if constexpr (LAST) {
         fW1 = sg.template view<32, 32>();
         fW1T = sg.template view<32, 32>();
         uW2T = sg.template view<32, 32>();
-        uW1T = sg.template view<64, 32>();
-        mW2T = sg.template view<32, 32>();
-} else {
+        uW1T = sg.template view<64, 32>();  // [U1h^T ; (U1m W2)^T]
+    } else {
         nW1h = sg.template view<32, 32>();
     }
     sg.load(md.img_fwd[l], &s_mbar);
@@ -1047,7 +1045,8 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
     T w1b[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
-    const T mb1 = msg.b1[lane], mb2 = msg.b2[lane], ub1 = upd.b1[lane], ub2 = upd.b2[lane];
+    const T mb1 = msg.b1[lane], ub1 = upd.b1[lane], ub2 = upd.b2[lane];
+    const T c1 = md.uc1[l][lane];  // U1m b2 (folded message output bias)
     const T fb1 = LAST ? md.fit.b1[lane] : T(0), fw2 = LAST ? md.fit.W2[lane] : T(0);
     const T fb2 = LAST ? md.fit.b2[0] : T(0);
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
@@ -1165,14 +1164,11 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
             Smem<T>::wait(&s_mbar);
             staged = true;
         }
-        sm.t[lane] = acc;
+        // update MLP on [h_i, msum] (64 -> 32 tanh -> 32), residual, with W2 folded:
+        // U1 [h; msum] = [U1h | U1m W2] [h; t] + ssum U1m b2,  t = sum_e s_e z_e
+        sm.x[kH + lane] = acc;
         __syncwarp();
-        // msum = W2 (sum_e s_e z_e) + (sum_e s_e) b2  -> second half of the update input
-        const T msum = twmv<T, 32>(mW2, sm.t, lane, tm, sm) + ssum * mb2;
-        sm.x[kH + lane] = msum;
-        __syncwarp();
-        // update MLP on [h_i, msum] (64 -> 32 tanh -> 32), residual
-        const T zu = d_tanh(twmv<T, 64>(uW1, sm.x, lane, tm, sm) + ub1);
+        const T zu = d_tanh((twmv<T, 64>(uW1, sm.x, lane, tm, sm) + ssum * c1) + ub1);
         if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
         sm.y[lane] = zu;
         __syncwarp();
@@ -1196,10 +1192,10 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
                                   lead ? ws.e_atom + i : nullptr, tm, sm);
             TP(7);
             if constexpr (PULL == 0)
-                msg_backward_warp<T, G, false>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i,
+                msg_backward_warp<T, G, false>(uW2T, uW1T, mb1, c1, w1b, gr, ws, sm, l, i,
                                                dh, zu, true, tm, pre, ar.e0, mloc);
             else  // the edges' share runs at their senders (k_msg_bwd_pull / k_embed_bwd_pull)
-                upd_bwd_pull<T, G>(uW2T, uW1T, mW2T, mb2, ws, sm, n, l, i, dh, zu, tm);
+                upd_bwd_pull<T, G>(uW2T, uW1T, c1, ws, sm, n, l, i, dh, zu, tm);
             TP(8);
         }
         __syncwarp();
@@ -1220,8 +1216,7 @@ __global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(Dev
     // W1h^(l+1)^T: rows 0..31 of msg[l+1].W1T ([in][32])
     const T* nW1hT = sg.template view<32, 32>();
     const T* uW2T = sg.template view<32, 32>();
-    const T* uW1T = sg.template view<64, 32>();
-    const T* mW2T = sg.template view<32, 32>();
+    const T* uW1T = sg.template view<64, 32>();  // [U1h^T ; (U1m W2)^T]
     sg.load(md.img_bwd[l], &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
@@ -1229,7 +1224,7 @@ __global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(Dev
     T w1b[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
-    const T mb1 = msg.b1[lane], mb2 = msg.b2[lane];
+    const T mb1 = msg.b1[lane], c1 = md.uc1[l][lane];
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
     pdl_wait();
@@ -1267,7 +1262,7 @@ __global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(Dev
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        msg_backward_warp<T, G, kRecomputeZ>(uW2T, uW1T, mW2T, mb1, mb2, w1b, gr, ws, sm, l, i, dh,
+        msg_backward_warp<T, G, kRecomputeZ>(uW2T, uW1T, mb1, c1, w1b, gr, ws, sm, l, i, dh,
                                              zu, false, tm, pre, ar.e0, mloc);
         __syncwarp();
     }
@@ -1377,8 +1372,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     __shared__ unsigned long long s_mbar;
     const T* nW1hT = sg.template view<32, 32>();  // W1h^(l+1)^T
     const T* uW2T = sg.template view<32, 32>();
-    const T* uW1T = sg.template view<64, 32>();
-    const T* mW2T = sg.template view<32, 32>();
+    const T* uW1T = sg.template view<64, 32>();  // [U1h^T ; (U1m W2)^T]
     sg.load(md.img_bwd[l], &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
     Team<G> tm;
@@ -1386,7 +1380,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     T w1b[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) w1b[k] = msgn.W1T[(kH + k) * kH + lane];
-    const T mb1n = msgn.b1[lane], mb2 = md.msg[l].b2[lane];
+    const T mb1n = msgn.b1[lane], c1 = md.uc1[l][lane];
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
     pdl_wait();
@@ -1413,7 +1407,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
         // dE/dh^{l+1}_k = own + W1h^(l+1)^T sum_e dz_e
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        upd_bwd_pull<T, G>(uW2T, uW1T, mW2T, mb2, ws, sm, n, l, k, dh, zu, tm);
+        upd_bwd_pull<T, G>(uW2T, uW1T, c1, ws, sm, n, l, k, dh, zu, tm);
     }
     if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
@@ -1747,9 +1741,9 @@ static int staged_elems(Phase p) {
     switch (p) {
         case Phase::EmbedFit: return 6 * m32;
         case Phase::Embed: return 3 * m32;
-        case Phase::MsgFwd: return 3 * m32 + m64;
-        case Phase::MsgFwdLast: return 6 * m32 + m64 + t64;
-        case Phase::MsgBwd: return 3 * m32 + t64;
+        case Phase::MsgFwd: return 2 * m32 + m64;
+        case Phase::MsgFwdLast: return 4 * m32 + m64 + t64;
+        case Phase::MsgBwd: return 2 * m32 + t64;
         case Phase::EmbedBwd: return 3 * m32;
     }
     return 0;
