@@ -382,6 +382,59 @@ struct WeightSet {
             ufT[l] = transpose(f, 32, 64);
             push(c1);
         }
+        // ... and the next consumer of the embedding output h^0 = eW2 z1 + eb2 (P^0 =
+        // W1h^0 h^0, or the fitting net at depth 1), and the fitting net through the
+        // top update's output layer h^M = h + U2 zu + b2u: products in FP64
+        auto matmul = [](const std::vector<double>& A, int ar, int ac, int lda,
+                         const std::vector<double>& B, int bc, int ldb) {  // A[:, :ac] B
+            std::vector<double> C(static_cast<size_t>(ar) * bc, 0.0);
+            for (int r = 0; r < ar; ++r)
+                for (int c = 0; c < bc; ++c) {
+                    double acc = 0.0;
+                    for (int k = 0; k < ac; ++k) acc += A[r * lda + k] * B[k * ldb + c];
+                    C[static_cast<size_t>(r) * bc + c] = acc;
+                }
+            return C;
+        };
+        auto matvec = [](const std::vector<double>& A, int ar, int ac, int lda,
+                         const std::vector<double>& x, const std::vector<double>* add) {
+            std::vector<double> y(ar, 0.0);
+            for (int r = 0; r < ar; ++r) {
+                double acc = 0.0;
+                for (int k = 0; k < ac; ++k) acc += A[r * lda + k] * x[k];
+                y[r] = acc + (add ? (*add)[r] : 0.0);
+            }
+            return y;
+        };
+        auto stack = [](const std::vector<double>& top, const std::vector<double>& bottom) {
+            std::vector<double> v(top);
+            v.insert(v.end(), bottom.begin(), bottom.end());
+            return v;
+        };
+        const std::vector<double>& eW2 = m.embedding.weights[1];  // [32][32]
+        const std::vector<double>& eb2 = m.embedding.biases[1];
+        const std::vector<double>& fW1 = m.fitting.weights[0];  // [32][32]
+        const std::vector<double>& fb1 = m.fitting.biases[0];
+        const int kin0 = kH + kK;
+        // consumer of h^0: rows of W1h^0 (the first 32 inputs of message layer 0) or fW1
+        const std::vector<double> Q = m.message.empty()
+                                          ? matmul(fW1, 32, 32, 32, eW2, 32, 32)
+                                          : matmul(m.message[0].weights[0], 32, 32, kin0, eW2, 32, 32);
+        const std::vector<double> eX2 = stack(eW2, Q);  // [eW2 ; Q] (64 x 32)
+        const std::vector<double> eQT = transpose(Q, 32, 32);
+        push(m.message.empty() ? matvec(fW1, 32, 32, 32, eb2, &fb1)
+                               : matvec(m.message[0].weights[0], 32, 32, kin0, eb2, nullptr));
+        std::vector<double> lX3, lY3;
+        if (!m.message.empty()) {
+            const size_t L = m.message.size() - 1;
+            const std::vector<double>& U2 = m.update[L].weights[1];  // [32][32]
+            const std::vector<double> FU = matmul(fW1, 32, 32, 32, U2, 32, 32);
+            lX3 = stack(U2, FU);
+            lY3 = stack(transpose(fW1, 32, 32), transpose(FU, 32, 32));
+            push(matvec(fW1, 32, 32, 32, m.update[L].biases[1], &fb1));
+        } else {
+            push(std::vector<double>(32, 0.0));
+        }
         // Per-kernel shared-memory images (hmdp_net.cu Stage order, rows padded by
         // 16 bytes): mat(mlp q, array a, rows, cols, leading dimension)
         enum { W1 = 0, W1T = 1, W2 = 3, W2T = 4 };
@@ -414,27 +467,23 @@ struct WeightSet {
             align();
             img.push_back(host.size());
         };
-        begin();  // embedding / embed_fit
+        begin();  // embedding / embed_fit: eW1, [eW2 ; Q] (+ Q^T, eW1^T for embed_fit)
         mat(E, W1, 32, 32, 32);
-        mat(E, W2, 32, 32, 32);
+        matv(eX2, 64, 32);
         if (M == 0) {
-            mat(F, W1, 32, 32, 32);
-            mat(F, W1T, 32, 32, 32);
-            mat(E, W2T, 32, 32, 32);
+            matv(eQT, 32, 32);
             mat(E, W1T, 32, 32, 32);
-        } else {
-            mat(Mq(0), W1, 32, 32, kin);
         }
         for (size_t l = 0; l < M; ++l) {  // message layer forward
             begin();
             matv(uf[l], 32, 64);
-            mat(Uq(l), W2, 32, 32, 32);
-            if (l + 1 == M) {
+            if (l + 1 == M) {  // fW1, [U2 ; fW1 U2], [fW1^T ; (fW1 U2)^T], [U1h^T ; (U1m W2)^T]
                 mat(F, W1, 32, 32, 32);
-                mat(F, W1T, 32, 32, 32);
-                mat(Uq(l), W2T, 32, 32, 32);
+                matv(lX3, 64, 32);
+                matv(lY3, 64, 32);
                 matv(ufT[l], 64, 32);
             } else {
+                mat(Uq(l), W2, 32, 32, 32);
                 mat(Mq(l + 1), W1, 32, 32, kin);
             }
         }
@@ -475,6 +524,8 @@ struct WeightSet {
             dev.upd[l] = next_mlp();
         }
         for (size_t l = 0; l < m.message.size(); ++l) dev.uc1[l] = base + offs[q++];
+        dev.eqb = base + offs[q++];
+        dev.fcl = base + offs[q++];
         size_t k = 0;
         dev.img_embed = base + img[k++];
         for (size_t l = 0; l < M; ++l) dev.img_fwd[l] = base + img[k++];

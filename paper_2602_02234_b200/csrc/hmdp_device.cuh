@@ -54,6 +54,11 @@ struct DevModel {
     // U1m b2 per message layer (the message MLP's output bias through the update
     // MLP's msum half; W2 itself is folded into the update matrices of the images)
     const T* uc1[kMaxMsg];
+    // the embedding output layer folded into its consumer: eqb = W1h^0 eb2 (P^0 bias) or
+    // fW1 eb2 + fb1 (the fitting pre-activation, depth 1); fcl = fW1 b2u + fb1 (the
+    // fitting through the top update's output layer)
+    const T* eqb;
+    const T* fcl;
     const T* img_fwd[kMaxMsg];
     const T* img_bwd[kMaxMsg];
     const T* img_embed_bwd;

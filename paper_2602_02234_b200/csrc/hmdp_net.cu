@@ -401,6 +401,44 @@ __device__ __forceinline__ void twmv2(const T* W, const T* x, int row0, int row1
     }
 }
 
+// Rows `row` of two matrices over the same input vector: ya = A[row] . x[0..NA),
+// yb = B[row] . x[0..NB) (NB <= NA: B reads a prefix of x), one team barrier.
+template <typename T, int NA, int NB, int G>
+__device__ __forceinline__ void twmv_pair(const T* A, const T* B, const T* x, int row, T& ya, T& yb,
+                                          Team<G>& tm, WarpSmem<T>& sm) {
+    if constexpr (G == 1) {
+        ya = wmv<T, NA>(A, x, row);
+        yb = wmv<T, NB>(B, x, row);
+    } else {
+        constexpr int KA = NA / G, KB = NB / G;
+        static_assert(KA % 4 == 0 && KB % 4 == 0, "bad team split");
+        const T* wa = A + row * pad_ld<T>(NA) + tm.w * KA;
+        const T* wb = B + row * pad_ld<T>(NB) + tm.w * KB;
+        const T* xa = x + tm.w * KA;
+        const T* xb = x + tm.w * KB;
+        T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
+#pragma unroll
+        for (int k = 0; k < KA; k += 4) {
+            const V4<T> w = ld4c(wa + k), v = ld4c(xa + k);
+            a0 += w.x * v.x;
+            a1 += w.y * v.y;
+            a0 += w.z * v.z;
+            a1 += w.w * v.w;
+        }
+#pragma unroll
+        for (int k = 0; k < KB; k += 4) {
+            const V4<T> w = ld4c(wb + k), v = ld4c(xb + k);
+            b0 += w.x * v.x;
+            b1 += w.y * v.y;
+            b0 += w.z * v.z;
+            b1 += w.w * v.w;
+        }
+        ya = a0 + a1;
+        yb = b0 + b1;
+        tm.sum2(ya, yb, sm);
+    }
+}
+
 // Sum of the pushed adjoint rows in i's mirror slots (+ remote partials in
 // domain decomposition), lane = channel, fixed order.
 template <typename T, int G>
@@ -425,25 +463,6 @@ __device__ __forceinline__ T gather_in(const T* D, const DevWork<T>& ws, const D
     return acc;
 }
 
-// Fitting net forward + backward on h (shared, channel-indexed): writes e_i for
-// owned atoms (0 for ghosts; e_out may be null), returns dE/dh[lane] (0 for
-// ghosts).  inference.cpp:288-311.  tmp: 32 elements of shared scratch.
-template <typename T, int G>
-__device__ __forceinline__ T fit_warp(const T* fW1, const T* fW1T, T fb1, T fw2, T fb2,
-                                      const T* h_s, T* tmp, bool owned, double* e_out,
-                                      Team<G>& tm, WarpSmem<T>& sm) {
-    const int lane = tm.lane;
-    const T zf = d_tanh(twmv<T, 32>(fW1, h_s, lane, tm, sm) + fb1);
-    // linear head 32 -> 1 and its adjoint (dout = 1)
-    const T e = warp_sum(fw2 * zf) + fb2;
-    if (e_out && lane == 0) *e_out = owned ? static_cast<double>(e) : 0.0;
-    tmp[lane] = (fw2 * T(1)) * (T(1) - zf * zf);
-    __syncwarp();
-    const T dh = twmv<T, 32>(fW1T, tmp, lane, tm, sm);
-    __syncwarp();
-    return owned ? dh : T(0);
-}
-
 // ---------------------------------------------------------------------------
 // Edge radial features + descriptor + embedding; pushes P^0 (message layer 0's
 // neighbour projection) or, for depth 1 (FUSE_FIT), runs the whole fitting and
@@ -461,15 +480,13 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     Smem<T> sg(reinterpret_cast<T*>(smem_raw));
     __shared__ unsigned long long s_mbar;
     const T* eW1 = sg.template view<32, 32>();
-    const T* eW2 = sg.template view<32, 32>();
-    const T *W1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *eW2T = nullptr, *eW1T = nullptr;
+    // [eW2 ; Q]: the embedding output layer and, folded through it, the next
+    // consumer of h^0: Q = W1h^0 eW2 (P^0) or Q = fW1 eW2 (the fitting net, FUSE_FIT)
+    const T* eX2 = sg.template view<64, 32>();
+    const T *fQT = nullptr, *eW1T = nullptr;
     if constexpr (FUSE_FIT) {
-        fW1 = sg.template view<32, 32>();
-        fW1T = sg.template view<32, 32>();
-        eW2T = sg.template view<32, 32>();
+        fQT = sg.template view<32, 32>();  // (fW1 eW2)^T: dE/dz1 from the fitting adjoint
         eW1T = sg.template view<32, 32>();
-} else {
-        W1h = sg.template view<32, 32>();
     }
     if constexpr (!DESC_ONLY) sg.load(md.img_embed, &s_mbar);
     WarpSmem<T>& sm = sg.warp_scratch();
@@ -477,7 +494,8 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     const int lane = tm.lane;
     const bool lead = tm.w == 0;
     const T eb1 = md.embed.b1[lane], eb2 = md.embed.b2[lane];
-    const T fb1 = FUSE_FIT ? md.fit.b1[lane] : T(0), fw2 = FUSE_FIT ? md.fit.W2[lane] : T(0);
+    const T qb = md.eqb[lane];  // W1h^0 eb2 (P^0) or fW1 eb2 + fb1 (the fitting pre-activation)
+    const T fw2 = FUSE_FIT ? md.fit.W2[lane] : T(0);
     const T fb2 = FUSE_FIT ? md.fit.b2[0] : T(0);
     const int nd = md.n_types * kK;
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
@@ -594,18 +612,22 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
         if (lead) ws.ez1[static_cast<long long>(i) * kH + lane] = z1;
         sm.y[lane] = z1;
         __syncwarp();
-        const T h0 = twmv<T, 32>(eW2, sm.y, lane, tm, sm) + eb2;
+        T h0, qz;  // h^0 - eb2 and Q z1
+        twmv2<T, 32>(eX2, sm.y, lane, lane + 32, h0, qz, tm, sm);
+        h0 += eb2;
         if (lead) ws.h[static_cast<long long>(i) * kH + lane] = h0;
-        sm.x[lane] = h0;
-        __syncwarp();
         if constexpr (FUSE_FIT) {
+            // fitting forward on h^0 (pre-activation fW1 h^0 + fb1 = Q z1 + qb) and its
+            // adjoint straight to z1: dE/dz1 = (fW1 eW2)^T (fw2 (1 - zf^2))
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.x, sm.t, owned,
-                                  lead ? ws.e_atom + i : nullptr, tm, sm);
-            sm.y[lane] = dh;
+            const T zf = d_tanh(qz + qb);
+            const T en = warp_sum(fw2 * zf) + fb2;
+            if (lead && lane == 0) ws.e_atom[i] = owned ? static_cast<double>(en) : 0.0;
+            sm.t[lane] = owned ? fw2 * (T(1) - zf * zf) : T(0);
             __syncwarp();
-            // embedding backward: linear layer 2 (W2^T), tanh layer 1 (W1^T, padded)
-            const T dz1 = twmv<T, 32>(eW2T, sm.y, lane, tm, sm) * (T(1) - z1 * z1);
+            // embedding backward: tanh layer 1 (W1^T, padded)
+            const T dz1 = twmv<T, 32>(fQT, sm.t, lane, tm, sm) * (T(1) - z1 * z1);
+            __syncwarp();
             sm.t[lane] = dz1;
             __syncwarp();
             const T dd = twmv<T, 32>(eW1T, sm.t, lane, tm, sm);
@@ -630,9 +652,9 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 if (!rev) ws.grev[gr.inv_pos[e]] = acc;
             }
         } else {
-            // P^0 = W1h^(0) h^0, one row per atom (L2-resident; gathered by the
-            // sources of i's in-edges in the message layer)
-            const T p = twmv<T, 32>(W1h, sm.x, lane, tm, sm);
+            // P^0 = W1h^(0) h^0 = Q z1 + W1h^(0) eb2, one row per atom (L2-resident;
+            // gathered by the sources of i's in-edges in the message layer)
+            const T p = qz + qb;
             if (lead) {
                 ws.pa[static_cast<long long>(i) * kH + lane] = p;
                 if (ws.p_atom) ws.p_atom[static_cast<long long>(i) * kH + lane] = p;
@@ -758,17 +780,22 @@ struct GatherPre {
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool RECOMP>
 __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, T mb1, T c1,
-                                                  const T (&w1b)[kK], const DevGraph& gr,
+                                                  T w_in, const T (&w1b)[kK], const DevGraph& gr,
                                                   const DevWork<T>& ws, WarpSmem<T>& sm, int l,
                                                   int i, T dh, T zu, bool first_g,
                                                   Team<G>& tm, BwdPre<T>& pre, long long e0,
                                                   int mloc) {
     const int lane = tm.lane;
     const long long S = ws.slots;
-    // update MLP backward (64 -> 32 tanh -> 32)
-    sm.t[lane] = dh;
-    __syncwarp();
-    const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
+    // update MLP backward (64 -> 32 tanh -> 32); uW2T null: w_in = uW2^T dh given
+    T dz;
+    if (uW2T) {
+        sm.t[lane] = dh;
+        __syncwarp();
+        dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
+    } else {
+        dz = w_in * (T(1) - zu * zu);
+    }
     sm.y[lane] = dz;
     __syncwarp();
     // rows 0..31: dE/dh (update input); rows 32..63 (folded): v = W2^T U1m^T dz
@@ -880,13 +907,18 @@ __device__ __forceinline__ void msg_backward_warp(const T* uW2T, const T* uW1T, 
 // activation zu): writes dhown (residual + update input), v^l_i = W2^T dmsum and
 // c0^l_i = dmsum . b2 for the senders of i's messages.
 template <typename T, int G>
-__device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, T c1,
+__device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, T c1, T w_in,
                                              const DevWork<T>& ws, WarpSmem<T>& sm, int n, int l,
                                              int i, T dh, T zu, Team<G>& tm) {
     const int lane = tm.lane;
-    sm.t[lane] = dh;
-    __syncwarp();
-    const T dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
+    T dz;  // uW2T null: w_in = uW2^T dh given
+    if (uW2T) {
+        sm.t[lane] = dh;
+        __syncwarp();
+        dz = twmv<T, 32>(uW2T, sm.t, lane, tm, sm) * (T(1) - zu * zu);
+    } else {
+        dz = w_in * (T(1) - zu * zu);
+    }
     sm.y[lane] = dz;
     __syncwarp();
     // rows 0..31: dE/dh (update input); rows 32..63 (folded): v = W2^T U1m^T dz
@@ -1027,14 +1059,17 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
     Smem<T> sg(reinterpret_cast<T*>(smem_raw));
     __shared__ unsigned long long s_mbar;
     const T* uW1 = sg.template view<32, 64>();  // [U1h | U1m W2] (folded)
-    const T* uW2 = sg.template view<32, 32>();
-    const T *nW1h = nullptr, *fW1 = nullptr, *fW1T = nullptr, *uW2T = nullptr, *uW1T = nullptr;
+    const T *uW2 = nullptr, *nW1h = nullptr, *fW1 = nullptr, *uX3 = nullptr, *fY3 = nullptr,
+            *uW1T = nullptr;
     if constexpr (LAST) {
+        // the fitting net folded through the top update's output layer:
+        // fW1 h^M = fW1 h + (fW1 U2) zu + fW1 b2u, and its adjoint back to zu
         fW1 = sg.template view<32, 32>();
-        fW1T = sg.template view<32, 32>();
-        uW2T = sg.template view<32, 32>();
+        uX3 = sg.template view<64, 32>();  // [U2 ; fW1 U2]
+        fY3 = sg.template view<64, 32>();  // [fW1^T ; (fW1 U2)^T]
         uW1T = sg.template view<64, 32>();  // [U1h^T ; (U1m W2)^T]
     } else {
+        uW2 = sg.template view<32, 32>();
         nW1h = sg.template view<32, 32>();
     }
     sg.load(md.img_fwd[l], &s_mbar);
@@ -1047,7 +1082,8 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
     for (int k = 0; k < kK; ++k) w1b[k] = msg.W1T[(kH + k) * kH + lane];
     const T mb1 = msg.b1[lane], ub1 = upd.b1[lane], ub2 = upd.b2[lane];
     const T c1 = md.uc1[l][lane];  // U1m b2 (folded message output bias)
-    const T fb1 = LAST ? md.fit.b1[lane] : T(0), fw2 = LAST ? md.fit.W2[lane] : T(0);
+    const T fcl = LAST ? md.fcl[lane] : T(0);  // fW1 b2u + fb1
+    const T fw2 = LAST ? md.fit.W2[lane] : T(0);
     const T fb2 = LAST ? md.fit.b2[0] : T(0);
     __syncthreads();  // publishes the mbarrier init; the copy is awaited at first use
     bool staged = false;
@@ -1168,16 +1204,16 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
         // U1 [h; msum] = [U1h | U1m W2] [h; t] + ssum U1m b2,  t = sum_e s_e z_e
         sm.x[kH + lane] = acc;
         __syncwarp();
-        const T zu = d_tanh((twmv<T, 64>(uW1, sm.x, lane, tm, sm) + ssum * c1) + ub1);
-        if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
-        sm.y[lane] = zu;
-        __syncwarp();
-        const T hn = hi + (twmv<T, 32>(uW2, sm.y, lane, tm, sm) + ub2);
-        if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
-        sm.t[lane] = hn;
-        __syncwarp();
-        TP(5);
         if constexpr (!LAST) {
+            const T zu = d_tanh((twmv<T, 64>(uW1, sm.x, lane, tm, sm) + ssum * c1) + ub1);
+            if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
+            sm.y[lane] = zu;
+            __syncwarp();
+            const T hn = hi + (twmv<T, 32>(uW2, sm.y, lane, tm, sm) + ub2);
+            if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
+            sm.t[lane] = hn;
+            __syncwarp();
+            TP(5);
             // P^{l+1}_i, one row per atom
             const T p = twmv<T, 32>(nW1h, sm.t, lane, tm, sm);
             if (lead) {
@@ -1186,16 +1222,34 @@ __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 
             }
             TP(6);
         } else {
+            // update input [h; t] for U1 and, on its h half, fW1 h (one team barrier)
+            T pu, fh;
+            twmv_pair<T, 64, 32>(uW1, fW1, sm.x, lane, pu, fh, tm, sm);
+            const T zu = d_tanh((pu + ssum * c1) + ub1);
+            if (lead) ws.uz1[(static_cast<long long>(l) * n + i) * kH + lane] = zu;
+            sm.y[lane] = zu;
+            __syncwarp();
+            T uh, up;  // U2 zu and (fW1 U2) zu
+            twmv2<T, 32>(uX3, sm.y, lane, lane + 32, uh, up, tm, sm);
+            const T hn = hi + (uh + ub2);
+            if (lead) ws.h[(static_cast<long long>(l + 1) * n + i) * kH + lane] = hn;
+            TP(5);
+            // fitting (inference.cpp:288-311): pre-activation fW1 h^M + fb1
             const bool owned = !(gr.is_ghost && gr.is_ghost[i]);
-            // fitting: h^M -> dE/dh^M
-            const T dh = fit_warp(fW1, fW1T, fb1, fw2, fb2, sm.t, sm.x, owned,
-                                  lead ? ws.e_atom + i : nullptr, tm, sm);
+            const T zf = d_tanh((fh + up) + fcl);
+            const T en = warp_sum(fw2 * zf) + fb2;
+            if (lead && lane == 0) ws.e_atom[i] = owned ? static_cast<double>(en) : 0.0;
+            sm.t[lane] = owned ? fw2 * (T(1) - zf * zf) : T(0);
+            __syncwarp();
+            T dh, w;  // dE/dh^M = fW1^T dzf and U2^T dE/dh^M = (fW1 U2)^T dzf
+            twmv2<T, 32>(fY3, sm.t, lane, lane + 32, dh, w, tm, sm);
+            __syncwarp();
             TP(7);
             if constexpr (PULL == 0)
-                msg_backward_warp<T, G, false>(uW2T, uW1T, mb1, c1, w1b, gr, ws, sm, l, i,
+                msg_backward_warp<T, G, false>(nullptr, uW1T, mb1, c1, w, w1b, gr, ws, sm, l, i,
                                                dh, zu, true, tm, pre, ar.e0, mloc);
             else  // the edges' share runs at their senders (k_msg_bwd_pull / k_embed_bwd_pull)
-                upd_bwd_pull<T, G>(uW2T, uW1T, c1, ws, sm, n, l, i, dh, zu, tm);
+                upd_bwd_pull<T, G>(nullptr, uW1T, c1, w, ws, sm, n, l, i, dh, zu, tm);
             TP(8);
         }
         __syncwarp();
@@ -1262,7 +1316,7 @@ __global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_msg_bwd(Dev
         // dE/dh^{l+1}_i = own + W1h^(l+1)^T S_i
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        msg_backward_warp<T, G, kRecomputeZ>(uW2T, uW1T, mb1, c1, w1b, gr, ws, sm, l, i, dh,
+        msg_backward_warp<T, G, kRecomputeZ>(uW2T, uW1T, mb1, c1, T(0), w1b, gr, ws, sm, l, i, dh,
                                              zu, false, tm, pre, ar.e0, mloc);
         __syncwarp();
     }
@@ -1407,7 +1461,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
         // dE/dh^{l+1}_k = own + W1h^(l+1)^T sum_e dz_e
         const T dh = own + twmv<T, 32>(nW1hT, sm.t, lane, tm, sm);
         __syncwarp();
-        upd_bwd_pull<T, G>(uW2T, uW1T, c1, ws, sm, n, l, k, dh, zu, tm);
+        upd_bwd_pull<T, G>(uW2T, uW1T, c1, T(0), ws, sm, n, l, k, dh, zu, tm);
     }
     if (!staged) Smem<T>::wait(&s_mbar);  // no CTA exits with its weight copy in flight
 }
@@ -1739,10 +1793,10 @@ template <typename T>
 static int staged_elems(Phase p) {
     const int m32 = mat_elems<T>(32, 32), m64 = mat_elems<T>(32, 64), t64 = mat_elems<T>(64, 32);
     switch (p) {
-        case Phase::EmbedFit: return 6 * m32;
-        case Phase::Embed: return 3 * m32;
+        case Phase::EmbedFit: return 3 * m32 + t64;
+        case Phase::Embed: return m32 + t64;
         case Phase::MsgFwd: return 2 * m32 + m64;
-        case Phase::MsgFwdLast: return 4 * m32 + m64 + t64;
+        case Phase::MsgFwdLast: return m32 + m64 + 3 * t64;
         case Phase::MsgBwd: return 2 * m32 + t64;
         case Phase::EmbedBwd: return 3 * m32;
     }
