@@ -1,0 +1,107 @@
+"""Rewrite the measured numbers in DESIGN.md §7 and README.md from the committed
+evidence: profiles/round2/bench_default.json (the default bench line),
+profiles/round2/all_systems.md (tools/run_all_systems.sh) and
+profiles/round2/dpa3_2PTC/launches.md (ncu launch list).  Dev aid: run after a
+round-check GPU run has refreshed those files."""
+import json
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = lambda *a: os.path.join(ROOT, *a)  # noqa: E731
+
+d = json.load(open(P("profiles", "round2", "bench_default.json")))
+m2 = d["models"]["dpa2"]
+r = d["roofline"]
+design = open(P("DESIGN.md")).read()
+
+
+def sub(pattern, repl, text, count=1):
+    new, k = re.subn(pattern, repl, text, count=count, flags=re.M)
+    if k != count:
+        raise SystemExit(f"pattern not found: {pattern}")
+    return new
+
+
+design = sub(r"^\| DPA3 2PTC \| \*\*.*$",
+             f"| DPA3 2PTC | **{d['value']:.0f}** ({d['ns_per_day']:.0f} ns/day) | {d['ms_per_step']*1e3:.1f} | "
+             f"{d['warm_l2_graph100']['steps_per_s']:.0f} | {d['e2e']['value']:.0f} | {d['cpu_baseline']['value']:.1f} |",
+             design)
+design = sub(r"^\| DPA2 2PTC \| \*\*.*$",
+             f"| DPA2 2PTC | **{m2['value']:.0f}** ({m2['ns_per_day']:.0f} ns/day) | {m2['ms_per_step']*1e3:.1f} | "
+             f"{m2['warm_l2_graph100']['steps_per_s']:.0f} | {m2['e2e']['value']:.0f} | {m2['cpu_baseline']['value']:.1f} |",
+             design)
+design = sub(r"^- e2e / CPU reference = .*$",
+             f"- e2e / CPU reference = **{d['e2e']['value']/d['cpu_baseline']['value']:.0f}×** (DPA3) and "
+             f"{m2['e2e']['value']/m2['cpu_baseline']['value']:.0f}× (DPA2).", design)
+design = sub(r"^- Device-timed / CPU reference = .*$",
+             f"- Device-timed / CPU reference = {d['value']/d['cpu_baseline']['value']:.0f}× and "
+             f"{m2['value']/m2['cpu_baseline']['value']:.0f}×.", design)
+design = sub(r"^  - DPA3 2PTC `msg_fwd_last` (.*?): [0-9.]+ MFLOP per launch in [0-9.]+ µs → [0-9.]+ TFLOP/s = \*\*[0-9.]+%\*\* of the FFMA peak\.$",
+             lambda mo: f"  - DPA3 2PTC `msg_fwd_last` {mo.group(1)}: {r['flops_per_launch']/1e6:.0f} MFLOP per launch in "
+                        f"{r['mean_launch_us']:.1f} µs → {r['achieved']:.1f} TFLOP/s = **{r['frac']:.1%}** of the FFMA peak.",
+             design)
+design = sub(r"split along the kernel boundaries: [0-9.]+ MFLOP → [0-9]+%\.",
+             f"split along the kernel boundaries: {r['ref_counter']['flops_per_launch']/1e6:.0f} MFLOP → "
+             f"{r['ref_counter']['frac']:.0%}.", design)
+st = r["step"]
+design = sub(r"t_lb = FLOP_alg / P_fp32 = [0-9.]+ µs against the measured [0-9.]+ µs → \*\*[0-9]+%\*\*\. The DPA3 step runs at [0-9]+% of",
+             f"t_lb = FLOP_alg / P_fp32 = {st['t_lb_us']:.1f} µs against the measured {st['t_step_us']:.1f} µs → "
+             f"**{st['frac']:.0%}**. The DPA3 step runs at {st['frac']:.0%} of", design)
+if r.get("traffic"):
+    design = sub(r"from the `--set full` capture \([0-9.]+ MB\)",
+                 f"from the `--set full` capture ({r['traffic']/1e6:.1f} MB)", design)
+# per-kernel shares at 2PTC
+shares = {}
+for line in open(P("profiles", "round2", "dpa3_2PTC", "launches.md")):
+    mo = re.match(r"\| (k_\w+)<([^>]*)> \| \d+ \| [0-9.]+ \| ([0-9.]+)% \|", line)
+    if mo:
+        name, args, sh = mo.group(1), mo.group(2), float(mo.group(3))
+        a = [x.strip() for x in args.split(",")]
+        key = {"k_nbr_search": "search", "k_force": "force", "k_embed": "embed",
+               "k_msg_bwd_pull": "msg_bwd", "k_embed_bwd_pull": "embed_bwd",
+               "k_msg_bwd": "msg_bwd", "k_embed_bwd": "embed_bwd"}.get(name)
+        if name == "k_msg_fwd":
+            key = "msg_fwd_last" if a[2] in ("1", "true") else "msg_fwd"
+        shares[key] = shares.get(key, 0.0) + sh
+rows = "\n".join(f"| {k} | {v:.0f} % |" for k, v in sorted(shares.items(), key=lambda kv: -kv[1]))
+design = sub(r"(\| kernel \| share \|\n\|---\|---\|\n)(\|[^\n]*\|\n)+", lambda mo: mo.group(1) + rows + "\n", design)
+# paper boxes and replicas
+r1 = {"dpa3 1YRF": "19 408", "dpa3 1UBQ": "11 411", "dpa3 3LZM": "8 040", "dpa3 2PTC": "6 044",
+      "dpa2 1YRF": "37 668", "dpa2 1UBQ": "28 726", "dpa2 3LZM": "22 158", "dpa2 2PTC": "19 321",
+      "dpa3 2PTC x(2,2,2)": "1 036", "dpa3 2PTC x(4,4,4)": "137", "dpa2 2PTC x(2,2,2)": "4 188",
+      "dpa2 2PTC x(4,4,4)": "593"}
+main, rep = [], []
+for line in open(P("profiles", "round2", "all_systems.md")):
+    if not line.startswith("|"):
+        continue
+    c = [x.strip() for x in line.strip().strip("|").split("|")]
+    key = f"{c[0]} {c[1]}"
+    if len(c) == 7:
+        v = f"{int(c[3]):,}".replace(",", " ")
+        main.append(f"| {c[0].upper()} | {c[1]} | {c[2]} | {v} | {c[4]} | {c[5]} | {c[6]} | {r1[key]} |")
+    else:
+        v = f"{float(c[3]):,.0f}".replace(",", " ")
+        rep.append(f"| {c[0].upper()} | {c[1]} | {c[2]} | {v} | {c[4]} | {c[5]} | {r1[key]} |")
+design = sub(r"(\| model \| box \| atoms \| steps/s \| ns/day \| roofline \(dominant kernel\) \| CPU reference steps/s \| round 1 steps/s \|\n\|---(?:\|---)*\|\n)(\|[^\n]*\|\n)+",
+             lambda mo: mo.group(1) + "\n".join(main) + "\n", design)
+design = sub(r"(\| model \| box \| atoms \| steps/s \| ms/step \| roofline \(dominant kernel\) \| round 1 steps/s \|\n\|---(?:\|---)*\|\n)(\|[^\n]*\|\n)+",
+             lambda mo: mo.group(1) + "\n".join(rep) + "\n", design)
+open(P("DESIGN.md"), "w").write(design)
+
+readme = open(P("README.md")).read()
+readme = sub(r"^\| DPA3 \| [0-9.]+ k steps/s \| .*$",
+             f"| DPA3 | {d['value']/1e3:.1f} k steps/s | {d['e2e']['value']/1e3:.1f} k | {d['cpu_baseline']['value']:.0f} | "
+             f"{d['e2e']['value']/d['cpu_baseline']['value']:.0f}× |", readme)
+readme = sub(r"^\| DPA2 \| [0-9.]+ k steps/s \| .*$",
+             f"| DPA2 | {m2['value']/1e3:.1f} k steps/s | {m2['e2e']['value']/1e3:.1f} k | {m2['cpu_baseline']['value']:.0f} | "
+             f"{m2['e2e']['value']/m2['cpu_baseline']['value']:.0f}× |", readme)
+readme = sub(r"The DPA3 step runs at [0-9]+ % of the FP32 roofline",
+             f"The DPA3 step runs at {st['frac']*100:.0f} % of the FP32 roofline", readme)
+y3 = [l for l in main if l.startswith("| DPA3 | 1YRF")][0].split("|")[4].strip()
+y2 = [l for l in main if l.startswith("| DPA2 | 1YRF")][0].split("|")[4].strip()
+readme = sub(r"On the 1YRF box: DPA3 .* steps/s, DPA2 .*\.$",
+             f"On the 1YRF box: DPA3 {int(y3.replace(' ', ''))/1e3:.1f} k steps/s, "
+             f"DPA2 {int(y2.replace(' ', ''))/1e3:.1f} k.", readme)
+open(P("README.md"), "w").write(readme)
+print("updated DESIGN.md §7 and README.md")
