@@ -38,6 +38,8 @@
 //   F_i = sum_q (gv_q - gv_rev(q)), W_ab = -sum_q d_a gv_b.
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "hmdp_common.cuh"
 
 namespace hmdp {
@@ -584,13 +586,17 @@ __device__ __forceinline__ T* rf_smem_rows() {
     extern __shared__ __align__(16) unsigned char rf_dyn[];
     return reinterpret_cast<T*>(rf_dyn);
 }
-template <typename T>
+// SR (compile time, = DevDpWork::smem_rows): the shared-memory rows, so every access
+// through these pointers compiles to LDS/STS instead of a generic load
+template <typename T, bool SR>
 __device__ __forceinline__ T* rf_rows_qkv(const DevDpWork<T>& dw, int start) {
-    return dw.smem_rows ? rf_smem_rows<T>() : dw.qkv + 96ll * start;
+    if constexpr (SR) return rf_smem_rows<T>();
+    else return dw.qkv + 96ll * start;
 }
-template <typename T>
+template <typename T, bool SR>
 __device__ __forceinline__ T* rf_rows_dob(const DevDpWork<T>& dw, int start) {
-    return dw.smem_rows ? rf_smem_rows<T>() + 96 * kRfSmemRows : dw.dob + 32ll * start;
+    if constexpr (SR) return rf_smem_rows<T>() + 96 * kRfSmemRows;
+    else return dw.dob + 32ll * start;
 }
 
 // Per-edge env row: s, w, h0, h1 | h2, dsw, r, type.
@@ -717,7 +723,7 @@ __global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_embed(DevDp<T> md, DevG
 // row: o_e = sum_f softmax_f(l_ef) w_e w_f (h_e . h_f) v_f into TMP rows; the
 // row max / normaliser go to dw.stat for the backward.
 template <typename T>
-__device__ void rf_attn_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+__device__ __forceinline__ void rf_attn_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
                             T* Q, T* TMP, long long S, int l, int start, int cnt) {
     proj<T, false>(L.q.W, L.q.b, dw.g2 + (long long)l * S * 32 + 32ll * start, 32, nullptr, 0, Q,
                    96, cnt);
@@ -779,7 +785,7 @@ __device__ void rf_attn_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const De
 // m_e = (1/anorm) sum_{f in A(i), f != e} omega_e omega_f tanh(aw c_ef + ab) * v_f
 // into TMP rows (zero for rows outside A(i)).  v rows are in Q + 64.
 template <typename T>
-__device__ void rf_angle_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+__device__ __forceinline__ void rf_angle_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
                              const T* Q, T* TMP, int start, int cnt, const RfSmem<T>& sm) {
     const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
     T aw[8], ab[8];
@@ -815,15 +821,15 @@ __device__ void rf_angle_fwd(const DevDp<T>& md, const DevDpLayer<T>& L, const D
 }
 
 // Layer l forward for the CTA's atom i; returns g1^{l+1}_i in warp 0 (lane = channel).
-template <typename T>
-__device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
+template <typename T, bool SR>
+__device__ __forceinline__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
                           long long S, int n, int l, int i, RfSmem<T>& sm) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const DevDpLayer<T>& L = md.L[l];
     const int start = gr.row_start[i], cnt = gr.nnei[i];
     const T* g2l = dw.g2 + (long long)l * S * 32;
     T* g2n = dw.g2 + (long long)(l + 1) * S * 32;
-    T* Q = rf_rows_qkv(dw, start);
+    T* Q = rf_rows_qkv<T, SR>(dw, start);
     T* TMP = dw.tmp + 96ll * start;
     if (md.family == kRepflow) {
         proj<T, false>(L.v.W, L.v.b, g2l + 32ll * start, 32, nullptr, 0, Q + 64, 96, cnt);
@@ -893,7 +899,7 @@ __device__ T rf_layer_fwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWor
 // (S_e, dq_e, row-side dw/dh), column pass (dk_f, dv_f, column-side dw/dh), then
 // dg2 = dg2hat + Wq^T dq + Wk^T dk + Wv^T dv.
 template <typename T>
-__device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+__device__ __forceinline__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
                             const T* g2l, T* Q, T* DOB, T* TMP, T* DG2, long long S, int l,
                             int start, int cnt, bool have_qkv) {
     // q, k, v (recomputed unless the forward of this layer just left them in Q)
@@ -1040,7 +1046,7 @@ __device__ void rf_attn_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const De
 //   dE/domega_e = sum_f omega_f / anorm sum_c (dm_e v_f + dm_f v_e) z
 // dv rows go to TMP + 64 (zero outside A(i)); (domega, du) accumulate into dua.
 template <typename T>
-__device__ void rf_angle_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
+__device__ __forceinline__ void rf_angle_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const DevDpWork<T>& dw,
                              const T* Q, const T* DOB, T* TMP, int start, int cnt, bool top,
                              const RfSmem<T>& sm) {
     const int rq = threadIdx.x >> 2, p = threadIdx.x & 3;
@@ -1114,8 +1120,8 @@ __device__ void rf_angle_bwd(const DevDp<T>& md, const DevDpLayer<T>& L, const D
 // adjoint of g1^{l+1}_i.  top: no g2 adjoint from above.  Writes dconv (scaled by
 // 1/nnorm) for the neighbours' P gather, the residual part of dg1^l (dw.dg1),
 // dg2 (adjoint of g2^l), and accumulates dwh.
-template <typename T>
-__device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
+template <typename T, bool SR>
+__device__ __forceinline__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDpWork<T>& dw,
                              long long S, int n, int l, int i, T dg1_out, bool top,
                              RfSmem<T>& sm) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1179,8 +1185,8 @@ __device__ void rf_layer_bwd(const DevDp<T>& md, const DevGraph& gr, const DevDp
         }
     }
     __syncthreads();
-    T* Q = rf_rows_qkv(dw, start);
-    T* DOB = rf_rows_dob(dw, start);
+    T* Q = rf_rows_qkv<T, SR>(dw, start);
+    T* DOB = rf_rows_dob<T, SR>(dw, start);
     T* TMP = dw.tmp + 96ll * start;
     T* DG2 = dw.dg2 + 32ll * start;
     if (md.family == kRepflow) {
@@ -1243,7 +1249,7 @@ __device__ __forceinline__ T rf_fit(const DevDp<T>& md, const DevGraph& gr, cons
 }
 
 // Layer l forward (l < L - 1): g1^{l+1}, P^{l+1}.
-template <typename T>
+template <typename T, bool SR>
 __global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_fwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                  DevDpWork<T> dw, int l) {
     __shared__ RfSmem<T> sm;
@@ -1251,7 +1257,7 @@ __global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_fwd(DevDp<T> md, DevGra
     pdl_wait();
     const int n = gr.n;
     for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
-        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, sm);
+        const T g1 = rf_layer_fwd<T, SR>(md, gr, dw, ws.slots, n, l, i, sm);
         if (threadIdx.x < 32)
             dw.P[((long long)(l + 1) * n + i) * 32 + threadIdx.x] =
                 cmv(md.L[l + 1].c.WT, md.L[l + 1].c.b, g1);
@@ -1260,7 +1266,7 @@ __global__ __launch_bounds__(kRfT, kRfMinB<T>) void k_rf_fwd(DevDp<T> md, DevGra
 }
 
 // Top layer forward + fitting + top layer backward (atom-local part).
-template <typename T>
+template <typename T, bool SR>
 __global__ __launch_bounds__(kRfT) void k_rf_top(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                  DevDpWork<T> dw) {
     __shared__ RfSmem<T> sm;
@@ -1268,15 +1274,15 @@ __global__ __launch_bounds__(kRfT) void k_rf_top(DevDp<T> md, DevGraph gr, DevWo
     pdl_wait();
     const int n = gr.n, l = md.n_layers - 1;
     for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
-        const T g1 = rf_layer_fwd(md, gr, dw, ws.slots, n, l, i, sm);
+        const T g1 = rf_layer_fwd<T, SR>(md, gr, dw, ws.slots, n, l, i, sm);
         T dg1 = T(0);
         if (threadIdx.x < 32) dg1 = rf_fit(md, gr, ws, i, g1);
-        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, true, sm);
+        rf_layer_bwd<T, SR>(md, gr, dw, ws.slots, n, l, i, dg1, true, sm);
     }
 }
 
 // Gather for layer l + 1, then layer l backward.
-template <typename T>
+template <typename T, bool SR>
 __global__ __launch_bounds__(kRfT) void k_rf_bwd(DevDp<T> md, DevGraph gr, DevWork<T> ws,
                                                  DevDpWork<T> dw, int l) {
     __shared__ RfSmem<T> sm;
@@ -1285,7 +1291,7 @@ __global__ __launch_bounds__(kRfT) void k_rf_bwd(DevDp<T> md, DevGraph gr, DevWo
     const int n = gr.n;
     for (int i = blockIdx.x; i < gr.n_active; i += gridDim.x) {
         const T dg1 = rf_gather_dg1(md, gr, dw, ws.slots, n, l + 1, i, sm);
-        rf_layer_bwd(md, gr, dw, ws.slots, n, l, i, dg1, false, sm);
+        rf_layer_bwd<T, SR>(md, gr, dw, ws.slots, n, l, i, dg1, false, sm);
     }
 }
 
@@ -1381,9 +1387,9 @@ cudaError_t rf_configure() {
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
     const int bytes = kRfSmemRows * 128 * sizeof(T);
     cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {cudaFuncSetAttribute(k_rf_fwd<T>, a, bytes),
-                          cudaFuncSetAttribute(k_rf_top<T>, a, bytes),
-                          cudaFuncSetAttribute(k_rf_bwd<T>, a, bytes)})
+    for (cudaError_t r : {cudaFuncSetAttribute(k_rf_fwd<T, true>, a, bytes),
+                          cudaFuncSetAttribute(k_rf_top<T, true>, a, bytes),
+                          cudaFuncSetAttribute(k_rf_bwd<T, true>, a, bytes)})
         if (r != cudaSuccess) e = r;
     return e;
 }
@@ -1431,16 +1437,23 @@ int launch_dp(const DevDp<T>& md, const DevGraph& gr, const DevWork<T>& ws,
     const size_t rsm = dws.smem_rows ? size_t(kRfSmemRows) * 128 * sizeof(T) : 0;
     launch_pdl(k_rf_embed<T>, rgrid, rblock, 0, st, md, gr, ws, dw, rev, mf);
     mk("rf_embed", st);
-    for (int l = 0; l + 1 < L; ++l) {
-        launch_pdl(k_rf_fwd<T>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
-        mk("rf_fwd", st);
-    }
-    launch_pdl(k_rf_top<T>, rgrid, rblock, rsm, st, md, g2, ws, dws);
-    mk("rf_top", st);
-    for (int l = L - 2; l >= 0; --l) {
-        launch_pdl(k_rf_bwd<T>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
-        mk("rf_bwd", st);
-    }
+    auto layers = [&](auto sr) {
+        constexpr bool SR = decltype(sr)::value;
+        for (int l = 0; l + 1 < L; ++l) {
+            launch_pdl(k_rf_fwd<T, SR>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
+            mk("rf_fwd", st);
+        }
+        launch_pdl(k_rf_top<T, SR>, rgrid, rblock, rsm, st, md, g2, ws, dws);
+        mk("rf_top", st);
+        for (int l = L - 2; l >= 0; --l) {
+            launch_pdl(k_rf_bwd<T, SR>, rgrid, rblock, rsm, st, md, g2, ws, dws, l);
+            mk("rf_bwd", st);
+        }
+    };
+    if (dws.smem_rows)
+        layers(std::true_type{});
+    else
+        layers(std::false_type{});
     launch_pdl(k_rf_embed_bwd<T>, rgrid, rblock, 0, st, md, g2, ws, dw);
     mk("rf_embed_bwd", st);
     launch_force<T>(g2, ws, forces, per_atom, out, st, mf);
