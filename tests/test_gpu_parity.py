@@ -219,6 +219,27 @@ def test_extensivity_replicated_box(golden_models):
         assert e8 == pytest.approx(8 * e1, rel=1e-12)
 
 
+def test_large_box_paths_agree(golden_models):
+    """Two kernel paths against each other in FP32.
+
+    The 2PTC box (4114 atoms) runs 2-warp teams, the 28-warp-CTA build and the pull
+    backward with stored z rows. Its (2,1,1) periodic replica (8228 atoms) runs
+    1-warp teams and the pull backward with z recomputed (hmdp_net.cu pull_mode).
+    The replica's energy is twice the box's, and each copy's forces equal the box's
+    (FP32 tolerances).
+    """
+    s = P.generate_synthetic_system(4114)
+    r = P.replicate(s, (2, 1, 1))
+    ctx = P.context_for(model(golden_models, "dpa3"))
+    one = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+    two = ctx.compute(r.positions, r.types, r.box, P.Precision.fp32)
+    assert abs(two.energy - 2 * one.energy) <= E_TOL * abs(2 * one.energy)
+    scale = rms(one.forces)
+    for k in range(2):
+        fk = two.forces[k * s.n_atoms:(k + 1) * s.n_atoms]
+        assert np.abs(fk - one.forces).max() <= F_TOL * scale
+
+
 def test_receptive_field_exactness(golden_models):
     """moving an atom beyond depth*rc of atom i leaves E_i bitwise unchanged."""
     s = P.generate_synthetic_system(2643)
