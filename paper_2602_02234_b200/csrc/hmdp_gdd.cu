@@ -274,16 +274,21 @@ __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, 
         const int i = gr.alist[k];
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         const bool own_row = role[i] == 1;
-        for (int q = 0; q < cnt; ++q) {
+        for (int base = 0; base < cnt; base += 32) {  // lane = slot, then the flagged rows
+            const int q = base + lane;
             const long long e = start + q;
-            if (role[gr.nbr[e]] != 1) {
-                if (d) {
-                    d[e * kH + lane] = T(0);
-                    d[(slots + e) * kH + lane] = T(0);
+            const bool flag = q < cnt && role[gr.nbr[e]] != 1;
+            if (flag) grev[e] = T(0);
+            if (!own_row && q < cnt) g[e] = T(0);
+            if (d) {
+                unsigned bal = __ballot_sync(FULL_MASK, flag);
+                while (bal) {
+                    const long long ef = start + base + (__ffs(bal) - 1);
+                    bal &= bal - 1;
+                    d[ef * kH + lane] = T(0);
+                    d[(slots + ef) * kH + lane] = T(0);
                 }
-                if (lane == 0) grev[e] = T(0);
             }
-            if (!own_row && lane == 0) g[e] = T(0);
         }
     }
 }
