@@ -76,7 +76,7 @@ struct GddGeom {
 void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t,
                       const int* = nullptr, const int* = nullptr);
 void launch_gdd_send_lists(const int*, const int*, int, const double*, const GddGeom&, int, int, int,
-                           int*, int*, unsigned*, cudaStream_t);
+                           int*, int*, unsigned*, cudaStream_t, unsigned char* = nullptr);
 template <typename E>
 void launch_gdd_pack(int, int, const int*, const int*, int, const E*, int, const E*, int, char*,
                      size_t, cudaStream_t);
@@ -684,6 +684,7 @@ struct hmdp_ctx {
         long long launches = 0;  // kernels enqueued by hmdp_gdd_phase so far
         GddGeom geom{};
         DBuf role, lists, counts;
+        DBuf bnd;  // [n] 1: owned atom in some peer's halo (the pull form's SUMS receivers)
         double box[3] = {0, 0, 0};
         double* pos = nullptr;   // [n][3] replicated positions
         void* p_atom = nullptr;  // [n][32] T, P rows exchange (sum all-reduce)
@@ -2245,6 +2246,16 @@ int hmdp_dd_result(hmdp_ctx* ctx, double* energy, double* virial9, double* viria
 // Global-index device domain decomposition (hmdp_gdd.cu)
 // ---------------------------------------------------------------------------
 namespace {
+// The halo-exchange engine runs the network's pull form (sender-side message
+// backward, stored z) unless HMDP_DD_PULL=0 selects the push form.
+bool gdd_pull(hmdp_ctx* ctx) {
+    static const bool on = [] {
+        const char* e = std::getenv("HMDP_DD_PULL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on && ctx->gdd.mode == 1 && ctx->n_msg() > 0;
+}
+
 DevGraph gdd_graph(hmdp_ctx* ctx, int list) {  // list 0 owned, 1 halo, 2 searched
     DevGraph gr = ctx->periodic_graph(ctx->gdd.n, ctx->types.as<int>());
     gr.n_active = ctx->gdd.n_est;  // launch sizing only; the loop bound is *alist_n
@@ -2282,6 +2293,7 @@ int hmdp_gdd_setup(hmdp_ctx* ctx, int n, const int* types, const double* box, co
         ctx->ensure_edges(static_cast<long long>(n) * ctx->cap);
         ctx->grid(box, ctx->model.rc, n);  // geometry checks + cell buffers
         g.role.ensure(n);
+        g.bnd.ensure(n);
         g.lists.ensure(3 * static_cast<size_t>(n) * sizeof(int));
         g.counts.ensure(4 * sizeof(int));
         cudaStream_t st = ctx->st();
@@ -2338,12 +2350,18 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
     char* spk = g.spk.as<char>();
     char* rpk = g.rpk.as<char>();
     const int W = g.world, R = g.geom.rank, C = g.C;
+    const bool pull = gdd_pull(ctx);
     auto run = [&](auto tag) {
         using T = decltype(tag);
         DevWork<T> w = ctx->work<T>(n, slots);
         w.p_atom = halo ? nullptr : static_cast<T*>(g.p_atom);
         w.s_remote = halo ? g.sremote.as<T>() : static_cast<T*>(g.sghost);
         T* hsum = halo ? g.hsum.as<T>() : static_cast<T*>(g.sghost);
+        if (pull) {
+            w.dd_role = g.role.as<unsigned char>();
+            w.dd_bnd = g.bnd.as<unsigned char>();
+            w.dd_sum = hsum;
+        }
         const DevModel<T>& md = [&]() -> const DevModel<T>& {
             if constexpr (sizeof(T) == 8) return ctx->wd.dev;
             else return ctx->wf.dev;
@@ -2379,13 +2397,16 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 ctx->cells_owner = nullptr;
                 launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
                 launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
-                                   M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
+                                   M > 0 && !pull ? w.d : nullptr, slots, pull ? nullptr : w.grev,
+                                   w.g, w.e_atom, st);
                 g.launches += 6;  // roles, bin, search, rev, zero, zero_energy
                 if (halo) {  // this step's send lists: owned -> peers' halos, halo -> owners
                     ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
                     ck(cudaMemsetAsync(g.rcnt.p, 0, W * sizeof(int), st), "memset");
+                    if (pull) ck(cudaMemsetAsync(g.bnd.p, 0, n, st), "memset");
                     launch_gdd_send_lists(lists, counts, g.n_est, g.pos, g.geom, W, 0, C,
-                                          g.flist.as<int>(), g.fcnt.as<int>(), err, st);
+                                          g.flist.as<int>(), g.fcnt.as<int>(), err, st,
+                                          pull ? g.bnd.as<unsigned char>() : nullptr);
                     launch_gdd_send_lists(lists + n, counts + 1, g.n_est, g.pos, g.geom, W, 1, C,
                                           g.rlist.as<int>(), g.rcnt.as<int>(), err, st);
                     g.launches += 2;
@@ -2405,10 +2426,16 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 break;
             case 2:
                 if (!halo && layer < M - 1) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
-                launch_dd_phase<T>(md, own, w, 2, layer, nullptr, g.forces, g.out, st);
+                launch_dd_phase<T>(md, own, w, pull ? 12 : 2, layer, nullptr, g.forces, g.out, st);
                 g.launches += 1;
                 break;
             case 3:
+                if (pull) {  // the sender half over owned + halo rows writes every row's sum
+                    launch_dd_phase<T>(md, gdd_graph(ctx, 2), w, 13, layer, nullptr, g.forces,
+                                       g.out, st);
+                    g.launches += 1;
+                    break;
+                }
                 ck(cudaMemsetAsync(hsum, 0, rows, st), "memset");
                 launch_gdd_halo_sums<T>(own, g.n_est, w.d + (layer & 1) * slots * kH, hsum,
                                         lists + n, counts + 1, st);
@@ -2416,11 +2443,12 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 break;
             case 4:
             case 5:
-                launch_dd_phase<T>(md, own, w, phase, layer, nullptr, g.forces, g.out, st);
+                launch_dd_phase<T>(md, own, w, pull ? phase + 10 : phase, layer, nullptr, g.forces,
+                                   g.out, st);
                 g.launches += 1;
                 break;
             case 6:  // forces of every row (halo rows: partials), (E, W, W9) partials
-                launch_dd_phase<T>(md, own, w, 6, 0, nullptr, g.forces, g.out, st);
+                launch_dd_phase<T>(md, own, w, pull ? 16 : 6, 0, nullptr, g.forces, g.out, st);
                 g.launches += 1;
                 break;
             case 7:  // velocity Verlet (halo mode: owned atoms only)

@@ -122,6 +122,11 @@ struct DevWork {
     // domain decomposition (nullable otherwise)
     T* p_atom;    // [n][32] per-atom P of the layer just produced (sent to ghost copies)
     T* s_remote;  // [n][32] adjoint partial sums received from ghost copies elsewhere
+    // halo-exchange DD, pull form (nullable otherwise): roles of the global-index rows
+    // (1 = owned) and the per-row dE/dh partial sums of the sender-side backward
+    const unsigned char* dd_role;
+    const unsigned char* dd_bnd;  // 1: owned row in some peer's halo (receives s_remote)
+    T* dd_sum;  // [n][32]
     // per atom
     T* desc;   // [n][32] descriptor (n_types*8 used)
     T* ez1;    // [n][32] embedding hidden activations

@@ -130,7 +130,7 @@ __host__ __device__ inline size_t gdd_pkt_bytes(int C, int W, int esz) {
 __global__ void k_gdd_send_lists(const int* __restrict__ src, const int* __restrict__ src_n,
                                  const double* __restrict__ pos, GddGeom g, int world, int by_owner,
                                  int C, int* __restrict__ lists, int* __restrict__ counts,
-                                 unsigned* err) {
+                                 unsigned* err, unsigned char* __restrict__ mark) {
     const int ns = *src_n;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += gridDim.x * blockDim.x) {
         const int i = src[k];
@@ -144,6 +144,7 @@ __global__ void k_gdd_send_lists(const int* __restrict__ src, const int* __restr
         } else {
             for (int q = 0; q < world; ++q) {
                 if (q == g.rank || !gdd_near(p, g, q)) continue;
+                if (mark) mark[i] = 1;  // in some peer's halo
                 const int s = atomicAdd(counts + q, 1);
                 if (s < C) lists[q * C + s] = i;
                 else atomicOr(err, kErrHaloOverflow);
@@ -274,12 +275,13 @@ __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, 
         const int i = gr.alist[k];
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         const bool own_row = role[i] == 1;
+        const bool all_g = grev == nullptr;  // pull form: every slot of every searched row
         for (int base = 0; base < cnt; base += 32) {  // lane = slot, then the flagged rows
             const int q = base + lane;
             const long long e = start + q;
             const bool flag = q < cnt && role[gr.nbr[e]] != 1;
-            if (flag) grev[e] = T(0);
-            if (!own_row && q < cnt) g[e] = T(0);
+            if (flag && !all_g) grev[e] = T(0);
+            if ((all_g || !own_row) && q < cnt) g[e] = T(0);
             if (d) {
                 unsigned bal = __ballot_sync(FULL_MASK, flag);
                 while (bal) {
@@ -367,10 +369,10 @@ void launch_gdd_roles(int n, const double* pos, const GddGeom& g, unsigned char*
 }
 void launch_gdd_send_lists(const int* src, const int* src_n, int n_est, const double* pos,
                            const GddGeom& g, int world, int by_owner, int C, int* lists,
-                           int* counts, unsigned* err, cudaStream_t st) {
+                           int* counts, unsigned* err, cudaStream_t st, unsigned char* mark) {
     const int blocks = (n_est + 255) / 256;
     k_gdd_send_lists<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(src, src_n, pos, g, world, by_owner, C,
-                                                              lists, counts, err);
+                                                              lists, counts, err, mark);
 }
 template <typename E>
 void launch_gdd_pack(int world, int rank, const int* lists, const int* counts, int C, const E* src0,

@@ -940,11 +940,17 @@ __device__ __forceinline__ void upd_bwd_pull(const T* uW2T, const T* uW1T, T c1,
 // slot (first_g: the first backward kernel to touch g overwrites it).
 //   z_e  = stored row (PULL 1) | tanh(W1b b_e + b1 + P_k) (PULL 2, pk = P_k[lane])
 //   dz_e = s_e v_i (1 - z_e^2);  dE/dr_e += s'_e (v_i . z_e + c0_i) + b'_e . (W1b^T dz_e)
-template <typename T, int G, int PULL>
+// DD (halo-exchange domain decomposition, PULL = 1): the sender k is any searched
+// row (owned or halo) and only messages into OWNED receivers are this rank's; the
+// others contribute nothing (mask row[3]; their v / z rows are stale and never used).
+// A halo sender's edge scalars were computed by the owned receiver's embedding at
+// the mirror slot (same |r|, bit-identical), so they are read there.
+template <typename T, int G, int PULL, bool DD = false>
 __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T* Z, const T* V,
                                         const T* C0, const DevGraph& gr, const DevWork<T>& ws,
                                         WarpSmem<T>& sm, long long e0, int mloc, bool first_g,
-                                        int lane) {
+                                        int lane, bool own_sender = true) {
+    static_assert(!DD || PULL == 1, "DD pull form: stored z only");
     T sdz = T(0);
     for (int base = 0; base < mloc; base += 32) {
         const int m = min(32, mloc - base);
@@ -954,17 +960,30 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
             const long long e = eb + static_cast<long long>(G) * lane;
             const int nb = gr.nbr[e];
             T* row = sm.ed[lane];
-            row[0] = ws.es[e];
-            row[1] = ws.eds[e];
-            const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
-            st4(row + 4, d0.x, d0.y, d0.z, d0.w);
-            st4(row + 8, d1.x, d1.y, d1.z, d1.w);
-            if constexpr (PULL == 2) {
-                const V4<T> b0 = ld4c(ws.eb + 8 * e), b1 = ld4c(ws.eb + 8 * e + 4);
-                st4(row + 12, b0.x, b0.y, b0.z, b0.w);
-                st4(row + 16, b1.x, b1.y, b1.z, b1.w);
+            if constexpr (DD) {
+                const bool rcv = ws.dd_role[nb] == 1;
+                const long long es = own_sender ? e : static_cast<long long>(gr.inv_pos[e]);
+                const V4<T> d0 = rcv ? ld4c(ws.edb + 8 * es) : V4<T>{},
+                            d1 = rcv ? ld4c(ws.edb + 8 * es + 4) : V4<T>{};
+                row[0] = rcv ? ws.es[es] : T(0);
+                row[1] = rcv ? ws.eds[es] : T(0);
+                row[2] = rcv ? C0[nb] : T(0);
+                row[3] = rcv ? T(1) : T(0);
+                st4(row + 4, d0.x, d0.y, d0.z, d0.w);
+                st4(row + 8, d1.x, d1.y, d1.z, d1.w);
+            } else {
+                row[0] = ws.es[e];
+                row[1] = ws.eds[e];
+                const V4<T> d0 = ld4c(ws.edb + 8 * e), d1 = ld4c(ws.edb + 8 * e + 4);
+                st4(row + 4, d0.x, d0.y, d0.z, d0.w);
+                st4(row + 8, d1.x, d1.y, d1.z, d1.w);
+                if constexpr (PULL == 2) {
+                    const V4<T> b0 = ld4c(ws.eb + 8 * e), b1 = ld4c(ws.eb + 8 * e + 4);
+                    st4(row + 12, b0.x, b0.y, b0.z, b0.w);
+                    st4(row + 16, b1.x, b1.y, b1.z, b1.w);
+                }
+                row[2] = C0[nb];
             }
-            row[2] = C0[nb];
             sm.enb[lane] = nb;
         }
         __syncwarp();
@@ -1018,7 +1037,9 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
                     } else {
                         z = zr[u];
                     }
-                    const T v = vr[u];
+                    T v = vr[u];
+                    if constexpr (DD)
+                        if (row[3] == T(0)) v = z = T(0);  // not this rank's message
                     const T d = s * v * (T(1) - z * z);
                     sdz += d;
                     term[u] = ds * v * z + d * wv;
@@ -1050,7 +1071,6 @@ __device__ __forceinline__ T pull_edges(const T (&w1b)[kK], T mb1, T pk, const T
 template <typename T, int G, bool LAST, bool LIST = false, int PULL = 0, bool WIDE = false>
 __global__ __launch_bounds__((PULL == 0 ? kPushWarps : kCtaWarps<T, G, WIDE>) * 32, kNetMinCTAs<G>) void k_msg_fwd(DevModel<T> md, DevGraph gr,
                                                                DevWork<T> ws, int l) {
-    static_assert(PULL == 0 || !LIST, "pull form needs every atom to run the network");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TP_START;
     pdl_launch_dependents();
@@ -1415,7 +1435,12 @@ __global__ __launch_bounds__(kPushWarps * 32, kNetMinCTAs<G>) void k_embed_bwd(D
 // Pull form, lower layers (l < M-1): the sender-side backward of layer l+1's
 // messages (gathering the receivers' v^{l+1} rows), dE/dh^{l+1}_k, then layer l's
 // update backward (v^l_k, c0^l_k for the next kernel).
-template <typename T, int G, int PULL, bool WIDE = false>
+//
+// DD (halo-exchange domain decomposition, alist-driven): 1 = the sender-side half
+// over the searched rows (owned + halo), dE/dh partial sums into ws.dd_sum (the
+// halo rows' travel to their owners in the SUMS round); 2 = the update half over
+// the owned rows, from dd_sum + s_remote.
+template <typename T, int G, int PULL, bool WIDE = false, int DD = 0>
 __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_msg_bwd_pull(DevModel<T> md,
                                                                     DevGraph gr, DevWork<T> ws,
                                                                     int l) {
@@ -1442,16 +1467,36 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     const T* Z = ws.z + static_cast<long long>(l + 1) * ws.slots * kH;
     const T* V = ws.vrow + static_cast<long long>((l + 1) & 1) * n * kH;
     const T* C0 = ws.vc0 + static_cast<long long>((l + 1) & 1) * n;
-    const bool first_g = l == md.n_msg - 2;
-    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
-        AtomRow<G> ar(gr, k, tm);
+    const bool first_g = DD == 0 && l == md.n_msg - 2;  // DD: g zeroed by k_gdd_zero
+    const int n_run = DD ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int k = DD ? gr.alist[k_at] : k_at;
+        if (DD == 2 && !ws.dd_bnd[k]) continue;  // finished by the sender half
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T zu = ws.uz1[(static_cast<long long>(l) * n + k) * kH + lane];
-        const T pk = PULL == 2 ? ws.pa[(static_cast<long long>(l + 1) * n + k) * kH + lane] : T(0);
-        const int mloc = ar.finish(tm);
-        T sdz = pull_edges<T, G, PULL>(w1b, mb1n, pk, Z, V, C0, gr, ws, sm, ar.e0, mloc, first_g,
-                                       lane);
-        sdz = tm.sum(sdz, sm);
+        T sdz;
+        if constexpr (DD == 2) {
+            sdz = ws.dd_sum[static_cast<long long>(k) * kH + lane] +
+                  ws.s_remote[static_cast<long long>(k) * kH + lane];
+        } else {
+            AtomRow<G> ar(gr, k, tm);
+            const T pk =
+                PULL == 2 ? ws.pa[(static_cast<long long>(l + 1) * n + k) * kH + lane] : T(0);
+            const int mloc = ar.finish(tm);
+            sdz = pull_edges<T, G, PULL, DD == 1>(w1b, mb1n, pk, Z, V, C0, gr, ws, sm, ar.e0, mloc,
+                                                  first_g, lane,
+                                                  DD == 0 || ws.dd_role[k] == 1);
+            sdz = tm.sum(sdz, sm);
+            if constexpr (DD == 1) {
+                // owned rows no peer sends partial sums to are finished here; the
+                // rest wait for the SUMS round (DD = 2)
+                if (ws.dd_role[k] != 1 || ws.dd_bnd[k]) {
+                    if (tm.w == 0) ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                    __syncwarp();
+                    continue;
+                }
+            }
+        }
         if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
             Smem<T>::wait(&s_mbar);
             staged = true;
@@ -1469,7 +1514,9 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
 // Pull form, embedding backward: the sender-side backward of layer 0's messages,
 // dE/dh^0_k, the embedding backward and the descriptor adjoint; pushes the final
 // g to the mirrors for the force gather.
-template <typename T, int G, int PULL, bool WIDE = false>
+// DD: as k_msg_bwd_pull (1 = sender half over the searched rows, 2 = the rest over
+// the owned rows; the force kernel then gathers the mirror g itself, no grev).
+template <typename T, int G, int PULL, bool WIDE = false, int DD = 0>
 __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_embed_bwd_pull(DevModel<T> md,
                                                                       DevGraph gr,
                                                                       DevWork<T> ws) {
@@ -1493,16 +1540,35 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     bool staged = false;
     pdl_wait();
     const int n = gr.n;
-    const bool first_g = md.n_msg == 1;
-    for (int k = tm.first; k < gr.n_active; k += tm.stride) {
+    const bool first_g = DD == 0 && md.n_msg == 1;  // DD: g zeroed by k_gdd_zero
+    const int n_run = DD ? *gr.alist_n : gr.n_active;
+    for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
+        const int k = DD ? gr.alist[k_at] : k_at;
+        if (DD == 2 && !ws.dd_bnd[k]) continue;  // finished by the sender half
         AtomRow<G> ar(gr, k, tm);
         const T own = ws.dhown[static_cast<long long>(k) * kH + lane];
         const T z1 = ws.ez1[static_cast<long long>(k) * kH + lane];
-        const T pk = PULL == 2 ? ws.pa[static_cast<long long>(k) * kH + lane] : T(0);
         const int mloc = ar.finish(tm);
-        T sdz = pull_edges<T, G, PULL>(w1b, mb1, pk, ws.z, ws.vrow, ws.vc0, gr, ws, sm, ar.e0,
-                                       mloc, first_g, lane);
-        sdz = tm.sum(sdz, sm);
+        T sdz;
+        if constexpr (DD == 2) {
+            sdz = ws.dd_sum[static_cast<long long>(k) * kH + lane] +
+                  ws.s_remote[static_cast<long long>(k) * kH + lane];
+        } else {
+            const T pk = PULL == 2 ? ws.pa[static_cast<long long>(k) * kH + lane] : T(0);
+            sdz = pull_edges<T, G, PULL, DD == 1>(w1b, mb1, pk, ws.z, ws.vrow, ws.vc0, gr, ws, sm,
+                                                  ar.e0, mloc, first_g, lane,
+                                                  DD == 0 || ws.dd_role[k] == 1);
+            sdz = tm.sum(sdz, sm);
+            if constexpr (DD == 1) {
+                // owned rows no peer sends partial sums to are finished here; the
+                // rest wait for the SUMS round (DD = 2)
+                if (ws.dd_role[k] != 1 || ws.dd_bnd[k]) {
+                    if (tm.w == 0) ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                    __syncwarp();
+                    continue;
+                }
+            }
+        }
         if (!staged) {  // weights (bulk copy issued at kernel entry) needed from here on
             Smem<T>::wait(&s_mbar);
             staged = true;
@@ -1534,7 +1600,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
             acc += dv[7] * d1.w;
             const T gv = ws.g[e] + acc;
             ws.g[e] = gv;
-            ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
+            if constexpr (DD == 0) ws.grev[gr.inv_pos[e]] = gv;  // mirror for the force gather
         }
         __syncwarp();
     }
@@ -1633,8 +1699,15 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
             for (int q = sub; q < cnt; q += FG) {
                 const int e = start + q;
                 const T gg = ws.g[e];
-                const T gm = gr.sym ? (ws.gather_mirror_g ? ws.g[gr.inv_pos[e]] : ws.grev[e])
-                                    : T(0);
+                T gm = T(0);
+                if (gr.sym) {
+                    if (ws.gather_mirror_g) {
+                        const int mq = gr.inv_pos[e];
+                        if (mq >= 0) gm = ws.g[mq];
+                    } else {
+                        gm = ws.grev[e];
+                    }
+                }
                 T x, y, z;
                 const double* d = gr.dr + 3ll * e;
                 const T r = edge_len<T>(d, x, y, z);
@@ -1999,9 +2072,19 @@ struct Net {
                                   cudaFuncSetAttribute(k_embed<T, G, false, LIST, true>, a, kMaxSmem),
                                   configure_p<0>()})
                 if (r != cudaSuccess) e = r;
-            if constexpr (!LIST)
+            if constexpr (!LIST) {
                 for (cudaError_t r : {configure_p<1>(), configure_p<2>()})
                     if (r != cudaSuccess) e = r;
+            } else {  // the halo-exchange DD's pull form
+                for (cudaError_t r :
+                     {cudaFuncSetAttribute(k_msg_fwd<T, G, true, true, 1>, a, kMaxSmem),
+                      cudaFuncSetAttribute(k_msg_fwd<T, G, false, true, 1>, a, kMaxSmem),
+                      cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1, false, 1>, a, kMaxSmem),
+                      cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1, false, 2>, a, kMaxSmem),
+                      cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1, false, 1>, a, kMaxSmem),
+                      cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1, false, 2>, a, kMaxSmem)})
+                    if (r != cudaSuccess) e = r;
+            }
             return e;
         }
     }
@@ -2099,6 +2182,27 @@ struct Net {
             case 4: msg_bwd<0>(sh, md, gr, ws, l, st); break;
             case 5: embed_bwd<0>(sh, md, gr, ws, st); break;
         }
+        if constexpr (LIST) {  // halo-exchange DD, pull form (stored z)
+            switch (phase) {
+                case 12: msg_fwd<1>(sh, md, gr, ws, l, st); break;
+                case 13:  // sender half of layer l's backward over the searched rows
+                    if (l > 0)
+                        launch_net<T>(k_msg_bwd_pull<T, G, 1, false, 1>, Phase::MsgBwd, sh, st, md,
+                                      gr, ws, l - 1);
+                    else
+                        launch_net<T>(k_embed_bwd_pull<T, G, 1, false, 1>, Phase::EmbedBwd, sh, st,
+                                      md, gr, ws);
+                    break;
+                case 14:  // layer l's update backward over the owned rows
+                    launch_net<T>(k_msg_bwd_pull<T, G, 1, false, 2>, Phase::MsgBwd, sh, st, md, gr,
+                                  ws, l);
+                    break;
+                case 15:
+                    launch_net<T>(k_embed_bwd_pull<T, G, 1, false, 2>, Phase::EmbedBwd, sh, st, md,
+                                  gr, ws);
+                    break;
+            }
+        }
     }
 };
 
@@ -2170,8 +2274,9 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
+    // the pull-form phases (12-15) take the pull form's CTA shape
     const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), false,
-                                  md.n_msg > 0);
+                                  md.n_msg > 0 && !(phase >= 12 && phase <= 15));
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:
@@ -2187,6 +2292,12 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
         case 6:
             launch_force_k<T>(gr, ws, forces, static_cast<double*>(nullptr), out, st, MdFuse{});
             break;
+        case 16: {  // pull form: each pair's terms sit at either end; gather the mirror g
+            DevWork<T> wf = ws;
+            wf.gather_mirror_g = 1;
+            launch_force_k<T>(gr, wf, forces, static_cast<double*>(nullptr), out, st, MdFuse{});
+            break;
+        }
         default:
             if (gr.alist) {  // global-index DD: the owned-atom list variants
                 if (sh.G == 4)

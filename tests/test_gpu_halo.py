@@ -107,6 +107,56 @@ def test_halo_dd_md_matches_device_md(mname, golden_models):
     hub.close()
 
 
+_PUSH_FORM = r"""
+import json, sys
+import numpy as np
+import paper_2602_02234_b200 as P
+from paper_2602_02234_b200 import dd
+m = P.model_from_json(json.load(open(sys.argv[1]))[sys.argv[2]])
+s = P.generate_synthetic_system(1231)
+ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+dims = (2, 2, 1)
+hub = dd.Hub(4)
+engs = [dd.HaloDD(P.Context(m, max_atoms=s.n_atoms), s.n_atoms, s.types, s.box, dims, r,
+                  P.Precision.fp64) for r in range(4)]
+for e in engs:
+    e.attach_hub(hub.handle)
+    e.load(s.positions)
+dd.run_hub(engs, "eval")
+F = np.full((s.n_atoms, 3), np.nan)
+for e in engs:
+    own, f = e.owned_forces()
+    F[own] = f[own]
+print(json.dumps({"dE": abs(engs[0].energy_virial()[0] - ref.energy) / abs(ref.energy),
+                  "dF": float(np.abs(F - ref.forces).max() / np.abs(ref.forces).max())}))
+hub.close()
+"""
+
+
+@pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
+def test_halo_dd_push_form_matches_single_domain(mname, tmp_path):
+    """The halo engine's push-form network (HMDP_DD_PULL=0: receivers push per-edge
+    adjoint rows, halo sums gathered from them) stays equal to the single domain
+    beside the default pull form (senders pull the owned receivers' v rows)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import GOLDEN
+
+    script = tmp_path / "push_form.py"
+    script.write_text(_PUSH_FORM)
+    env = dict(os.environ, HMDP_DD_PULL="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env["PYTHONPATH"] = root + os.pathsep + env.get("PYTHONPATH", "")
+    out = subprocess.run([sys.executable, str(script), os.path.join(GOLDEN, "models.json"), mname],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["dE"] < 1e-12 and r["dF"] < 1e-10
+
+
 def _gloo_worker(rank, world, port, model_json, q):
     import os
 
