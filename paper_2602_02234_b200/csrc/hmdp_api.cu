@@ -76,7 +76,8 @@ struct GddGeom {
 void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t,
                       const int* = nullptr, const int* = nullptr);
 void launch_gdd_send_lists(const int*, const int*, int, const double*, const GddGeom&, int, int, int,
-                           int*, int*, unsigned*, cudaStream_t, unsigned char* = nullptr);
+                           int*, int*, unsigned*, cudaStream_t, unsigned char* = nullptr,
+                           int* = nullptr);
 template <typename E>
 void launch_gdd_pack(int, int, const int*, const int*, int, const E*, int, const E*, int, char*,
                      size_t, cudaStream_t);
@@ -85,7 +86,6 @@ void launch_gdd_unpack_copy(int, int, int, const char*, size_t, E*, int, E*, int
                             cudaStream_t);
 template <typename E>
 void launch_gdd_unpack_add(int, int, int, const char*, size_t, E*, int, cudaStream_t);
-void launch_gdd_tick(int*, cudaStream_t);
 void launch_gdd_gather_list(int, int, const int*, const int*, int, int*, int*, unsigned*,
                             cudaStream_t);
 template <typename E>
@@ -123,7 +123,7 @@ void launch_ff(const FfDev&, const DevGraph&, const double*, double*, double*, d
 void launch_gdd_rev(const DevGraph&, int, int*, cudaStream_t);
 template <typename T>
 void launch_gdd_zero(const DevGraph&, int, const unsigned char*, T*, long long, T*, T*, double*,
-                     cudaStream_t);
+                     cudaStream_t, int* = nullptr);
 template <typename T>
 void launch_gdd_push_halo(const DevGraph&, int, const T*, T*, const int*, const int*, cudaStream_t);
 template <typename T>
@@ -2395,11 +2395,13 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                                   ctx->dr.as<double>(), ctx->types.as<int>(), ctx->ety.as<int>(),
                                   err, st, srch.alist, srch.alist_n);
                 ctx->cells_owner = nullptr;
-                launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
+                // mirror slots: a kernel of their own (push form), or set by the owned
+                // atoms' embedding with the halo-halo ones cleared here (pull form)
+                if (!pull) launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
                 launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
                                    M > 0 && !pull ? w.d : nullptr, slots, pull ? nullptr : w.grev,
-                                   w.g, w.e_atom, st);
-                g.launches += 6;  // roles, bin, search, rev, zero, zero_energy
+                                   w.g, w.e_atom, st, pull ? ctx->rev.as<int>() : nullptr);
+                g.launches += pull ? 4 : 5;  // roles, bin, search, [rev,] zero
                 if (halo) {  // this step's send lists: owned -> peers' halos, halo -> owners
                     ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
                     ck(cudaMemsetAsync(g.rcnt.p, 0, W * sizeof(int), st), "memset");
@@ -2415,7 +2417,8 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
             }
             case 0:
                 if (!halo) ck(cudaMemsetAsync(g.p_atom, 0, rows, st), "memset");
-                launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st);
+                launch_dd_phase<T>(md, own, w, 0, 0, nullptr, g.forces, g.out, st,
+                                   pull ? ctx->rev.as<int>() : nullptr);
                 g.launches += 1;
                 break;
             case 1:
@@ -2460,13 +2463,13 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 break;
             // ---- halo-exchange mode ----
             case 20:  // POS send lists (owned after the drift, near each peer) + pack (x, v)
-                launch_gdd_tick(g.cur.as<int>(), st);
                 ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
                 launch_gdd_send_lists(lists, counts, g.n_est, g.pos, g.geom, W, 0, C,
-                                      g.flist.as<int>(), g.fcnt.as<int>(), err, st);
+                                      g.flist.as<int>(), g.fcnt.as<int>(), err, st, nullptr,
+                                      g.cur.as<int>());  // + the step's stamp tick
                 launch_gdd_pack<double>(W, R, g.flist.as<int>(), g.fcnt.as<int>(), C, g.pos, 3,
                                         g.vel, g.vel ? 3 : 0, spk, g.stride, st);
-                g.launches += 3;
+                g.launches += 2;
                 break;
             case 21:  // unpack POS: received atoms become current for this step
                 launch_gdd_unpack_copy<double>(W, R, C, rpk, g.stride, g.pos, 3, g.vel,

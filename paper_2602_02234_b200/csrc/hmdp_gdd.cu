@@ -130,7 +130,8 @@ __host__ __device__ inline size_t gdd_pkt_bytes(int C, int W, int esz) {
 __global__ void k_gdd_send_lists(const int* __restrict__ src, const int* __restrict__ src_n,
                                  const double* __restrict__ pos, GddGeom g, int world, int by_owner,
                                  int C, int* __restrict__ lists, int* __restrict__ counts,
-                                 unsigned* err, unsigned char* __restrict__ mark) {
+                                 unsigned* err, unsigned char* __restrict__ mark, int* tick) {
+    if (tick && blockIdx.x == 0 && threadIdx.x == 0) *tick += 1;  // the POS round's new stamp
     const int ns = *src_n;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += gridDim.x * blockDim.x) {
         const int i = src[k];
@@ -218,8 +219,6 @@ __global__ void k_gdd_unpack_add(int q, int C, const char* __restrict__ pkts, si
     }
 }
 
-__global__ void k_gdd_tick(int* cur) { *cur += 1; }
-
 // OUT round: (E, W, W9) partials into every peer's packet slot; the totals are the
 // rank-ordered sum of all ranks' partials (own partial read from `out` itself), so
 // every rank ends with bitwise the same totals.
@@ -266,7 +265,11 @@ __global__ void k_gdd_rev(DevGraph gr, int* __restrict__ rev) {
 // Zero what no kernel on this rank will write this step (one warp per searched atom).
 template <typename T>
 __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, T* __restrict__ d,
-                           long long slots, T* __restrict__ grev, T* __restrict__ g) {
+                           long long slots, T* __restrict__ grev, T* __restrict__ g,
+                           int* __restrict__ rev, double* __restrict__ e_atom) {
+    // per-atom energies of every row this rank does not own
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < gr.n; i += gridDim.x * blockDim.x)
+        if (role[i] != 1) e_atom[i] = 0.0;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -281,6 +284,9 @@ __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, 
             const long long e = start + q;
             const bool flag = q < cnt && role[gr.nbr[e]] != 1;
             if (flag && !all_g) grev[e] = T(0);
+            // pull form: the embedding sets the mirrors of every pair with an owned atom;
+            // halo-halo pairs have none (their g is zero at both ends)
+            if (rev && flag && !own_row) rev[e] = -1;
             if ((all_g || !own_row) && q < cnt) g[e] = T(0);
             if (d) {
                 unsigned bal = __ballot_sync(FULL_MASK, flag);
@@ -293,12 +299,6 @@ __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, 
             }
         }
     }
-}
-
-__global__ void k_gdd_zero_energy(int n, const unsigned char* __restrict__ role,
-                                  double* __restrict__ e_atom) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && role[i] != 1) e_atom[i] = 0.0;
 }
 
 // Halo atoms take the P rows received from their owners into the layer's per-atom
@@ -369,10 +369,11 @@ void launch_gdd_roles(int n, const double* pos, const GddGeom& g, unsigned char*
 }
 void launch_gdd_send_lists(const int* src, const int* src_n, int n_est, const double* pos,
                            const GddGeom& g, int world, int by_owner, int C, int* lists,
-                           int* counts, unsigned* err, cudaStream_t st, unsigned char* mark) {
+                           int* counts, unsigned* err, cudaStream_t st, unsigned char* mark,
+                           int* tick) {
     const int blocks = (n_est + 255) / 256;
     k_gdd_send_lists<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(src, src_n, pos, g, world, by_owner, C,
-                                                              lists, counts, err, mark);
+                                                              lists, counts, err, mark, tick);
 }
 template <typename E>
 void launch_gdd_pack(int world, int rank, const int* lists, const int* counts, int C, const E* src0,
@@ -399,7 +400,6 @@ void launch_gdd_unpack_add(int world, int rank, int C, const char* pkts, size_t 
             k_gdd_unpack_add<E><<<bx < 1 ? 1 : (bx > 64 ? 64 : bx), 256, 0, st>>>(q, C, pkts,
                                                                               pkt_bytes, dst, W);
 }
-void launch_gdd_tick(int* cur, cudaStream_t st) { k_gdd_tick<<<1, 1, 0, st>>>(cur); }
 void launch_gdd_out_pack(int world, int rank, const double* out, char* pkts, size_t stride,
                          cudaStream_t st) {
     k_gdd_out_pack<<<world, 32, 0, st>>>(world, rank, out, pkts, stride);
@@ -420,9 +420,8 @@ void launch_gdd_rev(const DevGraph& gr, int n_est, int* rev, cudaStream_t st) {
 }
 template <typename T>
 void launch_gdd_zero(const DevGraph& gr, int n_est, const unsigned char* role, T* d,
-                     long long slots, T* grev, T* g, double* e_atom, cudaStream_t st) {
-    k_gdd_zero<T><<<warp_grid(n_est), 256, 0, st>>>(gr, role, d, slots, grev, g);
-    k_gdd_zero_energy<<<(gr.n + 255) / 256, 256, 0, st>>>(gr.n, role, e_atom);
+                     long long slots, T* grev, T* g, double* e_atom, cudaStream_t st, int* rev) {
+    k_gdd_zero<T><<<warp_grid(n_est), 256, 0, st>>>(gr, role, d, slots, grev, g, rev, e_atom);
 }
 template <typename T>
 void launch_gdd_push_halo(const DevGraph& gr, int n_est, const T* p_atom, T* pe,
@@ -443,7 +442,7 @@ void launch_gdd_integrate(int n, const double* f, double* x, double* v, const do
 
 #define HMDP_GDD_INST(T)                                                                       \
     template void launch_gdd_zero<T>(const DevGraph&, int, const unsigned char*, T*, long long, \
-                                     T*, T*, double*, cudaStream_t);                            \
+                                     T*, T*, double*, cudaStream_t, int*);                      \
     template void launch_gdd_push_halo<T>(const DevGraph&, int, const T*, T*, const int*,       \
                                           const int*, cudaStream_t);                            \
     template void launch_gdd_halo_sums<T>(const DevGraph&, int, const T*, T*, const int*,       \

@@ -549,8 +549,11 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 // both rev(e) and rev(rev(e)) = e; the others are set by their j.  Lane
                 // l reads entry l of each neighbour's list (one memory latency per 8
                 // edges); a ballot finds i.  rev is read only by later kernels.
-                const bool up = lane < m && j > i;
-                const int lo_lane = __popc(__ballot_sync(FULL_MASK, lane < m && !up));
+                // (pull-form DD, ws.dd_role set: an owned atom also searches for its
+                // halo neighbours, which run no embedding here)
+                const bool up = lane < m && (j > i || (ws.dd_role && ws.dd_role[j] != 1));
+                const unsigned upb = __ballot_sync(FULL_MASK, up);
+                const int lo_lane = upb ? __ffs(upb) - 1 : m;
                 const int rs_l = up ? gr.row_start[j] : 0;
                 const int nn_l = up ? gr.nnei[j] : 0;
                 int found = -1;
@@ -2274,9 +2277,9 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
-    // the pull-form phases (12-15) take the pull form's CTA shape
+    // the pull-form DD (ws.dd_role set) takes the pull form's CTA shape
     const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), false,
-                                  md.n_msg > 0 && !(phase >= 12 && phase <= 15));
+                                  md.n_msg > 0 && !ws.dd_role);
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:

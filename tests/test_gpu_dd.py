@@ -81,8 +81,8 @@ def test_device_dd_md_matches_device_md(golden_models):
     for step in range(5):
         l0 = engs[0].launches()
         run_local(engs, "md", 0.001)
-        # roles/bin/search/rev/zero x2, embed, (push, fwd) x2, (sums, bwd) x2, force, integrate
-        assert engs[0].launches() - l0 == 17
+        # roles/bin/search/rev/zero, embed, (push, fwd) x2, (sums, bwd) x2, force, integrate
+        assert engs[0].launches() - l0 == 16
     x = engs[0].pos.cpu().numpy()
     assert np.abs(x - engs[1].pos.cpu().numpy()).max() == 0.0  # replicated state
     # DeviceMD's state is the completed step (x(t), v(t)); the DD engines hold the
