@@ -73,11 +73,22 @@ struct GddGeom {
     int rank;
     double halo;
 };
+// Buffers the roles kernel clears on the way (phase 10's former memset nodes):
+// up to four int ranges and one byte range, nullable.
+struct GddZero {
+    int* i32[4];
+    int n32[4];
+    unsigned char* u8;
+    int n8;
+};
 void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t,
-                      const int* = nullptr, const int* = nullptr);
+                      const int* = nullptr, const int* = nullptr, const GddZero* = nullptr);
 void launch_gdd_send_lists(const int*, const int*, int, const double*, const GddGeom&, int, int, int,
                            int*, int*, unsigned*, cudaStream_t, unsigned char* = nullptr,
                            int* = nullptr);
+void launch_gdd_send_lists2(const int*, const int*, const int*, const int*, int, const double*,
+                            const GddGeom&, int, int, int*, int*, int*, int*, unsigned*,
+                            unsigned char*, cudaStream_t);
 template <typename E>
 void launch_gdd_pack(int, int, const int*, const int*, int, const E*, int, const E*, int, char*,
                      size_t, cudaStream_t);
@@ -2372,11 +2383,27 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
         switch (phase) {
             case 10: {  // roles, neighbour list of owned + halo atoms, mirrors, zeroing
                 ck(cudaMemsetAsync(g.counts.p, 0, 4 * sizeof(int), st), "memset");
-                launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), lists, counts, st,
-                                 halo ? g.stamp.as<int>() : nullptr, halo ? g.cur.as<int>() : nullptr);
                 const CellGrid cg = ctx->grid(g.box, ctx->model.rc, n);
-                ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
-                   "memset cells");
+                // the roles kernel also clears the cell counts, the neighbour counts
+                // and (halo mode) the send-list counts and boundary marks
+                GddZero zr{};
+                zr.i32[0] = ctx->cell_count.as<int>();
+                zr.n32[0] = static_cast<int>(hmdp_ctx::ncells(cg));
+                zr.i32[1] = ctx->nnei.as<int>();
+                zr.n32[1] = n;
+                if (halo) {
+                    zr.i32[2] = g.fcnt.as<int>();
+                    zr.n32[2] = W;
+                    zr.i32[3] = g.rcnt.as<int>();
+                    zr.n32[3] = W;
+                    if (pull) {
+                        zr.u8 = g.bnd.as<unsigned char>();
+                        zr.n8 = n;
+                    }
+                }
+                launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), lists, counts, st,
+                                 halo ? g.stamp.as<int>() : nullptr, halo ? g.cur.as<int>() : nullptr,
+                                 &zr);
                 ctx->cells_zero = false;
                 if (halo)  // only the current rows (owned + halo); the rest are stale
                     launch_cell_bin_list(lists + 2 * static_cast<size_t>(n), counts + 2,
@@ -2386,7 +2413,6 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 else
                     launch_cell_bin(n, g.pos, cg, ctx->cell_count.as<int>(), ctx->members.as<int>(),
                                     ctx->cell_of.as<int>(), err, st);
-                ck(cudaMemsetAsync(ctx->nnei.p, 0, n * sizeof(int), st), "memset nnei");
                 const DevGraph srch = gdd_graph(ctx, 2);
                 launch_nbr_search(std::min(n, 2 * g.n_est), g.pos, cg, ctx->cell_count.as<int>(),
                                   ctx->members.as<int>(), ctx->cell_of.as<int>(),
@@ -2403,15 +2429,11 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                                    w.g, w.e_atom, st, pull ? ctx->rev.as<int>() : nullptr);
                 g.launches += pull ? 4 : 5;  // roles, bin, search, [rev,] zero
                 if (halo) {  // this step's send lists: owned -> peers' halos, halo -> owners
-                    ck(cudaMemsetAsync(g.fcnt.p, 0, W * sizeof(int), st), "memset");
-                    ck(cudaMemsetAsync(g.rcnt.p, 0, W * sizeof(int), st), "memset");
-                    if (pull) ck(cudaMemsetAsync(g.bnd.p, 0, n, st), "memset");
-                    launch_gdd_send_lists(lists, counts, g.n_est, g.pos, g.geom, W, 0, C,
-                                          g.flist.as<int>(), g.fcnt.as<int>(), err, st,
-                                          pull ? g.bnd.as<unsigned char>() : nullptr);
-                    launch_gdd_send_lists(lists + n, counts + 1, g.n_est, g.pos, g.geom, W, 1, C,
-                                          g.rlist.as<int>(), g.rcnt.as<int>(), err, st);
-                    g.launches += 2;
+                    launch_gdd_send_lists2(lists, counts, lists + n, counts + 1, g.n_est, g.pos,
+                                           g.geom, W, C, g.flist.as<int>(), g.fcnt.as<int>(),
+                                           g.rlist.as<int>(), g.rcnt.as<int>(), err,
+                                           pull ? g.bnd.as<unsigned char>() : nullptr, st);
+                    g.launches += 1;
                 }
                 break;
             }
@@ -2495,7 +2517,8 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                 g.launches += 1;
                 break;
             case 25:  // owners: s_remote = sum over peers (rank order)
-                ck(cudaMemsetAsync(g.sremote.p, 0, rows, st), "memset");
+                // (pull form: the sender half zeroed the boundary rows, the only ones read)
+                if (!pull) ck(cudaMemsetAsync(g.sremote.p, 0, rows, st), "memset");
                 launch_gdd_unpack_add<T>(W, R, C, rpk, g.stride, g.sremote.as<T>(), kH, st);
                 g.launches += W - 1;
                 break;

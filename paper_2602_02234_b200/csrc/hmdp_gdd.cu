@@ -47,6 +47,15 @@ struct GddGeom {
     double halo;   // halo width (rc)
 };
 
+// Buffers the roles kernel clears on the way (phase 10's former memset nodes):
+// up to four int ranges and one byte range, nullable.
+struct GddZero {
+    int* i32[4];
+    int n32[4];
+    unsigned char* u8;
+    int n8;
+};
+
 // Wrapped coordinate (wrap_position, box.hpp:34-42, as dd.owners).
 __device__ __forceinline__ double gdd_wrap(double r, double L) {
     r = r - L * floor(r / L);
@@ -97,8 +106,15 @@ __device__ __forceinline__ bool gdd_near(const double* p, const GddGeom& g, int 
 __global__ void k_gdd_roles(int n, const double* __restrict__ pos, GddGeom g,
                             unsigned char* __restrict__ role, int* __restrict__ lists,
                             int* __restrict__ counts, const int* __restrict__ stamp,
-                            const int* __restrict__ cur) {
+                            const int* __restrict__ cur, GddZero z) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nt = gridDim.x * blockDim.x;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (z.i32[r])
+            for (int t = i; t < z.n32[r]; t += nt) z.i32[r][t] = 0;
+    if (z.u8)
+        for (int t = i; t < z.n8; t += nt) z.u8[t] = 0;
     if (i >= n) return;
     if (stamp && role[i] != 1 && stamp[i] != *cur) {
         role[i] = 0;
@@ -126,28 +142,37 @@ __host__ __device__ inline size_t gdd_pkt_bytes(int C, int W, int esz) {
 
 // send lists: src atoms (a list) that are near peer q's region, for every q != rank
 // (forward rounds: owned atoms -> the peers whose halo they are in), or grouped by
-// owner (reverse rounds: halo atoms -> their owners, by_owner = 1).
-__global__ void k_gdd_send_lists(const int* __restrict__ src, const int* __restrict__ src_n,
-                                 const double* __restrict__ pos, GddGeom g, int world, int by_owner,
-                                 int C, int* __restrict__ lists, int* __restrict__ counts,
-                                 unsigned* err, unsigned char* __restrict__ mark, int* tick) {
-    if (tick && blockIdx.x == 0 && threadIdx.x == 0) *tick += 1;  // the POS round's new stamp
-    const int ns = *src_n;
+// owner (reverse rounds: halo atoms -> their owners, by_owner = 1).  blockIdx.y
+// selects one of two sets (phase 10 builds both directions in one launch).
+struct SendSet {
+    const int* src;
+    const int* src_n;
+    int by_owner;
+    int* lists;
+    int* counts;
+    unsigned char* mark;  // forward: 1 for every atom in some peer's halo (nullable)
+};
+__global__ void k_gdd_send_lists(SendSet s0, SendSet s1, const double* __restrict__ pos, GddGeom g,
+                                 int world, int C, unsigned* err, int* tick) {
+    if (tick && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        *tick += 1;  // the POS round's new stamp
+    const SendSet& ss = blockIdx.y ? s1 : s0;
+    const int ns = *ss.src_n;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += gridDim.x * blockDim.x) {
-        const int i = src[k];
+        const int i = ss.src[k];
         const double* p = pos + 3 * i;
-        if (by_owner) {
+        if (ss.by_owner) {
             const int q = gdd_owner(p, g);
             if (q == g.rank) continue;
-            const int s = atomicAdd(counts + q, 1);
-            if (s < C) lists[q * C + s] = i;
+            const int s = atomicAdd(ss.counts + q, 1);
+            if (s < C) ss.lists[q * C + s] = i;
             else atomicOr(err, kErrHaloOverflow);
         } else {
             for (int q = 0; q < world; ++q) {
                 if (q == g.rank || !gdd_near(p, g, q)) continue;
-                if (mark) mark[i] = 1;  // in some peer's halo
-                const int s = atomicAdd(counts + q, 1);
-                if (s < C) lists[q * C + s] = i;
+                if (ss.mark) ss.mark[i] = 1;
+                const int s = atomicAdd(ss.counts + q, 1);
+                if (s < C) ss.lists[q * C + s] = i;
                 else atomicOr(err, kErrHaloOverflow);
             }
         }
@@ -364,16 +389,29 @@ __global__ void k_gdd_integrate(int n, const double* __restrict__ f, double* __r
 }
 
 void launch_gdd_roles(int n, const double* pos, const GddGeom& g, unsigned char* role, int* lists,
-                      int* counts, cudaStream_t st, const int* stamp, const int* cur) {
-    k_gdd_roles<<<(n + 255) / 256, 256, 0, st>>>(n, pos, g, role, lists, counts, stamp, cur);
+                      int* counts, cudaStream_t st, const int* stamp, const int* cur,
+                      const GddZero* zero) {
+    k_gdd_roles<<<(n + 255) / 256, 256, 0, st>>>(n, pos, g, role, lists, counts, stamp, cur,
+                                                 zero ? *zero : GddZero{});
 }
 void launch_gdd_send_lists(const int* src, const int* src_n, int n_est, const double* pos,
                            const GddGeom& g, int world, int by_owner, int C, int* lists,
                            int* counts, unsigned* err, cudaStream_t st, unsigned char* mark,
                            int* tick) {
     const int blocks = (n_est + 255) / 256;
-    k_gdd_send_lists<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(src, src_n, pos, g, world, by_owner, C,
-                                                              lists, counts, err, mark, tick);
+    const SendSet s0{src, src_n, by_owner, lists, counts, mark};
+    k_gdd_send_lists<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(s0, s0, pos, g, world, C, err, tick);
+}
+// Both directions of phase 10 in one launch: owned -> peers' halos (forward, with the
+// boundary marks) and halo -> owners.
+void launch_gdd_send_lists2(const int* own, const int* own_n, const int* halo, const int* halo_n,
+                            int n_est, const double* pos, const GddGeom& g, int world, int C,
+                            int* flist, int* fcnt, int* rlist, int* rcnt, unsigned* err,
+                            unsigned char* mark, cudaStream_t st) {
+    const int blocks = (n_est + 255) / 256;
+    const SendSet s0{own, own_n, 0, flist, fcnt, mark}, s1{halo, halo_n, 1, rlist, rcnt, nullptr};
+    k_gdd_send_lists<<<dim3(blocks < 1 ? 1 : blocks, 2), 256, 0, st>>>(s0, s1, pos, g, world, C, err,
+                                                                    nullptr);
 }
 template <typename E>
 void launch_gdd_pack(int world, int rank, const int* lists, const int* counts, int C, const E* src0,

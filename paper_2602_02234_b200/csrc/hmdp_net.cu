@@ -1494,7 +1494,11 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 // owned rows no peer sends partial sums to are finished here; the
                 // rest wait for the SUMS round (DD = 2)
                 if (ws.dd_role[k] != 1 || ws.dd_bnd[k]) {
-                    if (tm.w == 0) ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                    if (tm.w == 0) {
+                        ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                        if (ws.dd_role[k] == 1)  // the SUMS round adds the peers' rows here
+                            ws.s_remote[static_cast<long long>(k) * kH + lane] = T(0);
+                    }
                     __syncwarp();
                     continue;
                 }
@@ -1566,7 +1570,11 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 // owned rows no peer sends partial sums to are finished here; the
                 // rest wait for the SUMS round (DD = 2)
                 if (ws.dd_role[k] != 1 || ws.dd_bnd[k]) {
-                    if (tm.w == 0) ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                    if (tm.w == 0) {
+                        ws.dd_sum[static_cast<long long>(k) * kH + lane] = sdz;
+                        if (ws.dd_role[k] == 1)  // the SUMS round adds the peers' rows here
+                            ws.s_remote[static_cast<long long>(k) * kH + lane] = T(0);
+                    }
                     __syncwarp();
                     continue;
                 }
