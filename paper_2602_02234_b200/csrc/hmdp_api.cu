@@ -80,6 +80,7 @@ struct GddZero {
     int n32[4];
     unsigned char* u8;
     int n8;
+    double* e_atom;  // per-atom energies of the rows this rank does not own
 };
 void launch_gdd_roles(int, const double*, const GddGeom&, unsigned char*, int*, int*, cudaStream_t,
                       const int* = nullptr, const int* = nullptr, const GddZero* = nullptr);
@@ -134,7 +135,7 @@ void launch_ff(const FfDev&, const DevGraph&, const double*, double*, double*, d
 void launch_gdd_rev(const DevGraph&, int, int*, cudaStream_t);
 template <typename T>
 void launch_gdd_zero(const DevGraph&, int, const unsigned char*, T*, long long, T*, T*, double*,
-                     cudaStream_t, int* = nullptr);
+                     cudaStream_t);
 template <typename T>
 void launch_gdd_push_halo(const DevGraph&, int, const T*, T*, const int*, const int*, cudaStream_t);
 template <typename T>
@@ -2399,6 +2400,7 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                     if (pull) {
                         zr.u8 = g.bnd.as<unsigned char>();
                         zr.n8 = n;
+                        zr.e_atom = w.e_atom;
                     }
                 }
                 launch_gdd_roles(n, g.pos, g.geom, g.role.as<unsigned char>(), lists, counts, st,
@@ -2421,13 +2423,16 @@ void gdd_phase_impl(hmdp_ctx* ctx, int phase, int layer, double dt) {
                                   ctx->dr.as<double>(), ctx->types.as<int>(), ctx->ety.as<int>(),
                                   err, st, srch.alist, srch.alist_n);
                 ctx->cells_owner = nullptr;
-                // mirror slots: a kernel of their own (push form), or set by the owned
-                // atoms' embedding with the halo-halo ones cleared here (pull form)
-                if (!pull) launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
-                launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
-                                   M > 0 && !pull ? w.d : nullptr, slots, pull ? nullptr : w.grev,
-                                   w.g, w.e_atom, st, pull ? ctx->rev.as<int>() : nullptr);
-                g.launches += pull ? 4 : 5;  // roles, bin, search, [rev,] zero
+                // push form: mirror slots and slot zeroing kernels.  Pull form: the
+                // owned atoms' embedding sets the mirrors of every pair with an owned
+                // atom, the first backward kernel overwrites g at every searched slot,
+                // the roles kernel zeroed the energies of the rows not owned here.
+                if (!pull) {
+                    launch_gdd_rev(srch, std::min(n, 2 * g.n_est), ctx->rev.as<int>(), st);
+                    launch_gdd_zero<T>(srch, std::min(n, 2 * g.n_est), g.role.as<unsigned char>(),
+                                       M > 0 ? w.d : nullptr, slots, w.grev, w.g, w.e_atom, st);
+                }
+                g.launches += pull ? 3 : 5;  // roles, bin, search, [rev, zero]
                 if (halo) {  // this step's send lists: owned -> peers' halos, halo -> owners
                     launch_gdd_send_lists2(lists, counts, lists + n, counts + 1, g.n_est, g.pos,
                                            g.geom, W, C, g.flist.as<int>(), g.fcnt.as<int>(),

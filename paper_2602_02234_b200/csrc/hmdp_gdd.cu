@@ -54,6 +54,7 @@ struct GddZero {
     int n32[4];
     unsigned char* u8;
     int n8;
+    double* e_atom;  // per-atom energies of the rows this rank does not own
 };
 
 // Wrapped coordinate (wrap_position, box.hpp:34-42, as dd.owners).
@@ -118,12 +119,14 @@ __global__ void k_gdd_roles(int n, const double* __restrict__ pos, GddGeom g,
     if (i >= n) return;
     if (stamp && role[i] != 1 && stamp[i] != *cur) {
         role[i] = 0;
+        if (z.e_atom) z.e_atom[i] = 0.0;
         return;
     }
     const bool owned = gdd_owner(pos + 3 * i, g) == g.rank;
     const bool halo = !owned && gdd_near(pos + 3 * i, g, g.rank);
     const unsigned char ro = owned ? 1 : (halo ? 2 : 0);
     role[i] = ro;
+    if (z.e_atom && !owned) z.e_atom[i] = 0.0;
     if (owned) lists[atomicAdd(counts + 0, 1)] = i;
     if (halo) lists[n + atomicAdd(counts + 1, 1)] = i;
     if (ro) lists[2 * n + atomicAdd(counts + 2, 1)] = i;
@@ -291,7 +294,7 @@ __global__ void k_gdd_rev(DevGraph gr, int* __restrict__ rev) {
 template <typename T>
 __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, T* __restrict__ d,
                            long long slots, T* __restrict__ grev, T* __restrict__ g,
-                           int* __restrict__ rev, double* __restrict__ e_atom) {
+                           double* __restrict__ e_atom) {
     // per-atom energies of every row this rank does not own
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < gr.n; i += gridDim.x * blockDim.x)
         if (role[i] != 1) e_atom[i] = 0.0;
@@ -303,16 +306,12 @@ __global__ void k_gdd_zero(DevGraph gr, const unsigned char* __restrict__ role, 
         const int i = gr.alist[k];
         const int start = gr.row_start[i], cnt = gr.nnei[i];
         const bool own_row = role[i] == 1;
-        const bool all_g = grev == nullptr;  // pull form: every slot of every searched row
         for (int base = 0; base < cnt; base += 32) {  // lane = slot, then the flagged rows
             const int q = base + lane;
             const long long e = start + q;
             const bool flag = q < cnt && role[gr.nbr[e]] != 1;
-            if (flag && !all_g) grev[e] = T(0);
-            // pull form: the embedding sets the mirrors of every pair with an owned atom;
-            // halo-halo pairs have none (their g is zero at both ends)
-            if (rev && flag && !own_row) rev[e] = -1;
-            if ((all_g || !own_row) && q < cnt) g[e] = T(0);
+            if (flag) grev[e] = T(0);
+            if (!own_row && q < cnt) g[e] = T(0);
             if (d) {
                 unsigned bal = __ballot_sync(FULL_MASK, flag);
                 while (bal) {
@@ -458,8 +457,8 @@ void launch_gdd_rev(const DevGraph& gr, int n_est, int* rev, cudaStream_t st) {
 }
 template <typename T>
 void launch_gdd_zero(const DevGraph& gr, int n_est, const unsigned char* role, T* d,
-                     long long slots, T* grev, T* g, double* e_atom, cudaStream_t st, int* rev) {
-    k_gdd_zero<T><<<warp_grid(n_est), 256, 0, st>>>(gr, role, d, slots, grev, g, rev, e_atom);
+                     long long slots, T* grev, T* g, double* e_atom, cudaStream_t st) {
+    k_gdd_zero<T><<<warp_grid(n_est), 256, 0, st>>>(gr, role, d, slots, grev, g, e_atom);
 }
 template <typename T>
 void launch_gdd_push_halo(const DevGraph& gr, int n_est, const T* p_atom, T* pe,
@@ -480,7 +479,7 @@ void launch_gdd_integrate(int n, const double* f, double* x, double* v, const do
 
 #define HMDP_GDD_INST(T)                                                                       \
     template void launch_gdd_zero<T>(const DevGraph&, int, const unsigned char*, T*, long long, \
-                                     T*, T*, double*, cudaStream_t, int*);                      \
+                                     T*, T*, double*, cudaStream_t);                            \
     template void launch_gdd_push_halo<T>(const DevGraph&, int, const T*, T*, const int*,       \
                                           const int*, cudaStream_t);                            \
     template void launch_gdd_halo_sums<T>(const DevGraph&, int, const T*, T*, const int*,       \

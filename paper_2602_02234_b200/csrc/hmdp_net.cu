@@ -1470,7 +1470,9 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     const T* Z = ws.z + static_cast<long long>(l + 1) * ws.slots * kH;
     const T* V = ws.vrow + static_cast<long long>((l + 1) & 1) * n * kH;
     const T* C0 = ws.vc0 + static_cast<long long>((l + 1) & 1) * n;
-    const bool first_g = DD == 0 && l == md.n_msg - 2;  // DD: g zeroed by k_gdd_zero
+    // the first backward kernel overwrites g; DD: at every slot of every searched row
+    // (masked slots get 0), so no zeroing pass is needed
+    const bool first_g = l == md.n_msg - 2;
     const int n_run = DD ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int k = DD ? gr.alist[k_at] : k_at;
@@ -1547,7 +1549,7 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
     bool staged = false;
     pdl_wait();
     const int n = gr.n;
-    const bool first_g = DD == 0 && md.n_msg == 1;  // DD: g zeroed by k_gdd_zero
+    const bool first_g = md.n_msg == 1;  // (see k_msg_bwd_pull)
     const int n_run = DD ? *gr.alist_n : gr.n_active;
     for (int k_at = tm.first; k_at < n_run; k_at += tm.stride) {
         const int k = DD ? gr.alist[k_at] : k_at;
@@ -1713,8 +1715,12 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                 T gm = T(0);
                 if (gr.sym) {
                     if (ws.gather_mirror_g) {
+                        // (pull-form DD: pairs of two non-owned rows carry no terms and
+                        // have no mirror slot)
                         const int mq = gr.inv_pos[e];
-                        if (mq >= 0) gm = ws.g[mq];
+                        if (mq >= 0 && (!ws.dd_role || ws.dd_role[i] == 1 ||
+                                        ws.dd_role[gr.nbr[e]] == 1))
+                            gm = ws.g[mq];
                     } else {
                         gm = ws.grev[e];
                     }
