@@ -2055,7 +2055,7 @@ static int pull_mode(const DevGraph& gr, const DevWork<T>& ws, int n_msg) {
 // build of the FP32 2-warp-team kernels, single-domain periodic path only).
 template <typename T, int G, bool LIST = false, bool WIDE = false>
 struct Net {
-    static_assert(!WIDE || (!LIST && G == 2 && sizeof(T) == 4), "WIDE: FP32 2-warp teams only");
+    static_assert(!WIDE || (G == 2 && sizeof(T) == 4), "WIDE: FP32 2-warp teams only");
     template <int PULL>
     static cudaError_t configure_p() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -2077,7 +2077,18 @@ struct Net {
     static cudaError_t configure() {
         const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
-        if constexpr (WIDE) {
+        if constexpr (WIDE && LIST) {  // the halo-exchange DD's pull form, 28-warp CTAs
+            for (cudaError_t r :
+                 {cudaFuncSetAttribute(k_embed<T, G, false, true, false, true>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_msg_fwd<T, G, true, true, 1, true>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_msg_fwd<T, G, false, true, 1, true>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1, true, 1>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_msg_bwd_pull<T, G, 1, true, 2>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1, true, 1>, a, kMaxSmem),
+                  cudaFuncSetAttribute(k_embed_bwd_pull<T, G, 1, true, 2>, a, kMaxSmem)})
+                if (r != cudaSuccess) e = r;
+            return e;
+        } else if constexpr (WIDE) {
             for (cudaError_t r : {cudaFuncSetAttribute(k_embed<T, G, true, false, false, true>, a, kMaxSmem),
                                   cudaFuncSetAttribute(k_embed<T, G, false, false, false, true>, a, kMaxSmem),
                                   configure_p<1>(), configure_p<2>()})
@@ -2193,29 +2204,31 @@ struct Net {
     static void dd_phase(const NetShape& sh, const DevModel<T>& md, const DevGraph& gr,
                          const DevWork<T>& ws, int phase, int l, cudaStream_t st, int* rev) {
         const MdFuse none{};
-        switch (phase) {
-            case 0: embed(sh, md, gr, ws, rev, none, st); break;
-            case 2: msg_fwd<0>(sh, md, gr, ws, l, st); break;
-            case 4: msg_bwd<0>(sh, md, gr, ws, l, st); break;
-            case 5: embed_bwd<0>(sh, md, gr, ws, st); break;
+        if (phase == 0) embed(sh, md, gr, ws, rev, none, st);
+        if constexpr (!WIDE) {  // push form
+            switch (phase) {
+                case 2: msg_fwd<0>(sh, md, gr, ws, l, st); break;
+                case 4: msg_bwd<0>(sh, md, gr, ws, l, st); break;
+                case 5: embed_bwd<0>(sh, md, gr, ws, st); break;
+            }
         }
         if constexpr (LIST) {  // halo-exchange DD, pull form (stored z)
             switch (phase) {
                 case 12: msg_fwd<1>(sh, md, gr, ws, l, st); break;
                 case 13:  // sender half of layer l's backward over the searched rows
                     if (l > 0)
-                        launch_net<T>(k_msg_bwd_pull<T, G, 1, false, 1>, Phase::MsgBwd, sh, st, md,
+                        launch_net<T>(k_msg_bwd_pull<T, G, 1, WIDE, 1>, Phase::MsgBwd, sh, st, md,
                                       gr, ws, l - 1);
                     else
-                        launch_net<T>(k_embed_bwd_pull<T, G, 1, false, 1>, Phase::EmbedBwd, sh, st,
+                        launch_net<T>(k_embed_bwd_pull<T, G, 1, WIDE, 1>, Phase::EmbedBwd, sh, st,
                                       md, gr, ws);
                     break;
                 case 14:  // layer l's update backward over the owned rows
-                    launch_net<T>(k_msg_bwd_pull<T, G, 1, false, 2>, Phase::MsgBwd, sh, st, md, gr,
+                    launch_net<T>(k_msg_bwd_pull<T, G, 1, WIDE, 2>, Phase::MsgBwd, sh, st, md, gr,
                                   ws, l);
                     break;
                 case 15:
-                    launch_net<T>(k_embed_bwd_pull<T, G, 1, false, 2>, Phase::EmbedBwd, sh, st, md,
+                    launch_net<T>(k_embed_bwd_pull<T, G, 1, WIDE, 2>, Phase::EmbedBwd, sh, st, md,
                                   gr, ws);
                     break;
             }
@@ -2229,6 +2242,7 @@ cudaError_t net_configure() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {Net<float, 1>::configure(), Net<float, 2>::configure(),
                           Net<float, 2, false, true>::configure(),
+                          Net<float, 2, true, true>::configure(),
                           Net<float, 4>::configure(), Net<double, 1>::configure(),
                           Net<double, 2>::configure(), Net<double, 4>::configure(),
                           Net<float, 1, true>::configure(), Net<float, 2, true>::configure(),
@@ -2291,9 +2305,9 @@ void launch_reduce_partials(const double* partial, int n, double* out, cudaStrea
 template <typename T>
 void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>& ws, int phase,
                      int l, T* s_ghost, double* forces, double* out, cudaStream_t st, int* rev) {
-    // the pull-form DD (ws.dd_role set) takes the pull form's CTA shape
-    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)), false,
-                                  md.n_msg > 0 && !ws.dd_role);
+    // the pull-form DD (ws.dd_role set) takes the pull form's CTA shapes, 28-warp included
+    const NetShape sh = net_shape(gr.n_active, md.n_msg, static_cast<int>(sizeof(T)),
+                                  ws.dd_role != nullptr, md.n_msg > 0 && !ws.dd_role);
     const int ng = gr.n - gr.n_active;
     switch (phase) {
         case 1:
@@ -2317,6 +2331,11 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
         }
         default:
             if (gr.alist) {  // global-index DD: the owned-atom list variants
+                if constexpr (sizeof(T) == 4)
+                    if (sh.wide) {
+                        Net<T, 2, true, true>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
+                        break;
+                    }
                 if (sh.G == 4)
                     Net<T, 4, true>::dd_phase(sh, md, gr, ws, phase, l, st, rev);
                 else if (sh.G == 2)

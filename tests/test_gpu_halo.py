@@ -73,6 +73,23 @@ def test_halo_dd_fp32_within_tolerance(golden_models):
     hub.close()
 
 
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 1, 1)])
+def test_halo_dd_fp32_2ptc_kernel_shapes(dims, golden_models):
+    """2PTC in FP32: one rank takes the 28-warp-CTA owned-list kernels (2 atom rounds
+    instead of 3), two ranks the 20-warp ones; both within the north-star tolerances."""
+    s = P.generate_synthetic_system(4114)
+    m = P.model_from_json(golden_models["dpa3"])
+    ref = P.Context(m).compute(s.positions, s.types, s.box, P.Precision.fp64)
+    hub, engs = _engines(m, s, dims, P.Precision.fp32)
+    dd.run_hub(engs, "eval")
+    F, owned = _assemble(engs, s.n_atoms)
+    assert np.all(owned == 1)
+    E = engs[0].energy_virial()[0]
+    assert abs(E - ref.energy) <= E_TOL * abs(ref.energy)
+    assert np.abs(F - ref.forces).max() <= F_TOL * rms(ref.forces)
+    hub.close()
+
+
 @pytest.mark.parametrize("mname", ["dpa2", "dpa3"])
 def test_halo_dd_md_matches_device_md(mname, golden_models):
     """60 MD steps, each rank integrating only its own atoms (atoms migrate between
