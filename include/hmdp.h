@@ -260,6 +260,10 @@ int hmdp_peak_tcgen05_tf32(int device, int ms, double* tflops);
  * Each round packs one fixed-capacity packet per peer on the device (capacity
  * planned once from the initial geometry, x1.5 + 64 rows headroom; overflow latches
  * an error), so a whole MD step -- collectives included -- is one CUDA graph.
+ * The network runs in its pull form (senders -- owned and halo rows -- pull the
+ * owned receivers' adjoint rows; the SUMS round carries the halo senders' sums);
+ * the environment variable HMDP_DD_PULL=0 selects the push form.  Same results up
+ * to the summation order of the partial sums.
  * Transports: NCCL (grouped ncclSend/ncclRecv on the context's stream; libnccl is
  * loaded at run time), an in-process hub (simulated ranks = contexts on one GPU,
  * one host thread each), or a caller callback (e.g. gloo in tests).
