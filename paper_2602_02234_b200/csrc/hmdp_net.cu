@@ -551,9 +551,16 @@ __global__ __launch_bounds__(kCtaWarps<T, G, WIDE> * 32, kNetMinCTAs<G>) void k_
                 // edges); a ballot finds i.  rev is read only by later kernels.
                 // (pull-form DD, ws.dd_role set: an owned atom also searches for its
                 // halo neighbours, which run no embedding here)
-                const bool up = lane < m && (j > i || (ws.dd_role && ws.dd_role[j] != 1));
-                const unsigned upb = __ballot_sync(FULL_MASK, up);
-                const int lo_lane = upb ? __ffs(upb) - 1 : m;
+                bool up;
+                int lo_lane;
+                if constexpr (LIST) {
+                    up = lane < m && (j > i || (ws.dd_role && ws.dd_role[j] != 1));
+                    const unsigned upb = __ballot_sync(FULL_MASK, up);
+                    lo_lane = upb ? __ffs(upb) - 1 : m;
+                } else {
+                    up = lane < m && j > i;
+                    lo_lane = __popc(__ballot_sync(FULL_MASK, lane < m && !up));
+                }
                 const int rs_l = up ? gr.row_start[j] : 0;
                 const int nn_l = up ? gr.nnei[j] : 0;
                 int found = -1;
@@ -1642,7 +1649,8 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
-template <typename T, int FG>
+// DDG: the pull-form DD's variant (mirror gathers skip pairs of two non-owned rows).
+template <typename T, int FG, bool DDG = false>
 __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                                                      double* __restrict__ forces,
                                                      double* __restrict__ per_atom,
@@ -1718,7 +1726,7 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                         // (pull-form DD: pairs of two non-owned rows carry no terms and
                         // have no mirror slot)
                         const int mq = gr.inv_pos[e];
-                        if (mq >= 0 && (!ws.dd_role || ws.dd_role[i] == 1 ||
+                        if (mq >= 0 && (!DDG || ws.dd_role[i] == 1 ||
                                         ws.dd_role[gr.nbr[e]] == 1))
                             gm = ws.g[mq];
                     } else {
@@ -2015,13 +2023,20 @@ int force_grid(int n) {
 }
 template <typename T>
 static void launch_force_k(const DevGraph& gr, const DevWork<T>& ws, double* forces,
-                           double* per_atom, double* out, cudaStream_t st, const MdFuse& mf) {
-    if (force_fg(gr.n) == 8)
-        launch_pdl(k_force<T, 8>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
-                   per_atom, out, mf);
-    else
-        launch_pdl(k_force<T, 32>, dim3(force_grid(gr.n)), dim3(kForceCTA), 0, st, gr, ws, forces,
-                   per_atom, out, mf);
+                           double* per_atom, double* out, cudaStream_t st, const MdFuse& mf,
+                           bool ddg = false) {
+    const dim3 grid(force_grid(gr.n)), block(kForceCTA);
+    if (force_fg(gr.n) == 8) {
+        if (ddg)
+            launch_pdl(k_force<T, 8, true>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
+        else
+            launch_pdl(k_force<T, 8>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
+    } else {
+        if (ddg)
+            launch_pdl(k_force<T, 32, true>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
+        else
+            launch_pdl(k_force<T, 32>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
+    }
 }
 
 constexpr int kMaxSmem = 200 * 1024;
@@ -2326,7 +2341,8 @@ void launch_dd_phase(const DevModel<T>& md, const DevGraph& gr, const DevWork<T>
         case 16: {  // pull form: each pair's terms sit at either end; gather the mirror g
             DevWork<T> wf = ws;
             wf.gather_mirror_g = 1;
-            launch_force_k<T>(gr, wf, forces, static_cast<double*>(nullptr), out, st, MdFuse{});
+            launch_force_k<T>(gr, wf, forces, static_cast<double*>(nullptr), out, st, MdFuse{},
+                              true);
             break;
         }
         default:
