@@ -166,9 +166,13 @@ int hmdp_compute_group(hmdp_ctx* ctx, int n_total, const double* xyz, const int*
 
 /* ---------------------------------------------------------------------------
  * Device MD loop: velocity Verlet (integrators.cpp:32-47) with the finite-force
- * check (integrators.cpp:12-18) and the NN force provider, neighbour list
- * rebuilt every step (skin 0, as build_input_periodic), all on the device and
- * captured as one CUDA graph per `steps_per_graph` steps.
+ * check (integrators.cpp:12-18) and the NN force provider, all on the device and
+ * captured as one CUDA graph per `steps_per_graph` steps.  Every step evaluates
+ * the exact rc neighbour list of build_input_periodic (same pairs, order and
+ * edge_dr); it is filtered out of Verlet candidate rows within rc + skin that
+ * are rebuilt by the cell-list search only after some atom moved more than
+ * skin/2 (skin from HMDP_SKIN at hmdp_md_create, default 0.1 nm; 0, or a box
+ * where rc + skin exceeds half a length, searches every step).
  * ------------------------------------------------------------------------- */
 int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
                    const double* masses, const int* types, const double* box, double dt_ps,
@@ -179,6 +183,9 @@ int hmdp_md_run(hmdp_md* md, int steps);
 int hmdp_md_enqueue(hmdp_md* md, int steps);
 /* Copies the current state back; any pointer may be NULL. */
 int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* epot);
+/* The loop's Verlet skin (nm, 0 = none) and how many steps rebuilt the candidate
+ * rows so far (the first step always does); either pointer may be NULL. */
+int hmdp_md_stats(hmdp_md* md, double* skin, long long* rebuilds);
 int hmdp_md_destroy(hmdp_md* md);
 
 /* ---------------------------------------------------------------------------

@@ -63,6 +63,7 @@ SIGNATURES = {
     "hmdp_peak_fp32": (_c_int, [_c_int, _c_int, _vp]),
     "hmdp_peak_tf32x3": (_c_int, [_c_int, _c_int, _vp]),
     "hmdp_md_get": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "hmdp_md_stats": (_c_int, [_vp, _vp, _vp]),
     "hmdp_md_destroy": (_c_int, [_vp]),
     "hmdp_compute_group": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _vp, _c_int, _vp, _vp,
                                     _vp, _vp]),

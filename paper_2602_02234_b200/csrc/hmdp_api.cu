@@ -33,7 +33,8 @@ namespace hmdp {
 void launch_cell_bin(int, const double*, const CellGrid&, int*, int*, int*, unsigned*, cudaStream_t);
 void launch_nbr_search(int, const double*, const CellGrid&, const int*, const int*, const int*,
                        double, int, int*, int*, int*, double*, const int*, int*, unsigned*,
-                       cudaStream_t, const int* = nullptr, const int* = nullptr);
+                       cudaStream_t, const int* = nullptr, const int* = nullptr,
+                       const VList* = nullptr);
 void launch_edge_meta(int, const int*, const int*, int*, const int*, int*, cudaStream_t);
 void launch_csr_rows(int, const int*, int*, int*, cudaStream_t);
 void launch_in_edges(int, int, const int*, int*, int*, int*, int*, cudaStream_t);
@@ -66,7 +67,12 @@ int launch_dp(const DevDp<T>&, const DevGraph&, const DevWork<T>&, const DevDpWo
 cudaError_t nbr_configure();
 void launch_reduce_partials(const double*, int, double*, cudaStream_t);
 void launch_stage_bin(int, const double*, const int*, double*, int*, const CellGrid&, int*, int*,
-                      int*, unsigned*, cudaStream_t);
+                      int*, unsigned*, cudaStream_t, const double* = nullptr, int* = nullptr,
+                      double = 0.0);
+// Default Verlet skin (nm) of the device MD loop and the hmdp_compute graph path,
+// candidate rows hold the pairs within rc + skin and are rebuilt when
+// an atom moved more than skin/2; the exact rc list is filtered out of them.
+constexpr double kDefaultSkin = 0.1;
 struct GddGeom {
     int d[3];
     double L[3];
@@ -219,6 +225,7 @@ std::unique_lock<std::shared_mutex> alloc_lock() {
     return std::unique_lock<std::shared_mutex>(g_capture_mu);
 }
 
+constexpr size_t kTailPad = 16384;
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -230,12 +237,14 @@ struct DBuf {
         p = nullptr;
         bytes = 0;
         const size_t want = std::max<size_t>(need, 256);
-        ck(cudaMalloc(&p, want), "cudaMalloc");
+        // + a zeroed tail: row prefetches that run past the last row of a buffer
+        // (values discarded) stay inside the allocation whatever the layout
+        ck(cudaMalloc(&p, want + kTailPad), "cudaMalloc");
         // zero once: the batched row prefetches read slots past an atom's last
         // neighbour (values discarded); zeroed memory keeps compute-sanitizer's
         // initcheck clean.  Allocation is setup / growth only, never in a hot loop.
         // Zeroed on this thread's own stream (no device-wide sync, no legacy stream).
-        ck(cudaMemsetAsync(p, 0, want, cudaStreamPerThread), "cudaMemsetAsync");
+        ck(cudaMemsetAsync(p, 0, want + kTailPad, cudaStreamPerThread), "cudaMemsetAsync");
         ck(cudaStreamSynchronize(cudaStreamPerThread), "alloc sync");
         bytes = want;
     }
@@ -751,6 +760,14 @@ struct hmdp_ctx {
     // inputs into the device position / type arrays as it bins them
     const double* stage_hx = nullptr;
     const int* stage_ht = nullptr;
+    // Verlet rows of hmdp_compute's graph path (HMDP_SKIN, as the device MD loop):
+    // the staging kernel raises the flag when an atom moved more than skin/2 since
+    // the rows were built, and the search filters the exact rc list out of them;
+    // graph_vl is set while the graph is captured
+    double cg_skin = 0.0;
+    DBuf cvlist, cvcnt, cvxref, cvflag;
+    VList cvl{};
+    const VList* graph_vl = nullptr;
     int last_launches = 0;
     // set while a device MD loop enqueues its steps: the force kernel's per-CTA
     // (E, W, W9) partials go to the loop's own block, so another operation on this
@@ -813,7 +830,7 @@ struct hmdp_ctx {
                         &gdd.sremote, &gdd.hsum, &gdd.outs, &grp_xyz, &grp_types, &grp_idx, &gv, &gvrev,
                         &rf_env, &rf_g2, &rf_qkv, &rf_dg2, &rf_dwh, &rf_g1, &rf_P, &rf_uz, &rf_mz,
                         &rf_D, &rf_A, &rf_Ts, &rf_stat, &rf_dob, &rf_aux, &rf_tmp, &rf_dconv, &rf_dg1,
-                        &rf_envA, &rf_dua, &cg_out})
+                        &rf_envA, &rf_dua, &cg_out, &cvlist, &cvcnt, &cvxref, &cvflag})
             b->release();
         wf.buf.release();
         wd.buf.release();
@@ -949,7 +966,8 @@ struct hmdp_ctx {
     // kernel, or by the memset here when no network runs after the search).
     void neighbors(int n, const double* d_pos, const double* box, double rc, cudaStream_t st,
                    const int* d_types = nullptr) {
-        CellGrid cg = grid(box, rc, n);
+        const double vskin = graph_vl ? cg_skin : 0.0;
+        CellGrid cg = grid(box, rc + vskin, n);
         ensure_edges(static_cast<long long>(n) * cap);
         cells_owner = nullptr;
         if (!skip_cell_memset) {
@@ -960,20 +978,55 @@ struct hmdp_ctx {
         if (stage_hx)  // graph path: inputs staged from host-mapped memory by the binning
             launch_stage_bin(n, stage_hx, stage_ht, const_cast<double*>(d_pos),
                              const_cast<int*>(d_types), cg, cell_count.as<int>(),
-                             members.as<int>(), cell_of.as<int>(), err.as<unsigned>(), st);
+                             members.as<int>(), cell_of.as<int>(), err.as<unsigned>(), st,
+                             graph_vl ? graph_vl->xref : nullptr,
+                             graph_vl ? graph_vl->flag : nullptr, vskin_half2(vskin));
         else
             launch_cell_bin(n, d_pos, cg, cell_count.as<int>(), members.as<int>(),
                             cell_of.as<int>(), err.as<unsigned>(), st);
         mark("cell_bin", st);
-        search(n, d_pos, cg, rc, st, d_types);
+        search(n, d_pos, cg, rc, st, d_types, stage_hx ? graph_vl : nullptr);
+    }
+    static double vskin_half2(double skin) {
+        const double h = 0.5 * skin * (1.0 - 1e-9);  // strict: rounding never lets a pair slip
+        return h * h;
+    }
+    // Verlet skin for a box: HMDP_SKIN (default kDefaultSkin), 0 when rc + skin
+    // exceeds half a box length
+    double choose_skin(const double* box) const {
+        const char* e = std::getenv("HMDP_SKIN");
+        double skin = e ? std::atof(e) : kDefaultSkin;
+        if (!(skin > 0.0)) return 0.0;
+        for (int a = 0; a < 3; ++a)
+            if (model.rc + skin > 0.5 * box[a]) return 0.0;
+        return skin;
+    }
+    // candidate rows for n atoms at skin (capacity from the current ELL cap)
+    void verlet_rows(VList& vl, DBuf& list, DBuf& cnt, DBuf& xref, DBuf& flag, int n, double skin) {
+        const double g = (model.rc + skin) / model.rc;
+        const int vcap =
+            std::min(kCandMax, (static_cast<int>(std::ceil(1.15 * g * g * g * cap)) + 7) / 8 * 8);
+        list.ensure(static_cast<size_t>(n) * vcap * sizeof(int));
+        cnt.ensure(n * sizeof(int));
+        xref.ensure(3 * n * sizeof(double));
+        flag.ensure(4 * sizeof(int));
+        static const int flag0[4] = {1, 0, 0, 0};  // the first search builds the rows
+        ck(cudaMemcpyAsync(flag.p, flag0, sizeof flag0, cudaMemcpyHostToDevice, st()), "H2D");
+        vl.list = list.as<int>();
+        vl.cnt = cnt.as<int>();
+        vl.xref = xref.as<double>();
+        vl.flag = flag.as<int>();
+        vl.cap = vcap;
+        vl.range2 = (model.rc + skin) * (model.rc + skin);
     }
     // d_types (nullable): also record each edge's neighbour type (DevGraph::ety)
+    // vl (nullable): the device MD loop's Verlet candidate rows (k_nbr_search_v)
     void search(int n, const double* d_pos, const CellGrid& cg, double rc, cudaStream_t st,
-                const int* d_types) {
+                const int* d_types, const VList* vl = nullptr) {
         launch_nbr_search(n, d_pos, cg, cell_count.as<int>(), members.as<int>(), cell_of.as<int>(),
                           rc * rc, cap, nnei.as<int>(), row_start.as<int>(), nbr.as<int>(),
                           dr.as<double>(), d_types, d_types ? ety.as<int>() : nullptr,
-                          err.as<unsigned>(), st);
+                          err.as<unsigned>(), st, nullptr, nullptr, vl);
         mark("nbr_search", st);
     }
     static long long ncells(const CellGrid& cg) { return 1LL * cg.nc[0] * cg.nc[1] * cg.nc[2]; }
@@ -1123,6 +1176,12 @@ struct hmdp_md {
     DBuf x, v, f, m, types, energy;  // energy: [16] (E, W, W9) of the last evaluated step
     DBuf partial;         // this loop's force-kernel CTA partials (hmdp_ctx::partial_override)
     DBuf xs, vs;          // completed-step snapshot (what hmdp_md_get returns)
+    // Verlet skin (HMDP_SKIN, nm; 0 = the full cell-list search every step): the
+    // candidate rows within rc + skin, their reference positions and the rebuild
+    // flag (VList); the exact rc list is filtered out of them every step
+    double skin = 0.0;
+    DBuf vlist, vcnt, vxref, vflag;
+    VList vl{};
     bool primed = false;  // working (x, v) already carry the next step's opening kick
     int steps_per_graph = 1;
     std::map<int, cudaGraphExec_t> graphs;
@@ -1135,7 +1194,9 @@ struct hmdp_md {
     int graph_cap = 0, graph_ccap = 0;
     ~hmdp_md() {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-        for (DBuf* b : {&x, &v, &f, &m, &types, &energy, &partial, &xs, &vs}) b->release();
+        for (DBuf* b : {&x, &v, &f, &m, &types, &energy, &partial, &xs, &vs, &vlist, &vcnt, &vxref,
+                        &vflag})
+            b->release();
     }
 };
 
@@ -1382,10 +1443,22 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     ctx->cg_out.ensure(out_bytes);
                     dst = ctx->cg_out.as<double>();
                 }
+                // Verlet rows (mapped inputs only: the staging kernel checks the
+                // displacements); sized, and the cell grid of rc + skin allocated,
+                // before the capture
+                ctx->cg_skin = mapped_in ? ctx->choose_skin(box) : 0.0;
+                if (ctx->cg_skin > 0.0) {
+                    ctx->verlet_rows(ctx->cvl, ctx->cvlist, ctx->cvcnt, ctx->cvxref, ctx->cvflag, n,
+                                     ctx->cg_skin);
+                    ctx->grid(box, ctx->model.rc + ctx->cg_skin, n);
+                    ctx->grid(box, ctx->model.rc, n);  // (the network's cell zeroing, same ccap)
+                    ck(cudaStreamSynchronize(st), "sync");
+                }
                 CaptureGuard cguard;
                 try {
                     ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
                     ctx->skip_cell_memset = true;  // cleared by this call's network
+                    if (ctx->cg_skin > 0.0) ctx->graph_vl = &ctx->cvl;
                     if (mapped_in) {
                         ctx->stage_hx = reinterpret_cast<const double*>(hin);
                         ctx->stage_ht = reinterpret_cast<const int*>(hin + 3 * n * sizeof(double));
@@ -1405,6 +1478,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                            "out D2H");
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
+                    ctx->graph_vl = nullptr;
                     ctx->skip_cell_memset = false;
                     const cudaError_t ce = cudaStreamEndCapture(st, &g);
                     if (ce == cudaSuccess && g) {
@@ -1426,6 +1500,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     ctx->out_override = nullptr;
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
+                    ctx->graph_vl = nullptr;
                     ctx->skip_cell_memset = false;
                     cudaGraph_t gg = nullptr;
                     cudaStreamEndCapture(st, &gg);
@@ -1812,8 +1887,13 @@ void md_enqueue_steps(hmdp_md* md, int steps, bool primed, cudaStream_t st) {
     // the opening kick + drift + binning kernel (velocity Verlet,
     // integrators.cpp:32-47, split at the force evaluation).
     hmdp_ctx* ctx = md->ctx;
-    const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
+    const CellGrid cg = ctx->grid(md->box, ctx->model.rc + md->skin, md->n);
     MdFuse mf = ctx->zeroing(cg);
+    if (md->skin > 0.0) {
+        mf.xref = md->vxref.as<double>();
+        mf.vflag = md->vflag.as<int>();
+        mf.vhalf2 = hmdp_ctx::vskin_half2(md->skin);
+    }
     mf.x = md->x.as<double>();
     mf.v = md->v.as<double>();
     mf.m = md->m.as<double>();
@@ -1839,7 +1919,8 @@ void md_enqueue_steps(hmdp_md* md, int steps, bool primed, cudaStream_t st) {
         ~PartialScope() { c->partial_override = nullptr; }
     } pscope(ctx, md->partial.as<double>());
     for (int s = 0; s < steps; ++s) {
-        ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st, md->types.as<int>());
+        ctx->search(md->n, md->x.as<double>(), cg, ctx->model.rc, st, md->types.as<int>(),
+                    md->skin > 0.0 ? &md->vl : nullptr);
         if (md->precision == HMDP_FP64)
             ctx->network<double>(gr, slots, md->f.as<double>(), nullptr, st, ctx->rev.as<int>(), mf);
         else
@@ -1908,7 +1989,11 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
             ctx->work<double>(n, slots);
         else
             ctx->work<float>(n, slots);
-        ctx->grid(box, ctx->model.rc, n);
+        // Verlet skin: only when rc + skin still fits half the box on every axis
+        const double skin = ctx->choose_skin(box);
+        md->skin = skin;
+        if (skin > 0.0) ctx->verlet_rows(md->vl, md->vlist, md->vcnt, md->vxref, md->vflag, n, skin);
+        ctx->grid(box, ctx->model.rc + skin, n);
         ck(cudaMemcpyAsync(md->xs.p, md->x.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st),
            "D2D");
         ck(cudaMemcpyAsync(md->vs.p, md->v.p, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st),
@@ -1921,6 +2006,8 @@ int hmdp_md_create(hmdp_ctx* ctx, int n, const double* xyz, const double* vel,
 namespace {
 cudaGraphExec_t md_graph(hmdp_md* md, int chunk, cudaStream_t st) {
     const int key = 2 * chunk + (md->primed ? 1 : 0);
+    // cell grid (re)sized outside any capture: no allocation while capturing
+    md->ctx->grid(md->box, md->ctx->model.rc + md->skin, md->n);
     const hmdp_ctx* ctx = md->ctx;
     const bool valid = md->graph_stream == st && md->graph_prof == ctx->prof &&
                        md->graph_gen == g_alloc_gen.load() && md->graph_cap == ctx->cap &&
@@ -1963,7 +2050,7 @@ void md_launch(hmdp_md* md, int steps) {
     if (md->primed && ctx->cells_owner != md && steps > 0) {
         // another operation re-binned the cell lists: bin this loop's (drifted)
         // positions again before continuing
-        const CellGrid cg = ctx->grid(md->box, ctx->model.rc, md->n);
+        const CellGrid cg = ctx->grid(md->box, ctx->model.rc + md->skin, md->n);
         ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
            "memset cells");
         ctx->cells_zero = false;
@@ -2018,6 +2105,21 @@ int hmdp_md_get(hmdp_md* md, double* xyz, double* vel, double* forces, double* e
         ck(cudaStreamSynchronize(st), "sync");
         // errors latched by hmdp_md_enqueue'd steps (include/hmdp.h)
         hmdp_ctx::raise_bits(md->ctx->take_err());
+    });
+}
+
+int hmdp_md_stats(hmdp_md* md, double* skin, long long* rebuilds) {
+    return guarded([&] {
+        if (!md) fail(HMDP_INVALID_ARGUMENT, "null md");
+        if (skin) *skin = md->skin;
+        if (rebuilds) {
+            int f[4] = {0, 0, 0, 0};
+            if (md->skin > 0.0) {
+                set_device(md->ctx);
+                ck(copy_sync(f, md->vflag.p, sizeof f, cudaMemcpyDeviceToHost, md->ctx->st()), "D2H");
+            }
+            *rebuilds = f[2];
+        }
     });
 }
 

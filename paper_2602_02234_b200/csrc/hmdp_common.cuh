@@ -15,7 +15,6 @@ namespace hmdp {
 
 #define FULL_MASK 0xffffffffu
 constexpr int kAT = 128;       // threads per atom-CTA (4 warps)
-constexpr int kCandMax = 512;  // neighbour candidates kept per atom
 
 // ---------------------------------------------------------------------------
 // small device helpers
@@ -376,11 +375,11 @@ __device__ __forceinline__ void nbr_search_team(int i, const double* pos, const 
         const long long slot = static_cast<long long>(i) * cap + rank;
         nbr[slot] = v;
         if (ety) ety[slot] = types[v];
-        if (q < kCandDr) {  // the displacement the pair test computed
+        if (q < kCandDr && dr) {  // the displacement the pair test computed
             dr[3 * slot] = sm.cdr[q][0];
             dr[3 * slot + 1] = sm.cdr[q][1];
             dr[3 * slot + 2] = sm.cdr[q][2];
-        } else {
+        } else if (dr) {  // (dr null: a Verlet candidate row, indices only)
             dr[3 * slot] = min_image1(__dsub_rn(pos[3 * v], xi), L0);
             dr[3 * slot + 1] = min_image1(__dsub_rn(pos[3 * v + 1], yi), L1);
             dr[3 * slot + 2] = min_image1(__dsub_rn(pos[3 * v + 2], zi), L2);
@@ -388,13 +387,132 @@ __device__ __forceinline__ void nbr_search_team(int i, const double* pos, const 
     }
     if (w == 0 && lane == 0) {
         nnei[i] = m < cap ? m : cap;
-        row_start[i] = i * cap;
+        if (row_start) row_start[i] = i * cap;
     }
     // the lists are reused by the team's next atom
     if constexpr (G > 1)
         asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");
     else
         __syncwarp();
+}
+
+// Verlet filter (device MD loop with a skin): atom i's exact rc list out of its
+// candidate row.  The row is ascending in j, so the survivors come out in the
+// reference's sorted order (neighborlist.cpp:104-111) without a rank sort; the
+// pair test and edge_dr are nbr_search_team's (FP64, no FMA), so the list is the
+// one the full search builds.  G == 1: one pass with a running offset; G > 1:
+// the team's warps take interleaved 32-candidate blocks, count survivors per
+// block (shared), then recompute and write at the prefix offsets.
+template <int G>
+__device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict__ pos,
+                                                const CellGrid& cg, const VList& vl,
+                                                double range2, int cap, int* __restrict__ nnei,
+                                                int* __restrict__ row_start,
+                                                int* __restrict__ nbr, double* __restrict__ dr,
+                                                const int* __restrict__ types,
+                                                int* __restrict__ ety, unsigned* err,
+                                                NbrSmem* team_sm, int w, int lane, int bar) {
+    const double L[3] = {cg.L[0], cg.L[1], cg.L[2]};
+    const double xi[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    const int c = min(vl.cnt[i], vl.cap);
+    const int* row = vl.list + static_cast<long long>(i) * vl.cap;
+    const int nb = (c + 31) >> 5;
+    const long long base = static_cast<long long>(i) * cap;
+    constexpr int U = 4;
+    int* bcnt = team_sm[0].cand;  // G > 1: survivors per block (nb <= vl.cap / 32)
+    // one group of up to U of this warp's blocks: candidates, positions, pair test
+    auto test = [&](int b0, int bstep, int (&jr)[U], double (&d)[U][3], unsigned (&bal)[U]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = 32 * (b0 + bstep * u) + lane;
+            jr[u] = (b0 + bstep * u < nb && q < c) ? row[q] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) d[u][a] = jr[u] >= 0 ? pos[3 * jr[u] + a] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bool pass = false;
+            if (jr[u] >= 0) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) d[u][a] = min_image1(__dsub_rn(d[u][a], xi[a]), L[a]);
+                pass = !(norm2_rn(d[u][0], d[u][1], d[u][2]) > range2);
+            }
+            bal[u] = __ballot_sync(FULL_MASK, pass);
+        }
+    };
+    auto write = [&](int off, unsigned b, int j, const double (&d3)[3]) {
+        if (!((b >> lane) & 1u)) return;
+        const int idx = off + __popc(b & ((1u << lane) - 1u));
+        if (idx >= cap) return;  // overflow: flagged below
+        const long long slot = base + idx;
+        nbr[slot] = j;
+        if (ety) ety[slot] = types[j];
+        dr[3 * slot] = d3[0];
+        dr[3 * slot + 1] = d3[1];
+        dr[3 * slot + 2] = d3[2];
+    };
+    int total = 0;
+    if constexpr (G == 1) {
+        for (int b0 = 0; b0 < nb; b0 += U) {
+            int jr[U];
+            double d[U][3];
+            unsigned bal[U];
+            test(b0, 1, jr, d, bal);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                write(total, bal[u], jr[u], d[u]);
+                total += __popc(bal[u]);
+            }
+        }
+        __syncwarp();
+    } else {
+        for (int b0 = w; b0 < nb; b0 += G * U) {
+            int jr[U];
+            double d[U][3];
+            unsigned bal[U];
+            test(b0, G, jr, d, bal);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lane == 0 && b0 + G * u < nb) bcnt[b0 + G * u] = __popc(bal[u]);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");
+        for (int t = 0; t < nb; ++t) total += bcnt[t];
+        for (int b0 = w; b0 < nb; b0 += G * U) {
+            int jr[U];
+            double d[U][3];
+            unsigned bal[U];
+            test(b0, G, jr, d, bal);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int b = b0 + G * u;
+                if (b >= nb) break;
+                int off = 0;
+                for (int t = 0; t < b; ++t) off += bcnt[t];
+                write(off, bal[u], jr[u], d[u]);
+            }
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G * 32) : "memory");  // bcnt reuse
+    }
+    if (w == 0 && lane == 0) {
+        if (total > cap) atomicOr(err, kErrNbrOverflow);
+        nnei[i] = total < cap ? total : cap;
+        row_start[i] = i * cap;
+    }
+}
+
+// Device MD loop with a Verlet skin: after the drift, an atom farther than skin/2
+// from where the candidate rows were last built raises the rebuild flag.
+__device__ __forceinline__ void vlist_check(int i, const double* x3, const MdFuse& mf) {
+    if (!mf.vflag) return;
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double d = min_image1(x3[a] - mf.xref[3 * i + a], mf.cg.L[a]);
+        s += d * d;
+    }
+    if (s > mf.vhalf2) *mf.vflag = 1;
 }
 
 // Opening of a device-MD chunk for atom i: first half kick + drift + binning
@@ -414,6 +532,7 @@ __device__ __forceinline__ void vv_kick_drift_bin_atom(int i, const MdFuse& mf,
         mf.x[3 * i + a] = x3[a];
     }
     if (!finite) atomicOr(err, kErrNonFinite);
+    vlist_check(i, x3, mf);
     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, err);
 }
 }  // namespace hmdp

@@ -222,6 +222,8 @@ struct Marker {
     }
 };
 
+constexpr int kCandMax = 512;  // neighbour candidates kept per atom (search warp list)
+
 struct CellGrid {
     int nc[3];
     double L[3];
@@ -250,6 +252,24 @@ struct MdFuse {
     int n_cells_zero = 0;  // > 0: embed kernel zeroes cell_count[0..n)
     double* xs = nullptr;  // nullable: completed-step snapshot (x, v after the
     double* vs = nullptr;  // closing kick), what hmdp_md_get returns
+    // Verlet candidate list (device MD loop with a skin, VList): after the drift,
+    // any atom farther than skin/2 from its position at the last candidate build
+    // (xref, minimum image) sets *vflag, and the next search rebuilds.
+    const double* xref = nullptr;
+    int* vflag = nullptr;
+    double vhalf2 = 0.0;  // (skin/2)^2, slightly shrunk
+};
+
+// Verlet candidate list of the device MD loop (k_nbr_search_v): every step the
+// exact rc list is filtered out of the rows of candidates within rc + skin,
+// which are rebuilt by the cell-list scan only when *flag is set.
+struct VList {
+    int* list = nullptr;   // [n][cap] candidates, ascending j
+    int* cnt = nullptr;    // [n]
+    double* xref = nullptr;  // [n][3] positions at the last build
+    int* flag = nullptr;   // [0] rebuild flag, [1] CTA-done counter, [2] rebuilds so far
+    int cap = 0;
+    double range2 = 0.0;   // (rc + skin)^2
 };
 
 }  // namespace hmdp

@@ -30,7 +30,8 @@ __global__ void k_cell_bin(int n, const double* __restrict__ pos, CellGrid cg,
 __global__ void k_stage_bin(int n, const double* __restrict__ hx, const int* __restrict__ ht,
                             double* __restrict__ pos, int* __restrict__ types, CellGrid cg,
                             int* __restrict__ cell_count, int* __restrict__ members,
-                            int* __restrict__ cell_of, unsigned* err) {
+                            int* __restrict__ cell_of, unsigned* err,
+                            const double* __restrict__ xref, int* vflag, double vhalf2) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x3[3] = {hx[3 * i], hx[3 * i + 1], hx[3 * i + 2]};
@@ -38,6 +39,15 @@ __global__ void k_stage_bin(int n, const double* __restrict__ hx, const int* __r
     pos[3 * i] = x3[0];
     pos[3 * i + 1] = x3[1];
     pos[3 * i + 2] = x3[2];
+    if (vflag) {  // Verlet rows of the graph path: this call's atom moved past skin/2?
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double d = min_image1(x3[a] - xref[3 * i + a], cg.L[a]);
+            s += d * d;
+        }
+        if (!(s <= vhalf2)) *vflag = 1;  // (a NaN position rebuilds too)
+    }
     bin_atom(i, x3, cg, cell_count, members, cell_of, err);
 }
 
@@ -64,6 +74,50 @@ __global__ __launch_bounds__(kSearchCTA, 2) void k_nbr_search(
         nbr_search_team<G>(alist ? alist[k] : k, pos, cg, cell_count, members, cell_of, range2,
                            cap, nnei, row_start, nbr, dr, types, ety, err, sm + team * G, w, lane,
                            1 + team);
+}
+
+// Device MD loop with a Verlet skin: the exact rc list filtered out of each atom's
+// candidate row (within rc + skin), the rows rebuilt by the cell-list scan only on
+// steps whose flag a drift set (some atom moved more than skin/2 since the last
+// build).  Every CTA reads the flag first; the last CTA to finish a rebuild clears
+// it, so the force kernel's drift can raise it again for the next step.
+template <int G>
+__global__ __launch_bounds__(kSearchCTA, 2) void k_nbr_search_v(
+    int n, const double* __restrict__ pos, CellGrid cg, const int* __restrict__ cell_count,
+    const int* __restrict__ members, const int* __restrict__ cell_of, double range2, int cap,
+    int* __restrict__ nnei, int* __restrict__ row_start, int* __restrict__ nbr,
+    double* __restrict__ dr, const int* __restrict__ types, int* __restrict__ ety,
+    unsigned* err, VList vl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    NbrSmem* sm = reinterpret_cast<NbrSmem*>(smem_raw);
+    pdl_launch_dependents();
+    pdl_wait();
+    const bool rebuild = *reinterpret_cast<volatile int*>(vl.flag) != 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tpc = (blockDim.x >> 5) / G, team = warp / G, w = warp % G;
+    const int nt = gridDim.x * tpc;
+    for (int i = blockIdx.x * tpc + team; i < n; i += nt) {
+        if (rebuild) {  // candidate row (indices only, ascending) + reference position
+            nbr_search_team<G>(i, pos, cg, cell_count, members, cell_of, vl.range2, vl.cap,
+                               vl.cnt, nullptr, vl.list, nullptr, types, nullptr, err,
+                               sm + team * G, w, lane, 1 + team);
+            if (w == 0 && lane < 3) vl.xref[3 * i + lane] = pos[3 * i + lane];
+        }
+        nbr_filter_team<G>(i, pos, cg, vl, range2, cap, nnei, row_start, nbr, dr, types, ety, err,
+                           sm + team * G, w, lane, 1 + team);
+    }
+    if (rebuild) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            auto* done = reinterpret_cast<unsigned*>(vl.flag + 1);
+            if (atomicAdd(done, 1u) == gridDim.x - 1) {
+                *done = 0u;
+                vl.flag[0] = 0;
+                ++vl.flag[2];  // rebuild count (hmdp_md_stats)
+            }
+        }
+    }
 }
 
 // CSR offsets -> (row_start, nnei)
@@ -237,14 +291,16 @@ void launch_cell_bin(int n, const double* pos, const CellGrid& cg, int* cell_cou
 }
 void launch_stage_bin(int n, const double* hx, const int* ht, double* pos, int* types,
                       const CellGrid& cg, int* cell_count, int* members, int* cell_of,
-                      unsigned* err, cudaStream_t st) {
+                      unsigned* err, cudaStream_t st, const double* xref, int* vflag,
+                      double vhalf2) {
     k_stage_bin<<<(n + 127) / 128, 128, 0, st>>>(n, hx, ht, pos, types, cg, cell_count, members,
-                                                 cell_of, err);
+                                                 cell_of, err, xref, vflag, vhalf2);
 }
 void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* cell_count,
                        const int* members, const int* cell_of, double range2, int cap, int* nnei,
                        int* row_start, int* nbr, double* dr, const int* types, int* ety,
-                       unsigned* err, cudaStream_t st, const int* alist, const int* alist_n) {
+                       unsigned* err, cudaStream_t st, const int* alist, const int* alist_n,
+                       const VList* vl) {
     const int sms = num_sms();
     // team size by system size: 4 warps per atom up to 4 atoms per SM, 2 up to 16 per
     // SM (one round of 2-warp teams), then 1 (measured: 3LZM, 18 atoms per SM, with 1
@@ -288,6 +344,17 @@ void launch_nbr_search(int n, const double* pos, const CellGrid& cg, const int* 
                    cell_count, members, cell_of, range2, cap, nnei, row_start, nbr, dr, types, ety,
                    err, alist, alist_n);
     };
+    if (vl) {
+        auto vargs = [&](auto kernel) {
+            launch_pdl(kernel, dim3(grid > 0 ? grid : 1), dim3(threads), smem, st, n, pos, cg,
+                       cell_count, members, cell_of, range2, cap, nnei, row_start, nbr, dr, types,
+                       ety, err, *vl);
+        };
+        if (G == 4) vargs(k_nbr_search_v<4>);
+        else if (G == 2) vargs(k_nbr_search_v<2>);
+        else vargs(k_nbr_search_v<1>);
+        return;
+    }
     if (G == 4) args(k_nbr_search<4>);
     else if (G == 2) args(k_nbr_search<2>);
     else args(k_nbr_search<1>);
@@ -297,7 +364,10 @@ cudaError_t nbr_configure() {
     cudaError_t e = cudaSuccess;
     for (cudaError_t r : {cudaFuncSetAttribute(k_nbr_search<1>, a, 16 * sizeof(NbrSmem)),
                           cudaFuncSetAttribute(k_nbr_search<2>, a, 16 * sizeof(NbrSmem)),
-                          cudaFuncSetAttribute(k_nbr_search<4>, a, 16 * sizeof(NbrSmem))})
+                          cudaFuncSetAttribute(k_nbr_search<4>, a, 16 * sizeof(NbrSmem)),
+                          cudaFuncSetAttribute(k_nbr_search_v<1>, a, 16 * sizeof(NbrSmem)),
+                          cudaFuncSetAttribute(k_nbr_search_v<2>, a, 16 * sizeof(NbrSmem)),
+                          cudaFuncSetAttribute(k_nbr_search_v<4>, a, 16 * sizeof(NbrSmem))})
         if (r != cudaSuccess) e = r;
     return e;
 }

@@ -1791,8 +1791,10 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                     }
                     mf.v[3 * i + a] = va;
                 }
-                if (mf.mode == 2)
+                if (mf.mode == 2) {
+                    vlist_check(i, x3, mf);
                     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, ws.err);
+                }
             }
         }
     }

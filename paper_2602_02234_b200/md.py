@@ -44,6 +44,14 @@ class DeviceMD:
         check(lib().hmdp_md_get(self.handle, ptr(x), ptr(v), ptr(f), ctypes.byref(e)))
         return x, v, f, e.value
 
+    def stats(self):
+        """(skin in nm, candidate-row rebuilds so far): the exact rc list is filtered
+        out of Verlet rows within rc + skin every step (include/hmdp.h)."""
+        skin = ctypes.c_double()
+        rebuilds = ctypes.c_longlong()
+        check(lib().hmdp_md_stats(self.handle, ctypes.byref(skin), ctypes.byref(rebuilds)))
+        return skin.value, rebuilds.value
+
     def close(self):
         if getattr(self, "handle", None):
             lib().hmdp_md_destroy(self.handle)
