@@ -4,9 +4,12 @@
 Workload (BASELINE.json configs[4], the north-star target box, the largest paper
 box): DPA3 analog (make_model(message_passing, 3, 0.6, 2, 8, 32, seed 1)) on the
 synthetic 2PTC-shaped protein-in-water box (4114 atoms, generate_synthetic_system
-seed 7), velocity-Verlet MD at dt = 1 fs, neighbour list rebuilt every step (skin 0,
-as build_input_periodic), each step = kick+drift, cell-list neighbour search, full
-DP energy/force/virial evaluation, kick -- one CUDA graph per step.  The DPA2 analog
+seed 7), velocity-Verlet MD at dt = 1 fs, the exact rc neighbour list of
+build_input_periodic every step (filtered out of Verlet candidate rows within
+rc + 0.1 nm that the cell-list search rebuilds after an atom moved > 0.05 nm; the
+rebuild count of the timed steps is in the line), each step = kick+drift,
+neighbour list, full DP energy/force/virial evaluation, kick -- one CUDA graph per
+step.  The DPA2 analog
 (embed_fit, depth 1) on the same box is measured the same way in the same run and
 reported under "models": {"dpa2": {...}} with its own roofline / e2e / cpu_baseline.
 
@@ -257,7 +260,7 @@ def workload_config(args, model_name, world):
     reps = tuple(int(v) for v in args.replicas.split(","))
     n_rep = reps[0] * reps[1] * reps[2]
     return {"workload": f"{model_name.upper()} velocity-Verlet MD step on the {args.system}-shaped "
-                        f"box (dt 1 fs, neighbour list rebuilt every step, E+F+W every step)",
+                        f"box (dt 1 fs, exact rc neighbour list every step, E+F+W every step)",
             "model": model_name, "system": args.system, "atoms": n * n_rep,
             "replicas_per_rank": list(reps), "precision": args.precision,
             "parallelism": f"replicas x{world}"}
@@ -425,6 +428,7 @@ def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with
         check(enqueue(md.handle, 1))
     torch.cuda.synchronize(dev)
     check(L.hmdp_check(ctx.handle))
+    skin_nm, rebuilds0 = md.stats()
 
     # ---- timed region: one graph launch per MD step, L2 flushed between steps ----
     K = args.steps
@@ -448,6 +452,7 @@ def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with
         dist.barrier()
     t_ms = float(sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
     check(L.hmdp_md_get(md.handle, None, None, None, None))  # latched device errors
+    rebuilds = md.stats()[1] - rebuilds0
     if dist:
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -610,6 +615,10 @@ def measure(args, model_name, rank, world, local_rank, dist, stream, flush, with
         "dtype": "f32" if args.precision == "fp32" else "f64",
         "data": "synthetic (generate_synthetic_system seed 7), random-init weights (seed 1)",
         "config": workload_config(args, model_name, world),
+        "verlet": {"skin_nm": skin_nm, "rebuilds_in_timed_steps": rebuilds, "timed_steps": K,
+                   "note": "every step filters the exact rc list (bitwise the full search's, "
+                           "tests/test_gpu_skin.py) out of candidate rows within rc + skin; "
+                           "the rows are rebuilt by the cell-list search on the steps counted"},
         "workload_detail": {"edges": ne, "graph": "one CUDA graph launch per MD step",
                             "l2": "flushed (256 MiB write) before every timed step, outside "
                                   "the events"},

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -226,6 +227,40 @@ std::unique_lock<std::shared_mutex> alloc_lock() {
 }
 
 constexpr size_t kTailPad = 16384;
+
+// HMDP_E2E_PROBE=1: host-timer breakdown of hmdp_compute's graph-replay path (input
+// copy into the pinned block, cudaGraphLaunch, the wait, output copies), printed
+// to stderr at exit -- where an e2e step's time outside the kernels goes.
+struct E2eProbe {
+    static bool on() {
+        static const bool v = std::getenv("HMDP_E2E_PROBE") != nullptr;
+        return v;
+    }
+    std::atomic<long long> ns[4]{{0}, {0}, {0}, {0}};
+    std::atomic<long long> calls{0};
+    ~E2eProbe() {
+        const long long c = calls.load();
+        if (!c) return;
+        std::fprintf(stderr,
+                     "hmdp_compute graph path, %lld calls, us/call: copy-in %.2f  launch %.2f  "
+                     "wait %.2f  copy-out %.2f\n",
+                     c, ns[0] * 1e-3 / c, ns[1] * 1e-3 / c, ns[2] * 1e-3 / c, ns[3] * 1e-3 / c);
+    }
+    static E2eProbe& get() {
+        static E2eProbe p;
+        return p;
+    }
+    struct Tick {
+        std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+        void lap(int k) {
+            if (!on()) return;
+            const auto now = std::chrono::steady_clock::now();
+            get().ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - t).count();
+            if (k == 3) ++get().calls;
+            t = now;
+        }
+    };
+};
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -1368,6 +1403,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
         const size_t in_bytes = 3 * static_cast<size_t>(n) * sizeof(double) + n * sizeof(int);
         const size_t out_bytes = (16 + 4 * static_cast<size_t>(n)) * sizeof(double);
         if (!ctx->prof && ctx->cgraph.matches(n, precision, box, ctx->cap, ctx->ccap, st)) {
+            E2eProbe::Tick tk;
             std::memcpy(ctx->pin_in.p, xyz, 3 * n * sizeof(double));
             std::memcpy(static_cast<char*>(ctx->pin_in.p) + 3 * n * sizeof(double), types,
                         n * sizeof(int));
@@ -1376,10 +1412,13 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 ck(cudaMemsetAsync(ctx->cell_count.p, 0, hmdp_ctx::ncells(cg) * sizeof(int), st),
                    "memset cells");
             }
+            tk.lap(0);
             ck(cudaGraphLaunch(ctx->cgraph.exec, st), "graph launch");
+            tk.lap(1);
             ctx->cells_zero = true;
             ctx->cells_owner = nullptr;
             ck(cudaStreamSynchronize(st), "sync");
+            tk.lap(2);
             const double* hp = static_cast<const double*>(ctx->pin.p);
             const unsigned bits = static_cast<unsigned>(hp[12]);
             ctx->last_launches = ctx->cgraph.launches;
@@ -1390,6 +1429,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 if (virial9) std::memcpy(virial9, hp + 2, 9 * sizeof(double));
                 std::memcpy(forces, hp + 16, 3 * n * sizeof(double));
                 if (per_atom) std::memcpy(per_atom, hp + 16 + 3 * n, n * sizeof(double));
+                tk.lap(3);
                 return;
             }
             ctx->cgraph.reset();  // capacity overflow: grow below and recapture next time

@@ -45,7 +45,7 @@ def profile_name(name):
     head, _, args = name.partition("<")
     a = [x.strip() for x in args.rstrip(">").split(",")] if args else []
     on = lambda i: len(a) > i and a[i] in ("1", "true")
-    if head == "k_nbr_search":
+    if head in ("k_nbr_search", "k_nbr_search_v"):
         return "nbr_search"
     if head == "k_embed":
         return "embed_fit" if on(2) else "embed"

@@ -58,7 +58,7 @@ for line in open(P("profiles", "round2", "dpa3_2PTC", "launches.md")):
     if mo:
         name, args, sh = mo.group(1), mo.group(2), float(mo.group(3))
         a = [x.strip() for x in args.split(",")]
-        key = {"k_nbr_search": "search", "k_force": "force", "k_embed": "embed",
+        key = {"k_nbr_search": "search", "k_nbr_search_v": "search", "k_force": "force", "k_embed": "embed",
                "k_msg_bwd_pull": "msg_bwd", "k_embed_bwd_pull": "embed_bwd",
                "k_msg_bwd": "msg_bwd", "k_embed_bwd": "embed_bwd"}.get(name)
         if name == "k_msg_fwd":
