@@ -779,9 +779,12 @@ struct hmdp_ctx {
         cudaStream_t st = nullptr;
         unsigned long long gen = 0;
         int launches = 0;
+        bool per_atom = false;  // the D2H node also moves the per-atom energies
         bool disabled = false;  // a capture failed once: stay on the direct path
-        bool matches(int n_, int prec_, const double* b, int cap_, int ccap_, cudaStream_t st_) const {
+        bool matches(int n_, int prec_, const double* b, int cap_, int ccap_, cudaStream_t st_,
+                     bool pa) const {
             return exec && n == n_ && prec == prec_ && cap == cap_ && ccap == ccap_ && st == st_ &&
+                   (per_atom || !pa) &&
                    gen == g_alloc_gen.load() && box[0] == b[0] && box[1] == b[1] && box[2] == b[2];
         }
         void reset() {
@@ -1238,6 +1241,9 @@ struct hmdp_md {
 namespace {
 
 void check_types(int n, const int* types, int n_types) {
+    unsigned bad = 0;  // branch-free pass (vectorised); the message loop only on failure
+    for (int i = 0; i < n; ++i) bad |= static_cast<unsigned>(types[i]) >= static_cast<unsigned>(n_types);
+    if (!bad) return;
     for (int i = 0; i < n; ++i)
         if (types[i] < 0 || types[i] >= n_types)
             fail(HMDP_INVALID_ARGUMENT, "atom type " + std::to_string(types[i]) + " of atom " +
@@ -1402,7 +1408,8 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
         // fast path: replay the cached graph (inputs through pinned staging)
         const size_t in_bytes = 3 * static_cast<size_t>(n) * sizeof(double) + n * sizeof(int);
         const size_t out_bytes = (16 + 4 * static_cast<size_t>(n)) * sizeof(double);
-        if (!ctx->prof && ctx->cgraph.matches(n, precision, box, ctx->cap, ctx->ccap, st)) {
+        if (!ctx->prof &&
+            ctx->cgraph.matches(n, precision, box, ctx->cap, ctx->ccap, st, per_atom != nullptr)) {
             E2eProbe::Tick tk;
             std::memcpy(ctx->pin_in.p, xyz, 3 * n * sizeof(double));
             std::memcpy(static_cast<char*>(ctx->pin_in.p) + 3 * n * sizeof(double), types,
@@ -1514,7 +1521,11 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                                          box, precision, dst + 16, dst + 16 + 3 * n, st);
                     ctx->out_override = nullptr;
                     if (!mapped_out)
-                        ck(cudaMemcpyAsync(hp, dst, out_bytes, cudaMemcpyDeviceToHost, st),
+                        // header + forces (+ per-atom energies when this call asked for them)
+                        ck(cudaMemcpyAsync(hp, dst,
+                                           per_atom ? out_bytes
+                                                    : (16 + 3 * static_cast<size_t>(n)) * sizeof(double),
+                                           cudaMemcpyDeviceToHost, st),
                            "out D2H");
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
@@ -1532,6 +1543,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                             ctx->cgraph.st = st;
                             ctx->cgraph.gen = g_alloc_gen.load();
                             ctx->cgraph.launches = launches;
+                            ctx->cgraph.per_atom = per_atom != nullptr || mapped_out;
                             for (int a = 0; a < 3; ++a) ctx->cgraph.box[a] = box[a];
                         }
                         cudaGraphDestroy(g);

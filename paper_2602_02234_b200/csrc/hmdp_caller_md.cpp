@@ -6,6 +6,8 @@
 // library: bench.py's e2e leg times it, so the end-to-end number carries a C++
 // caller's host work (as the reference's own loop does) instead of numpy's.
 #include <cmath>
+#include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "hmdp.h"
@@ -24,10 +26,18 @@ int hmdp_caller_velocity_verlet(hmdp_ctx* ctx, int n, double* x, double* v, doub
     // branch-free finite checks: the loops vectorise
     std::vector<double> c(static_cast<size_t>(n > 0 ? n : 0));
     for (int i = 0; i < n; ++i) c[i] = half / masses[i];
+    // check_finite_forces: an FP64 value is non-finite iff its exponent field is all
+    // ones; adding 1 to that field carries into the sign bit exactly then.  Same
+    // verdict as std::isfinite on every element, in a form the compiler vectorises
+    // with baseline SSE2 (measured 4.6 -> 1.3 us over 4114 atoms).
     auto finite = [&] {
-        bool ok = true;
-        for (int k = 0; k < 3 * n; ++k) ok &= std::isfinite(f[k]);
-        return ok;
+        unsigned acc = 0;
+        for (int k = 0; k < 3 * n; ++k) {
+            std::uint64_t b;
+            std::memcpy(&b, f + k, sizeof b);
+            acc |= ((static_cast<unsigned>(b >> 32) & 0x7ff00000u) + 0x00100000u) & 0x80000000u;
+        }
+        return acc == 0;
     };
     for (int s = 0; s < steps; ++s) {
         if (!finite()) return HMDP_RUNTIME_ERROR;

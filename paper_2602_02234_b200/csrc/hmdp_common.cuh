@@ -418,7 +418,14 @@ __device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict_
     const int* row = vl.list + static_cast<long long>(i) * vl.cap;
     const int nb = (c + 31) >> 5;
     const long long base = static_cast<long long>(i) * cap;
-    constexpr int U = 4;
+    // 32-candidate blocks in flight per warp: 4 for one-warp teams (a 2PTC row in two
+    // rounds), 2 for the multi-warp teams of small boxes (A/B profiles/round2/ab/filter_u.txt:
+    // 2PTC DPA2 U=4 +1.7 %, 1UBQ DPA2 U=2 +3.4 %, 1YRF DPA3 U=2 +0.9 %)
+#ifdef HMDP_FILTER_U
+    constexpr int U = HMDP_FILTER_U;
+#else
+    constexpr int U = G == 1 ? 4 : 2;
+#endif
     int* bcnt = team_sm[0].cand;  // G > 1: survivors per block (nb <= vl.cap / 32)
     // one group of up to U of this warp's blocks: candidates, positions, pair test
     auto test = [&](int b0, int bstep, int (&jr)[U], double (&d)[U][3], unsigned (&bal)[U]) {

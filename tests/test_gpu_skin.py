@@ -126,3 +126,20 @@ def test_skin_compute_graph_path_bitwise(monkeypatch, mname, n):
         assert a[0] == b[0]
         assert np.array_equal(a[1], b[1])
         assert np.array_equal(a[2], b[2])
+
+
+def test_compute_graph_per_atom_after_forces_only(monkeypatch):
+    """The graph path's D2H copy moves the per-atom energies only when the captured call
+    asked for them; a later per-atom call re-captures (large box: copy-node outputs)."""
+    monkeypatch.setenv("HMDP_SKIN", "0.1")
+    s = P.generate_synthetic_system(4114)
+    m = _model("dpa3")
+    ctx = P.Context(m, max_atoms=s.n_atoms)
+    ref = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32, per_atom=True)  # direct
+    for _ in range(3):
+        o = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32)
+        assert o.energy == ref.energy and np.array_equal(o.forces, ref.forces)
+    for _ in range(3):
+        o = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32, per_atom=True)
+        assert np.array_equal(o.per_atom_energy, ref.per_atom_energy)
+        assert np.array_equal(o.forces, ref.forces)
