@@ -12,6 +12,22 @@
 
 #include "hmdp.h"
 
+namespace {
+// v += f * c (then x += v * dt) over m contiguous values; the restrict scopes end with
+// the call, so the force function may rewrite f between them
+void kick_drift(int m, double* __restrict__ v, double* __restrict__ x,
+                const double* __restrict__ f, const double* __restrict__ c, double dt) {
+    for (int k = 0; k < m; ++k) {
+        v[k] += f[k] * c[k];
+        x[k] += v[k] * dt;
+    }
+}
+void kick(int m, double* __restrict__ v, const double* __restrict__ f,
+          const double* __restrict__ c) {
+    for (int k = 0; k < m; ++k) v[k] += f[k] * c[k];
+}
+}  // namespace
+
 extern "C" {
 
 // Runs `steps` velocity-Verlet steps in place on x/v (n x 3, FP64), forces f in/out
@@ -24,8 +40,9 @@ int hmdp_caller_velocity_verlet(hmdp_ctx* ctx, int n, double* x, double* v, doub
     const double half = 0.5 * dt;
     // half / masses[i] once per call (the same values the reference forms each step) and
     // branch-free finite checks: the loops vectorise
-    std::vector<double> c(static_cast<size_t>(n > 0 ? n : 0));
-    for (int i = 0; i < n; ++i) c[i] = half / masses[i];
+    // (per component, so the kick and drift loops stream over 3n contiguous values)
+    std::vector<double> c(3 * static_cast<size_t>(n > 0 ? n : 0));
+    for (int i = 0; i < n; ++i) c[3 * i] = c[3 * i + 1] = c[3 * i + 2] = half / masses[i];
     // check_finite_forces: an FP64 value is non-finite iff its exponent field is all
     // ones; adding 1 to that field carries into the sign bit exactly then.  Same
     // verdict as std::isfinite on every element, in a form the compiler vectorises
@@ -41,18 +58,12 @@ int hmdp_caller_velocity_verlet(hmdp_ctx* ctx, int n, double* x, double* v, doub
     };
     for (int s = 0; s < steps; ++s) {
         if (!finite()) return HMDP_RUNTIME_ERROR;
-        for (int i = 0; i < n; ++i) {
-            for (int a = 0; a < 3; ++a) {
-                v[3 * i + a] += f[3 * i + a] * c[i];
-                x[3 * i + a] += v[3 * i + a] * dt;
-            }
-        }
+        kick_drift(3 * n, v, x, f, c.data(), dt);
         const int rc = hmdp_compute(ctx, n, x, types, box, precision, energy, nullptr, f,
                                     nullptr, nullptr);
         if (rc != HMDP_OK) return rc;
         if (!finite()) return HMDP_RUNTIME_ERROR;
-        for (int i = 0; i < n; ++i)
-            for (int a = 0; a < 3; ++a) v[3 * i + a] += f[3 * i + a] * c[i];
+        kick(3 * n, v, f, c.data());
     }
     return HMDP_OK;
 }
