@@ -511,15 +511,15 @@ __device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict_
 
 // Device MD loop with a Verlet skin: after the drift, an atom farther than skin/2
 // from where the candidate rows were last built raises the rebuild flag.
-__device__ __forceinline__ void vlist_check(int i, const double* x3, const MdFuse& mf) {
+__device__ __forceinline__ void vlist_check(const double* x3, const double* xr, const MdFuse& mf) {
     if (!mf.vflag) return;
     double s = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double d = min_image1(x3[a] - mf.xref[3 * i + a], mf.cg.L[a]);
+        const double d = min_image1(x3[a] - xr[a], mf.cg.L[a]);
         s += d * d;
     }
-    if (s > mf.vhalf2) *mf.vflag = 1;
+    if (!(s <= mf.vhalf2)) *mf.vflag = 1;  // (a NaN position rebuilds too)
 }
 
 // Opening of a device-MD chunk for atom i: first half kick + drift + binning
@@ -539,7 +539,10 @@ __device__ __forceinline__ void vv_kick_drift_bin_atom(int i, const MdFuse& mf,
         mf.x[3 * i + a] = x3[a];
     }
     if (!finite) atomicOr(err, kErrNonFinite);
-    vlist_check(i, x3, mf);
+    if (mf.vflag) {
+        const double xr[3] = {mf.xref[3 * i], mf.xref[3 * i + 1], mf.xref[3 * i + 2]};
+        vlist_check(x3, xr, mf);
+    }
     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, err);
 }
 }  // namespace hmdp

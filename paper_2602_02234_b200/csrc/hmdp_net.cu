@@ -1670,7 +1670,7 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
         const int i = base + grp;
         const bool act = i < gr.n;
         // MD state of atom i, loaded early (independent of the edge loads)
-        double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, mi = 1.0, ei = 0.0;
+        double xv[3] = {0, 0, 0}, vv[3] = {0, 0, 0}, xr[3] = {0, 0, 0}, mi = 1.0, ei = 0.0;
         if (act && sub == 0) {
             ei = ws.e_atom[i];
             if (mf.mode) {
@@ -1680,6 +1680,9 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                     xv[a] = mf.x[3 * i + a];
                 }
                 mi = mf.m[i];
+                if (mf.vflag)  // Verlet-row reference position, for the drift's check
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) xr[a] = mf.xref[3 * i + a];
             }
         }
         double fx = 0.0, fy = 0.0, fz = 0.0;
@@ -1792,7 +1795,7 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
                     mf.v[3 * i + a] = va;
                 }
                 if (mf.mode == 2) {
-                    vlist_check(i, x3, mf);
+                    vlist_check(x3, xr, mf);
                     bin_atom(i, x3, mf.cg, mf.cell_count, mf.members, mf.cell_of, ws.err);
                 }
             }
