@@ -431,8 +431,11 @@ __device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict_
     auto test = [&](int b0, int bstep, int (&jr)[U], double (&d)[U][3], unsigned (&bal)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            // the row load does not wait for the count (slots past it hold stale valid
+            // indices or zeros); the count only masks
             const int q = 32 * (b0 + bstep * u) + lane;
-            jr[u] = (b0 + bstep * u < nb && q < c) ? row[q] : -1;
+            const int raw = q < vl.cap ? row[q] : -1;
+            jr[u] = q < c ? raw : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -462,7 +465,8 @@ __device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict_
     };
     int total = 0;
     if constexpr (G == 1) {
-        for (int b0 = 0; b0 < nb; b0 += U) {
+        int b0 = 0;
+        do {  // (do-while: the first group's loads need not wait for the count)
             int jr[U];
             double d[U][3];
             unsigned bal[U];
@@ -472,7 +476,8 @@ __device__ __forceinline__ void nbr_filter_team(int i, const double* __restrict_
                 write(total, bal[u], jr[u], d[u]);
                 total += __popc(bal[u]);
             }
-        }
+            b0 += U;
+        } while (b0 < nb);
         __syncwarp();
     } else {
         for (int b0 = w; b0 < nb; b0 += G * U) {
