@@ -227,6 +227,9 @@ std::unique_lock<std::shared_mutex> alloc_lock() {
 }
 
 constexpr size_t kTailPad = 16384;
+// hmdp_compute's graph path writes its outputs straight to host-mapped memory below
+// this many atoms, through a D2H copy node above
+constexpr int kMappedOutMax = 16384;
 
 // HMDP_E2E_PROBE=1: host-timer breakdown of hmdp_compute's graph-replay path (input
 // copy into the pinned block, cudaGraphLaunch, the wait, output copies), printed
@@ -1154,6 +1157,7 @@ struct hmdp_ctx {
 
     // hmdp_compute's graph path: (E, W, W9, err) to this host-mapped block instead of `out`
     double* out_override = nullptr;
+    bool out_mapped = false;  // ... and it (with the force arrays) is host-mapped memory
     // hybrid MD: the DP branch's (E, W, W9) to the hybrid's own block (no error export)
     double* energy_out = nullptr;
 
@@ -1162,6 +1166,7 @@ struct hmdp_ctx {
                 cudaStream_t st, int* d_rev, const MdFuse& mf) {
         DevWork<T> w = work<T>(gr.n, slots);
         w.export_err = out_override != nullptr;
+        w.wide_out = out_override != nullptr && out_mapped;
         double* const o = out_override ? out_override : energy_out ? energy_out : out.as<double>();
         if (model.is_dp()) {
             const DevDpWork<T> d = dp_work<T>(gr.n, slots, w);
@@ -1472,12 +1477,16 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 // moves for large ones: the copy node costs ~4 us flat, the force
                 // kernel's scattered 8-byte PCIe writes grow with n (measured per
                 // call: 582 atoms 60.7 vs 64.5 us, 4114 atoms 92 vs 85 us; crossover
-                // near 1900 atoms).  HMDP_CGRAPH_MAPPED_OUT=0/1 pins it for A/B.
+                // near 1900 atoms).  Since each warp writes its atoms' forces as one
+                // contiguous store (DevWork::wide_out) the mapped writes win at 4114
+                // atoms too (e2e DPA2 2PTC +3.4 %, DPA3 +1.5 %, profiles/round2/ab/
+                // force_store.txt); the copy node stays for very large systems.
+                // HMDP_CGRAPH_MAPPED_OUT=0/1 pins it for A/B.
                 static const int mapped_env = [] {
                     const char* e = std::getenv("HMDP_CGRAPH_MAPPED_OUT");
                     return e ? std::atoi(e) : -1;
                 }();
-                const bool mapped_out = mapped_env >= 0 ? mapped_env != 0 : n < 2048;
+                const bool mapped_out = mapped_env >= 0 ? mapped_env != 0 : n < kMappedOutMax;
                 // inputs likewise: mapped reads by the binning kernel, or one H2D copy
                 // node per array from the pinned block (HMDP_CGRAPH_MAPPED_IN=0/1 for A/B)
                 static const int mapped_in_env = [] {
@@ -1516,10 +1525,12 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                                            n * sizeof(int), cudaMemcpyHostToDevice, st), "types H2D");
                     }
                     ctx->out_override = dst;
+                    ctx->out_mapped = mapped_out;
                     const int launches =
                         enqueue_periodic(ctx, n, ctx->pos.as<double>(), ctx->types.as<int>(),
                                          box, precision, dst + 16, dst + 16 + 3 * n, st);
                     ctx->out_override = nullptr;
+                    ctx->out_mapped = false;
                     if (!mapped_out)
                         // header + forces (+ per-atom energies when this call asked for them)
                         ck(cudaMemcpyAsync(hp, dst,
@@ -1550,6 +1561,7 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                     }
                 } catch (...) {  // the result above stands; stay on the direct path
                     ctx->out_override = nullptr;
+                    ctx->out_mapped = false;
                     ctx->stage_hx = nullptr;
                     ctx->stage_ht = nullptr;
                     ctx->graph_vl = nullptr;

@@ -151,6 +151,9 @@ struct DevWork {
     // 1: the force kernel's last CTA also exports the device error word into out[12]
     // and clears it (hmdp_compute's graph path, outputs in host-mapped memory)
     int export_err;
+    // 1: forces / per-atom energies go to host-mapped memory (hmdp_compute's graph
+    // path): the force kernel writes each warp's atoms as one contiguous store
+    int wide_out;
 };
 
 // ---------------------------------------------------------------------------

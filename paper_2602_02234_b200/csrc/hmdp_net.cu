@@ -1768,12 +1768,31 @@ __global__ __launch_bounds__(kForceCTA) void k_force(DevGraph gr, DevWork<T> ws,
         fx = group_sum<FG>(fx);
         fy = group_sum<FG>(fy);
         fz = group_sum<FG>(fz);
+        // forces (and per-atom energies) of the warp's APW consecutive atoms as one
+        // contiguous store per array (3 APW doubles): one wide write instead of 3 APW
+        // scattered ones, which matters when the output is host-mapped memory
+        // (hmdp_compute's graph path writes across PCIe)
+        const bool full = ws.wide_out && base + APW <= gr.n;  // warp-uniform
+        if (full) {
+            const int src = ((lane % (3 * APW)) / 3) * FG;
+            const double vx = __shfl_sync(FULL_MASK, fx, src);
+            const double vy = __shfl_sync(FULL_MASK, fy, src);
+            const double vz = __shfl_sync(FULL_MASK, fz, src);
+            const int c = lane % 3;
+            if (lane < 3 * APW) forces[3ll * base + lane] = c == 0 ? vx : (c == 1 ? vy : vz);
+            if (per_atom) {
+                const double e = __shfl_sync(FULL_MASK, ei, (lane % APW) * FG);
+                if (lane < APW) per_atom[base + lane] = e;
+            }
+        }
         if (act && sub == 0) {
             const double f3[3] = {fx, fy, fz};
-            forces[3 * i] = fx;
-            forces[3 * i + 1] = fy;
-            forces[3 * i + 2] = fz;
-            if (per_atom) per_atom[i] = ei;
+            if (!full) {
+                forces[3 * i] = fx;
+                forces[3 * i + 1] = fy;
+                forces[3 * i + 2] = fz;
+                if (per_atom) per_atom[i] = ei;
+            }
             acc[0] += ei;
             if (mf.mode) {
                 const double s = mf.half / mi;
