@@ -2029,15 +2029,18 @@ static void launch_net(void (*kernel)(Params...), Phase p, const NetShape& sh, c
 }
 
 // Lanes per atom of the force kernel: a warp per atom while the atoms do not fill
-// the SMs' resident warps (every SM gets atoms), 8 beyond (HMDP_FORCE_FG pins it).
+// the SMs' resident warps (every SM gets atoms), 16 up to 64 atoms per SM, 8 beyond
+// (HMDP_FORCE_FG pins it).  Measured (profiles/round2/ab/force_fg16.txt, force_fg2.txt):
+// at 3LZM / 2PTC (18 / 28 atoms per SM) 16 lanes beat 8 by 2 % (DPA3) and 5-7 % (DPA2);
+// at 1YRF / 1UBQ 32 lanes stay best, at 2PTC x8 (222 atoms per SM) 8.
 int force_fg(int n) {
     static const int env = [] {
         const char* e = std::getenv("HMDP_FORCE_FG");
         const int v = e ? std::atoi(e) : 0;
-        return (v == 8 || v == 32) ? v : 0;
+        return (v == 8 || v == 16 || v == 32) ? v : 0;
     }();
     if (env) return env;
-    return n > num_sms() * 16 ? 8 : 32;
+    return n <= num_sms() * 16 ? 32 : (n <= num_sms() * 64 ? 16 : 8);
 }
 int force_grid(int n) {
     const int apc = (kForceCTA / 32) * (32 / force_fg(n));  // atoms per CTA
@@ -2050,16 +2053,11 @@ static void launch_force_k(const DevGraph& gr, const DevWork<T>& ws, double* for
                            double* per_atom, double* out, cudaStream_t st, const MdFuse& mf,
                            bool ddg = false) {
     const dim3 grid(force_grid(gr.n)), block(kForceCTA);
-    if (force_fg(gr.n) == 8) {
-        if (ddg)
-            launch_pdl(k_force<T, 8, true>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
-        else
-            launch_pdl(k_force<T, 8>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
-    } else {
-        if (ddg)
-            launch_pdl(k_force<T, 32, true>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
-        else
-            launch_pdl(k_force<T, 32>, grid, block, 0, st, gr, ws, forces, per_atom, out, mf);
+    auto go = [&](auto k) { launch_pdl(k, grid, block, 0, st, gr, ws, forces, per_atom, out, mf); };
+    switch (force_fg(gr.n)) {
+        case 8: ddg ? go(k_force<T, 8, true>) : go(k_force<T, 8>); break;
+        case 16: ddg ? go(k_force<T, 16, true>) : go(k_force<T, 16>); break;
+        default: ddg ? go(k_force<T, 32, true>) : go(k_force<T, 32>); break;
     }
 }
 
