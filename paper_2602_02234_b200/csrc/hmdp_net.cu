@@ -137,7 +137,10 @@ constexpr bool kRecomputeZ = false;
 // DPA2 2PTC +11 %, DPA3 2PTC +2 %, DPA3 1YRF -33 % if forced to 2).
 template <int G>
 constexpr int kNetMinCTAs = G == 1 ? 2 : 1;
-constexpr int kForceCTA = 128;  // small CTAs: every SM gets atoms in small systems
+#ifndef HMDP_FORCE_CTA
+#define HMDP_FORCE_CTA 128
+#endif
+constexpr int kForceCTA = HMDP_FORCE_CTA;  // small CTAs: every SM gets atoms in small systems
 // edges per unrolled batch (row loads in flight per lane; fewer for FP64 registers)
 template <typename T>
 constexpr int kU = sizeof(T) == 4 ? 8 : 4;
