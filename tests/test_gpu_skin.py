@@ -143,3 +143,16 @@ def test_compute_graph_per_atom_after_forces_only(monkeypatch):
         o = ctx.compute(s.positions, s.types, s.box, P.Precision.fp32, per_atom=True)
         assert np.array_equal(o.per_atom_energy, ref.per_atom_energy)
         assert np.array_equal(o.forces, ref.forces)
+
+
+@pytest.mark.parametrize("mname,prec", [("dpa2", P.Precision.fp64), ("se_a", P.Precision.fp32),
+                                        ("repflow", P.Precision.fp32)])
+def test_skin_compute_graph_path_other_families(monkeypatch, mname, prec):
+    s = P.generate_synthetic_system(582)
+    m = _model(mname)
+    ref = _compute_series(monkeypatch, m, s, 0.0, prec, calls=15)
+    got = _compute_series(monkeypatch, m, s, 0.05, prec, calls=15)
+    for a, b in zip(ref, got):
+        assert a[0] == b[0]
+        assert np.array_equal(a[1], b[1])
+        assert np.array_equal(a[2], b[2])
