@@ -228,8 +228,11 @@ std::unique_lock<std::shared_mutex> alloc_lock() {
 
 constexpr size_t kTailPad = 16384;
 // hmdp_compute's graph path writes its outputs straight to host-mapped memory below
-// this many atoms, through a D2H copy node above
-constexpr int kMappedOutMax = 16384;
+// this many atoms, through a D2H copy node above (profiles/round2/ab/force_store.txt,
+// mapped_out_recheck.txt: at 2PTC the mapped writes won 1.5-3 % on one box and lost
+// 0.5-2 % on another, where the host's read of the SM-written block took 10-11 us
+// against 3.5 us after the copy node; the copy node is the steadier choice there)
+constexpr int kMappedOutMax = 2048;
 
 // HMDP_E2E_PROBE=1: host-timer breakdown of hmdp_compute's graph-replay path (input
 // copy into the pinned block, cudaGraphLaunch, the wait, output copies), printed
@@ -1477,10 +1480,8 @@ int hmdp_compute(hmdp_ctx* ctx, int n, const double* xyz, const int* types, cons
                 // moves for large ones: the copy node costs ~4 us flat, the force
                 // kernel's scattered 8-byte PCIe writes grow with n (measured per
                 // call: 582 atoms 60.7 vs 64.5 us, 4114 atoms 92 vs 85 us; crossover
-                // near 1900 atoms).  Since each warp writes its atoms' forces as one
-                // contiguous store (DevWork::wide_out) the mapped writes win at 4114
-                // atoms too (e2e DPA2 2PTC +3.4 %, DPA3 +1.5 %, profiles/round2/ab/
-                // force_store.txt); the copy node stays for very large systems.
+                // near 1900 atoms).  Each warp writes its atoms' forces as one
+                // contiguous store (DevWork::wide_out); see kMappedOutMax.
                 // HMDP_CGRAPH_MAPPED_OUT=0/1 pins it for A/B.
                 static const int mapped_env = [] {
                     const char* e = std::getenv("HMDP_CGRAPH_MAPPED_OUT");
